@@ -1,0 +1,224 @@
+/*
+ * kin_abi.h — C ABI of the B200 batched reaction-kinetics sweep engine.
+ *
+ * This is the drop-in boundary for the reference's ensemble layer
+ * (/root/reference/proj/include/kinetics/ensemble.hpp).  The reference has no
+ * FFI of its own: its seam is the C++ API
+ *
+ *   SweepResults  parameter_sweep(const ReactionNetwork&, const SweepConfig&,
+ *                                 unsigned workers);          ensemble.hpp:129-130
+ *   EnsembleStatistics run_ensemble(const ReactionNetwork&,
+ *                                 const EnsembleOptions&, const RunSink&);
+ *                                                             ensemble.hpp:97-99
+ *   Trajectory    run_single(const ReactionNetwork&, const Method&, double t_end,
+ *                            const std::vector<double>& grid, uint64_t seed);
+ *                                                             ensemble.hpp:74-76
+ *
+ * Each of those is replaced by one call below (kin_sweep_run covers all three:
+ * run_ensemble is a sweep with zero axes, run_single a sweep with zero axes and
+ * one run whose seed is given directly).  Plain C types only: borrowed const
+ * pointers for inputs, caller-allocated host buffers for outputs, an opaque
+ * context owning device memory.  No exceptions cross the ABI; errors map 1:1 to
+ * the reference's exception classes (errors.hpp:8-44) and CLI exit codes
+ * (cli.hpp:7-13).
+ */
+#ifndef KIN_ABI_H_
+#define KIN_ABI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KIN_ABI_VERSION 1
+
+/* ---- status codes (cli.hpp:8-13 ExitCode; errors.hpp classes) ------------ */
+enum kin_status {
+  KIN_OK = 0,
+  KIN_ERR_INPUT = 1,      /* ParseError / ValidationError (errors.hpp:14-37)   */
+  KIN_ERR_SIMULATION = 2, /* SimulationError (errors.hpp:39-44)                */
+  KIN_ERR_DEVICE = 3,     /* CUDA failure (new: no reference counterpart)      */
+  KIN_ERR_USAGE = 64      /* bad arguments (cli.hpp:12 kExitUsage)             */
+};
+
+/* per-simulation status word written by the kernels (SimulationError causes) */
+enum kin_sim_status {
+  KIN_SIM_OK = 0,
+  KIN_SIM_BUDGET = 1,      /* step budget (IntegratorConfig::max_steps) exhausted */
+  KIN_SIM_NONFINITE = 2,   /* integrator produced a non-finite value              */
+  KIN_SIM_NEGATIVE = 3,    /* apply_reaction would go negative (model.hpp:159-163)*/
+  KIN_SIM_STEP_UNDERFLOW = 4 /* step size underflow                               */
+};
+
+/* ---- model: ReactionNetwork (model.hpp:13-95) ---------------------------- */
+/* Reactant / product multisets are given CSR-by-reaction, species ascending
+ * inside each reaction (std::map order, model.hpp:33-34).  nu, its sparse
+ * columns/rows and g_i (highest reactant order) are derived by the loader. */
+typedef struct kin_model_desc {
+  int32_t n_species;
+  int32_t n_reactions;
+  int32_t n_params;
+  const int64_t* initial_amounts;   /* [n_species]  Species::initial_amount  */
+  const double* rate_constants;     /* [n_reactions] Reaction::rate_constant */
+  const int32_t* rate_param;        /* [n_reactions] param index or -1; NULL = none bound */
+  const double* param_values;       /* [n_params]   Parameter::value         */
+  const int32_t* reactant_ptr;      /* [n_reactions+1]                        */
+  const int32_t* reactant_species;  /* [reactant_ptr[M]]                      */
+  const int32_t* reactant_stoich;   /* [reactant_ptr[M]]  > 0                 */
+  const int32_t* product_ptr;       /* [n_reactions+1]                        */
+  const int32_t* product_species;
+  const int32_t* product_stoich;
+  int32_t max_order;                /* 2 = reference (model.hpp:38); 3 enables the
+                                       order-3 extension (Schlogl, Brusselator) */
+} kin_model_desc;
+
+/* ---- method: Method (ensemble.hpp:59-71) + IntegratorConfig --------------- */
+enum kin_method_kind {          /* Method::Kind order, ensemble.hpp:62 */
+  KIN_METHOD_SSA = 0,
+  KIN_METHOD_TAU_ADAPTIVE = 1,
+  KIN_METHOD_TAU_FIXED = 2,
+  KIN_METHOD_CLE = 3,           /* not provided by this engine (KIN_ERR_INPUT) */
+  KIN_METHOD_ODE = 4,           /* Dopri5 RRE, deterministic.hpp:38-95 */
+  KIN_METHOD_HYBRID = 5,        /* not provided by this engine (KIN_ERR_INPUT) */
+  KIN_METHOD_LSODA = 6          /* extension: Adams/BDF with stiffness switching */
+};
+
+typedef struct kin_integrator_config { /* deterministic.hpp:14-20 */
+  double rel_tol;     /* default 1e-6 */
+  double abs_tol;     /* default 1e-9 */
+  double h_init;      /* 0 = automatic */
+  double h_max;       /* +inf = unbounded */
+  uint64_t max_steps; /* default 1e7; also bounds stochastic decisions+events */
+} kin_integrator_config;
+
+typedef struct kin_method {
+  int32_t kind;       /* enum kin_method_kind */
+  double tau;         /* TauFixed step */
+  double epsilon;     /* TauAdaptive control, default 0.03 */
+  kin_integrator_config integrator;
+} kin_method;
+
+/* ---- sweep: SweepConfig (ensemble.hpp:101-113) ---------------------------- */
+enum kin_axis_kind {
+  KIN_AXIS_PARAM = 0,    /* rebinds Parameter `index` (with_param, model.hpp:78-80) */
+  KIN_AXIS_INITIAL = 1   /* extension: initial amount of species `index` (integral values) */
+};
+
+typedef struct kin_sweep_axis {
+  int32_t kind;          /* enum kin_axis_kind */
+  int32_t index;
+  int32_t n_values;
+  const double* values;
+} kin_sweep_axis;
+
+enum kin_rng_mode {
+  KIN_RNG_COMPAT = 0,    /* xoshiro256++ stream per run, bit-compatible with rng.cpp */
+  KIN_RNG_PHILOX = 1     /* counter-based Philox4x32-10 keyed per (run, step) */
+};
+
+enum kin_seed_mode {
+  KIN_SEED_SWEEP = 0,    /* point master = derive(master, k); run seed = derive(point master, r) */
+  KIN_SEED_ENSEMBLE = 1, /* run_ensemble: run seed = derive(master, r) (ensemble.hpp:91-99) */
+  KIN_SEED_DIRECT = 2    /* run_single: the run seed is master_seed itself */
+};
+
+typedef struct kin_sweep_desc {
+  kin_method method;
+  int32_t n_axes;
+  const kin_sweep_axis* axes;   /* Cartesian product, LAST axis fastest */
+  uint64_t runs_per_point;
+  uint64_t master_seed;
+  int32_t seed_mode;            /* enum kin_seed_mode */
+  int32_t rng_mode;             /* enum kin_rng_mode */
+  double t_end;
+  int32_t n_grid;
+  const double* grid;           /* strictly increasing, within [0, t_end] */
+  /* shard: global simulation indices [sim_begin, sim_end); sim = point*R + run.
+     sim_end == 0 means "all".  Per-point statistics are produced only for points
+     whose runs all lie inside the shard. */
+  uint64_t sim_begin;
+  uint64_t sim_end;
+} kin_sweep_desc;
+
+/* ---- outputs (caller-allocated HOST buffers; any may be NULL) ------------- */
+typedef struct kin_sweep_out {
+  double* traj;      /* [S][G][N]   Trajectory::samples per simulation of the shard */
+  uint64_t* meta;    /* [S][6]      TrajectoryMeta {steps, rejected_leaps,
+                                    clamp_events, fallback_ssa_steps, jumps, floored} */
+  int32_t* status;   /* [S]         enum kin_sim_status */
+  double* mean;      /* [P][G][N]   EnsembleStatistics mean (grid-major per point) */
+  double* m2;        /* [P][G][N]   EnsembleStatistics m2 */
+  uint64_t* work;    /* [S]         algorithmic FP64 op count per simulation (optional;
+                                    selects the instrumented kernel variant) */
+} kin_sweep_out;
+
+typedef struct kin_error {
+  int32_t code;            /* enum kin_status */
+  int32_t sim_status;      /* enum kin_sim_status of the failing run */
+  uint64_t sim_index;      /* lowest failing global simulation index */
+  uint64_t point_index;
+  uint64_t run_index;
+  char message[256];
+} kin_error;
+
+/* ---- context / device ownership ------------------------------------------ */
+typedef struct kin_ctx kin_ctx;
+typedef struct kin_model kin_model;
+
+/* One host thread per device; device_ids NULL/n=0 → device 0. */
+int kin_ctx_create(const int32_t* device_ids, int32_t n_devices, kin_ctx** out,
+                   kin_error* err);
+void kin_ctx_destroy(kin_ctx* ctx);
+int32_t kin_ctx_device_count(const kin_ctx* ctx);
+
+/* ReactionNetwork::create validation (model.hpp:47-53) + upload of the packed
+   device tables to every device of the context. */
+int kin_model_upload(kin_ctx* ctx, const kin_model_desc* desc, kin_model** out,
+                     kin_error* err);
+void kin_model_free(kin_model* model);
+
+/* Number of sweep points P and simulations S = P*R of a descriptor. */
+int kin_sweep_size(const kin_sweep_desc* desc, uint64_t* n_points,
+                   uint64_t* n_sims, kin_error* err);
+
+/* parameter_sweep / run_ensemble / run_single (ensemble.hpp:74-130) end to end:
+   H2D of the sweep tables, kernels on every device of the context (shard by
+   whole-point chunks, cyclic), D2H into `out`.  Blocking. */
+int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc,
+                  kin_sweep_out* out, kin_error* err);
+
+/* ---- device-resident form (benchmarks, chained consumers) -----------------
+   Runs the sweep on device `device_slot` of the context into context-owned
+   device buffers, on the context's stream, WITHOUT any host copies.  The
+   results stay resident until the next call; kin_sweep_fetch copies them out.
+   kin_sweep_launch does not synchronize. */
+int kin_sweep_launch(kin_ctx* ctx, const kin_model* model,
+                     const kin_sweep_desc* desc, int32_t device_slot,
+                     int32_t want_stats, int32_t want_work, kin_error* err);
+int kin_sweep_sync(kin_ctx* ctx, int32_t device_slot, kin_error* err);
+int kin_sweep_fetch(kin_ctx* ctx, int32_t device_slot, kin_sweep_out* out,
+                    kin_error* err);
+/* cudaStream_t of the device slot, as void* (for event timing by the caller). */
+void* kin_ctx_stream(kin_ctx* ctx, int32_t device_slot);
+
+/* ---- seams (device unit kernels; SPEC "from_uniforms"/"from_counts") ----- */
+uint64_t kin_splitmix64_mix(uint64_t v);                       /* rng.hpp:8-11 */
+uint64_t kin_derive_run_seed(uint64_t master, uint64_t index);  /* ensemble.hpp:15-18 */
+/* Device RNG draws from RngStream(seed): kind 0 next_u64, 1 draw_uniform,
+   2 draw_normal, 3 draw_poisson(mean).  Results as raw 64-bit words. */
+int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
+                         int32_t n, uint64_t* out_bits, kin_error* err);
+
+/* Peak FP64 FMA throughput of device slot 0 (TFLOP/s, FMA = 2 flops), from a
+   DFMA microbenchmark; used as the roofline denominator. */
+int kin_measure_fp64_peak(kin_ctx* ctx, double* tflops, kin_error* err);
+
+const char* kin_status_string(int32_t code);
+int32_t kin_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KIN_ABI_H_ */

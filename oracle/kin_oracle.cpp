@@ -1,0 +1,840 @@
+// oracle/kin_oracle.cpp — TEST INFRASTRUCTURE ONLY (CPU oracle / CPU baseline).
+//
+// Restates, from the reference's header contracts and SPEC (no .cpp exists for
+// them in /root/reference), the hot path of arxiv/paper_1309_7695's kinetics
+// library:
+//   ReactionNetwork::create ....... model.hpp:47-53
+//   propensities .................. model.hpp:145-157
+//   apply_reaction ................ model.hpp:159-163
+//   ssa_step(_from_uniforms) ...... stochastic.hpp:22-32
+//   simulate_ssa .................. stochastic.hpp:34-38
+//   select_tau .................... stochastic.hpp:40-46
+//   tau_leap_step(_from_counts) ... stochastic.hpp:48-62
+//   simulate_approx ............... stochastic.hpp:78-92
+//   rre_rhs / rk_step / Dopri5 .... deterministic.hpp:26-95
+//   derive_run_seed ............... ensemble.hpp:15-18
+//   EnsembleStatistics ............ ensemble.hpp:20-57
+//   run_ensemble / parameter_sweep  ensemble.hpp:78-130
+// Built with -O3 -DNDEBUG -ffp-contract=off (the reference Release flags,
+// proj/CMakeLists.txt:6-8, with contraction pinned off so the CUDA kernels,
+// compiled with -fmad=false on the parity path, round identically).
+#include "kin_oracle.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <thread>
+
+namespace kin_oracle {
+
+namespace {
+constexpr double kInf = std::numeric_limits<double>::infinity();
+
+void set_err(kin_error* e, int code, const std::string& msg) {
+  if (!e) return;
+  e->code = code;
+  std::snprintf(e->message, sizeof(e->message), "%s", msg.c_str());
+}
+}  // namespace
+
+void Scratch::resize(int n, int m) {
+  x.assign(n, 0.0);
+  xn.assign(n, 0.0);
+  x0.assign(n, 0.0);
+  a.assign(m, 0.0);
+  rates.assign(m, 0.0);
+  k.assign(m, 0);
+  for (auto& vv : v) vv.assign(static_cast<size_t>(n) * (n > 1 ? n : 1) + 1, 0.0);
+}
+
+int build_network(const kin_model_desc* d, Network* net, std::string* msg) {
+  if (!d) { *msg = "null model descriptor"; return KIN_ERR_USAGE; }
+  const int n = d->n_species, m = d->n_reactions, np = d->n_params;
+  if (n < 0 || m < 0 || np < 0) { *msg = "negative model dimension"; return KIN_ERR_INPUT; }
+  if ((n > 0 && !d->initial_amounts) || (m > 0 && (!d->rate_constants || !d->reactant_ptr || !d->product_ptr))) {
+    *msg = "missing model array"; return KIN_ERR_USAGE;
+  }
+  const int max_order = d->max_order <= 0 ? 2 : d->max_order;
+  if (max_order > 3) { *msg = "max_order above 3 is not supported"; return KIN_ERR_INPUT; }
+  Network& N = *net;
+  N = Network{};
+  N.n = n; N.m = m;
+  for (int i = 0; i < n; ++i) {
+    if (d->initial_amounts[i] < 0) { *msg = "species " + std::to_string(i) + ": negative initial amount"; return KIN_ERR_INPUT; }
+    N.x0.push_back(static_cast<double>(d->initial_amounts[i]));
+  }
+  for (int p = 0; p < np; ++p) {
+    if (!(d->param_values[p] > 0.0) || !std::isfinite(d->param_values[p])) { *msg = "param " + std::to_string(p) + ": rate must be positive"; return KIN_ERR_INPUT; }
+    N.params.push_back(d->param_values[p]);
+  }
+  N.rt_ptr.push_back(0);
+  N.col_ptr.push_back(0);
+  std::vector<int> nu(static_cast<size_t>(n) * m, 0);
+  N.g.assign(n, 1);
+  for (int j = 0; j < m; ++j) {
+    const int rp = d->rate_param ? d->rate_param[j] : -1;
+    if (rp >= np || rp < -1) { *msg = "reaction " + std::to_string(j) + ": unknown parameter"; return KIN_ERR_INPUT; }
+    const double c = rp >= 0 ? d->param_values[rp] : d->rate_constants[j];
+    if (!(c > 0.0) || !std::isfinite(c)) { *msg = "reaction " + std::to_string(j) + ": rate must be positive"; return KIN_ERR_INPUT; }
+    N.rate_base.push_back(d->rate_constants[j]);
+    N.rate_param.push_back(rp);
+    int order = 0, prev = -1;
+    for (int p = d->reactant_ptr[j]; p < d->reactant_ptr[j + 1]; ++p) {
+      const int s = d->reactant_species[p], st = d->reactant_stoich[p];
+      if (s < 0 || s >= n) { *msg = "reaction " + std::to_string(j) + ": undeclared species"; return KIN_ERR_INPUT; }
+      if (s <= prev) { *msg = "reaction " + std::to_string(j) + ": reactants must be species-ascending and unique"; return KIN_ERR_INPUT; }
+      if (st <= 0) { *msg = "reaction " + std::to_string(j) + ": stoichiometry must be positive"; return KIN_ERR_INPUT; }
+      prev = s;
+      order += st;
+      N.rt_species.push_back(s);
+      N.rt_stoich.push_back(st);
+      nu[static_cast<size_t>(s) * m + j] -= st;
+    }
+    if (order > max_order) { *msg = "reaction " + std::to_string(j) + ": reactant order " + std::to_string(order) + " exceeds " + std::to_string(max_order); return KIN_ERR_INPUT; }
+    for (int p = d->reactant_ptr[j]; p < d->reactant_ptr[j + 1]; ++p)
+      N.g[d->reactant_species[p]] = std::max(N.g[d->reactant_species[p]], order);
+    prev = -1;
+    for (int p = d->product_ptr[j]; p < d->product_ptr[j + 1]; ++p) {
+      const int s = d->product_species[p], st = d->product_stoich[p];
+      if (s < 0 || s >= n) { *msg = "reaction " + std::to_string(j) + ": undeclared species"; return KIN_ERR_INPUT; }
+      if (s <= prev) { *msg = "reaction " + std::to_string(j) + ": products must be species-ascending and unique"; return KIN_ERR_INPUT; }
+      if (st <= 0) { *msg = "reaction " + std::to_string(j) + ": stoichiometry must be positive"; return KIN_ERR_INPUT; }
+      prev = s;
+      nu[static_cast<size_t>(s) * m + j] += st;
+    }
+    N.order.push_back(order);
+    N.rt_ptr.push_back(static_cast<int>(N.rt_species.size()));
+    for (int s = 0; s < n; ++s) {
+      const int dl = nu[static_cast<size_t>(s) * m + j];
+      if (dl != 0) { N.col_species.push_back(s); N.col_delta.push_back(dl); }
+    }
+    N.col_ptr.push_back(static_cast<int>(N.col_species.size()));
+  }
+  N.row_ptr.push_back(0);
+  for (int s = 0; s < n; ++s) {
+    for (int j = 0; j < m; ++j) {
+      const int dl = nu[static_cast<size_t>(s) * m + j];
+      if (dl != 0) { N.row_reaction.push_back(j); N.row_delta.push_back(dl); }
+    }
+    N.row_ptr.push_back(static_cast<int>(N.row_reaction.size()));
+  }
+  return KIN_OK;
+}
+
+template <bool C>
+double select_tau(const Network& net, const double* x, const double* a, double eps, Work* w) {
+  double tau = kInf;
+  for (int i = 0; i < net.n; ++i) {
+    double mu = 0.0, s2 = 0.0;
+    for (int p = net.row_ptr[i]; p < net.row_ptr[i + 1]; ++p) {
+      const int dl = net.row_delta[p];
+      const double aj = a[net.row_reaction[p]];
+      mu = mu + static_cast<double>(dl) * aj;
+      s2 = s2 + static_cast<double>(dl * dl) * aj;
+    }
+    if constexpr (C) w->flops += 4 * static_cast<std::uint64_t>(net.row_ptr[i + 1] - net.row_ptr[i]);
+    if (mu == 0.0 && s2 == 0.0) continue;
+    double bound = eps * x[i] / static_cast<double>(net.g[i]);
+    if (bound < 1.0) bound = 1.0;
+    if constexpr (C) w->flops += 2;
+    if (mu != 0.0) {
+      const double t1 = bound / std::fabs(mu);
+      if (t1 < tau) tau = t1;
+      if constexpr (C) w->flops += 1;
+    }
+    if (s2 != 0.0) {
+      const double t2 = bound * bound / s2;
+      if (t2 < tau) tau = t2;
+      if constexpr (C) w->flops += 2;
+    }
+  }
+  return tau;
+}
+
+int ssa_select(const Network& net, const double* a, double a0, double u2) {
+  const double target = u2 * a0;
+  double c = 0.0;
+  int last = -1;
+  for (int j = 0; j < net.m; ++j) {
+    if (a[j] > 0.0) last = j;
+    c = c + a[j];
+    if (c > target) return j;
+  }
+  return last;
+}
+
+template <bool C>
+int simulate_stochastic(const Network& net, const double* rates, const double* x0,
+                        const kin_method& method, double t_end, const double* grid,
+                        int n_grid, std::uint64_t seed, double* out, std::uint64_t* meta,
+                        Scratch& sc, Work* w) {
+  const int n = net.n, m = net.m;
+  double* x = sc.x.data();
+  double* xn = sc.xn.data();
+  double* a = sc.a.data();
+  std::uint64_t* k = sc.k.data();
+  std::uint64_t* pf = C ? &w->flops : nullptr;
+  for (int i = 0; i < n; ++i) x[i] = x0[i];
+  for (int q = 0; q < 6; ++q) meta[q] = 0;
+  Stream rng(seed);
+  const int kind = method.kind;
+  double t = 0.0;
+  int gi = 0;
+  auto emit = [&]() {
+    std::memcpy(out + static_cast<size_t>(gi) * n, x, sizeof(double) * n);
+    ++gi;
+  };
+  while (gi < n_grid && grid[gi] <= t) emit();
+  const std::uint64_t budget = method.integrator.max_steps;
+  std::uint64_t used = 0;
+
+  while (t < t_end) {
+    if (++used > budget) return KIN_SIM_BUDGET;
+    propensities<C>(net, rates, x, a, w);
+    double a0 = 0.0;
+    for (int j = 0; j < m; ++j) a0 = a0 + a[j];
+    if constexpr (C) w->flops += m;
+    if (a0 == 0.0) break;  // every propensity vanished: the state is absorbing
+
+    double tau = 0.0;
+    bool burst = false;
+    if (kind == KIN_METHOD_SSA) {
+      burst = true;
+    } else if (kind == KIN_METHOD_TAU_ADAPTIVE) {
+      tau = select_tau<C>(net, x, a, method.epsilon, w);
+      if constexpr (C) w->flops += 1;
+      burst = tau < 10.0 / a0;  // SPEC.md:191 fallback threshold
+    } else {
+      tau = method.tau;
+    }
+
+    if (burst) {
+      // Exact SSA events (direct method); a tau method takes at most 100 of them
+      // before re-attempting a leap.
+      bool stop = false;
+      for (int b = 0;; ++b) {
+        if (b > 0) {
+          if (kind != KIN_METHOD_SSA && b >= 100) break;
+          if (++used > budget) return KIN_SIM_BUDGET;
+          propensities<C>(net, rates, x, a, w);
+          a0 = 0.0;
+          for (int j = 0; j < m; ++j) a0 = a0 + a[j];
+          if constexpr (C) w->flops += m;
+          if (a0 == 0.0) { stop = true; break; }
+        }
+        const double u1 = rng.draw_uniform();
+        const double u2 = rng.draw_uniform();
+        const double dt = std::log(1.0 / u1) / a0;
+        const double tn = t + dt;
+        if constexpr (C) w->flops += 4 + 4;
+        if (tn > t_end) { t = t_end; stop = true; break; }
+        while (gi < n_grid && grid[gi] < tn) emit();
+        const int j = ssa_select(net, a, a0, u2);
+        if constexpr (C) w->flops += 1 + static_cast<std::uint64_t>(j + 1);
+        for (int p = net.col_ptr[j]; p < net.col_ptr[j + 1]; ++p) {
+          const double v = x[net.col_species[p]] + static_cast<double>(net.col_delta[p]);
+          if (v < 0.0) return KIN_SIM_NEGATIVE;  // apply_reaction contract, model.hpp:159-161
+          x[net.col_species[p]] = v;
+        }
+        if constexpr (C) w->flops += static_cast<std::uint64_t>(net.col_ptr[j + 1] - net.col_ptr[j]);
+        t = tn;
+        if (kind == KIN_METHOD_SSA) ++meta[0]; else ++meta[3];
+        while (gi < n_grid && grid[gi] <= t) emit();
+      }
+      if (stop) break;
+      continue;
+    }
+
+    // Poisson leap, truncated at the next grid time (App. B #3) so every grid
+    // sample is an exact state; rejection halves tau.
+    const double t_stop = (gi < n_grid && grid[gi] < t_end) ? grid[gi] : t_end;
+    bool hit = false;
+    const double gap = t_stop - t;
+    if constexpr (C) w->flops += 1;
+    if (!(tau < gap)) { tau = gap; hit = true; }
+    for (;;) {
+      for (int j = 0; j < m; ++j) k[j] = rng.draw_poisson(a[j] * tau, pf);
+      for (int i = 0; i < n; ++i) xn[i] = x[i];
+      for (int j = 0; j < m; ++j) {
+        if (k[j] == 0) continue;
+        const double kj = static_cast<double>(k[j]);
+        for (int p = net.col_ptr[j]; p < net.col_ptr[j + 1]; ++p)
+          xn[net.col_species[p]] = xn[net.col_species[p]] + static_cast<double>(net.col_delta[p]) * kj;
+      }
+      if constexpr (C) w->flops += static_cast<std::uint64_t>(m) + 2 * static_cast<std::uint64_t>(net.col_ptr[m]);
+      bool neg = false;
+      for (int i = 0; i < n; ++i) neg |= xn[i] < 0.0;
+      if (!neg) break;
+      ++meta[1];
+      tau = tau * 0.5;
+      hit = false;
+      if constexpr (C) w->flops += 1;
+    }
+    std::swap(x, xn);
+    if (hit) {
+      t = t_stop;
+    } else {
+      t = t + tau;
+      if constexpr (C) w->flops += 1;
+    }
+    ++meta[0];
+    while (gi < n_grid && grid[gi] <= t) emit();
+  }
+  while (gi < n_grid) emit();
+  return KIN_SIM_OK;
+}
+
+// ---- Dormand-Prince 5(4) (deterministic.hpp:26-83) --------------------------
+// Coefficients: Dormand & Prince (1980); PI control, FSAL and the dense output
+// follow Hairer, Norsett & Wanner's DOPRI5 conventions.
+namespace dp {
+constexpr double c2 = 1.0 / 5.0, c3 = 3.0 / 10.0, c4 = 4.0 / 5.0, c5 = 8.0 / 9.0;
+constexpr double a21 = 1.0 / 5.0;
+constexpr double a31 = 3.0 / 40.0, a32 = 9.0 / 40.0;
+constexpr double a41 = 44.0 / 45.0, a42 = -56.0 / 15.0, a43 = 32.0 / 9.0;
+constexpr double a51 = 19372.0 / 6561.0, a52 = -25360.0 / 2187.0, a53 = 64448.0 / 6561.0,
+                 a54 = -212.0 / 729.0;
+constexpr double a61 = 9017.0 / 3168.0, a62 = -355.0 / 33.0, a63 = 46732.0 / 5247.0,
+                 a64 = 49.0 / 176.0, a65 = -5103.0 / 18656.0;
+constexpr double a71 = 35.0 / 384.0, a73 = 500.0 / 1113.0, a74 = 125.0 / 192.0,
+                 a75 = -2187.0 / 6784.0, a76 = 11.0 / 84.0;
+constexpr double e1 = 71.0 / 57600.0, e3 = -71.0 / 16695.0, e4 = 71.0 / 1920.0,
+                 e5 = -17253.0 / 339200.0, e6 = 22.0 / 525.0, e7 = -1.0 / 40.0;
+constexpr double d1 = -12715105075.0 / 11282082432.0, d3 = 87487479700.0 / 32700410799.0,
+                 d4 = -10690763975.0 / 1880347072.0, d5 = 701980252875.0 / 199316789632.0,
+                 d6 = -1453857185.0 / 822651844.0, d7 = 69997945.0 / 29380423.0;
+constexpr double kSafe = 0.9, kFacMinInv = 5.0 /* 1/0.2 */, kFacMaxInv = 0.1 /* 1/10 */;
+constexpr double kBeta = 0.04, kExpo1 = 0.2 - kBeta * 0.75;
+}  // namespace dp
+
+template <bool C>
+int integrate_rre(const Network& net, const double* rates, const double* x0,
+                  const kin_integrator_config& cfg, double t_end, const double* grid,
+                  int n_grid, double* out, std::uint64_t* meta, Scratch& sc, Work* w) {
+  using namespace dp;
+  const int n = net.n;
+  double* y = sc.v[0].data();
+  double* k1 = sc.v[1].data();
+  double* k2 = sc.v[2].data();
+  double* k3 = sc.v[3].data();
+  double* k4 = sc.v[4].data();
+  double* k5 = sc.v[5].data();
+  double* k6 = sc.v[6].data();
+  double* k7 = sc.v[7].data();
+  double* yn = sc.v[8].data();
+  double* ys = sc.v[9].data();
+  double* r1 = sc.v[10].data();
+  double* r2 = sc.v[11].data();
+  double* r3 = sc.v[12].data();
+  double* r4 = sc.v[13].data();
+  double* r5 = sc.v[14].data();
+  double* a = sc.a.data();
+  const double rtol = cfg.rel_tol, atol = cfg.abs_tol;
+  const double hmax = cfg.h_max > 0.0 ? cfg.h_max : kInf;
+  for (int q = 0; q < 6; ++q) meta[q] = 0;
+  bool floored = false;
+  for (int i = 0; i < n; ++i) y[i] = x0[i];
+  double t = 0.0;
+  int gi = 0;
+  while (gi < n_grid && grid[gi] <= t) {
+    std::memcpy(out + static_cast<size_t>(gi) * n, y, sizeof(double) * n);
+    ++gi;
+  }
+  if (!(t < t_end)) {
+    while (gi < n_grid) { std::memcpy(out + static_cast<size_t>(gi) * n, y, sizeof(double) * n); ++gi; }
+    return KIN_SIM_OK;
+  }
+  rre_rhs<C>(net, rates, y, a, k1, w);
+
+  double h;
+  if (cfg.h_init > 0.0) {
+    h = cfg.h_init;
+  } else {
+    // Automatic initial step (Hairer's HINIT, order 5).
+    double dnf = 0.0, dny = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double sk = atol + rtol * std::fabs(y[i]);
+      const double qf = k1[i] / sk, qy = y[i] / sk;
+      dnf = dnf + qf * qf;
+      dny = dny + qy * qy;
+    }
+    if constexpr (C) w->flops += 8 * static_cast<std::uint64_t>(n);
+    h = (dnf <= 1e-10 || dny <= 1e-10) ? 1.0e-6 : std::sqrt(dny / dnf) * 0.01;
+    if (h > hmax) h = hmax;
+    for (int i = 0; i < n; ++i) ys[i] = y[i] + h * k1[i];
+    rre_rhs<C>(net, rates, ys, a, k2, w);
+    double der2 = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double sk = atol + rtol * std::fabs(y[i]);
+      const double q = (k2[i] - k1[i]) / sk;
+      der2 = der2 + q * q;
+    }
+    der2 = std::sqrt(der2) / h;
+    const double der12 = std::max(der2, std::sqrt(dnf));
+    const double h1 = der12 <= 1e-15 ? std::max(1.0e-6, h * 1.0e-3) : std::pow(0.01 / der12, 0.2);
+    h = std::min(100.0 * h, h1);
+    if (h > hmax) h = hmax;
+    if constexpr (C) w->flops += 7 * static_cast<std::uint64_t>(n) + 12;
+  }
+
+  double facold = 1.0e-4;
+  bool last_rejected = false;
+  std::uint64_t attempts = 0;
+  while (t < t_end) {
+    if (attempts++ >= cfg.max_steps) return KIN_SIM_BUDGET;
+    double hh = h < hmax ? h : hmax;
+    bool hit = false;
+    if (t + hh >= t_end) { hh = t_end - t; hit = true; }
+    if (!(hh > 0.0) || t + hh == t) return KIN_SIM_STEP_UNDERFLOW;
+
+    for (int i = 0; i < n; ++i) ys[i] = y[i] + hh * (a21 * k1[i]);
+    rre_rhs<C>(net, rates, ys, a, k2, w);
+    for (int i = 0; i < n; ++i) ys[i] = y[i] + hh * (a31 * k1[i] + a32 * k2[i]);
+    rre_rhs<C>(net, rates, ys, a, k3, w);
+    for (int i = 0; i < n; ++i) ys[i] = y[i] + hh * (a41 * k1[i] + a42 * k2[i] + a43 * k3[i]);
+    rre_rhs<C>(net, rates, ys, a, k4, w);
+    for (int i = 0; i < n; ++i)
+      ys[i] = y[i] + hh * (a51 * k1[i] + a52 * k2[i] + a53 * k3[i] + a54 * k4[i]);
+    rre_rhs<C>(net, rates, ys, a, k5, w);
+    for (int i = 0; i < n; ++i)
+      ys[i] = y[i] + hh * (a61 * k1[i] + a62 * k2[i] + a63 * k3[i] + a64 * k4[i] + a65 * k5[i]);
+    rre_rhs<C>(net, rates, ys, a, k6, w);
+    for (int i = 0; i < n; ++i)
+      yn[i] = y[i] + hh * (a71 * k1[i] + a73 * k3[i] + a74 * k4[i] + a75 * k5[i] + a76 * k6[i]);
+    rre_rhs<C>(net, rates, yn, a, k7, w);
+
+    double sum = 0.0;
+    bool finite = true;
+    for (int i = 0; i < n; ++i) {
+      const double e = hh * (e1 * k1[i] + e3 * k3[i] + e4 * k4[i] + e5 * k5[i] + e6 * k6[i] + e7 * k7[i]);
+      const double sk = atol + rtol * std::max(std::fabs(y[i]), std::fabs(yn[i]));
+      const double q = e / sk;
+      sum = sum + q * q;
+      finite &= std::isfinite(yn[i]);
+    }
+    const double err = std::sqrt(sum / static_cast<double>(n));
+    if constexpr (C) w->flops += 63 * static_cast<std::uint64_t>(n) + 4;
+    if (!finite || !std::isfinite(err)) return KIN_SIM_NONFINITE;
+    const double fac11 = std::pow(err, kExpo1);
+
+    if (err <= 1.0) {
+      double fac = fac11 / std::pow(facold, kBeta);
+      fac = std::max(kFacMaxInv, std::min(kFacMinInv, fac / kSafe));
+      double hnew = hh / fac;
+      facold = std::max(err, 1.0e-4);
+      for (int i = 0; i < n; ++i) {
+        r1[i] = y[i];
+        const double yd = yn[i] - y[i];
+        r2[i] = yd;
+        const double bs = hh * k1[i] - yd;
+        r3[i] = bs;
+        r4[i] = yd - hh * k7[i] - bs;
+        r5[i] = hh * (d1 * k1[i] + d3 * k3[i] + d4 * k4[i] + d5 * k5[i] + d6 * k6[i] + d7 * k7[i]);
+      }
+      const double tprev = t;
+      t = hit ? t_end : t + hh;
+      for (int i = 0; i < n; ++i) { y[i] = yn[i]; k1[i] = k7[i]; }
+      if (last_rejected && hnew > hh) hnew = hh;
+      last_rejected = false;
+      h = hnew;
+      ++meta[0];
+      if constexpr (C) w->flops += 18 * static_cast<std::uint64_t>(n) + 8;
+      // Dense output onto every grid time in (tprev, t]; exact at
+      // the step end; floored at zero with a flag.
+      while (gi < n_grid && grid[gi] <= t) {
+        double* o = out + static_cast<size_t>(gi) * n;
+        if (grid[gi] == t) {
+          for (int i = 0; i < n; ++i) o[i] = y[i];
+        } else {
+          const double th = (grid[gi] - tprev) / hh;
+          const double th1 = 1.0 - th;
+          for (int i = 0; i < n; ++i)
+            o[i] = r1[i] + th * (r2[i] + th1 * (r3[i] + th * (r4[i] + th1 * r5[i])));
+          if constexpr (C) w->flops += 8 * static_cast<std::uint64_t>(n) + 3;
+        }
+        for (int i = 0; i < n; ++i)
+          if (o[i] < 0.0) { o[i] = 0.0; floored = true; }
+        ++gi;
+      }
+      bool lifted = false;
+      for (int i = 0; i < n; ++i)
+        if (y[i] < 0.0) { y[i] = 0.0; lifted = true; }
+      if (lifted) {
+        floored = true;
+        rre_rhs<C>(net, rates, y, a, k1, w);
+      }
+    } else {
+      h = hh / std::min(kFacMinInv, fac11 / kSafe);
+      last_rejected = true;
+      ++meta[1];
+      if constexpr (C) w->flops += 3;
+    }
+  }
+  while (gi < n_grid) {
+    std::memcpy(out + static_cast<size_t>(gi) * n, y, sizeof(double) * n);
+    ++gi;
+  }
+  meta[5] = floored ? 1 : 0;
+  return KIN_SIM_OK;
+}
+
+constexpr bool kLsodaAvailable = false;
+template <bool C>
+int integrate_lsoda(const Network&, const double*, const double*, const kin_integrator_config&,
+                    double, const double*, int, double*, std::uint64_t*, Scratch&, Work*) {
+  return KIN_SIM_NONFINITE;
+}
+
+// ---- sweep decoding (ensemble.hpp:101-130) ----------------------------------
+int sweep_layout(const kin_sweep_desc* d, SweepLayout* L, std::string* msg) {
+  if (!d) { *msg = "null sweep descriptor"; return KIN_ERR_USAGE; }
+  if (d->n_axes < 0 || (d->n_axes > 0 && !d->axes)) { *msg = "bad axes"; return KIN_ERR_USAGE; }
+  std::uint64_t P = 1;
+  for (int ax = 0; ax < d->n_axes; ++ax) {
+    const kin_sweep_axis& A = d->axes[ax];
+    if (A.n_values <= 0 || !A.values) { *msg = "axis " + std::to_string(ax) + ": empty value list"; return KIN_ERR_INPUT; }
+    if (P > (std::uint64_t{1} << 40) / static_cast<std::uint64_t>(A.n_values)) { *msg = "sweep too large"; return KIN_ERR_INPUT; }
+    P *= static_cast<std::uint64_t>(A.n_values);
+  }
+  if (d->runs_per_point == 0) { *msg = "runs_per_point must be >= 1"; return KIN_ERR_INPUT; }
+  L->n_points = P;
+  L->runs = d->runs_per_point;
+  L->n_sims = P * d->runs_per_point;
+  return KIN_OK;
+}
+
+void decode_sim(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, double* rates,
+                double* x0, std::uint64_t* seed) {
+  const std::uint64_t R = d->runs_per_point;
+  const std::uint64_t point = sim / R, run = sim % R;
+  double params[64];
+  std::vector<double> pbig;
+  double* pv = params;
+  if (net.params.size() > 64) { pbig = net.params; pv = pbig.data(); }
+  else for (size_t p = 0; p < net.params.size(); ++p) params[p] = net.params[p];
+  for (int i = 0; i < net.n; ++i) x0[i] = net.x0[i];
+  std::uint64_t rem = point;
+  for (int ax = d->n_axes - 1; ax >= 0; --ax) {
+    const kin_sweep_axis& A = d->axes[ax];
+    const std::uint64_t nv = static_cast<std::uint64_t>(A.n_values);
+    const double v = A.values[rem % nv];
+    rem /= nv;
+    if (A.kind == KIN_AXIS_PARAM) pv[A.index] = v;
+    else x0[A.index] = v;
+  }
+  for (int j = 0; j < net.m; ++j) rates[j] = net.rate_param[j] >= 0 ? pv[net.rate_param[j]] : net.rate_base[j];
+  switch (d->seed_mode) {
+    case KIN_SEED_ENSEMBLE: *seed = derive_run_seed(d->master_seed, sim); break;
+    case KIN_SEED_DIRECT: *seed = sim == 0 ? d->master_seed : derive_run_seed(d->master_seed, sim); break;
+    default: *seed = derive_run_seed(derive_run_seed(d->master_seed, point), run); break;
+  }
+}
+
+int validate_sweep(const Network& net, const kin_sweep_desc* d, std::string* msg) {
+  const kin_method& M = d->method;
+  if (M.kind == KIN_METHOD_CLE || M.kind == KIN_METHOD_HYBRID) { *msg = "method not provided by this engine (CLE/hybrid are out of scope)"; return KIN_ERR_INPUT; }
+  if (M.kind < 0 || M.kind > KIN_METHOD_LSODA) { *msg = "unknown method kind"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_LSODA && !kLsodaAvailable) { *msg = "LSODA not built"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_TAU_FIXED && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_TAU_ADAPTIVE && !(M.epsilon > 0.0 && M.epsilon < 1.0)) { *msg = "epsilon must be in (0,1)"; return KIN_ERR_INPUT; }
+  if (M.integrator.max_steps == 0) { *msg = "max_steps must be positive"; return KIN_ERR_INPUT; }
+  if ((M.kind == KIN_METHOD_ODE || M.kind == KIN_METHOD_LSODA) && !(M.integrator.rel_tol > 0.0 && M.integrator.abs_tol > 0.0)) { *msg = "tolerances must be positive"; return KIN_ERR_INPUT; }
+  if (!(d->t_end >= 0.0) || !std::isfinite(d->t_end)) { *msg = "t_end must be finite and non-negative"; return KIN_ERR_INPUT; }
+  if (d->n_grid < 0 || (d->n_grid > 0 && !d->grid)) { *msg = "bad grid"; return KIN_ERR_USAGE; }
+  for (int g = 0; g < d->n_grid; ++g) {
+    if (!(d->grid[g] >= 0.0 && d->grid[g] <= d->t_end)) { *msg = "grid point outside [0, t_end]"; return KIN_ERR_INPUT; }
+    if (g > 0 && !(d->grid[g] > d->grid[g - 1])) { *msg = "grid must be strictly increasing"; return KIN_ERR_INPUT; }
+  }
+  for (int ax = 0; ax < d->n_axes; ++ax) {
+    const kin_sweep_axis& A = d->axes[ax];
+    if (A.kind == KIN_AXIS_PARAM) {
+      if (A.index < 0 || A.index >= static_cast<int>(net.params.size())) { *msg = "axis " + std::to_string(ax) + ": unknown parameter"; return KIN_ERR_INPUT; }
+      for (int v = 0; v < A.n_values; ++v)
+        if (!(A.values[v] > 0.0) || !std::isfinite(A.values[v])) { *msg = "axis " + std::to_string(ax) + ": rate values must be positive"; return KIN_ERR_INPUT; }
+    } else if (A.kind == KIN_AXIS_INITIAL) {
+      if (A.index < 0 || A.index >= net.n) { *msg = "axis " + std::to_string(ax) + ": unknown species"; return KIN_ERR_INPUT; }
+      for (int v = 0; v < A.n_values; ++v)
+        if (!(A.values[v] >= 0.0) || A.values[v] != std::floor(A.values[v]) || A.values[v] > 9007199254740992.0) { *msg = "axis " + std::to_string(ax) + ": initial amounts must be non-negative integers"; return KIN_ERR_INPUT; }
+    } else {
+      *msg = "axis " + std::to_string(ax) + ": unknown axis kind"; return KIN_ERR_INPUT;
+    }
+  }
+  if (d->seed_mode == KIN_SEED_DIRECT) {
+    SweepLayout L; std::string m2;
+    if (sweep_layout(d, &L, &m2) == KIN_OK && L.n_sims != 1) { *msg = "direct seeding needs exactly one simulation"; return KIN_ERR_INPUT; }
+  }
+  return KIN_OK;
+}
+
+template <bool C>
+int run_one(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, double* traj,
+            std::uint64_t* meta, Scratch& sc, Work* w) {
+  std::uint64_t seed;
+  double* x0 = sc.x0.data();
+  decode_sim(net, d, sim, sc.rates.data(), x0, &seed);
+  const kin_method& M = d->method;
+  if (M.kind == KIN_METHOD_ODE)
+    return integrate_rre<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
+  if (M.kind == KIN_METHOD_LSODA)
+    return integrate_lsoda<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
+  return simulate_stochastic<C>(net, sc.rates.data(), x0, M, d->t_end, d->grid, d->n_grid, seed, traj, meta, sc, w);
+}
+
+// EnsembleStatistics::add (Welford), ensemble.hpp:29-30; App. B #9 order.
+inline void welford_add(std::uint64_t n_after, const double* x, double* mean, double* m2, size_t len) {
+  const double nn = static_cast<double>(n_after);
+  for (size_t q = 0; q < len; ++q) {
+    const double delta = x[q] - mean[q];
+    mean[q] = mean[q] + delta / nn;
+    m2[q] = m2[q] + delta * (x[q] - mean[q]);
+  }
+}
+
+}  // namespace kin_oracle
+
+// ============================ C API (ctypes) =================================
+using namespace kin_oracle;
+
+extern "C" {
+
+uint64_t kin_oracle_splitmix64_mix(uint64_t v) { return splitmix64_mix(v); }
+uint64_t kin_oracle_derive_run_seed(uint64_t m, uint64_t i) { return derive_run_seed(m, i); }
+
+// kind: 0 next_u64, 1 uniform, 2 normal, 3 poisson(mean); out as raw bits.
+void kin_oracle_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out) {
+  Stream r(seed);
+  for (int q = 0; q < n; ++q) {
+    uint64_t bits = 0;
+    double v;
+    switch (kind) {
+      case 0: bits = r.next_u64(); break;
+      case 1: v = r.draw_uniform(); std::memcpy(&bits, &v, 8); break;
+      case 2: v = r.draw_normal(); std::memcpy(&bits, &v, 8); break;
+      default: bits = r.draw_poisson(mean); break;
+    }
+    out[q] = bits;
+  }
+}
+
+// One stream: n_each draw_poisson for each mean in order, then n_normal
+// draw_normal (SURVEY Appendix A flag-insensitivity digest).  Normals as bits.
+void kin_oracle_rng_sequence(uint64_t seed, const double* means, int n_means, int n_each, int n_normal,
+                             uint64_t* out) {
+  Stream r(seed);
+  int q = 0;
+  for (int a = 0; a < n_means; ++a)
+    for (int e = 0; e < n_each; ++e) out[q++] = r.draw_poisson(means[a]);
+  for (int e = 0; e < n_normal; ++e) {
+    const double v = r.draw_normal();
+    std::memcpy(&out[q++], &v, 8);
+  }
+}
+
+static int load(const kin_model_desc* d, Network* net, kin_error* err) {
+  std::string msg;
+  const int rc = build_network(d, net, &msg);
+  if (rc != KIN_OK) set_err(err, rc, msg);
+  return rc;
+}
+
+int kin_oracle_model_check(const kin_model_desc* d, kin_error* err) {
+  Network net;
+  return load(d, &net, err);
+}
+
+int kin_oracle_propensities(const kin_model_desc* d, const double* x, double* a, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  std::vector<double> r(net.m);
+  for (int j = 0; j < net.m; ++j) r[j] = net.rate_param[j] >= 0 ? net.params[net.rate_param[j]] : net.rate_base[j];
+  propensities<false>(net, r.data(), x, a, nullptr);
+  return KIN_OK;
+}
+
+int kin_oracle_select_tau(const kin_model_desc* d, const double* x, double eps, double* tau, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  std::vector<double> r(net.m), a(net.m);
+  for (int j = 0; j < net.m; ++j) r[j] = net.rate_param[j] >= 0 ? net.params[net.rate_param[j]] : net.rate_base[j];
+  propensities<false>(net, r.data(), x, a.data(), nullptr);
+  double a0 = 0.0;
+  for (int j = 0; j < net.m; ++j) a0 = a0 + a[j];
+  *tau = a0 == 0.0 ? std::numeric_limits<double>::infinity() : select_tau<false>(net, x, a.data(), eps, nullptr);
+  return KIN_OK;
+}
+
+// ssa_step_from_uniforms: returns fired reaction (>=0) or -1 (Exhausted).
+int kin_oracle_ssa_step_from_uniforms(const kin_model_desc* d, const double* x, double u1, double u2,
+                                      double* dt, int* reaction, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  std::vector<double> r(net.m), a(net.m);
+  for (int j = 0; j < net.m; ++j) r[j] = net.rate_param[j] >= 0 ? net.params[net.rate_param[j]] : net.rate_base[j];
+  propensities<false>(net, r.data(), x, a.data(), nullptr);
+  double a0 = 0.0;
+  for (int j = 0; j < net.m; ++j) a0 = a0 + a[j];
+  if (a0 == 0.0) { *reaction = -1; *dt = 0.0; return KIN_OK; }
+  *dt = std::log(1.0 / u1) / a0;
+  *reaction = ssa_select(net, a.data(), a0, u2);
+  return KIN_OK;
+}
+
+// tau_leap_step_from_counts: *rejected = 1 when any amount would go negative.
+int kin_oracle_tau_leap_from_counts(const kin_model_desc* d, const double* x, const uint64_t* counts,
+                                    double* xout, int* rejected, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  for (int i = 0; i < net.n; ++i) xout[i] = x[i];
+  for (int j = 0; j < net.m; ++j) {
+    if (!counts[j]) continue;
+    for (int p = net.col_ptr[j]; p < net.col_ptr[j + 1]; ++p)
+      xout[net.col_species[p]] = xout[net.col_species[p]] + static_cast<double>(net.col_delta[p]) * static_cast<double>(counts[j]);
+  }
+  *rejected = 0;
+  for (int i = 0; i < net.n; ++i) if (xout[i] < 0.0) *rejected = 1;
+  return KIN_OK;
+}
+
+int kin_oracle_apply_reaction(const kin_model_desc* d, const double* x, int j, double* xout, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  for (int i = 0; i < net.n; ++i) xout[i] = x[i];
+  for (int p = net.col_ptr[j]; p < net.col_ptr[j + 1]; ++p) {
+    const double v = xout[net.col_species[p]] + net.col_delta[p];
+    if (v < 0.0) { set_err(err, KIN_ERR_SIMULATION, "apply_reaction: amount would become negative"); return KIN_ERR_SIMULATION; }
+    xout[net.col_species[p]] = v;
+  }
+  return KIN_OK;
+}
+
+int kin_oracle_rre_rhs(const kin_model_desc* d, const double* x, double* dx, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  std::vector<double> r(net.m), a(net.m);
+  for (int j = 0; j < net.m; ++j) r[j] = net.rate_param[j] >= 0 ? net.params[net.rate_param[j]] : net.rate_base[j];
+  rre_rhs<false>(net, r.data(), x, a.data(), dx, nullptr);
+  return KIN_OK;
+}
+
+// Chan merge (ensemble.hpp:31-33,56-57) of b into a.
+void kin_oracle_stats_merge(uint64_t* na, double* mean_a, double* m2_a, uint64_t nb,
+                            const double* mean_b, const double* m2_b, uint64_t len) {
+  if (nb == 0) return;
+  if (*na == 0) {
+    *na = nb;
+    for (uint64_t q = 0; q < len; ++q) { mean_a[q] = mean_b[q]; m2_a[q] = m2_b[q]; }
+    return;
+  }
+  const double fa = static_cast<double>(*na), fb = static_cast<double>(nb);
+  const double fn = fa + fb;
+  for (uint64_t q = 0; q < len; ++q) {
+    const double delta = mean_b[q] - mean_a[q];
+    mean_a[q] = mean_a[q] + delta * fb / fn;
+    m2_a[q] = m2_a[q] + m2_b[q] + delta * delta * fa * fb / fn;
+  }
+  *na += nb;
+}
+
+// parameter_sweep / run_ensemble / run_single on `workers` std::threads owning
+// contiguous simulation ranges (ensemble.hpp:91-99).  Outputs as in kin_abi.h
+// (host layout [S][G][N]).  Per-point statistics: Welford over each point's runs
+// in ascending run order (the workers=1 merge order).
+int kin_oracle_sweep(const kin_model_desc* md, const kin_sweep_desc* d, kin_sweep_out* out,
+                     kin_error* err, int workers) {
+  if (err) { std::memset(err, 0, sizeof(*err)); }
+  Network net;
+  if (int rc = load(md, &net, err)) return rc;
+  std::string msg;
+  SweepLayout L;
+  if (int rc = sweep_layout(d, &L, &msg)) { set_err(err, rc, msg); return rc; }
+  if (int rc = validate_sweep(net, d, &msg)) { set_err(err, rc, msg); return rc; }
+  const std::uint64_t s0 = d->sim_begin;
+  const std::uint64_t s1 = d->sim_end == 0 ? L.n_sims : std::min<std::uint64_t>(d->sim_end, L.n_sims);
+  if (s0 > s1) { set_err(err, KIN_ERR_USAGE, "empty or inverted simulation range"); return KIN_ERR_USAGE; }
+  const std::uint64_t S = s1 - s0;
+  const int G = d->n_grid, N = net.n;
+  const size_t per = static_cast<size_t>(G) * N;
+  std::vector<double> tmp_traj;
+  double* traj = out ? out->traj : nullptr;
+  const bool need_stats = out && (out->mean || out->m2);
+  if (!traj && need_stats) { tmp_traj.resize(S * per); traj = tmp_traj.data(); }
+  std::vector<std::uint64_t> tmp_meta;
+  std::vector<int32_t> status(S, 0);
+  if (workers < 1) workers = 1;
+  if (static_cast<std::uint64_t>(workers) > S) workers = static_cast<int>(std::max<std::uint64_t>(S, 1));
+  const bool count = out && out->work;
+  auto body = [&](std::uint64_t lo, std::uint64_t hi) {
+    Scratch sc;
+    sc.resize(N, net.m);
+    std::vector<double> scratch_traj(per);
+    std::uint64_t meta_local[6];
+    for (std::uint64_t s = lo; s < hi; ++s) {
+      double* tr = traj ? traj + (s - s0) * per : scratch_traj.data();
+      std::uint64_t* me = (out && out->meta) ? out->meta + (s - s0) * 6 : meta_local;
+      Work w;
+      const int st = count ? run_one<true>(net, d, s, tr, me, sc, &w) : run_one<false>(net, d, s, tr, me, sc, nullptr);
+      status[s - s0] = st;
+      if (count) out->work[s - s0] = w.flops;
+    }
+  };
+  std::vector<std::thread> pool;
+  const std::uint64_t chunk = (S + workers - 1) / std::max(workers, 1);
+  for (int wk = 0; wk < workers; ++wk) {
+    const std::uint64_t lo = s0 + std::min<std::uint64_t>(S, wk * chunk);
+    const std::uint64_t hi = s0 + std::min<std::uint64_t>(S, (wk + 1) * chunk);
+    if (lo >= hi) continue;
+    if (workers == 1) body(lo, hi); else pool.emplace_back(body, lo, hi);
+  }
+  for (auto& th : pool) th.join();
+  if (out && out->status) for (std::uint64_t s = 0; s < S; ++s) out->status[s] = status[s];
+  for (std::uint64_t s = 0; s < S; ++s) {
+    if (status[s] != KIN_SIM_OK) {
+      const std::uint64_t g = s0 + s;
+      if (err) {
+        err->code = KIN_ERR_SIMULATION;
+        err->sim_status = status[s];
+        err->sim_index = g;
+        err->point_index = g / L.runs;
+        err->run_index = g % L.runs;
+        std::snprintf(err->message, sizeof(err->message), "simulation %llu (point %llu, run %llu) failed: status %d",
+                      (unsigned long long)g, (unsigned long long)(g / L.runs), (unsigned long long)(g % L.runs), status[s]);
+      }
+      return KIN_ERR_SIMULATION;
+    }
+  }
+  if (need_stats) {
+    const std::uint64_t p0 = (s0 + L.runs - 1) / L.runs;
+    const std::uint64_t p1 = s1 / L.runs;
+    for (std::uint64_t p = p0; p < p1; ++p) {
+      double* mean = out->mean ? out->mean + (p - p0) * per : nullptr;
+      double* m2 = out->m2 ? out->m2 + (p - p0) * per : nullptr;
+      std::vector<double> mv(per, 0.0), qv(per, 0.0);
+      for (std::uint64_t r = 0; r < L.runs; ++r)
+        welford_add(r + 1, traj + (p * L.runs + r - s0) * per, mv.data(), qv.data(), per);
+      if (mean) std::memcpy(mean, mv.data(), per * sizeof(double));
+      if (m2) std::memcpy(m2, qv.data(), per * sizeof(double));
+    }
+  }
+  return KIN_OK;
+}
+
+int kin_oracle_sweep_size(const kin_sweep_desc* d, uint64_t* np, uint64_t* ns, kin_error* err) {
+  SweepLayout L;
+  std::string msg;
+  if (int rc = sweep_layout(d, &L, &msg)) { set_err(err, rc, msg); return rc; }
+  *np = L.n_points;
+  *ns = L.n_sims;
+  return KIN_OK;
+}
+
+}  // extern "C"
+
+// explicit instantiations used above
+namespace kin_oracle {
+template double select_tau<true>(const Network&, const double*, const double*, double, Work*);
+template double select_tau<false>(const Network&, const double*, const double*, double, Work*);
+}  // namespace kin_oracle

@@ -1,0 +1,145 @@
+// oracle/kin_rng.hpp — TEST INFRASTRUCTURE ONLY (CPU oracle; never on the product path).
+//
+// Restatement of the reference RNG layer, proj/src/rng.cpp + proj/include/kinetics/rng.hpp:
+//   splitmix64 finaliser ............ rng.cpp:18-23   (mix(0) = 0xE220A8397B1DCDAF, rng.hpp:10)
+//   RngStream seeding ............... rng.cpp:25-36   (4 splitmix steps, all-zero guard)
+//   xoshiro256++ next_u64 ........... rng.cpp:38-48
+//   draw_uniform .................... rng.cpp:50-52   (((x>>11)+0.5)*2^-53, open interval)
+//   draw_normal (Box-Muller+spare) .. rng.cpp:54-66
+//   draw_poisson .................... rng.cpp:68-109  (inversion < 10, Hormann PTRS >= 10)
+// Pinned against the reference itself: tests/test_oracle_rng.py compares this
+// restatement with oracle/_ref/ (the reference rng.cpp compiled from
+// /root/reference by oracle/Makefile) and with SURVEY Appendix A vectors.
+//
+// When KIN_ORACLE_REF_RNG is defined the oracle is built against the reference
+// class kinetics::RngStream instead (oracle/_ref/libkin_oracle_refrng.so).
+#pragma once
+
+#include <cmath>
+#include <cstdint>
+
+#ifdef KIN_ORACLE_REF_RNG
+#include "kinetics/rng.hpp"
+#endif
+
+namespace kin_oracle {
+
+inline constexpr std::uint64_t kPhi64 = 0x9E3779B97F4A7C15ULL;
+
+inline std::uint64_t splitmix64_mix(std::uint64_t v) {
+  std::uint64_t z = v + kPhi64;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// ensemble.hpp:15-18 / SPEC.md:411-419
+inline std::uint64_t derive_run_seed(std::uint64_t master, std::uint64_t i) {
+  return splitmix64_mix(master + i * kPhi64);
+}
+
+class Xoshiro256pp {
+ public:
+  explicit Xoshiro256pp(std::uint64_t seed) {
+    // Seeding walks the splitmix64 sequence from `seed`; word w is mix(seed + w*phi)
+    // (each step first advances the state by phi, then finalises it).
+    for (int w = 0; w < 4; ++w) s_[w] = splitmix64_mix(seed + static_cast<std::uint64_t>(w) * kPhi64);
+    if ((s_[0] | s_[1] | s_[2] | s_[3]) == 0) s_[0] = kPhi64;
+  }
+
+  std::uint64_t next_u64() {
+    const std::uint64_t out = rotl(s_[0] + s_[3], 23) + s_[0];
+    const std::uint64_t sh = s_[1] << 17;
+    s_[2] ^= s_[0];
+    s_[3] ^= s_[1];
+    s_[1] ^= s_[2];
+    s_[0] ^= s_[3];
+    s_[2] ^= sh;
+    s_[3] = rotl(s_[3], 45);
+    return out;
+  }
+
+  double draw_uniform() {
+    return (static_cast<double>(next_u64() >> 11) + 0.5) * 0x1.0p-53;
+  }
+
+  double draw_normal() {
+    if (spare_valid_) {
+      spare_valid_ = false;
+      return spare_;
+    }
+    const double u1 = draw_uniform();
+    const double u2 = draw_uniform();
+    const double radius = std::sqrt(-2.0 * std::log(u1));
+    const double angle = 2.0 * 3.141592653589793 * u2;  // 2*pi*u2, pi = std::numbers::pi
+    spare_ = radius * std::sin(angle);
+    spare_valid_ = true;
+    return radius * std::cos(angle);
+  }
+
+  // Work-instrumented Poisson draw; `flops` (may be null) receives the
+  // algorithmic FP64 op count (FMA=2; + - * / sqrt exp log lgamma = 1).
+  std::uint64_t draw_poisson(double mean, std::uint64_t* flops = nullptr) {
+    if (mean <= 0.0) return 0;
+    if (mean < 10.0) {
+      const double u = draw_uniform();
+      double p = std::exp(-mean);
+      double c = p;
+      std::uint64_t k = 0;
+      while (u > c && k < 256) {
+        ++k;
+        p *= mean / static_cast<double>(k);
+        c += p;
+      }
+      if (flops) *flops += 3 + 3 * k;
+      return k;
+    }
+    const double lm = std::log(mean);
+    const double b = 0.931 + 2.53 * std::sqrt(mean);
+    const double a = -0.059 + 0.02483 * b;
+    const double inv_alpha = 1.1239 + 1.1328 / (b - 3.4);
+    const double v_r = 0.9277 - 3.6224 / (b - 2.0);
+    if (flops) *flops += 12;  // log, sqrt, 2 mul, 6 add/sub, 2 div
+    for (;;) {
+      const double u = draw_uniform() - 0.5;
+      const double v = draw_uniform();
+      const double us = 0.5 - std::fabs(u);
+      const double kf = std::floor((2.0 * a / us + b) * u + mean + 0.43);
+      if (flops) *flops += 12;  // 2 uniforms (4) + 8 arithmetic
+      if (kf < 0.0) continue;
+      if (us >= 0.07 && v <= v_r) return static_cast<std::uint64_t>(kf);
+      if (us < 0.013 && v > us) continue;
+      const double lhs = std::log(v * inv_alpha / (a / (us * us) + b));
+      const double rhs = -mean + kf * lm - std::lgamma(kf + 1.0);
+      if (flops) *flops += 11;
+      if (lhs <= rhs) return static_cast<std::uint64_t>(kf);
+    }
+  }
+
+ private:
+  static std::uint64_t rotl(std::uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  std::uint64_t s_[4];
+  double spare_ = 0.0;
+  bool spare_valid_ = false;
+};
+
+#ifdef KIN_ORACLE_REF_RNG
+// The reference stream itself (proj/src/rng.cpp compiled from /root/reference).
+// Work counting is not available through the reference class.
+class RefStream {
+ public:
+  explicit RefStream(std::uint64_t seed) : r_(seed) {}
+  std::uint64_t next_u64() { return r_.next_u64(); }
+  double draw_uniform() { return r_.draw_uniform(); }
+  double draw_normal() { return r_.draw_normal(); }
+  std::uint64_t draw_poisson(double mean, std::uint64_t* = nullptr) { return r_.draw_poisson(mean); }
+
+ private:
+  kinetics::RngStream r_;
+};
+using Stream = RefStream;
+#else
+using Stream = Xoshiro256pp;
+#endif
+
+}  // namespace kin_oracle

@@ -1,0 +1,146 @@
+"""ctypes mirror of ``include/kin_abi.h`` (the C-ABI drop-in boundary).
+
+The structs below are field-for-field copies of the C declarations; the same
+descriptors are handed to the CUDA engine (``libkin_b200.so``) and, in tests
+only, to the CPU oracle (``oracle/lib/libkin_oracle.so``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+PKG_DIR = Path(__file__).resolve().parent
+REPO_DIR = PKG_DIR.parent
+LIB_PATH = PKG_DIR / "libkin_b200.so"
+
+# enum kin_status
+KIN_OK, KIN_ERR_INPUT, KIN_ERR_SIMULATION, KIN_ERR_DEVICE, KIN_ERR_USAGE = 0, 1, 2, 3, 64
+# enum kin_sim_status
+SIM_STATUS = {0: "ok", 1: "step budget exhausted", 2: "non-finite state",
+              3: "negative amount", 4: "step size underflow"}
+# enum kin_method_kind (Method::Kind order, ensemble.hpp:62)
+METHOD_SSA, METHOD_TAU_ADAPTIVE, METHOD_TAU_FIXED, METHOD_CLE, METHOD_ODE, METHOD_HYBRID, METHOD_LSODA = range(7)
+AXIS_PARAM, AXIS_INITIAL = 0, 1
+RNG_COMPAT, RNG_PHILOX = 0, 1
+SEED_SWEEP, SEED_ENSEMBLE, SEED_DIRECT = 0, 1, 2
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+u64p = C.POINTER(C.c_uint64)
+f64p = C.POINTER(C.c_double)
+
+
+class KinModelDesc(C.Structure):
+    _fields_ = [
+        ("n_species", C.c_int32), ("n_reactions", C.c_int32), ("n_params", C.c_int32),
+        ("initial_amounts", i64p), ("rate_constants", f64p), ("rate_param", i32p),
+        ("param_values", f64p),
+        ("reactant_ptr", i32p), ("reactant_species", i32p), ("reactant_stoich", i32p),
+        ("product_ptr", i32p), ("product_species", i32p), ("product_stoich", i32p),
+        ("max_order", C.c_int32),
+    ]
+
+
+class KinIntegratorConfig(C.Structure):
+    _fields_ = [("rel_tol", C.c_double), ("abs_tol", C.c_double), ("h_init", C.c_double),
+                ("h_max", C.c_double), ("max_steps", C.c_uint64)]
+
+
+class KinMethod(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("tau", C.c_double), ("epsilon", C.c_double),
+                ("integrator", KinIntegratorConfig)]
+
+
+class KinSweepAxis(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("index", C.c_int32), ("n_values", C.c_int32),
+                ("values", f64p)]
+
+
+class KinSweepDesc(C.Structure):
+    _fields_ = [
+        ("method", KinMethod), ("n_axes", C.c_int32), ("axes", C.POINTER(KinSweepAxis)),
+        ("runs_per_point", C.c_uint64), ("master_seed", C.c_uint64),
+        ("seed_mode", C.c_int32), ("rng_mode", C.c_int32),
+        ("t_end", C.c_double), ("n_grid", C.c_int32), ("grid", f64p),
+        ("sim_begin", C.c_uint64), ("sim_end", C.c_uint64),
+    ]
+
+
+class KinSweepOut(C.Structure):
+    _fields_ = [("traj", f64p), ("meta", u64p), ("status", i32p), ("mean", f64p),
+                ("m2", f64p), ("work", u64p)]
+
+
+class KinError(C.Structure):
+    _fields_ = [("code", C.c_int32), ("sim_status", C.c_int32), ("sim_index", C.c_uint64),
+                ("point_index", C.c_uint64), ("run_index", C.c_uint64),
+                ("message", C.c_char * 256)]
+
+    def text(self) -> str:
+        return self.message.decode(errors="replace")
+
+
+# Every symbol include/kin_abi.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = (
+    "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
+    "kin_model_free", "kin_sweep_size", "kin_sweep_run", "kin_sweep_launch", "kin_sweep_sync",
+    "kin_sweep_fetch", "kin_ctx_stream", "kin_splitmix64_mix", "kin_derive_run_seed",
+    "kin_device_rng_draws", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
+)
+
+
+def _declare(lib: C.CDLL) -> C.CDLL:
+    vp = C.c_void_p
+    E = C.POINTER(KinError)
+    sig = {
+        "kin_ctx_create": (C.c_int, [i32p, C.c_int32, C.POINTER(vp), E]),
+        "kin_ctx_destroy": (None, [vp]),
+        "kin_ctx_device_count": (C.c_int32, [vp]),
+        "kin_model_upload": (C.c_int, [vp, C.POINTER(KinModelDesc), C.POINTER(vp), E]),
+        "kin_model_free": (None, [vp]),
+        "kin_sweep_size": (C.c_int, [C.POINTER(KinSweepDesc), u64p, u64p, E]),
+        "kin_sweep_run": (C.c_int, [vp, vp, C.POINTER(KinSweepDesc), C.POINTER(KinSweepOut), E]),
+        "kin_sweep_launch": (C.c_int, [vp, vp, C.POINTER(KinSweepDesc), C.c_int32, C.c_int32, C.c_int32, E]),
+        "kin_sweep_sync": (C.c_int, [vp, C.c_int32, E]),
+        "kin_sweep_fetch": (C.c_int, [vp, C.c_int32, C.POINTER(KinSweepOut), E]),
+        "kin_ctx_stream": (vp, [vp, C.c_int32]),
+        "kin_splitmix64_mix": (C.c_uint64, [C.c_uint64]),
+        "kin_derive_run_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
+        "kin_device_rng_draws": (C.c_int, [vp, C.c_uint64, C.c_int32, C.c_double, C.c_int32, u64p, E]),
+        "kin_measure_fp64_peak": (C.c_int, [vp, f64p, E]),
+        "kin_status_string": (C.c_char_p, [C.c_int32]),
+        "kin_abi_version": (C.c_int32, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_LIB = None
+
+
+def load_library(path: os.PathLike | None = None) -> C.CDLL:
+    """Load the in-tree CUDA engine.  Fails loudly when it has not been built:
+    there is no CPU fallback on the product path."""
+    global _LIB
+    if _LIB is not None and path is None:
+        return _LIB
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"{p} is missing: build the CUDA engine first (python -c 'import __graft_entry__ as g; g.build()' "
+            "or make -C paper_1309_7695_b200/csrc). There is no CPU fallback.")
+    lib = _declare(C.CDLL(str(p)))
+    if path is None:
+        _LIB = lib
+    return lib
+
+
+def ptr(arr, ctype):
+    """Pointer to a contiguous numpy array (or None)."""
+    if arr is None:
+        return None
+    return arr.ctypes.data_as(C.POINTER(ctype))

@@ -1,0 +1,163 @@
+// kin_device.cuh — device-side model tables, RNG and propensity helpers.
+//
+// Every function here mirrors, operation for operation, the CPU oracle
+// (oracle/kin_oracle.cpp, oracle/kin_rng.hpp), which restates the reference
+// (proj/src/rng.cpp, model.hpp, stochastic.hpp).  The stochastic translation
+// unit is compiled with -fmad=false so + - * / round exactly as the oracle's
+// -ffp-contract=off build; integer work (xoshiro256++, firing counts, state
+// updates) is exact by construction.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "kin_tables.h"
+
+namespace kin {
+
+constexpr uint64_t kPhi64 = 0x9E3779B97F4A7C15ULL;
+
+// ---- table accessors (warp-uniform index -> constant-bank broadcast) -------
+__device__ __forceinline__ double tab_rate(const KinTables& T, int j) {
+  return reinterpret_cast<const double*>(T.blob + T.off_rate)[j];
+}
+__device__ __forceinline__ int tab_rate_axis(const KinTables& T, int j) {
+  return reinterpret_cast<const int8_t*>(T.blob + T.off_rate_axis)[j];
+}
+__device__ __forceinline__ double tab_x0(const KinTables& T, int i) {
+  return reinterpret_cast<const double*>(T.blob + T.off_x0)[i];
+}
+__device__ __forceinline__ int tab_x0_axis(const KinTables& T, int i) {
+  return reinterpret_cast<const int8_t*>(T.blob + T.off_x0_axis)[i];
+}
+__device__ __forceinline__ double tab_g(const KinTables& T, int i) {
+  return reinterpret_cast<const double*>(T.blob + T.off_g)[i];
+}
+__device__ __forceinline__ int tab_rt_ptr(const KinTables& T, int j) {
+  return reinterpret_cast<const int16_t*>(T.blob + T.off_rt_ptr)[j];
+}
+__device__ __forceinline__ uint32_t tab_rt(const KinTables& T, int p) {
+  return reinterpret_cast<const uint32_t*>(T.blob + T.off_rt)[p];
+}
+__device__ __forceinline__ int tab_col_ptr(const KinTables& T, int j) {
+  return reinterpret_cast<const int16_t*>(T.blob + T.off_col_ptr)[j];
+}
+__device__ __forceinline__ uint32_t tab_col(const KinTables& T, int p) {
+  return reinterpret_cast<const uint32_t*>(T.blob + T.off_col)[p];
+}
+__device__ __forceinline__ int tab_row_ptr(const KinTables& T, int i) {
+  return reinterpret_cast<const int16_t*>(T.blob + T.off_row_ptr)[i];
+}
+__device__ __forceinline__ uint32_t tab_row(const KinTables& T, int p) {
+  return reinterpret_cast<const uint32_t*>(T.blob + T.off_row)[p];
+}
+__device__ __forceinline__ double tab_grid(const KinTables& T, const KinSweepDev& S, int g) {
+  return T.off_grid ? reinterpret_cast<const double*>(T.blob + T.off_grid)[g] : __ldg(S.grid + g);
+}
+
+// ---- seeds (rng.cpp:18-23; ensemble.hpp:15-18) -------------------------------
+__host__ __device__ __forceinline__ uint64_t splitmix64_mix(uint64_t v) {
+  uint64_t z = v + kPhi64;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t derive_run_seed(uint64_t master, uint64_t i) {
+  return splitmix64_mix(master + i * kPhi64);
+}
+
+// Seed of global simulation `sim` (kin_abi.h enum kin_seed_mode).
+__device__ __forceinline__ uint64_t sim_seed(const KinSweepDev& S, uint64_t sim) {
+  if (S.seed_mode == 1) return derive_run_seed(S.master_seed, sim);
+  if (S.seed_mode == 2) return sim == 0 ? S.master_seed : derive_run_seed(S.master_seed, sim);
+  const uint64_t point = sim / S.runs, run = sim - point * S.runs;
+  return derive_run_seed(derive_run_seed(S.master_seed, point), run);
+}
+
+// ---- xoshiro256++ stream (rng.cpp:25-52) ------------------------------------
+struct Xoshiro {
+  uint64_t s0, s1, s2, s3;
+
+  __device__ __forceinline__ void seed(uint64_t seed) {
+    s0 = splitmix64_mix(seed);
+    s1 = splitmix64_mix(seed + kPhi64);
+    s2 = splitmix64_mix(seed + 2 * kPhi64);
+    s3 = splitmix64_mix(seed + 3 * kPhi64);
+    if ((s0 | s1 | s2 | s3) == 0) s0 = kPhi64;
+  }
+  __device__ __forceinline__ static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t out = rotl(s0 + s3, 23) + s0;
+    const uint64_t sh = s1 << 17;
+    s2 ^= s0;
+    s3 ^= s1;
+    s1 ^= s2;
+    s0 ^= s3;
+    s2 ^= sh;
+    s3 = rotl(s3, 45);
+    return out;
+  }
+  // ((x >> 11) + 0.5) * 2^-53: exact in double, identical on every platform.
+  __device__ __forceinline__ double uniform() {
+    return __dmul_rn(__dadd_rn(static_cast<double>(next() >> 11), 0.5), 0x1.0p-53);
+  }
+};
+
+// draw_poisson (rng.cpp:68-109): inversion below mean 10, Hormann PTRS above.
+// `flops` receives the algorithmic op count (same accounting as the oracle).
+template <bool kCount>
+__device__ __forceinline__ uint64_t poisson(Xoshiro& rng, double mean, uint64_t& flops) {
+  if (!(mean > 0.0)) return 0;
+  if (mean < 10.0) {
+    const double u = rng.uniform();
+    double p = exp(-mean);
+    double c = p;
+    uint64_t k = 0;
+    while (u > c && k < 256) {
+      ++k;
+      p = __dmul_rn(p, __ddiv_rn(mean, static_cast<double>(k)));
+      c = __dadd_rn(c, p);
+    }
+    if (kCount) flops += 3 + 3 * k;
+    return k;
+  }
+  const double lm = log(mean);
+  const double b = __dadd_rn(0.931, __dmul_rn(2.53, sqrt(mean)));
+  const double a = __dadd_rn(-0.059, __dmul_rn(0.02483, b));
+  const double inv_alpha = __dadd_rn(1.1239, __ddiv_rn(1.1328, __dsub_rn(b, 3.4)));
+  const double v_r = __dsub_rn(0.9277, __ddiv_rn(3.6224, __dsub_rn(b, 2.0)));
+  if (kCount) flops += 12;
+  for (;;) {
+    const double u = __dsub_rn(rng.uniform(), 0.5);
+    const double v = rng.uniform();
+    const double us = __dsub_rn(0.5, fabs(u));
+    const double kf = floor(__dadd_rn(__dadd_rn(__dmul_rn(__dadd_rn(__ddiv_rn(__dmul_rn(2.0, a), us), b), u), mean), 0.43));
+    if (kCount) flops += 12;
+    if (kf < 0.0) continue;
+    if (us >= 0.07 && v <= v_r) return static_cast<uint64_t>(kf);
+    if (us < 0.013 && v > us) continue;
+    const double lhs = log(__ddiv_rn(__dmul_rn(v, inv_alpha), __dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b)));
+    const double rhs = __dsub_rn(__dadd_rn(-mean, __dmul_rn(kf, lm)), lgamma(__dadd_rn(kf, 1.0)));
+    if (kCount) flops += 11;
+    if (lhs <= rhs) return static_cast<uint64_t>(kf);
+  }
+}
+
+// combinations (model.hpp:145-149) + order-3 extension; clamp >= 0.
+__device__ __forceinline__ double combinations(double x, int s) {
+  double h;
+  if (s == 1) {
+    h = x;
+  } else if (s == 2) {
+    h = __ddiv_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), 2.0);
+  } else if (s == 3) {
+    h = __ddiv_rn(__dmul_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), __dsub_rn(x, 2.0)), 6.0);
+  } else {
+    return 1.0;
+  }
+  return h < 0.0 ? 0.0 : h;
+}
+__device__ __forceinline__ int combinations_flops(int s) { return s <= 1 ? 0 : (s == 2 ? 3 : 5); }
+
+}  // namespace kin

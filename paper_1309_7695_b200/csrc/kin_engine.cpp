@@ -1,0 +1,751 @@
+// kin_engine.cpp — host side of the B200 sweep engine: the C ABI of
+// include/kin_abi.h.
+//
+// Replaces the reference's ensemble layer (proj/include/kinetics/ensemble.hpp):
+//   parameter_sweep  ensemble.hpp:126-130  -> kin_sweep_run (KIN_SEED_SWEEP)
+//   run_ensemble     ensemble.hpp:91-99    -> kin_sweep_run (KIN_SEED_ENSEMBLE)
+//   run_single       ensemble.hpp:73-76    -> kin_sweep_run (KIN_SEED_DIRECT)
+// and the model loader ReactionNetwork::create (model.hpp:47-53).
+//
+// The reference's worker pool (contiguous run ranges per std::thread,
+// ensemble.hpp:91-96) becomes one host thread per GPU of the context; the
+// simulation index space is cut into whole-point chunks assigned cyclically to
+// the GPUs (balances the cost gradient along the sweep axes).  Per-run results
+// depend only on the global simulation index, never on the device count
+// (SPEC.md:449).  No collective: each GPU copies its chunk's outputs straight
+// into the caller's host buffers at the chunk's global offset.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/kin_abi.h"
+#include "kin_device.cuh"
+#include "kin_launch.h"
+#include "kin_tables.h"
+
+namespace {
+
+void set_err(kin_error* e, int code, const std::string& msg) {
+  if (!e) return;
+  e->code = code;
+  std::snprintf(e->message, sizeof(e->message), "%s", msg.c_str());
+}
+
+// ---- model (ReactionNetwork::create, model.hpp:47-53) -------------------------
+struct HostModel {
+  int n = 0, m = 0;
+  std::vector<double> x0, rate_base, params;
+  std::vector<int> rate_param;
+  std::vector<int> rt_ptr, rt_species, rt_stoich;
+  std::vector<int> col_ptr, col_species, col_delta;
+  std::vector<int> row_ptr, row_reaction, row_delta;
+  std::vector<int> g;
+  int fprop = 0;
+};
+
+int load_model(const kin_model_desc* d, HostModel* H, std::string* msg) {
+  if (!d) { *msg = "null model descriptor"; return KIN_ERR_USAGE; }
+  const int n = d->n_species, m = d->n_reactions, np = d->n_params;
+  if (n < 0 || m < 0 || np < 0) { *msg = "negative model dimension"; return KIN_ERR_INPUT; }
+  if (n > 4096 || m > 8192) { *msg = "model too large for the device tables"; return KIN_ERR_INPUT; }
+  if ((n > 0 && !d->initial_amounts) || (m > 0 && (!d->rate_constants || !d->reactant_ptr || !d->product_ptr)) ||
+      (np > 0 && !d->param_values)) {
+    *msg = "missing model array";
+    return KIN_ERR_USAGE;
+  }
+  const int max_order = d->max_order <= 0 ? 2 : d->max_order;
+  if (max_order > 3) { *msg = "max_order above 3 is not supported"; return KIN_ERR_INPUT; }
+  HostModel& M = *H;
+  M = HostModel{};
+  M.n = n;
+  M.m = m;
+  for (int i = 0; i < n; ++i) {
+    if (d->initial_amounts[i] < 0) { *msg = "species " + std::to_string(i) + ": negative initial amount"; return KIN_ERR_INPUT; }
+    M.x0.push_back(static_cast<double>(d->initial_amounts[i]));
+  }
+  for (int p = 0; p < np; ++p) {
+    if (!(d->param_values[p] > 0.0) || !std::isfinite(d->param_values[p])) {
+      *msg = "param " + std::to_string(p) + ": rate must be positive";
+      return KIN_ERR_INPUT;
+    }
+    M.params.push_back(d->param_values[p]);
+  }
+  std::vector<int> nu(static_cast<size_t>(n) * m, 0);
+  M.g.assign(n, 1);
+  M.rt_ptr.push_back(0);
+  M.col_ptr.push_back(0);
+  for (int j = 0; j < m; ++j) {
+    const int rp = d->rate_param ? d->rate_param[j] : -1;
+    if (rp >= np || rp < -1) { *msg = "reaction " + std::to_string(j) + ": unknown parameter"; return KIN_ERR_INPUT; }
+    const double c = rp >= 0 ? d->param_values[rp] : d->rate_constants[j];
+    if (!(c > 0.0) || !std::isfinite(c)) { *msg = "reaction " + std::to_string(j) + ": rate must be positive"; return KIN_ERR_INPUT; }
+    M.rate_base.push_back(d->rate_constants[j]);
+    M.rate_param.push_back(rp);
+    int order = 0, prev = -1;
+    for (int p = d->reactant_ptr[j]; p < d->reactant_ptr[j + 1]; ++p) {
+      const int s = d->reactant_species[p], st = d->reactant_stoich[p];
+      if (s < 0 || s >= n) { *msg = "reaction " + std::to_string(j) + ": undeclared species"; return KIN_ERR_INPUT; }
+      if (s <= prev) { *msg = "reaction " + std::to_string(j) + ": reactants must be species-ascending and unique"; return KIN_ERR_INPUT; }
+      if (st <= 0) { *msg = "reaction " + std::to_string(j) + ": stoichiometry must be positive"; return KIN_ERR_INPUT; }
+      prev = s;
+      order += st;
+      M.rt_species.push_back(s);
+      M.rt_stoich.push_back(st);
+      M.fprop += 1 + (st <= 1 ? 0 : (st == 2 ? 3 : 5));
+      nu[static_cast<size_t>(s) * m + j] -= st;
+    }
+    if (order > max_order) {
+      *msg = "reaction " + std::to_string(j) + ": reactant order " + std::to_string(order) + " exceeds " + std::to_string(max_order);
+      return KIN_ERR_INPUT;
+    }
+    for (int p = d->reactant_ptr[j]; p < d->reactant_ptr[j + 1]; ++p)
+      M.g[d->reactant_species[p]] = std::max(M.g[d->reactant_species[p]], order);
+    prev = -1;
+    for (int p = d->product_ptr[j]; p < d->product_ptr[j + 1]; ++p) {
+      const int s = d->product_species[p], st = d->product_stoich[p];
+      if (s < 0 || s >= n) { *msg = "reaction " + std::to_string(j) + ": undeclared species"; return KIN_ERR_INPUT; }
+      if (s <= prev) { *msg = "reaction " + std::to_string(j) + ": products must be species-ascending and unique"; return KIN_ERR_INPUT; }
+      if (st <= 0) { *msg = "reaction " + std::to_string(j) + ": stoichiometry must be positive"; return KIN_ERR_INPUT; }
+      prev = s;
+      nu[static_cast<size_t>(s) * m + j] += st;
+    }
+    M.rt_ptr.push_back(static_cast<int>(M.rt_species.size()));
+    for (int s = 0; s < n; ++s) {
+      const int dl = nu[static_cast<size_t>(s) * m + j];
+      if (dl == 0) continue;
+      if (dl < -128 || dl > 127) { *msg = "reaction " + std::to_string(j) + ": net stoichiometry out of range"; return KIN_ERR_INPUT; }
+      M.col_species.push_back(s);
+      M.col_delta.push_back(dl);
+    }
+    M.col_ptr.push_back(static_cast<int>(M.col_species.size()));
+  }
+  M.row_ptr.push_back(0);
+  for (int s = 0; s < n; ++s) {
+    for (int j = 0; j < m; ++j) {
+      const int dl = nu[static_cast<size_t>(s) * m + j];
+      if (dl != 0) { M.row_reaction.push_back(j); M.row_delta.push_back(dl); }
+    }
+    M.row_ptr.push_back(static_cast<int>(M.row_reaction.size()));
+  }
+  return KIN_OK;
+}
+
+// ---- sweep validation (SweepConfig, ensemble.hpp:101-113) ----
+struct Layout {
+  uint64_t P = 1, R = 1, S = 1;
+};
+
+int sweep_layout(const kin_sweep_desc* d, Layout* L, std::string* msg) {
+  if (!d) { *msg = "null sweep descriptor"; return KIN_ERR_USAGE; }
+  if (d->n_axes < 0 || d->n_axes > KIN_MAX_AXES || (d->n_axes > 0 && !d->axes)) {
+    *msg = "at most " + std::to_string(KIN_MAX_AXES) + " sweep axes";
+    return KIN_ERR_INPUT;
+  }
+  uint64_t P = 1;
+  for (int ax = 0; ax < d->n_axes; ++ax) {
+    const kin_sweep_axis& A = d->axes[ax];
+    if (A.n_values <= 0 || !A.values) { *msg = "axis " + std::to_string(ax) + ": empty value list"; return KIN_ERR_INPUT; }
+    if (P > (uint64_t{1} << 40) / static_cast<uint64_t>(A.n_values)) { *msg = "sweep too large"; return KIN_ERR_INPUT; }
+    P *= static_cast<uint64_t>(A.n_values);
+  }
+  if (d->runs_per_point == 0) { *msg = "runs_per_point must be >= 1"; return KIN_ERR_INPUT; }
+  L->P = P;
+  L->R = d->runs_per_point;
+  L->S = P * d->runs_per_point;
+  return KIN_OK;
+}
+
+int validate_sweep(const HostModel& net, const kin_sweep_desc* d, const Layout& L, std::string* msg) {
+  const kin_method& M = d->method;
+  if (M.kind == KIN_METHOD_CLE || M.kind == KIN_METHOD_HYBRID) {
+    *msg = "method not provided by this engine (CLE/hybrid are out of scope)";
+    return KIN_ERR_INPUT;
+  }
+  if (M.kind == KIN_METHOD_LSODA) { *msg = "LSODA not built"; return KIN_ERR_INPUT; }
+  if (M.kind < 0 || M.kind > KIN_METHOD_LSODA) { *msg = "unknown method kind"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_TAU_FIXED && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_TAU_ADAPTIVE && !(M.epsilon > 0.0 && M.epsilon < 1.0)) { *msg = "epsilon must be in (0,1)"; return KIN_ERR_INPUT; }
+  if (M.integrator.max_steps == 0) { *msg = "max_steps must be positive"; return KIN_ERR_INPUT; }
+  if ((M.kind == KIN_METHOD_ODE || M.kind == KIN_METHOD_LSODA) && !(M.integrator.rel_tol > 0.0 && M.integrator.abs_tol > 0.0)) {
+    *msg = "tolerances must be positive";
+    return KIN_ERR_INPUT;
+  }
+  if (!(d->t_end >= 0.0) || !std::isfinite(d->t_end)) { *msg = "t_end must be finite and non-negative"; return KIN_ERR_INPUT; }
+  if (d->n_grid < 0 || (d->n_grid > 0 && !d->grid)) { *msg = "bad grid"; return KIN_ERR_USAGE; }
+  for (int g = 0; g < d->n_grid; ++g) {
+    if (!(d->grid[g] >= 0.0 && d->grid[g] <= d->t_end)) { *msg = "grid point outside [0, t_end]"; return KIN_ERR_INPUT; }
+    if (g > 0 && !(d->grid[g] > d->grid[g - 1])) { *msg = "grid must be strictly increasing"; return KIN_ERR_INPUT; }
+  }
+  for (int ax = 0; ax < d->n_axes; ++ax) {
+    const kin_sweep_axis& A = d->axes[ax];
+    if (A.kind == KIN_AXIS_PARAM) {
+      if (A.index < 0 || A.index >= static_cast<int>(net.params.size())) {
+        *msg = "axis " + std::to_string(ax) + ": unknown parameter";
+        return KIN_ERR_INPUT;
+      }
+      for (int v = 0; v < A.n_values; ++v)
+        if (!(A.values[v] > 0.0) || !std::isfinite(A.values[v])) {
+          *msg = "axis " + std::to_string(ax) + ": rate values must be positive";
+          return KIN_ERR_INPUT;
+        }
+    } else if (A.kind == KIN_AXIS_INITIAL) {
+      if (A.index < 0 || A.index >= net.n) { *msg = "axis " + std::to_string(ax) + ": unknown species"; return KIN_ERR_INPUT; }
+      for (int v = 0; v < A.n_values; ++v)
+        if (!(A.values[v] >= 0.0) || A.values[v] != std::floor(A.values[v]) || A.values[v] > 9007199254740992.0) {
+          *msg = "axis " + std::to_string(ax) + ": initial amounts must be non-negative integers";
+          return KIN_ERR_INPUT;
+        }
+    } else {
+      *msg = "axis " + std::to_string(ax) + ": unknown axis kind";
+      return KIN_ERR_INPUT;
+    }
+  }
+  if (d->seed_mode == KIN_SEED_DIRECT && L.S != 1) { *msg = "direct seeding needs exactly one simulation"; return KIN_ERR_INPUT; }
+  if (d->rng_mode != KIN_RNG_COMPAT) { *msg = "rng_mode: only the compat (reference xoshiro256++) stream is built"; return KIN_ERR_INPUT; }
+  return KIN_OK;
+}
+
+// Pack the model + the sweep's axis bindings into the kernel-parameter tables.
+int pack_tables(const HostModel& H, const kin_sweep_desc* d, KinTables* T, std::string* msg) {
+  std::memset(T, 0, sizeof(KinTables));
+  T->n = H.n;
+  T->m = H.m;
+  T->nnz = static_cast<int32_t>(H.col_species.size());
+  T->n_grid = d->n_grid;
+  T->fprop = H.fprop;
+  // effective parameter values (non-swept) and which axis overrides what
+  std::vector<int> param_axis(H.params.size(), -1), x0_axis(H.n, -1);
+  for (int ax = 0; ax < d->n_axes; ++ax) {
+    if (d->axes[ax].kind == KIN_AXIS_PARAM) param_axis[d->axes[ax].index] = ax;
+    else x0_axis[d->axes[ax].index] = ax;
+  }
+  size_t off = 0;
+  bool overflow = false;
+  auto put = [&](const void* src, size_t bytes, size_t align) -> uint32_t {
+    off = (off + align - 1) / align * align;
+    if (off + bytes > KIN_TABLE_BYTES) { overflow = true; return 0; }
+    const uint32_t at = static_cast<uint32_t>(off);
+    if (bytes) std::memcpy(T->blob + off, src, bytes);
+    off += bytes;
+    return at;
+  };
+  std::vector<double> rate(H.m);
+  std::vector<int8_t> rate_axis(H.m, -1);
+  for (int j = 0; j < H.m; ++j) {
+    const int rp = H.rate_param[j];
+    rate[j] = rp >= 0 ? H.params[rp] : H.rate_base[j];
+    if (rp >= 0 && param_axis[rp] >= 0) rate_axis[j] = static_cast<int8_t>(param_axis[rp]);
+  }
+  std::vector<int8_t> x0ax(H.n);
+  for (int i = 0; i < H.n; ++i) x0ax[i] = static_cast<int8_t>(x0_axis[i]);
+  std::vector<double> gd(H.g.begin(), H.g.end());
+  if (H.rt_species.size() > 32767 || H.col_species.size() > 32767) { *msg = "model too large for the device tables"; return KIN_ERR_INPUT; }
+  std::vector<int16_t> rt_ptr(H.rt_ptr.begin(), H.rt_ptr.end()), col_ptr(H.col_ptr.begin(), H.col_ptr.end()),
+      row_ptr(H.row_ptr.begin(), H.row_ptr.end());
+  std::vector<uint32_t> rt(H.rt_species.size()), col(H.col_species.size()), row(H.row_reaction.size());
+  for (size_t p = 0; p < rt.size(); ++p)
+    rt[p] = static_cast<uint32_t>(H.rt_species[p]) | (static_cast<uint32_t>(H.rt_stoich[p]) << 16);
+  for (size_t p = 0; p < col.size(); ++p)
+    col[p] = static_cast<uint32_t>(H.col_species[p]) | (static_cast<uint32_t>(H.col_delta[p] + 128) << 16);
+  for (size_t p = 0; p < row.size(); ++p)
+    row[p] = static_cast<uint32_t>(H.row_reaction[p]) | (static_cast<uint32_t>(H.row_delta[p] + 128) << 16);
+  for (size_t p = 0; p < H.rt_stoich.size(); ++p)
+    if (H.rt_stoich[p] > 255) { *msg = "stoichiometry out of range"; return KIN_ERR_INPUT; }
+  T->off_rate = put(rate.data(), rate.size() * 8, 8);
+  T->off_x0 = put(H.x0.data(), H.x0.size() * 8, 8);
+  T->off_g = put(gd.data(), gd.size() * 8, 8);
+  T->off_rt = put(rt.data(), rt.size() * 4, 4);
+  T->off_col = put(col.data(), col.size() * 4, 4);
+  T->off_row = put(row.data(), row.size() * 4, 4);
+  T->off_rt_ptr = put(rt_ptr.data(), rt_ptr.size() * 2, 2);
+  T->off_col_ptr = put(col_ptr.data(), col_ptr.size() * 2, 2);
+  T->off_row_ptr = put(row_ptr.data(), row_ptr.size() * 2, 2);
+  T->off_rate_axis = put(rate_axis.data(), rate_axis.size(), 1);
+  T->off_x0_axis = put(x0ax.data(), x0ax.size(), 1);
+  if (overflow) { *msg = "model too large for the device tables"; return KIN_ERR_INPUT; }
+  // the grid rides along when it fits (offset 0 = "use the global copy")
+  const size_t save = off;
+  const uint32_t og = put(d->grid, static_cast<size_t>(d->n_grid) * 8, 8);
+  if (overflow || d->n_grid == 0 || og == 0) {
+    overflow = false;
+    off = save;
+    T->off_grid = 0;
+  } else {
+    T->off_grid = og;
+  }
+  T->used = static_cast<uint32_t>(off);
+  return KIN_OK;
+}
+
+// ---- device slots -------------------------------------------------------------
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+    if (e == cudaSuccess) cap = n;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+struct Slot {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DevBuf<double> traj, traj_t, mean, m2, axis, grid;
+  DevBuf<uint64_t> meta, work;
+  DevBuf<int32_t> status;
+  void* stage = nullptr;
+  size_t stage_cap = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  // record of the last device-resident launch
+  uint64_t s0 = 0, s1 = 0, P0 = 0, nP = 0, R = 1;
+  int G = 0, N = 0;
+  bool have_stats = false, have_work = false, valid = false;
+  std::mutex mu;
+};
+
+}  // namespace
+
+struct kin_ctx {
+  std::vector<std::unique_ptr<Slot>> slots;
+};
+
+struct kin_model {
+  kin_ctx* ctx;
+  HostModel host;
+};
+
+namespace {
+
+int cuda_fail(kin_error* err, cudaError_t e, const char* what) {
+  set_err(err, KIN_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+  return KIN_ERR_DEVICE;
+}
+
+#define KIN_CUDA(call, what)                        \
+  do {                                              \
+    cudaError_t e_ = (call);                        \
+    if (e_ != cudaSuccess) return cuda_fail(err, e_, what); \
+  } while (0)
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// D2H into a caller buffer: direct when pinned, else through a pinned double buffer.
+int copy_d2h(Slot& sl, void* dst, const void* src, size_t bytes, kin_error* err) {
+  if (bytes == 0) return KIN_OK;
+  if (is_pinned(dst)) {
+    KIN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, sl.stream), "D2H");
+    KIN_CUDA(cudaStreamSynchronize(sl.stream), "D2H sync");
+    return KIN_OK;
+  }
+  const size_t piece = size_t{32} << 20;
+  if (!sl.stage) {
+    KIN_CUDA(cudaMallocHost(&sl.stage, 2 * piece), "pinned staging");
+    sl.stage_cap = 2 * piece;
+    KIN_CUDA(cudaEventCreateWithFlags(&sl.ev[0], cudaEventDisableTiming), "event");
+    KIN_CUDA(cudaEventCreateWithFlags(&sl.ev[1], cudaEventDisableTiming), "event");
+  }
+  char* out = static_cast<char*>(dst);
+  const char* in = static_cast<const char*>(src);
+  char* buf[2] = {static_cast<char*>(sl.stage), static_cast<char*>(sl.stage) + piece};
+  size_t pending_off = 0, pending_len = 0;
+  int pending_b = -1, b = 0;
+  for (size_t off = 0; off < bytes; off += piece) {
+    const size_t len = std::min(piece, bytes - off);
+    KIN_CUDA(cudaMemcpyAsync(buf[b], in + off, len, cudaMemcpyDeviceToHost, sl.stream), "D2H");
+    KIN_CUDA(cudaEventRecord(sl.ev[b], sl.stream), "event");
+    if (pending_b >= 0) {
+      KIN_CUDA(cudaEventSynchronize(sl.ev[pending_b]), "D2H sync");
+      std::memcpy(out + pending_off, buf[pending_b], pending_len);
+    }
+    pending_b = b;
+    pending_off = off;
+    pending_len = len;
+    b ^= 1;
+  }
+  KIN_CUDA(cudaEventSynchronize(sl.ev[pending_b]), "D2H sync");
+  std::memcpy(out + pending_off, buf[pending_b], pending_len);
+  return KIN_OK;
+}
+
+// Launch the simulation kernels for global sims [s0, s1) on a slot (device-resident).
+int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const Layout& L, uint64_t s0, uint64_t s1,
+                 bool want_stats, bool want_work, kin_error* err) {
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  KinTables* T = new KinTables;
+  std::unique_ptr<KinTables> Tguard(T);
+  std::string msg;
+  if (int rc = pack_tables(H, d, T, &msg)) { set_err(err, rc, msg); return rc; }
+  const uint64_t S = s1 - s0;
+  const int G = d->n_grid, N = H.n;
+  const size_t gn = static_cast<size_t>(G) * N;
+  KIN_CUDA(sl.traj.ensure(std::max<size_t>(gn * S, 1)), "cudaMalloc traj");
+  KIN_CUDA(sl.meta.ensure(std::max<uint64_t>(S * 6, 1)), "cudaMalloc meta");
+  KIN_CUDA(sl.status.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc status");
+  if (want_work) KIN_CUDA(sl.work.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc work");
+  // axis values and grid
+  size_t nax = 0;
+  for (int ax = 0; ax < d->n_axes; ++ax) nax += d->axes[ax].n_values;
+  KIN_CUDA(sl.axis.ensure(std::max<size_t>(nax, 1)), "cudaMalloc axes");
+  KIN_CUDA(sl.grid.ensure(std::max<int>(G, 1)), "cudaMalloc grid");
+  KinSweepDev SD;
+  std::memset(&SD, 0, sizeof(SD));
+  SD.kind = d->method.kind;
+  SD.rng_mode = d->rng_mode;
+  SD.tau = d->method.tau;
+  SD.epsilon = d->method.epsilon;
+  SD.rel_tol = d->method.integrator.rel_tol;
+  SD.abs_tol = d->method.integrator.abs_tol;
+  SD.h_init = d->method.integrator.h_init;
+  SD.h_max = d->method.integrator.h_max;
+  SD.max_steps = d->method.integrator.max_steps;
+  SD.n_axes = d->n_axes;
+  SD.seed_mode = d->seed_mode;
+  size_t at = 0;
+  for (int ax = 0; ax < d->n_axes; ++ax) {
+    SD.axis_kind[ax] = d->axes[ax].kind;
+    SD.axis_n[ax] = d->axes[ax].n_values;
+    SD.axis_values[ax] = sl.axis.p + at;
+    KIN_CUDA(cudaMemcpyAsync(sl.axis.p + at, d->axes[ax].values, sizeof(double) * d->axes[ax].n_values,
+                             cudaMemcpyHostToDevice, sl.stream), "H2D axes");
+    at += d->axes[ax].n_values;
+  }
+  if (G) KIN_CUDA(cudaMemcpyAsync(sl.grid.p, d->grid, sizeof(double) * G, cudaMemcpyHostToDevice, sl.stream), "H2D grid");
+  SD.runs = L.R;
+  SD.master_seed = d->master_seed;
+  SD.sim_begin = s0;
+  SD.n_local = S;
+  SD.t_end = d->t_end;
+  SD.grid = sl.grid.p;
+  KinOutDev O{sl.traj.p, sl.meta.p, sl.status.p, want_work ? sl.work.p : nullptr};
+  cudaError_t e;
+  const int kind = d->method.kind;
+  if (kind == KIN_METHOD_ODE) {
+    e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
+  } else {
+    e = kin::launch_stochastic(*T, SD, O, want_work, 64, sl.stream);
+  }
+  if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
+  // per-point statistics for points entirely inside [s0, s1)
+  const uint64_t P0 = (s0 + L.R - 1) / L.R, P1 = s1 / L.R;
+  const uint64_t nP = P1 > P0 ? P1 - P0 : 0;
+  if (want_stats && nP) {
+    KIN_CUDA(sl.mean.ensure(gn * nP), "cudaMalloc mean");
+    KIN_CUDA(sl.m2.ensure(gn * nP), "cudaMalloc m2");
+    e = kin::launch_point_stats(sl.traj.p, S, static_cast<int>(gn), L.R, P0 * L.R - s0, nP, sl.mean.p, sl.m2.p,
+                                sl.stream);
+    if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
+  }
+  sl.s0 = s0;
+  sl.s1 = s1;
+  sl.P0 = P0;
+  sl.nP = nP;
+  sl.R = L.R;
+  sl.G = G;
+  sl.N = N;
+  sl.have_stats = want_stats && nP;
+  sl.have_work = want_work;
+  sl.valid = true;
+  return KIN_OK;
+}
+
+// Copy the slot's last launch into caller buffers; offsets are relative to
+// (base_sim, base_point) of the caller's arrays.
+int fetch_range(Slot& sl, kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, kin_error* err) {
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  const uint64_t S = sl.s1 - sl.s0;
+  const size_t gn = static_cast<size_t>(sl.G) * sl.N;
+  const uint64_t so = sl.s0 - base_sim;
+  if (out->traj && S && gn) {
+    KIN_CUDA(sl.traj_t.ensure(gn * S), "cudaMalloc transpose");
+    cudaError_t e = kin::launch_transpose_traj(sl.traj.p, sl.traj_t.p, S, static_cast<int>(gn), sl.stream);
+    if (e != cudaSuccess) return cuda_fail(err, e, "transpose launch");
+    if (int rc = copy_d2h(sl, out->traj + so * gn, sl.traj_t.p, gn * S * sizeof(double), err)) return rc;
+  }
+  if (out->meta && S)
+    if (int rc = copy_d2h(sl, out->meta + so * 6, sl.meta.p, S * 6 * sizeof(uint64_t), err)) return rc;
+  if (out->status && S)
+    if (int rc = copy_d2h(sl, out->status + so, sl.status.p, S * sizeof(int32_t), err)) return rc;
+  if (out->work && S && sl.have_work)
+    if (int rc = copy_d2h(sl, out->work + so, sl.work.p, S * sizeof(uint64_t), err)) return rc;
+  if (sl.have_stats) {
+    const uint64_t po = sl.P0 - base_point;
+    if (out->mean)
+      if (int rc = copy_d2h(sl, out->mean + po * gn, sl.mean.p, sl.nP * gn * sizeof(double), err)) return rc;
+    if (out->m2)
+      if (int rc = copy_d2h(sl, out->m2 + po * gn, sl.m2.p, sl.nP * gn * sizeof(double), err)) return rc;
+  }
+  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
+  return KIN_OK;
+}
+
+int prepare(const kin_model* model, const kin_sweep_desc* desc, Layout* L, uint64_t* s0, uint64_t* s1,
+            kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!model || !desc) { set_err(err, KIN_ERR_USAGE, "null argument"); return KIN_ERR_USAGE; }
+  std::string msg;
+  if (int rc = sweep_layout(desc, L, &msg)) { set_err(err, rc, msg); return rc; }
+  if (int rc = validate_sweep(model->host, desc, *L, &msg)) { set_err(err, rc, msg); return rc; }
+  *s0 = desc->sim_begin;
+  *s1 = desc->sim_end == 0 ? L->S : std::min<uint64_t>(desc->sim_end, L->S);
+  if (*s0 > *s1) { set_err(err, KIN_ERR_USAGE, "inverted simulation range"); return KIN_ERR_USAGE; }
+  return KIN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t kin_abi_version(void) { return KIN_ABI_VERSION; }
+
+const char* kin_status_string(int32_t code) {
+  switch (code) {
+    case KIN_OK: return "ok";
+    case KIN_ERR_INPUT: return "input/validation error";
+    case KIN_ERR_SIMULATION: return "simulation failure";
+    case KIN_ERR_DEVICE: return "device (CUDA) error";
+    case KIN_ERR_USAGE: return "usage error";
+    default: return "unknown status";
+  }
+}
+
+uint64_t kin_splitmix64_mix(uint64_t v) { return kin::splitmix64_mix(v); }
+uint64_t kin_derive_run_seed(uint64_t m, uint64_t i) { return kin::derive_run_seed(m, i); }
+
+int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!out) { set_err(err, KIN_ERR_USAGE, "null output"); return KIN_ERR_USAGE; }
+  *out = nullptr;
+  int count = 0;
+  KIN_CUDA(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+  if (count == 0) { set_err(err, KIN_ERR_DEVICE, "no CUDA device"); return KIN_ERR_DEVICE; }
+  std::vector<int> devs;
+  if (!ids || n <= 0) devs.push_back(0);
+  else devs.assign(ids, ids + n);
+  auto ctx = std::make_unique<kin_ctx>();
+  for (int dv : devs) {
+    if (dv < 0 || dv >= count) { set_err(err, KIN_ERR_USAGE, "device id out of range"); return KIN_ERR_USAGE; }
+    auto sl = std::make_unique<Slot>();
+    sl->device = dv;
+    KIN_CUDA(cudaSetDevice(dv), "cudaSetDevice");
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dv);
+    if (major < 10) { set_err(err, KIN_ERR_DEVICE, "engine is built for sm_100a (B200) only"); return KIN_ERR_DEVICE; }
+    KIN_CUDA(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ctx->slots.push_back(std::move(sl));
+  }
+  *out = ctx.release();
+  return KIN_OK;
+}
+
+void kin_ctx_destroy(kin_ctx* ctx) {
+  if (!ctx) return;
+  for (auto& sl : ctx->slots) {
+    cudaSetDevice(sl->device);
+    cudaStreamSynchronize(sl->stream);
+    sl->traj.release(); sl->traj_t.release(); sl->mean.release(); sl->m2.release();
+    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->status.release();
+    if (sl->stage) cudaFreeHost(sl->stage);
+    for (auto& e : sl->ev) if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(sl->stream);
+  }
+  delete ctx;
+}
+
+int32_t kin_ctx_device_count(const kin_ctx* ctx) { return ctx ? static_cast<int32_t>(ctx->slots.size()) : 0; }
+
+void* kin_ctx_stream(kin_ctx* ctx, int32_t slot) {
+  if (!ctx || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) return nullptr;
+  return ctx->slots[slot]->stream;
+}
+
+int kin_model_upload(kin_ctx* ctx, const kin_model_desc* desc, kin_model** out, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || !out) { set_err(err, KIN_ERR_USAGE, "null argument"); return KIN_ERR_USAGE; }
+  auto m = std::make_unique<kin_model>();
+  m->ctx = ctx;
+  std::string msg;
+  if (int rc = load_model(desc, &m->host, &msg)) { set_err(err, rc, msg); return rc; }
+  *out = m.release();
+  return KIN_OK;
+}
+
+void kin_model_free(kin_model* model) { delete model; }
+
+int kin_sweep_size(const kin_sweep_desc* desc, uint64_t* np, uint64_t* ns, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  Layout L;
+  std::string msg;
+  if (int rc = sweep_layout(desc, &L, &msg)) { set_err(err, rc, msg); return rc; }
+  if (np) *np = L.P;
+  if (ns) *ns = L.S;
+  return KIN_OK;
+}
+
+int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc, kin_sweep_out* out,
+                  kin_error* err) {
+  if (!ctx) { set_err(err, KIN_ERR_USAGE, "null context"); return KIN_ERR_USAGE; }
+  Layout L;
+  uint64_t s0, s1;
+  if (int rc = prepare(model, desc, &L, &s0, &s1, err)) return rc;
+  kin_sweep_out none;
+  std::memset(&none, 0, sizeof(none));
+  if (!out) out = &none;
+  const uint64_t S = s1 - s0;
+  const uint64_t base_point = (s0 + L.R - 1) / L.R;
+  // whole-point chunks, cyclic over devices
+  const int D = static_cast<int>(ctx->slots.size());
+  const uint64_t n_chunks = D == 1 ? 1 : std::min<uint64_t>(std::max<uint64_t>(S / std::max<uint64_t>(L.R, 1), 1), 4 * static_cast<uint64_t>(D));
+  std::vector<uint64_t> bounds;
+  bounds.push_back(s0);
+  for (uint64_t c = 1; c < n_chunks; ++c) {
+    uint64_t b = s0 + S * c / n_chunks;
+    b = (b + L.R - 1) / L.R * L.R;  // snap to a point boundary
+    b = std::min(std::max(b, bounds.back()), s1);
+    bounds.push_back(b);
+  }
+  bounds.push_back(s1);
+  std::vector<int32_t> status_local;
+  int32_t* status = out->status;
+  if (!status) {
+    status_local.resize(std::max<uint64_t>(S, 1));
+    status = status_local.data();
+  }
+  kin_sweep_out o2 = *out;
+  o2.status = status;
+  std::vector<kin_error> errs(D);
+  std::vector<int> rcs(D, KIN_OK);
+  auto worker = [&](int dv) {
+    Slot& sl = *ctx->slots[dv];
+    std::lock_guard<std::mutex> lk(sl.mu);
+    for (uint64_t c = dv; c < n_chunks; c += D) {
+      const uint64_t c0 = bounds[c], c1 = bounds[c + 1];
+      if (c0 >= c1) continue;
+      const bool stats = (o2.mean || o2.m2);
+      int rc = launch_range(sl, model->host, desc, L, c0, c1, stats, o2.work != nullptr, &errs[dv]);
+      if (rc == KIN_OK) rc = fetch_range(sl, &o2, s0, base_point, &errs[dv]);
+      if (rc != KIN_OK) { rcs[dv] = rc; return; }
+    }
+  };
+  if (D == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int dv = 0; dv < D; ++dv) th.emplace_back(worker, dv);
+    for (auto& t : th) t.join();
+  }
+  for (int dv = 0; dv < D; ++dv)
+    if (rcs[dv] != KIN_OK) {
+      if (err) *err = errs[dv];
+      return rcs[dv];
+    }
+  for (uint64_t s = 0; s < S; ++s) {
+    if (status[s] != KIN_SIM_OK) {
+      const uint64_t g = s0 + s;
+      if (err) {
+        err->code = KIN_ERR_SIMULATION;
+        err->sim_status = status[s];
+        err->sim_index = g;
+        err->point_index = g / L.R;
+        err->run_index = g % L.R;
+        std::snprintf(err->message, sizeof(err->message), "simulation %llu (point %llu, run %llu) failed: status %d",
+                      (unsigned long long)g, (unsigned long long)(g / L.R), (unsigned long long)(g % L.R), status[s]);
+      }
+      return KIN_ERR_SIMULATION;
+    }
+  }
+  return KIN_OK;
+}
+
+int kin_sweep_launch(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc, int32_t slot,
+                     int32_t want_stats, int32_t want_work, kin_error* err) {
+  if (!ctx || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) {
+    set_err(err, KIN_ERR_USAGE, "bad context/slot");
+    return KIN_ERR_USAGE;
+  }
+  Layout L;
+  uint64_t s0, s1;
+  if (int rc = prepare(model, desc, &L, &s0, &s1, err)) return rc;
+  Slot& sl = *ctx->slots[slot];
+  std::lock_guard<std::mutex> lk(sl.mu);
+  return launch_range(sl, model->host, desc, L, s0, s1, want_stats != 0, want_work != 0, err);
+}
+
+int kin_sweep_sync(kin_ctx* ctx, int32_t slot, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) {
+    set_err(err, KIN_ERR_USAGE, "bad context/slot");
+    return KIN_ERR_USAGE;
+  }
+  Slot& sl = *ctx->slots[slot];
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
+  return KIN_OK;
+}
+
+int kin_sweep_fetch(kin_ctx* ctx, int32_t slot, kin_sweep_out* out, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || !out || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) {
+    set_err(err, KIN_ERR_USAGE, "bad argument");
+    return KIN_ERR_USAGE;
+  }
+  Slot& sl = *ctx->slots[slot];
+  std::lock_guard<std::mutex> lk(sl.mu);
+  if (!sl.valid) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
+  return fetch_range(sl, out, sl.s0, sl.P0, err);
+}
+
+int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean, int32_t n, uint64_t* out_bits,
+                         kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || ctx->slots.empty() || n < 0 || (n > 0 && !out_bits)) {
+    set_err(err, KIN_ERR_USAGE, "bad argument");
+    return KIN_ERR_USAGE;
+  }
+  Slot& sl = *ctx->slots[0];
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  uint64_t* d = nullptr;
+  KIN_CUDA(cudaMalloc(&d, sizeof(uint64_t) * std::max(n, 1)), "cudaMalloc");
+  cudaError_t e = kin::launch_rng_draws(seed, kind, mean, n, d, sl.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out_bits, d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, sl.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(err, e, "rng draws");
+  return KIN_OK;
+}
+
+int kin_measure_fp64_peak(kin_ctx* ctx, double* tflops, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || ctx->slots.empty() || !tflops) { set_err(err, KIN_ERR_USAGE, "bad argument"); return KIN_ERR_USAGE; }
+  Slot& sl = *ctx->slots[0];
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  KIN_CUDA(kin::measure_fp64_peak(sl.stream, tflops), "fp64 peak");
+  return KIN_OK;
+}
+
+}  // extern "C"

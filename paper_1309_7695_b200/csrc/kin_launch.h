@@ -1,0 +1,32 @@
+// kin_launch.h — host-side launchers of the engine's kernels (one per .cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+#include "../../include/kin_abi.h"
+#include "kin_tables.h"
+
+namespace kin {
+
+// kin_stochastic.cu: SSA / tau-adaptive / tau-fixed, thread per simulation.
+size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block);
+cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
+                              int block, cudaStream_t stream);
+
+// kin_ode.cu: Dopri5 RRE integration, L lanes per simulation (L = 0 picks).
+int ode_pick_lanes(int n_species);
+cudaError_t launch_dopri5(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, int lanes,
+                          cudaStream_t stream);
+
+// kin_post.cu: layout kernels and utilities.
+// traj_dev [G*N][n_local] (simulation-fastest) -> dst [n_local][G*N]
+cudaError_t launch_transpose_traj(const double* traj_dev, double* dst, uint64_t n_local, int gn, cudaStream_t stream);
+// per-point Welford over runs (ascending run order) -> mean/m2 [P][G*N]
+cudaError_t launch_point_stats(const double* traj_dev, uint64_t n_local, int gn, uint64_t runs,
+                               uint64_t first_point_offset, uint64_t n_points, double* mean, double* m2,
+                               cudaStream_t stream);
+cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, cudaStream_t stream);
+cudaError_t measure_fp64_peak(cudaStream_t stream, double* tflops);
+
+}  // namespace kin

@@ -1,0 +1,187 @@
+// kin_post.cu — output-layout kernels (K6 of DESIGN.md) and device utilities.
+//
+//   transpose_traj  [G*N][S] (simulation-fastest, as the simulators store it for
+//                   coalescing) -> [S][G][N] (Trajectory::samples per run,
+//                   model.hpp:113-120) before the single D2H copy.
+//   point_stats     EnsembleStatistics per sweep point (ensemble.hpp:20-57):
+//                   Welford add over the point's runs in ascending run order
+//                   (the workers=1 merge order), written grid-major
+//                   [P][G][N].  Compiled with -fmad=false so it rounds exactly
+//                   like the oracle's welford_add.
+// Both are HBM-bound 32x32 shared-memory tile transposes (coalesced on both
+// sides).
+#include "kin_device.cuh"
+#include "kin_launch.h"
+
+namespace kin {
+
+namespace {
+
+constexpr int TILE = 32;
+constexpr int ROWS = 8;
+
+__global__ void __launch_bounds__(TILE* ROWS) transpose_kernel(const double* __restrict__ src,
+                                                               double* __restrict__ dst, uint64_t n_cols,
+                                                               int n_rows) {
+  // src: [n_rows][n_cols], dst: [n_cols][n_rows]
+  __shared__ double tile[TILE][TILE + 1];
+  const uint64_t c0 = static_cast<uint64_t>(blockIdx.x) * TILE;
+  const int r0 = blockIdx.y * TILE;
+#pragma unroll
+  for (int k = 0; k < TILE; k += ROWS) {
+    const int r = r0 + threadIdx.y + k;
+    const uint64_t c = c0 + threadIdx.x;
+    if (r < n_rows && c < n_cols) tile[threadIdx.y + k][threadIdx.x] = __ldcs(src + static_cast<uint64_t>(r) * n_cols + c);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < TILE; k += ROWS) {
+    const uint64_t c = c0 + threadIdx.y + k;
+    const int r = r0 + threadIdx.x;
+    if (r < n_rows && c < n_cols) __stcs(dst + c * n_rows + r, tile[threadIdx.x][threadIdx.y + k]);
+  }
+}
+
+__global__ void __launch_bounds__(TILE* ROWS) stats_kernel(const double* __restrict__ traj, uint64_t n_local,
+                                                           int gn, uint64_t runs, uint64_t base,
+                                                           uint64_t n_points, double* __restrict__ mean,
+                                                           double* __restrict__ m2) {
+  __shared__ double tm[TILE][TILE + 1];
+  __shared__ double tq[TILE][TILE + 1];
+  const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * TILE;
+  const int q0 = blockIdx.y * TILE;
+#pragma unroll
+  for (int k = 0; k < TILE; k += ROWS) {
+    const int q = q0 + threadIdx.y + k;
+    const uint64_t p = p0 + threadIdx.x;
+    double mu = 0.0, s2 = 0.0;
+    if (q < gn && p < n_points) {
+      const double* col = traj + static_cast<uint64_t>(q) * n_local + base + p * runs;
+      for (uint64_t r = 0; r < runs; ++r) {
+        const double xv = col[r];
+        const double delta = __dsub_rn(xv, mu);
+        mu = __dadd_rn(mu, __ddiv_rn(delta, static_cast<double>(r + 1)));
+        s2 = __dadd_rn(s2, __dmul_rn(delta, __dsub_rn(xv, mu)));
+      }
+    }
+    tm[threadIdx.y + k][threadIdx.x] = mu;
+    tq[threadIdx.y + k][threadIdx.x] = s2;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < TILE; k += ROWS) {
+    const uint64_t p = p0 + threadIdx.y + k;
+    const int q = q0 + threadIdx.x;
+    if (q < gn && p < n_points) {
+      if (mean) __stcs(mean + p * gn + q, tm[threadIdx.x][threadIdx.y + k]);
+      if (m2) __stcs(m2 + p * gn + q, tq[threadIdx.x][threadIdx.y + k]);
+    }
+  }
+}
+
+__global__ void rng_kernel(uint64_t seed, int kind, double mean, int n, uint64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Xoshiro rng;
+  rng.seed(seed);
+  uint64_t dummy = 0;
+  double spare = 0.0;
+  bool have = false;
+  for (int q = 0; q < n; ++q) {
+    uint64_t bits;
+    if (kind == 0) {
+      bits = rng.next();
+    } else if (kind == 1) {
+      const double v = rng.uniform();
+      bits = __double_as_longlong(v);
+    } else if (kind == 2) {  // Box-Muller with cached spare (rng.cpp:54-66)
+      double v;
+      if (have) {
+        have = false;
+        v = spare;
+      } else {
+        const double u1 = rng.uniform();
+        const double u2 = rng.uniform();
+        const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+        const double ang = __dmul_rn(__dmul_rn(2.0, 3.141592653589793), u2);
+        spare = __dmul_rn(r, sin(ang));
+        have = true;
+        v = __dmul_rn(r, cos(ang));
+      }
+      bits = __double_as_longlong(v);
+    } else {
+      bits = poisson<false>(rng, mean, dummy);
+    }
+    out[q] = bits;
+  }
+}
+
+// DFMA throughput probe: 8 independent FMA chains per thread.
+__global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, double c) {
+  double a0 = threadIdx.x * 1e-9, a1 = a0 + 1e-9, a2 = a0 + 2e-9, a3 = a0 + 3e-9;
+  double a4 = a0 + 4e-9, a5 = a0 + 5e-9, a6 = a0 + 6e-9, a7 = a0 + 7e-9;
+  const double b = 0.999999999;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a0 = fma(a0, b, c); a1 = fma(a1, b, c); a2 = fma(a2, b, c); a3 = fma(a3, b, c);
+      a4 = fma(a4, b, c); a5 = fma(a5, b, c); a6 = fma(a6, b, c); a7 = fma(a7, b, c);
+    }
+  }
+  const double s = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+  if (s == 12345.678) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+}  // namespace
+
+cudaError_t launch_transpose_traj(const double* traj_dev, double* dst, uint64_t n_local, int gn, cudaStream_t st) {
+  if (n_local == 0 || gn == 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((n_local + TILE - 1) / TILE), static_cast<unsigned>((gn + TILE - 1) / TILE));
+  transpose_kernel<<<grid, dim3(TILE, ROWS), 0, st>>>(traj_dev, dst, n_local, gn);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_point_stats(const double* traj_dev, uint64_t n_local, int gn, uint64_t runs, uint64_t base,
+                               uint64_t n_points, double* mean, double* m2, cudaStream_t st) {
+  if (n_points == 0 || gn == 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((n_points + TILE - 1) / TILE), static_cast<unsigned>((gn + TILE - 1) / TILE));
+  stats_kernel<<<grid, dim3(TILE, ROWS), 0, st>>>(traj_dev, n_local, gn, runs, base, n_points, mean, m2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, cudaStream_t st) {
+  rng_kernel<<<1, 32, 0, st>>>(seed, kind, mean, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t measure_fp64_peak(cudaStream_t st, double* tflops) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int block = 256, blocks = sms * 8, iters = 2048;
+  double* out = nullptr;
+  cudaError_t e = cudaMalloc(&out, sizeof(double) * block * blocks);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_kernel<<<blocks, block, 0, st>>>(out, 64, 1e-12);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0, st);
+    dfma_kernel<<<blocks, block, 0, st>>>(out, iters, 1e-12);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
+  }
+  const double flops = 2.0 * 8 * 16 * static_cast<double>(iters) * block * blocks;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  e = cudaGetLastError();
+  cudaFree(out);
+  return e;
+}
+
+}  // namespace kin

@@ -1,0 +1,79 @@
+// kin_tables.h — host/device shared layout of the packed model tables and the
+// per-launch sweep descriptor.
+//
+// The model (ReactionNetwork, model.hpp:44-95) is packed into ONE flat struct
+// passed to every kernel as a __grid_constant__ parameter: it lives in the
+// kernel-parameter constant bank, so the warp-uniform table walks of the
+// thread-per-simulation kernels (loop over reactions j / species i, identical in
+// every lane) are served by the constant cache as broadcasts, with no global
+// state and no per-model __constant__ symbol (several models/sweeps can be in
+// flight on different streams).
+#pragma once
+
+#include <stdint.h>
+
+#define KIN_MAX_AXES 8
+#define KIN_TABLE_BYTES 30720  // < 32764-byte kernel parameter limit (sm_70+, CUDA >= 12.1)
+
+// packed entries
+//   reactant term : species (bits 0-15) | stoich (bits 16-23)
+//   nu entry      : index   (bits 0-15) | (delta + 128) (bits 16-23)
+#define KIN_TERM_SPECIES(e) ((int)((e) & 0xFFFF))
+#define KIN_TERM_STOICH(e) ((int)(((e) >> 16) & 0xFF))
+#define KIN_NU_INDEX(e) ((int)((e) & 0xFFFF))
+#define KIN_NU_DELTA(e) ((int)(((e) >> 16) & 0xFF) - 128)
+
+struct KinTables {
+  int32_t n;          // species
+  int32_t m;          // reactions
+  int32_t nnz;        // nonzeros of nu
+  int32_t n_grid;
+  int32_t fprop;      // algorithmic flops of one full propensity pass (FMA=2)
+  int32_t pad0_;
+  // byte offsets into blob
+  uint32_t off_rate;      // double [m]   rate constant with NON-swept params resolved
+  uint32_t off_rate_axis; // int8   [m]   -1, or sweep axis whose value is c_j
+  uint32_t off_x0;        // double [n]   initial amounts (exact integers)
+  uint32_t off_x0_axis;   // int8   [n]   -1, or sweep axis overriding x0_i
+  uint32_t off_g;         // double [n]   g_i (highest reactant order, 1 if none), as double
+  uint32_t off_rt_ptr;    // int16  [m+1] reactant CSR (species-ascending)
+  uint32_t off_rt;        // uint32 [..]  packed reactant terms
+  uint32_t off_col_ptr;   // int16  [m+1] nu columns (species-ascending)
+  uint32_t off_col;       // uint32 [nnz] packed (species, delta)
+  uint32_t off_row_ptr;   // int16  [n+1] nu rows (reaction-ascending)
+  uint32_t off_row;       // uint32 [nnz] packed (reaction, delta)
+  uint32_t off_grid;      // double [n_grid] sampling grid (0 when it did not fit: use SweepDev::grid)
+  uint32_t used;
+  uint32_t pad_;
+  alignas(16) unsigned char blob[KIN_TABLE_BYTES];
+};
+
+struct KinSweepDev {
+  // method (Method, ensemble.hpp:59-71; IntegratorConfig, deterministic.hpp:14-20)
+  int32_t kind;
+  int32_t rng_mode;
+  double tau;
+  double epsilon;
+  double rel_tol, abs_tol, h_init, h_max;
+  uint64_t max_steps;
+  // sweep (SweepConfig, ensemble.hpp:106-113)
+  int32_t n_axes;
+  int32_t seed_mode;
+  int32_t axis_kind[KIN_MAX_AXES];
+  int32_t axis_n[KIN_MAX_AXES];
+  const double* axis_values[KIN_MAX_AXES];  // device pointers
+  uint64_t runs;        // runs per point R
+  uint64_t master_seed;
+  uint64_t sim_begin;   // global index of local simulation 0
+  uint64_t n_local;     // simulations in this launch
+  double t_end;
+  const double* grid;   // device pointer [n_grid]
+};
+
+// Device outputs of one launch (local simulation index s in [0, n_local)).
+struct KinOutDev {
+  double* traj;      // [G][N][n_local]  simulation-fastest (coalesced stores)
+  uint64_t* meta;    // [n_local][6]
+  int32_t* status;   // [n_local]
+  uint64_t* work;    // [n_local] or null
+};

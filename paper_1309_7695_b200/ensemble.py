@@ -1,0 +1,332 @@
+"""Host-side mirror of the reference ensemble layer (proj/include/kinetics/ensemble.hpp).
+
+``parameter_sweep`` / ``run_ensemble`` / ``run_single`` keep the reference
+names, argument meaning and error behaviour (ensemble.hpp:74-130); underneath,
+each is ONE call of the C-ABI ``kin_sweep_run`` (include/kin_abi.h), which runs
+the simulations as CUDA kernels on the B200s of the engine context.  There is
+no CPU fallback: if ``libkin_b200.so`` is missing or no device is usable the
+call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+
+from . import abi
+from .model import DeviceError, ReactionNetwork, SimulationError, ValidationError
+
+
+class MethodKind(IntEnum):
+    """Method::Kind (ensemble.hpp:62) + the LSODA extension."""
+    Ssa = abi.METHOD_SSA
+    TauAdaptive = abi.METHOD_TAU_ADAPTIVE
+    TauFixed = abi.METHOD_TAU_FIXED
+    Cle = abi.METHOD_CLE
+    Ode = abi.METHOD_ODE
+    Hybrid = abi.METHOD_HYBRID
+    Lsoda = abi.METHOD_LSODA
+
+
+@dataclass
+class IntegratorConfig:
+    """deterministic.hpp:14-20."""
+    rel_tol: float = 1e-6
+    abs_tol: float = 1e-9
+    h_init: float = 0.0
+    h_max: float = math.inf
+    max_steps: int = 10_000_000
+
+    def c(self) -> abi.KinIntegratorConfig:
+        return abi.KinIntegratorConfig(self.rel_tol, self.abs_tol, self.h_init, self.h_max, self.max_steps)
+
+
+@dataclass
+class Method:
+    """ensemble.hpp:59-71."""
+    kind: MethodKind = MethodKind.Ssa
+    tau: float = 0.0
+    epsilon: float = 0.03
+    integrator: IntegratorConfig = field(default_factory=IntegratorConfig)
+
+    def deterministic(self) -> bool:
+        return self.kind in (MethodKind.Ode, MethodKind.Lsoda)
+
+    def name(self) -> str:
+        return {MethodKind.Ssa: "ssa", MethodKind.TauAdaptive: "tau-adaptive", MethodKind.TauFixed: "tau-fixed",
+                MethodKind.Cle: "cle", MethodKind.Ode: "ode", MethodKind.Hybrid: "hybrid",
+                MethodKind.Lsoda: "lsoda"}[MethodKind(self.kind)]
+
+    def c(self) -> abi.KinMethod:
+        return abi.KinMethod(int(self.kind), self.tau, self.epsilon, self.integrator.c())
+
+
+@dataclass
+class SweepAxis:
+    """ensemble.hpp:101-104.  ``param`` names a Parameter (reference semantics,
+    with_param) or, with ``kind="initial"``, a species whose initial amount is
+    swept (north-star extension)."""
+    param: str
+    values: Sequence[float]
+    kind: str = "param"
+
+
+@dataclass
+class SweepConfig:
+    """ensemble.hpp:106-113."""
+    axes: List[SweepAxis] = field(default_factory=list)
+    runs_per_point: int = 1
+    method: Method = field(default_factory=Method)
+    master_seed: int = 0
+    t_end: float = 0.0
+    grid: Sequence[float] = field(default_factory=list)
+
+
+@dataclass
+class TrajectoryMeta:
+    """model.hpp:104-111."""
+    steps: int = 0
+    rejected_leaps: int = 0
+    clamp_events: int = 0
+    fallback_ssa_steps: int = 0
+    jumps: int = 0
+    floored: bool = False
+
+
+@dataclass
+class Trajectory:
+    """model.hpp:113-120: samples[g][n]."""
+    grid: np.ndarray
+    samples: np.ndarray
+    method: str
+    seed: Optional[int]
+    meta: TrajectoryMeta
+
+
+@dataclass
+class EnsembleStatistics:
+    """ensemble.hpp:20-57: grid-major mean/m2."""
+    grid: np.ndarray
+    species_count: int
+    n: int
+    mean_: np.ndarray
+    m2_: np.ndarray
+
+    def runs(self) -> int:
+        return self.n
+
+    def mean(self, g: int, s: int) -> float:
+        return float(self.mean_[g, s])
+
+    def m2(self, g: int, s: int) -> float:
+        return float(self.m2_[g, s])
+
+    def variance(self, g: int, s: int) -> float:
+        return 0.0 if self.n < 2 else float(self.m2_[g, s] / (self.n - 1))
+
+
+@dataclass
+class SweepPointResult:
+    coordinates: List[float]
+    stats: EnsembleStatistics
+
+
+@dataclass
+class SweepResults:
+    axis_names: List[str]
+    points: List[SweepPointResult]
+
+
+def _meta(row) -> TrajectoryMeta:
+    return TrajectoryMeta(int(row[0]), int(row[1]), int(row[2]), int(row[3]), int(row[4]), bool(row[5]))
+
+
+def make_sweep_desc(network: ReactionNetwork, config: SweepConfig, *, seed_mode: int = abi.SEED_SWEEP,
+                    rng_mode: int = abi.RNG_COMPAT, sim_range=None):
+    """Pack a SweepConfig into kin_sweep_desc.  Returns (desc, keepalive)."""
+    keep = []
+    axes = (abi.KinSweepAxis * max(1, len(config.axes)))()
+    for i, ax in enumerate(config.axes):
+        vals = np.ascontiguousarray(ax.values, dtype=np.float64)
+        keep.append(vals)
+        if ax.kind == "param":
+            idx = network.param_index(ax.param)
+            if idx is None:
+                raise ValidationError(f"sweep axis: unknown parameter '{ax.param}'")
+            kind = abi.AXIS_PARAM
+        elif ax.kind == "initial":
+            idx = network.species_index(ax.param)
+            if idx is None:
+                raise ValidationError(f"sweep axis: unknown species '{ax.param}'")
+            kind = abi.AXIS_INITIAL
+        else:
+            raise ValidationError(f"sweep axis kind '{ax.kind}'")
+        axes[i] = abi.KinSweepAxis(kind, idx, len(vals), abi.ptr(vals, C.c_double))
+    grid = np.ascontiguousarray(config.grid, dtype=np.float64)
+    keep += [axes, grid]
+    s0, s1 = sim_range if sim_range else (0, 0)
+    d = abi.KinSweepDesc(config.method.c(), len(config.axes), axes, int(config.runs_per_point),
+                         int(config.master_seed) & 0xFFFFFFFFFFFFFFFF, seed_mode, rng_mode, float(config.t_end),
+                         len(grid), abi.ptr(grid, C.c_double) if len(grid) else None, s0, s1)
+    return d, keep
+
+
+def sweep_size(config: SweepConfig):
+    p = 1
+    for ax in config.axes:
+        p *= len(ax.values)
+    return p, p * int(config.runs_per_point)
+
+
+def uniform_grid(t_end: float, n: int) -> np.ndarray:
+    """grid[g] = t_end*g/(n-1)."""
+    return np.array([t_end * g / (n - 1) for g in range(n)], dtype=np.float64)
+
+
+class Engine:
+    """Owns a kin_ctx (device memory + one host thread per device)."""
+
+    def __init__(self, devices: Optional[Sequence[int]] = None):
+        self.lib = abi.load_library()
+        ids = np.ascontiguousarray(devices if devices is not None else [0], dtype=np.int32)
+        ctx = C.c_void_p()
+        err = abi.KinError()
+        rc = self.lib.kin_ctx_create(abi.ptr(ids, C.c_int32), len(ids), C.byref(ctx), C.byref(err))
+        if rc:
+            raise DeviceError(f"kin_ctx_create failed: {err.text()}")
+        self.ctx = ctx
+        self._models = {}
+
+    def close(self):
+        if self.ctx:
+            for h in self._models.values():
+                self.lib.kin_model_free(h[0])
+            self._models.clear()
+            self.lib.kin_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def model(self, network: ReactionNetwork):
+        key = id(network)
+        if key in self._models and self._models[key][1] is network:
+            return self._models[key][0]
+        h = C.c_void_p()
+        err = abi.KinError()
+        rc = self.lib.kin_model_upload(self.ctx, C.byref(network.desc()), C.byref(h), C.byref(err))
+        _raise(rc, err)
+        self._models[key] = (h, network)
+        return h
+
+    def sweep(self, network: ReactionNetwork, config: SweepConfig, *, seed_mode=abi.SEED_SWEEP,
+              rng_mode=abi.RNG_COMPAT, sim_range=None, want_traj=True, want_stats=True, want_work=False):
+        """Bulk form: returns dict of numpy arrays (traj [S,G,N], meta [S,6],
+        status [S], mean/m2 [P,G,N], work [S])."""
+        d, keep = make_sweep_desc(network, config, seed_mode=seed_mode, rng_mode=rng_mode, sim_range=sim_range)
+        P, S_all = sweep_size(config)
+        R = int(config.runs_per_point)
+        s0, s1 = sim_range if sim_range else (0, S_all)
+        s1 = s1 or S_all
+        S = s1 - s0
+        G, N = len(config.grid), network.species_count()
+        Pr = max(0, s1 // R - (s0 + R - 1) // R)
+        res = {
+            "traj": np.empty((S, G, N)) if want_traj else None,
+            "meta": np.empty((S, 6), dtype=np.uint64),
+            "status": np.empty(S, dtype=np.int32),
+            "mean": np.empty((Pr, G, N)) if want_stats else None,
+            "m2": np.empty((Pr, G, N)) if want_stats else None,
+            "work": np.empty(S, dtype=np.uint64) if want_work else None,
+        }
+        out = abi.KinSweepOut(abi.ptr(res["traj"], C.c_double), abi.ptr(res["meta"], C.c_uint64),
+                              abi.ptr(res["status"], C.c_int32), abi.ptr(res["mean"], C.c_double),
+                              abi.ptr(res["m2"], C.c_double), abi.ptr(res["work"], C.c_uint64))
+        err = abi.KinError()
+        rc = self.lib.kin_sweep_run(self.ctx, self.model(network), C.byref(d), C.byref(out), C.byref(err))
+        _raise(rc, err)
+        return res
+
+
+def _raise(rc: int, err: abi.KinError):
+    if rc == abi.KIN_OK:
+        return
+    msg = err.text()
+    if rc == abi.KIN_ERR_SIMULATION:
+        raise SimulationError(msg, err.sim_index, err.point_index, err.run_index, err.sim_status)
+    if rc == abi.KIN_ERR_DEVICE:
+        raise DeviceError(msg)
+    raise ValidationError(msg)
+
+
+_default_engine: Optional[Engine] = None
+
+
+def default_engine() -> Engine:
+    global _default_engine
+    if _default_engine is None:
+        _default_engine = Engine()
+    return _default_engine
+
+
+def parameter_sweep(network: ReactionNetwork, config: SweepConfig, workers: Optional[int] = None,
+                    engine: Optional[Engine] = None) -> SweepResults:
+    """ensemble.hpp:126-130.  ``workers`` is accepted for signature parity; the
+    device count of ``engine`` plays its role (per-run results never depend on
+    it)."""
+    eng = engine or default_engine()
+    res = eng.sweep(network, config, want_traj=False, want_stats=True)
+    grid = np.asarray(config.grid, dtype=np.float64)
+    shape = [len(ax.values) for ax in config.axes]
+    points = []
+    for k in range(res["mean"].shape[0]):
+        idx = np.unravel_index(k, shape) if shape else ()
+        coords = [float(config.axes[a].values[i]) for a, i in enumerate(idx)]
+        st = EnsembleStatistics(grid, network.species_count(), int(config.runs_per_point),
+                                res["mean"][k], res["m2"][k])
+        points.append(SweepPointResult(coords, st))
+    return SweepResults([ax.param for ax in config.axes], points)
+
+
+@dataclass
+class EnsembleOptions:
+    """ensemble.hpp:78-85."""
+    method: Method = field(default_factory=Method)
+    n_runs: int = 1
+    t_end: float = 0.0
+    grid: Sequence[float] = field(default_factory=list)
+    master_seed: int = 0
+    workers: int = 1
+
+
+def run_ensemble(network: ReactionNetwork, options: EnsembleOptions,
+                 sink: Optional[Callable[[int, Trajectory], None]] = None,
+                 engine: Optional[Engine] = None) -> EnsembleStatistics:
+    """ensemble.hpp:91-99: run i seeded with derive_run_seed(master, i)."""
+    eng = engine or default_engine()
+    cfg = SweepConfig([], options.n_runs, options.method, options.master_seed, options.t_end, options.grid)
+    res = eng.sweep(network, cfg, seed_mode=abi.SEED_ENSEMBLE, want_traj=sink is not None, want_stats=True)
+    grid = np.asarray(options.grid, dtype=np.float64)
+    if sink is not None:
+        lib = eng.lib
+        for i in range(options.n_runs):
+            sink(i, Trajectory(grid, res["traj"][i], options.method.name(),
+                               int(lib.kin_derive_run_seed(options.master_seed, i)), _meta(res["meta"][i])))
+    return EnsembleStatistics(grid, network.species_count(), options.n_runs, res["mean"][0], res["m2"][0])
+
+
+def run_single(network: ReactionNetwork, method: Method, t_end: float, grid: Sequence[float], seed: int,
+               engine: Optional[Engine] = None) -> Trajectory:
+    """ensemble.hpp:73-76."""
+    eng = engine or default_engine()
+    cfg = SweepConfig([], 1, method, seed, t_end, grid)
+    res = eng.sweep(network, cfg, seed_mode=abi.SEED_DIRECT, want_traj=True, want_stats=False)
+    return Trajectory(np.asarray(grid, dtype=np.float64), res["traj"][0], method.name(),
+                      None if method.deterministic() else int(seed), _meta(res["meta"][0]))

@@ -1,0 +1,73 @@
+"""The C-ABI library loads and exports every symbol include/kin_abi.h declares
+(CPU only: no compute calls).  Also: the product path has no CPU fallback."""
+import ctypes as C
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_1309_7695_b200 import abi
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "kin_abi.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w]+\s*\**\s*(kin_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_and_binding_agree():
+    assert sorted(abi.ABI_SYMBOLS) == declared_functions()
+
+
+def test_library_exports_every_symbol():
+    lib = abi.load_library()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.kin_abi_version() == 1
+    nm = subprocess.run(["nm", "-D", "--defined-only", str(abi.LIB_PATH)], capture_output=True, text=True).stdout
+    for name in declared_functions():
+        assert re.search(rf"\bT {name}\b", nm), name
+
+
+def test_pure_host_helpers():
+    lib = abi.load_library()
+    assert lib.kin_splitmix64_mix(0) == 0xE220A8397B1DCDAF
+    assert lib.kin_derive_run_seed(42, 7) == 0xCCF635EE9E9E2FA4
+    assert lib.kin_status_string(2) == b"simulation failure"
+
+
+def test_sweep_size_validation():
+    lib = abi.load_library()
+    from paper_1309_7695_b200 import workloads as W
+    from paper_1309_7695_b200.ensemble import make_sweep_desc
+    net, cfg = W.c4_config()
+    d, keep = make_sweep_desc(net, cfg)
+    p, s = C.c_uint64(), C.c_uint64()
+    err = abi.KinError()
+    assert lib.kin_sweep_size(C.byref(d), C.byref(p), C.byref(s), C.byref(err)) == 0
+    assert (p.value, s.value) == (65536, 65536)
+    d.runs_per_point = 0
+    assert lib.kin_sweep_size(C.byref(d), C.byref(p), C.byref(s), C.byref(err)) == abi.KIN_ERR_INPUT
+
+
+def test_no_cpu_fallback_without_gpu():
+    """On a machine without a usable B200 the engine refuses (KIN_ERR_DEVICE)."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    lib = abi.load_library()
+    ctx = C.c_void_p()
+    err = abi.KinError()
+    rc = lib.kin_ctx_create(None, 0, C.byref(ctx), C.byref(err))
+    assert rc == abi.KIN_ERR_DEVICE
+    from paper_1309_7695_b200 import Engine, DeviceError
+    with pytest.raises(DeviceError):
+        Engine()
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        abi.load_library(tmp_path / "nope.so")

@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the CPU oracle.
+
+Contract:
+  * stochastic methods in compat RNG mode: trajectories, TrajectoryMeta and the
+    algorithmic work counters are BIT-EXACT (np.array_equal);
+  * ODE (Dopri5): |gpu - oracle| <= 10 * (abs_tol + rel_tol * |y|) at every grid
+    point (the reference's own 10x-tolerance criterion);
+  * per-point statistics from identical trajectories: bit-exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1309_7695_b200 import abi, workloads as W
+from paper_1309_7695_b200.ensemble import (EnsembleOptions, IntegratorConfig, Method, MethodKind, SweepAxis,
+                                           SweepConfig, make_sweep_desc, parameter_sweep, run_ensemble,
+                                           run_single, uniform_grid)
+from paper_1309_7695_b200.model import SimulationError
+
+pytestmark = pytest.mark.gpu
+
+
+def both(engine, oracle, net, cfg, *, sim_range=None, seed_mode=abi.SEED_SWEEP, want_work=False, stats=False):
+    d, keep = make_sweep_desc(net, cfg, seed_mode=seed_mode, sim_range=sim_range)
+    ref = oracle.sweep(net, d, want_traj=True, want_stats=stats, want_work=want_work)
+    got = engine.sweep(net, cfg, seed_mode=seed_mode, sim_range=sim_range, want_traj=True, want_stats=stats,
+                       want_work=want_work)
+    return ref, got
+
+
+def assert_bit_exact(ref, got, work=False):
+    assert np.array_equal(ref["status"], got["status"])
+    diff = np.argwhere(ref["traj"] != got["traj"])
+    assert diff.size == 0, f"{len(diff)} samples differ, first at {diff[:3].tolist()}"
+    assert np.array_equal(ref["meta"], got["meta"])
+    if work:
+        assert np.array_equal(ref["work"], got["work"])
+
+
+# ---- RNG --------------------------------------------------------------------
+@pytest.mark.parametrize("kind,mean", [(0, 0.0), (1, 0.0), (3, 0.05), (3, 3.5), (3, 9.99), (3, 10.0), (3, 37.5),
+                                       (3, 250.0), (3, 812.0), (3, 1.0e6)])
+def test_device_rng_matches_oracle(engine, oracle, kind, mean):
+    lib = engine.lib
+    import ctypes as C
+    for seed in (0, 1, 42, 0xDEADBEEF):
+        n = 512
+        out = np.zeros(n, dtype=np.uint64)
+        err = abi.KinError()
+        rc = lib.kin_device_rng_draws(engine.ctx, seed, kind, mean, n, abi.ptr(out, C.c_uint64), C.byref(err))
+        assert rc == 0, err.text()
+        ref = oracle.rng_draws(seed, kind, n, mean)
+        assert np.array_equal(out, ref), (seed, kind, mean)
+
+
+def test_device_normal_close(engine, oracle):
+    import ctypes as C
+    n = 1000
+    out = np.zeros(n, dtype=np.uint64)
+    err = abi.KinError()
+    assert engine.lib.kin_device_rng_draws(engine.ctx, 42, 2, 0.0, n, abi.ptr(out, C.c_uint64), C.byref(err)) == 0
+    got = out.view(np.float64)
+    ref = oracle.rng_draws(42, 2, n).view(np.float64)
+    # sin/cos/log differ from glibc by <= 2 ulp (rng.hpp:16-19: float draws are
+    # toolchain-dependent)
+    assert np.allclose(got, ref, rtol=1e-14, atol=1e-15)
+    assert np.allclose(got[:4], [-0.26860736946209501, 0.58197105186288278, -0.054462170108150951,
+                                 -0.17177820812195743], rtol=1e-14)
+
+
+# ---- stochastic: bit-exact ----------------------------------------------------
+def test_c1_tau_adaptive_bit_exact(engine, oracle):
+    net, cfg = W.c1_config(MethodKind.TauAdaptive)
+    ref, got = both(engine, oracle, net, cfg, want_work=True)
+    assert_bit_exact(ref, got, work=True)
+
+
+def test_c1_ssa_bit_exact(engine, oracle):
+    net, cfg = W.c1_config(MethodKind.Ssa, side=8)
+    ref, got = both(engine, oracle, net, cfg, want_work=True)
+    assert_bit_exact(ref, got, work=True)
+
+
+def test_birth_death_ssa_ensemble_bit_exact(engine, oracle):
+    net = W.birth_death()
+    cfg = SweepConfig([], 512, Method(MethodKind.Ssa), 7, 20.0, uniform_grid(20.0, 41))
+    ref, got = both(engine, oracle, net, cfg, seed_mode=abi.SEED_ENSEMBLE, stats=True)
+    assert_bit_exact(ref, got)
+    assert np.array_equal(ref["mean"], got["mean"]) and np.array_equal(ref["m2"], got["m2"])
+
+
+@pytest.mark.parametrize("tau", [0.5, 0.1, 0.01])
+def test_tau_fixed_bit_exact(engine, oracle, tau):
+    net = W.birth_death(lam=5.0, c=1.0, x0=3)
+    cfg = SweepConfig([SweepAxis("lam", [0.5, 5.0, 50.0])], 128, Method(MethodKind.TauFixed, tau=tau), 11, 10.0,
+                      uniform_grid(10.0, 21))
+    ref, got = both(engine, oracle, net, cfg, want_work=True)
+    assert_bit_exact(ref, got, work=True)
+    if tau == 0.5:
+        assert got["meta"][:, 1].sum() > 0  # the reject-and-halve path ran
+
+
+def test_isomerization_conservation_bit_exact(engine, oracle):
+    net = W.isomerization()
+    for kind in (MethodKind.Ssa, MethodKind.TauAdaptive):
+        cfg = SweepConfig([SweepAxis("kf", [0.1, 1.0, 10.0])], 64, Method(kind), 3, 5.0, uniform_grid(5.0, 11))
+        ref, got = both(engine, oracle, net, cfg)
+        assert_bit_exact(ref, got)
+        tot = got["traj"].sum(axis=2)
+        assert np.all(tot == 100.0)  # SPEC.md:143,538 exact conservation
+
+
+def test_schlogl_order3_bit_exact(engine, oracle):
+    net, cfg = W.c2_config(points=64, runs=256)
+    ref, got = both(engine, oracle, net, cfg, sim_range=(0, 1024), stats=True, want_work=True)
+    assert_bit_exact(ref, got, work=True)
+    assert np.array_equal(ref["mean"], got["mean"]) and np.array_equal(ref["m2"], got["m2"])
+
+
+@pytest.mark.parametrize("rng", [(0, 512), (32768, 33280), (65536 - 300, 65536)])
+def test_c4_ras_scale_bit_exact(engine, oracle, rng):
+    net, cfg = W.c4_config()
+    ref, got = both(engine, oracle, net, cfg, sim_range=rng, want_work=True)
+    assert_bit_exact(ref, got, work=True)
+    assert got["meta"][:, 0].sum() > 0 and got["meta"][:, 3].sum() > 0  # leaps and SSA fallback both ran
+
+
+def test_c5_random_network_bit_exact(engine, oracle):
+    net, cfg = W.c5_config()
+    ref, got = both(engine, oracle, net, cfg, sim_range=(1000, 1128))
+    assert_bit_exact(ref, got)
+
+
+def test_shard_invariance(engine):
+    """Per-run output independent of how the index space is cut."""
+    net, cfg = W.c1_config(MethodKind.TauAdaptive)
+    full = engine.sweep(net, cfg, want_stats=False)
+    parts = [engine.sweep(net, cfg, sim_range=r, want_stats=False)["traj"] for r in [(0, 333), (333, 700), (700, 1024)]]
+    assert np.array_equal(full["traj"], np.concatenate(parts))
+
+
+def test_budget_error_lowest_index(engine, oracle):
+    net, cfg = W.c1_config(MethodKind.Ssa, side=4)
+    cfg.method.integrator = IntegratorConfig(max_steps=200)
+    d, keep = make_sweep_desc(net, cfg)
+    ref = oracle.sweep(net, d, raise_on_error=False)
+    assert ref["rc"] == abi.KIN_ERR_SIMULATION
+    with pytest.raises(SimulationError) as ei:
+        engine.sweep(net, cfg)
+    assert ei.value.sim_index == ref["error"].sim_index
+    assert ei.value.sim_status == 1  # KIN_SIM_BUDGET
+
+
+# ---- deterministic (Dopri5): tolerance ---------------------------------------
+def ode_bound(ref, cfg):
+    ic = cfg.method.integrator
+    return 10.0 * (ic.abs_tol + ic.rel_tol * np.abs(ref))
+
+
+def test_ode_decay_analytic(engine):
+    net = W.decay()
+    cfg = SweepConfig([SweepAxis("c", [0.5, 1.0, 2.0])], 1, Method(MethodKind.Ode), 0, 1.0, [0.0, 0.5, 1.0])
+    got = engine.sweep(net, cfg)
+    ends = got["traj"][:, -1, 0]
+    assert np.allclose(ends, [60.653066, 36.787944, 13.533528], rtol=1e-6)
+    exact = 100.0 * np.exp(-np.array([0.5, 1.0, 2.0])[:, None] * np.array([0.0, 0.5, 1.0])[None, :])
+    assert np.all(np.abs(got["traj"][:, :, 0] - exact) <= 1e-6 * exact)
+
+
+def test_ode_birth_death_analytic(engine):
+    net = W.birth_death(x0=0)
+    grid = uniform_grid(3.0, 31)
+    tr = run_single(net, Method(MethodKind.Ode), 3.0, grid, 0, engine=engine)
+    exact = 5.0 * (1.0 - np.exp(-grid))
+    assert abs(tr.samples[-1, 0] - 4.7510646582) < 1e-6 * 4.75
+    assert np.all(np.abs(tr.samples[1:, 0] - exact[1:]) <= 1e-6 * exact[1:])
+
+
+def test_c1_ode_tolerance(engine, oracle):
+    net, cfg = W.c1_config(MethodKind.Ode)
+    ref, got = both(engine, oracle, net, cfg)
+    assert np.all(np.abs(got["traj"] - ref["traj"]) <= ode_bound(ref["traj"], cfg))
+
+
+def test_c3_brusselator_ode_tolerance(engine, oracle):
+    net, cfg = W.c3_config(side=256)
+    ref, got = both(engine, oracle, net, cfg, sim_range=(0, 512))
+    err = np.abs(got["traj"] - ref["traj"]) / ode_bound(ref["traj"], cfg)
+    assert err.max() <= 1.0, err.max()
+
+
+@pytest.mark.parametrize("rng", [(0, 256), (40000, 40256)])
+def test_c4_ode_tolerance(engine, oracle, rng):
+    net, cfg = W.c4_config(method=MethodKind.Ode)
+    ref, got = both(engine, oracle, net, cfg, sim_range=rng)
+    err = np.abs(got["traj"] - ref["traj"]) / ode_bound(ref["traj"], cfg)
+    assert err.max() <= 1.0, err.max()
+
+
+# ---- reference-signature API --------------------------------------------------
+def test_parameter_sweep_api(engine, oracle):
+    """row order and decay endpoints through parameter_sweep."""
+    net = W.decay()
+    cfg = SweepConfig([SweepAxis("c", [0.5, 1.0, 2.0])], 1, Method(MethodKind.Ode), 0, 1.0, [0.0, 1.0])
+    res = parameter_sweep(net, cfg, engine=engine)
+    assert [p.coordinates for p in res.points] == [[0.5], [1.0], [2.0]]
+    ends = [p.stats.mean(1, 0) for p in res.points]
+    assert np.allclose(ends, [60.653066, 36.787944, 13.533528], rtol=1e-6)
+    assert all(p.stats.variance(1, 0) == 0.0 for p in res.points)
+
+
+def test_run_ensemble_matches_oracle(engine, oracle):
+    net = W.birth_death()
+    opts = EnsembleOptions(Method(MethodKind.Ssa), 1000, 20.0, uniform_grid(20.0, 21), 99, 4)
+    seen = {}
+    st = run_ensemble(net, opts, sink=lambda i, tr: seen.setdefault(i, tr), engine=engine)
+    cfg = SweepConfig([], 1000, opts.method, 99, 20.0, opts.grid)
+    d, keep = make_sweep_desc(net, cfg, seed_mode=abi.SEED_ENSEMBLE)
+    ref = oracle.sweep(net, d, want_stats=True)
+    assert np.array_equal(st.mean_, ref["mean"][0]) and np.array_equal(st.m2_, ref["m2"][0])
+    assert len(seen) == 1000 and np.array_equal(seen[17].samples, ref["traj"][17])
+    # endpoint mean within 3 standard errors of 5
+    assert abs(st.mean(20, 0) - 5.0) < 3 * math.sqrt(5.0 / 1000)
+
+
+def test_run_single_direct_seed(engine, oracle):
+    net = W.isomerization()
+    grid = uniform_grid(2.0, 5)
+    tr = run_single(net, Method(MethodKind.TauAdaptive), 2.0, grid, 123456789, engine=engine)
+    cfg = SweepConfig([], 1, Method(MethodKind.TauAdaptive), 123456789, 2.0, grid)
+    d, keep = make_sweep_desc(net, cfg, seed_mode=abi.SEED_DIRECT)
+    ref = oracle.sweep(net, d)
+    assert np.array_equal(tr.samples, ref["traj"][0]) and tr.seed == 123456789
