@@ -202,6 +202,11 @@ int kin_sweep_fetch(kin_ctx* ctx, int32_t device_slot, kin_sweep_out* out,
                     kin_error* err);
 /* cudaStream_t of the device slot, as void* (for event timing by the caller). */
 void* kin_ctx_stream(kin_ctx* ctx, int32_t device_slot);
+/* Device time (CUDA events on the slot's stream) of the last launch's
+   simulation kernel and of its statistics kernel (0 when none ran).  Call
+   after kin_sweep_sync. */
+int kin_sweep_kernel_ms(kin_ctx* ctx, int32_t device_slot, double* sim_ms,
+                        double* stats_ms, kin_error* err);
 
 /* ---- seams (device unit kernels; SPEC "from_uniforms"/"from_counts") ----- */
 uint64_t kin_splitmix64_mix(uint64_t v);                       /* rng.hpp:8-11 */

@@ -52,6 +52,15 @@ __device__ __forceinline__ int tab_row_ptr(const KinTables& T, int i) {
 __device__ __forceinline__ uint32_t tab_row(const KinTables& T, int p) {
   return reinterpret_cast<const uint32_t*>(T.blob + T.off_row)[p];
 }
+__device__ __forceinline__ uint64_t tab_rdesc(const KinTables& T, int j) {
+  return reinterpret_cast<const uint64_t*>(T.blob + T.off_rdesc)[j];
+}
+__device__ __forceinline__ int tab_dep_ptr(const KinTables& T, int j) {
+  return reinterpret_cast<const int16_t*>(T.blob + T.off_dep_ptr)[j];
+}
+__device__ __forceinline__ int tab_dep(const KinTables& T, int p) {
+  return reinterpret_cast<const uint16_t*>(T.blob + T.off_dep)[p];
+}
 __device__ __forceinline__ double tab_grid(const KinTables& T, const KinSweepDev& S, int g) {
   return T.off_grid ? reinterpret_cast<const double*>(T.blob + T.off_grid)[g] : __ldg(S.grid + g);
 }
@@ -150,7 +159,7 @@ __device__ __forceinline__ double combinations(double x, int s) {
   if (s == 1) {
     h = x;
   } else if (s == 2) {
-    h = __ddiv_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), 2.0);
+    h = __dmul_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), 0.5);  // == /2.0 exactly (power of two)
   } else if (s == 3) {
     h = __ddiv_rn(__dmul_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), __dsub_rn(x, 2.0)), 6.0);
   } else {

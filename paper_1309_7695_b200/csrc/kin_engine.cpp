@@ -268,6 +268,42 @@ int pack_tables(const HostModel& H, const kin_sweep_desc* d, KinTables* T, std::
   T->off_rt_ptr = put(rt_ptr.data(), rt_ptr.size() * 2, 2);
   T->off_col_ptr = put(col_ptr.data(), col_ptr.size() * 2, 2);
   T->off_row_ptr = put(row_ptr.data(), row_ptr.size() * 2, 2);
+  // compact reaction descriptors (<= 3 reactant terms, stoich <= 3 each)
+  std::vector<uint64_t> rdesc(H.m, 0);
+  for (int j = 0; j < H.m; ++j) {
+    const int nt = H.rt_ptr[j + 1] - H.rt_ptr[j];
+    if (nt > 3) { *msg = "reaction " + std::to_string(j) + ": more than 3 reactant species"; return KIN_ERR_INPUT; }
+    uint64_t dsc = static_cast<uint64_t>(nt) << 54;
+    for (int t = 0; t < nt; ++t) {
+      const int p = H.rt_ptr[j] + t;
+      dsc |= static_cast<uint64_t>(H.rt_species[p]) << (16 * t);
+      dsc |= static_cast<uint64_t>(H.rt_stoich[p] & 3) << (48 + 2 * t);
+    }
+    dsc |= static_cast<uint64_t>(rate_axis[j] + 1) << 56;
+    rdesc[j] = dsc;
+  }
+  // propensity dependency graph: firing j changes species col(j); every
+  // reaction with one of them as a reactant must be re-evaluated.
+  std::vector<int16_t> dep_ptr(1, 0);
+  std::vector<uint16_t> dep;
+  {
+    std::vector<std::vector<int>> by_species(H.n);
+    for (int k = 0; k < H.m; ++k)
+      for (int p = H.rt_ptr[k]; p < H.rt_ptr[k + 1]; ++p) by_species[H.rt_species[p]].push_back(k);
+    std::vector<char> mark(H.m);
+    for (int j = 0; j < H.m; ++j) {
+      std::fill(mark.begin(), mark.end(), 0);
+      for (int p = H.col_ptr[j]; p < H.col_ptr[j + 1]; ++p)
+        for (int k : by_species[H.col_species[p]]) mark[k] = 1;
+      for (int k = 0; k < H.m; ++k)
+        if (mark[k]) dep.push_back(static_cast<uint16_t>(k));
+      if (dep.size() > 32767) { *msg = "model too large for the device tables"; return KIN_ERR_INPUT; }
+      dep_ptr.push_back(static_cast<int16_t>(dep.size()));
+    }
+  }
+  T->off_rdesc = put(rdesc.data(), rdesc.size() * 8, 8);
+  T->off_dep = put(dep.data(), dep.size() * 2, 2);
+  T->off_dep_ptr = put(dep_ptr.data(), dep_ptr.size() * 2, 2);
   T->off_rate_axis = put(rate_axis.data(), rate_axis.size(), 1);
   T->off_x0_axis = put(x0ax.data(), x0ax.size(), 1);
   if (overflow) { *msg = "model too large for the device tables"; return KIN_ERR_INPUT; }
@@ -311,10 +347,13 @@ struct Slot {
   cudaStream_t stream = nullptr;
   DevBuf<double> traj, traj_t, mean, m2, axis, grid;
   DevBuf<uint64_t> meta, work;
+  DevBuf<unsigned long long> counter;
   DevBuf<int32_t> status;
   void* stage = nullptr;
   size_t stage_cap = 0;
   cudaEvent_t ev[2] = {nullptr, nullptr};
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // sim start, sim end, stats end
+  bool timed_stats = false;
   // record of the last device-resident launch
   uint64_t s0 = 0, s1 = 0, P0 = 0, nP = 0, R = 1;
   int G = 0, N = 0;
@@ -443,14 +482,20 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
   SD.t_end = d->t_end;
   SD.grid = sl.grid.p;
   KinOutDev O{sl.traj.p, sl.meta.p, sl.status.p, want_work ? sl.work.p : nullptr};
+  if (!sl.tev[0])
+    for (auto& ev : sl.tev) KIN_CUDA(cudaEventCreate(&ev), "event");
+  KIN_CUDA(cudaEventRecord(sl.tev[0], sl.stream), "event");
   cudaError_t e;
   const int kind = d->method.kind;
   if (kind == KIN_METHOD_ODE) {
     e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
   } else {
-    e = kin::launch_stochastic(*T, SD, O, want_work, 64, sl.stream);
+    KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
+    e = kin::launch_stochastic(*T, SD, O, want_work, 32, sl.counter.p, sl.stream);
   }
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
+  KIN_CUDA(cudaEventRecord(sl.tev[1], sl.stream), "event");
+  sl.timed_stats = false;
   // per-point statistics for points entirely inside [s0, s1)
   const uint64_t P0 = (s0 + L.R - 1) / L.R, P1 = s1 / L.R;
   const uint64_t nP = P1 > P0 ? P1 - P0 : 0;
@@ -460,6 +505,8 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
     e = kin::launch_point_stats(sl.traj.p, S, static_cast<int>(gn), L.R, P0 * L.R - s0, nP, sl.mean.p, sl.m2.p,
                                 sl.stream);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
+    KIN_CUDA(cudaEventRecord(sl.tev[2], sl.stream), "event");
+    sl.timed_stats = true;
   }
   sl.s0 = s0;
   sl.s1 = s1;
@@ -569,9 +616,10 @@ void kin_ctx_destroy(kin_ctx* ctx) {
     cudaSetDevice(sl->device);
     cudaStreamSynchronize(sl->stream);
     sl->traj.release(); sl->traj_t.release(); sl->mean.release(); sl->m2.release();
-    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->status.release();
+    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->status.release();
     if (sl->stage) cudaFreeHost(sl->stage);
     for (auto& e : sl->ev) if (e) cudaEventDestroy(e);
+    for (auto& e : sl->tev) if (e) cudaEventDestroy(e);
     cudaStreamDestroy(sl->stream);
   }
   delete ctx;
@@ -718,6 +766,23 @@ int kin_sweep_fetch(kin_ctx* ctx, int32_t slot, kin_sweep_out* out, kin_error* e
   std::lock_guard<std::mutex> lk(sl.mu);
   if (!sl.valid) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
   return fetch_range(sl, out, sl.s0, sl.P0, err);
+}
+
+int kin_sweep_kernel_ms(kin_ctx* ctx, int32_t slot, double* sim_ms, double* stats_ms, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) {
+    set_err(err, KIN_ERR_USAGE, "bad context/slot");
+    return KIN_ERR_USAGE;
+  }
+  Slot& sl = *ctx->slots[slot];
+  if (!sl.valid || !sl.tev[0]) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  float a = 0.0f, b = 0.0f;
+  KIN_CUDA(cudaEventElapsedTime(&a, sl.tev[0], sl.tev[1]), "event time");
+  if (sl.timed_stats) KIN_CUDA(cudaEventElapsedTime(&b, sl.tev[1], sl.tev[2]), "event time");
+  if (sim_ms) *sim_ms = a;
+  if (stats_ms) *stats_ms = sl.timed_stats ? b : 0.0;
+  return KIN_OK;
 }
 
 int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean, int32_t n, uint64_t* out_bits,

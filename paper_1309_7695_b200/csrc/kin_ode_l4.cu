@@ -1,0 +1,9 @@
+// Dopri5 instantiations (see kin_ode_impl.cuh).
+#include "kin_ode_impl.cuh"
+
+namespace kin {
+namespace ode {
+template cudaError_t launch_t<4, 4>(const KinTables&, const KinSweepDev&, const KinOutDev&, bool, cudaStream_t);
+template cudaError_t launch_t<8, 5>(const KinTables&, const KinSweepDev&, const KinOutDev&, bool, cudaStream_t);
+}  // namespace ode
+}  // namespace kin

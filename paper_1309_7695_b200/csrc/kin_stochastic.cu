@@ -3,12 +3,20 @@
 // One CUDA thread = one simulation (the paper's mapping), in
 // "compat" RNG mode: each thread owns the reference's xoshiro256++ stream seeded
 // by derive_run_seed (rng.cpp:25-48, ensemble.hpp:15-18), so firing counts are
-// bit-identical to the CPU reference's.  The per-thread state (amounts x and the
-// leap target buffer) lives in shared memory in [species][thread] layout:
-// lanes touch consecutive 8-byte words, conflict-free, and the model tables are
-// walked with warp-uniform indices out of the kernel-parameter constant bank.
+// bit-identical to the CPU reference's.
 //
-// Mirrors oracle/kin_oracle.cpp simulate_stochastic() statement for statement:
+// Per-thread state in shared memory, [slot][thread] layout (lanes touch
+// consecutive 8-byte words: conflict-free): amounts x[N] and propensities a[M]
+// (evaluated once per decision and reused by a0, select_tau, the Poisson means
+// and the SSA selection; SSA events re-evaluate only the reactions whose
+// reactants changed, via a dependency graph).  A leap updates x IN PLACE; a
+// rejected leap is rolled back by replaying the attempt's draws from a saved
+// copy of the RNG state (exact: integer-valued doubles).  Model tables are
+// walked with warp-uniform indices out of the kernel-parameter constant bank.
+// Persistent warps fetch 32 simulations at a time from a global counter, so the
+// grid is exactly one wave and the tail is one simulation, not one block.
+//
+// Mirrors oracle/kin_oracle.cpp simulate_stochastic() operation for operation:
 //   simulate_approx TauAdaptive/TauFixed ... stochastic.hpp:78-92
 //   select_tau ............................. stochastic.hpp:40-46
 //   tau_leap_step / rejection-halving ...... stochastic.hpp:48-57
@@ -23,58 +31,78 @@ namespace kin {
 namespace {
 
 constexpr double kInf = __builtin_huge_val();
+constexpr int kBlock = 32;  // one warp per block: finest smem granularity
 
-struct ThreadState {
+struct Sim {
   const KinTables& T;
-  const double* av;  // this thread's axis values (stride B)
+  double* x;         // x[i * B]
+  double* a;         // a[j * B]
+  const double* av;  // axis values av[ax * B]
   int B;
-  __device__ __forceinline__ double rate(int j) const {
-    const int ax = tab_rate_axis(T, j);
-    return ax < 0 ? tab_rate(T, j) : av[ax * B];
-  }
+
   // a_j(x) = c_j * prod h(x_s, stoich_s)   (model.hpp:151-157)
-  __device__ __forceinline__ double prop(int j, const double* x) const {
-    double aj = rate(j);
-    const int p1 = tab_rt_ptr(T, j + 1);
-    for (int p = tab_rt_ptr(T, j); p < p1; ++p) {
-      const uint32_t e = tab_rt(T, p);
-      aj = __dmul_rn(aj, combinations(x[KIN_TERM_SPECIES(e) * B], KIN_TERM_STOICH(e)));
+  __device__ __forceinline__ double prop(int j) const {
+    const uint64_t d = tab_rdesc(T, j);
+    const int ax = KIN_RD_AXIS(d);
+    double aj = ax < 0 ? tab_rate(T, j) : av[ax * B];
+    const int nt = KIN_RD_NTERMS(d);
+    if (nt > 0) {
+      aj = __dmul_rn(aj, combinations(x[KIN_RD_SPECIES(d, 0) * B], KIN_RD_STOICH(d, 0)));
+      if (nt > 1) {
+        aj = __dmul_rn(aj, combinations(x[KIN_RD_SPECIES(d, 1) * B], KIN_RD_STOICH(d, 1)));
+        if (nt > 2) aj = __dmul_rn(aj, combinations(x[KIN_RD_SPECIES(d, 2) * B], KIN_RD_STOICH(d, 2)));
+      }
     }
     return aj;
+  }
+  // all propensities; returns a0 summed in reaction order (oracle order)
+  __device__ __forceinline__ double all_props(int M) const {
+    double a0 = 0.0;
+    for (int j = 0; j < M; ++j) {
+      const double aj = prop(j);
+      a[j * B] = aj;
+      a0 = __dadd_rn(a0, aj);
+    }
+    return a0;
+  }
+  __device__ __forceinline__ double sum_props(int M) const {
+    double a0 = 0.0;
+    for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, a[j * B]);
+    return a0;
+  }
+  // x += sign * nu[:, j] * k
+  __device__ __forceinline__ void apply(int j, double kj) const {
+    const int p1 = tab_col_ptr(T, j + 1);
+    for (int p = tab_col_ptr(T, j); p < p1; ++p) {
+      const uint32_t e = tab_col(T, p);
+      double* xs = x + KIN_NU_INDEX(e) * B;
+      *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), kj));
+    }
   }
 };
 
 template <bool kCount>
-__global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__ KinTables T,
-                                                         const __grid_constant__ KinSweepDev S,
-                                                         KinOutDev O) {
-  extern __shared__ double smem[];
-  const int B = blockDim.x, tid = threadIdx.x;
-  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * B + tid;
-  if (s >= S.n_local) return;
+__device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                                             uint64_t s, double* x, double* a, double* av, int B) {
   const uint64_t sim = S.sim_begin + s;
   const int N = T.n, M = T.m, G = T.n_grid;
   const uint64_t nloc = S.n_local;
 
-  double* x = smem + tid;
-  double* xn = smem + static_cast<size_t>(N) * B + tid;
-  double* av = smem + static_cast<size_t>(2 * N) * B + tid;
-
   // Cartesian decode, last axis fastest.
   {
     uint64_t rem = sim / S.runs;
-    for (int a = S.n_axes - 1; a >= 0; --a) {
-      const uint64_t nv = static_cast<uint64_t>(S.axis_n[a]);
+    for (int ax = S.n_axes - 1; ax >= 0; --ax) {
+      const uint64_t nv = static_cast<uint64_t>(S.axis_n[ax]);
       const uint64_t q = rem / nv;
-      av[a * B] = __ldg(S.axis_values[a] + (rem - q * nv));
+      av[ax * B] = __ldg(S.axis_values[ax] + (rem - q * nv));
       rem = q;
     }
   }
-  ThreadState ts{T, av, B};
   for (int i = 0; i < N; ++i) {
     const int ax = tab_x0_axis(T, i);
     x[i * B] = ax < 0 ? tab_x0(T, i) : av[ax * B];
   }
+  const Sim sm{T, x, a, av, B};
 
   Xoshiro rng;
   rng.seed(sim_seed(S, sim));
@@ -82,11 +110,11 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
   const double t_end = S.t_end;
   double t = 0.0;
   int gi = 0;
-  uint64_t flops = 0, used = 0;
+  uint64_t flops = 0, used = 0, dummy = 0;
   uint64_t n_steps = 0, n_rej = 0, n_ssa = 0;
   int status = 0;
   const uint64_t budget = S.max_steps;
-  const uint64_t F_prop = static_cast<uint64_t>(T.fprop);  // algorithmic flops of one propensity pass
+  const uint64_t F_prop = static_cast<uint64_t>(T.fprop);
 
   auto emit = [&]() {
     double* o = O.traj + static_cast<size_t>(gi) * N * nloc + s;
@@ -95,11 +123,13 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
   };
 
   while (gi < G && tab_grid(T, S, gi) <= t) emit();
+  bool a_valid = false;
+  double a0 = 0.0;
 
   while (t < t_end) {
     if (++used > budget) { status = KIN_SIM_BUDGET; break; }
-    double a0 = 0.0;
-    for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, ts.prop(j, x));
+    if (!a_valid) a0 = sm.all_props(M);
+    a_valid = false;
     if (kCount) flops += F_prop + M;
     if (a0 == 0.0) break;
 
@@ -118,7 +148,7 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
         for (int p = p0; p < p1; ++p) {
           const uint32_t e = tab_row(T, p);
           const int dl = KIN_NU_DELTA(e);
-          const double aj = ts.prop(KIN_NU_INDEX(e), x);
+          const double aj = a[KIN_NU_INDEX(e) * B];
           mu = __dadd_rn(mu, __dmul_rn(static_cast<double>(dl), aj));
           s2 = __dadd_rn(s2, __dmul_rn(static_cast<double>(dl * dl), aj));
         }
@@ -148,10 +178,8 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
       bool stop = false;
       for (int b = 0;; ++b) {
         if (b > 0) {
-          if (kind != 0 && b >= 100) break;
+          if (kind != 0 && b >= 100) { a_valid = true; break; }
           if (++used > budget) { status = KIN_SIM_BUDGET; stop = true; break; }
-          a0 = 0.0;
-          for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, ts.prop(j, x));
           if (kCount) flops += F_prop + M;
           if (a0 == 0.0) { stop = true; break; }
         }
@@ -167,7 +195,7 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
         double c = 0.0;
         int sel = -1, last = -1;
         for (int j = 0; j < M; ++j) {
-          const double aj = ts.prop(j, x);
+          const double aj = a[j * B];
           if (aj > 0.0) last = j;
           c = __dadd_rn(c, aj);
           if (c > target) { sel = j; break; }
@@ -179,16 +207,23 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
         bool neg = false;
         for (int p = p0; p < p1; ++p) {
           const uint32_t e = tab_col(T, p);
-          const int sp = KIN_NU_INDEX(e);
-          const double v = __dadd_rn(x[sp * B], static_cast<double>(KIN_NU_DELTA(e)));
-          if (v < 0.0) neg = true;
-          x[sp * B] = v;
+          double* xs = x + KIN_NU_INDEX(e) * B;
+          const double v = __dadd_rn(*xs, static_cast<double>(KIN_NU_DELTA(e)));
+          neg |= v < 0.0;
+          *xs = v;
         }
         if (neg) { status = KIN_SIM_NEGATIVE; stop = true; break; }
         if (kCount) flops += static_cast<uint64_t>(p1 - p0);
         t = tn;
         if (kind == 0) ++n_steps; else ++n_ssa;
         while (gi < G && tab_grid(T, S, gi) <= t) emit();
+        // re-evaluate the propensities that changed, then a0 in oracle order
+        const int q1 = tab_dep_ptr(T, sel + 1);
+        for (int q = tab_dep_ptr(T, sel); q < q1; ++q) {
+          const int k = tab_dep(T, q);
+          a[k * B] = sm.prop(k);
+        }
+        a0 = sm.sum_props(M);
       }
       if (stop) break;
       continue;
@@ -200,29 +235,27 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
     const double gap = __dsub_rn(t_stop, t);
     if (kCount) flops += 1;
     if (!(tau < gap)) { tau = gap; hit = true; }
+    Xoshiro saved = rng;
     for (;;) {
-      for (int i = 0; i < N; ++i) xn[i * B] = x[i * B];
       for (int j = 0; j < M; ++j) {
-        const uint64_t k = poisson<kCount>(rng, __dmul_rn(ts.prop(j, x), tau), flops);
-        if (k == 0) continue;
-        const double kj = static_cast<double>(k);
-        const int p1 = tab_col_ptr(T, j + 1);
-        for (int p = tab_col_ptr(T, j); p < p1; ++p) {
-          const uint32_t e = tab_col(T, p);
-          const int sp = KIN_NU_INDEX(e);
-          xn[sp * B] = __dadd_rn(xn[sp * B], __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), kj));
-        }
+        const uint64_t k = poisson<kCount>(rng, __dmul_rn(a[j * B], tau), flops);
+        if (k != 0) sm.apply(j, static_cast<double>(k));
       }
       if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
       bool neg = false;
-      for (int i = 0; i < N; ++i) neg |= xn[i * B] < 0.0;
+      for (int i = 0; i < N; ++i) neg |= x[i * B] < 0.0;
       if (!neg) break;
+      // rejected: undo exactly by replaying the same draws, continue the stream
+      for (int j = 0; j < M; ++j) {
+        const uint64_t k = poisson<false>(saved, __dmul_rn(a[j * B], tau), dummy);
+        if (k != 0) sm.apply(j, -static_cast<double>(k));
+      }
+      saved = rng;
       ++n_rej;
       tau = __dmul_rn(tau, 0.5);
       hit = false;
       if (kCount) flops += 1;
     }
-    { double* tmp = x; x = xn; xn = tmp; }
     if (hit) {
       t = t_stop;
     } else {
@@ -246,24 +279,53 @@ __global__ void __launch_bounds__(256) stochastic_kernel(const __grid_constant__
   if (kCount && O.work) O.work[s] = flops;
 }
 
+template <bool kCount>
+__global__ void __launch_bounds__(kBlock) stochastic_kernel(const __grid_constant__ KinTables T,
+                                                            const __grid_constant__ KinSweepDev S, KinOutDev O,
+                                                            unsigned long long* __restrict__ next) {
+  extern __shared__ double smem[];
+  const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+  double* x = smem + tid;
+  double* a = smem + static_cast<size_t>(T.n) * B + tid;
+  double* av = smem + static_cast<size_t>(T.n + T.m) * B + tid;
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(next, 32ULL);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (base >= S.n_local) break;
+    const uint64_t s = base + lane;
+    if (s < S.n_local) simulate_one<kCount>(T, S, O, s, x, a, av, B);
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block) {
-  return static_cast<size_t>(2 * T.n + S.n_axes) * block * sizeof(double);
+  return static_cast<size_t>(T.n + T.m + S.n_axes) * block * sizeof(double);
 }
 
 cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
-                              int block, cudaStream_t stream) {
+                              int block, unsigned long long* counter, cudaStream_t stream) {
+  (void)block;
   if (S.n_local == 0) return cudaSuccess;
-  const size_t smem = stochastic_smem_bytes(T, S, block);
-  const unsigned grid = static_cast<unsigned>((S.n_local + block - 1) / block);
-  if (count) {
-    cudaFuncSetAttribute(stochastic_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    stochastic_kernel<true><<<grid, block, smem, stream>>>(T, S, O);
-  } else {
-    cudaFuncSetAttribute(stochastic_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    stochastic_kernel<false><<<grid, block, smem, stream>>>(T, S, O);
-  }
+  const size_t smem = stochastic_smem_bytes(T, S, kBlock);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  auto kern = count ? stochastic_kernel<true> : stochastic_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t warps = (S.n_local + 31) / 32;
+  const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,14 @@
 #define KIN_TERM_STOICH(e) ((int)(((e) >> 16) & 0xFF))
 #define KIN_NU_INDEX(e) ((int)((e) & 0xFFFF))
 #define KIN_NU_DELTA(e) ((int)(((e) >> 16) & 0xFF) - 128)
+//   reaction descriptor (uint64): reactant species t0,t1,t2 (16 bits each, bits
+//   0-47), their stoichiometries (2 bits each, bits 48-53), number of reactant
+//   terms (bits 54-55) and the sweep axis carrying c_j plus one (bits 56-63, 0 =
+//   none).  Terms are species-ascending (std::map order, model.hpp:33).
+#define KIN_RD_SPECIES(d, t) ((int)(((d) >> (16 * (t))) & 0xFFFF))
+#define KIN_RD_STOICH(d, t) ((int)(((d) >> (48 + 2 * (t))) & 0x3))
+#define KIN_RD_NTERMS(d) ((int)(((d) >> 54) & 0x3))
+#define KIN_RD_AXIS(d) ((int)(((d) >> 56) & 0xFF) - 1)
 
 struct KinTables {
   int32_t n;          // species
@@ -43,6 +51,10 @@ struct KinTables {
   uint32_t off_row_ptr;   // int16  [n+1] nu rows (reaction-ascending)
   uint32_t off_row;       // uint32 [nnz] packed (reaction, delta)
   uint32_t off_grid;      // double [n_grid] sampling grid (0 when it did not fit: use SweepDev::grid)
+  uint32_t off_rdesc;     // uint64 [m]   packed reaction descriptor (KIN_RD_* below)
+  uint32_t off_dep_ptr;   // int16  [m+1] reactions whose propensity changes when j fires
+  uint32_t off_dep;       // uint16 [..]
+  uint32_t pad1_;
   uint32_t used;
   uint32_t pad_;
   alignas(16) unsigned char blob[KIN_TABLE_BYTES];
