@@ -113,19 +113,59 @@ struct Xoshiro {
   }
 };
 
+// mean / k, correctly rounded.  Division by a power of two is exact scaling, so
+// mean*2^-j is bit-identical to mean/2^j; only other k need the IEEE divide.
+__device__ __forceinline__ double div_small(double mean, int k) {
+  switch (k) {
+    case 1: return mean;
+    case 2: return __dmul_rn(mean, 0.5);
+    case 4: return __dmul_rn(mean, 0.25);
+    case 8: return __dmul_rn(mean, 0.125);
+    default: return __ddiv_rn(mean, static_cast<double>(k));
+  }
+}
+
 // draw_poisson (rng.cpp:68-109): inversion below mean 10, Hormann PTRS above.
 // `flops` receives the algorithmic op count (same accounting as the oracle).
+// lgamma(k+1), k < KIN_LGAMMA_N, computed by the host's glibc (the oracle's libm)
+// and uploaded once per context (see kin_engine.cpp).
+#define KIN_LGAMMA_N 4096
 template <bool kCount>
-__device__ __forceinline__ uint64_t poisson(Xoshiro& rng, double mean, uint64_t& flops) {
+__device__ __forceinline__ uint64_t poisson(Xoshiro& rng, double mean, uint64_t& flops, const double* lgamma_tab) {
   if (!(mean > 0.0)) return 0;
   if (mean < 10.0) {
     const double u = rng.uniform();
+    // Fast decision path (returns exactly the k of the reference algorithm):
+    // search an approximate CDF c'_k built from the FP32 exponential.  With
+    // mean in (0,10), __expf errs by <= 13 float ulp (1.55e-6) and the
+    // float rounding of mean adds <= 6e-7; the double recursion with a float
+    // reciprocal adds <= k*6.1e-8.  So |c'_k - c_k| <= (2.2e-6 + k*6.1e-8) c_k
+    // for the reference's own c_k (itself within (k+2)*2^-52 of the exact
+    // value).  If u clears c'_{k-1} and c'_k by the guard G = 2e-5 (k <= 40:
+    // error <= 4.7e-6 < G/4), the reference stops at the same k.  Otherwise
+    // (probability ~4e-5 per draw) run the exact algorithm.
+    {
+      constexpr double G = 2e-5;
+      double pf = static_cast<double>(__expf(-static_cast<float>(mean)));
+      double cf = pf, cprev = 0.0;
+      int kk = 0;
+      while (u > cf * (1.0 + G) && kk < 40) {
+        ++kk;
+        pf = pf * (mean * static_cast<double>(__frcp_rn(static_cast<float>(kk))));
+        cprev = cf;
+        cf = cf + pf;
+      }
+      if (kk < 40 && u < cf * (1.0 - G) && (kk == 0 || u > cprev * (1.0 + G))) {
+        if (kCount) flops += 3 + 3 * static_cast<uint64_t>(kk);
+        return static_cast<uint64_t>(kk);
+      }
+    }
     double p = exp(-mean);
     double c = p;
     uint64_t k = 0;
     while (u > c && k < 256) {
       ++k;
-      p = __dmul_rn(p, __ddiv_rn(mean, static_cast<double>(k)));
+      p = __dmul_rn(p, div_small(mean, static_cast<int>(k)));
       c = __dadd_rn(c, p);
     }
     if (kCount) flops += 3 + 3 * k;
@@ -146,9 +186,22 @@ __device__ __forceinline__ uint64_t poisson(Xoshiro& rng, double mean, uint64_t&
     if (kf < 0.0) continue;
     if (us >= 0.07 && v <= v_r) return static_cast<uint64_t>(kf);
     if (us < 0.013 && v > us) continue;
-    const double lhs = log(__ddiv_rn(__dmul_rn(v, inv_alpha), __dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b)));
-    const double rhs = __dsub_rn(__dadd_rn(-mean, __dmul_rn(kf, lm)), lgamma(__dadd_rn(kf, 1.0)));
+    const double arg = __ddiv_rn(__dmul_rn(v, inv_alpha), __dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b));
+    // lgamma(kf+1): glibc's own values (host table) for kf < KIN_LGAMMA_N
+    const double lg = kf < static_cast<double>(KIN_LGAMMA_N) ? __ldg(lgamma_tab + static_cast<int>(kf))
+                                                             : lgamma(__dadd_rn(kf, 1.0));
+    const double rhs = __dsub_rn(__dadd_rn(-mean, __dmul_rn(kf, lm)), lg);
     if (kCount) flops += 11;
+    // Fast decision on lhs = log(arg): __logf errs by <= 2^-21.41 absolute on
+    // [0.5,2] and <= 3 ulp elsewhere, float rounding of arg adds <= 6e-8; a
+    // guard of 1e-4*max(1,|lhs|) (> 100x that) decides lhs <= rhs exactly
+    // unless lhs is within the guard of rhs, where the double log is used.
+    const float lf = __logf(static_cast<float>(arg));
+    const double lfa = static_cast<double>(lf);
+    const double guard = 1e-4 * fmax(1.0, fabs(lfa));
+    if (isfinite(lfa) && lfa + guard < rhs) return static_cast<uint64_t>(kf);
+    if (isfinite(lfa) && lfa - guard > rhs) continue;
+    const double lhs = log(arg);
     if (lhs <= rhs) return static_cast<uint64_t>(kf);
   }
 }

@@ -348,6 +348,7 @@ struct Slot {
   DevBuf<double> traj, traj_t, mean, m2, axis, grid;
   DevBuf<uint64_t> meta, work;
   DevBuf<unsigned long long> counter;
+  DevBuf<double> lgamma_tab;  // glibc lgamma(k+1), k < KIN_LGAMMA_N
   DevBuf<int32_t> status;
   void* stage = nullptr;
   size_t stage_cap = 0;
@@ -481,6 +482,7 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
   SD.n_local = S;
   SD.t_end = d->t_end;
   SD.grid = sl.grid.p;
+  SD.lgamma_tab = sl.lgamma_tab.p;
   KinOutDev O{sl.traj.p, sl.meta.p, sl.status.p, want_work ? sl.work.p : nullptr};
   if (!sl.tev[0])
     for (auto& ev : sl.tev) KIN_CUDA(cudaEventCreate(&ev), "event");
@@ -604,6 +606,11 @@ int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err)
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dv);
     if (major < 10) { set_err(err, KIN_ERR_DEVICE, "engine is built for sm_100a (B200) only"); return KIN_ERR_DEVICE; }
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    // lgamma(k+1) from the host libm (the oracle's, glibc) for the PTRS test
+    std::vector<double> lg(KIN_LGAMMA_N);
+    for (int k = 0; k < KIN_LGAMMA_N; ++k) lg[k] = std::lgamma(static_cast<double>(k) + 1.0);
+    KIN_CUDA(sl->lgamma_tab.ensure(KIN_LGAMMA_N), "cudaMalloc lgamma table");
+    KIN_CUDA(cudaMemcpy(sl->lgamma_tab.p, lg.data(), sizeof(double) * KIN_LGAMMA_N, cudaMemcpyHostToDevice), "H2D lgamma");
     ctx->slots.push_back(std::move(sl));
   }
   *out = ctx.release();
@@ -616,7 +623,7 @@ void kin_ctx_destroy(kin_ctx* ctx) {
     cudaSetDevice(sl->device);
     cudaStreamSynchronize(sl->stream);
     sl->traj.release(); sl->traj_t.release(); sl->mean.release(); sl->m2.release();
-    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->status.release();
+    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->lgamma_tab.release(); sl->status.release();
     if (sl->stage) cudaFreeHost(sl->stage);
     for (auto& e : sl->ev) if (e) cudaEventDestroy(e);
     for (auto& e : sl->tev) if (e) cudaEventDestroy(e);
@@ -796,7 +803,7 @@ int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
   uint64_t* d = nullptr;
   KIN_CUDA(cudaMalloc(&d, sizeof(uint64_t) * std::max(n, 1)), "cudaMalloc");
-  cudaError_t e = kin::launch_rng_draws(seed, kind, mean, n, d, sl.stream);
+  cudaError_t e = kin::launch_rng_draws(seed, kind, mean, n, d, sl.lgamma_tab.p, sl.stream);
   if (e == cudaSuccess) e = cudaMemcpyAsync(out_bits, d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, sl.stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
   cudaFree(d);

@@ -27,7 +27,8 @@ cudaError_t launch_transpose_traj(const double* traj_dev, double* dst, uint64_t 
 cudaError_t launch_point_stats(const double* traj_dev, uint64_t n_local, int gn, uint64_t runs,
                                uint64_t first_point_offset, uint64_t n_points, double* mean, double* m2,
                                cudaStream_t stream);
-cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, cudaStream_t stream);
+cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, const double* lgamma_tab,
+                             cudaStream_t stream);
 cudaError_t measure_fp64_peak(cudaStream_t stream, double* tflops);
 
 }  // namespace kin

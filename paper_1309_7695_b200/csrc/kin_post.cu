@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(TILE* ROWS) stats_kernel(const double* __restr
   }
 }
 
-__global__ void rng_kernel(uint64_t seed, int kind, double mean, int n, uint64_t* out) {
+__global__ void rng_kernel(uint64_t seed, int kind, double mean, int n, uint64_t* out, const double* lgamma_tab) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   Xoshiro rng;
   rng.seed(seed);
@@ -109,7 +109,7 @@ __global__ void rng_kernel(uint64_t seed, int kind, double mean, int n, uint64_t
       }
       bits = __double_as_longlong(v);
     } else {
-      bits = poisson<false>(rng, mean, dummy);
+      bits = poisson<false>(rng, mean, dummy, lgamma_tab);
     }
     out[q] = bits;
   }
@@ -148,8 +148,9 @@ cudaError_t launch_point_stats(const double* traj_dev, uint64_t n_local, int gn,
   return cudaGetLastError();
 }
 
-cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, cudaStream_t st) {
-  rng_kernel<<<1, 32, 0, st>>>(seed, kind, mean, n, out);
+cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, const double* lgamma_tab,
+                             cudaStream_t st) {
+  rng_kernel<<<1, 32, 0, st>>>(seed, kind, mean, n, out, lgamma_tab);
   return cudaGetLastError();
 }
 

@@ -154,17 +154,30 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         }
         if (kCount) flops += 4 * static_cast<uint64_t>(p1 - p0);
         if (mu == 0.0 && s2 == 0.0) continue;
-        double bound = __ddiv_rn(__dmul_rn(eps, x[i * B]), tab_g(T, i));
+        // (eps*x)/g with g in {1,2,3}: /1 and /2 are exact scalings
+        const double ex = __dmul_rn(eps, x[i * B]);
+        const double g = tab_g(T, i);
+        double bound = g == 1.0 ? ex : (g == 2.0 ? __dmul_rn(ex, 0.5) : __ddiv_rn(ex, g));
         if (bound < 1.0) bound = 1.0;
         if (kCount) flops += 2;
+        // A quotient q = num/den can only lower tau if num <= tau*den (up to
+        // rounding).  fl(tau*den) errs by <= 2^-53 relative, so num >
+        // fl(tau*den)*(1 + 2^-50) proves q > tau, hence fl(q) >= tau and the
+        // (exact, same-as-oracle) division can be skipped.
         if (mu != 0.0) {
-          const double t1 = __ddiv_rn(bound, fabs(mu));
-          if (t1 < tau) tau = t1;
+          const double amu = fabs(mu);
+          if (!(bound > __dmul_rn(__dmul_rn(tau, amu), 1.0 + 0x1p-50))) {
+            const double t1 = __ddiv_rn(bound, amu);
+            if (t1 < tau) tau = t1;
+          }
           if (kCount) flops += 1;
         }
         if (s2 != 0.0) {
-          const double t2 = __ddiv_rn(__dmul_rn(bound, bound), s2);
-          if (t2 < tau) tau = t2;
+          const double bb = __dmul_rn(bound, bound);
+          if (!(bb > __dmul_rn(__dmul_rn(tau, s2), 1.0 + 0x1p-50))) {
+            const double t2 = __ddiv_rn(bb, s2);
+            if (t2 < tau) tau = t2;
+          }
           if (kCount) flops += 2;
         }
       }
@@ -238,7 +251,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     Xoshiro saved = rng;
     for (;;) {
       for (int j = 0; j < M; ++j) {
-        const uint64_t k = poisson<kCount>(rng, __dmul_rn(a[j * B], tau), flops);
+        const uint64_t k = poisson<kCount>(rng, __dmul_rn(a[j * B], tau), flops, S.lgamma_tab);
         if (k != 0) sm.apply(j, static_cast<double>(k));
       }
       if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
@@ -247,7 +260,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
       if (!neg) break;
       // rejected: undo exactly by replaying the same draws, continue the stream
       for (int j = 0; j < M; ++j) {
-        const uint64_t k = poisson<false>(saved, __dmul_rn(a[j * B], tau), dummy);
+        const uint64_t k = poisson<false>(saved, __dmul_rn(a[j * B], tau), dummy, S.lgamma_tab);
         if (k != 0) sm.apply(j, -static_cast<double>(k));
       }
       saved = rng;

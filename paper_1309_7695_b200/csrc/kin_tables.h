@@ -80,6 +80,7 @@ struct KinSweepDev {
   uint64_t n_local;     // simulations in this launch
   double t_end;
   const double* grid;   // device pointer [n_grid]
+  const double* lgamma_tab;  // device pointer [KIN_LGAMMA_N]: glibc lgamma(k+1)
 };
 
 // Device outputs of one launch (local simulation index s in [0, n_local)).

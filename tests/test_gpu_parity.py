@@ -54,6 +54,20 @@ def test_device_rng_matches_oracle(engine, oracle, kind, mean):
         assert np.array_equal(out, ref), (seed, kind, mean)
 
 
+def test_device_poisson_dense_mean_scan(engine, oracle):
+    """Exactness of the decision fast paths: 400 means over 10 decades (dense
+    around the inversion/PTRS switch at 10), 2,000 draws each."""
+    import ctypes as C
+    means = np.concatenate([np.logspace(-4, 6.5, 360), np.linspace(9.9, 10.1, 40)])
+    for q, mean in enumerate(means):
+        out = np.zeros(2000, dtype=np.uint64)
+        err = abi.KinError()
+        rc = engine.lib.kin_device_rng_draws(engine.ctx, 1000 + q, 3, float(mean), 2000, abi.ptr(out, C.c_uint64),
+                                             C.byref(err))
+        assert rc == 0, err.text()
+        assert np.array_equal(out, oracle.rng_draws(1000 + q, 3, 2000, float(mean))), mean
+
+
 def test_device_normal_close(engine, oracle):
     import ctypes as C
     n = 1000
