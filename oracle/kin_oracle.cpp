@@ -19,6 +19,8 @@
 // proj/CMakeLists.txt:6-8, with contraction pinned off so the CUDA kernels,
 // compiled with -fmad=false on the parity path, round identically).
 #include "kin_oracle.hpp"
+#include "kin_lsoda.hpp"
+#include "kin_portable_math.hpp"
 
 #include <algorithm>
 #include <atomic>
@@ -45,6 +47,10 @@ void Scratch::resize(int n, int m) {
   x.assign(n, 0.0);
   xn.assign(n, 0.0);
   x0.assign(n, 0.0);
+  z.assign(static_cast<size_t>(kLsodaL) * n + 1, 0.0);
+  jac.assign(static_cast<size_t>(n) * n + 1, 0.0);
+  jac2.assign(static_cast<size_t>(n) * n + 1, 0.0);
+  piv.assign(n + 1, 0);
   a.assign(m, 0.0);
   rates.assign(m, 0.0);
   k.assign(m, 0);
@@ -482,11 +488,432 @@ int integrate_rre(const Network& net, const double* rates, const double* x0,
   return KIN_SIM_OK;
 }
 
-constexpr bool kLsodaAvailable = false;
+constexpr bool kLsodaAvailable = true;
+
+// Analytic Jacobian of the RRE, J = nu * da/dx (row-major N x N), continuous
+// combinations with the same clamp as propensities (zero slope where clamped).
 template <bool C>
-int integrate_lsoda(const Network&, const double*, const double*, const kin_integrator_config&,
-                    double, const double*, int, double*, std::uint64_t*, Scratch&, Work*) {
-  return KIN_SIM_NONFINITE;
+void rre_jacobian(const Network& net, const double* rates, const double* x, double* J, Work* w) {
+  const int n = net.n;
+  for (int q = 0; q < n * n; ++q) J[q] = 0.0;
+  for (int k = 0; k < net.m; ++k) {
+    const int p0 = net.rt_ptr[k], p1 = net.rt_ptr[k + 1];
+    for (int p = p0; p < p1; ++p) {
+      // d a_k / d x_s for reactant term p
+      const int s = net.rt_species[p], st = net.rt_stoich[p];
+      const double xs = x[s];
+      double dh;
+      const double h = combinations(xs, st);
+      if (st == 1) dh = xs < 0.0 ? 0.0 : 1.0;
+      else if (st == 2) dh = h > 0.0 ? xs - 0.5 : 0.0;
+      else dh = h > 0.0 ? ((3.0 * xs - 6.0) * xs + 2.0) / 6.0 : 0.0;
+      double d = rates[k] * dh;
+      for (int q = p0; q < p1; ++q)
+        if (q != p) d = d * combinations(x[net.rt_species[q]], net.rt_stoich[q]);
+      for (int c = net.col_ptr[k]; c < net.col_ptr[k + 1]; ++c)
+        J[net.col_species[c] * n + s] += static_cast<double>(net.col_delta[c]) * d;
+      if constexpr (C) w->flops += 4 + (p1 - p0) + 2 * static_cast<std::uint64_t>(net.col_ptr[k + 1] - net.col_ptr[k]);
+    }
+  }
+}
+
+// LU with partial pivoting, in place (row-major), piv[i] = pivot row.
+// Returns false when singular.
+template <bool C>
+bool lu_factor(double* A, int n, int* piv, Work* w) {
+  for (int k = 0; k < n; ++k) {
+    int pr = k;
+    double best = std::fabs(A[k * n + k]);
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(A[i * n + k]) > best) { best = std::fabs(A[i * n + k]); pr = i; }
+    piv[k] = pr;
+    if (best == 0.0) return false;
+    if (pr != k)
+      for (int j = 0; j < n; ++j) std::swap(A[k * n + j], A[pr * n + j]);
+    const double inv = 1.0 / A[k * n + k];
+    for (int i = k + 1; i < n; ++i) {
+      const double l = A[i * n + k] * inv;
+      A[i * n + k] = l;
+      for (int j = k + 1; j < n; ++j) A[i * n + j] -= l * A[k * n + j];
+    }
+  }
+  if constexpr (C) w->flops += static_cast<std::uint64_t>(2 * n * n * n / 3 + n);
+  return true;
+}
+
+template <bool C>
+void lu_solve(const double* A, int n, const int* piv, double* b, Work* w) {
+  for (int k = 0; k < n; ++k) {
+    if (piv[k] != k) std::swap(b[k], b[piv[k]]);
+    for (int i = k + 1; i < n; ++i) b[i] -= A[i * n + k] * b[k];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < n; ++j) s -= A[i * n + j] * b[j];
+    b[i] = s / A[i * n + i];
+  }
+  if constexpr (C) w->flops += static_cast<std::uint64_t>(2 * n * n);
+}
+
+// LSODA-style integration of the RRE (see oracle/kin_lsoda.hpp for sources).
+// Nordsieck history Z[j] = h^j y^(j)/j!, j = 0..12; Adams orders 1..12 with
+// functional iteration, BDF orders 1..5 with chord Newton on P = I - h*l0*J;
+// LSODE error test, order/step selection every nq+1 steps; LSODA method
+// switching (stiffness ratio 5, Adams stability sizes sm1, Jacobian norm).
+// Grid values by Nordsieck interpolation inside each accepted step, floored at
+// zero (flag); the state itself is not modified.
+template <bool C>
+int integrate_lsoda(const Network& net, const double* rates, const double* x0, const kin_integrator_config& cfg,
+                    double t_end, const double* grid, int n_grid, double* out, std::uint64_t* meta, Scratch& sc,
+                    Work* w) {
+  static const LsodaCoeffs CO = [] { LsodaCoeffs c; kin_lsoda_coeffs(&c); return c; }();
+  const int n = net.n;
+  const double rtol = cfg.rel_tol, atol = cfg.abs_tol;
+  const double hmax = cfg.h_max > 0.0 ? cfg.h_max : kInf;
+  const std::uint64_t F_rhs = static_cast<std::uint64_t>(
+      [&] { std::uint64_t f = 0; for (int p = 0; p < static_cast<int>(net.rt_species.size()); ++p) f += 1 + combinations_flops(net.rt_stoich[p]); return f; }() +
+      2 * net.row_reaction.size());
+  double* Z = sc.z.data();  // 13 x n
+  double* acor = sc.v[0].data();
+  double* savf = sc.v[1].data();
+  double* ewt = sc.v[2].data();
+  double* y = sc.v[3].data();
+  double* tmp = sc.v[4].data();
+  double* P = sc.jac.data();
+  int* piv = sc.piv.data();
+  double* a = sc.a.data();
+  auto Zr = [&](int j) { return Z + static_cast<size_t>(j) * n; };
+  for (int q = 0; q < 6; ++q) meta[q] = 0;
+  bool floored = false;
+  auto rhs = [&](const double* yy, double* f) {
+    rre_rhs<false>(net, rates, yy, a, f, nullptr);
+    if constexpr (C) w->flops += F_rhs;
+  };
+  auto wrms = [&](const double* v) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) { const double q = v[i] / ewt[i]; s += q * q; }
+    if constexpr (C) w->flops += 3 * static_cast<std::uint64_t>(n) + 2;
+    return std::sqrt(s / n);
+  };
+  auto emit = [&](int g, const double* v) {
+    double* o = out + static_cast<size_t>(g) * n;
+    for (int i = 0; i < n; ++i) {
+      double vi = v[i];
+      if (vi < 0.0) { vi = 0.0; floored = true; }
+      o[i] = vi;
+    }
+  };
+
+  double t = 0.0;
+  int gi = 0;
+  for (int i = 0; i < n; ++i) y[i] = x0[i];
+  while (gi < n_grid && grid[gi] <= t) emit(gi++, y);
+  if (!(t < t_end)) {
+    while (gi < n_grid) emit(gi++, y);
+    return KIN_SIM_OK;
+  }
+  for (int i = 0; i < n; ++i) { Zr(0)[i] = y[i]; ewt[i] = rtol * std::fabs(y[i]) + atol; }
+  rhs(y, savf);
+  double h;
+  if (cfg.h_init > 0.0) {
+    h = cfg.h_init;
+  } else {
+    // LSODA's starting step: h0 = (1/(tol*w0^2) + tol*||f0||^2)^(-1/2), weighted
+    // max-norm, tol = rtol clamped to [100*uround, 1e-3], w0 = tdist = t_end
+    double tol = rtol;
+    if (tol < 100.0 * 2.220446049250313e-16) tol = 100.0 * 2.220446049250313e-16;
+    if (tol > 1e-3) tol = 1e-3;
+    double fn = 0.0;
+    for (int i = 0; i < n; ++i) fn = std::max(fn, std::fabs(savf[i]) / ewt[i]);
+    const double w0 = t_end;
+    const double sum = 1.0 / (tol * w0 * w0) + tol * fn * fn;
+    h = 1.0 / std::sqrt(sum);
+    if (h > t_end) h = t_end;
+    if (h > hmax) h = hmax;
+    if constexpr (C) w->flops += 2 * static_cast<std::uint64_t>(n) + 10;
+  }
+  for (int i = 0; i < n; ++i) Zr(1)[i] = h * savf[i];
+
+  int meth = 0;  // 0 Adams, 1 BDF
+  int nq = 1;
+  int ialth = 2;
+  int icount = 20;
+  double rmax = 1.0e4;
+  double crate = 0.7;
+  bool ipup = false, jcur = false, have_p = false;
+  double hl0_p = 0.0;  // h*l0 when P was formed
+  std::uint64_t nst = 0, nslp = 0, attempts = 0;
+  const double* el = CO.elco[meth][nq];
+  auto maxord = [&]() { return meth == 0 ? kLsodaMaxOrdAdams : kLsodaMaxOrdBdf; };
+  auto set_order = [&](int m, int q) { meth = m; nq = q; el = CO.elco[meth][nq]; };
+  auto rescale = [&](double rh) {
+    double r = rh;
+    for (int j = 1; j <= nq; ++j) {
+      double* zj = Zr(j);
+      for (int i = 0; i < n; ++i) zj[i] *= r;
+      r *= rh;
+    }
+    h *= rh;
+    if constexpr (C) w->flops += static_cast<std::uint64_t>(nq) * (n + 1);
+  };
+  auto predict = [&]() {
+    for (int k = 0; k < nq; ++k)
+      for (int j = nq - 1; j >= k; --j) {
+        double* a0 = Zr(j);
+        const double* a1 = Zr(j + 1);
+        for (int i = 0; i < n; ++i) a0[i] += a1[i];
+      }
+    if constexpr (C) w->flops += static_cast<std::uint64_t>(nq) * (nq + 1) / 2 * n;
+  };
+  auto unpredict = [&]() {
+    for (int k = nq - 1; k >= 0; --k)
+      for (int j = k; j <= nq - 1; ++j) {
+        double* a0 = Zr(j);
+        const double* a1 = Zr(j + 1);
+        for (int i = 0; i < n; ++i) a0[i] -= a1[i];
+      }
+  };
+  auto form_p = [&](const double* yy) {
+    rre_jacobian<C>(net, rates, yy, P, w);
+    const double hl0 = h * el[0];
+    for (int q = 0; q < n * n; ++q) P[q] = -hl0 * P[q];
+    for (int i = 0; i < n; ++i) P[i * n + i] += 1.0;
+    hl0_p = hl0;
+    have_p = lu_factor<C>(P, n, piv, w);
+    return have_p;
+  };
+  // weighted max-row-sum norm of J at yy (LSODA fnorm with weights 1/ewt)
+  auto jac_norm = [&](const double* yy) {
+    rre_jacobian<C>(net, rates, yy, sc.jac2.data(), w);
+    const double* J = sc.jac2.data();
+    double nm = 0.0;
+    for (int i = 0; i < n; ++i) {
+      double sr = 0.0;
+      for (int j = 0; j < n; ++j) sr += std::fabs(J[i * n + j]) * ewt[j];
+      nm = std::max(nm, sr / ewt[i]);
+    }
+    if constexpr (C) w->flops += 2 * static_cast<std::uint64_t>(n) * n + n;
+    return nm;
+  };
+  auto sm1 = [](int q) { return kLsodaSm1[q]; };
+  auto cm1 = [&](int q) { return CO.tesco[0][q][1] * CO.elco[0][q][q]; };
+  auto cm2 = [&](int q) { return CO.tesco[1][q][1] * CO.elco[1][q][q]; };
+
+  int kflag = 0;
+  int ncf = 0;
+  while (t < t_end) {
+    // ---- one accepted step (stode) ----
+    for (int i = 0; i < n; ++i) ewt[i] = rtol * std::fabs(Zr(0)[i]) + atol;
+    kflag = 0;
+    ncf = 0;
+    double dsm = 0.0;
+    for (;;) {
+      if (attempts++ >= cfg.max_steps) return KIN_SIM_BUDGET;
+      if (!(h > 0.0) || t + h == t) return KIN_SIM_STEP_UNDERFLOW;
+      if (meth == 1 && (!have_p || std::fabs(h * el[0] / hl0_p - 1.0) > 0.3 || nst >= nslp + 20)) ipup = true;
+      const double tn = t + h;
+      predict();
+      bool conv = false;
+      for (;;) {  // corrector (re-entered once with a fresh Jacobian)
+        for (int i = 0; i < n; ++i) y[i] = Zr(0)[i];
+        rhs(y, savf);
+        if (meth == 1 && ipup) {
+          if (!form_p(y)) return KIN_SIM_NONFINITE;
+          ipup = false;
+          jcur = true;
+          crate = 0.7;
+          nslp = nst;
+        }
+        for (int i = 0; i < n; ++i) acor[i] = 0.0;
+        double delp = 0.0;
+        int m = 0;
+        for (;;) {
+          double del;
+          if (meth == 1) {
+            for (int i = 0; i < n; ++i) tmp[i] = h * savf[i] - (Zr(1)[i] + acor[i]);
+            lu_solve<C>(P, n, piv, tmp, w);
+            del = wrms(tmp);
+            for (int i = 0; i < n; ++i) { acor[i] += tmp[i]; y[i] = Zr(0)[i] + el[0] * acor[i]; }
+          } else {
+            for (int i = 0; i < n; ++i) tmp[i] = h * savf[i] - Zr(1)[i];
+            for (int i = 0; i < n; ++i) acor[i] = tmp[i] - acor[i];
+            del = wrms(acor);
+            for (int i = 0; i < n; ++i) { y[i] = Zr(0)[i] + el[0] * tmp[i]; acor[i] = tmp[i]; }
+          }
+          if constexpr (C) w->flops += 5 * static_cast<std::uint64_t>(n);
+          if (!std::isfinite(del)) { conv = false; break; }
+          if (m != 0) crate = std::max(0.2 * crate, del / delp);
+          const double conit = 0.5 / (nq + 2);
+          const double dcon = del * std::min(1.0, 1.5 * crate) / (CO.tesco[meth][nq][1] * conit);
+          if (dcon <= 1.0) { conv = true; break; }
+          ++m;
+          if (m == 3 || (m >= 2 && del > 2.0 * delp)) break;
+          delp = del;
+          rhs(y, savf);
+        }
+        if (conv) break;
+        if (meth == 1 && !jcur) { ipup = true; continue; }
+        break;
+      }
+      if (!conv) {
+        unpredict();
+        ++meta[1];
+        if (++ncf >= 10) return KIN_SIM_STEP_UNDERFLOW;
+        rescale(0.25);
+        if (meth == 1) ipup = true;
+        continue;
+      }
+      jcur = false;
+      dsm = wrms(acor) / CO.tesco[meth][nq][1];
+      if (dsm > 1.0) {
+        unpredict();
+        ++meta[1];
+        --kflag;
+        if (kflag <= -3) {
+          // repeated error-test failures: restart at order 1 with h/10
+          for (int i = 0; i < n; ++i) y[i] = Zr(0)[i];
+          h *= 0.1;
+          rhs(y, savf);
+          for (int i = 0; i < n; ++i) Zr(1)[i] = h * savf[i];
+          set_order(meth, 1);
+          ialth = 5;
+          if (meth == 1) ipup = true;
+          continue;
+        }
+        const double rhsm = 1.0 / (1.2 * pm_pow(dsm, 1.0 / (nq + 1)) + 1.2e-6);
+        double rhdn = 0.0;
+        if (nq > 1) {
+          const double ddn = wrms(Zr(nq)) / CO.tesco[meth][nq][0];
+          rhdn = 1.0 / (1.3 * pm_pow(ddn, 1.0 / nq) + 1.3e-6);
+        }
+        double rh;
+        if (rhsm >= rhdn) {
+          rh = rhsm;
+        } else {
+          rh = rhdn;
+          set_order(meth, nq - 1);
+        }
+        rh = std::min(rh, 1.0);
+        if (kflag <= -2) rh = std::min(rh, 0.2);
+        rescale(rh);
+        if (meth == 1) ipup = true;
+        ialth = nq + 1;
+        continue;
+      }
+      // ---- accepted ----
+      ++nst;
+      ++meta[0];
+      for (int j = 0; j <= nq; ++j) {
+        double* zj = Zr(j);
+        const double e = el[j];
+        for (int i = 0; i < n; ++i) zj[i] += e * acor[i];
+      }
+      if constexpr (C) w->flops += 2 * static_cast<std::uint64_t>(nq + 1) * n;
+      const double tprev = t;
+      t = tn;
+      while (gi < n_grid && grid[gi] <= t && grid[gi] > tprev) {
+        const double s = (grid[gi] - t) / h;
+        for (int i = 0; i < n; ++i) {
+          double v = Zr(nq)[i];
+          for (int j = nq - 1; j >= 0; --j) v = Zr(j)[i] + s * v;
+          tmp[i] = v;
+        }
+        if constexpr (C) w->flops += 2 * static_cast<std::uint64_t>(nq) * n + 2;
+        emit(gi++, tmp);
+      }
+      break;
+    }
+    // ---- order / step / method selection ----
+    --ialth;
+    if (ialth == 0) {
+      const double rhsm = 1.0 / (1.2 * pm_pow(dsm, 1.0 / (nq + 1)) + 1.2e-6);
+      double rhsm_cap;
+      double rhup = 0.0;
+      if (nq < maxord()) {
+        const double* sv = Zr(kLsodaL - 1);
+        for (int i = 0; i < n; ++i) tmp[i] = acor[i] - sv[i];
+        const double dup = wrms(tmp) / CO.tesco[meth][nq][2];
+        rhup = 1.0 / (1.4 * pm_pow(dup, 1.0 / (nq + 2)) + 1.4e-6);
+      }
+      double rhdn = 0.0;
+      if (nq > 1) {
+        const double ddn = wrms(Zr(nq)) / CO.tesco[meth][nq][0];
+        rhdn = 1.0 / (1.3 * pm_pow(ddn, 1.0 / nq) + 1.3e-6);
+      }
+      // Adams steps are also capped by the stability region (LSODA sm1):
+      // h*||J|| <= sm1(order) for the order each candidate would use.
+      double pdnorm = -1.0;
+      if (meth == 0) {
+        pdnorm = jac_norm(Zr(0));
+        const double pdh = std::max(h * pdnorm, 1.0e-6);
+        if (nq < kLsodaMaxOrdAdams) rhup = std::min(rhup, sm1(nq + 1) / pdh);
+        rhsm_cap = std::min(rhsm, sm1(nq) / pdh);
+        if (nq > 1) rhdn = std::min(rhdn, sm1(nq - 1) / pdh);
+      } else {
+        rhsm_cap = rhsm;
+      }
+      int newq = nq;
+      double rh = rhsm_cap;
+      if (rhsm_cap >= rhup) {
+        if (rhsm_cap < rhdn) { newq = nq - 1; rh = rhdn; }
+      } else if (rhup > rhdn) {
+        newq = nq + 1;
+        rh = rhup;
+      } else {
+        newq = nq - 1;
+        rh = rhdn;
+      }
+      // LSODA stiffness switch (Petzold): compare the step each method could take
+      int newm = meth;
+      if (icount > 0) {
+        --icount;
+      } else {
+        if (pdnorm < 0.0) pdnorm = jac_norm(Zr(0));
+        const double exsm = 1.0 / (nq + 1);
+        if (meth == 0 && nq <= kLsodaMaxOrdBdf) {
+          // Adams -> BDF when BDF could step ratio*5 farther than the
+          // (stability-capped) Adams choice
+          const double rh1 = rh;
+          const double dm2 = dsm * (cm1(nq) / cm2(nq));
+          const double rh2 = 1.0 / (1.2 * pm_pow(dm2, exsm) + 1.2e-6);
+          if (rh2 >= 5.0 * rh1) { newm = 1; newq = nq; rh = rh2; }
+        } else if (meth == 1) {
+          const double dm1 = dsm * (cm2(nq) / cm1(nq));
+          double rh1 = 1.0 / (1.2 * pm_pow(dm1, exsm) + 1.2e-6);
+          double rh1it = 2.0 * rh1;
+          const double pdh = pdnorm * h;
+          if (pdh * rh1 > 1e-5) rh1it = sm1(nq) / pdh;
+          rh1 = std::min(rh1, rh1it);
+          const double rh2 = rh;
+          if (rh1 >= rh2) { newm = 0; newq = nq; rh = rh1; }
+        }
+        if (newm != meth) icount = 20;
+        else icount = 0;
+      }
+      if (newm == meth && newq == nq && rh < 1.1) {
+        ialth = 3;
+      } else {
+        if (newq == nq + 1) {
+          const double r = el[nq] / (nq + 1);
+          double* zq = Zr(newq);
+          for (int i = 0; i < n; ++i) zq[i] = acor[i] * r;
+        }
+        rh = std::min(rh, rmax);
+        rh = rh / std::max(1.0, h * rh / hmax);
+        if (newm != meth || newq != nq) set_order(newm, newq);
+        rescale(rh);
+        ialth = nq + 1;
+        if (meth == 1) ipup = true;
+      }
+      rmax = 10.0;
+    } else if (ialth == 1 && nq < maxord()) {
+      double* sv = Zr(kLsodaL - 1);
+      for (int i = 0; i < n; ++i) sv[i] = acor[i];
+    }
+  }
+  while (gi < n_grid) emit(gi++, Zr(0));
+  meta[5] = floored ? 1 : 0;
+  return KIN_SIM_OK;
 }
 
 // ---- sweep decoding (ensemble.hpp:101-130) ----------------------------------

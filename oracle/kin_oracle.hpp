@@ -65,6 +65,8 @@ struct Scratch {
   std::vector<std::uint64_t> k;
   // Dopri5 / LSODA
   std::vector<double> v[24];
+  std::vector<double> z, jac, jac2;
+  std::vector<int> piv;
   void resize(int n, int m);
 };
 

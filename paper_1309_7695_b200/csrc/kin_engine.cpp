@@ -169,7 +169,6 @@ int validate_sweep(const HostModel& net, const kin_sweep_desc* d, const Layout& 
     *msg = "method not provided by this engine (CLE/hybrid are out of scope)";
     return KIN_ERR_INPUT;
   }
-  if (M.kind == KIN_METHOD_LSODA) { *msg = "LSODA not built"; return KIN_ERR_INPUT; }
   if (M.kind < 0 || M.kind > KIN_METHOD_LSODA) { *msg = "unknown method kind"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_TAU_FIXED && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_TAU_ADAPTIVE && !(M.epsilon > 0.0 && M.epsilon < 1.0)) { *msg = "epsilon must be in (0,1)"; return KIN_ERR_INPUT; }
@@ -321,6 +320,65 @@ int pack_tables(const HostModel& H, const kin_sweep_desc* d, KinTables* T, std::
   return KIN_OK;
 }
 
+// ---- LSODA coefficients (cfode; same recurrences as oracle/kin_lsoda.hpp) ------
+void lsoda_coeffs(std::vector<double>* out) {
+  double elco[2][13][14] = {};
+  double tesco[2][13][3] = {};
+  {
+    double pc[13];
+    elco[0][1][0] = 1.0;
+    elco[0][1][1] = 1.0;
+    tesco[0][1][0] = 0.0;
+    tesco[0][1][1] = 2.0;
+    tesco[0][2][0] = 1.0;
+    tesco[0][12][2] = 0.0;
+    pc[0] = 1.0;
+    double rqfac = 1.0;
+    for (int nq = 2; nq <= 12; ++nq) {
+      const double rq1fac = rqfac;
+      rqfac = rqfac / nq;
+      const int nqm1 = nq - 1;
+      const double fnqm1 = nqm1;
+      pc[nq - 1] = 0.0;
+      for (int i = nq - 1; i >= 1; --i) pc[i] = pc[i - 1] + fnqm1 * pc[i];
+      pc[0] = fnqm1 * pc[0];
+      double pint = pc[0], xpin = pc[0] / 2.0, tsign = 1.0;
+      for (int i = 1; i < nq; ++i) {
+        tsign = -tsign;
+        pint += tsign * pc[i] / (i + 1);
+        xpin += tsign * pc[i] / (i + 2);
+      }
+      elco[0][nq][0] = pint * rq1fac;
+      elco[0][nq][1] = 1.0;
+      for (int i = 1; i < nq; ++i) elco[0][nq][i + 1] = rq1fac * pc[i] / (i + 1);
+      const double agamq = rqfac * xpin;
+      const double ragq = 1.0 / agamq;
+      tesco[0][nq][1] = ragq;
+      if (nq < 12) tesco[0][nq + 1][0] = ragq * rqfac / (nq + 1);
+      tesco[0][nq - 1][2] = ragq;
+    }
+  }
+  {
+    double pc[7];
+    pc[0] = 1.0;
+    double rq1fac = 1.0;
+    for (int nq = 1; nq <= 5; ++nq) {
+      const double fnq = nq;
+      pc[nq] = 0.0;
+      for (int i = nq; i >= 1; --i) pc[i] = pc[i - 1] + fnq * pc[i];
+      pc[0] = fnq * pc[0];
+      for (int i = 0; i <= nq; ++i) elco[1][nq][i] = pc[i] / pc[1];
+      elco[1][nq][1] = 1.0;
+      tesco[1][nq][0] = rq1fac;
+      tesco[1][nq][1] = (nq + 1) / elco[1][nq][0];
+      tesco[1][nq][2] = (nq + 2) / elco[1][nq][0];
+      rq1fac = rq1fac / fnq;
+    }
+  }
+  out->assign(&elco[0][0][0], &elco[0][0][0] + 2 * 13 * 14);
+  out->insert(out->end(), &tesco[0][0][0], &tesco[0][0][0] + 2 * 13 * 3);
+}
+
 // ---- device slots -------------------------------------------------------------
 template <class T>
 struct DevBuf {
@@ -349,6 +407,7 @@ struct Slot {
   DevBuf<uint64_t> meta, work;
   DevBuf<unsigned long long> counter;
   DevBuf<double> lgamma_tab;  // glibc lgamma(k+1), k < KIN_LGAMMA_N
+  DevBuf<double> lsoda_co;    // cfode elco/tesco
   DevBuf<int32_t> status;
   void* stage = nullptr;
   size_t stage_cap = 0;
@@ -491,6 +550,13 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
   const int kind = d->method.kind;
   if (kind == KIN_METHOD_ODE) {
     e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
+  } else if (kind == KIN_METHOD_LSODA) {
+    KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
+    if (kin::lsoda_smem_bytes(*T, SD) > 227 * 1024) {
+      set_err(err, KIN_ERR_INPUT, "model too large for the LSODA kernel (per-simulation state exceeds shared memory)");
+      return KIN_ERR_INPUT;
+    }
+    e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, sl.counter.p, sl.stream);
   } else {
     KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
     e = kin::launch_stochastic(*T, SD, O, want_work, 32, sl.counter.p, sl.stream);
@@ -611,6 +677,10 @@ int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err)
     for (int k = 0; k < KIN_LGAMMA_N; ++k) lg[k] = std::lgamma(static_cast<double>(k) + 1.0);
     KIN_CUDA(sl->lgamma_tab.ensure(KIN_LGAMMA_N), "cudaMalloc lgamma table");
     KIN_CUDA(cudaMemcpy(sl->lgamma_tab.p, lg.data(), sizeof(double) * KIN_LGAMMA_N, cudaMemcpyHostToDevice), "H2D lgamma");
+    std::vector<double> co;
+    lsoda_coeffs(&co);
+    KIN_CUDA(sl->lsoda_co.ensure(co.size()), "cudaMalloc lsoda coefficients");
+    KIN_CUDA(cudaMemcpy(sl->lsoda_co.p, co.data(), sizeof(double) * co.size(), cudaMemcpyHostToDevice), "H2D lsoda");
     ctx->slots.push_back(std::move(sl));
   }
   *out = ctx.release();
@@ -623,7 +693,7 @@ void kin_ctx_destroy(kin_ctx* ctx) {
     cudaSetDevice(sl->device);
     cudaStreamSynchronize(sl->stream);
     sl->traj.release(); sl->traj_t.release(); sl->mean.release(); sl->m2.release();
-    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->lgamma_tab.release(); sl->status.release();
+    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->lgamma_tab.release(); sl->lsoda_co.release(); sl->status.release();
     if (sl->stage) cudaFreeHost(sl->stage);
     for (auto& e : sl->ev) if (e) cudaEventDestroy(e);
     for (auto& e : sl->tev) if (e) cudaEventDestroy(e);

@@ -20,6 +20,12 @@ int ode_pick_lanes(int n_species);
 cudaError_t launch_dopri5(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, int lanes,
                           cudaStream_t stream);
 
+// kin_lsoda.cu: LSODA-style Adams/BDF, thread per simulation, state in smem.
+// coeffs: elco [2][13][14] then tesco [2][13][3] (device).
+size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S);
+cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, const double* coeffs,
+                         unsigned long long* counter, cudaStream_t stream);
+
 // kin_post.cu: layout kernels and utilities.
 // traj_dev [G*N][n_local] (simulation-fastest) -> dst [n_local][G*N]
 cudaError_t launch_transpose_traj(const double* traj_dev, double* dst, uint64_t n_local, int gn, cudaStream_t stream);

@@ -54,6 +54,14 @@ def isomerization(a0=50, b0=50, kf=1.0, kb=2.0):
                 [("fwd", {"A": 1}, {"B": 1}, "kf"), ("bwd", {"B": 1}, {"A": 1}, "kb")])
 
 
+def robertson(omega=1e6):
+    """Robertson's stiff chemical kinetics (A->B, 2B->B+C, B+C->A+C) in molecule
+    counts with volume omega (stiffness test for the LSODA extension)."""
+    return _net([("A", int(omega)), ("B", 0), ("C", 0)], [("k1", 0.04), ("k2", 2 * 3e7 / omega), ("k3", 1e4 / omega)],
+                [("r1", {"A": 1}, {"B": 1}, "k1"), ("r2", {"B": 2}, {"B": 1, "C": 1}, "k2"),
+                 ("r3", {"B": 1, "C": 1}, {"A": 1, "C": 1}, "k3")])
+
+
 # ---- C1 Michaelis-Menten (Wilkinson) ----------------------------------------
 def michaelis_menten():
     return _net([("S", 301), ("E", 120), ("ES", 0), ("P", 0)],
@@ -103,7 +111,7 @@ def brusselator(omega=1000.0, A=1.0, B=3.0, stiff=1.0):
                  ("outflow", {"X": 1}, {"E": 1}, "kE")], max_order=3)
 
 
-def c3_config(side=256, method: MethodKind = MethodKind.Ode, omega=1000.0, stiff=1.0):
+def c3_config(side=256, method: MethodKind = MethodKind.Lsoda, omega=1000.0, stiff=1.0):
     net = brusselator(omega, stiff=stiff)
     vals = [float(round(v)) for v in np.linspace(0.0, 5.0 * omega, side)]
     cfg = SweepConfig(axes=[SweepAxis("X", vals, "initial"), SweepAxis("Y", vals, "initial")], runs_per_point=1,

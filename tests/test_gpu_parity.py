@@ -198,7 +198,7 @@ def test_c1_ode_tolerance(engine, oracle):
 
 
 def test_c3_brusselator_ode_tolerance(engine, oracle):
-    net, cfg = W.c3_config(side=256)
+    net, cfg = W.c3_config(side=256, method=MethodKind.Ode)
     ref, got = both(engine, oracle, net, cfg, sim_range=(0, 512))
     err = np.abs(got["traj"] - ref["traj"]) / ode_bound(ref["traj"], cfg)
     assert err.max() <= 1.0, err.max()
@@ -210,6 +210,29 @@ def test_c4_ode_tolerance(engine, oracle, rng):
     ref, got = both(engine, oracle, net, cfg, sim_range=rng)
     err = np.abs(got["traj"] - ref["traj"]) / ode_bound(ref["traj"], cfg)
     assert err.max() <= 1.0, err.max()
+
+
+# ---- LSODA-style Adams/BDF: bit-exact (only correctly rounded IEEE ops) ---------
+@pytest.mark.parametrize("rng", [(0, 512), (30000, 30256), (65536 - 256, 65536)])
+def test_c3_brusselator_lsoda_bit_exact(engine, oracle, rng):
+    net, cfg = W.c3_config(side=256)
+    ref, got = both(engine, oracle, net, cfg, sim_range=rng)
+    assert_bit_exact(ref, got)
+
+
+def test_robertson_lsoda_bit_exact(engine, oracle):
+    g = np.concatenate([[0.0], np.logspace(-4, 4, 33)])
+    ic = IntegratorConfig(rel_tol=1e-6, abs_tol=1e-6, max_steps=200000)
+    cfg = SweepConfig([SweepAxis("k3", [1e-3, 1e-2, 1e-1])], 1, Method(MethodKind.Lsoda, integrator=ic), 0, 1e4, g)
+    ref, got = both(engine, oracle, W.robertson(1e6), cfg)
+    assert_bit_exact(ref, got)
+    assert got["meta"][:, 0].max() < 2000
+
+
+def test_c1_lsoda_bit_exact(engine, oracle):
+    net, cfg = W.c1_config(MethodKind.Lsoda)
+    ref, got = both(engine, oracle, net, cfg)
+    assert_bit_exact(ref, got)
 
 
 # ---- reference-signature API --------------------------------------------------

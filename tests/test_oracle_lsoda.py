@@ -1,0 +1,66 @@
+"""The oracle's LSODA-style integrator (north-star extension; no reference
+implementation exists): analytic solutions, a stiff problem where it must
+switch to BDF, and accuracy parity with scipy's LSODA on the Brusselator."""
+import numpy as np
+import pytest
+from scipy.integrate import solve_ivp
+
+from oracle import oracle as O
+from paper_1309_7695_b200 import workloads as W
+from paper_1309_7695_b200.ensemble import IntegratorConfig, Method, MethodKind, SweepAxis, SweepConfig, make_sweep_desc, uniform_grid
+
+LS = MethodKind.Lsoda
+
+
+def run(net, cfg, rng=None):
+    d, keep = make_sweep_desc(net, cfg, sim_range=rng)
+    return O.sweep(net, d, workers=4, raise_on_error=False)
+
+
+def test_decay_and_birth_death_analytic():
+    r = run(W.decay(), SweepConfig([SweepAxis("c", [0.5, 1.0, 2.0])], 1, Method(LS), 0, 1.0, [0.0, 0.5, 1.0]))
+    assert r["rc"] == 0
+    ex = 100 * np.exp(-np.array([0.5, 1, 2])[:, None] * np.array([0, .5, 1])[None, :])
+    assert np.max(np.abs(r["traj"][:, :, 0] - ex) / ex) < 2e-5
+    g = uniform_grid(3.0, 31)
+    r = run(W.birth_death(), SweepConfig([], 1, Method(LS), 0, 3.0, g))
+    assert np.max(np.abs(r["traj"][0, 1:, 0] - 5 * (1 - np.exp(-g[1:])))) < 1e-4
+
+
+def robertson_rhs(omega):
+    def f(t, x):
+        a = np.array([0.04 * x[0], 2 * 3e7 / omega * max(x[1] * (x[1] - 1) / 2, 0.0), 1e4 / omega * x[1] * x[2]])
+        return np.array([-a[0] + a[2], a[0] - a[1] - a[2], a[1]])
+    return f
+
+
+def test_robertson_stiff_switches_to_bdf():
+    om = 1e6
+    g = np.concatenate([[0.0], np.logspace(-4, 4, 33)])
+    ic = IntegratorConfig(rel_tol=1e-6, abs_tol=1e-6, max_steps=200000)
+    r = run(W.robertson(om), SweepConfig([], 1, Method(LS, integrator=ic), 0, 1e4, g))
+    assert r["rc"] == 0 and r["meta"][0, 0] < 2000  # a non-stiff method needs >1e5 steps
+    ref = solve_ivp(robertson_rhs(om), (0, 1e4), [om, 0, 0], method="Radau", rtol=1e-12, atol=1e-10, t_eval=g).y.T
+    err = np.abs(r["traj"][0] - ref) / (1e-6 * np.abs(ref) + 1e-6)
+    assert err.max() < 50
+    # Dopri5 on the same problem exhausts the step budget (stiffness)
+    rd = run(W.robertson(om), SweepConfig([], 1, Method(MethodKind.Ode, integrator=IntegratorConfig(max_steps=20000)), 0, 1e4, g))
+    assert rd["rc"] == 2
+
+
+@pytest.mark.parametrize("sim", [5, 2000, 40000, 65000])
+def test_brusselator_accuracy_like_scipy_lsoda(sim):
+    net, cfg = W.c3_config()
+    r = run(net, cfg, (sim, sim + 1))
+    x0 = r["traj"][0, 0]
+
+    def fb(t, x):
+        a = np.array([1000.0, 2e-6 * max(x[0] * (x[0] - 1) / 2, 0.0) * x[1], 3.0 * x[0], 1.0 * x[0]])
+        return np.array([a[0] + a[1] - a[2] - a[3], a[2] - a[1], a[2], a[3]])
+
+    ref = solve_ivp(fb, (0, 20), x0, method="DOP853", rtol=1e-12, atol=1e-9, t_eval=cfg.grid).y.T
+    sp = solve_ivp(fb, (0, 20), x0, method="LSODA", rtol=1e-6, atol=1e-6, t_eval=cfg.grid).y.T
+    tol = 1e-6 * np.abs(ref) + 1e-6
+    ours = np.max(np.abs(r["traj"][0] - ref) / tol)
+    theirs = np.max(np.abs(sp - ref) / tol)
+    assert ours < max(3 * theirs, 50), (ours, theirs)

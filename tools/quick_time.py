@@ -16,7 +16,8 @@ cfgs = {
     "c4_ode": W.c4_config(method=MethodKind.Ode),
     "c1_tau": W.c1_config(),
     "c2": W.c2_config(),
-    "c3_ode": W.c3_config(),
+    "c3_ode": W.c3_config(method=MethodKind.Ode),
+    "c3_lsoda": W.c3_config(),
     "c5_tau": W.c5_config(),
 }
 names = sys.argv[1:] or list(cfgs)
