@@ -216,10 +216,11 @@ def bench_ours(args, world, rank, local):
     from paper_1309_7695_b200 import abi
     from paper_1309_7695_b200.ensemble import Engine, make_sweep_desc
 
+    from paper_1309_7695_b200 import shard
     n = world
     net, tau_cfg, ode_cfg = workload(n)
     per = SIDE * SIDE
-    rng = (rank * per, (rank + 1) * per)
+    rng = shard.rank_range(per * n, 1, rank, n)  # whole points, rank-contiguous
     eng = Engine([local])
     lib = eng.lib
     h = eng.model(net)

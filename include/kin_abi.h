@@ -189,6 +189,14 @@ int kin_sweep_size(const kin_sweep_desc* desc, uint64_t* n_points,
 int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc,
                   kin_sweep_out* out, kin_error* err);
 
+/* The chunk plan kin_sweep_run uses for n_devices GPUs over simulations
+   [s0, s1) with R runs per point: n_chunks = (n_devices == 1 ? 1 : min(#points,
+   4*n_devices)) whole-point chunks (boundaries snapped to multiples of R),
+   chunk c -> device c % n_devices.  bounds receives n_chunks+1 entries
+   (capacity max_chunks+1).  Pure host function (no device needed). */
+int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t runs_per_point, int32_t n_devices,
+                   int32_t max_chunks, uint64_t* bounds, int32_t* n_chunks, kin_error* err);
+
 /* ---- device-resident form (benchmarks, chained consumers) -----------------
    Runs the sweep on device `device_slot` of the context into context-owned
    device buffers, on the context's stream, WITHOUT any host copies.  The

@@ -127,6 +127,13 @@ __device__ __forceinline__ double div_small(double mean, int k) {
 
 // draw_poisson (rng.cpp:68-109): inversion below mean 10, Hormann PTRS above.
 // `flops` receives the algorithmic op count (same accounting as the oracle).
+// correctly rounded float reciprocals 1/k, k = 1..40 (index 0 unused)
+__device__ __constant__ float c_rcp40[41] = {
+    0.0f, 1.0f / 1, 1.0f / 2, 1.0f / 3, 1.0f / 4, 1.0f / 5, 1.0f / 6, 1.0f / 7, 1.0f / 8, 1.0f / 9, 1.0f / 10,
+    1.0f / 11, 1.0f / 12, 1.0f / 13, 1.0f / 14, 1.0f / 15, 1.0f / 16, 1.0f / 17, 1.0f / 18, 1.0f / 19, 1.0f / 20,
+    1.0f / 21, 1.0f / 22, 1.0f / 23, 1.0f / 24, 1.0f / 25, 1.0f / 26, 1.0f / 27, 1.0f / 28, 1.0f / 29, 1.0f / 30,
+    1.0f / 31, 1.0f / 32, 1.0f / 33, 1.0f / 34, 1.0f / 35, 1.0f / 36, 1.0f / 37, 1.0f / 38, 1.0f / 39, 1.0f / 40};
+
 // lgamma(k+1), k < KIN_LGAMMA_N, computed by the host's glibc (the oracle's libm)
 // and uploaded once per context (see kin_engine.cpp).
 #define KIN_LGAMMA_N 4096
@@ -136,26 +143,30 @@ __device__ __forceinline__ uint64_t poisson(Xoshiro& rng, double mean, uint64_t&
   if (mean < 10.0) {
     const double u = rng.uniform();
     // Fast decision path (returns exactly the k of the reference algorithm):
-    // search an approximate CDF c'_k built from the FP32 exponential.  With
-    // mean in (0,10), __expf errs by <= 13 float ulp (1.55e-6) and the
-    // float rounding of mean adds <= 6e-7; the double recursion with a float
-    // reciprocal adds <= k*6.1e-8.  So |c'_k - c_k| <= (2.2e-6 + k*6.1e-8) c_k
-    // for the reference's own c_k (itself within (k+2)*2^-52 of the exact
-    // value).  If u clears c'_{k-1} and c'_k by the guard G = 2e-5 (k <= 40:
-    // error <= 4.7e-6 < G/4), the reference stops at the same k.  Otherwise
-    // (probability ~4e-5 per draw) run the exact algorithm.
+    // search an approximate CDF c'_k in FP32.  Error budget relative to the
+    // reference's c_k (whose own rounding, (k+2)*2^-52, is negligible):
+    //   p'_0 = __expf(-float(mean)): <= 13 float ulp (1.55e-6) + mean*2^-24
+    //          (<= 6e-7) = 2.15e-6 for mean in (0,10);
+    //   each recursion step p' *= float(mean)*rcp(k): 4 roundings, <= 2.4e-7;
+    //   each cumulative add: <= 6e-8;  float(u): <= 6e-8.
+    // So |c'_k - c_k| <= (2.15e-6 + 3e-7*k) c_k <= 1.42e-5 c_k for k <= 40, and a
+    // guard G = 4e-5 (> 2x that) makes "u < c'_k(1-G) and u > c'_{k-1}(1+G)"
+    // imply the reference stops at exactly k.  Otherwise (probability ~1e-4 per
+    // draw) run the exact algorithm below.
     {
-      constexpr double G = 2e-5;
-      double pf = static_cast<double>(__expf(-static_cast<float>(mean)));
-      double cf = pf, cprev = 0.0;
+      constexpr float G = 4e-5f;
+      const float uf = static_cast<float>(u);
+      const float mf = static_cast<float>(mean);
+      float pf = __expf(-mf);
+      float cf = pf, cprev = 0.0f;
       int kk = 0;
-      while (u > cf * (1.0 + G) && kk < 40) {
+      while (uf > cf * (1.0f + G) && kk < 40) {
         ++kk;
-        pf = pf * (mean * static_cast<double>(__frcp_rn(static_cast<float>(kk))));
+        pf = pf * (mf * c_rcp40[kk]);
         cprev = cf;
         cf = cf + pf;
       }
-      if (kk < 40 && u < cf * (1.0 - G) && (kk == 0 || u > cprev * (1.0 + G))) {
+      if (kk < 40 && uf < cf * (1.0f - G) && (kk == 0 || uf > cprev * (1.0f + G))) {
         if (kCount) flops += 3 + 3 * static_cast<uint64_t>(kk);
         return static_cast<uint64_t>(kk);
       }

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -559,7 +560,7 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
     e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, sl.counter.p, sl.stream);
   } else {
     KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
-    e = kin::launch_stochastic(*T, SD, O, want_work, 32, sl.counter.p, sl.stream);
+    e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.stream);
   }
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
   KIN_CUDA(cudaEventRecord(sl.tev[1], sl.stream), "event");
@@ -617,6 +618,23 @@ int fetch_range(Slot& sl, kin_sweep_out* out, uint64_t base_sim, uint64_t base_p
   }
   KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
   return KIN_OK;
+}
+
+// Chunk plan of kin_sweep_run (see kin_abi.h kin_sweep_plan).
+std::vector<uint64_t> plan_chunks(uint64_t s0, uint64_t s1, uint64_t R, int D) {
+  const uint64_t S = s1 - s0;
+  const uint64_t n_chunks =
+      D <= 1 ? 1 : std::min<uint64_t>(std::max<uint64_t>(S / std::max<uint64_t>(R, 1), 1), 4 * static_cast<uint64_t>(D));
+  std::vector<uint64_t> bounds;
+  bounds.push_back(s0);
+  for (uint64_t c = 1; c < n_chunks; ++c) {
+    uint64_t b = s0 + S * c / n_chunks;
+    b = (b + R - 1) / R * R;  // snap to a point boundary
+    b = std::min(std::max(b, bounds.back()), s1);
+    bounds.push_back(b);
+  }
+  bounds.push_back(s1);
+  return bounds;
 }
 
 int prepare(const kin_model* model, const kin_sweep_desc* desc, Layout* L, uint64_t* s0, uint64_t* s1,
@@ -745,16 +763,8 @@ int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* de
   const uint64_t base_point = (s0 + L.R - 1) / L.R;
   // whole-point chunks, cyclic over devices
   const int D = static_cast<int>(ctx->slots.size());
-  const uint64_t n_chunks = D == 1 ? 1 : std::min<uint64_t>(std::max<uint64_t>(S / std::max<uint64_t>(L.R, 1), 1), 4 * static_cast<uint64_t>(D));
-  std::vector<uint64_t> bounds;
-  bounds.push_back(s0);
-  for (uint64_t c = 1; c < n_chunks; ++c) {
-    uint64_t b = s0 + S * c / n_chunks;
-    b = (b + L.R - 1) / L.R * L.R;  // snap to a point boundary
-    b = std::min(std::max(b, bounds.back()), s1);
-    bounds.push_back(b);
-  }
-  bounds.push_back(s1);
+  const std::vector<uint64_t> bounds = plan_chunks(s0, s1, L.R, D);
+  const uint64_t n_chunks = bounds.size() - 1;
   std::vector<int32_t> status_local;
   int32_t* status = out->status;
   if (!status) {
@@ -804,6 +814,17 @@ int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* de
       return KIN_ERR_SIMULATION;
     }
   }
+  return KIN_OK;
+}
+
+int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t R, int32_t D, int32_t max_chunks, uint64_t* bounds,
+                   int32_t* n_chunks, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (s1 < s0 || R == 0 || D < 1 || !bounds || !n_chunks) { set_err(err, KIN_ERR_USAGE, "bad argument"); return KIN_ERR_USAGE; }
+  const std::vector<uint64_t> b = plan_chunks(s0, s1, R, D);
+  if (static_cast<int64_t>(b.size()) - 1 > max_chunks) { set_err(err, KIN_ERR_USAGE, "max_chunks too small"); return KIN_ERR_USAGE; }
+  for (size_t i = 0; i < b.size(); ++i) bounds[i] = b[i];
+  *n_chunks = static_cast<int32_t>(b.size() - 1);
   return KIN_OK;
 }
 

@@ -13,7 +13,7 @@ namespace kin {
 size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block);
 // `counter` is a device word used by the persistent warps to fetch work.
 cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
-                              int block, unsigned long long* counter, cudaStream_t stream);
+                              unsigned long long* counter, cudaStream_t stream);
 
 // kin_ode.cu: Dopri5 RRE integration, L lanes per simulation (L = 0 picks).
 int ode_pick_lanes(int n_species);

@@ -55,6 +55,9 @@ struct Sim {
     }
     return aj;
   }
+  // a_j as evaluated at the start of the decision (leaps update x in place,
+  // so the propensities must be the cached ones)
+  __device__ __forceinline__ double aval(int j) const { return a[j * B]; }
   // all propensities; returns a0 summed in reaction order (oracle order)
   __device__ __forceinline__ double all_props(int M) const {
     double a0 = 0.0;
@@ -67,7 +70,7 @@ struct Sim {
   }
   __device__ __forceinline__ double sum_props(int M) const {
     double a0 = 0.0;
-    for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, a[j * B]);
+    for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, aval(j));
     return a0;
   }
   // x += sign * nu[:, j] * k
@@ -148,7 +151,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         for (int p = p0; p < p1; ++p) {
           const uint32_t e = tab_row(T, p);
           const int dl = KIN_NU_DELTA(e);
-          const double aj = a[KIN_NU_INDEX(e) * B];
+          const double aj = sm.aval(KIN_NU_INDEX(e));
           mu = __dadd_rn(mu, __dmul_rn(static_cast<double>(dl), aj));
           s2 = __dadd_rn(s2, __dmul_rn(static_cast<double>(dl * dl), aj));
         }
@@ -208,7 +211,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         double c = 0.0;
         int sel = -1, last = -1;
         for (int j = 0; j < M; ++j) {
-          const double aj = a[j * B];
+          const double aj = sm.aval(j);
           if (aj > 0.0) last = j;
           c = __dadd_rn(c, aj);
           if (c > target) { sel = j; break; }
@@ -231,10 +234,12 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         if (kind == 0) ++n_steps; else ++n_ssa;
         while (gi < G && tab_grid(T, S, gi) <= t) emit();
         // re-evaluate the propensities that changed, then a0 in oracle order
-        const int q1 = tab_dep_ptr(T, sel + 1);
-        for (int q = tab_dep_ptr(T, sel); q < q1; ++q) {
-          const int k = tab_dep(T, q);
-          a[k * B] = sm.prop(k);
+        {
+          const int q1 = tab_dep_ptr(T, sel + 1);
+          for (int q = tab_dep_ptr(T, sel); q < q1; ++q) {
+            const int k = tab_dep(T, q);
+            a[k * B] = sm.prop(k);
+          }
         }
         a0 = sm.sum_props(M);
       }
@@ -251,7 +256,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     Xoshiro saved = rng;
     for (;;) {
       for (int j = 0; j < M; ++j) {
-        const uint64_t k = poisson<kCount>(rng, __dmul_rn(a[j * B], tau), flops, S.lgamma_tab);
+        const uint64_t k = poisson<kCount>(rng, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
         if (k != 0) sm.apply(j, static_cast<double>(k));
       }
       if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
@@ -260,7 +265,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
       if (!neg) break;
       // rejected: undo exactly by replaying the same draws, continue the stream
       for (int j = 0; j < M; ++j) {
-        const uint64_t k = poisson<false>(saved, __dmul_rn(a[j * B], tau), dummy, S.lgamma_tab);
+        const uint64_t k = poisson<false>(saved, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
         if (k != 0) sm.apply(j, -static_cast<double>(k));
       }
       saved = rng;
@@ -319,8 +324,7 @@ size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block
 }
 
 cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
-                              int block, unsigned long long* counter, cudaStream_t stream) {
-  (void)block;
+                              unsigned long long* counter, cudaStream_t stream) {
   if (S.n_local == 0) return cudaSuccess;
   const size_t smem = stochastic_smem_bytes(T, S, kBlock);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;

@@ -1,0 +1,87 @@
+"""N>1 path on CPU: world_size-2 gloo processes shard a sweep by whole-point
+ranges (the bench's torchrun layout), each rank simulates its shard, rank 0
+gathers; the result must equal the single-process run bit for bit (per-run
+output independent of the device count).  The per-rank simulator
+here is the CPU oracle standing in for a GPU; the sharding and gather logic is
+the product's (paper_1309_7695_b200/shard.py).  Also checks the engine's
+in-process chunk plan (kin_sweep_plan)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1309_7695_b200 import shard, workloads as W
+from paper_1309_7695_b200.ensemble import MethodKind, make_sweep_desc, sweep_size
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, which, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as O
+    net, cfg = {"c1": lambda: W.c1_config(MethodKind.TauAdaptive, side=8),
+                "c2": lambda: W.c2_config(points=4, runs=16)}[which]()
+    P, S = sweep_size(cfg)
+    s0, s1 = shard.rank_range(P, cfg.runs_per_point, rank, world)
+    d, keep = make_sweep_desc(net, cfg, sim_range=(s0, s1))
+    r = O.sweep(net, d, workers=1, want_stats=True)
+    parts = [None] * world
+    dist.all_gather_object(parts, (s0, s1, r["traj"], r["mean"], r["m2"]))
+    if rank == 0:
+        out_q.put(parts)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("which", ["c1", "c2"])
+def test_two_rank_shard_equals_single_process(which):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, which, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from oracle import oracle as O
+    net, cfg = {"c1": lambda: W.c1_config(MethodKind.TauAdaptive, side=8),
+                "c2": lambda: W.c2_config(points=4, runs=16)}[which]()
+    d, keep = make_sweep_desc(net, cfg)
+    full = O.sweep(net, d, workers=3, want_stats=True)
+    assert parts[0][0] == 0 and parts[0][1] == parts[1][0] and parts[1][1] == len(full["traj"])
+    assert np.array_equal(shard.gather([p[2] for p in parts]), full["traj"])
+    assert np.array_equal(shard.gather([p[3] for p in parts]), full["mean"])
+    assert np.array_equal(shard.gather([p[4] for p in parts]), full["m2"])
+
+
+@pytest.mark.parametrize("s0,s1,R,D", [(0, 65536, 1, 8), (0, 16384, 256, 8), (100, 1000, 7, 3), (0, 10, 1, 1),
+                                        (5, 5, 1, 4), (0, 512, 256, 8)])
+def test_engine_chunk_plan(s0, s1, R, D):
+    chunks = shard.plan(s0, s1, R, D)
+    assert chunks[0][0] == s0 and chunks[-1][1] == s1
+    for (a0, a1, dv), (b0, b1, _) in zip(chunks, chunks[1:]):
+        assert a1 == b0 and a0 <= a1
+    for c0, c1, dv in chunks[1:]:
+        if c0 not in (s0, s1):
+            assert c0 % R == 0  # whole points: every interior boundary on a point boundary
+    assert [c[2] for c in chunks] == [i % D for i in range(len(chunks))]
+    if D == 1:
+        assert len(chunks) == 1
+
+
+def test_rank_range_partition():
+    for P, R, world in [(65536, 1, 8), (64, 256, 3), (5, 2, 8)]:
+        rngs = [shard.rank_range(P, R, r, world) for r in range(world)]
+        assert rngs[0][0] == 0 and rngs[-1][1] == P * R
+        assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
+        assert all(r[0] % R == 0 for r in rngs)
