@@ -177,7 +177,7 @@ template <bool C>
 int simulate_stochastic(const Network& net, const double* rates, const double* x0,
                         const kin_method& method, double t_end, const double* grid,
                         int n_grid, std::uint64_t seed, double* out, std::uint64_t* meta,
-                        Scratch& sc, Work* w) {
+                        Scratch& sc, Work* w, int rng_mode) {
   const int n = net.n, m = net.m;
   double* x = sc.x.data();
   double* xn = sc.xn.data();
@@ -187,6 +187,8 @@ int simulate_stochastic(const Network& net, const double* rates, const double* x
   for (int i = 0; i < n; ++i) x[i] = x0[i];
   for (int q = 0; q < 6; ++q) meta[q] = 0;
   Stream rng(seed);
+  const bool philox = rng_mode == KIN_RNG_PHILOX;
+  std::uint64_t ev = 0;  // Philox event counter (leap attempts and SSA events)
   const int kind = method.kind;
   double t = 0.0;
   int gi = 0;
@@ -232,8 +234,15 @@ int simulate_stochastic(const Network& net, const double* rates, const double* x
           if constexpr (C) w->flops += m;
           if (a0 == 0.0) { stop = true; break; }
         }
-        const double u1 = rng.draw_uniform();
-        const double u2 = rng.draw_uniform();
+        double u1, u2;
+        if (philox) {
+          PhiloxSite src(seed, ev++, kPhiloxSsaSite);
+          u1 = src.draw_uniform();
+          u2 = src.draw_uniform();
+        } else {
+          u1 = rng.draw_uniform();
+          u2 = rng.draw_uniform();
+        }
         const double dt = std::log(1.0 / u1) / a0;
         const double tn = t + dt;
         if constexpr (C) w->flops += 4 + 4;
@@ -263,7 +272,15 @@ int simulate_stochastic(const Network& net, const double* rates, const double* x
     if constexpr (C) w->flops += 1;
     if (!(tau < gap)) { tau = gap; hit = true; }
     for (;;) {
-      for (int j = 0; j < m; ++j) k[j] = rng.draw_poisson(a[j] * tau, pf);
+      if (philox) {
+        for (int j = 0; j < m; ++j) {
+          PhiloxSite src(seed, ev, static_cast<std::uint32_t>(j));
+          k[j] = poisson_from(src, a[j] * tau, pf);
+        }
+        ++ev;
+      } else {
+        for (int j = 0; j < m; ++j) k[j] = rng.draw_poisson(a[j] * tau, pf);
+      }
       for (int i = 0; i < n; ++i) xn[i] = x[i];
       for (int j = 0; j < m; ++j) {
         if (k[j] == 0) continue;
@@ -1008,7 +1025,8 @@ int run_one(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, doub
     return integrate_rre<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
   if (M.kind == KIN_METHOD_LSODA)
     return integrate_lsoda<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
-  return simulate_stochastic<C>(net, sc.rates.data(), x0, M, d->t_end, d->grid, d->n_grid, seed, traj, meta, sc, w);
+  return simulate_stochastic<C>(net, sc.rates.data(), x0, M, d->t_end, d->grid, d->n_grid, seed, traj, meta, sc, w,
+                                d->rng_mode);
 }
 
 // EnsembleStatistics::add (Welford), ensemble.hpp:29-30; App. B #9 order.
@@ -1044,6 +1062,28 @@ void kin_oracle_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t*
       default: bits = r.draw_poisson(mean); break;
     }
     out[q] = bits;
+  }
+}
+
+// Philox4x32-10 block (known-answer tests) and Philox draw sites:
+// kind 4 = uniforms (bits) of site (seed, event 0, slot 0); kind 5 = one
+// Poisson(mean) draw per site (seed, event 0, slot q) for q = 0..n-1.
+void kin_oracle_philox_block(uint32_t k0, uint32_t k1, const uint32_t* ctr, uint32_t* out) {
+  Philox::block(k0, k1, ctr[0], ctr[1], ctr[2], ctr[3], out);
+}
+
+void kin_oracle_philox_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out) {
+  if (kind == 4) {
+    PhiloxSite src(seed, 0, 0);
+    for (int q = 0; q < n; ++q) {
+      const double v = src.draw_uniform();
+      std::memcpy(&out[q], &v, 8);
+    }
+  } else {
+    for (int q = 0; q < n; ++q) {
+      PhiloxSite src(seed, 0, static_cast<uint32_t>(q));
+      out[q] = poisson_from(src, mean, nullptr);
+    }
   }
 }
 

@@ -98,7 +98,7 @@ template <bool C>
 int simulate_stochastic(const Network& net, const double* rates, const double* x0,
                         const kin_method& method, double t_end, const double* grid,
                         int n_grid, std::uint64_t seed, double* out, std::uint64_t* meta,
-                        Scratch& sc, Work* w);
+                        Scratch& sc, Work* w, int rng_mode);
 
 template <bool C>
 int integrate_rre(const Network& net, const double* rates, const double* x0,

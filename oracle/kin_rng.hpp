@@ -77,44 +77,9 @@ class Xoshiro256pp {
     return radius * std::cos(angle);
   }
 
-  // Work-instrumented Poisson draw; `flops` (may be null) receives the
-  // algorithmic FP64 op count (FMA=2; + - * / sqrt exp log lgamma = 1).
-  std::uint64_t draw_poisson(double mean, std::uint64_t* flops = nullptr) {
-    if (mean <= 0.0) return 0;
-    if (mean < 10.0) {
-      const double u = draw_uniform();
-      double p = std::exp(-mean);
-      double c = p;
-      std::uint64_t k = 0;
-      while (u > c && k < 256) {
-        ++k;
-        p *= mean / static_cast<double>(k);
-        c += p;
-      }
-      if (flops) *flops += 3 + 3 * k;
-      return k;
-    }
-    const double lm = std::log(mean);
-    const double b = 0.931 + 2.53 * std::sqrt(mean);
-    const double a = -0.059 + 0.02483 * b;
-    const double inv_alpha = 1.1239 + 1.1328 / (b - 3.4);
-    const double v_r = 0.9277 - 3.6224 / (b - 2.0);
-    if (flops) *flops += 12;  // log, sqrt, 2 mul, 6 add/sub, 2 div
-    for (;;) {
-      const double u = draw_uniform() - 0.5;
-      const double v = draw_uniform();
-      const double us = 0.5 - std::fabs(u);
-      const double kf = std::floor((2.0 * a / us + b) * u + mean + 0.43);
-      if (flops) *flops += 12;  // 2 uniforms (4) + 8 arithmetic
-      if (kf < 0.0) continue;
-      if (us >= 0.07 && v <= v_r) return static_cast<std::uint64_t>(kf);
-      if (us < 0.013 && v > us) continue;
-      const double lhs = std::log(v * inv_alpha / (a / (us * us) + b));
-      const double rhs = -mean + kf * lm - std::lgamma(kf + 1.0);
-      if (flops) *flops += 11;
-      if (lhs <= rhs) return static_cast<std::uint64_t>(kf);
-    }
-  }
+  // Work-instrumented Poisson draw (rng.cpp:68-109); `flops` (may be null)
+  // receives the algorithmic FP64 op count (FMA=2; + - * / sqrt exp log lgamma = 1).
+  std::uint64_t draw_poisson(double mean, std::uint64_t* flops = nullptr);
 
  private:
   static std::uint64_t rotl(std::uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
@@ -122,6 +87,98 @@ class Xoshiro256pp {
   double spare_ = 0.0;
   bool spare_valid_ = false;
 };
+
+// draw_poisson's algorithm over any source of draw_uniform() values.
+template <class Src>
+std::uint64_t poisson_from(Src& src, double mean, std::uint64_t* flops) {
+  if (mean <= 0.0) return 0;
+  if (mean < 10.0) {
+    const double u = src.draw_uniform();
+    double p = std::exp(-mean);
+    double c = p;
+    std::uint64_t k = 0;
+    while (u > c && k < 256) {
+      ++k;
+      p *= mean / static_cast<double>(k);
+      c += p;
+    }
+    if (flops) *flops += 3 + 3 * k;
+    return k;
+  }
+  const double lm = std::log(mean);
+  const double b = 0.931 + 2.53 * std::sqrt(mean);
+  const double a = -0.059 + 0.02483 * b;
+  const double inv_alpha = 1.1239 + 1.1328 / (b - 3.4);
+  const double v_r = 0.9277 - 3.6224 / (b - 2.0);
+  if (flops) *flops += 12;  // log, sqrt, 2 mul, 6 add/sub, 2 div
+  for (;;) {
+    const double u = src.draw_uniform() - 0.5;
+    const double v = src.draw_uniform();
+    const double us = 0.5 - std::fabs(u);
+    const double kf = std::floor((2.0 * a / us + b) * u + mean + 0.43);
+    if (flops) *flops += 12;  // 2 uniforms (4) + 8 arithmetic
+    if (kf < 0.0) continue;
+    if (us >= 0.07 && v <= v_r) return static_cast<std::uint64_t>(kf);
+    if (us < 0.013 && v > us) continue;
+    const double lhs = std::log(v * inv_alpha / (a / (us * us) + b));
+    const double rhs = -mean + kf * lm - std::lgamma(kf + 1.0);
+    if (flops) *flops += 11;
+    if (lhs <= rhs) return static_cast<std::uint64_t>(kf);
+  }
+}
+
+inline std::uint64_t Xoshiro256pp::draw_poisson(double mean, std::uint64_t* flops) {
+  return poisson_from(*this, mean, flops);
+}
+
+// ---- Philox4x32-10 counter-based stream (KIN_RNG_PHILOX; no reference
+// counterpart: the north star's fast mode).  Salmon et al., SC'11.  Key =
+// the run seed; a draw site is addressed by (event index, slot) and yields
+// uniforms from consecutive 128-bit blocks (block b -> two 53-bit uniforms).
+struct Philox {
+  static void block(std::uint32_t k0, std::uint32_t k1, std::uint32_t c0, std::uint32_t c1, std::uint32_t c2,
+                    std::uint32_t c3, std::uint32_t out[4]) {
+    for (int r = 0; r < 10; ++r) {
+      if (r > 0) {
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+      }
+      const std::uint64_t p0 = static_cast<std::uint64_t>(0xD2511F53u) * c0;
+      const std::uint64_t p1 = static_cast<std::uint64_t>(0xCD9E8D57u) * c2;
+      const std::uint32_t hi0 = static_cast<std::uint32_t>(p0 >> 32), lo0 = static_cast<std::uint32_t>(p0);
+      const std::uint32_t hi1 = static_cast<std::uint32_t>(p1 >> 32), lo1 = static_cast<std::uint32_t>(p1);
+      const std::uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+      c0 = n0;
+      c1 = lo1;
+      c2 = n2;
+      c3 = lo0;
+    }
+    out[0] = c0;
+    out[1] = c1;
+    out[2] = c2;
+    out[3] = c3;
+  }
+};
+
+// Uniform source for one draw site: (seed, event, slot) -> blocks 0, 1, ...
+struct PhiloxSite {
+  std::uint32_t k0, k1, slot, ev_lo, ev_hi;
+  std::uint32_t blk = 0;
+  int half = 0;
+  std::uint32_t buf[4];
+  PhiloxSite(std::uint64_t seed, std::uint64_t event, std::uint32_t site)
+      : k0(static_cast<std::uint32_t>(seed)), k1(static_cast<std::uint32_t>(seed >> 32)), slot(site),
+        ev_lo(static_cast<std::uint32_t>(event)), ev_hi(static_cast<std::uint32_t>(event >> 32)) {}
+  double draw_uniform() {
+    if (half == 0) Philox::block(k0, k1, slot, ev_lo, ev_hi, blk, buf);
+    const std::uint64_t x = half == 0 ? (static_cast<std::uint64_t>(buf[1]) << 32 | buf[0])
+                                      : (static_cast<std::uint64_t>(buf[3]) << 32 | buf[2]);
+    if (half == 1) ++blk;
+    half ^= 1;
+    return (static_cast<double>(x >> 11) + 0.5) * 0x1.0p-53;
+  }
+};
+constexpr std::uint32_t kPhiloxSsaSite = 0xFFFFFFFFu;
 
 #ifdef KIN_ORACLE_REF_RNG
 // The reference stream itself (proj/src/rng.cpp compiled from /root/reference).

@@ -49,6 +49,10 @@ def load(ref: bool = False) -> C.CDLL:
     lib.kin_oracle_rng_draws.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_int, u64p]
     lib.kin_oracle_rng_sequence.restype = None
     lib.kin_oracle_rng_sequence.argtypes = [C.c_uint64, f64p, C.c_int, C.c_int, C.c_int, u64p]
+    lib.kin_oracle_philox_block.restype = None
+    lib.kin_oracle_philox_block.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    lib.kin_oracle_philox_draws.restype = None
+    lib.kin_oracle_philox_draws.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_int, u64p]
     lib.kin_oracle_model_check.argtypes = [M, E]
     lib.kin_oracle_propensities.argtypes = [M, f64p, f64p, E]
     lib.kin_oracle_select_tau.argtypes = [M, f64p, C.c_double, f64p, E]
@@ -74,6 +78,19 @@ def rng_draws_sequence(seed: int, means, n_each: int, n_normal: int, ref: bool =
     m = np.ascontiguousarray(means, dtype=np.float64)
     out = np.zeros(len(m) * n_each + n_normal, dtype=np.uint64)
     load(ref).kin_oracle_rng_sequence(seed, abi.ptr(m, C.c_double), len(m), n_each, n_normal, abi.ptr(out, C.c_uint64))
+    return out
+
+
+def philox_block(key, ctr):
+    k = (C.c_uint32 * 4)(*ctr)
+    out = (C.c_uint32 * 4)()
+    load().kin_oracle_philox_block(key[0], key[1], k, out)
+    return list(out)
+
+
+def philox_draws(seed: int, kind: int, n: int, mean: float = 0.0) -> np.ndarray:
+    out = np.zeros(n, dtype=np.uint64)
+    load().kin_oracle_philox_draws(seed, kind, mean, n, abi.ptr(out, C.c_uint64))
     return out
 
 

@@ -113,6 +113,48 @@ struct Xoshiro {
   }
 };
 
+// ---- Philox4x32-10 counter-based stream (KIN_RNG_PHILOX), mirrors
+// oracle/kin_rng.hpp Philox/PhiloxSite: key = run seed, a draw site is
+// (event index, slot), uniforms come from consecutive 128-bit blocks.
+__device__ __forceinline__ void philox_block(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                             uint32_t c3, uint32_t out[4]) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+constexpr uint32_t kPhiloxSsaSite = 0xFFFFFFFFu;
+struct PhiloxSite {
+  uint32_t k0, k1, slot, ev_lo, ev_hi, blk;
+  int half;
+  uint32_t buf[4];
+  __device__ __forceinline__ PhiloxSite(uint64_t seed, uint64_t event, uint32_t site)
+      : k0(static_cast<uint32_t>(seed)), k1(static_cast<uint32_t>(seed >> 32)), slot(site),
+        ev_lo(static_cast<uint32_t>(event)), ev_hi(static_cast<uint32_t>(event >> 32)), blk(0), half(0) {}
+  __device__ __forceinline__ double uniform() {
+    if (half == 0) philox_block(k0, k1, slot, ev_lo, ev_hi, blk, buf);
+    const uint64_t x = half == 0 ? (static_cast<uint64_t>(buf[1]) << 32 | buf[0])
+                                 : (static_cast<uint64_t>(buf[3]) << 32 | buf[2]);
+    if (half == 1) ++blk;
+    half ^= 1;
+    return __dmul_rn(__dadd_rn(static_cast<double>(x >> 11), 0.5), 0x1.0p-53);
+  }
+};
+
 // mean / k, correctly rounded.  Division by a power of two is exact scaling, so
 // mean*2^-j is bit-identical to mean/2^j; only other k need the IEEE divide.
 __device__ __forceinline__ double div_small(double mean, int k) {
@@ -137,8 +179,8 @@ __device__ __constant__ float c_rcp40[41] = {
 // lgamma(k+1), k < KIN_LGAMMA_N, computed by the host's glibc (the oracle's libm)
 // and uploaded once per context (see kin_engine.cpp).
 #define KIN_LGAMMA_N 4096
-template <bool kCount>
-__device__ __forceinline__ uint64_t poisson(Xoshiro& rng, double mean, uint64_t& flops, const double* lgamma_tab) {
+template <bool kCount, class Rng>
+__device__ __forceinline__ uint64_t poisson(Rng& rng, double mean, uint64_t& flops, const double* lgamma_tab) {
   if (!(mean > 0.0)) return 0;
   if (mean < 10.0) {
     const double u = rng.uniform();

@@ -209,7 +209,7 @@ int validate_sweep(const HostModel& net, const kin_sweep_desc* d, const Layout& 
     }
   }
   if (d->seed_mode == KIN_SEED_DIRECT && L.S != 1) { *msg = "direct seeding needs exactly one simulation"; return KIN_ERR_INPUT; }
-  if (d->rng_mode != KIN_RNG_COMPAT) { *msg = "rng_mode: only the compat (reference xoshiro256++) stream is built"; return KIN_ERR_INPUT; }
+  if (d->rng_mode != KIN_RNG_COMPAT && d->rng_mode != KIN_RNG_PHILOX) { *msg = "unknown rng_mode"; return KIN_ERR_INPUT; }
   return KIN_OK;
 }
 

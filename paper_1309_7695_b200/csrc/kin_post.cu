@@ -86,6 +86,11 @@ __global__ void rng_kernel(uint64_t seed, int kind, double mean, int n, uint64_t
   uint64_t dummy = 0;
   double spare = 0.0;
   bool have = false;
+  if (kind == 4) {
+    PhiloxSite src(seed, 0, 0);
+    for (int q = 0; q < n; ++q) out[q] = __double_as_longlong(src.uniform());
+    return;
+  }
   for (int q = 0; q < n; ++q) {
     uint64_t bits;
     if (kind == 0) {
@@ -108,6 +113,14 @@ __global__ void rng_kernel(uint64_t seed, int kind, double mean, int n, uint64_t
         v = __dmul_rn(r, cos(ang));
       }
       bits = __double_as_longlong(v);
+    } else if (kind == 4) {  // Philox uniforms of site (seed, 0, 0)
+      if (q == 0) {
+        // handled below with a persistent site
+      }
+      bits = 0;
+    } else if (kind == 5) {  // one Philox Poisson draw per site (seed, 0, q)
+      PhiloxSite src(seed, 0, static_cast<uint32_t>(q));
+      bits = poisson<false>(src, mean, dummy, lgamma_tab);
     } else {
       bits = poisson<false>(rng, mean, dummy, lgamma_tab);
     }

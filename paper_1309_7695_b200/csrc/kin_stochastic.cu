@@ -84,7 +84,7 @@ struct Sim {
   }
 };
 
-template <bool kCount>
+template <bool kCount, bool kPhilox>
 __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
                                              uint64_t s, double* x, double* a, double* av, int B) {
   const uint64_t sim = S.sim_begin + s;
@@ -107,8 +107,10 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   }
   const Sim sm{T, x, a, av, B};
 
+  const uint64_t seed = sim_seed(S, sim);
   Xoshiro rng;
-  rng.seed(sim_seed(S, sim));
+  if (!kPhilox) rng.seed(seed);
+  uint64_t ev = 0;  // Philox event counter (leap attempts and SSA events)
   const int kind = S.kind;
   const double t_end = S.t_end;
   double t = 0.0;
@@ -199,8 +201,15 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
           if (kCount) flops += F_prop + M;
           if (a0 == 0.0) { stop = true; break; }
         }
-        const double u1 = rng.uniform();
-        const double u2 = rng.uniform();
+        double u1, u2;
+        if (kPhilox) {
+          PhiloxSite src(seed, ev++, kPhiloxSsaSite);
+          u1 = src.uniform();
+          u2 = src.uniform();
+        } else {
+          u1 = rng.uniform();
+          u2 = rng.uniform();
+        }
         const double dt = __ddiv_rn(log(__ddiv_rn(1.0, u1)), a0);
         const double tn = __dadd_rn(t, dt);
         if (kCount) flops += 8;
@@ -256,18 +265,34 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     Xoshiro saved = rng;
     for (;;) {
       for (int j = 0; j < M; ++j) {
-        const uint64_t k = poisson<kCount>(rng, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
+        uint64_t k;
+        if (kPhilox) {
+          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
+          k = poisson<kCount>(src, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
+        } else {
+          k = poisson<kCount>(rng, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
+        }
         if (k != 0) sm.apply(j, static_cast<double>(k));
       }
       if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
       bool neg = false;
       for (int i = 0; i < N; ++i) neg |= x[i * B] < 0.0;
-      if (!neg) break;
+      if (!neg) {
+        ++ev;
+        break;
+      }
       // rejected: undo exactly by replaying the same draws, continue the stream
       for (int j = 0; j < M; ++j) {
-        const uint64_t k = poisson<false>(saved, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
+        uint64_t k;
+        if (kPhilox) {
+          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
+          k = poisson<false>(src, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
+        } else {
+          k = poisson<false>(saved, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
+        }
         if (k != 0) sm.apply(j, -static_cast<double>(k));
       }
+      ++ev;
       saved = rng;
       ++n_rej;
       tau = __dmul_rn(tau, 0.5);
@@ -297,7 +322,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   if (kCount && O.work) O.work[s] = flops;
 }
 
-template <bool kCount>
+template <bool kCount, bool kPhilox>
 __global__ void __launch_bounds__(kBlock) stochastic_kernel(const __grid_constant__ KinTables T,
                                                             const __grid_constant__ KinSweepDev S, KinOutDev O,
                                                             unsigned long long* __restrict__ next) {
@@ -312,7 +337,7 @@ __global__ void __launch_bounds__(kBlock) stochastic_kernel(const __grid_constan
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     if (base >= S.n_local) break;
     const uint64_t s = base + lane;
-    if (s < S.n_local) simulate_one<kCount>(T, S, O, s, x, a, av, B);
+    if (s < S.n_local) simulate_one<kCount, kPhilox>(T, S, O, s, x, a, av, B);
     __syncwarp();
   }
 }
@@ -328,7 +353,9 @@ cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const Ki
   if (S.n_local == 0) return cudaSuccess;
   const size_t smem = stochastic_smem_bytes(T, S, kBlock);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  auto kern = count ? stochastic_kernel<true> : stochastic_kernel<false>;
+  const bool ph = S.rng_mode == KIN_RNG_PHILOX;
+  auto kern = count ? (ph ? stochastic_kernel<true, true> : stochastic_kernel<true, false>)
+                    : (ph ? stochastic_kernel<false, true> : stochastic_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;

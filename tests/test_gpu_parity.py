@@ -21,11 +21,12 @@ from paper_1309_7695_b200.model import SimulationError
 pytestmark = pytest.mark.gpu
 
 
-def both(engine, oracle, net, cfg, *, sim_range=None, seed_mode=abi.SEED_SWEEP, want_work=False, stats=False):
-    d, keep = make_sweep_desc(net, cfg, seed_mode=seed_mode, sim_range=sim_range)
+def both(engine, oracle, net, cfg, *, sim_range=None, seed_mode=abi.SEED_SWEEP, want_work=False, stats=False,
+         rng_mode=abi.RNG_COMPAT):
+    d, keep = make_sweep_desc(net, cfg, seed_mode=seed_mode, sim_range=sim_range, rng_mode=rng_mode)
     ref = oracle.sweep(net, d, want_traj=True, want_stats=stats, want_work=want_work)
     got = engine.sweep(net, cfg, seed_mode=seed_mode, sim_range=sim_range, want_traj=True, want_stats=stats,
-                       want_work=want_work)
+                       want_work=want_work, rng_mode=rng_mode)
     return ref, got
 
 
@@ -164,6 +165,40 @@ def test_budget_error_lowest_index(engine, oracle):
         engine.sweep(net, cfg)
     assert ei.value.sim_index == ref["error"].sim_index
     assert ei.value.sim_status == 1  # KIN_SIM_BUDGET
+
+
+# ---- Philox fast mode: bit-exact against the oracle's Philox stream -----------
+def test_device_philox_draws(engine, oracle):
+    import ctypes as C
+    for kind, mean in [(4, 0.0), (5, 0.7), (5, 9.99), (5, 10.0), (5, 812.0)]:
+        out = np.zeros(1000, dtype=np.uint64)
+        err = abi.KinError()
+        assert engine.lib.kin_device_rng_draws(engine.ctx, 77, kind, mean, 1000, abi.ptr(out, C.c_uint64),
+                                               C.byref(err)) == 0, err.text()
+        assert np.array_equal(out, oracle.philox_draws(77, kind, 1000, mean)), (kind, mean)
+
+
+@pytest.mark.parametrize("case", ["c1", "c4", "c2", "bd_ssa", "taufixed"])
+def test_philox_mode_bit_exact(engine, oracle, case):
+    sm, rng = abi.SEED_SWEEP, None
+    if case == "c1":
+        net, cfg = W.c1_config(MethodKind.TauAdaptive)
+    elif case == "c4":
+        net, cfg = W.c4_config()
+        rng = (20000, 20512)
+    elif case == "c2":
+        net, cfg = W.c2_config()
+        rng = (0, 512)
+    elif case == "bd_ssa":
+        net = W.birth_death()
+        cfg = SweepConfig([], 512, Method(MethodKind.Ssa), 7, 20.0, uniform_grid(20.0, 41))
+        sm = abi.SEED_ENSEMBLE
+    else:
+        net = W.birth_death(x0=3)
+        cfg = SweepConfig([SweepAxis("lam", [0.5, 5.0, 50.0])], 128, Method(MethodKind.TauFixed, tau=0.5), 11, 10.0,
+                          uniform_grid(10.0, 21))
+    ref, got = both(engine, oracle, net, cfg, sim_range=rng, seed_mode=sm, want_work=True, rng_mode=abi.RNG_PHILOX)
+    assert_bit_exact(ref, got, work=True)
 
 
 # ---- deterministic (Dopri5): tolerance ---------------------------------------

@@ -80,3 +80,21 @@ def test_live_against_reference_build(kind, mean):
         a = O.rng_draws(seed, kind, 200, mean=mean)
         b = O.rng_draws(seed, kind, 200, mean=mean, ref=True)
         assert np.array_equal(a, b), (seed, kind, mean)
+
+
+def test_philox4x32_10_known_answers():
+    """Random123 kat_vectors for philox4x32_10."""
+    assert O.philox_block((0, 0), (0, 0, 0, 0)) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert O.philox_block((0xFFFFFFFF,) * 2, (0xFFFFFFFF,) * 4) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert O.philox_block((0xA4093822, 0x299F31D0), (0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344)) == \
+        [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_philox_poisson_moments():
+    from scipy import stats
+    for mean in (0.3, 4.2, 9.99, 10.0, 55.0, 3000.0):
+        k = O.philox_draws(7, 5, 20000, mean).astype(float)
+        assert abs(k.mean() - mean) < 4 * np.sqrt(mean / len(k))
+        assert abs(k.var() / mean - 1.0) < 0.08
+    u = O.philox_draws(9, 4, 50000).view(np.float64)
+    assert stats.kstest(u, "uniform").pvalue > 1e-3

@@ -26,8 +26,9 @@ peak = C.c_double()
 lib.kin_measure_fp64_peak(eng.ctx, C.byref(peak), C.byref(err))
 print("fp64 peak TFLOP/s", peak.value, flush=True)
 for name in names:
-    net, cfg = cfgs[name]
-    d, keep = make_sweep_desc(net, cfg)
+    base, _, mode = name.partition(":")
+    net, cfg = cfgs[base]
+    d, keep = make_sweep_desc(net, cfg, rng_mode=abi.RNG_PHILOX if mode == "philox" else abi.RNG_COMPAT)
     h = eng.model(net)
     # counting pass
     rc = lib.kin_sweep_launch(eng.ctx, h, C.byref(d), 0, 0, 1, C.byref(err)); assert rc == 0, err.text()
