@@ -560,7 +560,14 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
     e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, sl.counter.p, sl.stream);
   } else {
     KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
-    e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.stream);
+    // Philox mode: L lanes per simulation (KIN_GROUP_LANES overrides; 1 = one
+    // thread per simulation).  Compat mode is always one thread per simulation.
+    int lanes = 0;
+    if (const char* v = std::getenv("KIN_GROUP_LANES")) lanes = std::atoi(v);
+    if (d->rng_mode == KIN_RNG_PHILOX && lanes != 1)
+      e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, sl.counter.p, sl.stream);
+    else
+      e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.stream);
   }
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
   KIN_CUDA(cudaEventRecord(sl.tev[1], sl.stream), "event");

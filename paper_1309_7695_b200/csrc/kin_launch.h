@@ -15,6 +15,11 @@ size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block
 cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                               unsigned long long* counter, cudaStream_t stream);
 
+// kin_stochastic_group.cu: Philox mode, L lanes per simulation (lanes <= 0 picks).
+int stochastic_group_pick_lanes(int n_species, int n_reactions);
+cudaError_t launch_stochastic_group(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
+                                    int lanes, unsigned long long* counter, cudaStream_t stream);
+
 // kin_ode.cu: Dopri5 RRE integration, L lanes per simulation (L = 0 picks).
 int ode_pick_lanes(int n_species);
 cudaError_t launch_dopri5(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, int lanes,

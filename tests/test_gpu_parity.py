@@ -178,8 +178,12 @@ def test_device_philox_draws(engine, oracle):
         assert np.array_equal(out, oracle.philox_draws(77, kind, 1000, mean)), (kind, mean)
 
 
-@pytest.mark.parametrize("case", ["c1", "c4", "c2", "bd_ssa", "taufixed"])
-def test_philox_mode_bit_exact(engine, oracle, case):
+@pytest.mark.parametrize("lanes", ["0", "1", "4", "32"])
+@pytest.mark.parametrize("case", ["c1", "c4", "c2", "bd_ssa", "taufixed", "c5"])
+def test_philox_mode_bit_exact(engine, oracle, case, lanes, monkeypatch):
+    """Philox mode through the lane-group kernel (auto / 4 / 32 lanes per
+    simulation) and the thread-per-simulation kernel (lanes=1)."""
+    monkeypatch.setenv("KIN_GROUP_LANES", lanes)
     sm, rng = abi.SEED_SWEEP, None
     if case == "c1":
         net, cfg = W.c1_config(MethodKind.TauAdaptive)
@@ -189,6 +193,9 @@ def test_philox_mode_bit_exact(engine, oracle, case):
     elif case == "c2":
         net, cfg = W.c2_config()
         rng = (0, 512)
+    elif case == "c5":
+        net, cfg = W.c5_config()
+        rng = (300, 364)
     elif case == "bd_ssa":
         net = W.birth_death()
         cfg = SweepConfig([], 512, Method(MethodKind.Ssa), 7, 20.0, uniform_grid(20.0, 41))

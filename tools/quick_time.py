@@ -25,8 +25,14 @@ err = abi.KinError()
 peak = C.c_double()
 lib.kin_measure_fp64_peak(eng.ctx, C.byref(peak), C.byref(err))
 print("fp64 peak TFLOP/s", peak.value, flush=True)
+import os
 for name in names:
     base, _, mode = name.partition(":")
+    if "@" in mode:
+        mode, lanes = mode.split("@")
+        os.environ["KIN_GROUP_LANES"] = lanes
+    else:
+        os.environ.pop("KIN_GROUP_LANES", None)
     net, cfg = cfgs[base]
     d, keep = make_sweep_desc(net, cfg, rng_mode=abi.RNG_PHILOX if mode == "philox" else abi.RNG_COMPAT)
     h = eng.model(net)
