@@ -419,6 +419,14 @@ struct Slot {
   uint64_t s0 = 0, s1 = 0, P0 = 0, nP = 0, R = 1;
   int G = 0, N = 0;
   bool have_stats = false, have_work = false, valid = false;
+  // replay record for the int32-amount retry
+  DevBuf<int> ovf;
+  std::unique_ptr<KinTables> last_T;
+  KinSweepDev last_SD{};
+  KinOutDev last_O{};
+  bool last_int_state = false, last_count = false, pending_check = false;
+  uint64_t last_base = 0, last_S = 0;
+  int last_gn = 0;
   std::mutex mu;
 };
 
@@ -560,14 +568,37 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
     e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, sl.counter.p, sl.stream);
   } else {
     KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
+    KIN_CUDA(sl.ovf.ensure(1), "cudaMalloc overflow flag");
     // Philox mode: L lanes per simulation (KIN_GROUP_LANES overrides; 1 = one
     // thread per simulation).  Compat mode is always one thread per simulation.
     int lanes = 0;
     if (const char* v = std::getenv("KIN_GROUP_LANES")) lanes = std::atoi(v);
-    if (d->rng_mode == KIN_RNG_PHILOX && lanes != 1)
+    if (d->rng_mode != KIN_RNG_PHILOX) lanes = 1;
+    else if (lanes <= 0) lanes = kin::stochastic_group_pick_lanes(H.n, H.m);
+    if (lanes != 1) {
       e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, sl.counter.p, sl.stream);
-    else
-      e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.stream);
+      sl.last_int_state = false;
+    } else {
+      // int32 amounts when every initial amount is far inside int32 range
+      // (KIN_INT_STATE=0 forces doubles)
+      double xmax = 0.0;
+      for (double v : H.x0) xmax = std::max(xmax, v);
+      for (int ax = 0; ax < d->n_axes; ++ax)
+        if (d->axes[ax].kind == KIN_AXIS_INITIAL)
+          for (int v = 0; v < d->axes[ax].n_values; ++v) xmax = std::max(xmax, d->axes[ax].values[v]);
+      bool int_state = xmax < 1073741824.0;
+      if (const char* v = std::getenv("KIN_INT_STATE")) int_state = int_state && std::atoi(v) != 0;
+      KIN_CUDA(cudaMemsetAsync(sl.ovf.p, 0, sizeof(int), sl.stream), "memset");
+      e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.ovf.p, int_state, sl.stream);
+      sl.last_int_state = int_state;
+    }
+    if (sl.last_int_state) {
+      if (!sl.last_T) sl.last_T.reset(new KinTables);
+      *sl.last_T = *T;
+      sl.last_SD = SD;
+      sl.last_O = O;
+      sl.last_count = want_work;
+    }
   }
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
   KIN_CUDA(cudaEventRecord(sl.tev[1], sl.stream), "event");
@@ -584,6 +615,10 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
     KIN_CUDA(cudaEventRecord(sl.tev[2], sl.stream), "event");
     sl.timed_stats = true;
   }
+  sl.pending_check = sl.last_int_state;
+  sl.last_base = P0 * L.R - s0;
+  sl.last_S = S;
+  sl.last_gn = static_cast<int>(gn);
   sl.s0 = s0;
   sl.s1 = s1;
   sl.P0 = P0;
@@ -597,10 +632,33 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
   return KIN_OK;
 }
 
+// Complete a launch: wait for it and, if an int32 amount overflowed, re-run the
+// stochastic kernel with double amounts (and the statistics) — same results.
+int finish_launch(Slot& sl, kin_error* err) {
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
+  if (!sl.pending_check) return KIN_OK;
+  sl.pending_check = false;
+  int flag = 0;
+  KIN_CUDA(cudaMemcpy(&flag, sl.ovf.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H overflow flag");
+  if (!flag) return KIN_OK;
+  KIN_CUDA(cudaMemsetAsync(sl.ovf.p, 0, sizeof(int), sl.stream), "memset");
+  cudaError_t e = kin::launch_stochastic(*sl.last_T, sl.last_SD, sl.last_O, sl.last_count, sl.counter.p, sl.ovf.p,
+                                         false, sl.stream);
+  if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel relaunch");
+  if (sl.have_stats) {
+    e = kin::launch_point_stats(sl.traj.p, sl.last_S, sl.last_gn, sl.R, sl.last_base, sl.nP, sl.mean.p, sl.m2.p,
+                                sl.stream);
+    if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel relaunch");
+  }
+  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
+  return KIN_OK;
+}
+
 // Copy the slot's last launch into caller buffers; offsets are relative to
 // (base_sim, base_point) of the caller's arrays.
 int fetch_range(Slot& sl, kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, kin_error* err) {
-  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  if (int rc = finish_launch(sl, err)) return rc;
   const uint64_t S = sl.s1 - sl.s0;
   const size_t gn = static_cast<size_t>(sl.G) * sl.N;
   const uint64_t so = sl.s0 - base_sim;
@@ -718,7 +776,7 @@ void kin_ctx_destroy(kin_ctx* ctx) {
     cudaSetDevice(sl->device);
     cudaStreamSynchronize(sl->stream);
     sl->traj.release(); sl->traj_t.release(); sl->mean.release(); sl->m2.release();
-    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->lgamma_tab.release(); sl->lsoda_co.release(); sl->status.release();
+    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->lgamma_tab.release(); sl->lsoda_co.release(); sl->ovf.release(); sl->status.release();
     if (sl->stage) cudaFreeHost(sl->stage);
     for (auto& e : sl->ev) if (e) cudaEventDestroy(e);
     for (auto& e : sl->tev) if (e) cudaEventDestroy(e);
@@ -856,9 +914,8 @@ int kin_sweep_sync(kin_ctx* ctx, int32_t slot, kin_error* err) {
     return KIN_ERR_USAGE;
   }
   Slot& sl = *ctx->slots[slot];
-  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
-  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
-  return KIN_OK;
+  std::lock_guard<std::mutex> lk(sl.mu);
+  return finish_launch(sl, err);
 }
 
 int kin_sweep_fetch(kin_ctx* ctx, int32_t slot, kin_sweep_out* out, kin_error* err) {

@@ -10,10 +10,11 @@
 namespace kin {
 
 // kin_stochastic.cu: SSA / tau-adaptive / tau-fixed, thread per simulation.
-size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block);
-// `counter` is a device word used by the persistent warps to fetch work.
+// `counter` is a device word used by the persistent warps to fetch work;
+// int_state stores amounts as int32 (more resident simulations) and sets
+// *ovf_flag if one leaves int32 range (the caller re-runs with double amounts).
 cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
-                              unsigned long long* counter, cudaStream_t stream);
+                              unsigned long long* counter, int* ovf_flag, bool int_state, cudaStream_t stream);
 
 // kin_stochastic_group.cu: Philox mode, L lanes per simulation (lanes <= 0 picks).
 int stochastic_group_pick_lanes(int n_species, int n_reactions);

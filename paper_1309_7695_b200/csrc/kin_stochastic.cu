@@ -33,13 +33,19 @@ namespace {
 constexpr double kInf = __builtin_huge_val();
 constexpr int kBlock = 32;  // one warp per block: finest smem granularity
 
+// Amounts are exact integers.  XT = double (any magnitude below 2^53, the
+// reference's SystemState) or int32_t (half the shared memory, so more resident
+// simulations; an update leaving int32 range raises *ovf and the engine re-runs
+// the launch with the double variant — results are identical either way).
+template <class XT>
 struct Sim {
   const KinTables& T;
-  double* x;         // x[i * B]
+  XT* x;             // x[i * B]
   double* a;         // a[j * B]
   const double* av;  // axis values av[ax * B]
   int B;
 
+  __device__ __forceinline__ double xv(int i) const { return static_cast<double>(x[i * B]); }
   // a_j(x) = c_j * prod h(x_s, stoich_s)   (model.hpp:151-157)
   __device__ __forceinline__ double prop(int j) const {
     const uint64_t d = tab_rdesc(T, j);
@@ -47,10 +53,10 @@ struct Sim {
     double aj = ax < 0 ? tab_rate(T, j) : av[ax * B];
     const int nt = KIN_RD_NTERMS(d);
     if (nt > 0) {
-      aj = __dmul_rn(aj, combinations(x[KIN_RD_SPECIES(d, 0) * B], KIN_RD_STOICH(d, 0)));
+      aj = __dmul_rn(aj, combinations(xv(KIN_RD_SPECIES(d, 0)), KIN_RD_STOICH(d, 0)));
       if (nt > 1) {
-        aj = __dmul_rn(aj, combinations(x[KIN_RD_SPECIES(d, 1) * B], KIN_RD_STOICH(d, 1)));
-        if (nt > 2) aj = __dmul_rn(aj, combinations(x[KIN_RD_SPECIES(d, 2) * B], KIN_RD_STOICH(d, 2)));
+        aj = __dmul_rn(aj, combinations(xv(KIN_RD_SPECIES(d, 1)), KIN_RD_STOICH(d, 1)));
+        if (nt > 2) aj = __dmul_rn(aj, combinations(xv(KIN_RD_SPECIES(d, 2)), KIN_RD_STOICH(d, 2)));
       }
     }
     return aj;
@@ -73,20 +79,46 @@ struct Sim {
     for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, aval(j));
     return a0;
   }
-  // x += sign * nu[:, j] * k
-  __device__ __forceinline__ void apply(int j, double kj) const {
+  // x += nu[:, j] * k  (k signed: negative undoes a rejected leap)
+  __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const {
     const int p1 = tab_col_ptr(T, j + 1);
     for (int p = tab_col_ptr(T, j); p < p1; ++p) {
       const uint32_t e = tab_col(T, p);
-      double* xs = x + KIN_NU_INDEX(e) * B;
-      *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), kj));
+      XT* xs = x + KIN_NU_INDEX(e) * B;
+      if constexpr (sizeof(XT) == 8) {
+        *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), static_cast<double>(k)));
+      } else {
+        const long long v = static_cast<long long>(*xs) + static_cast<long long>(KIN_NU_DELTA(e)) * k;
+        ovf |= v > 2147483647LL || v < -2147483647LL;
+        *xs = static_cast<XT>(v);
+      }
     }
+  }
+  // one SSA event: x += nu[:, j]; returns true if an amount went negative
+  __device__ __forceinline__ bool fire(int j, bool& ovf) const {
+    bool neg = false;
+    const int p1 = tab_col_ptr(T, j + 1);
+    for (int p = tab_col_ptr(T, j); p < p1; ++p) {
+      const uint32_t e = tab_col(T, p);
+      XT* xs = x + KIN_NU_INDEX(e) * B;
+      if constexpr (sizeof(XT) == 8) {
+        const double v = __dadd_rn(*xs, static_cast<double>(KIN_NU_DELTA(e)));
+        neg |= v < 0.0;
+        *xs = v;
+      } else {
+        const long long v = static_cast<long long>(*xs) + KIN_NU_DELTA(e);
+        ovf |= v > 2147483647LL;
+        neg |= v < 0;
+        *xs = static_cast<XT>(v);
+      }
+    }
+    return neg;
   }
 };
 
-template <bool kCount, bool kPhilox>
+template <bool kCount, bool kPhilox, class XT>
 __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
-                                             uint64_t s, double* x, double* a, double* av, int B) {
+                                             uint64_t s, XT* x, double* a, double* av, int B, int* ovf_flag) {
   const uint64_t sim = S.sim_begin + s;
   const int N = T.n, M = T.m, G = T.n_grid;
   const uint64_t nloc = S.n_local;
@@ -101,11 +133,14 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
       rem = q;
     }
   }
+  bool ovf = false;
   for (int i = 0; i < N; ++i) {
     const int ax = tab_x0_axis(T, i);
-    x[i * B] = ax < 0 ? tab_x0(T, i) : av[ax * B];
+    const double v = ax < 0 ? tab_x0(T, i) : av[ax * B];
+    if (sizeof(XT) != 8) ovf |= v > 2147483647.0;
+    x[i * B] = static_cast<XT>(v);
   }
-  const Sim sm{T, x, a, av, B};
+  const Sim<XT> sm{T, x, a, av, B};
 
   const uint64_t seed = sim_seed(S, sim);
   Xoshiro rng;
@@ -123,7 +158,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
 
   auto emit = [&]() {
     double* o = O.traj + static_cast<size_t>(gi) * N * nloc + s;
-    for (int i = 0; i < N; ++i) o[static_cast<size_t>(i) * nloc] = x[i * B];
+    for (int i = 0; i < N; ++i) o[static_cast<size_t>(i) * nloc] = sm.xv(i);
     ++gi;
   };
 
@@ -131,7 +166,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   bool a_valid = false;
   double a0 = 0.0;
 
-  while (t < t_end) {
+  while (t < t_end && !ovf) {
     if (++used > budget) { status = KIN_SIM_BUDGET; break; }
     if (!a_valid) a0 = sm.all_props(M);
     a_valid = false;
@@ -160,7 +195,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         if (kCount) flops += 4 * static_cast<uint64_t>(p1 - p0);
         if (mu == 0.0 && s2 == 0.0) continue;
         // (eps*x)/g with g in {1,2,3}: /1 and /2 are exact scalings
-        const double ex = __dmul_rn(eps, x[i * B]);
+        const double ex = __dmul_rn(eps, sm.xv(i));
         const double g = tab_g(T, i);
         double bound = g == 1.0 ? ex : (g == 2.0 ? __dmul_rn(ex, 0.5) : __ddiv_rn(ex, g));
         if (bound < 1.0) bound = 1.0;
@@ -229,15 +264,8 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         if (kCount) flops += 1 + static_cast<uint64_t>(sel + 1);
         const int p1 = tab_col_ptr(T, sel + 1);
         const int p0 = tab_col_ptr(T, sel);
-        bool neg = false;
-        for (int p = p0; p < p1; ++p) {
-          const uint32_t e = tab_col(T, p);
-          double* xs = x + KIN_NU_INDEX(e) * B;
-          const double v = __dadd_rn(*xs, static_cast<double>(KIN_NU_DELTA(e)));
-          neg |= v < 0.0;
-          *xs = v;
-        }
-        if (neg) { status = KIN_SIM_NEGATIVE; stop = true; break; }
+        if (sm.fire(sel, ovf)) { status = KIN_SIM_NEGATIVE; stop = true; break; }
+        if (ovf) { stop = true; break; }
         if (kCount) flops += static_cast<uint64_t>(p1 - p0);
         t = tn;
         if (kind == 0) ++n_steps; else ++n_ssa;
@@ -272,11 +300,12 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         } else {
           k = poisson<kCount>(rng, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
         }
-        if (k != 0) sm.apply(j, static_cast<double>(k));
+        if (k != 0) sm.apply(j, static_cast<long long>(k), ovf);
       }
       if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
+      if (ovf) break;
       bool neg = false;
-      for (int i = 0; i < N; ++i) neg |= x[i * B] < 0.0;
+      for (int i = 0; i < N; ++i) neg |= x[i * B] < static_cast<XT>(0);
       if (!neg) {
         ++ev;
         break;
@@ -290,7 +319,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         } else {
           k = poisson<false>(saved, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
         }
-        if (k != 0) sm.apply(j, -static_cast<double>(k));
+        if (k != 0) sm.apply(j, -static_cast<long long>(k), ovf);
       }
       ++ev;
       saved = rng;
@@ -299,6 +328,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
       hit = false;
       if (kCount) flops += 1;
     }
+    if (ovf) break;
     if (hit) {
       t = t_stop;
     } else {
@@ -307,6 +337,10 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     }
     ++n_steps;
     while (gi < G && tab_grid(T, S, gi) <= t) emit();
+  }
+  if (ovf) {
+    status = KIN_SIM_INTERNAL_RETRY;
+    atomicExch(ovf_flag, 1);
   }
   if (status == 0)
     while (gi < G) emit();
@@ -322,40 +356,39 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   if (kCount && O.work) O.work[s] = flops;
 }
 
-template <bool kCount, bool kPhilox>
+template <bool kCount, bool kPhilox, class XT>
 __global__ void __launch_bounds__(kBlock) stochastic_kernel(const __grid_constant__ KinTables T,
                                                             const __grid_constant__ KinSweepDev S, KinOutDev O,
-                                                            unsigned long long* __restrict__ next) {
+                                                            unsigned long long* __restrict__ next, int* ovf_flag) {
   extern __shared__ double smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
-  double* x = smem + tid;
-  double* a = smem + static_cast<size_t>(T.n) * B + tid;
-  double* av = smem + static_cast<size_t>(T.n + T.m) * B + tid;
+  double* a = smem + tid;
+  double* av = smem + static_cast<size_t>(T.m) * B + tid;
+  XT* x = reinterpret_cast<XT*>(smem + static_cast<size_t>(T.m + S.n_axes) * B) + tid;
   for (;;) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(next, 32ULL);
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     if (base >= S.n_local) break;
     const uint64_t s = base + lane;
-    if (s < S.n_local) simulate_one<kCount, kPhilox>(T, S, O, s, x, a, av, B);
+    if (s < S.n_local) simulate_one<kCount, kPhilox, XT>(T, S, O, s, x, a, av, B, ovf_flag);
     __syncwarp();
   }
 }
 
-}  // namespace
-
-size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block) {
-  return static_cast<size_t>(T.n + T.m + S.n_axes) * block * sizeof(double);
+size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block, bool int_state) {
+  return static_cast<size_t>(T.m + S.n_axes) * block * sizeof(double) +
+         static_cast<size_t>(T.n) * block * (int_state ? sizeof(int32_t) : sizeof(double));
 }
 
-cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
-                              unsigned long long* counter, cudaStream_t stream) {
-  if (S.n_local == 0) return cudaSuccess;
-  const size_t smem = stochastic_smem_bytes(T, S, kBlock);
+template <class XT>
+cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
+                      unsigned long long* counter, int* ovf_flag, cudaStream_t stream) {
+  const size_t smem = stochastic_smem_bytes(T, S, kBlock, sizeof(XT) == 4);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   const bool ph = S.rng_mode == KIN_RNG_PHILOX;
-  auto kern = count ? (ph ? stochastic_kernel<true, true> : stochastic_kernel<true, false>)
-                    : (ph ? stochastic_kernel<false, true> : stochastic_kernel<false, false>);
+  auto kern = count ? (ph ? stochastic_kernel<true, true, XT> : stochastic_kernel<true, false, XT>)
+                    : (ph ? stochastic_kernel<false, true, XT> : stochastic_kernel<false, false, XT>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -369,8 +402,17 @@ cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const Ki
   const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter);
+  kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter, ovf_flag);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
+                              unsigned long long* counter, int* ovf_flag, bool int_state, cudaStream_t stream) {
+  if (S.n_local == 0) return cudaSuccess;
+  if (int_state) return launch_xt<int32_t>(T, S, O, count, counter, ovf_flag, stream);
+  return launch_xt<double>(T, S, O, count, counter, ovf_flag, stream);
 }
 
 }  // namespace kin

@@ -377,7 +377,6 @@ cudaError_t launch_stochastic_group(const KinTables& T, const KinSweepDev& S, co
                                     int lanes, unsigned long long* counter, cudaStream_t stream) {
   if (S.n_local == 0) return cudaSuccess;
   if (lanes <= 0) lanes = stochastic_group_pick_lanes(T.n, T.m);
-  if (lanes == 1) return launch_stochastic(T, S, O, count, counter, stream);
   switch (lanes) {
     case 4: return launch_L<4>(T, S, O, count, counter, stream);
     case 8: return launch_L<8>(T, S, O, count, counter, stream);

@@ -13,6 +13,9 @@
 #include <stdint.h>
 
 #define KIN_MAX_AXES 8
+// internal per-simulation status: an int32 amount would overflow; the engine
+// re-runs the launch with double amounts (never returned to callers)
+#define KIN_SIM_INTERNAL_RETRY 100
 #define KIN_TABLE_BYTES 30720  // < 32764-byte kernel parameter limit (sm_70+, CUDA >= 12.1)
 
 // packed entries

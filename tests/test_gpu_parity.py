@@ -147,6 +147,27 @@ def test_c5_random_network_bit_exact(engine, oracle):
     assert_bit_exact(ref, got)
 
 
+def test_int32_amount_overflow_retry(engine, oracle):
+    """Amounts are kept as int32 on the device when they start far inside the
+    range; a run that leaves it is transparently re-run with double amounts."""
+    from paper_1309_7695_b200.model import Parameter, Reaction, ReactionNetwork, Species
+    net = ReactionNetwork.create([Species("A", 1_000_000_000), Species("B", 5)], [Parameter("lam", 2e9)],
+                                 [Reaction("birth", {}, {0: 1}, 2e9, 0), Reaction("conv", {1: 1}, {0: 1}, 1.0)])
+    for kind in (MethodKind.TauAdaptive, MethodKind.TauFixed):
+        cfg = SweepConfig([SweepAxis("lam", [1e8, 2e9])], 8, Method(kind, tau=0.05), 3, 1.0, uniform_grid(1.0, 11))
+        ref, got = both(engine, oracle, net, cfg)
+        assert_bit_exact(ref, got)
+        assert got["traj"][:, -1, 0].max() > 2**31  # crossed the int32 range
+
+
+@pytest.mark.parametrize("int_state", ["0", "1"])
+def test_c4_double_and_int32_amounts_agree(engine, oracle, int_state, monkeypatch):
+    monkeypatch.setenv("KIN_INT_STATE", int_state)
+    net, cfg = W.c4_config()
+    ref, got = both(engine, oracle, net, cfg, sim_range=(7000, 7256), want_work=True)
+    assert_bit_exact(ref, got, work=True)
+
+
 def test_shard_invariance(engine):
     """Per-run output independent of how the index space is cut."""
     net, cfg = W.c1_config(MethodKind.TauAdaptive)
