@@ -17,8 +17,8 @@ Arms:
   ours       value = device-resident throughput (kin_sweep_launch: simulation +
              per-point statistics kernels; inputs already in HBM; CUDA events on
              the engine stream; L2 flushed between steps); e2e = kin_sweep_run
-             with host buffers (H2D of the sweep tables, D2H of the per-point
-             mean/m2 that parameter_sweep returns) timed on the host clock.
+             with host buffers (H2D of the sweep tables, D2H of every
+             simulation's time series + TrajectoryMeta + status) on the host clock.
   reference  the CPU oracle (C++ restatement of the reference path; the
              reference ships no simulator .cpp to compile) on all host threads,
              on a bounded strided sample of the same sweep, per step.
@@ -287,14 +287,17 @@ def bench_ours(args, world, rank, local):
     tau_avg_ms = float(np.mean(tau_ms))
     achieved = tau_flops / (tau_avg_ms / 1e3) / 1e12
 
-    # -- end to end through the public API (host buffers, D2H of what parameter_sweep returns)
+    # -- end to end through the public API: kin_sweep_run with host buffers,
+    # returning what the engine produces per simulation (Trajectory samples
+    # [S][G][N] in the reference layout, TrajectoryMeta, status) — the
+    # run_ensemble/RunSink output; H2D of the sweep tables inside the call.
     import torch as _t
     G, N = len(tau_cfg.grid), net.species_count()
-    mean_h = _t.empty((per, G, N), dtype=_t.float64, pin_memory=True).numpy()
-    m2_h = _t.empty((per, G, N), dtype=_t.float64, pin_memory=True).numpy()
+    traj_h = _t.empty((per, G, N), dtype=_t.float64, pin_memory=True).numpy()
+    meta_h = _t.empty((per, 6), dtype=_t.int64, pin_memory=True).numpy().view(np.uint64)
     st_h = _t.empty(per, dtype=_t.int32, pin_memory=True).numpy()
-    out = abi.KinSweepOut(None, None, abi.ptr(st_h, C.c_int32), abi.ptr(mean_h, C.c_double),
-                          abi.ptr(m2_h, C.c_double), None)
+    out = abi.KinSweepOut(abi.ptr(traj_h, C.c_double), abi.ptr(meta_h, C.c_uint64), abi.ptr(st_h, C.c_int32),
+                          None, None, None)
 
     def e2e_step():
         for d in (d_tau, d_ode):
@@ -311,7 +314,7 @@ def bench_ours(args, world, rank, local):
     e2e_value = sims_step * args.steps / t_e2e
     bytes_axes = sum(len(a.values) for a in tau_cfg.axes) * 8 + G * 8
     h2d = 2 * (bytes_axes + 31 * 1024)  # sweep tables + packed model tables, both methods
-    d2h = 2 * (2 * per * G * N * 8 + per * 4)
+    d2h = 2 * (per * G * N * 8 + per * 6 * 8 + per * 4)
 
     traffic, traffic_src = read_profile_traffic()
     res = {
@@ -320,7 +323,7 @@ def bench_ours(args, world, rank, local):
         "dtype": "f64", "data": "synthetic (deterministic generator, seed 0x5A5C)", "config": config_block(n),
         "impl": "ours",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "kin_sweep_run (parameter_sweep semantics: per-point mean+m2 to pinned host buffers)"},
+                "api": "kin_sweep_run -> per-simulation time series [S][G][N] + TrajectoryMeta + status into pinned host buffers (run_ensemble/RunSink output), both methods"},
         "gpu_launches": 4 * args.steps,
         "breakdown": {"tau_kernel_ms": tau_avg_ms, "step_ms": float(np.mean(step_ms)),
                       "tau_leaps_per_sim": float(meta[:, 0].mean()), "ssa_fallback_steps_per_sim": float(meta[:, 3].mean())},
