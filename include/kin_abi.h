@@ -25,8 +25,10 @@
 #ifndef KIN_ABI_H_
 #define KIN_ABI_H_
 
+#ifndef __CUDACC_RTC__
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -223,6 +225,12 @@ uint64_t kin_derive_run_seed(uint64_t master, uint64_t index);  /* ensemble.hpp:
    2 draw_normal, 3 draw_poisson(mean).  Results as raw 64-bit words. */
 int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
                          int32_t n, uint64_t* out_bits, kin_error* err);
+
+/* Diagnostic: generate and NVRTC-compile (sm_100a) the per-model specialised
+   stochastic kernel for this model + sweep binding, without a GPU.  log gets
+   the compiler output. */
+int kin_jit_check(const kin_model_desc* model, const kin_sweep_desc* sweep, char* log,
+                  int32_t log_cap, kin_error* err);
 
 /* Peak FP64 FMA throughput of device slot 0 (TFLOP/s, FMA = 2 flops), from a
    DFMA microbenchmark; used as the roofline denominator. */

@@ -86,7 +86,7 @@ ABI_SYMBOLS = (
     "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
     "kin_model_free", "kin_sweep_size", "kin_sweep_plan", "kin_sweep_run", "kin_sweep_launch", "kin_sweep_sync",
     "kin_sweep_fetch", "kin_ctx_stream", "kin_sweep_kernel_ms", "kin_splitmix64_mix", "kin_derive_run_seed",
-    "kin_device_rng_draws", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
+    "kin_device_rng_draws", "kin_jit_check", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
 )
 
 
@@ -110,6 +110,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "kin_splitmix64_mix": (C.c_uint64, [C.c_uint64]),
         "kin_derive_run_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
         "kin_device_rng_draws": (C.c_int, [vp, C.c_uint64, C.c_int32, C.c_double, C.c_int32, u64p, E]),
+        "kin_jit_check": (C.c_int, [C.POINTER(KinModelDesc), C.POINTER(KinSweepDesc), C.c_char_p, C.c_int32, E]),
         "kin_measure_fp64_peak": (C.c_int, [vp, f64p, E]),
         "kin_status_string": (C.c_char_p, [C.c_int32]),
         "kin_abi_version": (C.c_int32, []),

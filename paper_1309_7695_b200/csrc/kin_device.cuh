@@ -8,11 +8,14 @@
 // updates) is exact by construction.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#endif
 
 #include "kin_tables.h"
+#include "../../include/kin_abi.h"
 
 namespace kin {
 

@@ -29,6 +29,7 @@
 
 #include "../../include/kin_abi.h"
 #include "kin_device.cuh"
+#include "kin_jit.h"
 #include "kin_launch.h"
 #include "kin_tables.h"
 
@@ -424,7 +425,7 @@ struct Slot {
   std::unique_ptr<KinTables> last_T;
   KinSweepDev last_SD{};
   KinOutDev last_O{};
-  bool last_int_state = false, last_count = false, pending_check = false;
+  bool last_int_state = false, last_count = false, pending_check = false, last_jit = false;
   uint64_t last_base = 0, last_S = 0;
   int last_gn = 0;
   std::mutex mu;
@@ -499,6 +500,44 @@ int copy_d2h(Slot& sl, void* dst, const void* src, size_t bytes, kin_error* err)
   KIN_CUDA(cudaEventSynchronize(sl.ev[pending_b]), "D2H sync");
   std::memcpy(out + pending_off, buf[pending_b], pending_len);
   return KIN_OK;
+}
+
+// Model structure + sweep binding for the per-model JIT kernel.
+kin::JitModel jit_model(const HostModel& H, const kin_sweep_desc* d) {
+  kin::JitModel j;
+  j.n = H.n;
+  j.m = H.m;
+  j.rt_ptr = H.rt_ptr;
+  j.rt_species = H.rt_species;
+  j.rt_stoich = H.rt_stoich;
+  j.col_ptr = H.col_ptr;
+  j.col_species = H.col_species;
+  j.col_delta = H.col_delta;
+  j.row_ptr = H.row_ptr;
+  j.row_reaction = H.row_reaction;
+  j.row_delta = H.row_delta;
+  j.g.assign(H.g.begin(), H.g.end());
+  std::vector<int> param_axis(H.params.size(), -1);
+  for (int ax = 0; ax < d->n_axes; ++ax)
+    if (d->axes[ax].kind == KIN_AXIS_PARAM) param_axis[d->axes[ax].index] = ax;
+  j.rate_axis.assign(H.m, -1);
+  for (int r = 0; r < H.m; ++r)
+    if (H.rate_param[r] >= 0) j.rate_axis[r] = param_axis[H.rate_param[r]];
+  // dependency graph (same construction as pack_tables)
+  std::vector<std::vector<int>> by_species(H.n);
+  for (int k = 0; k < H.m; ++k)
+    for (int p = H.rt_ptr[k]; p < H.rt_ptr[k + 1]; ++p) by_species[H.rt_species[p]].push_back(k);
+  std::vector<char> mark(H.m);
+  j.dep_ptr.push_back(0);
+  for (int r = 0; r < H.m; ++r) {
+    std::fill(mark.begin(), mark.end(), 0);
+    for (int p = H.col_ptr[r]; p < H.col_ptr[r + 1]; ++p)
+      for (int k : by_species[H.col_species[p]]) mark[k] = 1;
+    for (int k = 0; k < H.m; ++k)
+      if (mark[k]) j.dep.push_back(k);
+    j.dep_ptr.push_back(static_cast<int>(j.dep.size()));
+  }
+  return j;
 }
 
 // Launch the simulation kernels for global sims [s0, s1) on a slot (device-resident).
@@ -589,7 +628,15 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
       bool int_state = xmax < 1073741824.0;
       if (const char* v = std::getenv("KIN_INT_STATE")) int_state = int_state && std::atoi(v) != 0;
       KIN_CUDA(cudaMemsetAsync(sl.ovf.p, 0, sizeof(int), sl.stream), "memset");
-      e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.ovf.p, int_state, sl.stream);
+      bool used = false;
+      e = cudaSuccess;
+      if (kin::jit_wanted(S)) {
+        const kin::JitModel jm = jit_model(H, d);
+        e = kin::launch_stochastic_jit(jm, *T, SD, O, want_work, sl.counter.p, sl.ovf.p, int_state, sl.stream, &used);
+      }
+      if (e == cudaSuccess && !used)
+        e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.ovf.p, int_state, sl.stream);
+      sl.last_jit = used;
       sl.last_int_state = int_state;
     }
     if (sl.last_int_state) {
@@ -928,6 +975,21 @@ int kin_sweep_fetch(kin_ctx* ctx, int32_t slot, kin_sweep_out* out, kin_error* e
   std::lock_guard<std::mutex> lk(sl.mu);
   if (!sl.valid) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
   return fetch_range(sl, out, sl.s0, sl.P0, err);
+}
+
+int kin_jit_check(const kin_model_desc* desc, const kin_sweep_desc* sweep, char* log, int32_t log_cap,
+                  kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  HostModel H;
+  std::string msg;
+  if (int rc = load_model(desc, &H, &msg)) { set_err(err, rc, msg); return rc; }
+  if (!sweep) { set_err(err, KIN_ERR_USAGE, "null sweep"); return KIN_ERR_USAGE; }
+  const kin::JitModel jm = jit_model(H, sweep);
+  std::string lg;
+  const bool ok = kin::jit_compile_check(jm, false, sweep->rng_mode == KIN_RNG_PHILOX, true, &lg);
+  if (log && log_cap > 0) std::snprintf(log, static_cast<size_t>(log_cap), "%s", lg.c_str());
+  if (!ok) { set_err(err, KIN_ERR_INPUT, "NVRTC compilation of the model kernel failed"); return KIN_ERR_INPUT; }
+  return KIN_OK;
 }
 
 int kin_sweep_kernel_ms(kin_ctx* ctx, int32_t slot, double* sim_ms, double* stats_ms, kin_error* err) {

@@ -1,0 +1,352 @@
+// kin_jit.cpp — per-model specialisation of the SSA / tau-leaping kernel.
+//
+// The table-driven kernel (kin_stochastic.cu) walks the model's packed tables
+// at run time: ~60% of its instructions (profiles/r1_v4_tau_lines.txt) decode
+// reaction descriptors, nu rows/columns and shared-memory addresses.  Here the
+// host generates, from the model's structure, a model policy whose
+// propensities, select_tau rows, state updates and dependency updates are
+// straight-line code with literal species/reaction indices, stoichiometries
+// and g_i (rate constants still come from the constant-bank tables, so one
+// compiled kernel serves every sweep point).  The policy plugs into the same
+// kernel body (kin_stochastic_impl.cuh) and performs the same floating-point
+// operations in the same order, so the results stay bit-identical to the
+// oracle.  Compiled once per (model structure, sweep-axis binding, variant)
+// with NVRTC for sm_100a (-fmad=false) and cached for the process.
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/kin_abi.h"
+#include "kin_jit.h"
+
+namespace kin {
+
+namespace {
+
+#include "build/kin_jit_sources.inc"  // kJitHeaders[] = {name, text}
+
+struct JitKernel {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  bool ok = false;
+  std::string log;
+};
+
+std::mutex g_mu;
+std::map<std::string, std::shared_ptr<JitKernel>> g_cache;
+
+bool jit_debug() {
+  static const bool d = std::getenv("KIN_JIT_DEBUG") != nullptr;
+  return d;
+}
+
+std::string dlit(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%.17g", v);
+  std::string s(b);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+  return s;
+}
+
+// Model policy source for one model structure (see kin_stochastic_impl.cuh
+// TableModel for the reference semantics of each member).
+std::string generate_policy(const JitModel& m) {
+  std::ostringstream o;
+  o << "namespace kin { namespace stoch {\n"
+       "template <class XT> struct GenModel {\n"
+       "  const KinTables& T; XT* x; double* a; const double* av;\n"
+       "  static constexpr int B = kBlock;\n"
+    << "  __device__ __forceinline__ int n() const { return " << m.n << "; }\n"
+    << "  __device__ __forceinline__ int m() const { return " << m.m << "; }\n"
+       "  __device__ __forceinline__ double xv(int i) const { return static_cast<double>(x[i * B]); }\n"
+       "  __device__ __forceinline__ double aval(int j) const { return a[j * B]; }\n"
+       "  __device__ __forceinline__ void upd(int i, int d, long long k, bool& ovf) const {\n"
+       "    XT* xs = x + i * B;\n"
+       "    if constexpr (sizeof(XT) == 8) {\n"
+       "      *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(d), static_cast<double>(k)));\n"
+       "    } else {\n"
+       "      const long long v = static_cast<long long>(*xs) + static_cast<long long>(d) * k;\n"
+       "      ovf |= v > 2147483647LL || v < -2147483647LL;\n"
+       "      *xs = static_cast<XT>(v);\n"
+       "    }\n"
+       "  }\n"
+       "  __device__ __forceinline__ bool upd1(int i, int d, bool& ovf) const {\n"
+       "    XT* xs = x + i * B;\n"
+       "    if constexpr (sizeof(XT) == 8) {\n"
+       "      const double v = __dadd_rn(*xs, static_cast<double>(d));\n"
+       "      *xs = v;\n"
+       "      return v < 0.0;\n"
+       "    } else {\n"
+       "      const long long v = static_cast<long long>(*xs) + d;\n"
+       "      ovf |= v > 2147483647LL;\n"
+       "      *xs = static_cast<XT>(v);\n"
+       "      return v < 0;\n"
+       "    }\n"
+       "  }\n";
+  // propensity of reaction j (model.hpp:151-157, oracle order)
+  o << "  __device__ __forceinline__ double prop(const int j) const {\n    double aj;\n    switch (j) {\n";
+  for (int j = 0; j < m.m; ++j) {
+    o << "      case " << j << ": aj = ";
+    if (m.rate_axis[j] >= 0) o << "av[" << m.rate_axis[j] << " * B]";
+    else o << "tab_rate(T, " << j << ")";
+    o << ";";
+    for (int p = m.rt_ptr[j]; p < m.rt_ptr[j + 1]; ++p)
+      o << " aj = __dmul_rn(aj, combinations(xv(" << m.rt_species[p] << "), " << m.rt_stoich[p] << "));";
+    o << " return aj;\n";
+  }
+  o << "    }\n    return 0.0;\n  }\n";
+  o << "  __device__ __forceinline__ double all_props(int) const {\n    double a0 = 0.0, aj;\n";
+  for (int j = 0; j < m.m; ++j)
+    o << "    aj = prop(" << j << "); a[" << j << " * B] = aj; a0 = __dadd_rn(a0, aj);\n";
+  o << "    return a0;\n  }\n";
+  o << "  __device__ __forceinline__ double sum_props(int) const {\n    double a0 = 0.0;\n";
+  for (int j = 0; j < m.m; ++j) o << "    a0 = __dadd_rn(a0, a[" << j << " * B]);\n";
+  o << "    return a0;\n  }\n";
+  // select_tau (stochastic.hpp:40-44): per species, its nu row in reaction order
+  o << "  template <bool kCount> __device__ __forceinline__ double select_tau(double eps, uint64_t& flops) const {\n"
+       "    double tau = KIN_INF;\n";
+  for (int i = 0; i < m.n; ++i) {
+    const int p0 = m.row_ptr[i], p1 = m.row_ptr[i + 1];
+    if (p0 == p1) {
+      continue;  // mu = sigma2 = 0 exactly: skipped by the reference too
+    }
+    o << "    { double mu = 0.0, s2 = 0.0;";
+    for (int p = p0; p < p1; ++p) {
+      const int j = m.row_reaction[p], d = m.row_delta[p];
+      o << " mu = __dadd_rn(mu, __dmul_rn(" << dlit(d) << ", a[" << j << " * B]));"
+        << " s2 = __dadd_rn(s2, __dmul_rn(" << dlit(static_cast<double>(d) * d) << ", a[" << j << " * B]));";
+    }
+    o << "\n      if (kCount) flops += " << 4 * (p1 - p0) << ";\n"
+      << "      if (!(mu == 0.0 && s2 == 0.0)) tau = tau_bound<kCount>(tau, eps, xv(" << i << "), " << dlit(m.g[i])
+      << ", mu, s2, flops); }\n";
+  }
+  o << "    return tau;\n  }\n";
+  // state updates
+  o << "  __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const {\n    switch (j) {\n";
+  for (int j = 0; j < m.m; ++j) {
+    o << "      case " << j << ":";
+    for (int p = m.col_ptr[j]; p < m.col_ptr[j + 1]; ++p)
+      o << " upd(" << m.col_species[p] << ", " << m.col_delta[p] << ", k, ovf);";
+    o << " break;\n";
+  }
+  o << "    }\n  }\n";
+  o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const {\n    bool neg = false;\n    switch (j) {\n";
+  for (int j = 0; j < m.m; ++j) {
+    o << "      case " << j << ":";
+    for (int p = m.col_ptr[j]; p < m.col_ptr[j + 1]; ++p)
+      o << " neg |= upd1(" << m.col_species[p] << ", " << m.col_delta[p] << ", ovf);";
+    o << " break;\n";
+  }
+  o << "    }\n    return neg;\n  }\n";
+  o << "  __device__ __forceinline__ void dep_update(int sel) const {\n    switch (sel) {\n";
+  for (int j = 0; j < m.m; ++j) {
+    o << "      case " << j << ":";
+    for (int q = m.dep_ptr[j]; q < m.dep_ptr[j + 1]; ++q)
+      o << " a[" << m.dep[q] << " * B] = prop(" << m.dep[q] << ");";
+    o << " break;\n";
+  }
+  o << "    }\n  }\n";
+  o << "  __device__ __forceinline__ bool any_negative() const {\n    bool neg = false;\n"
+    << "#pragma unroll\n    for (int i = 0; i < " << m.n << "; ++i) neg |= x[i * B] < static_cast<XT>(0);\n"
+    << "    return neg;\n  }\n";
+  o << "  __device__ __forceinline__ int col_len(int j) const { return tab_col_ptr(T, j + 1) - tab_col_ptr(T, j); }\n";
+  o << "};\n}}  // namespace kin::stoch\n";
+  return o.str();
+}
+
+// NVRTC: policy source -> sm_100a cubin.  Returns false with the log on error.
+bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_state, std::vector<char>* cubin,
+                   std::string* log) {
+  std::string src = "#include \"kin_stochastic_impl.cuh\"\n" + policy +
+                    "extern \"C\" __global__ void __launch_bounds__(32) kin_jit_stoch(\n"
+                    "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
+                    "    unsigned long long* __restrict__ next, int* ovf) {\n"
+                    "  kin::stoch::stochastic_body<kin::stoch::GenModel<XT_>, KCOUNT_, KPHILOX_, XT_>(T, S, O, next, ovf);\n"
+                    "}\n";
+  std::vector<const char*> hs, hn;
+  for (const auto& h : kJitHeaders) {
+    hn.push_back(h.name);
+    hs.push_back(h.text);
+  }
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "kin_jit_stoch.cu", static_cast<int>(hs.size()), hs.data(), hn.data()) !=
+      NVRTC_SUCCESS) {
+    *log = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const std::string d_xt = std::string("-DXT_=") + (int_state ? "int" : "double");
+  const std::string d_c = std::string("-DKCOUNT_=") + (count ? "true" : "false");
+  const std::string d_p = std::string("-DKPHILOX_=") + (philox ? "true" : "false");
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo",
+                        "-default-device",             d_xt.c_str(), d_c.c_str(), d_p.c_str()};
+  const nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
+  size_t log_size = 0;
+  nvrtcGetProgramLogSize(prog, &log_size);
+  if (log_size > 1) {
+    log->resize(log_size);
+    nvrtcGetProgramLog(prog, &(*log)[0]);
+  }
+  if (rc != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return false;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin->resize(n);
+  nvrtcGetCUBIN(prog, cubin->data());
+  nvrtcDestroyProgram(&prog);
+  return true;
+}
+
+// On-disk cubin cache (optimisation only): $KIN_JIT_CACHE, else
+// $HOME/.cache/kin_b200_jit; keyed by a hash of the full source + variant.
+std::string cache_path(const std::string& key) {
+  const char* dir = std::getenv("KIN_JIT_CACHE");
+  std::string d;
+  if (dir && *dir) {
+    d = dir;
+  } else {
+    const char* home = std::getenv("HOME");
+    if (!home) return "";
+    d = std::string(home) + "/.cache/kin_b200_jit";
+  }
+  std::string full = key;
+  for (const auto& h : kJitHeaders) full += h.text;
+  uint64_t hsh = 1469598103934665603ULL;  // FNV-1a 64
+  for (unsigned char c : full) hsh = (hsh ^ c) * 1099511628211ULL;
+  char name[64];
+  std::snprintf(name, sizeof name, "/%016llx.cubin", static_cast<unsigned long long>(hsh));
+  return d + name;
+}
+
+bool read_file(const std::string& p, std::vector<char>* out) {
+  if (p.empty()) return false;
+  FILE* f = std::fopen(p.c_str(), "rb");
+  if (!f) return false;
+  std::fseek(f, 0, SEEK_END);
+  const long n = std::ftell(f);
+  std::fseek(f, 0, SEEK_SET);
+  out->resize(n > 0 ? static_cast<size_t>(n) : 0);
+  const bool ok = n > 0 && std::fread(out->data(), 1, out->size(), f) == out->size();
+  std::fclose(f);
+  return ok;
+}
+
+void write_file(const std::string& p, const std::vector<char>& data) {
+  if (p.empty()) return;
+  const std::string dir = p.substr(0, p.rfind('/'));
+  std::string cmd_dir;
+  for (size_t i = 1; i <= dir.size(); ++i)  // mkdir -p
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+  const std::string tmp = p + ".tmp" + std::to_string(getpid());
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  const bool ok = std::fwrite(data.data(), 1, data.size(), f) == data.size();
+  std::fclose(f);
+  if (ok) std::rename(tmp.c_str(), p.c_str());
+  else std::remove(tmp.c_str());
+}
+
+std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool philox, bool int_state) {
+  auto jk = std::make_shared<JitKernel>();
+  std::vector<char> cubin;
+  const std::string path =
+      cache_path(policy + (count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D"));
+  if (!read_file(path, &cubin)) {
+    if (!nvrtc_compile(policy, count, philox, int_state, &cubin, &jk->log)) {
+      if (jit_debug()) std::fprintf(stderr, "[kin_jit] compile failed:\n%s\n", jk->log.c_str());
+      return jk;
+    }
+    write_file(path, cubin);
+  }
+  if (cudaLibraryLoadData(&jk->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
+      cudaLibraryGetKernel(&jk->kern, jk->lib, "kin_jit_stoch") != cudaSuccess) {
+    jk->log += "\ncudaLibraryLoadData/GetKernel failed";
+    cudaGetLastError();
+    return jk;
+  }
+  jk->ok = true;
+  if (jit_debug())
+    std::fprintf(stderr, "[kin_jit] compiled %zu-byte policy (%zu-byte cubin)\n", policy.size(), cubin.size());
+  return jk;
+}
+
+}  // namespace
+
+bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log) {
+  std::vector<char> cubin;
+  return nvrtc_compile(generate_policy(model), count, philox, int_state, &cubin, log);
+}
+
+// KIN_JIT=0: never; KIN_JIT=1: always; unset: launches of >= 8,192
+// simulations (where the one-time NVRTC compilation, ~10 s per variant, cached
+// in memory and on disk, is amortised).
+bool jit_wanted(uint64_t n_sims) {
+  const char* v = std::getenv("KIN_JIT");
+  if (v && *v) return std::atoi(v) != 0;
+  return n_sims >= 8192;
+}
+
+cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S,
+                                  const KinOutDev& O, bool count, unsigned long long* counter, int* ovf_flag,
+                                  bool int_state, cudaStream_t stream, bool* used) {
+  *used = false;
+  if (S.n_local == 0) {
+    *used = true;
+    return cudaSuccess;
+  }
+  const bool philox = S.rng_mode == KIN_RNG_PHILOX;
+  const std::string policy = generate_policy(model);
+  const std::string key = policy + (count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D");
+  std::shared_ptr<JitKernel> jk;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+      jk = it->second;
+    } else {
+      jk = compile(policy, count, philox, int_state);
+      g_cache[key] = jk;
+    }
+  }
+  if (!jk->ok) return cudaSuccess;  // caller falls back to the table-driven kernel
+  const size_t smem = static_cast<size_t>(T.m + S.n_axes) * 32 * sizeof(double) +
+                      static_cast<size_t>(T.n) * 32 * (int_state ? sizeof(int32_t) : sizeof(double));
+  if (smem > 227 * 1024) return cudaSuccess;
+  const void* fn = reinterpret_cast<const void*>(jk->kern);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaSuccess;
+  const uint64_t warps = (S.n_local + 31) / 32;
+  const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  KinTables* Tp = const_cast<KinTables*>(&T);
+  KinSweepDev* Sp = const_cast<KinSweepDev*>(&S);
+  KinOutDev Oc = O;
+  void* args[] = {Tp, Sp, &Oc, &counter, &ovf_flag};
+  e = cudaLaunchKernel(fn, dim3(grid), dim3(32), args, smem, stream);
+  if (e == cudaSuccess) *used = true;
+  return e;
+}
+
+}  // namespace kin

@@ -1,0 +1,35 @@
+// kin_jit.h — per-model specialised stochastic kernels (kin_jit.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "kin_tables.h"
+
+namespace kin {
+
+// Model structure the generated policy is specialised on (no rate values).
+struct JitModel {
+  int n = 0, m = 0;
+  std::vector<int> rt_ptr, rt_species, rt_stoich;    // reactants per reaction (species-ascending)
+  std::vector<int> rate_axis;                        // -1, or the sweep axis carrying c_j
+  std::vector<int> col_ptr, col_species, col_delta;  // nu columns
+  std::vector<int> row_ptr, row_reaction, row_delta; // nu rows
+  std::vector<int> dep_ptr, dep;                     // propensity dependency graph
+  std::vector<double> g;                             // highest reactant order per species
+};
+
+bool jit_wanted(uint64_t n_sims);  // KIN_JIT=0/1 overrides the size policy
+
+// Generate + NVRTC-compile the policy without loading it (no GPU needed).
+bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log);
+
+// Launch the specialised kernel; *used = false means "not available" (NVRTC
+// failure or unsupported configuration): the caller launches the table kernel.
+cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S,
+                                  const KinOutDev& O, bool count, unsigned long long* counter, int* ovf_flag,
+                                  bool int_state, cudaStream_t stream, bool* used);
+
+}  // namespace kin

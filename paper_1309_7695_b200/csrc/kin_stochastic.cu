@@ -23,357 +23,22 @@
 //   ssa_step fallback (bursts of 100) ...... stochastic.hpp:22-26
 //   simulate_ssa grid semantics ............ stochastic.hpp:34-38
 // Compiled with -fmad=false (see Makefile): no contraction on the parity path.
-#include "kin_device.cuh"
 #include "kin_launch.h"
+#include "kin_stochastic_impl.cuh"
 
 namespace kin {
 
 namespace {
 
-constexpr double kInf = __builtin_huge_val();
-constexpr int kBlock = 32;  // one warp per block: finest smem granularity
-
-// Amounts are exact integers.  XT = double (any magnitude below 2^53, the
-// reference's SystemState) or int32_t (half the shared memory, so more resident
-// simulations; an update leaving int32 range raises *ovf and the engine re-runs
-// the launch with the double variant — results are identical either way).
-template <class XT>
-struct Sim {
-  const KinTables& T;
-  XT* x;             // x[i * B]
-  double* a;         // a[j * B]
-  const double* av;  // axis values av[ax * B]
-  int B;
-
-  __device__ __forceinline__ double xv(int i) const { return static_cast<double>(x[i * B]); }
-  // a_j(x) = c_j * prod h(x_s, stoich_s)   (model.hpp:151-157)
-  __device__ __forceinline__ double prop(int j) const {
-    const uint64_t d = tab_rdesc(T, j);
-    const int ax = KIN_RD_AXIS(d);
-    double aj = ax < 0 ? tab_rate(T, j) : av[ax * B];
-    const int nt = KIN_RD_NTERMS(d);
-    if (nt > 0) {
-      aj = __dmul_rn(aj, combinations(xv(KIN_RD_SPECIES(d, 0)), KIN_RD_STOICH(d, 0)));
-      if (nt > 1) {
-        aj = __dmul_rn(aj, combinations(xv(KIN_RD_SPECIES(d, 1)), KIN_RD_STOICH(d, 1)));
-        if (nt > 2) aj = __dmul_rn(aj, combinations(xv(KIN_RD_SPECIES(d, 2)), KIN_RD_STOICH(d, 2)));
-      }
-    }
-    return aj;
-  }
-  // a_j as evaluated at the start of the decision (leaps update x in place,
-  // so the propensities must be the cached ones)
-  __device__ __forceinline__ double aval(int j) const { return a[j * B]; }
-  // all propensities; returns a0 summed in reaction order (oracle order)
-  __device__ __forceinline__ double all_props(int M) const {
-    double a0 = 0.0;
-    for (int j = 0; j < M; ++j) {
-      const double aj = prop(j);
-      a[j * B] = aj;
-      a0 = __dadd_rn(a0, aj);
-    }
-    return a0;
-  }
-  __device__ __forceinline__ double sum_props(int M) const {
-    double a0 = 0.0;
-    for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, aval(j));
-    return a0;
-  }
-  // x += nu[:, j] * k  (k signed: negative undoes a rejected leap)
-  __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const {
-    const int p1 = tab_col_ptr(T, j + 1);
-    for (int p = tab_col_ptr(T, j); p < p1; ++p) {
-      const uint32_t e = tab_col(T, p);
-      XT* xs = x + KIN_NU_INDEX(e) * B;
-      if constexpr (sizeof(XT) == 8) {
-        *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), static_cast<double>(k)));
-      } else {
-        const long long v = static_cast<long long>(*xs) + static_cast<long long>(KIN_NU_DELTA(e)) * k;
-        ovf |= v > 2147483647LL || v < -2147483647LL;
-        *xs = static_cast<XT>(v);
-      }
-    }
-  }
-  // one SSA event: x += nu[:, j]; returns true if an amount went negative
-  __device__ __forceinline__ bool fire(int j, bool& ovf) const {
-    bool neg = false;
-    const int p1 = tab_col_ptr(T, j + 1);
-    for (int p = tab_col_ptr(T, j); p < p1; ++p) {
-      const uint32_t e = tab_col(T, p);
-      XT* xs = x + KIN_NU_INDEX(e) * B;
-      if constexpr (sizeof(XT) == 8) {
-        const double v = __dadd_rn(*xs, static_cast<double>(KIN_NU_DELTA(e)));
-        neg |= v < 0.0;
-        *xs = v;
-      } else {
-        const long long v = static_cast<long long>(*xs) + KIN_NU_DELTA(e);
-        ovf |= v > 2147483647LL;
-        neg |= v < 0;
-        *xs = static_cast<XT>(v);
-      }
-    }
-    return neg;
-  }
-};
+using stoch::kBlock;
+using stoch::TableModel;
 
 template <bool kCount, bool kPhilox, class XT>
-__device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
-                                             uint64_t s, XT* x, double* a, double* av, int B, int* ovf_flag) {
-  const uint64_t sim = S.sim_begin + s;
-  const int N = T.n, M = T.m, G = T.n_grid;
-  const uint64_t nloc = S.n_local;
-
-  // Cartesian decode, last axis fastest.
-  {
-    uint64_t rem = sim / S.runs;
-    for (int ax = S.n_axes - 1; ax >= 0; --ax) {
-      const uint64_t nv = static_cast<uint64_t>(S.axis_n[ax]);
-      const uint64_t q = rem / nv;
-      av[ax * B] = __ldg(S.axis_values[ax] + (rem - q * nv));
-      rem = q;
-    }
-  }
-  bool ovf = false;
-  for (int i = 0; i < N; ++i) {
-    const int ax = tab_x0_axis(T, i);
-    const double v = ax < 0 ? tab_x0(T, i) : av[ax * B];
-    if (sizeof(XT) != 8) ovf |= v > 2147483647.0;
-    x[i * B] = static_cast<XT>(v);
-  }
-  const Sim<XT> sm{T, x, a, av, B};
-
-  const uint64_t seed = sim_seed(S, sim);
-  Xoshiro rng;
-  if (!kPhilox) rng.seed(seed);
-  uint64_t ev = 0;  // Philox event counter (leap attempts and SSA events)
-  const int kind = S.kind;
-  const double t_end = S.t_end;
-  double t = 0.0;
-  int gi = 0;
-  uint64_t flops = 0, used = 0, dummy = 0;
-  uint64_t n_steps = 0, n_rej = 0, n_ssa = 0;
-  int status = 0;
-  const uint64_t budget = S.max_steps;
-  const uint64_t F_prop = static_cast<uint64_t>(T.fprop);
-
-  auto emit = [&]() {
-    double* o = O.traj + static_cast<size_t>(gi) * N * nloc + s;
-    for (int i = 0; i < N; ++i) o[static_cast<size_t>(i) * nloc] = sm.xv(i);
-    ++gi;
-  };
-
-  while (gi < G && tab_grid(T, S, gi) <= t) emit();
-  bool a_valid = false;
-  double a0 = 0.0;
-
-  while (t < t_end && !ovf) {
-    if (++used > budget) { status = KIN_SIM_BUDGET; break; }
-    if (!a_valid) a0 = sm.all_props(M);
-    a_valid = false;
-    if (kCount) flops += F_prop + M;
-    if (a0 == 0.0) break;
-
-    double tau = 0.0;
-    bool burst = false;
-    if (kind == 0) {
-      burst = true;
-    } else if (kind == 1) {
-      // select_tau, header form (stochastic.hpp:40-44)
-      tau = kInf;
-      const double eps = S.epsilon;
-      for (int i = 0; i < N; ++i) {
-        double mu = 0.0, s2 = 0.0;
-        const int p1 = tab_row_ptr(T, i + 1);
-        const int p0 = tab_row_ptr(T, i);
-        for (int p = p0; p < p1; ++p) {
-          const uint32_t e = tab_row(T, p);
-          const int dl = KIN_NU_DELTA(e);
-          const double aj = sm.aval(KIN_NU_INDEX(e));
-          mu = __dadd_rn(mu, __dmul_rn(static_cast<double>(dl), aj));
-          s2 = __dadd_rn(s2, __dmul_rn(static_cast<double>(dl * dl), aj));
-        }
-        if (kCount) flops += 4 * static_cast<uint64_t>(p1 - p0);
-        if (mu == 0.0 && s2 == 0.0) continue;
-        // (eps*x)/g with g in {1,2,3}: /1 and /2 are exact scalings
-        const double ex = __dmul_rn(eps, sm.xv(i));
-        const double g = tab_g(T, i);
-        double bound = g == 1.0 ? ex : (g == 2.0 ? __dmul_rn(ex, 0.5) : __ddiv_rn(ex, g));
-        if (bound < 1.0) bound = 1.0;
-        if (kCount) flops += 2;
-        // A quotient q = num/den can only lower tau if num <= tau*den (up to
-        // rounding).  fl(tau*den) errs by <= 2^-53 relative, so num >
-        // fl(tau*den)*(1 + 2^-50) proves q > tau, hence fl(q) >= tau and the
-        // (exact, same-as-oracle) division can be skipped.
-        if (mu != 0.0) {
-          const double amu = fabs(mu);
-          if (!(bound > __dmul_rn(__dmul_rn(tau, amu), 1.0 + 0x1p-50))) {
-            const double t1 = __ddiv_rn(bound, amu);
-            if (t1 < tau) tau = t1;
-          }
-          if (kCount) flops += 1;
-        }
-        if (s2 != 0.0) {
-          const double bb = __dmul_rn(bound, bound);
-          if (!(bb > __dmul_rn(__dmul_rn(tau, s2), 1.0 + 0x1p-50))) {
-            const double t2 = __ddiv_rn(bb, s2);
-            if (t2 < tau) tau = t2;
-          }
-          if (kCount) flops += 2;
-        }
-      }
-      if (kCount) flops += 1;
-      burst = tau < __ddiv_rn(10.0, a0);
-    } else {
-      tau = S.tau;
-    }
-
-    if (burst) {
-      bool stop = false;
-      for (int b = 0;; ++b) {
-        if (b > 0) {
-          if (kind != 0 && b >= 100) { a_valid = true; break; }
-          if (++used > budget) { status = KIN_SIM_BUDGET; stop = true; break; }
-          if (kCount) flops += F_prop + M;
-          if (a0 == 0.0) { stop = true; break; }
-        }
-        double u1, u2;
-        if (kPhilox) {
-          PhiloxSite src(seed, ev++, kPhiloxSsaSite);
-          u1 = src.uniform();
-          u2 = src.uniform();
-        } else {
-          u1 = rng.uniform();
-          u2 = rng.uniform();
-        }
-        const double dt = __ddiv_rn(log(__ddiv_rn(1.0, u1)), a0);
-        const double tn = __dadd_rn(t, dt);
-        if (kCount) flops += 8;
-        if (tn > t_end) { t = t_end; stop = true; break; }
-        while (gi < G && tab_grid(T, S, gi) < tn) emit();
-        // first j with cumulative propensity > u2*a0
-        const double target = __dmul_rn(u2, a0);
-        double c = 0.0;
-        int sel = -1, last = -1;
-        for (int j = 0; j < M; ++j) {
-          const double aj = sm.aval(j);
-          if (aj > 0.0) last = j;
-          c = __dadd_rn(c, aj);
-          if (c > target) { sel = j; break; }
-        }
-        if (sel < 0) sel = last;
-        if (kCount) flops += 1 + static_cast<uint64_t>(sel + 1);
-        const int p1 = tab_col_ptr(T, sel + 1);
-        const int p0 = tab_col_ptr(T, sel);
-        if (sm.fire(sel, ovf)) { status = KIN_SIM_NEGATIVE; stop = true; break; }
-        if (ovf) { stop = true; break; }
-        if (kCount) flops += static_cast<uint64_t>(p1 - p0);
-        t = tn;
-        if (kind == 0) ++n_steps; else ++n_ssa;
-        while (gi < G && tab_grid(T, S, gi) <= t) emit();
-        // re-evaluate the propensities that changed, then a0 in oracle order
-        {
-          const int q1 = tab_dep_ptr(T, sel + 1);
-          for (int q = tab_dep_ptr(T, sel); q < q1; ++q) {
-            const int k = tab_dep(T, q);
-            a[k * B] = sm.prop(k);
-          }
-        }
-        a0 = sm.sum_props(M);
-      }
-      if (stop) break;
-      continue;
-    }
-
-    // Poisson leap truncated at the next grid time; reject -> halve
-    const double t_stop = (gi < G && tab_grid(T, S, gi) < t_end) ? tab_grid(T, S, gi) : t_end;
-    bool hit = false;
-    const double gap = __dsub_rn(t_stop, t);
-    if (kCount) flops += 1;
-    if (!(tau < gap)) { tau = gap; hit = true; }
-    Xoshiro saved = rng;
-    for (;;) {
-      for (int j = 0; j < M; ++j) {
-        uint64_t k;
-        if (kPhilox) {
-          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
-          k = poisson<kCount>(src, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
-        } else {
-          k = poisson<kCount>(rng, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
-        }
-        if (k != 0) sm.apply(j, static_cast<long long>(k), ovf);
-      }
-      if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
-      if (ovf) break;
-      bool neg = false;
-      for (int i = 0; i < N; ++i) neg |= x[i * B] < static_cast<XT>(0);
-      if (!neg) {
-        ++ev;
-        break;
-      }
-      // rejected: undo exactly by replaying the same draws, continue the stream
-      for (int j = 0; j < M; ++j) {
-        uint64_t k;
-        if (kPhilox) {
-          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
-          k = poisson<false>(src, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
-        } else {
-          k = poisson<false>(saved, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
-        }
-        if (k != 0) sm.apply(j, -static_cast<long long>(k), ovf);
-      }
-      ++ev;
-      saved = rng;
-      ++n_rej;
-      tau = __dmul_rn(tau, 0.5);
-      hit = false;
-      if (kCount) flops += 1;
-    }
-    if (ovf) break;
-    if (hit) {
-      t = t_stop;
-    } else {
-      t = __dadd_rn(t, tau);
-      if (kCount) flops += 1;
-    }
-    ++n_steps;
-    while (gi < G && tab_grid(T, S, gi) <= t) emit();
-  }
-  if (ovf) {
-    status = KIN_SIM_INTERNAL_RETRY;
-    atomicExch(ovf_flag, 1);
-  }
-  if (status == 0)
-    while (gi < G) emit();
-
-  uint64_t* me = O.meta + s * 6;
-  me[0] = n_steps;
-  me[1] = n_rej;
-  me[2] = 0;
-  me[3] = n_ssa;
-  me[4] = 0;
-  me[5] = 0;
-  O.status[s] = status;
-  if (kCount && O.work) O.work[s] = flops;
-}
-
-template <bool kCount, bool kPhilox, class XT>
-__global__ void __launch_bounds__(kBlock) stochastic_kernel(const __grid_constant__ KinTables T,
-                                                            const __grid_constant__ KinSweepDev S, KinOutDev O,
-                                                            unsigned long long* __restrict__ next, int* ovf_flag) {
-  extern __shared__ double smem[];
-  const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
-  double* a = smem + tid;
-  double* av = smem + static_cast<size_t>(T.m) * B + tid;
-  XT* x = reinterpret_cast<XT*>(smem + static_cast<size_t>(T.m + S.n_axes) * B) + tid;
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(next, 32ULL);
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    if (base >= S.n_local) break;
-    const uint64_t s = base + lane;
-    if (s < S.n_local) simulate_one<kCount, kPhilox, XT>(T, S, O, s, x, a, av, B, ovf_flag);
-    __syncwarp();
-  }
+__global__ void __launch_bounds__(stoch::kBlock) stochastic_kernel(const __grid_constant__ KinTables T,
+                                                                   const __grid_constant__ KinSweepDev S, KinOutDev O,
+                                                                   unsigned long long* __restrict__ next,
+                                                                   int* ovf_flag) {
+  stoch::stochastic_body<TableModel<XT>, kCount, kPhilox, XT>(T, S, O, next, ovf_flag);
 }
 
 size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block, bool int_state) {

@@ -10,7 +10,19 @@
 // flight on different streams).
 #pragma once
 
+#ifdef __CUDACC_RTC__
+// NVRTC (per-model JIT kernels, kin_jit.cpp): no libc headers
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned short uint16_t;
+typedef short int16_t;
+typedef unsigned char uint8_t;
+typedef signed char int8_t;
+#else
 #include <stdint.h>
+#endif
 
 #define KIN_MAX_AXES 8
 // internal per-simulation status: an int32 amount would overflow; the engine

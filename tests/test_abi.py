@@ -71,3 +71,25 @@ def test_no_cpu_fallback_without_gpu():
 def test_missing_library_fails_loudly(tmp_path):
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         abi.load_library(tmp_path / "nope.so")
+
+
+@pytest.mark.parametrize("which", ["c1", "c2", "c4", "c5", "iso"])
+def test_jit_kernel_compiles_without_gpu(which):
+    """The per-model specialised kernel source is generated and compiled by
+    NVRTC for sm_100a (no GPU needed)."""
+    import time
+    from paper_1309_7695_b200 import workloads as W
+    from paper_1309_7695_b200.ensemble import Method, MethodKind, SweepAxis, SweepConfig, make_sweep_desc
+    if which == "iso":
+        net = W.isomerization()
+        cfg = SweepConfig([SweepAxis("kf", [1.0, 2.0])], 4, Method(MethodKind.Ssa), 1, 1.0, [0.0, 1.0])
+    else:
+        net, cfg = getattr(W, f"{which}_config")()
+    d, keep = make_sweep_desc(net, cfg)
+    lib = abi.load_library()
+    log = C.create_string_buffer(1 << 16)
+    err = abi.KinError()
+    t0 = time.time()
+    rc = lib.kin_jit_check(C.byref(net.desc()), C.byref(d), log, len(log), C.byref(err))
+    assert rc == 0, log.value.decode()[-2000:]
+    assert time.time() - t0 < 60

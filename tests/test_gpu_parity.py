@@ -168,6 +168,39 @@ def test_c4_double_and_int32_amounts_agree(engine, oracle, int_state, monkeypatc
     assert_bit_exact(ref, got, work=True)
 
 
+# ---- per-model JIT kernels (NVRTC, kin_jit.cpp): same results as the table kernel --
+@pytest.mark.parametrize("case", ["c4", "c4_double", "c4_philox", "c2", "c1_ssa", "taufixed", "overflow"])
+def test_jit_kernel_bit_exact(engine, oracle, case, monkeypatch):
+    monkeypatch.setenv("KIN_JIT", "1")
+    kw = dict(want_work=True)
+    if case.startswith("c4"):
+        net, cfg = W.c4_config()
+        kw["sim_range"] = (12000, 12512)
+        if case == "c4_double":
+            monkeypatch.setenv("KIN_INT_STATE", "0")
+        if case == "c4_philox":
+            monkeypatch.setenv("KIN_GROUP_LANES", "1")
+            kw["rng_mode"] = abi.RNG_PHILOX
+    elif case == "c2":
+        net, cfg = W.c2_config()
+        kw["sim_range"] = (256, 768)
+    elif case == "c1_ssa":
+        net, cfg = W.c1_config(MethodKind.Ssa, side=8)
+    elif case == "taufixed":
+        net = W.birth_death(x0=3)
+        cfg = SweepConfig([SweepAxis("lam", [0.5, 5.0, 50.0])], 128, Method(MethodKind.TauFixed, tau=0.5), 11, 10.0,
+                          uniform_grid(10.0, 21))
+    else:
+        from paper_1309_7695_b200.model import Parameter, Reaction, ReactionNetwork, Species
+        net = ReactionNetwork.create([Species("A", 1_000_000_000), Species("B", 5)], [Parameter("lam", 2e9)],
+                                     [Reaction("birth", {}, {0: 1}, 2e9, 0), Reaction("conv", {1: 1}, {0: 1}, 1.0)])
+        cfg = SweepConfig([SweepAxis("lam", [1e8, 2e9])], 8, Method(MethodKind.TauAdaptive), 3, 1.0,
+                          uniform_grid(1.0, 11))
+        kw = {}
+    ref, got = both(engine, oracle, net, cfg, **kw)
+    assert_bit_exact(ref, got, work=bool(kw.get("want_work")))
+
+
 def test_shard_invariance(engine):
     """Per-run output independent of how the index space is cut."""
     net, cfg = W.c1_config(MethodKind.TauAdaptive)
