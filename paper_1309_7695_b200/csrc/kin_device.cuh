@@ -179,6 +179,15 @@ __device__ __constant__ float c_rcp40[41] = {
     1.0f / 21, 1.0f / 22, 1.0f / 23, 1.0f / 24, 1.0f / 25, 1.0f / 26, 1.0f / 27, 1.0f / 28, 1.0f / 29, 1.0f / 30,
     1.0f / 31, 1.0f / 32, 1.0f / 33, 1.0f / 34, 1.0f / 35, 1.0f / 36, 1.0f / 37, 1.0f / 38, 1.0f / 39, 1.0f / 40};
 
+// lgamma(z) for z >= KIN_LGAMMA_N + 1 by the Stirling series (terms to z^-7;
+// truncation < 1e-25 there, i.e. within an ulp like libm's lgamma) — far
+// smaller code than the general-purpose lgamma.
+__device__ __forceinline__ double lgamma_stirling(double z) {
+  const double r = 1.0 / z, r2 = r * r;
+  const double series = r * (1.0 / 12.0 - r2 * (1.0 / 360.0 - r2 * (1.0 / 1260.0 - r2 * (1.0 / 1680.0))));
+  return (z - 0.5) * log(z) - z + 0.91893853320467274178 + series;
+}
+
 // lgamma(k+1), k < KIN_LGAMMA_N, computed by the host's glibc (the oracle's libm)
 // and uploaded once per context (see kin_engine.cpp).
 #define KIN_LGAMMA_N 4096
@@ -245,7 +254,7 @@ __device__ __forceinline__ uint64_t poisson(Rng& rng, double mean, uint64_t& flo
     const double arg = __ddiv_rn(__dmul_rn(v, inv_alpha), __dadd_rn(__ddiv_rn(a, __dmul_rn(us, us)), b));
     // lgamma(kf+1): glibc's own values (host table) for kf < KIN_LGAMMA_N
     const double lg = kf < static_cast<double>(KIN_LGAMMA_N) ? __ldg(lgamma_tab + static_cast<int>(kf))
-                                                             : lgamma(__dadd_rn(kf, 1.0));
+                                                             : lgamma_stirling(__dadd_rn(kf, 1.0));
     const double rhs = __dsub_rn(__dadd_rn(-mean, __dmul_rn(kf, lm)), lg);
     if (kCount) flops += 11;
     // Fast decision on lhs = log(arg): __logf errs by <= 2^-21.41 absolute on

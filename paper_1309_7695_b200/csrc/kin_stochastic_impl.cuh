@@ -295,17 +295,36 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     if (kCount) flops += 1;
     if (!(tau < gap)) { tau = gap; hit = true; }
     Xoshiro saved = rng;
+    // One Poisson call site (code size): pass 0 draws and applies; a rejected
+    // attempt runs pass 1, which replays the same draws from the saved stream
+    // (or the same Philox counters) and subtracts them, then retries with tau/2.
+    int pass = 0;
     for (;;) {
 #pragma unroll 1
       for (int j = 0; j < M; ++j) {
         uint64_t k;
+        const double mean = __dmul_rn(sm.aval(j), tau);
         if (kPhilox) {
           PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
-          k = poisson<kCount>(src, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
+          k = pass == 0 ? poisson<kCount>(src, mean, flops, S.lgamma_tab)
+                        : poisson<false>(src, mean, dummy, S.lgamma_tab);
         } else {
-          k = poisson<kCount>(rng, __dmul_rn(sm.aval(j), tau), flops, S.lgamma_tab);
+          Xoshiro& r = pass == 0 ? rng : saved;
+          k = pass == 0 ? poisson<kCount>(r, mean, flops, S.lgamma_tab)
+                        : poisson<false>(r, mean, dummy, S.lgamma_tab);
         }
-        if (k != 0) sm.apply(j, static_cast<long long>(k), ovf);
+        if (k != 0) sm.apply(j, pass == 0 ? static_cast<long long>(k) : -static_cast<long long>(k), ovf);
+      }
+      if (pass == 1) {
+        // undone: continue the stream with half the step
+        pass = 0;
+        ++ev;
+        saved = rng;
+        ++n_rej;
+        tau = __dmul_rn(tau, 0.5);
+        hit = false;
+        if (kCount) flops += 1;
+        continue;
       }
       if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
       if (ovf) break;
@@ -313,24 +332,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         ++ev;
         break;
       }
-      // rejected: undo exactly by replaying the same draws, continue the stream
-#pragma unroll 1
-      for (int j = 0; j < M; ++j) {
-        uint64_t k;
-        if (kPhilox) {
-          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
-          k = poisson<false>(src, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
-        } else {
-          k = poisson<false>(saved, __dmul_rn(sm.aval(j), tau), dummy, S.lgamma_tab);
-        }
-        if (k != 0) sm.apply(j, -static_cast<long long>(k), ovf);
-      }
-      ++ev;
-      saved = rng;
-      ++n_rej;
-      tau = __dmul_rn(tau, 0.5);
-      hit = false;
-      if (kCount) flops += 1;
+      pass = 1;
     }
     if (ovf) break;
     if (hit) {
