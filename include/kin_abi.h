@@ -199,6 +199,16 @@ int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* de
 int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t runs_per_point, int32_t n_devices,
                    int32_t max_chunks, uint64_t* bounds, int32_t* n_chunks, kin_error* err);
 
+/* Asynchronous form of kin_sweep_run: enqueue the sweep (kernels on the
+   device's compute stream, transposes + copy-out into `out` on its copy stream)
+   and return a ticket at once; kin_sweep_wait blocks until the results are in
+   `out` and reports errors exactly as kin_sweep_run.  Copy-out of one sweep
+   overlaps the kernels of the next.  Outputs must stay valid until the wait;
+   with pageable (non-pinned) outputs the copy-out is synchronous. */
+int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc,
+                     kin_sweep_out* out, uint64_t* ticket, kin_error* err);
+int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err);
+
 /* ---- device-resident form (benchmarks, chained consumers) -----------------
    Runs the sweep on device `device_slot` of the context into context-owned
    device buffers, on the context's stream, WITHOUT any host copies.  The

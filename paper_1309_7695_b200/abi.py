@@ -84,7 +84,7 @@ class KinError(C.Structure):
 # Every symbol include/kin_abi.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
     "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
-    "kin_model_free", "kin_sweep_size", "kin_sweep_plan", "kin_sweep_run", "kin_sweep_launch", "kin_sweep_sync",
+    "kin_model_free", "kin_sweep_size", "kin_sweep_plan", "kin_sweep_run", "kin_sweep_submit", "kin_sweep_wait", "kin_sweep_launch", "kin_sweep_sync",
     "kin_sweep_fetch", "kin_ctx_stream", "kin_sweep_kernel_ms", "kin_splitmix64_mix", "kin_derive_run_seed",
     "kin_device_rng_draws", "kin_jit_check", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
 )
@@ -102,6 +102,8 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "kin_sweep_size": (C.c_int, [C.POINTER(KinSweepDesc), u64p, u64p, E]),
         "kin_sweep_plan": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, u64p, i32p, E]),
         "kin_sweep_run": (C.c_int, [vp, vp, C.POINTER(KinSweepDesc), C.POINTER(KinSweepOut), E]),
+        "kin_sweep_submit": (C.c_int, [vp, vp, C.POINTER(KinSweepDesc), C.POINTER(KinSweepOut), u64p, E]),
+        "kin_sweep_wait": (C.c_int, [vp, C.c_uint64, E]),
         "kin_sweep_launch": (C.c_int, [vp, vp, C.POINTER(KinSweepDesc), C.c_int32, C.c_int32, C.c_int32, E]),
         "kin_sweep_sync": (C.c_int, [vp, C.c_int32, E]),
         "kin_sweep_fetch": (C.c_int, [vp, C.c_int32, C.POINTER(KinSweepOut), E]),

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -402,39 +403,77 @@ struct DevBuf {
   }
 };
 
-struct Slot {
-  int device = 0;
-  cudaStream_t stream = nullptr;
+// Per-launch device state: outputs, scratch, the launch record used by the
+// int32-overflow retry, and the events ordering compute -> copy-out.  A slot
+// owns one Buffers for the device-resident API (kin_sweep_launch/fetch) and a
+// pool reused by asynchronous jobs (kin_sweep_submit/wait).
+struct Buffers {
   DevBuf<double> traj, traj_t, mean, m2, axis, grid;
   DevBuf<uint64_t> meta, work;
-  DevBuf<unsigned long long> counter;
-  DevBuf<double> lgamma_tab;  // glibc lgamma(k+1), k < KIN_LGAMMA_N
-  DevBuf<double> lsoda_co;    // cfode elco/tesco
   DevBuf<int32_t> status;
-  void* stage = nullptr;
-  size_t stage_cap = 0;
-  cudaEvent_t ev[2] = {nullptr, nullptr};
+  DevBuf<unsigned long long> counter;
+  DevBuf<int> ovf;
+  int* ovf_host = nullptr;  // pinned copy of the overflow flag
   cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // sim start, sim end, stats end
+  cudaEvent_t ev_done = nullptr, ev_copied = nullptr;
   bool timed_stats = false;
-  // record of the last device-resident launch
   uint64_t s0 = 0, s1 = 0, P0 = 0, nP = 0, R = 1;
   int G = 0, N = 0;
   bool have_stats = false, have_work = false, valid = false;
-  // replay record for the int32-amount retry
-  DevBuf<int> ovf;
   std::unique_ptr<KinTables> last_T;
   KinSweepDev last_SD{};
   KinOutDev last_O{};
   bool last_int_state = false, last_count = false, pending_check = false, last_jit = false;
   uint64_t last_base = 0, last_S = 0;
   int last_gn = 0;
+  void release() {
+    traj.release(); traj_t.release(); mean.release(); m2.release(); axis.release(); grid.release();
+    meta.release(); work.release(); status.release(); counter.release(); ovf.release();
+    if (ovf_host) cudaFreeHost(ovf_host);
+    ovf_host = nullptr;
+    for (auto& e : tev) if (e) cudaEventDestroy(e);
+    if (ev_done) cudaEventDestroy(ev_done);
+    if (ev_copied) cudaEventDestroy(ev_copied);
+    ev_done = ev_copied = nullptr;
+    for (auto& e : tev) e = nullptr;
+  }
+};
+
+struct Slot {
+  int device = 0;
+  cudaStream_t stream = nullptr;       // kernels
+  cudaStream_t copy_stream = nullptr;  // transposes + copy-out of async jobs
+  DevBuf<double> lgamma_tab;  // glibc lgamma(k+1), k < KIN_LGAMMA_N
+  DevBuf<double> lsoda_co;    // cfode elco/tesco
+  void* stage = nullptr;
+  size_t stage_cap = 0;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  Buffers main;
+  std::vector<std::unique_ptr<Buffers>> pool;
   std::mutex mu;
+};
+
+struct Job {
+  struct Part {
+    int slot;
+    Buffers* buf;
+  };
+  std::vector<Part> parts;
+  kin_sweep_out out{};
+  uint64_t s0 = 0, s1 = 0, base_point = 0;
+  Layout L;
+  int32_t* status_pinned = nullptr;  // when the caller did not ask for status
+  int rc = KIN_OK;
+  kin_error err{};
 };
 
 }  // namespace
 
 struct kin_ctx {
   std::vector<std::unique_ptr<Slot>> slots;
+  std::mutex jobs_mu;
+  uint64_t next_ticket = 1;
+  std::map<uint64_t, std::unique_ptr<Job>> jobs;
 };
 
 struct kin_model {
@@ -464,12 +503,14 @@ bool is_pinned(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
-// D2H into a caller buffer: direct when pinned, else through a pinned double buffer.
-int copy_d2h(Slot& sl, void* dst, const void* src, size_t bytes, kin_error* err) {
+// D2H into a caller buffer on `st`: asynchronous when the destination is pinned
+// (sync=false leaves it in flight), else staged through a pinned double buffer
+// (always synchronous).
+int copy_d2h(Slot& sl, cudaStream_t st, void* dst, const void* src, size_t bytes, bool sync, kin_error* err) {
   if (bytes == 0) return KIN_OK;
   if (is_pinned(dst)) {
-    KIN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, sl.stream), "D2H");
-    KIN_CUDA(cudaStreamSynchronize(sl.stream), "D2H sync");
+    KIN_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+    if (sync) KIN_CUDA(cudaStreamSynchronize(st), "D2H sync");
     return KIN_OK;
   }
   const size_t piece = size_t{32} << 20;
@@ -486,8 +527,8 @@ int copy_d2h(Slot& sl, void* dst, const void* src, size_t bytes, kin_error* err)
   int pending_b = -1, b = 0;
   for (size_t off = 0; off < bytes; off += piece) {
     const size_t len = std::min(piece, bytes - off);
-    KIN_CUDA(cudaMemcpyAsync(buf[b], in + off, len, cudaMemcpyDeviceToHost, sl.stream), "D2H");
-    KIN_CUDA(cudaEventRecord(sl.ev[b], sl.stream), "event");
+    KIN_CUDA(cudaMemcpyAsync(buf[b], in + off, len, cudaMemcpyDeviceToHost, st), "D2H");
+    KIN_CUDA(cudaEventRecord(sl.ev[b], st), "event");
     if (pending_b >= 0) {
       KIN_CUDA(cudaEventSynchronize(sl.ev[pending_b]), "D2H sync");
       std::memcpy(out + pending_off, buf[pending_b], pending_len);
@@ -541,7 +582,7 @@ kin::JitModel jit_model(const HostModel& H, const kin_sweep_desc* d) {
 }
 
 // Launch the simulation kernels for global sims [s0, s1) on a slot (device-resident).
-int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const Layout& L, uint64_t s0, uint64_t s1,
+int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc* d, const Layout& L, uint64_t s0, uint64_t s1,
                  bool want_stats, bool want_work, kin_error* err) {
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
   KinTables* T = new KinTables;
@@ -551,15 +592,15 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
   const uint64_t S = s1 - s0;
   const int G = d->n_grid, N = H.n;
   const size_t gn = static_cast<size_t>(G) * N;
-  KIN_CUDA(sl.traj.ensure(std::max<size_t>(gn * S, 1)), "cudaMalloc traj");
-  KIN_CUDA(sl.meta.ensure(std::max<uint64_t>(S * 6, 1)), "cudaMalloc meta");
-  KIN_CUDA(sl.status.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc status");
-  if (want_work) KIN_CUDA(sl.work.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc work");
+  KIN_CUDA(bf.traj.ensure(std::max<size_t>(gn * S, 1)), "cudaMalloc traj");
+  KIN_CUDA(bf.meta.ensure(std::max<uint64_t>(S * 6, 1)), "cudaMalloc meta");
+  KIN_CUDA(bf.status.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc status");
+  if (want_work) KIN_CUDA(bf.work.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc work");
   // axis values and grid
   size_t nax = 0;
   for (int ax = 0; ax < d->n_axes; ++ax) nax += d->axes[ax].n_values;
-  KIN_CUDA(sl.axis.ensure(std::max<size_t>(nax, 1)), "cudaMalloc axes");
-  KIN_CUDA(sl.grid.ensure(std::max<int>(G, 1)), "cudaMalloc grid");
+  KIN_CUDA(bf.axis.ensure(std::max<size_t>(nax, 1)), "cudaMalloc axes");
+  KIN_CUDA(bf.grid.ensure(std::max<int>(G, 1)), "cudaMalloc grid");
   KinSweepDev SD;
   std::memset(&SD, 0, sizeof(SD));
   SD.kind = d->method.kind;
@@ -577,37 +618,37 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
   for (int ax = 0; ax < d->n_axes; ++ax) {
     SD.axis_kind[ax] = d->axes[ax].kind;
     SD.axis_n[ax] = d->axes[ax].n_values;
-    SD.axis_values[ax] = sl.axis.p + at;
-    KIN_CUDA(cudaMemcpyAsync(sl.axis.p + at, d->axes[ax].values, sizeof(double) * d->axes[ax].n_values,
+    SD.axis_values[ax] = bf.axis.p + at;
+    KIN_CUDA(cudaMemcpyAsync(bf.axis.p + at, d->axes[ax].values, sizeof(double) * d->axes[ax].n_values,
                              cudaMemcpyHostToDevice, sl.stream), "H2D axes");
     at += d->axes[ax].n_values;
   }
-  if (G) KIN_CUDA(cudaMemcpyAsync(sl.grid.p, d->grid, sizeof(double) * G, cudaMemcpyHostToDevice, sl.stream), "H2D grid");
+  if (G) KIN_CUDA(cudaMemcpyAsync(bf.grid.p, d->grid, sizeof(double) * G, cudaMemcpyHostToDevice, sl.stream), "H2D grid");
   SD.runs = L.R;
   SD.master_seed = d->master_seed;
   SD.sim_begin = s0;
   SD.n_local = S;
   SD.t_end = d->t_end;
-  SD.grid = sl.grid.p;
+  SD.grid = bf.grid.p;
   SD.lgamma_tab = sl.lgamma_tab.p;
-  KinOutDev O{sl.traj.p, sl.meta.p, sl.status.p, want_work ? sl.work.p : nullptr};
-  if (!sl.tev[0])
-    for (auto& ev : sl.tev) KIN_CUDA(cudaEventCreate(&ev), "event");
-  KIN_CUDA(cudaEventRecord(sl.tev[0], sl.stream), "event");
+  KinOutDev O{bf.traj.p, bf.meta.p, bf.status.p, want_work ? bf.work.p : nullptr};
+  if (!bf.tev[0])
+    for (auto& ev : bf.tev) KIN_CUDA(cudaEventCreate(&ev), "event");
+  KIN_CUDA(cudaEventRecord(bf.tev[0], sl.stream), "event");
   cudaError_t e;
   const int kind = d->method.kind;
   if (kind == KIN_METHOD_ODE) {
     e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
   } else if (kind == KIN_METHOD_LSODA) {
-    KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
     if (kin::lsoda_smem_bytes(*T, SD) > 227 * 1024) {
       set_err(err, KIN_ERR_INPUT, "model too large for the LSODA kernel (per-simulation state exceeds shared memory)");
       return KIN_ERR_INPUT;
     }
-    e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, sl.counter.p, sl.stream);
+    e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, sl.stream);
   } else {
-    KIN_CUDA(sl.counter.ensure(1), "cudaMalloc counter");
-    KIN_CUDA(sl.ovf.ensure(1), "cudaMalloc overflow flag");
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
+    KIN_CUDA(bf.ovf.ensure(1), "cudaMalloc overflow flag");
     // Philox mode: L lanes per simulation (KIN_GROUP_LANES overrides; 1 = one
     // thread per simulation).  Compat mode is always one thread per simulation.
     int lanes = 0;
@@ -615,8 +656,8 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
     if (d->rng_mode != KIN_RNG_PHILOX) lanes = 1;
     else if (lanes <= 0) lanes = kin::stochastic_group_pick_lanes(H.n, H.m);
     if (lanes != 1) {
-      e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, sl.counter.p, sl.stream);
-      sl.last_int_state = false;
+      e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, bf.counter.p, sl.stream);
+      bf.last_int_state = false;
     } else {
       // int32 amounts when every initial amount is far inside int32 range
       // (KIN_INT_STATE=0 forces doubles)
@@ -627,74 +668,74 @@ int launch_range(Slot& sl, const HostModel& H, const kin_sweep_desc* d, const La
           for (int v = 0; v < d->axes[ax].n_values; ++v) xmax = std::max(xmax, d->axes[ax].values[v]);
       bool int_state = xmax < 1073741824.0;
       if (const char* v = std::getenv("KIN_INT_STATE")) int_state = int_state && std::atoi(v) != 0;
-      KIN_CUDA(cudaMemsetAsync(sl.ovf.p, 0, sizeof(int), sl.stream), "memset");
+      KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), sl.stream), "memset");
       bool used = false;
       e = cudaSuccess;
       if (kin::jit_wanted(S)) {
         const kin::JitModel jm = jit_model(H, d);
-        e = kin::launch_stochastic_jit(jm, *T, SD, O, want_work, sl.counter.p, sl.ovf.p, int_state, sl.stream, &used);
+        e = kin::launch_stochastic_jit(jm, *T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, sl.stream, &used);
       }
       if (e == cudaSuccess && !used)
-        e = kin::launch_stochastic(*T, SD, O, want_work, sl.counter.p, sl.ovf.p, int_state, sl.stream);
-      sl.last_jit = used;
-      sl.last_int_state = int_state;
+        e = kin::launch_stochastic(*T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, sl.stream);
+      bf.last_jit = used;
+      bf.last_int_state = int_state;
     }
-    if (sl.last_int_state) {
-      if (!sl.last_T) sl.last_T.reset(new KinTables);
-      *sl.last_T = *T;
-      sl.last_SD = SD;
-      sl.last_O = O;
-      sl.last_count = want_work;
+    if (bf.last_int_state) {
+      if (!bf.last_T) bf.last_T.reset(new KinTables);
+      *bf.last_T = *T;
+      bf.last_SD = SD;
+      bf.last_O = O;
+      bf.last_count = want_work;
     }
   }
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
-  KIN_CUDA(cudaEventRecord(sl.tev[1], sl.stream), "event");
-  sl.timed_stats = false;
+  KIN_CUDA(cudaEventRecord(bf.tev[1], sl.stream), "event");
+  bf.timed_stats = false;
   // per-point statistics for points entirely inside [s0, s1)
   const uint64_t P0 = (s0 + L.R - 1) / L.R, P1 = s1 / L.R;
   const uint64_t nP = P1 > P0 ? P1 - P0 : 0;
   if (want_stats && nP) {
-    KIN_CUDA(sl.mean.ensure(gn * nP), "cudaMalloc mean");
-    KIN_CUDA(sl.m2.ensure(gn * nP), "cudaMalloc m2");
-    e = kin::launch_point_stats(sl.traj.p, S, static_cast<int>(gn), L.R, P0 * L.R - s0, nP, sl.mean.p, sl.m2.p,
+    KIN_CUDA(bf.mean.ensure(gn * nP), "cudaMalloc mean");
+    KIN_CUDA(bf.m2.ensure(gn * nP), "cudaMalloc m2");
+    e = kin::launch_point_stats(bf.traj.p, S, static_cast<int>(gn), L.R, P0 * L.R - s0, nP, bf.mean.p, bf.m2.p,
                                 sl.stream);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
-    KIN_CUDA(cudaEventRecord(sl.tev[2], sl.stream), "event");
-    sl.timed_stats = true;
+    KIN_CUDA(cudaEventRecord(bf.tev[2], sl.stream), "event");
+    bf.timed_stats = true;
   }
-  sl.pending_check = sl.last_int_state;
-  sl.last_base = P0 * L.R - s0;
-  sl.last_S = S;
-  sl.last_gn = static_cast<int>(gn);
-  sl.s0 = s0;
-  sl.s1 = s1;
-  sl.P0 = P0;
-  sl.nP = nP;
-  sl.R = L.R;
-  sl.G = G;
-  sl.N = N;
-  sl.have_stats = want_stats && nP;
-  sl.have_work = want_work;
-  sl.valid = true;
+  bf.pending_check = bf.last_int_state;
+  bf.last_base = P0 * L.R - s0;
+  bf.last_S = S;
+  bf.last_gn = static_cast<int>(gn);
+  bf.s0 = s0;
+  bf.s1 = s1;
+  bf.P0 = P0;
+  bf.nP = nP;
+  bf.R = L.R;
+  bf.G = G;
+  bf.N = N;
+  bf.have_stats = want_stats && nP;
+  bf.have_work = want_work;
+  bf.valid = true;
   return KIN_OK;
 }
 
 // Complete a launch: wait for it and, if an int32 amount overflowed, re-run the
 // stochastic kernel with double amounts (and the statistics) — same results.
-int finish_launch(Slot& sl, kin_error* err) {
+int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
   KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
-  if (!sl.pending_check) return KIN_OK;
-  sl.pending_check = false;
+  if (!bf.pending_check) return KIN_OK;
+  bf.pending_check = false;
   int flag = 0;
-  KIN_CUDA(cudaMemcpy(&flag, sl.ovf.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H overflow flag");
+  KIN_CUDA(cudaMemcpy(&flag, bf.ovf.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H overflow flag");
   if (!flag) return KIN_OK;
-  KIN_CUDA(cudaMemsetAsync(sl.ovf.p, 0, sizeof(int), sl.stream), "memset");
-  cudaError_t e = kin::launch_stochastic(*sl.last_T, sl.last_SD, sl.last_O, sl.last_count, sl.counter.p, sl.ovf.p,
+  KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), sl.stream), "memset");
+  cudaError_t e = kin::launch_stochastic(*bf.last_T, bf.last_SD, bf.last_O, bf.last_count, bf.counter.p, bf.ovf.p,
                                          false, sl.stream);
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel relaunch");
-  if (sl.have_stats) {
-    e = kin::launch_point_stats(sl.traj.p, sl.last_S, sl.last_gn, sl.R, sl.last_base, sl.nP, sl.mean.p, sl.m2.p,
+  if (bf.have_stats) {
+    e = kin::launch_point_stats(bf.traj.p, bf.last_S, bf.last_gn, bf.R, bf.last_base, bf.nP, bf.mean.p, bf.m2.p,
                                 sl.stream);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel relaunch");
   }
@@ -702,34 +743,44 @@ int finish_launch(Slot& sl, kin_error* err) {
   return KIN_OK;
 }
 
-// Copy the slot's last launch into caller buffers; offsets are relative to
-// (base_sim, base_point) of the caller's arrays.
-int fetch_range(Slot& sl, kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, kin_error* err) {
-  if (int rc = finish_launch(sl, err)) return rc;
-  const uint64_t S = sl.s1 - sl.s0;
-  const size_t gn = static_cast<size_t>(sl.G) * sl.N;
-  const uint64_t so = sl.s0 - base_sim;
+// Copy a launch's results into caller buffers (offsets relative to base_sim /
+// base_point of the caller's arrays).  async: on the slot's copy stream, left
+// in flight (the caller orders it after the launch); otherwise synchronous on
+// the compute stream.
+int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, bool sync,
+             kin_error* err) {
+  cudaStream_t st = sync ? sl.stream : sl.copy_stream;
+  const uint64_t S = bf.s1 - bf.s0;
+  const size_t gn = static_cast<size_t>(bf.G) * bf.N;
+  const uint64_t so = bf.s0 - base_sim;
   if (out->traj && S && gn) {
-    KIN_CUDA(sl.traj_t.ensure(gn * S), "cudaMalloc transpose");
-    cudaError_t e = kin::launch_transpose_traj(sl.traj.p, sl.traj_t.p, S, static_cast<int>(gn), sl.stream);
+    KIN_CUDA(bf.traj_t.ensure(gn * S), "cudaMalloc transpose");
+    cudaError_t e = kin::launch_transpose_traj(bf.traj.p, bf.traj_t.p, S, static_cast<int>(gn), st);
     if (e != cudaSuccess) return cuda_fail(err, e, "transpose launch");
-    if (int rc = copy_d2h(sl, out->traj + so * gn, sl.traj_t.p, gn * S * sizeof(double), err)) return rc;
+    if (int rc = copy_d2h(sl, st, out->traj + so * gn, bf.traj_t.p, gn * S * sizeof(double), sync, err)) return rc;
   }
   if (out->meta && S)
-    if (int rc = copy_d2h(sl, out->meta + so * 6, sl.meta.p, S * 6 * sizeof(uint64_t), err)) return rc;
+    if (int rc = copy_d2h(sl, st, out->meta + so * 6, bf.meta.p, S * 6 * sizeof(uint64_t), sync, err)) return rc;
   if (out->status && S)
-    if (int rc = copy_d2h(sl, out->status + so, sl.status.p, S * sizeof(int32_t), err)) return rc;
-  if (out->work && S && sl.have_work)
-    if (int rc = copy_d2h(sl, out->work + so, sl.work.p, S * sizeof(uint64_t), err)) return rc;
-  if (sl.have_stats) {
-    const uint64_t po = sl.P0 - base_point;
+    if (int rc = copy_d2h(sl, st, out->status + so, bf.status.p, S * sizeof(int32_t), sync, err)) return rc;
+  if (out->work && S && bf.have_work)
+    if (int rc = copy_d2h(sl, st, out->work + so, bf.work.p, S * sizeof(uint64_t), sync, err)) return rc;
+  if (bf.have_stats) {
+    const uint64_t po = bf.P0 - base_point;
     if (out->mean)
-      if (int rc = copy_d2h(sl, out->mean + po * gn, sl.mean.p, sl.nP * gn * sizeof(double), err)) return rc;
+      if (int rc = copy_d2h(sl, st, out->mean + po * gn, bf.mean.p, bf.nP * gn * sizeof(double), sync, err)) return rc;
     if (out->m2)
-      if (int rc = copy_d2h(sl, out->m2 + po * gn, sl.m2.p, sl.nP * gn * sizeof(double), err)) return rc;
+      if (int rc = copy_d2h(sl, st, out->m2 + po * gn, bf.m2.p, bf.nP * gn * sizeof(double), sync, err)) return rc;
   }
-  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
+  if (bf.pending_check && bf.ovf_host)
+    KIN_CUDA(cudaMemcpyAsync(bf.ovf_host, bf.ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
+  if (sync) KIN_CUDA(cudaStreamSynchronize(st), "stream sync");
   return KIN_OK;
+}
+
+int fetch_range(Slot& sl, Buffers& bf, kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, kin_error* err) {
+  if (int rc = finish_launch(sl, bf, err)) return rc;
+  return copy_out(sl, bf, out, base_sim, base_point, true, err);
 }
 
 // Chunk plan of kin_sweep_run (see kin_abi.h kin_sweep_plan).
@@ -802,6 +853,7 @@ int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err)
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dv);
     if (major < 10) { set_err(err, KIN_ERR_DEVICE, "engine is built for sm_100a (B200) only"); return KIN_ERR_DEVICE; }
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    KIN_CUDA(cudaStreamCreateWithFlags(&sl->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     // lgamma(k+1) from the host libm (the oracle's, glibc) for the PTRS test
     std::vector<double> lg(KIN_LGAMMA_N);
     for (int k = 0; k < KIN_LGAMMA_N; ++k) lg[k] = std::lgamma(static_cast<double>(k) + 1.0);
@@ -819,15 +871,23 @@ int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err)
 
 void kin_ctx_destroy(kin_ctx* ctx) {
   if (!ctx) return;
+  for (auto& kv : ctx->jobs) {
+    kin_error e;
+    (void)e;
+    if (kv.second->status_pinned) cudaFreeHost(kv.second->status_pinned);
+  }
   for (auto& sl : ctx->slots) {
     cudaSetDevice(sl->device);
     cudaStreamSynchronize(sl->stream);
-    sl->traj.release(); sl->traj_t.release(); sl->mean.release(); sl->m2.release();
-    sl->axis.release(); sl->grid.release(); sl->meta.release(); sl->work.release(); sl->counter.release(); sl->lgamma_tab.release(); sl->lsoda_co.release(); sl->ovf.release(); sl->status.release();
+    cudaStreamSynchronize(sl->copy_stream);
+    sl->main.release();
+    for (auto& b : sl->pool) b->release();
+    sl->lgamma_tab.release();
+    sl->lsoda_co.release();
     if (sl->stage) cudaFreeHost(sl->stage);
     for (auto& e : sl->ev) if (e) cudaEventDestroy(e);
-    for (auto& e : sl->tev) if (e) cudaEventDestroy(e);
     cudaStreamDestroy(sl->stream);
+    cudaStreamDestroy(sl->copy_stream);
   }
   delete ctx;
 }
@@ -864,69 +924,114 @@ int kin_sweep_size(const kin_sweep_desc* desc, uint64_t* np, uint64_t* ns, kin_e
 
 int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc, kin_sweep_out* out,
                   kin_error* err) {
-  if (!ctx) { set_err(err, KIN_ERR_USAGE, "null context"); return KIN_ERR_USAGE; }
-  Layout L;
+  uint64_t ticket = 0;
+  if (int rc = kin_sweep_submit(ctx, model, desc, out, &ticket, err)) return rc;
+  return kin_sweep_wait(ctx, ticket, err);
+}
+
+int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc, kin_sweep_out* out,
+                     uint64_t* ticket, kin_error* err) {
+  if (!ctx || !ticket) { set_err(err, KIN_ERR_USAGE, "null argument"); return KIN_ERR_USAGE; }
+  auto job = std::make_unique<Job>();
   uint64_t s0, s1;
-  if (int rc = prepare(model, desc, &L, &s0, &s1, err)) return rc;
-  kin_sweep_out none;
-  std::memset(&none, 0, sizeof(none));
-  if (!out) out = &none;
+  if (int rc = prepare(model, desc, &job->L, &s0, &s1, err)) return rc;
+  const Layout& L = job->L;
+  if (out) job->out = *out;
+  job->s0 = s0;
+  job->s1 = s1;
+  job->base_point = (s0 + L.R - 1) / L.R;
   const uint64_t S = s1 - s0;
-  const uint64_t base_point = (s0 + L.R - 1) / L.R;
-  // whole-point chunks, cyclic over devices
+  if (!job->out.status && S) {
+    KIN_CUDA(cudaMallocHost(&job->status_pinned, sizeof(int32_t) * S), "pinned status");
+    job->out.status = job->status_pinned;
+  }
   const int D = static_cast<int>(ctx->slots.size());
   const std::vector<uint64_t> bounds = plan_chunks(s0, s1, L.R, D);
-  const uint64_t n_chunks = bounds.size() - 1;
-  std::vector<int32_t> status_local;
-  int32_t* status = out->status;
-  if (!status) {
-    status_local.resize(std::max<uint64_t>(S, 1));
-    status = status_local.data();
-  }
-  kin_sweep_out o2 = *out;
-  o2.status = status;
-  std::vector<kin_error> errs(D);
-  std::vector<int> rcs(D, KIN_OK);
-  auto worker = [&](int dv) {
+  const bool stats = job->out.mean || job->out.m2;
+  for (size_t c = 0; c + 1 < bounds.size(); ++c) {
+    const uint64_t c0 = bounds[c], c1 = bounds[c + 1];
+    if (c0 >= c1) continue;
+    const int dv = static_cast<int>(c % D);
     Slot& sl = *ctx->slots[dv];
     std::lock_guard<std::mutex> lk(sl.mu);
-    for (uint64_t c = dv; c < n_chunks; c += D) {
-      const uint64_t c0 = bounds[c], c1 = bounds[c + 1];
-      if (c0 >= c1) continue;
-      const bool stats = (o2.mean || o2.m2);
-      int rc = launch_range(sl, model->host, desc, L, c0, c1, stats, o2.work != nullptr, &errs[dv]);
-      if (rc == KIN_OK) rc = fetch_range(sl, &o2, s0, base_point, &errs[dv]);
-      if (rc != KIN_OK) { rcs[dv] = rc; return; }
+    KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+    Buffers* bf;
+    if (!sl.pool.empty()) {
+      bf = sl.pool.back().release();
+      sl.pool.pop_back();
+    } else {
+      bf = new Buffers;
     }
-  };
-  if (D == 1) {
-    worker(0);
-  } else {
-    std::vector<std::thread> th;
-    for (int dv = 0; dv < D; ++dv) th.emplace_back(worker, dv);
-    for (auto& t : th) t.join();
+    job->parts.push_back({dv, bf});
+    if (int rc = launch_range(sl, *bf, model->host, desc, L, c0, c1, stats, job->out.work != nullptr, err)) return rc;
+    if (!bf->ev_done) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_done, cudaEventDisableTiming), "event");
+    if (!bf->ev_copied) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_copied, cudaEventDisableTiming), "event");
+    if (!bf->ovf_host) KIN_CUDA(cudaMallocHost(&bf->ovf_host, sizeof(int)), "pinned flag");
+    KIN_CUDA(cudaEventRecord(bf->ev_done, sl.stream), "event");
+    // copy-out on the copy stream, overlapping the next launches on `stream`
+    KIN_CUDA(cudaStreamWaitEvent(sl.copy_stream, bf->ev_done, 0), "stream wait");
+    if (int rc = copy_out(sl, *bf, &job->out, s0, job->base_point, false, err)) return rc;
+    KIN_CUDA(cudaEventRecord(bf->ev_copied, sl.copy_stream), "event");
   }
-  for (int dv = 0; dv < D; ++dv)
-    if (rcs[dv] != KIN_OK) {
-      if (err) *err = errs[dv];
-      return rcs[dv];
-    }
-  for (uint64_t s = 0; s < S; ++s) {
-    if (status[s] != KIN_SIM_OK) {
-      const uint64_t g = s0 + s;
-      if (err) {
-        err->code = KIN_ERR_SIMULATION;
-        err->sim_status = status[s];
-        err->sim_index = g;
-        err->point_index = g / L.R;
-        err->run_index = g % L.R;
-        std::snprintf(err->message, sizeof(err->message), "simulation %llu (point %llu, run %llu) failed: status %d",
-                      (unsigned long long)g, (unsigned long long)(g / L.R), (unsigned long long)(g % L.R), status[s]);
-      }
-      return KIN_ERR_SIMULATION;
-    }
-  }
+  std::lock_guard<std::mutex> lk(ctx->jobs_mu);
+  *ticket = ctx->next_ticket++;
+  ctx->jobs[*ticket] = std::move(job);
   return KIN_OK;
+}
+
+int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  std::unique_ptr<Job> job;
+  if (!ctx) { set_err(err, KIN_ERR_USAGE, "null context"); return KIN_ERR_USAGE; }
+  {
+    std::lock_guard<std::mutex> lk(ctx->jobs_mu);
+    if (!ctx->jobs.count(ticket)) { set_err(err, KIN_ERR_USAGE, "unknown ticket"); return KIN_ERR_USAGE; }
+    job = std::move(ctx->jobs[ticket]);
+    ctx->jobs.erase(ticket);
+  }
+  int rc = KIN_OK;
+  for (auto& part : job->parts) {
+    Slot& sl = *ctx->slots[part.slot];
+    Buffers& bf = *part.buf;
+    if (rc == KIN_OK) {
+      KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+      KIN_CUDA(cudaEventSynchronize(bf.ev_copied), "copy-out");
+      if (bf.pending_check && *bf.ovf_host) {
+        // an int32 amount overflowed: redo this chunk with double amounts
+        std::lock_guard<std::mutex> lk(sl.mu);
+        bf.pending_check = true;
+        if ((rc = finish_launch(sl, bf, err)) == KIN_OK)
+          rc = copy_out(sl, bf, &job->out, job->s0, job->base_point, true, err);
+      }
+      bf.pending_check = false;
+    }
+    std::lock_guard<std::mutex> lk(sl.mu);
+    sl.pool.emplace_back(part.buf);
+  }
+  job->parts.clear();
+  if (rc == KIN_OK) {
+    const uint64_t S = job->s1 - job->s0;
+    for (uint64_t s = 0; s < S; ++s) {
+      const int32_t st = job->out.status[s];
+      if (st != KIN_SIM_OK) {
+        const uint64_t g = job->s0 + s;
+        if (err) {
+          err->code = KIN_ERR_SIMULATION;
+          err->sim_status = st;
+          err->sim_index = g;
+          err->point_index = g / job->L.R;
+          err->run_index = g % job->L.R;
+          std::snprintf(err->message, sizeof(err->message), "simulation %llu (point %llu, run %llu) failed: status %d",
+                        (unsigned long long)g, (unsigned long long)(g / job->L.R),
+                        (unsigned long long)(g % job->L.R), st);
+        }
+        rc = KIN_ERR_SIMULATION;
+        break;
+      }
+    }
+  }
+  if (job->status_pinned) cudaFreeHost(job->status_pinned);
+  return rc;
 }
 
 int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t R, int32_t D, int32_t max_chunks, uint64_t* bounds,
@@ -951,7 +1056,7 @@ int kin_sweep_launch(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
   if (int rc = prepare(model, desc, &L, &s0, &s1, err)) return rc;
   Slot& sl = *ctx->slots[slot];
   std::lock_guard<std::mutex> lk(sl.mu);
-  return launch_range(sl, model->host, desc, L, s0, s1, want_stats != 0, want_work != 0, err);
+  return launch_range(sl, sl.main, model->host, desc, L, s0, s1, want_stats != 0, want_work != 0, err);
 }
 
 int kin_sweep_sync(kin_ctx* ctx, int32_t slot, kin_error* err) {
@@ -962,7 +1067,7 @@ int kin_sweep_sync(kin_ctx* ctx, int32_t slot, kin_error* err) {
   }
   Slot& sl = *ctx->slots[slot];
   std::lock_guard<std::mutex> lk(sl.mu);
-  return finish_launch(sl, err);
+  return finish_launch(sl, sl.main, err);
 }
 
 int kin_sweep_fetch(kin_ctx* ctx, int32_t slot, kin_sweep_out* out, kin_error* err) {
@@ -973,8 +1078,8 @@ int kin_sweep_fetch(kin_ctx* ctx, int32_t slot, kin_sweep_out* out, kin_error* e
   }
   Slot& sl = *ctx->slots[slot];
   std::lock_guard<std::mutex> lk(sl.mu);
-  if (!sl.valid) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
-  return fetch_range(sl, out, sl.s0, sl.P0, err);
+  if (!sl.main.valid) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
+  return fetch_range(sl, sl.main, out, sl.main.s0, sl.main.P0, err);
 }
 
 int kin_jit_check(const kin_model_desc* desc, const kin_sweep_desc* sweep, char* log, int32_t log_cap,
@@ -999,13 +1104,14 @@ int kin_sweep_kernel_ms(kin_ctx* ctx, int32_t slot, double* sim_ms, double* stat
     return KIN_ERR_USAGE;
   }
   Slot& sl = *ctx->slots[slot];
-  if (!sl.valid || !sl.tev[0]) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
+  const Buffers& bm = sl.main;
+  if (!bm.valid || !bm.tev[0]) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
   float a = 0.0f, b = 0.0f;
-  KIN_CUDA(cudaEventElapsedTime(&a, sl.tev[0], sl.tev[1]), "event time");
-  if (sl.timed_stats) KIN_CUDA(cudaEventElapsedTime(&b, sl.tev[1], sl.tev[2]), "event time");
+  KIN_CUDA(cudaEventElapsedTime(&a, bm.tev[0], bm.tev[1]), "event time");
+  if (bm.timed_stats) KIN_CUDA(cudaEventElapsedTime(&b, bm.tev[1], bm.tev[2]), "event time");
   if (sim_ms) *sim_ms = a;
-  if (stats_ms) *stats_ms = sl.timed_stats ? b : 0.0;
+  if (stats_ms) *stats_ms = bm.timed_stats ? b : 0.0;
   return KIN_OK;
 }
 

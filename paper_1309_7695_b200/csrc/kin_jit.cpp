@@ -61,6 +61,9 @@ std::string dlit(double v) {
   return s;
 }
 
+// Largest model whose divergent SSA updates are emitted as a switch.
+constexpr int kSwitchMaxReactions = 8;
+
 // Model policy source for one model structure (see kin_stochastic_impl.cuh
 // TableModel for the reference semantics of each member).
 std::string generate_policy(const JitModel& m) {
@@ -143,22 +146,31 @@ std::string generate_policy(const JitModel& m) {
     o << " break;\n";
   }
   o << "    }\n  }\n";
-  o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const {\n    bool neg = false;\n    switch (j) {\n";
-  for (int j = 0; j < m.m; ++j) {
-    o << "      case " << j << ":";
-    for (int p = m.col_ptr[j]; p < m.col_ptr[j + 1]; ++p)
-      o << " neg |= upd1(" << m.col_species[p] << ", " << m.col_delta[p] << ", ovf);";
-    o << " break;\n";
+  // SSA events: `sel` differs from lane to lane, and a switch over reactions
+  // serialises a warp over every distinct case it holds (up to M of them).
+  // Small models keep the straight-line cases; larger ones walk the tables
+  // (TableModel: the lanes stay converged, only trip counts differ).
+  if (m.m <= kSwitchMaxReactions) {
+    o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const {\n    bool neg = false;\n    switch (j) {\n";
+    for (int j = 0; j < m.m; ++j) {
+      o << "      case " << j << ":";
+      for (int p = m.col_ptr[j]; p < m.col_ptr[j + 1]; ++p)
+        o << " neg |= upd1(" << m.col_species[p] << ", " << m.col_delta[p] << ", ovf);";
+      o << " break;\n";
+    }
+    o << "    }\n    return neg;\n  }\n";
+    o << "  __device__ __forceinline__ void dep_update(int sel) const {\n    switch (sel) {\n";
+    for (int j = 0; j < m.m; ++j) {
+      o << "      case " << j << ":";
+      for (int q = m.dep_ptr[j]; q < m.dep_ptr[j + 1]; ++q)
+        o << " a[" << m.dep[q] << " * B] = prop(" << m.dep[q] << ");";
+      o << " break;\n";
+    }
+    o << "    }\n  }\n";
+  } else {
+    o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const { return TableModel<XT>{T, x, a, av}.fire(j, ovf); }\n"
+         "  __device__ __forceinline__ void dep_update(int sel) const { TableModel<XT>{T, x, a, av}.dep_update(sel); }\n";
   }
-  o << "    }\n    return neg;\n  }\n";
-  o << "  __device__ __forceinline__ void dep_update(int sel) const {\n    switch (sel) {\n";
-  for (int j = 0; j < m.m; ++j) {
-    o << "      case " << j << ":";
-    for (int q = m.dep_ptr[j]; q < m.dep_ptr[j + 1]; ++q)
-      o << " a[" << m.dep[q] << " * B] = prop(" << m.dep[q] << ");";
-    o << " break;\n";
-  }
-  o << "    }\n  }\n";
   o << "  __device__ __forceinline__ bool any_negative() const {\n    bool neg = false;\n"
     << "#pragma unroll\n    for (int i = 0; i < " << m.n << "; ++i) neg |= x[i * B] < static_cast<XT>(0);\n"
     << "    return neg;\n  }\n";
@@ -208,6 +220,18 @@ bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_
   cubin->resize(n);
   nvrtcGetCUBIN(prog, cubin->data());
   nvrtcDestroyProgram(&prog);
+  if (const char* dump = std::getenv("KIN_JIT_DUMP")) {  // offline inspection (cuobjdump / nvcc -Xptxas -v)
+    const std::string base = std::string(dump) + "/kin_jit_" + (count ? "C" : "c") + (philox ? "P" : "p") +
+                             (int_state ? "I" : "D");
+    if (FILE* f = std::fopen((base + ".cu").c_str(), "wb")) {
+      std::fwrite(src.data(), 1, src.size(), f);
+      std::fclose(f);
+    }
+    if (FILE* f = std::fopen((base + ".cubin").c_str(), "wb")) {
+      std::fwrite(cubin->data(), 1, cubin->size(), f);
+      std::fclose(f);
+    }
+  }
   return true;
 }
 

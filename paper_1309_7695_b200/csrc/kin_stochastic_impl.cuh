@@ -204,7 +204,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   const double t_end = S.t_end;
   double t = 0.0;
   int gi = 0;
-  uint64_t flops = 0, used = 0, dummy = 0;
+  uint64_t flops = 0, used = 0;
   uint64_t n_steps = 0, n_rej = 0, n_ssa = 0;
   int status = 0;
   const uint64_t budget = S.max_steps;
@@ -294,31 +294,32 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     const double gap = __dsub_rn(t_stop, t);
     if (kCount) flops += 1;
     if (!(tau < gap)) { tau = gap; hit = true; }
-    Xoshiro saved = rng;
+    Xoshiro saved = rng, resume;
     // One Poisson call site (code size): pass 0 draws and applies; a rejected
-    // attempt runs pass 1, which replays the same draws from the saved stream
-    // (or the same Philox counters) and subtracts them, then retries with tau/2.
-    int pass = 0;
+    // attempt runs pass 1, which replays the same draws (the saved stream is
+    // swapped into `rng`, or the same Philox counters) and subtracts them, then
+    // resumes the stream where pass 0 left it and retries with tau/2.  The
+    // streams are swapped by value so they stay in registers.
+    long long sign = 1;
     for (;;) {
 #pragma unroll 1
       for (int j = 0; j < M; ++j) {
-        uint64_t k;
+        uint64_t k, fl = 0;
         const double mean = __dmul_rn(sm.aval(j), tau);
         if (kPhilox) {
           PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
-          k = pass == 0 ? poisson<kCount>(src, mean, flops, S.lgamma_tab)
-                        : poisson<false>(src, mean, dummy, S.lgamma_tab);
+          k = poisson<kCount>(src, mean, fl, S.lgamma_tab);
         } else {
-          Xoshiro& r = pass == 0 ? rng : saved;
-          k = pass == 0 ? poisson<kCount>(r, mean, flops, S.lgamma_tab)
-                        : poisson<false>(r, mean, dummy, S.lgamma_tab);
+          k = poisson<kCount>(rng, mean, fl, S.lgamma_tab);
         }
-        if (k != 0) sm.apply(j, pass == 0 ? static_cast<long long>(k) : -static_cast<long long>(k), ovf);
+        if (kCount && sign > 0) flops += fl;
+        if (k != 0) sm.apply(j, sign * static_cast<long long>(k), ovf);
       }
-      if (pass == 1) {
+      if (sign < 0) {
         // undone: continue the stream with half the step
-        pass = 0;
+        sign = 1;
         ++ev;
+        rng = resume;
         saved = rng;
         ++n_rej;
         tau = __dmul_rn(tau, 0.5);
@@ -332,7 +333,9 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         ++ev;
         break;
       }
-      pass = 1;
+      sign = -1;
+      resume = rng;
+      rng = saved;
     }
     if (ovf) break;
     if (hit) {

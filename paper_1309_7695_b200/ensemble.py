@@ -226,6 +226,30 @@ class Engine:
         self._models[key] = (h, network)
         return h
 
+    def submit(self, network: ReactionNetwork, config: SweepConfig, out: dict, *, seed_mode=abi.SEED_SWEEP,
+               rng_mode=abi.RNG_COMPAT, sim_range=None):
+        """Asynchronous sweep (kin_sweep_submit): results land in the numpy
+        arrays of `out` (keys as in sweep(); pinned memory for overlap) once
+        wait(ticket) returns."""
+        d, keep = make_sweep_desc(network, config, seed_mode=seed_mode, rng_mode=rng_mode, sim_range=sim_range)
+        o = abi.KinSweepOut(abi.ptr(out.get("traj"), C.c_double), abi.ptr(out.get("meta"), C.c_uint64),
+                            abi.ptr(out.get("status"), C.c_int32), abi.ptr(out.get("mean"), C.c_double),
+                            abi.ptr(out.get("m2"), C.c_double), abi.ptr(out.get("work"), C.c_uint64))
+        ticket = C.c_uint64()
+        err = abi.KinError()
+        rc = self.lib.kin_sweep_submit(self.ctx, self.model(network), C.byref(d), C.byref(o), C.byref(ticket),
+                                       C.byref(err))
+        _raise(rc, err)
+        self._inflight = getattr(self, "_inflight", {})
+        self._inflight[ticket.value] = (d, keep, o, out)
+        return ticket.value
+
+    def wait(self, ticket: int):
+        err = abi.KinError()
+        rc = self.lib.kin_sweep_wait(self.ctx, ticket, C.byref(err))
+        self._inflight.pop(ticket, None)
+        _raise(rc, err)
+
     def sweep(self, network: ReactionNetwork, config: SweepConfig, *, seed_mode=abi.SEED_SWEEP,
               rng_mode=abi.RNG_COMPAT, sim_range=None, want_traj=True, want_stats=True, want_work=False):
         """Bulk form: returns dict of numpy arrays (traj [S,G,N], meta [S,6],

@@ -201,6 +201,55 @@ def test_jit_kernel_bit_exact(engine, oracle, case, monkeypatch):
     assert_bit_exact(ref, got, work=bool(kw.get("want_work")))
 
 
+def _launch_kernel_ms(engine, net, d, reps=3):
+    import ctypes as C
+    lib, err, h = engine.lib, abi.KinError(), engine.model(net)
+    best = float("inf")
+    for _ in range(reps + 1):  # first launch compiles (JIT) / warms up
+        assert lib.kin_sweep_launch(engine.ctx, h, C.byref(d), 0, 0, 0, C.byref(err)) == 0, err.text()
+        assert lib.kin_sweep_sync(engine.ctx, 0, C.byref(err)) == 0, err.text()
+        a, b = C.c_double(), C.c_double()
+        assert lib.kin_sweep_kernel_ms(engine.ctx, 0, C.byref(a), C.byref(b), C.byref(err)) == 0
+        best = min(best, a.value)
+    return best
+
+
+@pytest.mark.parametrize("int_state", ["0", "1"])
+def test_jit_kernel_not_slower_than_table(engine, monkeypatch, int_state):
+    """Performance guard: the per-model JIT kernel must not lose to the
+    table-driven kernel on C4 (a register-to-memory demotion of the RNG state
+    once made the int32 JIT variant 33x slower while staying bit-exact)."""
+    monkeypatch.setenv("KIN_INT_STATE", int_state)
+    net, cfg = W.c4_config()
+    d, keep = make_sweep_desc(net, cfg, sim_range=(0, 16384))
+    monkeypatch.setenv("KIN_JIT", "0")
+    t_table = _launch_kernel_ms(engine, net, d)
+    monkeypatch.setenv("KIN_JIT", "1")
+    t_jit = _launch_kernel_ms(engine, net, d)
+    print(f"int_state={int_state}: table {t_table:.2f} ms, jit {t_jit:.2f} ms")
+    assert t_jit < 1.2 * t_table, (t_jit, t_table)
+
+
+def test_async_submit_wait_pipelined(engine):
+    """Several sweeps in flight (copy-out of one overlapping the next) give the
+    same results as blocking runs."""
+    jobs = [W.c1_config(MethodKind.TauAdaptive), W.c1_config(MethodKind.Ode), W.c2_config(points=2, runs=64),
+            W.c3_config(side=16)]
+    ref = [engine.sweep(net, cfg, want_stats=True) for net, cfg in jobs]
+    outs, tickets = [], []
+    for net, cfg in jobs:
+        P, S = len(cfg.axes[0].values) * (len(cfg.axes[1].values) if len(cfg.axes) > 1 else 1), None
+        r0 = engine.sweep(net, cfg, want_stats=True)
+        o = {k: np.zeros_like(v) for k, v in r0.items() if v is not None}
+        outs.append(o)
+        tickets.append(engine.submit(net, cfg, o))
+    for t in tickets:
+        engine.wait(t)
+    for r, o in zip(ref, outs):
+        for k in o:
+            assert np.array_equal(r[k], o[k]), k
+
+
 def test_shard_invariance(engine):
     """Per-run output independent of how the index space is cut."""
     net, cfg = W.c1_config(MethodKind.TauAdaptive)
