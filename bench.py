@@ -199,12 +199,15 @@ def sum_over_ranks(world, value: float, local: int) -> float:
     return float(t.item())
 
 
-def read_profile_traffic():
+def read_profile_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed `ncu --set full` capture summary (profiles/ncu_summary.json)."""
     p = REPO / "profiles" / "ncu_summary.json"
     if p.exists():
         try:
-            d = json.loads(p.read_text())
-            return d.get("tau_kernel_dram_bytes_per_launch"), d.get("source")
+            d = json.loads(p.read_text()).get("kernels", {}).get(kernel)
+            if d:
+                return d.get("dram_bytes_per_launch"), d.get("source")
         except Exception:
             pass
     return None, None
@@ -251,9 +254,12 @@ def bench_ours(args, world, rank, local):
     peak = C.c_double()
     check(lib.kin_measure_fp64_peak(eng.ctx, C.byref(peak), C.byref(err)))
 
+    tau_kernel = []
+
     def step():
         check(lib.kin_sweep_launch(eng.ctx, h, C.byref(d_tau), 0, 1, 0, C.byref(err)))
         check(lib.kin_sweep_sync(eng.ctx, 0, C.byref(err)))
+        tau_kernel.append(lib.kin_sweep_kernel_name(eng.ctx, 0).decode())
         ms_tau = C.c_double()
         ms_st = C.c_double()
         check(lib.kin_sweep_kernel_ms(eng.ctx, 0, C.byref(ms_tau), C.byref(ms_st), C.byref(err)))
@@ -337,7 +343,8 @@ def bench_ours(args, world, rank, local):
     h2d = 2 * (bytes_axes + 31 * 1024)  # sweep tables + packed model tables, both methods
     d2h = 2 * (per * G * N * 8 + per * 6 * 8 + per * 4)
 
-    traffic, traffic_src = read_profile_traffic()
+    kname = tau_kernel[-1]
+    traffic, traffic_src = read_profile_traffic(kname)
     res = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -348,7 +355,7 @@ def bench_ours(args, world, rank, local):
         "gpu_launches": 4 * args.steps,
         "breakdown": {"tau_kernel_ms": tau_avg_ms, "step_ms": float(np.mean(step_ms)),
                       "tau_leaps_per_sim": float(meta[:, 0].mean()), "ssa_fallback_steps_per_sim": float(meta[:, 3].mean())},
-        "roofline": {"bound": "fp64", "kernel": "stochastic_kernel (tau-leap + SSA fallback)",
+        "roofline": {"bound": "fp64", "kernel": f"{kname} (tau-leap + SSA fallback)",
                      "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value,
                      "peak_source": "measured DFMA microbenchmark (kin_measure_fp64_peak) in this run; FP64 is not in MEASURED_PEAKS.json",
                      "algorithmic_flops_per_launch": tau_flops,

@@ -227,6 +227,10 @@ void* kin_ctx_stream(kin_ctx* ctx, int32_t device_slot);
    after kin_sweep_sync. */
 int kin_sweep_kernel_ms(kin_ctx* ctx, int32_t device_slot, double* sim_ms,
                         double* stats_ms, kin_error* err);
+/* Name of the simulation kernel the last launch on this slot ran (as ncu
+   lists it: "kin_jit_stoch", "stochastic_kernel", "stochastic_group_kernel",
+   "dopri5_kernel", "lsoda_kernel"); "" before the first launch. */
+const char* kin_sweep_kernel_name(kin_ctx* ctx, int32_t device_slot);
 
 /* ---- seams (device unit kernels; SPEC "from_uniforms"/"from_counts") ----- */
 uint64_t kin_splitmix64_mix(uint64_t v);                       /* rng.hpp:8-11 */

@@ -85,7 +85,7 @@ class KinError(C.Structure):
 ABI_SYMBOLS = (
     "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
     "kin_model_free", "kin_sweep_size", "kin_sweep_plan", "kin_sweep_run", "kin_sweep_submit", "kin_sweep_wait", "kin_sweep_launch", "kin_sweep_sync",
-    "kin_sweep_fetch", "kin_ctx_stream", "kin_sweep_kernel_ms", "kin_splitmix64_mix", "kin_derive_run_seed",
+    "kin_sweep_fetch", "kin_ctx_stream", "kin_sweep_kernel_ms", "kin_sweep_kernel_name", "kin_splitmix64_mix", "kin_derive_run_seed",
     "kin_device_rng_draws", "kin_jit_check", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
 )
 
@@ -109,6 +109,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "kin_sweep_fetch": (C.c_int, [vp, C.c_int32, C.POINTER(KinSweepOut), E]),
         "kin_ctx_stream": (vp, [vp, C.c_int32]),
         "kin_sweep_kernel_ms": (C.c_int, [vp, C.c_int32, f64p, f64p, E]),
+        "kin_sweep_kernel_name": (C.c_char_p, [vp, C.c_int32]),
         "kin_splitmix64_mix": (C.c_uint64, [C.c_uint64]),
         "kin_derive_run_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
         "kin_device_rng_draws": (C.c_int, [vp, C.c_uint64, C.c_int32, C.c_double, C.c_int32, u64p, E]),

@@ -424,6 +424,7 @@ struct Buffers {
   KinSweepDev last_SD{};
   KinOutDev last_O{};
   bool last_int_state = false, last_count = false, pending_check = false, last_jit = false;
+  const char* kernel_name = "";
   uint64_t last_base = 0, last_S = 0;
   int last_gn = 0;
   void release() {
@@ -639,6 +640,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   const int kind = d->method.kind;
   if (kind == KIN_METHOD_ODE) {
     e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
+    bf.kernel_name = "dopri5_kernel";
   } else if (kind == KIN_METHOD_LSODA) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
     if (kin::lsoda_smem_bytes(*T, SD) > 227 * 1024) {
@@ -646,6 +648,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
       return KIN_ERR_INPUT;
     }
     e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, sl.stream);
+    bf.kernel_name = "lsoda_kernel";
   } else {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
     KIN_CUDA(bf.ovf.ensure(1), "cudaMalloc overflow flag");
@@ -658,6 +661,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
     if (lanes != 1) {
       e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, bf.counter.p, sl.stream);
       bf.last_int_state = false;
+      bf.kernel_name = "stochastic_group_kernel";
     } else {
       // int32 amounts when every initial amount is far inside int32 range
       // (KIN_INT_STATE=0 forces doubles)
@@ -678,6 +682,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
       if (e == cudaSuccess && !used)
         e = kin::launch_stochastic(*T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, sl.stream);
       bf.last_jit = used;
+      bf.kernel_name = used ? "kin_jit_stoch" : "stochastic_kernel";
       bf.last_int_state = int_state;
     }
     if (bf.last_int_state) {
@@ -1113,6 +1118,11 @@ int kin_sweep_kernel_ms(kin_ctx* ctx, int32_t slot, double* sim_ms, double* stat
   if (sim_ms) *sim_ms = a;
   if (stats_ms) *stats_ms = bm.timed_stats ? b : 0.0;
   return KIN_OK;
+}
+
+const char* kin_sweep_kernel_name(kin_ctx* ctx, int32_t slot) {
+  if (!ctx || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) return "";
+  return ctx->slots[slot]->main.kernel_name;
 }
 
 int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean, int32_t n, uint64_t* out_bits,

@@ -179,6 +179,9 @@ std::string generate_policy(const JitModel& m) {
   return o.str();
 }
 
+const char* const kNvrtcOpts[5] = {"--gpu-architecture=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo",
+                                   "-default-device"};
+
 // NVRTC: policy source -> sm_100a cubin.  Returns false with the log on error.
 bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_state, std::vector<char>* cubin,
                    std::string* log) {
@@ -202,8 +205,8 @@ bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_
   const std::string d_xt = std::string("-DXT_=") + (int_state ? "int" : "double");
   const std::string d_c = std::string("-DKCOUNT_=") + (count ? "true" : "false");
   const std::string d_p = std::string("-DKPHILOX_=") + (philox ? "true" : "false");
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-fmad=false", "-std=c++17", "-lineinfo",
-                        "-default-device",             d_xt.c_str(), d_c.c_str(), d_p.c_str()};
+  const char* opts[] = {kNvrtcOpts[0], kNvrtcOpts[1], kNvrtcOpts[2], kNvrtcOpts[3], kNvrtcOpts[4],
+                        d_xt.c_str(),  d_c.c_str(),   d_p.c_str()};
   const nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
   size_t log_size = 0;
   nvrtcGetProgramLogSize(prog, &log_size);
@@ -247,7 +250,10 @@ std::string cache_path(const std::string& key) {
     if (!home) return "";
     d = std::string(home) + "/.cache/kin_b200_jit";
   }
-  std::string full = key;
+  int major = 0, minor = 0;
+  nvrtcVersion(&major, &minor);  // statically linked (Makefile), but keyed anyway
+  std::string full = key + "|nvrtc " + std::to_string(major) + "." + std::to_string(minor);
+  for (const char* o : kNvrtcOpts) full += std::string("|") + o;
   for (const auto& h : kJitHeaders) full += h.text;
   uint64_t hsh = 1469598103934665603ULL;  // FNV-1a 64
   for (unsigned char c : full) hsh = (hsh ^ c) * 1099511628211ULL;

@@ -16,6 +16,6 @@ if [ "${SKIP_NCU:-0}" = "0" ]; then
   timeout 300 python tools/quick_time.py c4_tau > gpurun_out/${TAG}_qt.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
       python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_ncu_launches.log 2>&1; echo "ncu launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stochastic_kernel -s 1 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:kin_jit_stoch|stochastic_kernel" -s 1 -c 1 \
       -o gpurun_out/${TAG}_tau python tools/quick_time.py c4_tau > gpurun_out/${TAG}_ncu_full.log 2>&1; echo "ncu full rc=$?"
 fi
