@@ -63,6 +63,19 @@ std::string dlit(double v) {
 
 // Largest model whose divergent SSA updates are emitted as a switch.
 constexpr int kSwitchMaxReactions = 8;
+// Largest number of species with a nu row whose select_tau is fully inlined.
+constexpr int kInlineTauMaxSpecies = 8;
+// Largest nnz(nu) whose leap update is a switch of straight-line updates.
+constexpr int kSwitchApplyMaxNnz = 16;
+// Largest M whose all_props is straight-line (above: uniform loop over prop(j)).
+constexpr int kInlinePropsMaxReactions = 1 << 30;
+
+// Development knobs (KIN_JIT_TAU_INLINE / KIN_JIT_APPLY_SWITCH override the
+// thresholds; they change the generated source, hence the cache key).
+int jit_knob(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v && *v ? std::atoi(v) : dflt;
+}
 
 // Model policy source for one model structure (see kin_stochastic_impl.cuh
 // TableModel for the reference semantics of each member).
@@ -111,41 +124,75 @@ std::string generate_policy(const JitModel& m) {
     o << " return aj;\n";
   }
   o << "    }\n    return 0.0;\n  }\n";
-  o << "  __device__ __forceinline__ double all_props(int) const {\n    double a0 = 0.0, aj;\n";
-  for (int j = 0; j < m.m; ++j)
-    o << "    aj = prop(" << j << "); a[" << j << " * B] = aj; a0 = __dadd_rn(a0, aj);\n";
-  o << "    return a0;\n  }\n";
+  if (m.m <= jit_knob("KIN_JIT_PROPS_INLINE", kInlinePropsMaxReactions)) {
+    o << "  __device__ __forceinline__ double all_props(int) const {\n    double a0 = 0.0, aj;\n";
+    for (int j = 0; j < m.m; ++j)
+      o << "    aj = prop(" << j << "); a[" << j << " * B] = aj; a0 = __dadd_rn(a0, aj);\n";
+    o << "    return a0;\n  }\n";
+  } else {
+    o << "  __device__ __forceinline__ double all_props(int) const {\n    double a0 = 0.0;\n"
+         "#pragma unroll 1\n    for (int j = 0; j < " << m.m << "; ++j) { const double aj = prop(j); a[j * B] = aj; a0 = __dadd_rn(a0, aj); }\n"
+         "    return a0;\n  }\n";
+  }
   o << "  __device__ __forceinline__ double sum_props(int) const {\n    double a0 = 0.0;\n";
   for (int j = 0; j < m.m; ++j) o << "    a0 = __dadd_rn(a0, a[" << j << " * B]);\n";
   o << "    return a0;\n  }\n";
-  // select_tau (stochastic.hpp:40-44): per species, its nu row in reaction order
+  // select_tau (stochastic.hpp:40-44): per species, its nu row in reaction
+  // order.  Straight-line code for every species would inline tau_bound N times
+  // and overflow the instruction cache on larger models, so above
+  // kInlineTauMaxSpecies the species are walked by a warp-uniform, non-unrolled
+  // loop whose switch holds only each species' mu/sigma^2 sums (one tau_bound).
+  int n_act = 0;
+  for (int i = 0; i < m.n; ++i) n_act += m.row_ptr[i] != m.row_ptr[i + 1];
   o << "  template <bool kCount> __device__ __forceinline__ double select_tau(double eps, uint64_t& flops) const {\n"
        "    double tau = KIN_INF;\n";
-  for (int i = 0; i < m.n; ++i) {
-    const int p0 = m.row_ptr[i], p1 = m.row_ptr[i + 1];
-    if (p0 == p1) {
-      continue;  // mu = sigma2 = 0 exactly: skipped by the reference too
+  if (n_act <= jit_knob("KIN_JIT_TAU_INLINE", kInlineTauMaxSpecies)) {
+    for (int i = 0; i < m.n; ++i) {
+      const int p0 = m.row_ptr[i], p1 = m.row_ptr[i + 1];
+      if (p0 == p1) continue;  // mu = sigma2 = 0 exactly: skipped by the reference too
+      o << "    { double mu = 0.0, s2 = 0.0;";
+      for (int p = p0; p < p1; ++p) {
+        const int j = m.row_reaction[p], d = m.row_delta[p];
+        o << " mu = __dadd_rn(mu, __dmul_rn(" << dlit(d) << ", a[" << j << " * B]));"
+          << " s2 = __dadd_rn(s2, __dmul_rn(" << dlit(static_cast<double>(d) * d) << ", a[" << j << " * B]));";
+      }
+      o << "\n      if (kCount) flops += " << 4 * (p1 - p0) << ";\n"
+        << "      if (!(mu == 0.0 && s2 == 0.0)) tau = tau_bound<kCount>(tau, eps, xv(" << i << "), " << dlit(m.g[i])
+        << ", mu, s2, flops); }\n";
     }
-    o << "    { double mu = 0.0, s2 = 0.0;";
-    for (int p = p0; p < p1; ++p) {
-      const int j = m.row_reaction[p], d = m.row_delta[p];
-      o << " mu = __dadd_rn(mu, __dmul_rn(" << dlit(d) << ", a[" << j << " * B]));"
-        << " s2 = __dadd_rn(s2, __dmul_rn(" << dlit(static_cast<double>(d) * d) << ", a[" << j << " * B]));";
+  } else {
+    o << "#pragma unroll 1\n    for (int q = 0; q < " << n_act << "; ++q) {\n"
+         "      double mu = 0.0, s2 = 0.0, g = 1.0; int sp = 0, nt = 0;\n      switch (q) {\n";
+    int q = 0;
+    for (int i = 0; i < m.n; ++i) {
+      const int p0 = m.row_ptr[i], p1 = m.row_ptr[i + 1];
+      if (p0 == p1) continue;
+      o << "        case " << q++ << ": sp = " << i << "; g = " << dlit(m.g[i]) << "; nt = " << 4 * (p1 - p0) << ";";
+      for (int p = p0; p < p1; ++p) {
+        const int j = m.row_reaction[p], d = m.row_delta[p];
+        o << " mu = __dadd_rn(mu, __dmul_rn(" << dlit(d) << ", a[" << j << " * B]));"
+          << " s2 = __dadd_rn(s2, __dmul_rn(" << dlit(static_cast<double>(d) * d) << ", a[" << j << " * B]));";
+      }
+      o << " break;\n";
     }
-    o << "\n      if (kCount) flops += " << 4 * (p1 - p0) << ";\n"
-      << "      if (!(mu == 0.0 && s2 == 0.0)) tau = tau_bound<kCount>(tau, eps, xv(" << i << "), " << dlit(m.g[i])
-      << ", mu, s2, flops); }\n";
+    o << "      }\n      if (kCount) flops += nt;\n"
+         "      if (!(mu == 0.0 && s2 == 0.0)) tau = tau_bound<kCount>(tau, eps, xv(sp), g, mu, s2, flops);\n    }\n";
   }
   o << "    return tau;\n  }\n";
-  // state updates
-  o << "  __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const {\n    switch (j) {\n";
-  for (int j = 0; j < m.m; ++j) {
-    o << "      case " << j << ":";
-    for (int p = m.col_ptr[j]; p < m.col_ptr[j + 1]; ++p)
-      o << " upd(" << m.col_species[p] << ", " << m.col_delta[p] << ", k, ovf);";
-    o << " break;\n";
+  // leap updates x += nu[:, j] * k (j warp-uniform): a switch of straight-line
+  // updates for small models, the CSC walk above kSwitchApplyMaxNnz (code size)
+  if (m.col_ptr[m.m] <= jit_knob("KIN_JIT_APPLY_SWITCH", kSwitchApplyMaxNnz)) {
+    o << "  __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const {\n    switch (j) {\n";
+    for (int j = 0; j < m.m; ++j) {
+      o << "      case " << j << ":";
+      for (int p = m.col_ptr[j]; p < m.col_ptr[j + 1]; ++p)
+        o << " upd(" << m.col_species[p] << ", " << m.col_delta[p] << ", k, ovf);";
+      o << " break;\n";
+    }
+    o << "    }\n  }\n";
+  } else {
+    o << "  __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const { TableModel<XT>{T, x, a, av}.apply(j, k, ovf); }\n";
   }
-  o << "    }\n  }\n";
   // SSA events: `sel` differs from lane to lane, and a switch over reactions
   // serialises a warp over every distinct case it holds (up to M of them).
   // Small models keep the straight-line cases; larger ones walk the tables
