@@ -200,7 +200,7 @@ int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t runs_per_point, int32_t n_
                    int32_t max_chunks, uint64_t* bounds, int32_t* n_chunks, kin_error* err);
 
 /* Asynchronous form of kin_sweep_run: enqueue the sweep (kernels on the
-   device's compute stream, transposes + copy-out into `out` on its copy stream)
+   device's compute stream, copy-out into `out` on its copy stream)
    and return a ticket at once; kin_sweep_wait blocks until the results are in
    `out` and reports errors exactly as kin_sweep_run.  Copy-out of one sweep
    overlaps the kernels of the next.  Outputs must stay valid until the wait;

@@ -408,7 +408,7 @@ struct DevBuf {
 // owns one Buffers for the device-resident API (kin_sweep_launch/fetch) and a
 // pool reused by asynchronous jobs (kin_sweep_submit/wait).
 struct Buffers {
-  DevBuf<double> traj, traj_t, mean, m2, axis, grid;
+  DevBuf<double> traj, mean, m2, axis, grid;
   DevBuf<uint64_t> meta, work;
   DevBuf<int32_t> status;
   DevBuf<unsigned long long> counter;
@@ -428,7 +428,7 @@ struct Buffers {
   uint64_t last_base = 0, last_S = 0;
   int last_gn = 0;
   void release() {
-    traj.release(); traj_t.release(); mean.release(); m2.release(); axis.release(); grid.release();
+    traj.release(); mean.release(); m2.release(); axis.release(); grid.release();
     meta.release(); work.release(); status.release(); counter.release(); ovf.release();
     if (ovf_host) cudaFreeHost(ovf_host);
     ovf_host = nullptr;
@@ -443,7 +443,7 @@ struct Buffers {
 struct Slot {
   int device = 0;
   cudaStream_t stream = nullptr;       // kernels
-  cudaStream_t copy_stream = nullptr;  // transposes + copy-out of async jobs
+  cudaStream_t copy_stream = nullptr;  // copy-out of async jobs
   DevBuf<double> lgamma_tab;  // glibc lgamma(k+1), k < KIN_LGAMMA_N
   DevBuf<double> lsoda_co;    // cfode elco/tesco
   void* stage = nullptr;
@@ -702,7 +702,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   if (want_stats && nP) {
     KIN_CUDA(bf.mean.ensure(gn * nP), "cudaMalloc mean");
     KIN_CUDA(bf.m2.ensure(gn * nP), "cudaMalloc m2");
-    e = kin::launch_point_stats(bf.traj.p, S, static_cast<int>(gn), L.R, P0 * L.R - s0, nP, bf.mean.p, bf.m2.p,
+    e = kin::launch_point_stats(bf.traj.p, static_cast<int>(gn), L.R, P0 * L.R - s0, nP, bf.mean.p, bf.m2.p,
                                 sl.stream);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
     KIN_CUDA(cudaEventRecord(bf.tev[2], sl.stream), "event");
@@ -740,8 +740,7 @@ int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
                                          false, sl.stream);
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel relaunch");
   if (bf.have_stats) {
-    e = kin::launch_point_stats(bf.traj.p, bf.last_S, bf.last_gn, bf.R, bf.last_base, bf.nP, bf.mean.p, bf.m2.p,
-                                sl.stream);
+    e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.R, bf.last_base, bf.nP, bf.mean.p, bf.m2.p, sl.stream);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel relaunch");
   }
   KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
@@ -758,12 +757,8 @@ int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_sim,
   const uint64_t S = bf.s1 - bf.s0;
   const size_t gn = static_cast<size_t>(bf.G) * bf.N;
   const uint64_t so = bf.s0 - base_sim;
-  if (out->traj && S && gn) {
-    KIN_CUDA(bf.traj_t.ensure(gn * S), "cudaMalloc transpose");
-    cudaError_t e = kin::launch_transpose_traj(bf.traj.p, bf.traj_t.p, S, static_cast<int>(gn), st);
-    if (e != cudaSuccess) return cuda_fail(err, e, "transpose launch");
-    if (int rc = copy_d2h(sl, st, out->traj + so * gn, bf.traj_t.p, gn * S * sizeof(double), sync, err)) return rc;
-  }
+  if (out->traj && S && gn)  // device layout == host layout [S][G][N]: one contiguous copy
+    if (int rc = copy_d2h(sl, st, out->traj + so * gn, bf.traj.p, gn * S * sizeof(double), sync, err)) return rc;
   if (out->meta && S)
     if (int rc = copy_d2h(sl, st, out->meta + so * 6, bf.meta.p, S * 6 * sizeof(uint64_t), sync, err)) return rc;
   if (out->status && S)

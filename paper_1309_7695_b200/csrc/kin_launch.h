@@ -32,13 +32,11 @@ size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S);
 cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, const double* coeffs,
                          unsigned long long* counter, cudaStream_t stream);
 
-// kin_post.cu: layout kernels and utilities.
-// traj_dev [G*N][n_local] (simulation-fastest) -> dst [n_local][G*N]
-cudaError_t launch_transpose_traj(const double* traj_dev, double* dst, uint64_t n_local, int gn, cudaStream_t stream);
-// per-point Welford over runs (ascending run order) -> mean/m2 [P][G*N]
-cudaError_t launch_point_stats(const double* traj_dev, uint64_t n_local, int gn, uint64_t runs,
-                               uint64_t first_point_offset, uint64_t n_points, double* mean, double* m2,
-                               cudaStream_t stream);
+// kin_post.cu: statistics and utilities.
+// per-point Welford over runs (ascending run order) of traj_dev [n_local][G*N]
+// starting at local simulation first_sim -> mean/m2 [P][G*N]
+cudaError_t launch_point_stats(const double* traj_dev, int gn, uint64_t runs, uint64_t first_sim, uint64_t n_points,
+                               double* mean, double* m2, cudaStream_t stream);
 cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, const double* lgamma_tab,
                              cudaStream_t stream);
 cudaError_t measure_fp64_peak(cudaStream_t stream, double* tflops);

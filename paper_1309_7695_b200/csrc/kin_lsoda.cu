@@ -214,7 +214,6 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
                           double* smem_base, int* ismem_base, int B, int tid) {
   const uint64_t sim = S.sim_begin + s;
   const int n = T.n, m = T.m, G = T.n_grid;
-  const uint64_t nloc = S.n_local;
   Lsoda L{T, S, co, B, n, m};
   double* p = smem_base + tid;
   L.Z = p;
@@ -257,11 +256,11 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   int status = 0;
 
   auto emit = [&](int g, const double* vv) {
-    double* o = O.traj + static_cast<size_t>(g) * n * nloc + s;
+    double* o = O.traj + (static_cast<size_t>(s) * G + g) * n;  // [sim][g][n]
     for (int i = 0; i < n; ++i) {
       double vi = vv[i * B];
       if (vi < 0.0) { vi = 0.0; floored = true; }
-      o[static_cast<size_t>(i) * nloc] = vi;
+      o[i] = vi;
     }
   };
 

@@ -73,7 +73,6 @@ __global__ void __launch_bounds__(128) dopri5_kernel(const __grid_constant__ Kin
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * gpb + grp;
   if (s >= S.n_local) return;  // whole groups retire together
   const int N = T.n, M = T.m, G = T.n_grid;
-  const uint64_t nloc = S.n_local;
   const uint64_t sim = S.sim_begin + s;
   Group<L> grpc;
   grpc.mask = (L == 32) ? 0xFFFFFFFFu : (((1u << L) - 1u) << ((threadIdx.x & 31) / L * L));
@@ -144,11 +143,11 @@ __global__ void __launch_bounds__(128) dopri5_kernel(const __grid_constant__ Kin
     }
   };
   auto emit = [&](int g, const double* v) {
-    double* o = O.traj + static_cast<size_t>(g) * N * nloc + s;
+    double* o = O.traj + (static_cast<size_t>(s) * G + g) * N;  // [sim][g][n]
 #pragma unroll
     for (int q = 0; q < SL; ++q) {
       const int i = lane + q * L;
-      if (i < N) o[static_cast<size_t>(i) * nloc] = v[q];
+      if (i < N) o[i] = v[q];
     }
   };
 

@@ -1,15 +1,15 @@
-// kin_post.cu — output-layout kernels (K6 of DESIGN.md) and device utilities.
+// kin_post.cu — statistics kernel (K6 of DESIGN.md) and device utilities.
 //
-//   transpose_traj  [G*N][S] (simulation-fastest, as the simulators store it for
-//                   coalescing) -> [S][G][N] (Trajectory::samples per run,
-//                   model.hpp:113-120) before the single D2H copy.
+// The simulators write trajectories directly in the host layout [S][G][N]
+// (Trajectory::samples per run, model.hpp:113-120), so results leave the GPU
+// with one contiguous D2H copy and no transpose.
 //   point_stats     EnsembleStatistics per sweep point (ensemble.hpp:20-57):
 //                   Welford add over the point's runs in ascending run order
 //                   (the workers=1 merge order), written grid-major
 //                   [P][G][N].  Compiled with -fmad=false so it rounds exactly
-//                   like the oracle's welford_add.
-// Both are HBM-bound 32x32 shared-memory tile transposes (coalesced on both
-// sides).
+//                   like the oracle's welford_add.  HBM-bound streaming read.
+#include <algorithm>
+
 #include "kin_device.cuh"
 #include "kin_launch.h"
 
@@ -17,65 +17,28 @@ namespace kin {
 
 namespace {
 
-constexpr int TILE = 32;
-constexpr int ROWS = 8;
 
-__global__ void __launch_bounds__(TILE* ROWS) transpose_kernel(const double* __restrict__ src,
-                                                               double* __restrict__ dst, uint64_t n_cols,
-                                                               int n_rows) {
-  // src: [n_rows][n_cols], dst: [n_cols][n_rows]
-  __shared__ double tile[TILE][TILE + 1];
-  const uint64_t c0 = static_cast<uint64_t>(blockIdx.x) * TILE;
-  const int r0 = blockIdx.y * TILE;
-#pragma unroll
-  for (int k = 0; k < TILE; k += ROWS) {
-    const int r = r0 + threadIdx.y + k;
-    const uint64_t c = c0 + threadIdx.x;
-    if (r < n_rows && c < n_cols) tile[threadIdx.y + k][threadIdx.x] = __ldcs(src + static_cast<uint64_t>(r) * n_cols + c);
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < TILE; k += ROWS) {
-    const uint64_t c = c0 + threadIdx.y + k;
-    const int r = r0 + threadIdx.x;
-    if (r < n_rows && c < n_cols) __stcs(dst + c * n_rows + r, tile[threadIdx.x][threadIdx.y + k]);
-  }
-}
-
-__global__ void __launch_bounds__(TILE* ROWS) stats_kernel(const double* __restrict__ traj, uint64_t n_local,
-                                                           int gn, uint64_t runs, uint64_t base,
-                                                           uint64_t n_points, double* __restrict__ mean,
-                                                           double* __restrict__ m2) {
-  __shared__ double tm[TILE][TILE + 1];
-  __shared__ double tq[TILE][TILE + 1];
-  const uint64_t p0 = static_cast<uint64_t>(blockIdx.x) * TILE;
-  const int q0 = blockIdx.y * TILE;
-#pragma unroll
-  for (int k = 0; k < TILE; k += ROWS) {
-    const int q = q0 + threadIdx.y + k;
-    const uint64_t p = p0 + threadIdx.x;
+// One thread per (point, grid*species element): the point's runs are
+// consecutive [sim][g][n] rows, so each run's read is coalesced across the
+// threads of a point and the [P][G][N] writes are contiguous.
+__global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ traj, int gn, uint64_t runs,
+                                                    uint64_t base, uint64_t n_points, double* __restrict__ mean,
+                                                    double* __restrict__ m2) {
+  const uint64_t total = n_points * static_cast<uint64_t>(gn);
+  for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t p = e / gn;
+    const uint64_t q = e - p * gn;
+    const double* col = traj + (base + p * runs) * gn + q;
     double mu = 0.0, s2 = 0.0;
-    if (q < gn && p < n_points) {
-      const double* col = traj + static_cast<uint64_t>(q) * n_local + base + p * runs;
-      for (uint64_t r = 0; r < runs; ++r) {
-        const double xv = col[r];
-        const double delta = __dsub_rn(xv, mu);
-        mu = __dadd_rn(mu, __ddiv_rn(delta, static_cast<double>(r + 1)));
-        s2 = __dadd_rn(s2, __dmul_rn(delta, __dsub_rn(xv, mu)));
-      }
+    for (uint64_t r = 0; r < runs; ++r) {
+      const double xv = __ldcs(col + r * gn);
+      const double delta = __dsub_rn(xv, mu);
+      mu = __dadd_rn(mu, __ddiv_rn(delta, static_cast<double>(r + 1)));
+      s2 = __dadd_rn(s2, __dmul_rn(delta, __dsub_rn(xv, mu)));
     }
-    tm[threadIdx.y + k][threadIdx.x] = mu;
-    tq[threadIdx.y + k][threadIdx.x] = s2;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < TILE; k += ROWS) {
-    const uint64_t p = p0 + threadIdx.y + k;
-    const int q = q0 + threadIdx.x;
-    if (q < gn && p < n_points) {
-      if (mean) __stcs(mean + p * gn + q, tm[threadIdx.x][threadIdx.y + k]);
-      if (m2) __stcs(m2 + p * gn + q, tq[threadIdx.x][threadIdx.y + k]);
-    }
+    if (mean) __stcs(mean + e, mu);
+    if (m2) __stcs(m2 + e, s2);
   }
 }
 
@@ -146,18 +109,12 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, doubl
 
 }  // namespace
 
-cudaError_t launch_transpose_traj(const double* traj_dev, double* dst, uint64_t n_local, int gn, cudaStream_t st) {
-  if (n_local == 0 || gn == 0) return cudaSuccess;
-  dim3 grid(static_cast<unsigned>((n_local + TILE - 1) / TILE), static_cast<unsigned>((gn + TILE - 1) / TILE));
-  transpose_kernel<<<grid, dim3(TILE, ROWS), 0, st>>>(traj_dev, dst, n_local, gn);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_point_stats(const double* traj_dev, uint64_t n_local, int gn, uint64_t runs, uint64_t base,
-                               uint64_t n_points, double* mean, double* m2, cudaStream_t st) {
+cudaError_t launch_point_stats(const double* traj_dev, int gn, uint64_t runs, uint64_t base, uint64_t n_points,
+                               double* mean, double* m2, cudaStream_t st) {
   if (n_points == 0 || gn == 0) return cudaSuccess;
-  dim3 grid(static_cast<unsigned>((n_points + TILE - 1) / TILE), static_cast<unsigned>((gn + TILE - 1) / TILE));
-  stats_kernel<<<grid, dim3(TILE, ROWS), 0, st>>>(traj_dev, n_local, gn, runs, base, n_points, mean, m2);
+  const uint64_t total = n_points * static_cast<uint64_t>(gn);
+  const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
+  stats_kernel<<<blocks, 256, 0, st>>>(traj_dev, gn, runs, base, n_points, mean, m2);
   return cudaGetLastError();
 }
 

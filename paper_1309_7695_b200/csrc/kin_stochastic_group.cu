@@ -64,7 +64,6 @@ __device__ void simulate_group(const KinTables& T, const KinSweepDev& S, const K
                                double* x, double* a, double* kk, double* av, int lane, const GroupSync<L>& gs) {
   const uint64_t sim = S.sim_begin + s;
   const int N = T.n, M = T.m, G = T.n_grid;
-  const uint64_t nloc = S.n_local;
 
   if (lane == 0) {
     uint64_t rem = sim / S.runs;
@@ -100,8 +99,8 @@ __device__ void simulate_group(const KinTables& T, const KinSweepDev& S, const K
     return a0;
   };
   auto emit = [&](int g) {
-    double* o = O.traj + static_cast<size_t>(g) * N * nloc + s;
-    for (int i = lane; i < N; i += L) o[static_cast<size_t>(i) * nloc] = x[i];
+    double* o = O.traj + (static_cast<size_t>(s) * G + g) * N;  // [sim][g][n]
+    for (int i = lane; i < N; i += L) o[i] = x[i];
   };
 
   const uint64_t seed = sim_seed(S, sim);

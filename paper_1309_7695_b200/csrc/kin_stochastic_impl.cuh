@@ -176,7 +176,6 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   const uint64_t sim = S.sim_begin + s;
   const Model sm{T, x, a, av};
   const int N = sm.n(), M = sm.m(), G = T.n_grid;
-  const uint64_t nloc = S.n_local;
 
   // Cartesian decode, last axis fastest.
   {
@@ -211,8 +210,8 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   const uint64_t F_prop = static_cast<uint64_t>(T.fprop);
 
   auto emit = [&]() {
-    double* o = O.traj + static_cast<size_t>(gi) * N * nloc + s;
-    for (int i = 0; i < N; ++i) o[static_cast<size_t>(i) * nloc] = sm.xv(i);
+    double* o = O.traj + (static_cast<size_t>(s) * G + gi) * N;  // [sim][g][n]: one contiguous run per emit
+    for (int i = 0; i < N; ++i) o[i] = sm.xv(i);
     ++gi;
   };
 

@@ -100,7 +100,7 @@ struct KinSweepDev {
 
 // Device outputs of one launch (local simulation index s in [0, n_local)).
 struct KinOutDev {
-  double* traj;      // [G][N][n_local]  simulation-fastest (coalesced stores)
+  double* traj;      // [n_local][G][N]  the host layout: each emit is one contiguous run
   uint64_t* meta;    // [n_local][6]
   int32_t* status;   // [n_local]
   uint64_t* work;    // [n_local] or null
