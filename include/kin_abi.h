@@ -169,6 +169,9 @@ typedef struct kin_error {
 typedef struct kin_ctx kin_ctx;
 typedef struct kin_model kin_model;
 
+/* Number of CUDA devices visible to this process (0 without a GPU). */
+int32_t kin_visible_devices(void);
+
 /* One host thread per device; device_ids NULL/n=0 → device 0. */
 int kin_ctx_create(const int32_t* device_ids, int32_t n_devices, kin_ctx** out,
                    kin_error* err);

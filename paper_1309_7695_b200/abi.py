@@ -81,9 +81,25 @@ class KinError(C.Structure):
         return self.message.decode(errors="replace")
 
 
-# Every symbol include/kin_abi.h declares (checked by tests/test_abi.py).
+CSV_TRAJECTORY, CSV_STATISTICS, CSV_SWEEP = 0, 1, 2  # include/kin_io.h
+
+
+class KinCsvTable(C.Structure):
+    """include/kin_io.h kin_csv_table."""
+    _fields_ = [("kind", C.c_int32), ("n_species", C.c_int32), ("species", C.POINTER(C.c_char_p)),
+                ("n_grid", C.c_int32), ("grid", f64p), ("n_axes", C.c_int32),
+                ("axis_names", C.POINTER(C.c_char_p)), ("n_points", C.c_uint64), ("point_values", f64p),
+                ("samples", f64p), ("mean", f64p), ("m2", f64p), ("n_runs", C.c_uint64)]
+
+
+# Every symbol include/*.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = (
-    "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
+    "kin_cli_main",
+    "kin_model_parse", "kin_model_text_free", "kin_model_text_desc", "kin_model_text_species_name",
+    "kin_model_text_param_name", "kin_model_text_reaction_name", "kin_model_text_species_index",
+    "kin_model_text_param_index", "kin_model_render",
+    "kin_format_double", "kin_fnv1a64", "kin_fnv1a64_update", "kin_csv_render", "kin_csv_write",
+    "kin_visible_devices", "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
     "kin_model_free", "kin_sweep_size", "kin_sweep_plan", "kin_sweep_run", "kin_sweep_submit", "kin_sweep_wait", "kin_sweep_launch", "kin_sweep_sync",
     "kin_sweep_fetch", "kin_ctx_stream", "kin_sweep_kernel_ms", "kin_sweep_kernel_name", "kin_splitmix64_mix", "kin_derive_run_seed",
     "kin_device_rng_draws", "kin_jit_check", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
@@ -94,6 +110,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     vp = C.c_void_p
     E = C.POINTER(KinError)
     sig = {
+        "kin_visible_devices": (C.c_int32, []),
         "kin_ctx_create": (C.c_int, [i32p, C.c_int32, C.POINTER(vp), E]),
         "kin_ctx_destroy": (None, [vp]),
         "kin_ctx_device_count": (C.c_int32, [vp]),
@@ -116,6 +133,21 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "kin_jit_check": (C.c_int, [C.POINTER(KinModelDesc), C.POINTER(KinSweepDesc), C.c_char_p, C.c_int32, E]),
         "kin_measure_fp64_peak": (C.c_int, [vp, f64p, E]),
         "kin_status_string": (C.c_char_p, [C.c_int32]),
+        "kin_cli_main": (C.c_int32, [C.c_int32, C.POINTER(C.c_char_p)]),
+        "kin_model_parse": (C.c_int, [C.c_char_p, C.c_int64, C.c_int32, C.POINTER(vp), E]),
+        "kin_model_text_free": (None, [vp]),
+        "kin_model_text_desc": (C.POINTER(KinModelDesc), [vp]),
+        "kin_model_text_species_name": (C.c_char_p, [vp, C.c_int32]),
+        "kin_model_text_param_name": (C.c_char_p, [vp, C.c_int32]),
+        "kin_model_text_reaction_name": (C.c_char_p, [vp, C.c_int32]),
+        "kin_model_text_species_index": (C.c_int32, [vp, C.c_char_p]),
+        "kin_model_text_param_index": (C.c_int32, [vp, C.c_char_p]),
+        "kin_model_render": (C.c_int64, [vp, C.c_char_p, C.c_int64]),
+        "kin_format_double": (C.c_int32, [C.c_double, C.c_char_p, C.c_int32]),
+        "kin_fnv1a64": (C.c_uint64, [C.c_void_p, C.c_uint64]),
+        "kin_fnv1a64_update": (C.c_uint64, [C.c_uint64, C.c_void_p, C.c_uint64]),
+        "kin_csv_render": (C.c_int64, [C.POINTER(KinCsvTable), C.c_char_p, C.c_int64, E]),
+        "kin_csv_write": (C.c_int, [C.POINTER(KinCsvTable), C.c_char_p, C.c_int32, u64p, u64p, E]),
         "kin_abi_version": (C.c_int32, []),
     }
     for name, (res, args) in sig.items():

@@ -833,6 +833,15 @@ const char* kin_status_string(int32_t code) {
 uint64_t kin_splitmix64_mix(uint64_t v) { return kin::splitmix64_mix(v); }
 uint64_t kin_derive_run_seed(uint64_t m, uint64_t i) { return kin::derive_run_seed(m, i); }
 
+int32_t kin_visible_devices(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return count;
+}
+
 int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (!out) { set_err(err, KIN_ERR_USAGE, "null output"); return KIN_ERR_USAGE; }

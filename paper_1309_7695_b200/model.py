@@ -226,6 +226,12 @@ def combinations(amount: float, stoichiometry: int) -> float:
 
 # ---- model text format (model.hpp:130-143) -----------------
 _TOKEN = re.compile(r"\s*(?:(\d+)\s+)?([A-Za-z_][A-Za-z0-9_]*|0)\s*$")
+_REAL = re.compile(r"[+-]?(?:\d+(?:\.\d*)?|\.\d+)(?:[eE][+-]?\d+)?")
+
+
+def _parse_real(text: str) -> Optional[float]:
+    """Strict decimal real (the grammar csrc/kin_model_text.cpp accepts)."""
+    return float(text) if _REAL.fullmatch(text) else None
 
 
 def _parse_side(text: str, species_ix: Dict[str, int], line: int, col0: int) -> Dict[int, int]:
@@ -277,10 +283,9 @@ def parse_model(text: str, max_order: int = 2) -> ReactionNetwork:
                 sidx[name] = len(species)
                 species.append(Species(name, int(val)))
             else:
-                try:
-                    v = float(val)
-                except ValueError:
-                    raise ParseError("parameter value must be a real number", ln, vcol) from None
+                v = _parse_real(val)
+                if v is None:
+                    raise ParseError("parameter value must be a real number", ln, vcol)
                 if not (v > 0 and math.isfinite(v)):
                     raise ParseError("parameter value must be positive", ln, vcol)
                 pidx[name] = len(params)
@@ -303,10 +308,9 @@ def parse_model(text: str, max_order: int = 2) -> ReactionNetwork:
                 rate = params[rp].value
             else:
                 rp = None
-                try:
-                    rate = float(rate_txt)
-                except ValueError:
-                    raise ParseError(f"unknown parameter '{rate_txt}'", ln, rcol) from None
+                rate = _parse_real(rate_txt)
+                if rate is None:
+                    raise ParseError(f"unknown parameter '{rate_txt}'", ln, rcol)
                 if not (rate > 0 and math.isfinite(rate)):
                     raise ParseError("rate constant must be positive", ln, rcol)
             order = sum(lhs.values())
@@ -322,7 +326,9 @@ def parse_model(text: str, max_order: int = 2) -> ReactionNetwork:
 
 
 def _fmt(v: float) -> str:
-    return repr(float(v))
+    """Shortest round-trip text, the library's format_double (io.hpp:13-16)."""
+    from .io import format_double
+    return format_double(v)
 
 
 def render_model(net: ReactionNetwork) -> str:

@@ -1,4 +1,4 @@
-"""The C-ABI library loads and exports every symbol include/kin_abi.h declares
+"""The C-ABI library loads and exports every symbol include/*.h declares
 (CPU only: no compute calls).  Also: the product path has no CPU fallback."""
 import ctypes as C
 import re
@@ -9,13 +9,15 @@ import pytest
 
 from paper_1309_7695_b200 import abi
 
-HEADER = Path(__file__).resolve().parent.parent / "include" / "kin_abi.h"
+HEADERS = sorted((Path(__file__).resolve().parent.parent / "include").glob("*.h"))
 
 
 def declared_functions():
-    text = HEADER.read_text()
-    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?[\w]+\s*\**\s*(kin_\w+)\s*\(", text, flags=re.M)))
+    names = set()
+    for h in HEADERS:
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        names |= set(re.findall(r"^\s*(?:const\s+)?[\w]+\s*\**\s*(kin_\w+)\s*\(", text, flags=re.M))
+    return sorted(names)
 
 
 def test_header_and_binding_agree():
