@@ -81,7 +81,7 @@ enum kin_method_kind {          /* Method::Kind order, ensemble.hpp:62 */
   KIN_METHOD_SSA = 0,
   KIN_METHOD_TAU_ADAPTIVE = 1,
   KIN_METHOD_TAU_FIXED = 2,
-  KIN_METHOD_CLE = 3,           /* not provided by this engine (KIN_ERR_INPUT) */
+  KIN_METHOD_CLE = 3,           /* Chemical Langevin, Euler-Maruyama with step tau (stochastic.hpp:64-75) */
   KIN_METHOD_ODE = 4,           /* Dopri5 RRE, deterministic.hpp:38-95 */
   KIN_METHOD_HYBRID = 5,        /* not provided by this engine (KIN_ERR_INPUT) */
   KIN_METHOD_LSODA = 6          /* extension: Adams/BDF with stiffness switching */

@@ -2,7 +2,7 @@
  * (cli.hpp:15-17 run_cli: "Entry point behind the binary; separated so tests
  * can invoke the CLI in-process").  bin/kinetics-b200 is a thin main() over it.
  *
- *   simulate --model PATH --method {ssa|tau|ode|lsoda|cle|hybrid} --t-end T
+ *   simulate --model PATH --method {ssa|tau|cle|ode|lsoda} --t-end T
  *            --samples N --seed S [--runs R] [--epsilon E] [--tau T]
  *            [--rtol R] [--atol A] [--tol R[,A]] [--max-steps N]
  *            [--rng compat|philox] [--max-order 2|3] [--workers N] --out PATH

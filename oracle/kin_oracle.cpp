@@ -311,6 +311,99 @@ int simulate_stochastic(const Network& net, const double* rates, const double* x
   return KIN_SIM_OK;
 }
 
+// ---- Chemical Langevin Equation, Euler-Maruyama (stochastic.hpp:64-75,
+// SPEC.md:163-171, :192) ----------------------------------------------------
+// x' = x + sum_j nu_j a_j h + sum_j nu_j sqrt(a_j h) z_j with one standard normal
+// per reaction (RngStream::draw_normal, rng.cpp:54-66: Box-Muller with a cached
+// spare), reactions in index order, each reaction's drift and noise applied as
+// one increment a_j h + sqrt(a_j h) z_j; then components below zero are clamped
+// to 0 and counted (TrajectoryMeta::clamp_events).  Steps are
+// truncated at the next grid time like the tau leaps (App. B #3), so samples are
+// states at exactly the grid times.  Philox mode: z_j is the Box-Muller cosine
+// of the two uniforms of site (seed, step, j).
+// cle_step_from_normals (stochastic.hpp:71-75) on propensities a[] evaluated at
+// x: x += nu_j (a_j h + sqrt(a_j h) z_j) for j in index order, then clamp.
+template <bool C>
+void cle_step_from_normals(const Network& net, double* x, const double* a, double h, const double* z,
+                           std::uint64_t* clamped, Work* w) {
+  for (int j = 0; j < net.m; ++j) {
+    const double d = a[j] * h;
+    const double inc = d + std::sqrt(d) * z[j];
+    if constexpr (C) w->flops += 4;
+    for (int p = net.col_ptr[j]; p < net.col_ptr[j + 1]; ++p)
+      x[net.col_species[p]] = x[net.col_species[p]] + static_cast<double>(net.col_delta[p]) * inc;
+    if constexpr (C) w->flops += 2 * static_cast<std::uint64_t>(net.col_ptr[j + 1] - net.col_ptr[j]);
+  }
+  for (int i = 0; i < net.n; ++i)
+    if (x[i] < 0.0) {
+      x[i] = 0.0;
+      ++*clamped;
+    }
+}
+
+template <bool C>
+int simulate_cle(const Network& net, const double* rates, const double* x0, const kin_method& method,
+                 double t_end, const double* grid, int n_grid, std::uint64_t seed, double* out,
+                 std::uint64_t* meta, Scratch& sc, Work* w, int rng_mode) {
+  const int n = net.n, m = net.m;
+  double* x = sc.x.data();
+  double* a = sc.a.data();
+  for (int i = 0; i < n; ++i) x[i] = x0[i];
+  for (int q = 0; q < 6; ++q) meta[q] = 0;
+  Stream rng(seed);
+  const bool philox = rng_mode == KIN_RNG_PHILOX;
+  double t = 0.0;
+  int gi = 0;
+  auto emit = [&]() {
+    std::memcpy(out + static_cast<size_t>(gi) * n, x, sizeof(double) * n);
+    ++gi;
+  };
+  while (gi < n_grid && grid[gi] <= t) emit();
+  const std::uint64_t budget = method.integrator.max_steps;
+  std::uint64_t used = 0, step = 0, n_normal = 0;
+  thread_local std::vector<double> z;
+  z.resize(static_cast<size_t>(m));
+  while (t < t_end) {
+    if (++used > budget) return KIN_SIM_BUDGET;
+    const double t_stop = (gi < n_grid && grid[gi] < t_end) ? grid[gi] : t_end;
+    double h = method.tau;
+    bool hit = false;
+    const double gap = t_stop - t;
+    if constexpr (C) w->flops += 1;
+    if (!(h < gap)) { h = gap; hit = true; }
+    propensities<C>(net, rates, x, a, w);
+    for (int j = 0; j < m; ++j) {
+      if (philox) {
+        PhiloxSite src(seed, step, static_cast<std::uint32_t>(j));
+        const double u1 = src.draw_uniform();
+        const double u2 = src.draw_uniform();
+        z[j] = std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+        if constexpr (C) w->flops += 4 + 3 + 1 + 2;
+      } else {  // RngStream::draw_normal: a fresh Box-Muller pair every second draw
+        z[j] = rng.draw_normal();
+        if constexpr (C) w->flops += (n_normal % 2 == 0) ? 4 + 3 + 1 + 2 + 2 : 0;
+        ++n_normal;
+      }
+    }
+    std::uint64_t clamped = 0;
+    cle_step_from_normals<C>(net, x, a, h, z.data(), &clamped, w);
+    meta[2] += clamped;
+    for (int i = 0; i < n; ++i)
+      if (!std::isfinite(x[i])) return KIN_SIM_NONFINITE;
+    ++step;
+    if (hit) {
+      t = t_stop;
+    } else {
+      t = t + h;
+      if constexpr (C) w->flops += 1;
+    }
+    ++meta[0];
+    while (gi < n_grid && grid[gi] <= t) emit();
+  }
+  while (gi < n_grid) emit();
+  return KIN_SIM_OK;
+}
+
 // ---- Dormand-Prince 5(4) (deterministic.hpp:26-83) --------------------------
 // Coefficients: Dormand & Prince (1980); PI control, FSAL and the dense output
 // follow Hairer, Norsett & Wanner's DOPRI5 conventions.
@@ -980,7 +1073,8 @@ void decode_sim(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, 
 
 int validate_sweep(const Network& net, const kin_sweep_desc* d, std::string* msg) {
   const kin_method& M = d->method;
-  if (M.kind == KIN_METHOD_CLE || M.kind == KIN_METHOD_HYBRID) { *msg = "method not provided by this engine (CLE/hybrid are out of scope)"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_HYBRID) { *msg = "method not provided by this engine (hybrid is out of scope)"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_CLE && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
   if (M.kind < 0 || M.kind > KIN_METHOD_LSODA) { *msg = "unknown method kind"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_LSODA && !kLsodaAvailable) { *msg = "LSODA not built"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_TAU_FIXED && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
@@ -1025,6 +1119,9 @@ int run_one(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, doub
     return integrate_rre<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
   if (M.kind == KIN_METHOD_LSODA)
     return integrate_lsoda<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
+  if (M.kind == KIN_METHOD_CLE)
+    return simulate_cle<C>(net, sc.rates.data(), x0, M, d->t_end, d->grid, d->n_grid, seed, traj, meta, sc, w,
+                           d->rng_mode);
   return simulate_stochastic<C>(net, sc.rates.data(), x0, M, d->t_end, d->grid, d->n_grid, seed, traj, meta, sc, w,
                                 d->rng_mode);
 }
@@ -1163,6 +1260,20 @@ int kin_oracle_tau_leap_from_counts(const kin_model_desc* d, const double* x, co
   }
   *rejected = 0;
   for (int i = 0; i < net.n; ++i) if (xout[i] < 0.0) *rejected = 1;
+  return KIN_OK;
+}
+
+int kin_oracle_cle_step(const kin_model_desc* d, const double* x, double h, const double* z, double* xout,
+                        uint64_t* clamped, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  std::vector<double> r(net.m), a(net.m);
+  for (int j = 0; j < net.m; ++j) r[j] = net.rate_param[j] >= 0 ? net.params[net.rate_param[j]] : net.rate_base[j];
+  propensities<false>(net, r.data(), x, a.data(), nullptr);
+  for (int i = 0; i < net.n; ++i) xout[i] = x[i];
+  std::uint64_t c = 0;
+  cle_step_from_normals<false>(net, xout, a.data(), h, z, &c, nullptr);
+  *clamped = c;
   return KIN_OK;
 }
 

@@ -59,6 +59,7 @@ def load(ref: bool = False) -> C.CDLL:
     lib.kin_oracle_ssa_step_from_uniforms.argtypes = [M, f64p, C.c_double, C.c_double, f64p, C.POINTER(C.c_int), E]
     lib.kin_oracle_tau_leap_from_counts.argtypes = [M, f64p, u64p, f64p, C.POINTER(C.c_int), E]
     lib.kin_oracle_apply_reaction.argtypes = [M, f64p, C.c_int, f64p, E]
+    lib.kin_oracle_cle_step.argtypes = [M, f64p, C.c_double, f64p, f64p, u64p, E]
     lib.kin_oracle_rre_rhs.argtypes = [M, f64p, f64p, E]
     lib.kin_oracle_stats_merge.restype = None
     lib.kin_oracle_stats_merge.argtypes = [u64p, f64p, f64p, C.c_uint64, f64p, f64p, C.c_uint64]
@@ -145,6 +146,18 @@ def apply_reaction(net, x, j):
     err = abi.KinError()
     rc = load().kin_oracle_apply_reaction(C.byref(net.desc()), abi.ptr(x, C.c_double), j, abi.ptr(out, C.c_double), C.byref(err))
     return (rc, out, err.text())
+
+
+def cle_step(net, x, h, z):
+    """cle_step_from_normals (stochastic.hpp:71-75): returns (x', clamped)."""
+    x, z = _f64(x), _f64(z)
+    out = np.zeros_like(x)
+    cl = C.c_uint64()
+    err = abi.KinError()
+    rc = load().kin_oracle_cle_step(C.byref(net.desc()), abi.ptr(x, C.c_double), float(h), abi.ptr(z, C.c_double),
+                                    abi.ptr(out, C.c_double), C.byref(cl), C.byref(err))
+    assert rc == 0, err.text()
+    return out, int(cl.value)
 
 
 def rre_rhs(net, x):

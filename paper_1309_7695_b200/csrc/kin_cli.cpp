@@ -35,7 +35,7 @@ struct Fail {
 [[noreturn]] void input(const std::string& m) { throw Fail{KIN_EXIT_INPUT, m}; }
 
 const char* kUsage =
-    "usage: kinetics-b200 simulate --model PATH --method {ssa|tau|ode|lsoda|cle|hybrid} --t-end T --samples N\n"
+    "usage: kinetics-b200 simulate --model PATH --method {ssa|tau|cle|ode|lsoda} --t-end T --samples N\n"
     "                              --seed S [--runs R] [--epsilon E] [--tau T] [--rtol R] [--atol A]\n"
     "                              [--tol R[,A]] [--max-steps N] [--rng compat|philox] [--max-order 2|3]\n"
     "                              [--workers N] --out PATH\n"
@@ -96,6 +96,7 @@ struct MethodSpec {
     else if (name == "tau") m.kind = tau > 0.0 ? KIN_METHOD_TAU_FIXED : KIN_METHOD_TAU_ADAPTIVE;
     else if (name == "ode") m.kind = KIN_METHOD_ODE;
     else if (name == "lsoda") m.kind = KIN_METHOD_LSODA;
+    else if (name == "cle") m.kind = KIN_METHOD_CLE;
     m.tau = tau;
     m.epsilon = epsilon;
     m.integrator.rel_tol = rtol;
@@ -112,10 +113,11 @@ struct MethodSpec {
 };
 
 void check_method(const MethodSpec& m) {
-  if (m.name == "cle" || m.name == "hybrid")
-    input("method '" + m.name + "' is not provided by this engine (SURVEY.md section 8 scope: ssa, tau, ode, lsoda)");
-  if (m.name != "ssa" && m.name != "tau" && m.name != "ode" && m.name != "lsoda")
+  if (m.name == "hybrid")
+    input("method 'hybrid' is not provided by this engine (methods: ssa, tau, cle, ode, lsoda)");
+  if (m.name != "ssa" && m.name != "tau" && m.name != "ode" && m.name != "lsoda" && m.name != "cle")
     usage("unknown method '" + m.name + "'");
+  if (m.name == "cle" && !(m.tau > 0.0)) input("method 'cle' needs a positive step (--tau, or tau= in a sweep file)");
 }
 
 // ---- sweep file ---------------------------------------------
@@ -419,7 +421,7 @@ int cmd_simulate(const std::vector<std::string>& args, Written* result) {
     if (c != std::string::npos) ms.atol = num("--tol", t.substr(c + 1));
   }
   if (f.has("--max-steps")) ms.max_steps = unum("--max-steps", f.get("--max-steps"));
-  if (ms.name != "tau" && f.has("--tau")) usage("--tau applies to --method tau");
+  if (ms.name != "tau" && ms.name != "cle" && f.has("--tau")) usage("--tau applies to --method tau or cle");
   Common c;
   load_common(f, &c);
   check_method(ms);

@@ -168,12 +168,12 @@ int sweep_layout(const kin_sweep_desc* d, Layout* L, std::string* msg) {
 
 int validate_sweep(const HostModel& net, const kin_sweep_desc* d, const Layout& L, std::string* msg) {
   const kin_method& M = d->method;
-  if (M.kind == KIN_METHOD_CLE || M.kind == KIN_METHOD_HYBRID) {
-    *msg = "method not provided by this engine (CLE/hybrid are out of scope)";
+  if (M.kind == KIN_METHOD_HYBRID) {
+    *msg = "method not provided by this engine (hybrid is out of scope)";
     return KIN_ERR_INPUT;
   }
   if (M.kind < 0 || M.kind > KIN_METHOD_LSODA) { *msg = "unknown method kind"; return KIN_ERR_INPUT; }
-  if (M.kind == KIN_METHOD_TAU_FIXED && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
+  if ((M.kind == KIN_METHOD_TAU_FIXED || M.kind == KIN_METHOD_CLE) && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_TAU_ADAPTIVE && !(M.epsilon > 0.0 && M.epsilon < 1.0)) { *msg = "epsilon must be in (0,1)"; return KIN_ERR_INPUT; }
   if (M.integrator.max_steps == 0) { *msg = "max_steps must be positive"; return KIN_ERR_INPUT; }
   if ((M.kind == KIN_METHOD_ODE || M.kind == KIN_METHOD_LSODA) && !(M.integrator.rel_tol > 0.0 && M.integrator.abs_tol > 0.0)) {
@@ -638,9 +638,14 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   KIN_CUDA(cudaEventRecord(bf.tev[0], sl.stream), "event");
   cudaError_t e;
   const int kind = d->method.kind;
+  bf.last_int_state = false;  // set below only by the int32-state stochastic launch
   if (kind == KIN_METHOD_ODE) {
     e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
     bf.kernel_name = "dopri5_kernel";
+  } else if (kind == KIN_METHOD_CLE) {
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
+    e = kin::launch_cle(*T, SD, O, want_work, bf.counter.p, sl.stream);
+    bf.kernel_name = "cle_kernel";
   } else if (kind == KIN_METHOD_LSODA) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
     if (kin::lsoda_smem_bytes(*T, SD) > 227 * 1024) {

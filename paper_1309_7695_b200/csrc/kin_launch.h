@@ -32,6 +32,10 @@ size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S);
 cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, const double* coeffs,
                          unsigned long long* counter, cudaStream_t stream);
 
+// kin_stochastic.cu: Chemical Langevin (Euler-Maruyama) sweep, double amounts.
+cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
+                       unsigned long long* counter, cudaStream_t stream);
+
 // kin_post.cu: statistics and utilities.
 // per-point Welford over runs (ascending run order) of traj_dev [n_local][G*N]
 // starting at local simulation first_sim -> mean/m2 [P][G*N]

@@ -41,6 +41,135 @@ __global__ void __launch_bounds__(stoch::kBlock) stochastic_kernel(const __grid_
   stoch::stochastic_body<TableModel<XT>, kCount, kPhilox, XT>(T, S, O, next, ovf_flag);
 }
 
+// ---- Chemical Langevin Equation, Euler-Maruyama (stochastic.hpp:64-75) ------
+// Mirrors oracle/kin_oracle.cpp simulate_cle: per step, propensities at the
+// step start; per reaction j (index order) one normal z_j (compat:
+// RngStream::draw_normal, Box-Muller with a cached spare, rng.cpp:54-66) and
+// the increment a_j h + sqrt(a_j h) z_j applied along nu[:, j]; then negative
+// components clamp to 0 (counted).  Steps truncate at grid times.
+// Double amounts (the state is real-valued).  log/sin/cos are CUDA's (<= 1-2
+// ulp from glibc's), so parity with the oracle is within a tolerance, not bit
+// for bit.
+template <bool kCount, bool kPhilox>
+__device__ __forceinline__ void simulate_cle_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                                                 uint64_t s, double* x, double* a, double* av) {
+  constexpr int B = kBlock;
+  const uint64_t sim = S.sim_begin + s;
+  const TableModel<double> sm{T, x, a, av};
+  const int N = T.n, M = T.m, G = T.n_grid;
+  stoch::init_state<double>(T, S, sim, N, x, av);
+  const uint64_t seed = sim_seed(S, sim);
+  Xoshiro rng;
+  if (!kPhilox) rng.seed(seed);
+  const double t_end = S.t_end, tau = S.tau;
+  double t = 0.0;
+  int gi = 0;
+  uint64_t flops = 0, used = 0, step = 0, n_normal = 0, n_clamp = 0;
+  int status = 0;
+  bool spare_ok = false;
+  double spare = 0.0;
+  const uint64_t F_prop = static_cast<uint64_t>(T.fprop);
+  auto emit = [&]() {
+    double* o = O.traj + (static_cast<size_t>(s) * G + gi) * N;
+    for (int i = 0; i < N; ++i) o[i] = x[i * B];
+    ++gi;
+  };
+  while (gi < G && tab_grid(T, S, gi) <= t) emit();
+  while (t < t_end) {
+    if (++used > S.max_steps) { status = KIN_SIM_BUDGET; break; }
+    const double t_stop = (gi < G && tab_grid(T, S, gi) < t_end) ? tab_grid(T, S, gi) : t_end;
+    double h = tau;
+    bool hit = false;
+    const double gap = __dsub_rn(t_stop, t);
+    if (kCount) flops += 1;
+    if (!(h < gap)) { h = gap; hit = true; }
+    sm.all_props(M);
+    if (kCount) flops += F_prop;
+    for (int j = 0; j < M; ++j) {
+      double z;
+      if (kPhilox) {
+        PhiloxSite src(seed, step, static_cast<uint32_t>(j));
+        const double u1 = src.uniform();
+        const double u2 = src.uniform();
+        z = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(2.0 * 3.141592653589793, u2)));
+        if (kCount) flops += 4 + 3 + 1 + 2;
+      } else if (spare_ok) {
+        spare_ok = false;
+        z = spare;
+      } else {
+        const double u1 = rng.uniform();
+        const double u2 = rng.uniform();
+        const double r = sqrt(__dmul_rn(-2.0, log(u1)));
+        const double ang = __dmul_rn(2.0 * 3.141592653589793, u2);
+        spare = __dmul_rn(r, sin(ang));
+        spare_ok = true;
+        z = __dmul_rn(r, cos(ang));
+        if (kCount) flops += 4 + 3 + 1 + 2 + 2;
+      }
+      if (!kPhilox) ++n_normal;
+      const double d = __dmul_rn(sm.aval(j), h);
+      const double inc = __dadd_rn(d, __dmul_rn(sqrt(d), z));
+      const int p1 = tab_col_ptr(T, j + 1);
+      for (int p = tab_col_ptr(T, j); p < p1; ++p) {
+        const uint32_t e = tab_col(T, p);
+        double* xs = x + KIN_NU_INDEX(e) * B;
+        *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), inc));
+      }
+      if (kCount) flops += 4 + 2 * static_cast<uint64_t>(p1 - tab_col_ptr(T, j));
+    }
+    bool bad = false;
+    for (int i = 0; i < N; ++i) {
+      const double v = x[i * B];
+      bad |= !isfinite(v);
+      if (v < 0.0) {
+        x[i * B] = 0.0;
+        ++n_clamp;
+      }
+    }
+    if (bad) { status = KIN_SIM_NONFINITE; break; }
+    ++step;
+    if (hit) {
+      t = t_stop;
+    } else {
+      t = __dadd_rn(t, h);
+      if (kCount) flops += 1;
+    }
+    while (gi < G && tab_grid(T, S, gi) <= t) emit();
+  }
+  while (gi < G) emit();
+  (void)n_normal;
+  uint64_t* me = O.meta + s * 6;
+  me[0] = step;
+  me[1] = 0;
+  me[2] = n_clamp;
+  me[3] = 0;
+  me[4] = 0;
+  me[5] = 0;
+  O.status[s] = status;
+  if (kCount && O.work) O.work[s] = flops;
+}
+
+template <bool kCount, bool kPhilox>
+__global__ void __launch_bounds__(stoch::kBlock) cle_kernel(const __grid_constant__ KinTables T,
+                                                            const __grid_constant__ KinSweepDev S, KinOutDev O,
+                                                            unsigned long long* __restrict__ next) {
+  extern __shared__ double smem[];
+  constexpr int B = kBlock;
+  const int tid = threadIdx.x, lane = tid & 31;
+  double* a = smem + tid;
+  double* av = smem + static_cast<size_t>(T.m) * B + tid;
+  double* x = smem + static_cast<size_t>(T.m + S.n_axes) * B + tid;
+  for (;;) {
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(next, 32ULL);
+    base = __shfl_sync(0xFFFFFFFFu, base, 0);
+    if (base >= S.n_local) break;
+    const uint64_t s = base + lane;
+    if (s < S.n_local) simulate_cle_one<kCount, kPhilox>(T, S, O, s, x, a, av);
+    __syncwarp();
+  }
+}
+
 size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block, bool int_state) {
   return static_cast<size_t>(T.m + S.n_axes) * block * sizeof(double) +
          static_cast<size_t>(T.n) * block * (int_state ? sizeof(int32_t) : sizeof(double));
@@ -72,6 +201,31 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
 }
 
 }  // namespace
+
+cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
+                       unsigned long long* counter, cudaStream_t stream) {
+  if (S.n_local == 0) return cudaSuccess;
+  const size_t smem = stochastic_smem_bytes(T, S, kBlock, false);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  const bool ph = S.rng_mode == KIN_RNG_PHILOX;
+  auto kern = count ? (ph ? cle_kernel<true, true> : cle_kernel<true, false>)
+                    : (ph ? cle_kernel<false, true> : cle_kernel<false, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  const uint64_t warps = (S.n_local + 31) / 32;
+  const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_stochastic(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                               unsigned long long* counter, int* ovf_flag, bool int_state, cudaStream_t stream) {

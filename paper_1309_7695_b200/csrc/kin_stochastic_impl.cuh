@@ -169,23 +169,19 @@ struct TableModel {
   __device__ __forceinline__ int col_len(int j) const { return tab_col_ptr(T, j + 1) - tab_col_ptr(T, j); }
 };
 
-template <class Model, bool kCount, bool kPhilox, class XT>
-__device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
-                                             uint64_t s, XT* x, double* a, double* av, int* ovf_flag) {
+// The simulation's sweep coordinates (Cartesian decode, last axis fastest,
+// SPEC.md:441) into av[], and its initial amounts into x[]; returns true when
+// an amount does not fit XT = int32.
+template <class XT>
+__device__ __forceinline__ bool init_state(const KinTables& T, const KinSweepDev& S, uint64_t sim, int N, XT* x,
+                                           double* av) {
   constexpr int B = kBlock;
-  const uint64_t sim = S.sim_begin + s;
-  const Model sm{T, x, a, av};
-  const int N = sm.n(), M = sm.m(), G = T.n_grid;
-
-  // Cartesian decode, last axis fastest.
-  {
-    uint64_t rem = sim / S.runs;
-    for (int ax = S.n_axes - 1; ax >= 0; --ax) {
-      const uint64_t nv = static_cast<uint64_t>(S.axis_n[ax]);
-      const uint64_t q = rem / nv;
-      av[ax * B] = __ldg(S.axis_values[ax] + (rem - q * nv));
-      rem = q;
-    }
+  uint64_t rem = sim / S.runs;
+  for (int ax = S.n_axes - 1; ax >= 0; --ax) {
+    const uint64_t nv = static_cast<uint64_t>(S.axis_n[ax]);
+    const uint64_t q = rem / nv;
+    av[ax * B] = __ldg(S.axis_values[ax] + (rem - q * nv));
+    rem = q;
   }
   bool ovf = false;
   for (int i = 0; i < N; ++i) {
@@ -194,6 +190,18 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     if (sizeof(XT) != 8) ovf |= v > 2147483647.0;
     x[i * B] = static_cast<XT>(v);
   }
+  return ovf;
+}
+
+template <class Model, bool kCount, bool kPhilox, class XT>
+__device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                                             uint64_t s, XT* x, double* a, double* av, int* ovf_flag) {
+  constexpr int B = kBlock;
+  const uint64_t sim = S.sim_begin + s;
+  const Model sm{T, x, a, av};
+  const int N = sm.n(), M = sm.m(), G = T.n_grid;
+
+  bool ovf = init_state<XT>(T, S, sim, N, x, av);
 
   const uint64_t seed = sim_seed(S, sim);
   Xoshiro rng;

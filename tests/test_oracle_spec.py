@@ -186,6 +186,44 @@ def test_tau_convergence_monotone():
     assert errs[0] > errs[1] > errs[2] or errs[0] > errs[2]
 
 
+# ---- Chemical Langevin (stochastic.hpp:64-75) ---------------
+def test_cle_step_examples():
+    decay = net1({0: 1}, {}, 1.0)
+    x, cl = O.cle_step(decay, [100, 0, 0], 0.01, [1.0])
+    assert x[0] == 98.0 and cl == 0                     # 100 - 1 - 1
+    mm = W.michaelis_menten()
+    x0 = mm.initial_amounts()
+    x, cl = O.cle_step(mm, x0, 0.1, np.zeros(mm.reaction_count()))
+    euler = x0 + 0.1 * O.rre_rhs(mm, x0)                # z = 0: one explicit Euler step
+    assert np.allclose(x, euler, rtol=1e-15, atol=0) and cl == 0
+    x, cl = O.cle_step(decay, [0.5, 0, 0], 0.01, [50.0])  # nu = -1: a large z pushes x below 0
+    assert x[0] == 0.0 and cl == 1                      # clamped, counted
+
+
+def test_cle_oracle_matches_reference_stream():
+    """The restatement's draw_normal and the reference's own rng.cpp
+    (oracle/_ref) drive identical CLE paths."""
+    net, cfg = W.c1_config(MethodKind.Cle, side=3)
+    cfg.method = Method(MethodKind.Cle, tau=0.05)
+    d, keep = make_sweep_desc(net, cfg)
+    a = O.sweep(net, d, workers=4)
+    b = O.sweep(net, d, workers=4, ref=True)
+    assert np.array_equal(a["traj"], b["traj"]) and np.array_equal(a["meta"], b["meta"])
+    assert a["meta"][:, 0].min() > 0
+
+
+def test_cle_decay_matches_rre():
+    """decay from 1e6 with cle -> endpoint within 5 ensemble
+    standard errors of the RRE endpoint (small step: Euler bias ~ x0/e * tau/2)."""
+    x0 = 10**6
+    r = run(W.decay(x0=x0), SweepConfig([], 400, Method(MethodKind.Cle, tau=1e-4), 3, 1.0, [0.0, 1.0]),
+            abi.SEED_ENSEMBLE, workers=8)
+    end = r["traj"][:, 1, 0]
+    se = end.std(ddof=1) / math.sqrt(len(end))
+    assert abs(end.mean() - x0 / math.e) < 5 * se
+    assert (r["status"] == 0).all() and 10**4 <= r["meta"][:, 0].min() <= r["meta"][:, 0].max() <= 10**4 + 1
+
+
 # ---- golden trajectories (reference RNG) --------------------------------------
 @pytest.mark.parametrize("case", ["birth_death_ssa", "birth_death_taufixed", "isomerization_tau", "c1_tau",
                                   "c2_schlogl", "c4_tau"])
