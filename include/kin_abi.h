@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define KIN_ABI_VERSION 1
+#define KIN_ABI_VERSION 2
 
 /* ---- status codes (cli.hpp:8-13 ExitCode; errors.hpp classes) ------------ */
 enum kin_status {
@@ -83,7 +83,7 @@ enum kin_method_kind {          /* Method::Kind order, ensemble.hpp:62 */
   KIN_METHOD_TAU_FIXED = 2,
   KIN_METHOD_CLE = 3,           /* Chemical Langevin, Euler-Maruyama with step tau (stochastic.hpp:64-75) */
   KIN_METHOD_ODE = 4,           /* Dopri5 RRE, deterministic.hpp:38-95 */
-  KIN_METHOD_HYBRID = 5,        /* not provided by this engine (KIN_ERR_INPUT) */
+  KIN_METHOD_HYBRID = 5,        /* PDMP: fast reactions by RRE, slow ones by hazard-inversion jumps (hybrid.hpp) */
   KIN_METHOD_LSODA = 6          /* extension: Adams/BDF with stiffness switching */
 };
 
@@ -97,9 +97,13 @@ typedef struct kin_integrator_config { /* deterministic.hpp:14-20 */
 
 typedef struct kin_method {
   int32_t kind;       /* enum kin_method_kind */
-  double tau;         /* TauFixed step */
+  double tau;         /* TauFixed / Cle step */
   double epsilon;     /* TauAdaptive control, default 0.03 */
   kin_integrator_config integrator;
+  /* HybridConfig (hybrid.hpp:21-26), read for KIN_METHOD_HYBRID only */
+  double theta_x;              /* amount_threshold, reference default 100 (may be +inf) */
+  double theta_a;              /* propensity_threshold, reference default 10 */
+  double repartition_interval; /* 0 selects t_end / 100 */
 } kin_method;
 
 /* ---- sweep: SweepConfig (ensemble.hpp:101-113) ---------------------------- */

@@ -2,9 +2,10 @@
  * (cli.hpp:15-17 run_cli: "Entry point behind the binary; separated so tests
  * can invoke the CLI in-process").  bin/kinetics-b200 is a thin main() over it.
  *
- *   simulate --model PATH --method {ssa|tau|cle|ode|lsoda} --t-end T
+ *   simulate --model PATH --method {ssa|tau|cle|ode|lsoda|hybrid} --t-end T
  *            --samples N --seed S [--runs R] [--epsilon E] [--tau T]
  *            [--rtol R] [--atol A] [--tol R[,A]] [--max-steps N]
+ *            [--theta-x X] [--theta-a A] [--repartition R]
  *            [--rng compat|philox] [--max-order 2|3] [--workers N] --out PATH
  *   sweep    --model PATH --sweep PATH --t-end T --samples N [--rng ...]
  *            [--max-order 2|3] [--workers N] --out PATH

@@ -62,8 +62,12 @@ kin_method method_of(const Method& m) {
   k.kind = static_cast<int32_t>(m.kind);  // Method::Kind order == enum kin_method_kind
   k.tau = m.tau;
   k.epsilon = m.epsilon;
-  k.integrator = {m.integrator.rel_tol, m.integrator.abs_tol, m.integrator.h_init, m.integrator.h_max,
-                  m.integrator.max_steps};
+  // a hybrid run integrates with HybridConfig::integrator (hybrid.hpp:21-26)
+  const IntegratorConfig& ic = m.kind == Method::Kind::Hybrid ? m.hybrid.integrator : m.integrator;
+  k.integrator = {ic.rel_tol, ic.abs_tol, ic.h_init, ic.h_max, ic.max_steps};
+  k.theta_x = static_cast<double>(m.hybrid.amount_threshold);
+  k.theta_a = m.hybrid.propensity_threshold;
+  k.repartition_interval = m.hybrid.repartition_interval;
   return k;
 }
 

@@ -598,6 +598,315 @@ int integrate_rre(const Network& net, const double* rates, const double* x0,
   return KIN_SIM_OK;
 }
 
+// ---- Hybrid PDMP (hybrid.hpp:14-62) -------------------------
+// Per segment: partition_reactions (slow iff a_j < theta_a or a reactant amount
+// < theta_x), horizon = min(t + repartition_interval, t_end), threshold
+// E = -ln(u); Dopri5 (the integrate_rre scheme) on the augmented system
+// y = (x, G): dx/dt = sum_{j fast} nu_j a_j (row order, as rre_rhs), dG/dt =
+// sum_{j slow} a_j (index order); error norm over all N+1 components.  On the
+// accepted step where G reaches E, the root is bisected on the dense output
+// until the bracket is <= 1e-10 relative in t; t* is the bracket's upper end.
+// Grid times before t* take dense values, x(t*) the dense state; the firing
+// slow reaction is the first slow j whose cumulative propensity at x(t*)
+// exceeds u2 * sum_slow a (ssa_select rule over the slow set); nu_j is added
+// to the continuous state (no rounding) and components below 0
+// clamp to 0 (counted); grid times <= t* then take the post-jump state.  Each
+// segment restarts the integrator (HINIT).  Step-size control and E use the
+// portable pow/log (kin_portable_math.hpp) so the CUDA kernel reproduces the
+// step sequence bit for bit.  meta: steps = accepted steps, rejected_leaps =
+// rejected steps, clamp_events, jumps, floored.  Philox mode: u and u2 are the
+// two uniforms of site (seed, segment, 0).
+namespace {
+struct HybridRhs {
+  const Network& net;
+  const double* rates;
+  const std::vector<char>& slow;
+  double* a;
+  template <bool C>
+  void operator()(const double* y, double* f, Work* w) const {
+    const int n = net.n, m = net.m;
+    propensities<C>(net, rates, y, a, w);
+    for (int i = 0; i < n; ++i) {
+      double acc = 0.0;
+      for (int p = net.row_ptr[i]; p < net.row_ptr[i + 1]; ++p)
+        if (!slow[net.row_reaction[p]]) acc = acc + static_cast<double>(net.row_delta[p]) * a[net.row_reaction[p]];
+      f[i] = acc;
+      if constexpr (C) w->flops += 2 * static_cast<std::uint64_t>(net.row_ptr[i + 1] - net.row_ptr[i]);
+    }
+    double g = 0.0;
+    for (int j = 0; j < m; ++j)
+      if (slow[j]) g = g + a[j];
+    f[n] = g;
+    if constexpr (C) w->flops += static_cast<std::uint64_t>(m);
+  }
+};
+}  // namespace
+
+// next_jump_with_threshold (hybrid.hpp:43-48): from (t, x = y[0..n-1]) under
+// partition `slow`, integrate the augmented system toward t_hor until G = E.
+// Grid samples on the way go to out[gi..] (pre-jump values).  On return t is
+// t* (jumped) or t_hor, and y holds the (pre-jump, floored) state there.
+template <bool C>
+int hybrid_segment(const Network& net, const double* rates, const std::vector<char>& slow,
+                   const kin_integrator_config& cfg, double E, double t_hor, double& t, Scratch& sc, Work* w,
+                   const double* grid, int n_grid, int& gi, double* out, bool& floored, std::uint64_t& attempts,
+                   std::uint64_t* meta, bool* jumped) {
+  using namespace dp;
+  const int n = net.n, n1 = n + 1;
+  double* y = sc.v[0].data();
+  double* k1 = sc.v[1].data();
+  double* k2 = sc.v[2].data();
+  double* k3 = sc.v[3].data();
+  double* k4 = sc.v[4].data();
+  double* k5 = sc.v[5].data();
+  double* k6 = sc.v[6].data();
+  double* k7 = sc.v[7].data();
+  double* yn = sc.v[8].data();
+  double* ys = sc.v[9].data();
+  double* r1 = sc.v[10].data();
+  double* r2 = sc.v[11].data();
+  double* r3 = sc.v[12].data();
+  double* r4 = sc.v[13].data();
+  double* r5 = sc.v[14].data();
+  const HybridRhs f{net, rates, slow, sc.a.data()};
+  const double rtol = cfg.rel_tol, atol = cfg.abs_tol;
+  const double hmax = cfg.h_max > 0.0 ? cfg.h_max : kInf;
+  auto dense = [&](double th, int i) {
+    const double th1 = 1.0 - th;
+    return r1[i] + th * (r2[i] + th1 * (r3[i] + th * (r4[i] + th1 * r5[i])));
+  };
+  *jumped = false;
+  y[n] = 0.0;  // G
+  f.template operator()<C>(y, k1, w);
+  double h;
+  if (cfg.h_init > 0.0) {
+    h = cfg.h_init;
+  } else {  // HINIT over the N+1 components
+    double dnf = 0.0, dny = 0.0;
+    for (int i = 0; i < n1; ++i) {
+      const double sk = atol + rtol * std::fabs(y[i]);
+      const double qf = k1[i] / sk, qy = y[i] / sk;
+      dnf = dnf + qf * qf;
+      dny = dny + qy * qy;
+    }
+    h = (dnf <= 1e-10 || dny <= 1e-10) ? 1.0e-6 : std::sqrt(dny / dnf) * 0.01;
+    if (h > hmax) h = hmax;
+    for (int i = 0; i < n1; ++i) ys[i] = y[i] + h * k1[i];
+    f.template operator()<C>(ys, k2, w);
+    double der2 = 0.0;
+    for (int i = 0; i < n1; ++i) {
+      const double sk = atol + rtol * std::fabs(y[i]);
+      const double q = (k2[i] - k1[i]) / sk;
+      der2 = der2 + q * q;
+    }
+    der2 = std::sqrt(der2) / h;
+    const double der12 = std::max(der2, std::sqrt(dnf));
+    const double h1 = der12 <= 1e-15 ? std::max(1.0e-6, h * 1.0e-3) : pm_pow(0.01 / der12, 0.2);
+    h = std::min(100.0 * h, h1);
+    if (h > hmax) h = hmax;
+    if constexpr (C) w->flops += 15 * static_cast<std::uint64_t>(n1) + 12;
+  }
+  double facold = 1.0e-4;
+  bool last_rejected = false;
+  while (t < t_hor) {
+    if (attempts++ >= cfg.max_steps) return KIN_SIM_BUDGET;
+    double hh = h < hmax ? h : hmax;
+    bool hit = false;
+    if (t + hh >= t_hor) { hh = t_hor - t; hit = true; }
+    if (!(hh > 0.0) || t + hh == t) return KIN_SIM_STEP_UNDERFLOW;
+    for (int i = 0; i < n1; ++i) ys[i] = y[i] + hh * (a21 * k1[i]);
+    f.template operator()<C>(ys, k2, w);
+    for (int i = 0; i < n1; ++i) ys[i] = y[i] + hh * (a31 * k1[i] + a32 * k2[i]);
+    f.template operator()<C>(ys, k3, w);
+    for (int i = 0; i < n1; ++i) ys[i] = y[i] + hh * (a41 * k1[i] + a42 * k2[i] + a43 * k3[i]);
+    f.template operator()<C>(ys, k4, w);
+    for (int i = 0; i < n1; ++i) ys[i] = y[i] + hh * (a51 * k1[i] + a52 * k2[i] + a53 * k3[i] + a54 * k4[i]);
+    f.template operator()<C>(ys, k5, w);
+    for (int i = 0; i < n1; ++i)
+      ys[i] = y[i] + hh * (a61 * k1[i] + a62 * k2[i] + a63 * k3[i] + a64 * k4[i] + a65 * k5[i]);
+    f.template operator()<C>(ys, k6, w);
+    for (int i = 0; i < n1; ++i)
+      yn[i] = y[i] + hh * (a71 * k1[i] + a73 * k3[i] + a74 * k4[i] + a75 * k5[i] + a76 * k6[i]);
+    f.template operator()<C>(yn, k7, w);
+    double sum = 0.0;
+    bool finite = true;
+    for (int i = 0; i < n1; ++i) {
+      const double e = hh * (e1 * k1[i] + e3 * k3[i] + e4 * k4[i] + e5 * k5[i] + e6 * k6[i] + e7 * k7[i]);
+      const double sk = atol + rtol * std::max(std::fabs(y[i]), std::fabs(yn[i]));
+      const double q = e / sk;
+      sum = sum + q * q;
+      finite &= std::isfinite(yn[i]);
+    }
+    const double err = std::sqrt(sum / static_cast<double>(n1));
+    if constexpr (C) w->flops += 63 * static_cast<std::uint64_t>(n1) + 4;
+    if (!finite || !std::isfinite(err)) return KIN_SIM_NONFINITE;
+    const double fac11 = pm_pow(err, kExpo1);
+    if (err > 1.0) {
+      h = hh / std::min(kFacMinInv, fac11 / kSafe);
+      last_rejected = true;
+      ++meta[1];
+      if constexpr (C) w->flops += 3;
+      continue;
+    }
+    double fac = fac11 / pm_pow(facold, kBeta);
+    fac = std::max(kFacMaxInv, std::min(kFacMinInv, fac / kSafe));
+    double hnew = hh / fac;
+    facold = std::max(err, 1.0e-4);
+    for (int i = 0; i < n1; ++i) {
+      r1[i] = y[i];
+      const double yd = yn[i] - y[i];
+      r2[i] = yd;
+      const double bs = hh * k1[i] - yd;
+      r3[i] = bs;
+      r4[i] = yd - hh * k7[i] - bs;
+      r5[i] = hh * (d1 * k1[i] + d3 * k3[i] + d4 * k4[i] + d5 * k5[i] + d6 * k6[i] + d7 * k7[i]);
+    }
+    if (last_rejected && hnew > hh) hnew = hh;
+    last_rejected = false;
+    h = hnew;
+    ++meta[0];
+    if constexpr (C) w->flops += 18 * static_cast<std::uint64_t>(n1) + 8;
+    const double tprev = t;
+    const double tnew = hit ? t_hor : t + hh;
+    if (yn[n] >= E) {
+      // G reaches E inside (tprev, tnew]: bisection on the dense G until the
+      // bracket is <= 1e-10 relative in t; t* = the bracket's upper end
+      double lo = 0.0, hi = 1.0;
+      for (int it = 0; it < 200; ++it) {
+        const double tl = tprev + lo * hh, th = tprev + hi * hh;
+        if (!(th - tl > 1e-10 * std::fabs(th))) break;
+        const double mid = 0.5 * (lo + hi);
+        if (dense(mid, n) >= E) hi = mid; else lo = mid;
+        if constexpr (C) w->flops += 12;
+      }
+      const double ts = hi == 1.0 ? tnew : tprev + hi * hh;
+      while (gi < n_grid && grid[gi] < ts) {
+        double* o = out + static_cast<size_t>(gi) * n;
+        const double th = (grid[gi] - tprev) / hh;
+        for (int i = 0; i < n; ++i) {
+          o[i] = dense(th, i);
+          if (o[i] < 0.0) { o[i] = 0.0; floored = true; }
+        }
+        if constexpr (C) w->flops += 8 * static_cast<std::uint64_t>(n) + 3;
+        ++gi;
+      }
+      for (int i = 0; i < n; ++i) {
+        y[i] = hi == 1.0 ? yn[i] : dense(hi, i);
+        if (y[i] < 0.0) { y[i] = 0.0; floored = true; }
+      }
+      t = ts;
+      *jumped = true;
+      return KIN_SIM_OK;
+    }
+    // no jump in this step: dense output onto (tprev, tnew], as integrate_rre
+    t = tnew;
+    for (int i = 0; i < n1; ++i) { y[i] = yn[i]; k1[i] = k7[i]; }
+    while (gi < n_grid && grid[gi] <= t) {
+      double* o = out + static_cast<size_t>(gi) * n;
+      if (grid[gi] == t) {
+        for (int i = 0; i < n; ++i) o[i] = y[i];
+      } else {
+        const double th = (grid[gi] - tprev) / hh;
+        for (int i = 0; i < n; ++i) o[i] = dense(th, i);
+        if constexpr (C) w->flops += 8 * static_cast<std::uint64_t>(n) + 3;
+      }
+      for (int i = 0; i < n; ++i)
+        if (o[i] < 0.0) { o[i] = 0.0; floored = true; }
+      ++gi;
+    }
+    bool lifted = false;
+    for (int i = 0; i < n; ++i)
+      if (y[i] < 0.0) { y[i] = 0.0; lifted = true; }
+    if (lifted) {
+      floored = true;
+      f.template operator()<C>(y, k1, w);
+    }
+  }
+  return KIN_SIM_OK;
+}
+
+// partition_reactions (hybrid.hpp:28-33): slow iff a_j < theta_a or a reactant
+// amount < theta_x.  a[] = propensities at x.
+inline void hybrid_partition(const Network& net, const double* x, const double* a, double theta_x, double theta_a,
+                             std::vector<char>* slow) {
+  slow->assign(static_cast<size_t>(net.m), 0);
+  for (int j = 0; j < net.m; ++j) {
+    bool sl = a[j] < theta_a;
+    for (int p = net.rt_ptr[j]; p < net.rt_ptr[j + 1]; ++p) sl |= x[net.rt_species[p]] < theta_x;
+    (*slow)[j] = sl;
+  }
+}
+
+template <bool C>
+int simulate_hybrid(const Network& net, const double* rates, const double* x0, const kin_method& method,
+                    double t_end, const double* grid, int n_grid, std::uint64_t seed, double* out,
+                    std::uint64_t* meta, Scratch& sc, Work* w, int rng_mode) {
+  const int n = net.n, m = net.m;
+  double* y = sc.v[0].data();
+  double* a = sc.a.data();
+  thread_local std::vector<char> slow;
+  const double rep = method.repartition_interval > 0.0 ? method.repartition_interval : t_end / 100.0;
+  for (int q = 0; q < 6; ++q) meta[q] = 0;
+  bool floored = false;
+  for (int i = 0; i < n; ++i) y[i] = x0[i];
+  Stream rng(seed);
+  const bool philox = rng_mode == KIN_RNG_PHILOX;
+  double t = 0.0;
+  int gi = 0;
+  auto emit_state = [&]() {
+    std::memcpy(out + static_cast<size_t>(gi) * n, y, sizeof(double) * n);
+    ++gi;
+  };
+  while (gi < n_grid && grid[gi] <= t) emit_state();
+  std::uint64_t attempts = 0, seg = 0;
+  while (t < t_end) {
+    propensities<C>(net, rates, y, a, w);
+    hybrid_partition(net, y, a, method.theta_x, method.theta_a, &slow);
+    const double t_hor = t + rep < t_end ? t + rep : t_end;
+    PhiloxSite site(seed, seg, 0);
+    const double u = philox ? site.draw_uniform() : rng.draw_uniform();
+    const double E = -pm_log(u);
+    if constexpr (C) w->flops += 3;
+    bool jumped = false;
+    const int rc = hybrid_segment<C>(net, rates, slow, method.integrator, E, t_hor, t, sc, w, grid, n_grid, gi, out,
+                                     floored, attempts, meta, &jumped);
+    if (rc != KIN_SIM_OK) return rc;
+    if (jumped) {
+      // the caller's selection (hybrid.hpp:39-40): first slow j whose cumulative
+      // propensity at x(t*) exceeds u2 * sum_slow a
+      propensities<C>(net, rates, y, a, w);
+      double as = 0.0;
+      for (int j = 0; j < m; ++j)
+        if (slow[j]) as = as + a[j];
+      const double u2 = philox ? site.draw_uniform() : rng.draw_uniform();
+      if (as > 0.0) {
+        const double target = u2 * as;
+        double c = 0.0;
+        int sel = -1, last = -1;
+        for (int j = 0; j < m; ++j) {
+          if (!slow[j]) continue;
+          if (a[j] > 0.0) last = j;
+          c = c + a[j];
+          if (c > target) { sel = j; break; }
+        }
+        if (sel < 0) sel = last;
+        for (int p = net.col_ptr[sel]; p < net.col_ptr[sel + 1]; ++p) {
+          double& v = y[net.col_species[p]];
+          v = v + static_cast<double>(net.col_delta[p]);
+          if (v < 0.0) { v = 0.0; ++meta[2]; }
+        }
+        ++meta[4];
+        if constexpr (C) w->flops += 2 * static_cast<std::uint64_t>(m) + 1;
+      }
+      while (gi < n_grid && grid[gi] <= t) emit_state();
+    }
+    ++seg;
+  }
+  while (gi < n_grid) emit_state();
+  meta[5] = floored ? 1 : 0;
+  return KIN_SIM_OK;
+}
+
 constexpr bool kLsodaAvailable = true;
 
 // Analytic Jacobian of the RRE, J = nu * da/dx (row-major N x N), continuous
@@ -1073,7 +1382,8 @@ void decode_sim(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, 
 
 int validate_sweep(const Network& net, const kin_sweep_desc* d, std::string* msg) {
   const kin_method& M = d->method;
-  if (M.kind == KIN_METHOD_HYBRID) { *msg = "method not provided by this engine (hybrid is out of scope)"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_HYBRID && !(M.theta_x >= 0.0 && M.theta_a >= 0.0 && M.repartition_interval >= 0.0)) { *msg = "hybrid thresholds and repartition interval must be non-negative"; return KIN_ERR_INPUT; }
+  if (M.kind == KIN_METHOD_HYBRID && !(M.integrator.rel_tol > 0.0 && M.integrator.abs_tol > 0.0)) { *msg = "tolerances must be positive"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_CLE && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
   if (M.kind < 0 || M.kind > KIN_METHOD_LSODA) { *msg = "unknown method kind"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_LSODA && !kLsodaAvailable) { *msg = "LSODA not built"; return KIN_ERR_INPUT; }
@@ -1119,6 +1429,9 @@ int run_one(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, doub
     return integrate_rre<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
   if (M.kind == KIN_METHOD_LSODA)
     return integrate_lsoda<C>(net, sc.rates.data(), x0, M.integrator, d->t_end, d->grid, d->n_grid, traj, meta, sc, w);
+  if (M.kind == KIN_METHOD_HYBRID)
+    return simulate_hybrid<C>(net, sc.rates.data(), x0, M, d->t_end, d->grid, d->n_grid, seed, traj, meta, sc, w,
+                              d->rng_mode);
   if (M.kind == KIN_METHOD_CLE)
     return simulate_cle<C>(net, sc.rates.data(), x0, M, d->t_end, d->grid, d->n_grid, seed, traj, meta, sc, w,
                            d->rng_mode);
@@ -1275,6 +1588,42 @@ int kin_oracle_cle_step(const kin_model_desc* d, const double* x, double h, cons
   cle_step_from_normals<false>(net, xout, a.data(), h, z, &c, nullptr);
   *clamped = c;
   return KIN_OK;
+}
+
+// next_jump_with_threshold (hybrid.hpp:43-48) from t = 0: returns 1 with *tstar
+// and the pre-jump state when G reaches `threshold` before t_end, else 0 with
+// the state at t_end.  slow_mask[j] != 0 marks slow reactions (NULL: use the
+// thresholds at x via partition_reactions).
+int kin_oracle_next_jump(const kin_model_desc* d, const double* x, const int32_t* slow_mask, double theta_x,
+                         double theta_a, double t_end, double threshold, const kin_integrator_config* cfg,
+                         double* tstar, double* xout, kin_error* err) {
+  Network net;
+  if (int rc = load(d, &net, err)) return -1;
+  std::vector<double> r(net.m);
+  for (int j = 0; j < net.m; ++j) r[j] = net.rate_param[j] >= 0 ? net.params[net.rate_param[j]] : net.rate_base[j];
+  Scratch sc;
+  sc.resize(net.n, net.m);
+  std::vector<char> slow(static_cast<size_t>(net.m), 0);
+  propensities<false>(net, r.data(), x, sc.a.data(), nullptr);
+  if (slow_mask) {
+    for (int j = 0; j < net.m; ++j) slow[j] = slow_mask[j] != 0;
+  } else {
+    hybrid_partition(net, x, sc.a.data(), theta_x, theta_a, &slow);
+  }
+  for (int i = 0; i < net.n; ++i) sc.v[0][i] = x[i];
+  double t = 0.0;
+  int gi = 0;
+  bool floored = false, jumped = false;
+  std::uint64_t attempts = 0, meta[6] = {0, 0, 0, 0, 0, 0};
+  const int rc = hybrid_segment<false>(net, r.data(), slow, *cfg, threshold, t_end, t, sc, nullptr, nullptr, 0, gi,
+                                       nullptr, floored, attempts, meta, &jumped);
+  if (rc != KIN_SIM_OK) {
+    set_err(err, KIN_ERR_SIMULATION, "integrator failure");
+    return -1;
+  }
+  *tstar = t;
+  for (int i = 0; i < net.n; ++i) xout[i] = sc.v[0][i];
+  return jumped ? 1 : 0;
 }
 
 int kin_oracle_apply_reaction(const kin_model_desc* d, const double* x, int j, double* xout, kin_error* err) {

@@ -60,6 +60,8 @@ def load(ref: bool = False) -> C.CDLL:
     lib.kin_oracle_tau_leap_from_counts.argtypes = [M, f64p, u64p, f64p, C.POINTER(C.c_int), E]
     lib.kin_oracle_apply_reaction.argtypes = [M, f64p, C.c_int, f64p, E]
     lib.kin_oracle_cle_step.argtypes = [M, f64p, C.c_double, f64p, f64p, u64p, E]
+    lib.kin_oracle_next_jump.argtypes = [M, f64p, C.POINTER(C.c_int32), C.c_double, C.c_double, C.c_double,
+                                         C.c_double, C.POINTER(abi.KinIntegratorConfig), f64p, f64p, E]
     lib.kin_oracle_rre_rhs.argtypes = [M, f64p, f64p, E]
     lib.kin_oracle_stats_merge.restype = None
     lib.kin_oracle_stats_merge.argtypes = [u64p, f64p, f64p, C.c_uint64, f64p, f64p, C.c_uint64]
@@ -158,6 +160,22 @@ def cle_step(net, x, h, z):
                                     abi.ptr(out, C.c_double), C.byref(cl), C.byref(err))
     assert rc == 0, err.text()
     return out, int(cl.value)
+
+
+def next_jump(net, x, t_end, threshold, slow=None, theta_x=100.0, theta_a=10.0, integrator=None):
+    """next_jump_with_threshold (hybrid.hpp:43-48) from t = 0: (t* or None, state)."""
+    from paper_1309_7695_b200.ensemble import IntegratorConfig
+    x = _f64(x)
+    out = np.zeros_like(x)
+    ts = C.c_double()
+    mask = None if slow is None else (C.c_int32 * len(slow))(*[int(v) for v in slow])
+    cfg = (integrator or IntegratorConfig()).c()
+    err = abi.KinError()
+    rc = load().kin_oracle_next_jump(C.byref(net.desc()), abi.ptr(x, C.c_double), mask, float(theta_x),
+                                     float(theta_a), float(t_end), float(threshold), C.byref(cfg), C.byref(ts),
+                                     abi.ptr(out, C.c_double), C.byref(err))
+    assert rc >= 0, err.text()
+    return (ts.value if rc == 1 else None), out
 
 
 def rre_rhs(net, x):

@@ -49,7 +49,8 @@ class KinIntegratorConfig(C.Structure):
 
 class KinMethod(C.Structure):
     _fields_ = [("kind", C.c_int32), ("tau", C.c_double), ("epsilon", C.c_double),
-                ("integrator", KinIntegratorConfig)]
+                ("integrator", KinIntegratorConfig), ("theta_x", C.c_double), ("theta_a", C.c_double),
+                ("repartition_interval", C.c_double)]
 
 
 class KinSweepAxis(C.Structure):

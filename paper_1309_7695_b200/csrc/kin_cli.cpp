@@ -35,10 +35,10 @@ struct Fail {
 [[noreturn]] void input(const std::string& m) { throw Fail{KIN_EXIT_INPUT, m}; }
 
 const char* kUsage =
-    "usage: kinetics-b200 simulate --model PATH --method {ssa|tau|cle|ode|lsoda} --t-end T --samples N\n"
+    "usage: kinetics-b200 simulate --model PATH --method {ssa|tau|cle|ode|lsoda|hybrid} --t-end T --samples N\n"
     "                              --seed S [--runs R] [--epsilon E] [--tau T] [--rtol R] [--atol A]\n"
     "                              [--tol R[,A]] [--max-steps N] [--rng compat|philox] [--max-order 2|3]\n"
-    "                              [--workers N] --out PATH\n"
+    "                              [--theta-x X] [--theta-a A] [--repartition R] [--workers N] --out PATH\n"
     "       kinetics-b200 sweep --model PATH --sweep PATH --t-end T --samples N [--rng compat|philox]\n"
     "                           [--max-order 2|3] [--workers N] --out PATH\n"
     "       kinetics-b200 replay MANIFEST\n";
@@ -88,6 +88,7 @@ uint64_t unum(const std::string& flag, const std::string& v) {
 struct MethodSpec {
   std::string name = "";
   double epsilon = 0.03, tau = 0.0, rtol = 1e-6, atol = 1e-9;  // ensemble.hpp:59-71, deterministic.hpp:14-20
+  double theta_x = 100.0, theta_a = 10.0, repartition = 0.0;    // HybridConfig, hybrid.hpp:21-26
   uint64_t max_steps = 10000000;
   kin_method to_c() const {
     kin_method m;
@@ -97,7 +98,11 @@ struct MethodSpec {
     else if (name == "ode") m.kind = KIN_METHOD_ODE;
     else if (name == "lsoda") m.kind = KIN_METHOD_LSODA;
     else if (name == "cle") m.kind = KIN_METHOD_CLE;
+    else if (name == "hybrid") m.kind = KIN_METHOD_HYBRID;
     m.tau = tau;
+    m.theta_x = theta_x;
+    m.theta_a = theta_a;
+    m.repartition_interval = repartition;
     m.epsilon = epsilon;
     m.integrator.rel_tol = rtol;
     m.integrator.abs_tol = atol;
@@ -113,10 +118,11 @@ struct MethodSpec {
 };
 
 void check_method(const MethodSpec& m) {
-  if (m.name == "hybrid")
-    input("method 'hybrid' is not provided by this engine (methods: ssa, tau, cle, ode, lsoda)");
-  if (m.name != "ssa" && m.name != "tau" && m.name != "ode" && m.name != "lsoda" && m.name != "cle")
+  if (m.name != "ssa" && m.name != "tau" && m.name != "ode" && m.name != "lsoda" && m.name != "cle" &&
+      m.name != "hybrid")
     usage("unknown method '" + m.name + "'");
+  if (m.name == "hybrid" && !(m.theta_x >= 0.0 && m.theta_a >= 0.0 && m.repartition >= 0.0))
+    input("hybrid thresholds and repartition interval must be non-negative");
   if (m.name == "cle" && !(m.tau > 0.0)) input("method 'cle' needs a positive step (--tau, or tau= in a sweep file)");
 }
 
@@ -229,6 +235,9 @@ SweepFile parse_sweep_file(const std::string& text) {
         else if (k == "rtol") sf.method.rtol = d;
         else if (k == "atol") sf.method.atol = d;
         else if (k == "max_steps") sf.method.max_steps = static_cast<uint64_t>(d);
+        else if (k == "theta_x") sf.method.theta_x = d;
+        else if (k == "theta_a") sf.method.theta_a = d;
+        else if (k == "repartition") sf.method.repartition = d;
         else throw bad("unknown method option '" + k + "'");
       }
       sf.have_method = true;
@@ -393,6 +402,9 @@ std::vector<std::pair<std::string, std::string>> common_fields(const Common& c, 
           {"rel_tol", fmt(ms.rtol)},
           {"abs_tol", fmt(ms.atol)},
           {"max_steps", std::to_string(ms.max_steps)},
+          {"theta_x", fmt(ms.theta_x)},
+          {"theta_a", fmt(ms.theta_a)},
+          {"repartition_interval", fmt(ms.repartition)},
           {"rng", c.rng == KIN_RNG_PHILOX ? "philox" : "compat"},
           {"max_order", std::to_string(c.max_order)},
           {"t_end", fmt(c.t_end)},
@@ -404,7 +416,7 @@ int cmd_simulate(const std::vector<std::string>& args, Written* result) {
   const auto t0 = std::chrono::steady_clock::now();
   const Flags f = parse_flags(args, 2, {"--model", "--method", "--t-end", "--samples", "--seed", "--runs",
                                         "--epsilon", "--tau", "--rtol", "--atol", "--tol", "--max-steps", "--rng",
-                                        "--max-order", "--workers", "--out", "--theta-x", "--theta-a"});
+                                        "--max-order", "--workers", "--out", "--theta-x", "--theta-a", "--repartition"});
   MethodSpec ms;
   ms.name = f.get("--method");
   const uint64_t seed = unum("--seed", f.get("--seed"));
@@ -421,11 +433,15 @@ int cmd_simulate(const std::vector<std::string>& args, Written* result) {
     if (c != std::string::npos) ms.atol = num("--tol", t.substr(c + 1));
   }
   if (f.has("--max-steps")) ms.max_steps = unum("--max-steps", f.get("--max-steps"));
+  if (f.has("--theta-x")) ms.theta_x = num("--theta-x", f.get("--theta-x"));  // "inf" accepted
+  if (f.has("--theta-a")) ms.theta_a = num("--theta-a", f.get("--theta-a"));
+  if (f.has("--repartition")) ms.repartition = num("--repartition", f.get("--repartition"));
   if (ms.name != "tau" && ms.name != "cle" && f.has("--tau")) usage("--tau applies to --method tau or cle");
   Common c;
   load_common(f, &c);
   check_method(ms);
-  if (f.has("--theta-x") || f.has("--theta-a")) input("--theta-x/--theta-a configure the hybrid method, which this engine does not provide");
+  if ((f.has("--theta-x") || f.has("--theta-a") || f.has("--repartition")) && ms.name != "hybrid")
+    usage("--theta-x/--theta-a/--repartition apply to --method hybrid");
   Ctx x;
   open_engine(c, f, &x);
   const kin_model_desc* md = kin_model_text_desc(c.model.m);

@@ -168,15 +168,17 @@ int sweep_layout(const kin_sweep_desc* d, Layout* L, std::string* msg) {
 
 int validate_sweep(const HostModel& net, const kin_sweep_desc* d, const Layout& L, std::string* msg) {
   const kin_method& M = d->method;
-  if (M.kind == KIN_METHOD_HYBRID) {
-    *msg = "method not provided by this engine (hybrid is out of scope)";
+  if (M.kind == KIN_METHOD_HYBRID &&
+      !(M.theta_x >= 0.0 && M.theta_a >= 0.0 && M.repartition_interval >= 0.0)) {
+    *msg = "hybrid thresholds and repartition interval must be non-negative";
     return KIN_ERR_INPUT;
   }
   if (M.kind < 0 || M.kind > KIN_METHOD_LSODA) { *msg = "unknown method kind"; return KIN_ERR_INPUT; }
   if ((M.kind == KIN_METHOD_TAU_FIXED || M.kind == KIN_METHOD_CLE) && !(M.tau > 0.0)) { *msg = "tau must be positive"; return KIN_ERR_INPUT; }
   if (M.kind == KIN_METHOD_TAU_ADAPTIVE && !(M.epsilon > 0.0 && M.epsilon < 1.0)) { *msg = "epsilon must be in (0,1)"; return KIN_ERR_INPUT; }
   if (M.integrator.max_steps == 0) { *msg = "max_steps must be positive"; return KIN_ERR_INPUT; }
-  if ((M.kind == KIN_METHOD_ODE || M.kind == KIN_METHOD_LSODA) && !(M.integrator.rel_tol > 0.0 && M.integrator.abs_tol > 0.0)) {
+  if ((M.kind == KIN_METHOD_ODE || M.kind == KIN_METHOD_LSODA || M.kind == KIN_METHOD_HYBRID) &&
+      !(M.integrator.rel_tol > 0.0 && M.integrator.abs_tol > 0.0)) {
     *msg = "tolerances must be positive";
     return KIN_ERR_INPUT;
   }
@@ -613,6 +615,9 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   SD.h_init = d->method.integrator.h_init;
   SD.h_max = d->method.integrator.h_max;
   SD.max_steps = d->method.integrator.max_steps;
+  SD.hyb_theta_x = d->method.theta_x;
+  SD.hyb_theta_a = d->method.theta_a;
+  SD.hyb_rep = d->method.repartition_interval;
   SD.n_axes = d->n_axes;
   SD.seed_mode = d->seed_mode;
   size_t at = 0;
@@ -642,6 +647,14 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   if (kind == KIN_METHOD_ODE) {
     e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
     bf.kernel_name = "dopri5_kernel";
+  } else if (kind == KIN_METHOD_HYBRID) {
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
+    if (kin::hybrid_smem_bytes(*T, SD) > 227 * 1024) {
+      set_err(err, KIN_ERR_INPUT, "model too large for the hybrid kernel (per-simulation state exceeds shared memory)");
+      return KIN_ERR_INPUT;
+    }
+    e = kin::launch_hybrid(*T, SD, O, want_work, bf.counter.p, sl.stream);
+    bf.kernel_name = "hybrid_kernel";
   } else if (kind == KIN_METHOD_CLE) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
     e = kin::launch_cle(*T, SD, O, want_work, bf.counter.p, sl.stream);

@@ -36,6 +36,11 @@ cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutD
 cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                        unsigned long long* counter, cudaStream_t stream);
 
+// kin_hybrid.cu: hybrid PDMP sweep (one thread per simulation, smem state).
+size_t hybrid_smem_bytes(const KinTables& T, const KinSweepDev& S);
+cudaError_t launch_hybrid(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
+                          unsigned long long* counter, cudaStream_t stream);
+
 // kin_post.cu: statistics and utilities.
 // per-point Welford over runs (ascending run order) of traj_dev [n_local][G*N]
 // starting at local simulation first_sim -> mean/m2 [P][G*N]

@@ -83,6 +83,7 @@ struct KinSweepDev {
   double epsilon;
   double rel_tol, abs_tol, h_init, h_max;
   uint64_t max_steps;
+  double hyb_theta_x, hyb_theta_a, hyb_rep;  // HybridConfig (hybrid.hpp:21-26)
   // sweep (SweepConfig, ensemble.hpp:106-113)
   int32_t n_axes;
   int32_t seed_mode;

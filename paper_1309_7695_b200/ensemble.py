@@ -52,6 +52,10 @@ class Method:
     tau: float = 0.0
     epsilon: float = 0.03
     integrator: IntegratorConfig = field(default_factory=IntegratorConfig)
+    # HybridConfig (hybrid.hpp:21-26)
+    theta_x: float = 100.0
+    theta_a: float = 10.0
+    repartition_interval: float = 0.0
 
     def deterministic(self) -> bool:
         return self.kind in (MethodKind.Ode, MethodKind.Lsoda)
@@ -62,7 +66,8 @@ class Method:
                 MethodKind.Lsoda: "lsoda"}[MethodKind(self.kind)]
 
     def c(self) -> abi.KinMethod:
-        return abi.KinMethod(int(self.kind), self.tau, self.epsilon, self.integrator.c())
+        return abi.KinMethod(int(self.kind), self.tau, self.epsilon, self.integrator.c(), float(self.theta_x),
+                             float(self.theta_a), float(self.repartition_interval))
 
 
 @dataclass

@@ -62,7 +62,8 @@ def test_malformed_model_exits_1_without_output(files):
 
 
 @pytest.mark.parametrize("extra,code", [
-    (["--method", "cle"], 1), (["--method", "cle", "--tau", "-1"], 1), (["--method", "hybrid"], 1),
+    (["--method", "cle"], 1), (["--method", "cle", "--tau", "-1"], 1), (["--method", "hybrid", "--theta-x", "-1"], 1),
+    (["--method", "tau", "--theta-a", "5"], 64),
     (["--method", "warp"], 64),
     (["--method", "tau", "--samples", "1"], 64), (["--method", "ode", "--t-end", "x"], 64),
     (["--method", "ode", "--tau", "0.1"], 64), (["--method", "tau", "--rng", "mt"], 64),

@@ -240,3 +240,64 @@ def test_golden_trajectories(case):
         assert np.array_equal(r["traj"], g["traj"]) and np.array_equal(r["meta"], g["meta"])
         return
     raise AssertionError(case)
+
+
+# ---- hybrid PDMP (hybrid.hpp) ----------------------------------
+def test_next_jump_examples():
+    # single slow reaction with constant a = 2, E = 1 -> t* = 0.5
+    birth = ReactionNetwork.create([Species("A", 0)], [], [Reaction("b", {}, {0: 1}, 2.0)])
+    ts, x = O.next_jump(birth, [0], 10.0, 1.0)
+    assert abs(ts - 0.5) <= 1e-10 * 0.5 and x[0] == 0.0
+    # slow set empty -> none; the state is the RRE solution at t_end
+    ts, x = O.next_jump(W.decay(x0=100), [100], 1.0, 1.0, slow=[0])
+    assert ts is None and abs(x[0] - 100 / math.e) < 1e-5
+    # hazard a(t) = t (B grows linearly by a fast birth, C is made at rate B) -> t* = sqrt(2)
+    lin = ReactionNetwork.create([Species("B", 0), Species("C", 0)], [],
+                                 [Reaction("grow", {}, {0: 1}, 1.0), Reaction("make", {0: 1}, {0: 1, 1: 1}, 1.0)])
+    ts, x = O.next_jump(lin, [0, 0], 10.0, 1.0, slow=[0, 1])
+    assert abs(ts - math.sqrt(2)) <= 1e-9 and abs(x[0] - math.sqrt(2)) < 1e-6 and x[1] == 0.0
+
+
+def _hybrid(theta_x, theta_a, **kw):
+    return Method(MethodKind.Hybrid, theta_x=theta_x, theta_a=theta_a, **kw)
+
+
+def test_hybrid_all_fast_matches_rre():
+    """theta_x = theta_a = 0 -> every reaction fast -> integrate_rre
+    within 10x the integrator tolerance at every grid point."""
+    net, cfg = W.c1_config(MethodKind.Ode, side=2)
+    g = np.asarray(cfg.grid)
+    ode = run(net, cfg)
+    cfg.method = _hybrid(0.0, 0.0)
+    hyb = run(net, cfg)
+    tol = 10 * (1e-9 + 1e-6 * np.abs(ode["traj"]))
+    assert (np.abs(hyb["traj"] - ode["traj"]) <= tol).all()
+    assert (hyb["meta"][:, 4] == 0).all() and len(g) == 101
+
+
+def test_hybrid_all_slow_matches_ssa_distribution():
+    """theta_x = inf -> all slow -> birth-death endpoint
+    distribution within TV 0.03 of simulate_ssa's (10^4 runs)."""
+    bd = W.birth_death(lam=5.0, c=1.0)
+    grid = [0.0, 10.0]
+    hyb = run(bd, SweepConfig([], 10000, _hybrid(math.inf, 10.0), 21, 10.0, grid), abi.SEED_ENSEMBLE, workers=8)
+    ssa = run(bd, SweepConfig([], 10000, Method(MethodKind.Ssa), 22, 10.0, grid), abi.SEED_ENSEMBLE, workers=8)
+    a = np.bincount(hyb["traj"][:, 1, 0].astype(int), minlength=40)[:40] / 10000
+    b = np.bincount(ssa["traj"][:, 1, 0].astype(int), minlength=40)[:40] / 10000
+    assert 0.5 * np.abs(a - b).sum() <= 0.03
+    assert (hyb["traj"][:, 1, 0] == np.round(hyb["traj"][:, 1, 0])).all()  # integer-valued: no fast reactions
+    assert hyb["meta"][:, 4].mean() > 10
+
+
+def test_hybrid_two_scale_poisson():
+    """fast A<->B at 1e3, slow 0->C at 1 -> C(5) ~ Poisson(5), TV <= 0.03."""
+    net = ReactionNetwork.create([Species("A", 500), Species("B", 500), Species("C", 0)], [],
+                                 [Reaction("ab", {0: 1}, {1: 1}, 1e3), Reaction("ba", {1: 1}, {0: 1}, 1e3),
+                                  Reaction("c", {}, {2: 1}, 1.0)])
+    r = run(net, SweepConfig([], 10000, _hybrid(100.0, 10.0), 5, 5.0, [0.0, 5.0]), abi.SEED_ENSEMBLE, workers=8)
+    c = r["traj"][:, 1, 2].astype(int)
+    emp = np.bincount(c, minlength=30)[:30] / len(c)
+    k = np.arange(30)
+    pois = np.exp(-5.0) * 5.0 ** k / np.array([math.factorial(int(v)) for v in k])
+    assert 0.5 * np.abs(emp - pois).sum() <= 0.03
+    assert np.allclose(r["traj"][:, 1, 0] + r["traj"][:, 1, 1], 1000.0, rtol=1e-9)  # A+B conserved by the flow
