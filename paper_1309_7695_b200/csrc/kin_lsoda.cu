@@ -160,7 +160,7 @@ struct Lsoda {
 
 template <bool kCount>
 __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, const double* co, uint64_t s,
-                          double* smem_base, int* ismem_base, int B, int tid) {
+                          double* smem_base, int* ismem_base, int B, int tid, unsigned mask) {
   const uint64_t sim = S.sim_begin + s;
   const int n = T.n, m = T.m, G = T.n_grid;
   Lsoda L{T, S, co, B, n, m};
@@ -295,7 +295,14 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
     auto cm1 = [&](int q) { return L.tesco(0, q, 1) * L.elco(0, q, q); };
     auto cm2 = [&](int q) { return L.tesco(1, q, 1) * L.elco(1, q, q); };
 
-    while (t < t_end && status == 0) {
+    // One accepted step per iteration, warp-synchronous: the lanes of `mask`
+    // (one simulation each) reconverge at every step, so the shared
+    // predictor / corrector / error-test code runs with the warp together
+    // instead of drifting apart into 32 serial simulations.
+    bool running = t < t_end && status == 0;
+    while (__any_sync(mask, running)) {
+      if (!running) continue;
+      do {
       for (int i = 0; i < n; ++i) L.ewt[i * B] = rtol * fabs(L.z(0, i)) + atol;
       int kflag = 0, ncf = 0;
       double dsm = 0.0;
@@ -500,6 +507,8 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
       } else if (ialth == 1 && nq < maxord()) {
         for (int i = 0; i < n; ++i) L.z(kL - 1, i) = L.acor[i * B];
       }
+      } while (0);
+      running = t < t_end && status == 0;
     }
     if (status == 0)
       while (gi < G) emit(gi++, &L.z(0, 0));
@@ -533,7 +542,8 @@ __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ K
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     if (base >= S.n_local) break;
     const uint64_t s = base + lane;
-    if (s < S.n_local) lsoda_one<kCount>(T, S, O, co, s, smem, ism, B, tid);
+    const unsigned mask = __ballot_sync(0xFFFFFFFFu, s < S.n_local);
+    if (s < S.n_local) lsoda_one<kCount>(T, S, O, co, s, smem, ism, B, tid, mask);
     __syncwarp();
   }
 }
