@@ -40,6 +40,9 @@ constexpr double d1 = -12715105075.0 / 11282082432.0, d3 = 87487479700.0 / 32700
 constexpr double kSafe = 0.9, kFacMinInv = 5.0, kFacMaxInv = 0.1, kBeta = 0.04, kExpo1 = 0.2 - kBeta * 0.75;
 }  // namespace dp
 
+// bytes of the table blob a block copies to shared memory (16-byte multiple)
+__host__ __device__ __forceinline__ uint32_t table_smem_bytes(const KinTables& T) { return (T.used + 15u) & ~15u; }
+
 template <int L>
 struct Group {
   unsigned mask;
@@ -68,6 +71,14 @@ __global__ void __launch_bounds__(128) dopri5_kernel(const __grid_constant__ Kin
                                                      const __grid_constant__ KinSweepDev S, KinOutDev O) {
   using namespace dp;
   extern __shared__ double smem[];
+  // The model tables go to shared memory once per block: the RHS walks them
+  // with lane-dependent indices (lane l handles reactions l, l+L, ...), which
+  // the constant bank would serialise across the distinct addresses of a warp.
+  const uint32_t tb = table_smem_bytes(T);
+  unsigned char* tblob = reinterpret_cast<unsigned char*>(smem);
+  for (uint32_t o = threadIdx.x * 16u; o < tb; o += blockDim.x * 16u)
+    *reinterpret_cast<uint4*>(tblob + o) = *reinterpret_cast<const uint4*>(T.blob + o);
+  __syncthreads();
   const int gpb = blockDim.x / L;
   const int grp = threadIdx.x / L, lane = threadIdx.x % L;
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * gpb + grp;
@@ -78,7 +89,13 @@ __global__ void __launch_bounds__(128) dopri5_kernel(const __grid_constant__ Kin
   grpc.mask = (L == 32) ? 0xFFFFFFFFu : (((1u << L) - 1u) << ((threadIdx.x & 31) / L * L));
 
   const int stride = N + M + S.n_axes;
-  double* xs = smem + static_cast<size_t>(grp) * stride;
+  double* xs = smem + tb / sizeof(double) + static_cast<size_t>(grp) * stride;
+  const double* s_rate = reinterpret_cast<const double*>(tblob + T.off_rate);
+  const int8_t* s_rate_axis = reinterpret_cast<const int8_t*>(tblob + T.off_rate_axis);
+  const int16_t* s_rt_ptr = reinterpret_cast<const int16_t*>(tblob + T.off_rt_ptr);
+  const uint32_t* s_rt = reinterpret_cast<const uint32_t*>(tblob + T.off_rt);
+  const int16_t* s_row_ptr = reinterpret_cast<const int16_t*>(tblob + T.off_row_ptr);
+  const uint32_t* s_row = reinterpret_cast<const uint32_t*>(tblob + T.off_row);
   double* a = xs + N;
   double* av = a + M;
 
@@ -110,11 +127,11 @@ __global__ void __launch_bounds__(128) dopri5_kernel(const __grid_constant__ Kin
   auto rhs = [&](double* out) {
     grpc.sync();
     for (int j = lane; j < M; j += L) {
-      const int ax = tab_rate_axis(T, j);
-      double aj = ax < 0 ? tab_rate(T, j) : av[ax];
-      const int p1 = tab_rt_ptr(T, j + 1);
-      for (int p = tab_rt_ptr(T, j); p < p1; ++p) {
-        const uint32_t e = tab_rt(T, p);
+      const int ax = s_rate_axis[j];
+      double aj = ax < 0 ? s_rate[j] : av[ax];
+      const int p1 = s_rt_ptr[j + 1];
+      for (int p = s_rt_ptr[j]; p < p1; ++p) {
+        const uint32_t e = s_rt[p];
         aj = aj * combinations(xs[KIN_TERM_SPECIES(e)], KIN_TERM_STOICH(e));
       }
       a[j] = aj;
@@ -125,9 +142,9 @@ __global__ void __launch_bounds__(128) dopri5_kernel(const __grid_constant__ Kin
       const int i = lane + q * L;
       double acc = 0.0;
       if (i < N) {
-        const int p1 = tab_row_ptr(T, i + 1);
-        for (int p = tab_row_ptr(T, i); p < p1; ++p) {
-          const uint32_t e = tab_row(T, p);
+        const int p1 = s_row_ptr[i + 1];
+        for (int p = s_row_ptr[i]; p < p1; ++p) {
+          const uint32_t e = s_row[p];
           acc = acc + static_cast<double>(KIN_NU_DELTA(e)) * a[KIN_NU_INDEX(e)];
         }
       }
@@ -329,7 +346,7 @@ template <int L, int SL>
 cudaError_t launch_t(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, cudaStream_t st) {
   constexpr int kBlock = 128;
   constexpr int gpb = kBlock / L;
-  const size_t smem = static_cast<size_t>(gpb) * (T.n + T.m + S.n_axes) * sizeof(double);
+  const size_t smem = table_smem_bytes(T) + static_cast<size_t>(gpb) * (T.n + T.m + S.n_axes) * sizeof(double);
   const unsigned grid = static_cast<unsigned>((S.n_local + gpb - 1) / gpb);
   if (count) {
     cudaFuncSetAttribute(dopri5_kernel<L, SL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -19,7 +19,11 @@ cfgs = {
     "c3_ode": W.c3_config(method=MethodKind.Ode),
     "c3_lsoda": W.c3_config(),
     "c5_tau": W.c5_config(),
+    "c5_ode": W.c5_config(method=MethodKind.Ode),
+    "c1_hybrid": W.c1_config(MethodKind.Hybrid, side=128),
+    "c1_cle": W.c1_config(MethodKind.Cle, side=128),
 }
+cfgs["c1_cle"][1].method = __import__("paper_1309_7695_b200").ensemble.Method(MethodKind.Cle, tau=0.05)
 names = sys.argv[1:] or list(cfgs)
 err = abi.KinError()
 peak = C.c_double()
