@@ -6,7 +6,13 @@ import time
 import numpy as np
 
 sys.path.insert(0, ".")
+import os
+from pathlib import Path
+
 from paper_1309_7695_b200 import abi, workloads as W
+
+if os.environ.get("KIN_LIB"):  # A/B another build of the engine
+    abi.LIB_PATH = Path(os.environ["KIN_LIB"])
 from paper_1309_7695_b200.ensemble import Engine, MethodKind, make_sweep_desc
 
 eng = Engine([0])
