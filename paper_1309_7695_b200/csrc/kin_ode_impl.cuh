@@ -67,7 +67,7 @@ struct Group {
 };
 
 template <int L, int SL, bool kCount>
-__global__ void __launch_bounds__(128) dopri5_kernel(const __grid_constant__ KinTables T,
+__global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ KinTables T,
                                                      const __grid_constant__ KinSweepDev S, KinOutDev O) {
   using namespace dp;
   extern __shared__ double smem[];
