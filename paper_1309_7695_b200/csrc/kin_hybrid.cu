@@ -23,7 +23,7 @@ namespace {
 
 using pmath::pm_log;
 using pmath::pm_pow;
-using stoch::kBlock;
+constexpr int kBlock = 32;  // one warp per block: the per-thread state is large
 using stoch::TableModel;
 
 // Dormand-Prince 5(4) tableau (the oracle's dp:: constants)
@@ -51,7 +51,7 @@ template <bool kCount>
 struct Hybrid {
   const KinTables& T;
   const KinSweepDev& S;
-  TableModel<double> sm;  // propensities over y (x = y[0..n-1])
+  TableModel<double, kBlock> sm;  // propensities over y (x = y[0..n-1])
   int n, m, n1;
   double* V;         // kVecs vectors of n1, [vec][comp][thread]
   uint32_t* slowm;   // [word][thread]
@@ -63,7 +63,7 @@ struct Hybrid {
 
   // augmented RHS: f = (sum_fast nu a (row order), sum_slow a) at state `yv`
   __device__ void rhs(int yv, int fv) {
-    TableModel<double> st{T, vp(yv), sm.a, sm.av};
+    TableModel<double, kBlock> st{T, vp(yv), sm.a, sm.av};
     for (int j = 0; j < m; ++j) sm.a[j * kBlock] = st.prop(j);
     if (kCount) flops += static_cast<uint64_t>(T.fprop);
     for (int i = 0; i < n; ++i) {
@@ -98,8 +98,8 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
   constexpr int B = kBlock;
   const uint64_t sim = S.sim_begin + s;
   const int n = T.n, m = T.m, G = T.n_grid, n1 = n + 1;
-  Hybrid<kCount> H{T, S, TableModel<double>{T, V, a, av}, n, m, n1, V, slowm};
-  stoch::init_state<double>(T, S, sim, n, V, av);  // y[0..n-1] = x0 (vector Y is the first)
+  Hybrid<kCount> H{T, S, TableModel<double, kBlock>{T, V, a, av}, n, m, n1, V, slowm};
+  stoch::init_state<double, kBlock>(T, S, sim, n, V, av);  // y[0..n-1] = x0 (vector Y is the first)
   const uint64_t seed = sim_seed(S, sim);
   Xoshiro rng;
   if (!kPhilox) rng.seed(seed);
@@ -121,7 +121,7 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
   while (t < t_end) {
     // partition_reactions at the current state
     {
-      TableModel<double> st{T, V, a, av};
+      TableModel<double, kBlock> st{T, V, a, av};
       const int words = (m + 31) >> 5;
       for (int w = 0; w < words; ++w) slowm[w * B] = 0u;
       for (int j = 0; j < m; ++j) {
@@ -307,7 +307,7 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
     }
     if (status) break;
     if (jumped) {
-      TableModel<double> st{T, V, a, av};
+      TableModel<double, kBlock> st{T, V, a, av};
       for (int j = 0; j < m; ++j) a[j * B] = st.prop(j);
       if (kCount) H.flops += static_cast<uint64_t>(T.fprop);
       double as = 0.0;

@@ -233,7 +233,7 @@ const char* const kNvrtcOpts[5] = {"--gpu-architecture=sm_100a", "-fmad=false", 
 bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_state, std::vector<char>* cubin,
                    std::string* log) {
   std::string src = "#include \"kin_stochastic_impl.cuh\"\n" + policy +
-                    "extern \"C\" __global__ void __launch_bounds__(32) kin_jit_stoch(\n"
+                    "extern \"C\" __global__ void __launch_bounds__(KIN_STOCH_BLOCK) kin_jit_stoch(\n"
                     "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
                     "    unsigned long long* __restrict__ next, int* ovf) {\n"
                     "  kin::stoch::stochastic_body<kin::stoch::GenModel<XT_>, KCOUNT_, KPHILOX_, XT_>(T, S, O, next, ovf);\n"
@@ -400,8 +400,8 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
     }
   }
   if (!jk->ok) return cudaSuccess;  // caller falls back to the table-driven kernel
-  const size_t smem = static_cast<size_t>(T.m + S.n_axes) * 32 * sizeof(double) +
-                      static_cast<size_t>(T.n) * 32 * (int_state ? sizeof(int32_t) : sizeof(double));
+  const size_t smem = static_cast<size_t>(T.m + S.n_axes) * KIN_STOCH_BLOCK * sizeof(double) +
+                      static_cast<size_t>(T.n) * KIN_STOCH_BLOCK * (int_state ? sizeof(int32_t) : sizeof(double));
   if (smem > 227 * 1024) return cudaSuccess;
   const void* fn = reinterpret_cast<const void*>(jk->kern);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -409,19 +409,19 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, KIN_STOCH_BLOCK, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaSuccess;
-  const uint64_t warps = (S.n_local + 31) / 32;
+  const uint64_t blocks = (S.n_local + KIN_STOCH_BLOCK - 1) / KIN_STOCH_BLOCK;
   const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
-  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   KinTables* Tp = const_cast<KinTables*>(&T);
   KinSweepDev* Sp = const_cast<KinSweepDev*>(&S);
   KinOutDev Oc = O;
   void* args[] = {Tp, Sp, &Oc, &counter, &ovf_flag};
-  e = cudaLaunchKernel(fn, dim3(grid), dim3(32), args, smem, stream);
+  e = cudaLaunchKernel(fn, dim3(grid), dim3(KIN_STOCH_BLOCK), args, smem, stream);
   if (e == cudaSuccess) *used = true;
   return e;
 }

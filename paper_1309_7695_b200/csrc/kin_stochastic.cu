@@ -191,9 +191,9 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t warps = (S.n_local + 31) / 32;
+  const uint64_t blocks = (S.n_local + kBlock - 1) / kBlock;
   const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
-  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter, ovf_flag);
@@ -218,9 +218,9 @@ cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t warps = (S.n_local + 31) / 32;
+  const uint64_t blocks = (S.n_local + kBlock - 1) / kBlock;
   const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
-  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter);

@@ -28,7 +28,12 @@ typedef signed char int8_t;
 // internal per-simulation status: an int32 amount would overflow; the engine
 // re-runs the launch with double amounts (never returned to callers)
 #define KIN_SIM_INTERNAL_RETRY 100
-#define KIN_TABLE_BYTES 30720  // < 32764-byte kernel parameter limit (sm_70+, CUDA >= 12.1)
+#define KIN_TABLE_BYTES 30720
+// threads per block of the thread-per-simulation stochastic kernels (a multiple
+// of 32; per-thread state is strided by it in shared memory)
+#ifndef KIN_STOCH_BLOCK
+#define KIN_STOCH_BLOCK 32
+#endif  // < 32764-byte kernel parameter limit (sm_70+, CUDA >= 12.1)
 
 // packed entries
 //   reactant term : species (bits 0-15) | stoich (bits 16-23)
