@@ -199,6 +199,16 @@ def sum_over_ranks(world, value: float, local: int) -> float:
     return float(t.item())
 
 
+def read_profile_entry(kernel):
+    p = REPO / "profiles" / "ncu_summary.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()).get("kernels", {}).get(kernel) or {}
+        except Exception:
+            pass
+    return {}
+
+
 def read_profile_traffic(kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
     the committed `ncu --set full` capture summary (profiles/ncu_summary.json)."""
@@ -362,6 +372,20 @@ def bench_ours(args, world, rank, local):
                      "traffic": traffic, "traffic_source": traffic_src},
     }
     res["clocks"] = clk.summary()
+    # Instruction-issue roofline of the same kernel: the warp-instructions one
+    # launch of this (deterministic) workload executes, from the committed ncu
+    # capture, over the live kernel time and the issue peak at the sampled SM
+    # clock (148 SMs x 4 schedulers x 1 warp-instruction per cycle).
+    ent = read_profile_entry(kname)
+    winst = ent.get("warp_instructions_per_launch")
+    if winst and res["clocks"].get("sm_mhz"):
+        import torch as _tt
+        sms = _tt.cuda.get_device_properties(local).multi_processor_count
+        peak_issue = sms * 4 * res["clocks"]["sm_mhz"] * 1e6
+        achieved_issue = winst / (tau_avg_ms / 1e3)
+        res["roofline"]["issue"] = {"achieved_warp_inst_per_s": achieved_issue, "peak_warp_inst_per_s": peak_issue,
+                                    "frac": achieved_issue / peak_issue, "warp_instructions_per_launch": winst,
+                                    "source": ent.get("source")}
     eng.close()
     return res
 
