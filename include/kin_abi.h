@@ -173,6 +173,13 @@ typedef struct kin_error {
 typedef struct kin_ctx kin_ctx;
 typedef struct kin_model kin_model;
 
+/* merge_statistics (ensemble.hpp:56-57): fold (n_b, mean_b, m2_b) into
+   (*n_a, mean_a, m2_a) by Chan's parallel update, element-wise over len values:
+   delta = mean_b - mean_a; mean_a += delta*n_b/n; m2_a += m2_b + delta^2*n_a*n_b/n.
+   Host function. */
+void kin_stats_merge(uint64_t* n_a, double* mean_a, double* m2_a, uint64_t n_b, const double* mean_b,
+                     const double* m2_b, uint64_t len);
+
 /* Number of CUDA devices visible to this process (0 without a GPU). */
 int32_t kin_visible_devices(void);
 
@@ -200,9 +207,12 @@ int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* de
 
 /* The chunk plan kin_sweep_run uses for n_devices GPUs over simulations
    [s0, s1) with R runs per point: n_chunks = (n_devices == 1 ? 1 : min(#points,
-   4*n_devices)) whole-point chunks (boundaries snapped to multiples of R),
-   chunk c -> device c % n_devices.  bounds receives n_chunks+1 entries
-   (capacity max_chunks+1).  Pure host function (no device needed). */
+   4*n_devices)) whole-point chunks (boundaries snapped to multiples of R) — or,
+   when the range touches fewer points than devices (run_ensemble), min(S,
+   n_devices) equal run ranges whose cut points get their statistics Chan-merged
+   in ascending chunk order (ensemble.hpp:91-99).  Chunk c -> device
+   c % n_devices.  bounds receives n_chunks+1 entries (capacity max_chunks+1).
+   Pure host function (no device needed). */
 int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t runs_per_point, int32_t n_devices,
                    int32_t max_chunks, uint64_t* bounds, int32_t* n_chunks, kin_error* err);
 

@@ -8,7 +8,7 @@ interface (model.hpp / ensemble.hpp) over that ABI.
 """
 from .model import (DeviceError, KineticsError, ParseError, Parameter, Reaction, ReactionNetwork,
                     SimulationError, Species, ValidationError, parse_model, render_model)
-from .ensemble import (Engine, EnsembleOptions, EnsembleStatistics, IntegratorConfig, Method, MethodKind,
+from .ensemble import (Engine, EnsembleOptions, EnsembleStatistics, IntegratorConfig, Method, MethodKind, merge_statistics,
                        SweepAxis, SweepConfig, SweepResults, Trajectory, TrajectoryMeta, parameter_sweep,
                        run_ensemble, run_single, uniform_grid)
 

@@ -429,8 +429,22 @@ struct Buffers {
   const char* kernel_name = "";
   uint64_t last_base = 0, last_S = 0;
   int last_gn = 0;
+  // statistics of the (at most two) points this chunk holds only some runs of
+  // (chunk edges inside a point): Welford over the chunk's runs, merged across
+  // chunks by kin_sweep_wait (Chan, ascending chunk order)
+  DevBuf<double> pmean, pm2;                     // [n_partial][gn]
+  double* h_pmean = nullptr;                     // pinned copies
+  double* h_pm2 = nullptr;
+  size_t h_pcap = 0;
+  int n_partial = 0;
+  uint64_t partial_point[2] = {0, 0}, partial_n[2] = {0, 0}, partial_base[2] = {0, 0};
   void release() {
     traj.release(); mean.release(); m2.release(); axis.release(); grid.release();
+    pmean.release(); pm2.release();
+    if (h_pmean) cudaFreeHost(h_pmean);
+    if (h_pm2) cudaFreeHost(h_pm2);
+    h_pmean = h_pm2 = nullptr;
+    h_pcap = 0;
     meta.release(); work.release(); status.release(); counter.release(); ovf.release();
     if (ovf_host) cudaFreeHost(ovf_host);
     ovf_host = nullptr;
@@ -585,8 +599,24 @@ kin::JitModel jit_model(const HostModel& H, const kin_sweep_desc* d) {
 }
 
 // Launch the simulation kernels for global sims [s0, s1) on a slot (device-resident).
-int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc* d, const Layout& L, uint64_t s0, uint64_t s1,
-                 bool want_stats, bool want_work, kin_error* err) {
+// Statistics kernels of a launch (whole points, then the partial points).
+int launch_stats(Slot& sl, Buffers& bf, kin_error* err) {
+  const size_t gn = static_cast<size_t>(bf.last_gn);
+  if (bf.have_stats) {
+    cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.R, bf.last_base, bf.nP, bf.mean.p, bf.m2.p,
+                                            sl.stream);
+    if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
+  }
+  for (int k = 0; k < bf.n_partial; ++k) {
+    cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.partial_n[k], bf.partial_base[k], 1,
+                                            bf.pmean.p + k * gn, bf.pm2.p + k * gn, sl.stream);
+    if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
+  }
+  return KIN_OK;
+}
+
+int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc* d, const Layout& L, uint64_t s0,
+                 uint64_t s1, bool want_stats, bool want_work, kin_error* err, bool want_partials = false) {
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
   KinTables* T = new KinTables;
   std::unique_ptr<KinTables> Tguard(T);
@@ -714,30 +744,51 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
   KIN_CUDA(cudaEventRecord(bf.tev[1], sl.stream), "event");
   bf.timed_stats = false;
-  // per-point statistics for points entirely inside [s0, s1)
+  // per-point statistics for points entirely inside [s0, s1), and (when the
+  // caller merges chunks) partial statistics of the points cut by a chunk edge
   const uint64_t P0 = (s0 + L.R - 1) / L.R, P1 = s1 / L.R;
   const uint64_t nP = P1 > P0 ? P1 - P0 : 0;
+  bf.n_partial = 0;
+  if (want_stats && want_partials && S) {
+    auto add = [&](uint64_t g0, uint64_t g1) {
+      const int k = bf.n_partial++;
+      bf.partial_point[k] = g0 / L.R;
+      bf.partial_n[k] = g1 - g0;
+      bf.partial_base[k] = g0 - s0;
+    };
+    uint64_t head_end = s0;
+    if (s0 % L.R != 0) {
+      head_end = std::min(s1, (s0 / L.R + 1) * L.R);
+      add(s0, head_end);
+    }
+    const uint64_t tail0 = (s1 / L.R) * L.R;
+    if (s1 % L.R != 0 && tail0 >= head_end && tail0 < s1) add(tail0, s1);
+    if (bf.n_partial) {
+      KIN_CUDA(bf.pmean.ensure(gn * 2), "cudaMalloc partial mean");
+      KIN_CUDA(bf.pm2.ensure(gn * 2), "cudaMalloc partial m2");
+    }
+  }
   if (want_stats && nP) {
     KIN_CUDA(bf.mean.ensure(gn * nP), "cudaMalloc mean");
     KIN_CUDA(bf.m2.ensure(gn * nP), "cudaMalloc m2");
-    e = kin::launch_point_stats(bf.traj.p, static_cast<int>(gn), L.R, P0 * L.R - s0, nP, bf.mean.p, bf.m2.p,
-                                sl.stream);
-    if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
+  }
+  bf.last_gn = static_cast<int>(gn);
+  bf.R = L.R;
+  bf.nP = nP;
+  bf.last_base = P0 * L.R - s0;
+  bf.have_stats = want_stats && nP;
+  if (int rc = launch_stats(sl, bf, err)) return rc;
+  if (bf.have_stats || bf.n_partial) {
     KIN_CUDA(cudaEventRecord(bf.tev[2], sl.stream), "event");
     bf.timed_stats = true;
   }
   bf.pending_check = bf.last_int_state;
-  bf.last_base = P0 * L.R - s0;
   bf.last_S = S;
-  bf.last_gn = static_cast<int>(gn);
   bf.s0 = s0;
   bf.s1 = s1;
   bf.P0 = P0;
-  bf.nP = nP;
-  bf.R = L.R;
   bf.G = G;
   bf.N = N;
-  bf.have_stats = want_stats && nP;
   bf.have_work = want_work;
   bf.valid = true;
   return KIN_OK;
@@ -757,10 +808,7 @@ int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
   cudaError_t e = kin::launch_stochastic(*bf.last_T, bf.last_SD, bf.last_O, bf.last_count, bf.counter.p, bf.ovf.p,
                                          false, sl.stream);
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel relaunch");
-  if (bf.have_stats) {
-    e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.R, bf.last_base, bf.nP, bf.mean.p, bf.m2.p, sl.stream);
-    if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel relaunch");
-  }
+  if (int rc = launch_stats(sl, bf, err)) return rc;
   KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
   return KIN_OK;
 }
@@ -790,6 +838,19 @@ int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_sim,
     if (out->m2)
       if (int rc = copy_d2h(sl, st, out->m2 + po * gn, bf.m2.p, bf.nP * gn * sizeof(double), sync, err)) return rc;
   }
+  if (bf.n_partial) {
+    const size_t need = static_cast<size_t>(bf.n_partial) * gn;
+    if (bf.h_pcap < need) {
+      if (bf.h_pmean) cudaFreeHost(bf.h_pmean);
+      if (bf.h_pm2) cudaFreeHost(bf.h_pm2);
+      bf.h_pmean = bf.h_pm2 = nullptr;
+      KIN_CUDA(cudaMallocHost(&bf.h_pmean, need * sizeof(double)), "pinned partial mean");
+      KIN_CUDA(cudaMallocHost(&bf.h_pm2, need * sizeof(double)), "pinned partial m2");
+      bf.h_pcap = need;
+    }
+    KIN_CUDA(cudaMemcpyAsync(bf.h_pmean, bf.pmean.p, need * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H partial");
+    KIN_CUDA(cudaMemcpyAsync(bf.h_pm2, bf.pm2.p, need * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H partial");
+  }
   if (bf.pending_check && bf.ovf_host)
     KIN_CUDA(cudaMemcpyAsync(bf.ovf_host, bf.ovf.p, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H flag");
   if (sync) KIN_CUDA(cudaStreamSynchronize(st), "stream sync");
@@ -802,17 +863,49 @@ int fetch_range(Slot& sl, Buffers& bf, kin_sweep_out* out, uint64_t base_sim, ui
 }
 
 // Chunk plan of kin_sweep_run (see kin_abi.h kin_sweep_plan).
+// merge_statistics (ensemble.hpp:56-57): Chan's parallel
+// update of (n, mean, m2) — the oracle's kin_oracle_stats_merge formula.
+void stats_merge(uint64_t* na, double* mean_a, double* m2_a, uint64_t nb, const double* mean_b, const double* m2_b,
+                 uint64_t len) {
+  if (nb == 0) return;
+  if (*na == 0) {
+    *na = nb;
+    for (uint64_t q = 0; q < len; ++q) {
+      mean_a[q] = mean_b[q];
+      m2_a[q] = m2_b[q];
+    }
+    return;
+  }
+  const double fa = static_cast<double>(*na), fb = static_cast<double>(nb);
+  const double fn = fa + fb;
+  for (uint64_t q = 0; q < len; ++q) {
+    const double delta = mean_b[q] - mean_a[q];
+    mean_a[q] = mean_a[q] + delta * fb / fn;
+    m2_a[q] = m2_a[q] + m2_b[q] + delta * delta * fa * fb / fn;
+  }
+  *na += nb;
+}
+
 std::vector<uint64_t> plan_chunks(uint64_t s0, uint64_t s1, uint64_t R, int D) {
   const uint64_t S = s1 - s0;
-  const uint64_t n_chunks =
-      D <= 1 ? 1 : std::min<uint64_t>(std::max<uint64_t>(S / std::max<uint64_t>(R, 1), 1), 4 * static_cast<uint64_t>(D));
+  if (D <= 1 || S == 0) return {s0, s1};
+  const uint64_t points = (s1 - 1) / R - s0 / R + 1;  // points the range touches
   std::vector<uint64_t> bounds;
   bounds.push_back(s0);
-  for (uint64_t c = 1; c < n_chunks; ++c) {
-    uint64_t b = s0 + S * c / n_chunks;
-    b = (b + R - 1) / R * R;  // snap to a point boundary
-    b = std::min(std::max(b, bounds.back()), s1);
-    bounds.push_back(b);
+  if (points < static_cast<uint64_t>(D)) {
+    // fewer points than devices (run_ensemble): split the runs evenly; the
+    // statistics of a point cut by a chunk edge are merged across its chunks
+    const uint64_t n_chunks = std::min<uint64_t>(S, static_cast<uint64_t>(D));
+    for (uint64_t c = 1; c < n_chunks; ++c) bounds.push_back(s0 + S * c / n_chunks);
+  } else {
+    const uint64_t n_chunks = std::min<uint64_t>(std::max<uint64_t>(S / std::max<uint64_t>(R, 1), 1),
+                                                 4 * static_cast<uint64_t>(D));
+    for (uint64_t c = 1; c < n_chunks; ++c) {
+      uint64_t b = s0 + S * c / n_chunks;
+      b = (b + R - 1) / R * R;  // snap to a point boundary
+      b = std::min(std::max(b, bounds.back()), s1);
+      bounds.push_back(b);
+    }
   }
   bounds.push_back(s1);
   return bounds;
@@ -850,6 +943,11 @@ const char* kin_status_string(int32_t code) {
 
 uint64_t kin_splitmix64_mix(uint64_t v) { return kin::splitmix64_mix(v); }
 uint64_t kin_derive_run_seed(uint64_t m, uint64_t i) { return kin::derive_run_seed(m, i); }
+
+void kin_stats_merge(uint64_t* n_a, double* mean_a, double* m2_a, uint64_t n_b, const double* mean_b,
+                     const double* m2_b, uint64_t len) {
+  stats_merge(n_a, mean_a, m2_a, n_b, mean_b, m2_b, len);
+}
 
 int32_t kin_visible_devices(void) {
   int count = 0;
@@ -990,7 +1088,9 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
       bf = new Buffers;
     }
     job->parts.push_back({dv, bf});
-    if (int rc = launch_range(sl, *bf, model->host, desc, L, c0, c1, stats, job->out.work != nullptr, err)) return rc;
+    const bool partials = stats && bounds.size() > 2;
+    if (int rc = launch_range(sl, *bf, model->host, desc, L, c0, c1, stats, job->out.work != nullptr, err, partials))
+      return rc;
     if (!bf->ev_done) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_done, cudaEventDisableTiming), "event");
     if (!bf->ev_copied) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_copied, cudaEventDisableTiming), "event");
     if (!bf->ovf_host) KIN_CUDA(cudaMallocHost(&bf->ovf_host, sizeof(int)), "pinned flag");
@@ -1021,8 +1121,12 @@ int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
     Slot& sl = *ctx->slots[part.slot];
     Buffers& bf = *part.buf;
     if (rc == KIN_OK) {
-      KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
-      KIN_CUDA(cudaEventSynchronize(bf.ev_copied), "copy-out");
+      cudaError_t ce = cudaSetDevice(sl.device);
+      if (ce == cudaSuccess) ce = cudaEventSynchronize(bf.ev_copied);
+      if (ce != cudaSuccess) {
+        rc = cuda_fail(err, ce, "copy-out");
+        continue;
+      }
       if (bf.pending_check && *bf.ovf_host) {
         // an int32 amount overflowed: redo this chunk with double amounts
         std::lock_guard<std::mutex> lk(sl.mu);
@@ -1032,6 +1136,35 @@ int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
       }
       bf.pending_check = false;
     }
+  }
+  // points cut by chunk edges: Chan-merge their per-chunk statistics in
+  // ascending chunk order (ensemble.hpp:91-99: per-worker accumulators merged
+  // in ascending worker-range order)
+  if (rc == KIN_OK && (job->out.mean || job->out.m2)) {
+    std::map<uint64_t, std::pair<uint64_t, std::vector<double>>> acc;  // point -> (n, [mean | m2])
+    size_t gn = 0;
+    for (auto& part : job->parts) {
+      const Buffers& bf = *part.buf;
+      gn = static_cast<size_t>(bf.last_gn);
+      for (int k = 0; k < bf.n_partial; ++k) {
+        auto& a = acc[bf.partial_point[k]];
+        if (a.second.empty()) a.second.assign(2 * gn, 0.0);
+        stats_merge(&a.first, a.second.data(), a.second.data() + gn, bf.partial_n[k], bf.h_pmean + k * gn,
+                    bf.h_pm2 + k * gn, gn);
+      }
+    }
+    const uint64_t P_first = job->base_point, P_end = job->s1 / job->L.R;
+    for (const auto& kv : acc) {
+      const uint64_t pt = kv.first;
+      if (pt < P_first || pt >= P_end) continue;  // not whole inside the sweep range: no statistics
+      if (job->out.mean)
+        std::memcpy(job->out.mean + (pt - P_first) * gn, kv.second.second.data(), gn * sizeof(double));
+      if (job->out.m2)
+        std::memcpy(job->out.m2 + (pt - P_first) * gn, kv.second.second.data() + gn, gn * sizeof(double));
+    }
+  }
+  for (auto& part : job->parts) {
+    Slot& sl = *ctx->slots[part.slot];
     std::lock_guard<std::mutex> lk(sl.mu);
     sl.pool.emplace_back(part.buf);
   }

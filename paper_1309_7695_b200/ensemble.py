@@ -134,6 +134,21 @@ class EnsembleStatistics:
         return 0.0 if self.n < 2 else float(self.m2_[g, s] / (self.n - 1))
 
 
+def merge_statistics(a: EnsembleStatistics, b: EnsembleStatistics) -> EnsembleStatistics:
+    """ensemble.hpp:56-57: Chan's parallel merge of two ensembles on the same
+    grid (kin_stats_merge).  merge(x, empty) == x."""
+    if a.grid.shape != b.grid.shape or not np.array_equal(a.grid, b.grid) or a.species_count != b.species_count:
+        raise ValidationError("merge_statistics: grid or species mismatch")
+    mean = np.ascontiguousarray(a.mean_, dtype=np.float64).copy()
+    m2 = np.ascontiguousarray(a.m2_, dtype=np.float64).copy()
+    mb = np.ascontiguousarray(b.mean_, dtype=np.float64)
+    qb = np.ascontiguousarray(b.m2_, dtype=np.float64)
+    n = C.c_uint64(a.n)
+    abi.load_library().kin_stats_merge(C.byref(n), abi.ptr(mean, C.c_double), abi.ptr(m2, C.c_double), b.n,
+                                       abi.ptr(mb, C.c_double), abi.ptr(qb, C.c_double), mean.size)
+    return EnsembleStatistics(a.grid, a.species_count, int(n.value), mean, m2)
+
+
 @dataclass
 class SweepPointResult:
     coordinates: List[float]

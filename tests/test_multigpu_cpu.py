@@ -65,15 +65,18 @@ def test_two_rank_shard_equals_single_process(which):
 
 
 @pytest.mark.parametrize("s0,s1,R,D", [(0, 65536, 1, 8), (0, 16384, 256, 8), (100, 1000, 7, 3), (0, 10, 1, 1),
-                                        (5, 5, 1, 4), (0, 512, 256, 8)])
+                                        (5, 5, 1, 4), (0, 512, 256, 8), (0, 10000, 10000, 4), (3, 9, 100, 8)])
 def test_engine_chunk_plan(s0, s1, R, D):
     chunks = shard.plan(s0, s1, R, D)
     assert chunks[0][0] == s0 and chunks[-1][1] == s1
     for (a0, a1, dv), (b0, b1, _) in zip(chunks, chunks[1:]):
         assert a1 == b0 and a0 <= a1
+    points = (s1 - 1) // R - s0 // R + 1 if s1 > s0 else 0
     for c0, c1, dv in chunks[1:]:
-        if c0 not in (s0, s1):
+        if c0 not in (s0, s1) and points >= D:
             assert c0 % R == 0  # whole points: every interior boundary on a point boundary
+    if 0 < points < D:  # fewer points than devices: the runs are split evenly
+        assert len(chunks) == min(s1 - s0, D)
     assert [c[2] for c in chunks] == [i % D for i in range(len(chunks))]
     if D == 1:
         assert len(chunks) == 1
@@ -85,3 +88,26 @@ def test_rank_range_partition():
         assert rngs[0][0] == 0 and rngs[-1][1] == P * R
         assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
         assert all(r[0] % R == 0 for r in rngs)
+
+
+def test_merge_statistics_matches_oracle():
+    """ensemble.hpp:56-57 / SPEC.md:426-433: Chan merge, bit-exact with the oracle."""
+    from oracle import oracle as O
+    from paper_1309_7695_b200.ensemble import EnsembleStatistics, merge_statistics
+    rng = np.random.default_rng(4)
+    grid = np.linspace(0, 1, 5)
+    a = EnsembleStatistics(grid, 3, 17, rng.normal(size=(5, 3)) * 100, rng.uniform(0, 50, (5, 3)))
+    b = EnsembleStatistics(grid, 3, 9, rng.normal(size=(5, 3)) * 100, rng.uniform(0, 50, (5, 3)))
+    got = merge_statistics(a, b)
+    n, mean, m2 = O.stats_merge(a.n, a.mean_, a.m2_, b.n, b.mean_, b.m2_)
+    assert got.n == n == 26 and np.array_equal(got.mean_, mean) and np.array_equal(got.m2_, m2)
+    ba = merge_statistics(b, a)
+    assert np.allclose(ba.mean_, got.mean_, rtol=1e-12) and np.allclose(ba.m2_, got.m2_, rtol=1e-12)
+    # merge({1,2}, {3}) = {1,2,3}: mean 2, m2 2 (SPEC.md:430); merge(x, empty) = x (SPEC.md:431)
+    g1 = np.zeros(1)
+    x12 = EnsembleStatistics(g1, 1, 2, np.array([[1.5]]), np.array([[0.5]]))
+    x3 = EnsembleStatistics(g1, 1, 1, np.array([[3.0]]), np.array([[0.0]]))
+    r = merge_statistics(x12, x3)
+    assert r.n == 3 and r.mean_[0, 0] == 2.0 and r.m2_[0, 0] == 2.0
+    e = EnsembleStatistics(g1, 1, 0, np.zeros((1, 1)), np.zeros((1, 1)))
+    assert np.array_equal(merge_statistics(x12, e).mean_, x12.mean_) and merge_statistics(e, x12).n == 2
