@@ -13,9 +13,11 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <charconv>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -183,31 +185,66 @@ int kin_csv_write(const kin_csv_table* table, const char* path, int32_t threads,
   bool ok = std::fwrite(head.data(), 1, head.size(), f) == head.size();
   if (content_fnv1a64) h = kin_fnv1a64_update(h, head.data(), head.size());
   total += head.size();
-  // waves of nt*4 blocks: formatted in parallel, written (and hashed) in order
-  const uint64_t wave = static_cast<uint64_t>(nt) * 4;
-  std::vector<std::string> bufs(wave);
-  for (uint64_t b0 = 0; b0 < n_blocks && ok; b0 += wave) {
-    const uint64_t nb = std::min(wave, n_blocks - b0);
-    std::atomic<uint64_t> next{0};
-    auto work = [&]() {
-      for (uint64_t k; (k = next.fetch_add(1)) < nb;) {
-        std::string& s = bufs[k];
-        s.clear();
-        const uint64_t r0 = (b0 + k) * block, r1 = std::min(R, r0 + block);
-        for (uint64_t r = r0; r < r1; ++r) T.row(s, r);
+  // Pipeline: worker threads format blocks into a ring of slots while this
+  // thread writes (and hashes) the completed blocks in row order.
+  const size_t ring = static_cast<size_t>(nt) * 4;
+  std::vector<std::string> slot(ring);
+  std::vector<int> ready(ring, 0);                  // 1 = slot holds block `owner[slot]`
+  std::vector<uint64_t> owner(ring, ~0ull);
+  std::mutex mu;
+  std::condition_variable cv_ready, cv_free;
+  uint64_t written = 0;                              // blocks consumed by the writer
+  std::atomic<uint64_t> next{0};
+  std::atomic<bool> stop{false};
+  auto work = [&]() {
+    for (;;) {
+      const uint64_t b = next.fetch_add(1);
+      if (b >= n_blocks || stop.load()) return;
+      const size_t k = static_cast<size_t>(b % ring);
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_free.wait(lk, [&] { return b < written + ring || stop.load(); });  // slot k released
+        if (stop.load()) return;
       }
-    };
-    const int nw = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(nt), nb));
-    std::vector<std::thread> pool;
-    for (int w = 1; w < nw; ++w) pool.emplace_back(work);
-    work();
-    for (auto& th : pool) th.join();
-    for (uint64_t k = 0; k < nb && ok; ++k) {
-      ok = std::fwrite(bufs[k].data(), 1, bufs[k].size(), f) == bufs[k].size();
-      if (content_fnv1a64) h = kin_fnv1a64_update(h, bufs[k].data(), bufs[k].size());
-      total += bufs[k].size();
+      std::string& sb = slot[k];
+      sb.clear();
+      const uint64_t r0 = b * block, r1 = std::min(R, r0 + block);
+      for (uint64_t r = r0; r < r1; ++r) T.row(sb, r);
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        owner[k] = b;
+        ready[k] = 1;
+      }
+      cv_ready.notify_all();
+    }
+  };
+  std::vector<std::thread> pool;
+  const int nw = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(nt), std::max<uint64_t>(n_blocks, 1)));
+  for (int w = 0; w < nw; ++w) pool.emplace_back(work);
+  for (uint64_t b = 0; b < n_blocks; ++b) {
+    const size_t k = static_cast<size_t>(b % ring);
+    {
+      std::unique_lock<std::mutex> lk(mu);
+      cv_ready.wait(lk, [&] { return ready[k] && owner[k] == b; });
+    }
+    if (ok) {
+      ok = std::fwrite(slot[k].data(), 1, slot[k].size(), f) == slot[k].size();
+      if (content_fnv1a64) h = kin_fnv1a64_update(h, slot[k].data(), slot[k].size());
+      total += slot[k].size();
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      ready[k] = 0;
+      ++written;
+    }
+    cv_free.notify_all();
+    if (!ok) {
+      stop.store(true);
+      cv_free.notify_all();
+      break;
     }
   }
+  for (auto& th : pool) th.join();
   ok = (std::fclose(f) == 0) && ok;
   if (!ok) {
     set_err(err, KIN_ERR_INPUT, (std::string("write failed: ") + path).c_str());
