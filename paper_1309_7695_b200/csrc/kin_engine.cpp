@@ -741,6 +741,15 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
       bf.last_count = want_work;
     }
   }
+  if (e == cudaErrorInvalidConfiguration) {
+    // the launchers' own pre-check: the per-simulation state of this model does
+    // not fit the kernel's shared-memory budget (a property of the input)
+    cudaGetLastError();
+    set_err(err, KIN_ERR_INPUT,
+            std::string("model too large for the ") + bf.kernel_name +
+                " (per-simulation state exceeds the shared-memory budget)");
+    return KIN_ERR_INPUT;
+  }
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
   KIN_CUDA(cudaEventRecord(bf.tev[1], sl.stream), "event");
   bf.timed_stats = false;

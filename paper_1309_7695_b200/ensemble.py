@@ -168,6 +168,8 @@ def _meta(row) -> TrajectoryMeta:
 def make_sweep_desc(network: ReactionNetwork, config: SweepConfig, *, seed_mode: int = abi.SEED_SWEEP,
                     rng_mode: int = abi.RNG_COMPAT, sim_range=None):
     """Pack a SweepConfig into kin_sweep_desc.  Returns (desc, keepalive)."""
+    if int(config.runs_per_point) < 1:
+        raise ValidationError("runs_per_point must be >= 1")  # the engine's sweep_layout check
     keep = []
     axes = (abi.KinSweepAxis * max(1, len(config.axes)))()
     for i, ax in enumerate(config.axes):
