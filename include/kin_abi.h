@@ -205,6 +205,21 @@ int kin_sweep_size(const kin_sweep_desc* desc, uint64_t* n_points,
 int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc,
                   kin_sweep_out* out, kin_error* err);
 
+/* run_ensemble (ensemble.hpp:91-99): n_runs runs of one model, run i seeded
+   with derive_run_seed(master_seed, i); outputs as kin_sweep_run with one
+   point (traj [n_runs][G][N], meta/status [n_runs], mean/m2 [G][N]).  Runs are
+   split across the context's devices; their statistics are Chan-merged in
+   ascending device-range order. */
+int kin_ensemble_run(kin_ctx* ctx, const kin_model* model, const kin_method* method, uint64_t n_runs,
+                     uint64_t master_seed, double t_end, const double* grid, int32_t n_grid, int32_t rng_mode,
+                     kin_sweep_out* out, kin_error* err);
+
+/* run_single (ensemble.hpp:73-76): one run seeded with `seed` itself;
+   samples [G][N] and meta[6] (either may be NULL). */
+int kin_run_single(kin_ctx* ctx, const kin_model* model, const kin_method* method, double t_end,
+                   const double* grid, int32_t n_grid, uint64_t seed, int32_t rng_mode, double* samples,
+                   uint64_t* meta, kin_error* err);
+
 /* The chunk plan kin_sweep_run uses for n_devices GPUs over simulations
    [s0, s1) with R runs per point: n_chunks = (n_devices == 1 ? 1 : min(#points,
    4*n_devices)) whole-point chunks (boundaries snapped to multiples of R) — or,

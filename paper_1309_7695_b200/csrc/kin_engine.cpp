@@ -1115,6 +1115,44 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
   return KIN_OK;
 }
 
+int kin_ensemble_run(kin_ctx* ctx, const kin_model* model, const kin_method* method, uint64_t n_runs,
+                     uint64_t master_seed, double t_end, const double* grid, int32_t n_grid, int32_t rng_mode,
+                     kin_sweep_out* out, kin_error* err) {
+  if (!method) { set_err(err, KIN_ERR_USAGE, "null method"); return KIN_ERR_USAGE; }
+  kin_sweep_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.method = *method;
+  d.runs_per_point = n_runs;
+  d.master_seed = master_seed;
+  d.seed_mode = KIN_SEED_ENSEMBLE;
+  d.rng_mode = rng_mode;
+  d.t_end = t_end;
+  d.n_grid = n_grid;
+  d.grid = grid;
+  return kin_sweep_run(ctx, model, &d, out, err);
+}
+
+int kin_run_single(kin_ctx* ctx, const kin_model* model, const kin_method* method, double t_end,
+                   const double* grid, int32_t n_grid, uint64_t seed, int32_t rng_mode, double* samples,
+                   uint64_t* meta, kin_error* err) {
+  if (!method) { set_err(err, KIN_ERR_USAGE, "null method"); return KIN_ERR_USAGE; }
+  kin_sweep_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.method = *method;
+  d.runs_per_point = 1;
+  d.master_seed = seed;
+  d.seed_mode = KIN_SEED_DIRECT;
+  d.rng_mode = rng_mode;
+  d.t_end = t_end;
+  d.n_grid = n_grid;
+  d.grid = grid;
+  kin_sweep_out o;
+  std::memset(&o, 0, sizeof o);
+  o.traj = samples;
+  o.meta = meta;
+  return kin_sweep_run(ctx, model, &d, &o, err);
+}
+
 int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   std::unique_ptr<Job> job;

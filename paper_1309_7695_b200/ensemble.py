@@ -355,24 +355,44 @@ class EnsembleOptions:
 def run_ensemble(network: ReactionNetwork, options: EnsembleOptions,
                  sink: Optional[Callable[[int, Trajectory], None]] = None,
                  engine: Optional[Engine] = None) -> EnsembleStatistics:
-    """ensemble.hpp:91-99: run i seeded with derive_run_seed(master, i)."""
+    """ensemble.hpp:91-99 (kin_ensemble_run): run i seeded with
+    derive_run_seed(master, i); the runs are split over the engine's devices
+    and their statistics Chan-merged in ascending device-range order."""
     eng = engine or default_engine()
-    cfg = SweepConfig([], options.n_runs, options.method, options.master_seed, options.t_end, options.grid)
-    res = eng.sweep(network, cfg, seed_mode=abi.SEED_ENSEMBLE, want_traj=sink is not None, want_stats=True)
-    grid = np.asarray(options.grid, dtype=np.float64)
+    grid = np.ascontiguousarray(options.grid, dtype=np.float64)
+    R, G, N = int(options.n_runs), len(grid), network.species_count()
+    if R < 1:
+        raise ValidationError("n_runs must be >= 1")
+    traj = np.zeros((R, G, N)) if sink is not None else None
+    meta = np.zeros((R, 6), dtype=np.uint64)
+    status = np.zeros(R, dtype=np.int32)
+    mean, m2 = np.zeros((G, N)), np.zeros((G, N))
+    o = abi.KinSweepOut(abi.ptr(traj, C.c_double), abi.ptr(meta, C.c_uint64), abi.ptr(status, C.c_int32),
+                        abi.ptr(mean, C.c_double), abi.ptr(m2, C.c_double), None)
+    m = options.method.c()
+    err = abi.KinError()
+    rc = eng.lib.kin_ensemble_run(eng.ctx, eng.model(network), C.byref(m), R, int(options.master_seed),
+                                  float(options.t_end), abi.ptr(grid, C.c_double), G, abi.RNG_COMPAT, C.byref(o),
+                                  C.byref(err))
+    _raise(rc, err)
     if sink is not None:
-        lib = eng.lib
-        for i in range(options.n_runs):
-            sink(i, Trajectory(grid, res["traj"][i], options.method.name(),
-                               int(lib.kin_derive_run_seed(options.master_seed, i)), _meta(res["meta"][i])))
-    return EnsembleStatistics(grid, network.species_count(), options.n_runs, res["mean"][0], res["m2"][0])
+        for i in range(R):
+            sink(i, Trajectory(grid, traj[i], options.method.name(),
+                               int(eng.lib.kin_derive_run_seed(options.master_seed, i)), _meta(meta[i])))
+    return EnsembleStatistics(grid, N, R, mean, m2)
 
 
 def run_single(network: ReactionNetwork, method: Method, t_end: float, grid: Sequence[float], seed: int,
                engine: Optional[Engine] = None) -> Trajectory:
-    """ensemble.hpp:73-76."""
+    """ensemble.hpp:73-76 (kin_run_single): one run seeded with `seed` itself."""
     eng = engine or default_engine()
-    cfg = SweepConfig([], 1, method, seed, t_end, grid)
-    res = eng.sweep(network, cfg, seed_mode=abi.SEED_DIRECT, want_traj=True, want_stats=False)
-    return Trajectory(np.asarray(grid, dtype=np.float64), res["traj"][0], method.name(),
-                      None if method.deterministic() else int(seed), _meta(res["meta"][0]))
+    g = np.ascontiguousarray(grid, dtype=np.float64)
+    samples = np.zeros((len(g), network.species_count()))
+    meta = np.zeros(6, dtype=np.uint64)
+    m = method.c()
+    err = abi.KinError()
+    rc = eng.lib.kin_run_single(eng.ctx, eng.model(network), C.byref(m), float(t_end), abi.ptr(g, C.c_double), len(g),
+                                int(seed), abi.RNG_COMPAT, abi.ptr(samples, C.c_double), abi.ptr(meta, C.c_uint64),
+                                C.byref(err))
+    _raise(rc, err)
+    return Trajectory(g, samples, method.name(), None if method.deterministic() else int(seed), _meta(meta))
