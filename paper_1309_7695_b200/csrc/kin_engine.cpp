@@ -416,6 +416,7 @@ struct Buffers {
   DevBuf<unsigned long long> counter;
   DevBuf<int> ovf;
   int* ovf_host = nullptr;  // pinned copy of the overflow flag
+  cudaStream_t st = nullptr;  // compute stream of this launch (one of the slot's)
   cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // sim start, sim end, stats end
   cudaEvent_t ev_done = nullptr, ev_copied = nullptr;
   bool timed_stats = false;
@@ -458,8 +459,12 @@ struct Buffers {
 
 struct Slot {
   int device = 0;
-  cudaStream_t stream = nullptr;       // kernels
+  cudaStream_t stream = nullptr;       // kernels (device-resident API; every other async job)
+  cudaStream_t aux_stream = nullptr;   // kernels of the alternate async jobs: two independent
+                                       // sweeps in flight overlap (one fills the SMs the
+                                       // other's tail leaves idle)
   cudaStream_t copy_stream = nullptr;  // copy-out of async jobs
+  unsigned job_rr = 0;
   DevBuf<double> lgamma_tab;  // glibc lgamma(k+1), k < KIN_LGAMMA_N
   DevBuf<double> lsoda_co;    // cfode elco/tesco
   void* stage = nullptr;
@@ -604,12 +609,12 @@ int launch_stats(Slot& sl, Buffers& bf, kin_error* err) {
   const size_t gn = static_cast<size_t>(bf.last_gn);
   if (bf.have_stats) {
     cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.R, bf.last_base, bf.nP, bf.mean.p, bf.m2.p,
-                                            sl.stream);
+                                            bf.st);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
   }
   for (int k = 0; k < bf.n_partial; ++k) {
     cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.partial_n[k], bf.partial_base[k], 1,
-                                            bf.pmean.p + k * gn, bf.pm2.p + k * gn, sl.stream);
+                                            bf.pmean.p + k * gn, bf.pm2.p + k * gn, bf.st);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
   }
   return KIN_OK;
@@ -617,6 +622,7 @@ int launch_stats(Slot& sl, Buffers& bf, kin_error* err) {
 
 int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc* d, const Layout& L, uint64_t s0,
                  uint64_t s1, bool want_stats, bool want_work, kin_error* err, bool want_partials = false) {
+  if (!bf.st) bf.st = sl.stream;
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
   KinTables* T = new KinTables;
   std::unique_ptr<KinTables> Tguard(T);
@@ -656,10 +662,10 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
     SD.axis_n[ax] = d->axes[ax].n_values;
     SD.axis_values[ax] = bf.axis.p + at;
     KIN_CUDA(cudaMemcpyAsync(bf.axis.p + at, d->axes[ax].values, sizeof(double) * d->axes[ax].n_values,
-                             cudaMemcpyHostToDevice, sl.stream), "H2D axes");
+                             cudaMemcpyHostToDevice, bf.st), "H2D axes");
     at += d->axes[ax].n_values;
   }
-  if (G) KIN_CUDA(cudaMemcpyAsync(bf.grid.p, d->grid, sizeof(double) * G, cudaMemcpyHostToDevice, sl.stream), "H2D grid");
+  if (G) KIN_CUDA(cudaMemcpyAsync(bf.grid.p, d->grid, sizeof(double) * G, cudaMemcpyHostToDevice, bf.st), "H2D grid");
   SD.runs = L.R;
   SD.master_seed = d->master_seed;
   SD.sim_begin = s0;
@@ -670,12 +676,12 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   KinOutDev O{bf.traj.p, bf.meta.p, bf.status.p, want_work ? bf.work.p : nullptr};
   if (!bf.tev[0])
     for (auto& ev : bf.tev) KIN_CUDA(cudaEventCreate(&ev), "event");
-  KIN_CUDA(cudaEventRecord(bf.tev[0], sl.stream), "event");
+  KIN_CUDA(cudaEventRecord(bf.tev[0], bf.st), "event");
   cudaError_t e;
   const int kind = d->method.kind;
   bf.last_int_state = false;  // set below only by the int32-state stochastic launch
   if (kind == KIN_METHOD_ODE) {
-    e = kin::launch_dopri5(*T, SD, O, want_work, 0, sl.stream);
+    e = kin::launch_dopri5(*T, SD, O, want_work, 0, bf.st);
     bf.kernel_name = "dopri5_kernel";
   } else if (kind == KIN_METHOD_HYBRID) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
@@ -683,11 +689,11 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
       set_err(err, KIN_ERR_INPUT, "model too large for the hybrid kernel (per-simulation state exceeds shared memory)");
       return KIN_ERR_INPUT;
     }
-    e = kin::launch_hybrid(*T, SD, O, want_work, bf.counter.p, sl.stream);
+    e = kin::launch_hybrid(*T, SD, O, want_work, bf.counter.p, bf.st);
     bf.kernel_name = "hybrid_kernel";
   } else if (kind == KIN_METHOD_CLE) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
-    e = kin::launch_cle(*T, SD, O, want_work, bf.counter.p, sl.stream);
+    e = kin::launch_cle(*T, SD, O, want_work, bf.counter.p, bf.st);
     bf.kernel_name = "cle_kernel";
   } else if (kind == KIN_METHOD_LSODA) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
@@ -695,7 +701,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
       set_err(err, KIN_ERR_INPUT, "model too large for the LSODA kernel (per-simulation state exceeds shared memory)");
       return KIN_ERR_INPUT;
     }
-    e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, sl.stream);
+    e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, bf.st);
     bf.kernel_name = "lsoda_kernel";
   } else {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
@@ -707,7 +713,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
     if (d->rng_mode != KIN_RNG_PHILOX) lanes = 1;
     else if (lanes <= 0) lanes = kin::stochastic_group_pick_lanes(H.n, H.m);
     if (lanes != 1) {
-      e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, bf.counter.p, sl.stream);
+      e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, bf.counter.p, bf.st);
       bf.last_int_state = false;
       bf.kernel_name = "stochastic_group_kernel";
     } else {
@@ -720,15 +726,15 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
           for (int v = 0; v < d->axes[ax].n_values; ++v) xmax = std::max(xmax, d->axes[ax].values[v]);
       bool int_state = xmax < 1073741824.0;
       if (const char* v = std::getenv("KIN_INT_STATE")) int_state = int_state && std::atoi(v) != 0;
-      KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), sl.stream), "memset");
+      KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), bf.st), "memset");
       bool used = false;
       e = cudaSuccess;
       if (kin::jit_wanted(S)) {
         const kin::JitModel jm = jit_model(H, d);
-        e = kin::launch_stochastic_jit(jm, *T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, sl.stream, &used);
+        e = kin::launch_stochastic_jit(jm, *T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, bf.st, &used);
       }
       if (e == cudaSuccess && !used)
-        e = kin::launch_stochastic(*T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, sl.stream);
+        e = kin::launch_stochastic(*T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, bf.st);
       bf.last_jit = used;
       bf.kernel_name = used ? "kin_jit_stoch" : "stochastic_kernel";
       bf.last_int_state = int_state;
@@ -751,7 +757,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
     return KIN_ERR_INPUT;
   }
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
-  KIN_CUDA(cudaEventRecord(bf.tev[1], sl.stream), "event");
+  KIN_CUDA(cudaEventRecord(bf.tev[1], bf.st), "event");
   bf.timed_stats = false;
   // per-point statistics for points entirely inside [s0, s1), and (when the
   // caller merges chunks) partial statistics of the points cut by a chunk edge
@@ -788,7 +794,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   bf.have_stats = want_stats && nP;
   if (int rc = launch_stats(sl, bf, err)) return rc;
   if (bf.have_stats || bf.n_partial) {
-    KIN_CUDA(cudaEventRecord(bf.tev[2], sl.stream), "event");
+    KIN_CUDA(cudaEventRecord(bf.tev[2], bf.st), "event");
     bf.timed_stats = true;
   }
   bf.pending_check = bf.last_int_state;
@@ -807,18 +813,18 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
 // stochastic kernel with double amounts (and the statistics) — same results.
 int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
-  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
+  KIN_CUDA(cudaStreamSynchronize(bf.st), "stream sync");
   if (!bf.pending_check) return KIN_OK;
   bf.pending_check = false;
   int flag = 0;
   KIN_CUDA(cudaMemcpy(&flag, bf.ovf.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H overflow flag");
   if (!flag) return KIN_OK;
-  KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), sl.stream), "memset");
+  KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), bf.st), "memset");
   cudaError_t e = kin::launch_stochastic(*bf.last_T, bf.last_SD, bf.last_O, bf.last_count, bf.counter.p, bf.ovf.p,
-                                         false, sl.stream);
+                                         false, bf.st);
   if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel relaunch");
   if (int rc = launch_stats(sl, bf, err)) return rc;
-  KIN_CUDA(cudaStreamSynchronize(sl.stream), "stream sync");
+  KIN_CUDA(cudaStreamSynchronize(bf.st), "stream sync");
   return KIN_OK;
 }
 
@@ -828,7 +834,7 @@ int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
 // the compute stream.
 int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, bool sync,
              kin_error* err) {
-  cudaStream_t st = sync ? sl.stream : sl.copy_stream;
+  cudaStream_t st = sync ? bf.st : sl.copy_stream;
   const uint64_t S = bf.s1 - bf.s0;
   const size_t gn = static_cast<size_t>(bf.G) * bf.N;
   const uint64_t so = bf.s0 - base_sim;
@@ -987,6 +993,7 @@ int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err)
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dv);
     if (major < 10) { set_err(err, KIN_ERR_DEVICE, "engine is built for sm_100a (B200) only"); return KIN_ERR_DEVICE; }
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    KIN_CUDA(cudaStreamCreateWithFlags(&sl->aux_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     // lgamma(k+1) from the host libm (the oracle's, glibc) for the PTRS test
     std::vector<double> lg(KIN_LGAMMA_N);
@@ -1013,6 +1020,7 @@ void kin_ctx_destroy(kin_ctx* ctx) {
   for (auto& sl : ctx->slots) {
     cudaSetDevice(sl->device);
     cudaStreamSynchronize(sl->stream);
+    cudaStreamSynchronize(sl->aux_stream);
     cudaStreamSynchronize(sl->copy_stream);
     sl->main.release();
     for (auto& b : sl->pool) b->release();
@@ -1021,6 +1029,7 @@ void kin_ctx_destroy(kin_ctx* ctx) {
     if (sl->stage) cudaFreeHost(sl->stage);
     for (auto& e : sl->ev) if (e) cudaEventDestroy(e);
     cudaStreamDestroy(sl->stream);
+    cudaStreamDestroy(sl->aux_stream);
     cudaStreamDestroy(sl->copy_stream);
   }
   delete ctx;
@@ -1097,13 +1106,14 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
       bf = new Buffers;
     }
     job->parts.push_back({dv, bf});
+    bf->st = (sl.job_rr++ & 1u) ? sl.aux_stream : sl.stream;
     const bool partials = stats && bounds.size() > 2;
     if (int rc = launch_range(sl, *bf, model->host, desc, L, c0, c1, stats, job->out.work != nullptr, err, partials))
       return rc;
     if (!bf->ev_done) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_done, cudaEventDisableTiming), "event");
     if (!bf->ev_copied) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_copied, cudaEventDisableTiming), "event");
     if (!bf->ovf_host) KIN_CUDA(cudaMallocHost(&bf->ovf_host, sizeof(int)), "pinned flag");
-    KIN_CUDA(cudaEventRecord(bf->ev_done, sl.stream), "event");
+    KIN_CUDA(cudaEventRecord(bf->ev_done, bf->st), "event");
     // copy-out on the copy stream, overlapping the next launches on `stream`
     KIN_CUDA(cudaStreamWaitEvent(sl.copy_stream, bf->ev_done, 0), "stream wait");
     if (int rc = copy_out(sl, *bf, &job->out, s0, job->base_point, false, err)) return rc;
