@@ -1091,33 +1091,50 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
   const int D = static_cast<int>(ctx->slots.size());
   const std::vector<uint64_t> bounds = plan_chunks(s0, s1, L.R, D);
   const bool stats = job->out.mean || job->out.m2;
-  for (size_t c = 0; c + 1 < bounds.size(); ++c) {
-    const uint64_t c0 = bounds[c], c1 = bounds[c + 1];
-    if (c0 >= c1) continue;
-    const int dv = static_cast<int>(c % D);
-    Slot& sl = *ctx->slots[dv];
-    std::lock_guard<std::mutex> lk(sl.mu);
-    KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
-    Buffers* bf;
-    if (!sl.pool.empty()) {
-      bf = sl.pool.back().release();
-      sl.pool.pop_back();
-    } else {
-      bf = new Buffers;
+  auto enqueue = [&]() -> int {
+    for (size_t c = 0; c + 1 < bounds.size(); ++c) {
+      const uint64_t c0 = bounds[c], c1 = bounds[c + 1];
+      if (c0 >= c1) continue;
+      const int dv = static_cast<int>(c % D);
+      Slot& sl = *ctx->slots[dv];
+      std::lock_guard<std::mutex> lk(sl.mu);
+      KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+      Buffers* bf;
+      if (!sl.pool.empty()) {
+        bf = sl.pool.back().release();
+        sl.pool.pop_back();
+      } else {
+        bf = new Buffers;
+      }
+      job->parts.push_back({dv, bf});
+      bf->st = (sl.job_rr++ & 1u) ? sl.aux_stream : sl.stream;
+      const bool partials = stats && bounds.size() > 2;
+      if (int rc = launch_range(sl, *bf, model->host, desc, L, c0, c1, stats, job->out.work != nullptr, err, partials))
+        return rc;
+      if (!bf->ev_done) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_done, cudaEventDisableTiming), "event");
+      if (!bf->ev_copied) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_copied, cudaEventDisableTiming), "event");
+      if (!bf->ovf_host) KIN_CUDA(cudaMallocHost(&bf->ovf_host, sizeof(int)), "pinned flag");
+      KIN_CUDA(cudaEventRecord(bf->ev_done, bf->st), "event");
+      // copy-out on the copy stream, overlapping the next launches on `stream`
+      KIN_CUDA(cudaStreamWaitEvent(sl.copy_stream, bf->ev_done, 0), "stream wait");
+      if (int rc = copy_out(sl, *bf, &job->out, s0, job->base_point, false, err)) return rc;
+      KIN_CUDA(cudaEventRecord(bf->ev_copied, sl.copy_stream), "event");
     }
-    job->parts.push_back({dv, bf});
-    bf->st = (sl.job_rr++ & 1u) ? sl.aux_stream : sl.stream;
-    const bool partials = stats && bounds.size() > 2;
-    if (int rc = launch_range(sl, *bf, model->host, desc, L, c0, c1, stats, job->out.work != nullptr, err, partials))
-      return rc;
-    if (!bf->ev_done) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_done, cudaEventDisableTiming), "event");
-    if (!bf->ev_copied) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_copied, cudaEventDisableTiming), "event");
-    if (!bf->ovf_host) KIN_CUDA(cudaMallocHost(&bf->ovf_host, sizeof(int)), "pinned flag");
-    KIN_CUDA(cudaEventRecord(bf->ev_done, bf->st), "event");
-    // copy-out on the copy stream, overlapping the next launches on `stream`
-    KIN_CUDA(cudaStreamWaitEvent(sl.copy_stream, bf->ev_done, 0), "stream wait");
-    if (int rc = copy_out(sl, *bf, &job->out, s0, job->base_point, false, err)) return rc;
-    KIN_CUDA(cudaEventRecord(bf->ev_copied, sl.copy_stream), "event");
+    return KIN_OK;
+  };
+  if (int rc = enqueue()) {
+    // a chunk failed to enqueue: drain the chunks already in flight and give
+    // their buffers back, so nothing writes into `out` after we return
+    for (auto& part : job->parts) {
+      Slot& sl = *ctx->slots[part.slot];
+      cudaSetDevice(sl.device);
+      if (part.buf->st) cudaStreamSynchronize(part.buf->st);
+      cudaStreamSynchronize(sl.copy_stream);
+      std::lock_guard<std::mutex> lk(sl.mu);
+      sl.pool.emplace_back(part.buf);
+    }
+    job->parts.clear();
+    return rc;
   }
   std::lock_guard<std::mutex> lk(ctx->jobs_mu);
   *ticket = ctx->next_ticket++;

@@ -81,3 +81,21 @@ def test_zero_runs_is_input_error(engine):
     cfg = SweepConfig([], 0, Method(MethodKind.Ssa), 1, 1.0, [0.0, 1.0])
     with pytest.raises(ValidationError):
         engine.sweep(net, cfg)
+
+
+def test_failed_submit_leaves_engine_usable():
+    """A sweep that fails to enqueue (here: state too large for the hybrid
+    kernel) returns its in-flight chunks' buffers; the context keeps working."""
+    from paper_1309_7695_b200 import Engine
+    eng = Engine([0, 0])
+    try:
+        big = decay_chain(64)
+        cfg = SweepConfig([], 64, method(MethodKind.Hybrid), 1, 1.0, uniform_grid(1.0, 3))
+        for _ in range(3):
+            with pytest.raises(ValidationError, match="too large"):
+                eng.sweep(big, cfg)
+        net, ok_cfg = W.c1_config(MethodKind.TauAdaptive, side=4)
+        a = eng.sweep(net, ok_cfg, want_traj=True)
+        assert (a["status"] == 0).all()
+    finally:
+        eng.close()
