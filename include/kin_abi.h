@@ -272,6 +272,17 @@ uint64_t kin_derive_run_seed(uint64_t master, uint64_t index);  /* ensemble.hpp:
 int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
                          int32_t n, uint64_t* out_bits, kin_error* err);
 
+/* Device unit seams (SPEC's from_uniforms / from_counts / from_normals forms):
+   one function of the path on one state x[N] of `model`, through the same
+   device code the sweep kernels run (propensities from the packed tables).
+     kind 0 propensities (model.hpp:151-157)          out[M] = a(x)
+     kind 1 select_tau (stochastic.hpp:40-46)         params {eps} -> out[0] = tau (+inf if a0 = 0)
+     kind 2 ssa_step_from_uniforms (:28-32)           params {u1, u2} -> out {dt, j} ({+inf, -1} if a0 = 0)
+     kind 3 tau_leap_step_from_counts (:59-62)        params counts[M] -> out[0..N-1] = x', out[N] = rejected
+     kind 4 cle_step_from_normals (:71-75)            params {h, z[M]} -> out[0..N-1] = x', out[N] = clamped */
+int kin_device_unit(kin_ctx* ctx, const kin_model* model, int32_t kind, const double* x, const double* params,
+                    int32_t n_params, double* out, int32_t out_cap, kin_error* err);
+
 /* Diagnostic: generate and NVRTC-compile (sm_100a) the per-model specialised
    stochastic kernel for this model + sweep binding, without a GPU.  log gets
    the compiler output. */

@@ -100,7 +100,7 @@ ABI_SYMBOLS = (
     "kin_model_text_param_name", "kin_model_text_reaction_name", "kin_model_text_species_index",
     "kin_model_text_param_index", "kin_model_render",
     "kin_format_double", "kin_fnv1a64", "kin_fnv1a64_update", "kin_csv_render", "kin_csv_write",
-    "kin_ensemble_run", "kin_run_single", "kin_stats_merge", "kin_visible_devices", "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
+    "kin_device_unit", "kin_ensemble_run", "kin_run_single", "kin_stats_merge", "kin_visible_devices", "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
     "kin_model_free", "kin_sweep_size", "kin_sweep_plan", "kin_sweep_run", "kin_sweep_submit", "kin_sweep_wait", "kin_sweep_launch", "kin_sweep_sync",
     "kin_sweep_fetch", "kin_ctx_stream", "kin_sweep_kernel_ms", "kin_sweep_kernel_name", "kin_splitmix64_mix", "kin_derive_run_seed",
     "kin_device_rng_draws", "kin_jit_check", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
@@ -111,6 +111,7 @@ def _declare(lib: C.CDLL) -> C.CDLL:
     vp = C.c_void_p
     E = C.POINTER(KinError)
     sig = {
+        "kin_device_unit": (C.c_int, [vp, vp, C.c_int32, f64p, f64p, C.c_int32, f64p, C.c_int32, E]),
         "kin_ensemble_run": (C.c_int, [vp, vp, C.POINTER(KinMethod), C.c_uint64, C.c_uint64, C.c_double, f64p,
                                        C.c_int32, C.c_int32, C.POINTER(KinSweepOut), E]),
         "kin_run_single": (C.c_int, [vp, vp, C.POINTER(KinMethod), C.c_double, f64p, C.c_int32, C.c_uint64, C.c_int32,

@@ -1373,6 +1373,49 @@ int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
   return KIN_OK;
 }
 
+int kin_device_unit(kin_ctx* ctx, const kin_model* model, int32_t kind, const double* x, const double* params,
+                    int32_t n_params, double* out, int32_t out_cap, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || ctx->slots.empty() || !model || !x || !out || kind < 0 || kind > 4) {
+    set_err(err, KIN_ERR_USAGE, "bad argument");
+    return KIN_ERR_USAGE;
+  }
+  const HostModel& H = model->host;
+  const int need_params[5] = {0, 1, 2, H.m, 1 + H.m};
+  const int need_out[5] = {H.m, 1, 2, H.n + 1, H.n + 1};
+  if (n_params < need_params[kind] || (need_params[kind] && !params) || out_cap < need_out[kind]) {
+    set_err(err, KIN_ERR_USAGE, "params/out too small for this unit");
+    return KIN_ERR_USAGE;
+  }
+  // tables for a sweep with no axes (the unit reads rates, reactant terms and nu)
+  const double g0 = 0.0;
+  kin_sweep_desc d;
+  std::memset(&d, 0, sizeof d);
+  d.runs_per_point = 1;
+  d.n_grid = 1;
+  d.grid = &g0;
+  auto T = std::make_unique<KinTables>();
+  std::string msg;
+  if (int rc = pack_tables(H, &d, T.get(), &msg)) { set_err(err, rc, msg); return rc; }
+  Slot& sl = *ctx->slots[0];
+  std::lock_guard<std::mutex> lk(sl.mu);
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  const size_t nx = static_cast<size_t>(std::max(H.n, 1)), np = static_cast<size_t>(std::max(n_params, 1));
+  const size_t no = static_cast<size_t>(need_out[kind]);
+  double* dev = nullptr;
+  KIN_CUDA(cudaMalloc(&dev, sizeof(double) * (nx + np + no)), "cudaMalloc");
+  cudaError_t e = cudaMemcpyAsync(dev, x, sizeof(double) * H.n, cudaMemcpyHostToDevice, sl.stream);
+  if (e == cudaSuccess && n_params > 0)
+    e = cudaMemcpyAsync(dev + nx, params, sizeof(double) * n_params, cudaMemcpyHostToDevice, sl.stream);
+  if (e == cudaSuccess) e = kin::launch_unit(*T, kind, dev, dev + nx, dev + nx + np, sl.stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(out, dev + nx + np, sizeof(double) * no, cudaMemcpyDeviceToHost, sl.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
+  cudaFree(dev);
+  if (e != cudaSuccess) return cuda_fail(err, e, "unit kernel");
+  return KIN_OK;
+}
+
 int kin_measure_fp64_peak(kin_ctx* ctx, double* tflops, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
   if (!ctx || ctx->slots.empty() || !tflops) { set_err(err, KIN_ERR_USAGE, "bad argument"); return KIN_ERR_USAGE; }

@@ -32,6 +32,9 @@ size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S);
 cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, const double* coeffs,
                          unsigned long long* counter, cudaStream_t stream);
 
+// kin_stochastic.cu: unit seam (one path function on one state, kin_device_unit).
+cudaError_t launch_unit(const KinTables& T, int kind, const double* x, const double* params, double* out,
+                        cudaStream_t stream);
 // kin_stochastic.cu: Chemical Langevin (Euler-Maruyama) sweep, double amounts.
 cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                        unsigned long long* counter, cudaStream_t stream);

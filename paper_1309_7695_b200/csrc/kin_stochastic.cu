@@ -50,6 +50,36 @@ __global__ void __launch_bounds__(stoch::kBlock) stochastic_kernel(const __grid_
 // Double amounts (the state is real-valued).  log/sin/cos are CUDA's (<= 1-2
 // ulp from glibc's), so parity with the oracle is within a tolerance, not bit
 // for bit.
+// cle_step_from_normals pieces (stochastic.hpp:71-75), shared with the
+// kin_device_unit seam: the increment a_j h + sqrt(a_j h) z_j, its application
+// along nu[:, j], and the final clamp (count of components set to 0).
+__device__ __forceinline__ double cle_increment(double aj, double h, double z) {
+  const double d = __dmul_rn(aj, h);
+  return __dadd_rn(d, __dmul_rn(sqrt(d), z));
+}
+template <int B>
+__device__ __forceinline__ void cle_apply(const KinTables& T, double* x, int j, double inc) {
+  const int p1 = tab_col_ptr(T, j + 1);
+  for (int p = tab_col_ptr(T, j); p < p1; ++p) {
+    const uint32_t e = tab_col(T, p);
+    double* xs = x + KIN_NU_INDEX(e) * B;
+    *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), inc));
+  }
+}
+template <int B>
+__device__ __forceinline__ uint64_t cle_clamp(double* x, int N, bool* bad) {
+  uint64_t n = 0;
+  for (int i = 0; i < N; ++i) {
+    const double v = x[i * B];
+    *bad |= !isfinite(v);
+    if (v < 0.0) {
+      x[i * B] = 0.0;
+      ++n;
+    }
+  }
+  return n;
+}
+
 template <bool kCount, bool kPhilox>
 __device__ __forceinline__ void simulate_cle_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
                                                  uint64_t s, double* x, double* a, double* av) {
@@ -107,25 +137,11 @@ __device__ __forceinline__ void simulate_cle_one(const KinTables& T, const KinSw
         if (kCount) flops += 4 + 3 + 1 + 2 + 2;
       }
       if (!kPhilox) ++n_normal;
-      const double d = __dmul_rn(sm.aval(j), h);
-      const double inc = __dadd_rn(d, __dmul_rn(sqrt(d), z));
-      const int p1 = tab_col_ptr(T, j + 1);
-      for (int p = tab_col_ptr(T, j); p < p1; ++p) {
-        const uint32_t e = tab_col(T, p);
-        double* xs = x + KIN_NU_INDEX(e) * B;
-        *xs = __dadd_rn(*xs, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), inc));
-      }
-      if (kCount) flops += 4 + 2 * static_cast<uint64_t>(p1 - tab_col_ptr(T, j));
+      cle_apply<B>(T, x, j, cle_increment(sm.aval(j), h, z));
+      if (kCount) flops += 4 + 2 * static_cast<uint64_t>(tab_col_ptr(T, j + 1) - tab_col_ptr(T, j));
     }
     bool bad = false;
-    for (int i = 0; i < N; ++i) {
-      const double v = x[i * B];
-      bad |= !isfinite(v);
-      if (v < 0.0) {
-        x[i * B] = 0.0;
-        ++n_clamp;
-      }
-    }
+    n_clamp += cle_clamp<B>(x, N, &bad);
     if (bad) { status = KIN_SIM_NONFINITE; break; }
     ++step;
     if (hit) {
@@ -170,6 +186,48 @@ __global__ void __launch_bounds__(stoch::kBlock) cle_kernel(const __grid_constan
   }
 }
 
+// ---- unit seams (kin_device_unit): one path function on one state, through
+// the same device code the sweep kernels run.  One thread; the state sits in
+// shared memory with the kernels' [slot][thread] stride.
+__global__ void __launch_bounds__(32) unit_kernel(const __grid_constant__ KinTables T, int kind, const double* x_in,
+                                                  const double* params, double* out) {
+  extern __shared__ double smem[];
+  if (threadIdx.x != 0) return;
+  constexpr int B = kBlock;
+  const int N = T.n, M = T.m;
+  double* a = smem;                                        // a[j * B]
+  double* x = smem + static_cast<size_t>(M) * B;           // x[i * B]
+  for (int i = 0; i < N; ++i) x[i * B] = x_in[i];
+  const TableModel<double> sm{T, x, a, nullptr};
+  const double a0 = sm.all_props(M);
+  if (kind == 0) {                                          // propensities
+    for (int j = 0; j < M; ++j) out[j] = sm.aval(j);
+  } else if (kind == 1) {                                   // select_tau (+inf when a0 == 0)
+    uint64_t fl = 0;
+    out[0] = a0 == 0.0 ? KIN_INF : sm.select_tau<false>(params[0], fl);
+  } else if (kind == 2) {                                   // ssa_step_from_uniforms
+    if (a0 == 0.0) {
+      out[0] = KIN_INF;
+      out[1] = -1.0;
+    } else {
+      out[0] = stoch::ssa_dt(params[0], a0);
+      out[1] = static_cast<double>(stoch::ssa_select(sm, M, a0, params[1]));
+    }
+  } else if (kind == 3) {                                   // tau_leap_step_from_counts
+    bool ovf = false;
+    for (int j = 0; j < M; ++j)
+      if (params[j] != 0.0) sm.apply(j, static_cast<long long>(params[j]), ovf);
+    for (int i = 0; i < N; ++i) out[i] = x[i * B];
+    out[N] = sm.any_negative() ? 1.0 : 0.0;
+  } else if (kind == 4) {                                   // cle_step_from_normals
+    for (int j = 0; j < M; ++j) cle_apply<B>(T, x, j, cle_increment(sm.aval(j), params[0], params[1 + j]));
+    bool bad = false;
+    const uint64_t c = cle_clamp<B>(x, N, &bad);
+    for (int i = 0; i < N; ++i) out[i] = x[i * B];
+    out[N] = static_cast<double>(c);
+  }
+}
+
 size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block, bool int_state) {
   return static_cast<size_t>(T.m + S.n_axes) * block * sizeof(double) +
          static_cast<size_t>(T.n) * block * (int_state ? sizeof(int32_t) : sizeof(double));
@@ -201,6 +259,16 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
 }
 
 }  // namespace
+
+cudaError_t launch_unit(const KinTables& T, int kind, const double* x, const double* params, double* out,
+                        cudaStream_t stream) {
+  const size_t smem = static_cast<size_t>(T.m + T.n) * kBlock * sizeof(double);
+  if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  unit_kernel<<<1, 32, smem, stream>>>(T, kind, x, params, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                        unsigned long long* counter, cudaStream_t stream) {

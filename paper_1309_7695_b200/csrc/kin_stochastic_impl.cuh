@@ -175,6 +175,26 @@ struct TableModel {
 // The simulation's sweep coordinates (Cartesian decode, last axis fastest,
 // SPEC.md:441) into av[], and its initial amounts into x[]; returns true when
 // an amount does not fit XT = int32.
+// ssa_step_from_uniforms (stochastic.hpp:28-32): the waiting
+// time ln(1/u1)/a0 and the first reaction whose cumulative propensity exceeds
+// u2*a0 (the last one with a_j > 0 if rounding leaves none).  Shared by the
+// kernels and the kin_device_unit seam.
+__device__ __forceinline__ double ssa_dt(double u1, double a0) { return __ddiv_rn(log(__ddiv_rn(1.0, u1)), a0); }
+
+template <class Model>
+__device__ __forceinline__ int ssa_select(const Model& sm, int M, double a0, double u2) {
+  const double target = __dmul_rn(u2, a0);
+  double c = 0.0;
+  int sel = -1, last = -1;
+  for (int j = 0; j < M; ++j) {
+    const double aj = sm.aval(j);
+    if (aj > 0.0) last = j;
+    c = __dadd_rn(c, aj);
+    if (c > target) { sel = j; break; }
+  }
+  return sel < 0 ? last : sel;
+}
+
 template <class XT, int B = kBlock>
 __device__ __forceinline__ bool init_state(const KinTables& T, const KinSweepDev& S, uint64_t sim, int N, XT* x,
                                            double* av) {
@@ -266,22 +286,12 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
           u1 = rng.uniform();
           u2 = rng.uniform();
         }
-        const double dt = __ddiv_rn(log(__ddiv_rn(1.0, u1)), a0);
+        const double dt = ssa_dt(u1, a0);
         const double tn = __dadd_rn(t, dt);
         if (kCount) flops += 8;
         if (tn > t_end) { t = t_end; stop = true; break; }
         while (gi < G && tab_grid(T, S, gi) < tn) emit();
-        // first j with cumulative propensity > u2*a0
-        const double target = __dmul_rn(u2, a0);
-        double c = 0.0;
-        int sel = -1, last = -1;
-        for (int j = 0; j < M; ++j) {
-          const double aj = sm.aval(j);
-          if (aj > 0.0) last = j;
-          c = __dadd_rn(c, aj);
-          if (c > target) { sel = j; break; }
-        }
-        if (sel < 0) sel = last;
+        const int sel = ssa_select(sm, M, a0, u2);
         if (kCount) flops += 1 + static_cast<uint64_t>(sel + 1);
         if (sm.fire(sel, ovf)) { status = KIN_SIM_NEGATIVE; stop = true; break; }
         if (ovf) { stop = true; break; }

@@ -272,6 +272,22 @@ class Engine:
         self._inflight.pop(ticket, None)
         _raise(rc, err)
 
+    UNIT_PROPENSITIES, UNIT_SELECT_TAU, UNIT_SSA_STEP, UNIT_TAU_LEAP, UNIT_CLE_STEP = 0, 1, 2, 3, 4
+
+    def unit(self, network: ReactionNetwork, kind: int, x, params=()) -> np.ndarray:
+        """kin_device_unit: one path function on one state, on the GPU (the
+        reference's from_uniforms / from_counts / from_normals seams)."""
+        xs = np.ascontiguousarray(x, dtype=np.float64)
+        ps = np.ascontiguousarray(params, dtype=np.float64)
+        n, m = network.species_count(), network.reaction_count()
+        out = np.zeros(max(m, n + 1, 2))
+        err = abi.KinError()
+        rc = self.lib.kin_device_unit(self.ctx, self.model(network), int(kind), abi.ptr(xs, C.c_double),
+                                      abi.ptr(ps, C.c_double) if ps.size else None, int(ps.size),
+                                      abi.ptr(out, C.c_double), out.size, C.byref(err))
+        _raise(rc, err)
+        return out
+
     def sweep(self, network: ReactionNetwork, config: SweepConfig, *, seed_mode=abi.SEED_SWEEP,
               rng_mode=abi.RNG_COMPAT, sim_range=None, want_traj=True, want_stats=True, want_work=False):
         """Bulk form: returns dict of numpy arrays (traj [S,G,N], meta [S,6],

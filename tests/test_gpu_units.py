@@ -1,0 +1,93 @@
+"""Device unit seams (kin_device_unit) against the SPEC's known answers and the
+oracle: each function of the path on one state, through the kernels' own
+device code."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_1309_7695_b200 import workloads as W
+from paper_1309_7695_b200.model import Reaction, ReactionNetwork, Species
+
+pytestmark = pytest.mark.gpu
+
+
+def net1(reactants, products, c):
+    return ReactionNetwork.create([Species(n, 0) for n in "ABC"], [], [Reaction("r", reactants, products, c)])
+
+
+def test_propensity_examples(engine):
+    U = engine.UNIT_PROPENSITIES
+    assert engine.unit(net1({0: 1}, {1: 1}, 2.0), U, [5, 0, 0])[0] == 10.0
+    assert engine.unit(net1({0: 1, 1: 1}, {2: 1}, 0.5), U, [4, 3, 0])[0] == 6.0
+    assert engine.unit(net1({0: 2}, {1: 1}, 1.0), U, [5, 0, 0])[0] == 10.0
+    assert engine.unit(net1({0: 1}, {1: 1}, 2.0), U, [0, 0, 0])[0] == 0.0
+
+
+def test_ssa_step_examples(engine):
+    U = engine.UNIT_SSA_STEP
+    dt, j = engine.unit(net1({0: 1}, {}, 2.0), U, [1, 0, 0], [0.5, 0.5])[:2]
+    assert j == 0 and abs(dt - math.log(2) / 2) < 1e-15
+    two = ReactionNetwork.create([Species("A", 0)], [], [Reaction("r1", {}, {0: 1}, 3.0),
+                                                         Reaction("r2", {}, {0: 1}, 1.0)])
+    assert engine.unit(two, U, [0], [0.5, 0.7])[1] == 0
+    assert engine.unit(two, U, [0], [0.5, 0.8])[1] == 1
+    dt, j = engine.unit(net1({0: 1}, {}, 2.0), U, [0, 0, 0], [0.5, 0.5])[:2]
+    assert j == -1 and dt == math.inf                                                  # SPEC.md:135 Exhausted
+
+
+def test_select_tau_examples(engine):
+    U = engine.UNIT_SELECT_TAU
+    birth = ReactionNetwork.create([Species("A", 100)], [], [Reaction("b", {}, {0: 1}, 10.0)])
+    assert abs(engine.unit(birth, U, [100], [0.03])[0] - 0.3) < 1e-15
+    assert engine.unit(net1({0: 1}, {}, 1.0), U, [0, 0, 0], [0.03])[0] == math.inf
+    assert abs(engine.unit(W.birth_death(lam=5.0, c=1.0), U, [5], [0.03])[0] - 0.1) < 1e-15
+
+
+def test_tau_leap_from_counts_examples(engine):
+    U = engine.UNIT_TAU_LEAP
+    n = net1({0: 1}, {1: 1}, 1.0)
+    out = engine.unit(n, U, [10, 0, 0], [3])
+    assert list(out[:2]) == [7, 3] and out[3] == 0
+    out = engine.unit(net1({0: 1}, {}, 1.0), U, [2, 0, 0], [5])
+    assert out[3] == 1                                                                 # SPEC.md:161 Rejected
+    assert list(engine.unit(n, U, [4, 1, 0], [0])[:3]) == [4, 1, 0]
+
+
+def test_cle_step_examples(engine):
+    U = engine.UNIT_CLE_STEP
+    out = engine.unit(net1({0: 1}, {}, 1.0), U, [100, 0, 0], [0.01, 1.0])
+    assert out[0] == 98.0 and out[3] == 0
+    out = engine.unit(net1({0: 1}, {}, 1.0), U, [0.5, 0, 0], [0.01, 50.0])
+    assert out[0] == 0.0 and out[3] == 1
+
+
+@pytest.mark.parametrize("model", ["c4", "c5", "schlogl"])
+def test_units_match_oracle_on_random_states(engine, oracle, model):
+    net = {"c4": W.ras_scale(), "c5": W.random_network(), "schlogl": W.schlogl()}[model]
+    n, m = net.species_count(), net.reaction_count()
+    rng = np.random.default_rng(17)
+    for trial in range(20):
+        x = np.floor(rng.uniform(0, 10 ** rng.uniform(0, 6), n))
+        a = engine.unit(net, engine.UNIT_PROPENSITIES, x)[:m]
+        assert np.array_equal(a, oracle.propensities(net, x))
+        tau = engine.unit(net, engine.UNIT_SELECT_TAU, x, [0.03])[0]
+        assert tau == oracle.select_tau(net, x, 0.03)
+        u1, u2 = rng.uniform(1e-9, 1, 2)
+        dt, j = engine.unit(net, engine.UNIT_SSA_STEP, x, [u1, u2])[:2]
+        odt, oj = oracle.ssa_step_from_uniforms(net, x, u1, u2)
+        if oj is None:  # exhausted: a0 = 0
+            assert (dt, int(j)) == (math.inf, -1)
+        else:
+            assert (dt, int(j)) == (odt, oj)
+        counts = rng.poisson(np.minimum(a * 1e-3, 50))
+        xn = engine.unit(net, engine.UNIT_TAU_LEAP, x, counts)
+        ref = oracle.tau_leap_from_counts(net, x, counts)
+        if ref is None:
+            assert xn[n] == 1
+        else:
+            assert xn[n] == 0 and np.array_equal(xn[:n], ref)
+        z = rng.standard_normal(m)
+        xc = engine.unit(net, engine.UNIT_CLE_STEP, x, np.concatenate([[1e-3], z]))
+        rc, clamped = oracle.cle_step(net, x, 1e-3, z)
+        assert np.array_equal(xc[:n], rc) and xc[n] == clamped                         # no transcendentals: bit-exact
