@@ -411,6 +411,7 @@ struct DevBuf {
 // pool reused by asynchronous jobs (kin_sweep_submit/wait).
 struct Buffers {
   DevBuf<double> traj, mean, m2, axis, grid;
+  DevBuf<double> gstate;  // per-warp simulation state in global memory (large models)
   DevBuf<uint64_t> meta, work;
   DevBuf<int32_t> status;
   DevBuf<unsigned long long> counter;
@@ -440,7 +441,7 @@ struct Buffers {
   int n_partial = 0;
   uint64_t partial_point[2] = {0, 0}, partial_n[2] = {0, 0}, partial_base[2] = {0, 0};
   void release() {
-    traj.release(); mean.release(); m2.release(); axis.release(); grid.release();
+    traj.release(); mean.release(); m2.release(); axis.release(); grid.release(); gstate.release();
     pmean.release(); pm2.release();
     if (h_pmean) cudaFreeHost(h_pmean);
     if (h_pm2) cudaFreeHost(h_pm2);
@@ -726,6 +727,24 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
           for (int v = 0; v < d->axes[ax].n_values; ++v) xmax = std::max(xmax, d->axes[ax].values[v]);
       bool int_state = xmax < 1073741824.0;
       if (const char* v = std::getenv("KIN_INT_STATE")) int_state = int_state && std::atoi(v) != 0;
+      // Large models: when a warp's state would take more than 24 KB of shared
+      // memory (fewer than ~9 resident warps per SM), keep it in global memory
+      // instead — same [slot][lane] layout, L1/L2-cached — and let registers
+      // set the residency (KIN_GSTATE=0/1 forces the choice).
+      const size_t smem_warp = static_cast<size_t>(T->m + SD.n_axes) * 32 * sizeof(double) +
+                               static_cast<size_t>(T->n) * 32 * (int_state ? sizeof(int32_t) : sizeof(double));
+      bool gst = smem_warp > 24 * 1024;
+      if (const char* v = std::getenv("KIN_GSTATE")) gst = std::atoi(v) != 0;
+      if (gst) {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sl.device);
+        const uint64_t cap = std::min<uint64_t>((S + 31) / 32, static_cast<uint64_t>(sms) * 24);
+        // sized for double amounts: the int32-overflow re-run reuses it
+        const size_t per = static_cast<size_t>(T->m + SD.n_axes + T->n) * 32;
+        KIN_CUDA(bf.gstate.ensure(cap * per), "cudaMalloc simulation state");
+        SD.gstate = bf.gstate.p;
+        SD.gstate_warps = cap;
+      }
       KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), bf.st), "memset");
       bool used = false;
       e = cudaSuccess;

@@ -33,12 +33,12 @@ namespace {
 using stoch::kBlock;
 using stoch::TableModel;
 
-template <bool kCount, bool kPhilox, class XT>
+template <bool kCount, bool kPhilox, class XT, bool kGlobal>
 __global__ void __launch_bounds__(stoch::kBlock) stochastic_kernel(const __grid_constant__ KinTables T,
                                                                    const __grid_constant__ KinSweepDev S, KinOutDev O,
                                                                    unsigned long long* __restrict__ next,
                                                                    int* ovf_flag) {
-  stoch::stochastic_body<TableModel<XT>, kCount, kPhilox, XT>(T, S, O, next, ovf_flag);
+  stoch::stochastic_body<TableModel<XT>, kCount, kPhilox, XT, kGlobal>(T, S, O, next, ovf_flag);
 }
 
 // ---- Chemical Langevin Equation, Euler-Maruyama (stochastic.hpp:64-75) ------
@@ -236,11 +236,13 @@ size_t stochastic_smem_bytes(const KinTables& T, const KinSweepDev& S, int block
 template <class XT>
 cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                       unsigned long long* counter, int* ovf_flag, cudaStream_t stream) {
-  const size_t smem = stochastic_smem_bytes(T, S, kBlock, sizeof(XT) == 4);
+  const size_t smem = S.gstate ? 0 : stochastic_smem_bytes(T, S, kBlock, sizeof(XT) == 4);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   const bool ph = S.rng_mode == KIN_RNG_PHILOX;
-  auto kern = count ? (ph ? stochastic_kernel<true, true, XT> : stochastic_kernel<true, false, XT>)
-                    : (ph ? stochastic_kernel<false, true, XT> : stochastic_kernel<false, false, XT>);
+  auto kern = S.gstate ? (count ? (ph ? stochastic_kernel<true, true, XT, true> : stochastic_kernel<true, false, XT, true>)
+                                : (ph ? stochastic_kernel<false, true, XT, true> : stochastic_kernel<false, false, XT, true>))
+                       : (count ? (ph ? stochastic_kernel<true, true, XT, false> : stochastic_kernel<true, false, XT, false>)
+                                : (ph ? stochastic_kernel<false, true, XT, false> : stochastic_kernel<false, false, XT, false>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -250,7 +252,8 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t blocks = (S.n_local + kBlock - 1) / kBlock;
-  const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  if (S.gstate && resident > S.gstate_warps) resident = S.gstate_warps;
   const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;

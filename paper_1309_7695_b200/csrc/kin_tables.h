@@ -102,6 +102,11 @@ struct KinSweepDev {
   double t_end;
   const double* grid;   // device pointer [n_grid]
   const double* lgamma_tab;  // device pointer [KIN_LGAMMA_N]: glibc lgamma(k+1)
+  // Stochastic kernels, large models: per-simulation state in global memory
+  // (null: shared memory).  Block b owns gstate + b * (its per-warp size); the
+  // grid never exceeds gstate_warps blocks.
+  double* gstate;
+  uint64_t gstate_warps;
 };
 
 // Device outputs of one launch (local simulation index s in [0, n_local)).

@@ -147,6 +147,16 @@ def test_c5_random_network_bit_exact(engine, oracle):
     assert_bit_exact(ref, got)
 
 
+@pytest.mark.parametrize("gstate", ["0", "1"])
+def test_table_kernel_global_state_bit_exact(engine, oracle, gstate, monkeypatch):
+    """Table kernel with the state in shared or global memory: same results."""
+    monkeypatch.setenv("KIN_JIT", "0")
+    monkeypatch.setenv("KIN_GSTATE", gstate)
+    net, cfg = W.c4_config()
+    ref, got = both(engine, oracle, net, cfg, sim_range=(3000, 3256), want_work=True)
+    assert_bit_exact(ref, got, work=True)
+
+
 def test_int32_amount_overflow_retry(engine, oracle):
     """Amounts are kept as int32 on the device when they start far inside the
     range; a run that leaves it is transparently re-run with double amounts."""
@@ -169,15 +179,21 @@ def test_c4_double_and_int32_amounts_agree(engine, oracle, int_state, monkeypatc
 
 
 # ---- per-model JIT kernels (NVRTC, kin_jit.cpp): same results as the table kernel --
-@pytest.mark.parametrize("case", ["c4", "c4_double", "c4_philox", "c2", "c1_ssa", "taufixed", "overflow"])
+@pytest.mark.parametrize("case", ["c4", "c4_double", "c4_philox", "c4_gstate", "c5_gstate", "c2", "c1_ssa", "taufixed",
+                                  "overflow"])
 def test_jit_kernel_bit_exact(engine, oracle, case, monkeypatch):
     monkeypatch.setenv("KIN_JIT", "1")
     kw = dict(want_work=True)
-    if case.startswith("c4"):
+    if case == "c5_gstate":  # large model: per-simulation state in global memory (KinSweepDev::gstate)
+        net, cfg = W.c5_config(n_grid=11)
+        kw["sim_range"] = (40000, 40256)
+    elif case.startswith("c4"):
         net, cfg = W.c4_config()
         kw["sim_range"] = (12000, 12512)
         if case == "c4_double":
             monkeypatch.setenv("KIN_INT_STATE", "0")
+        if case == "c4_gstate":
+            monkeypatch.setenv("KIN_GSTATE", "1")
         if case == "c4_philox":
             monkeypatch.setenv("KIN_GROUP_LANES", "1")
             kw["rng_mode"] = abi.RNG_PHILOX
