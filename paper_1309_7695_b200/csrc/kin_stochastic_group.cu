@@ -365,11 +365,13 @@ cudaError_t launch_L(const KinTables& T, const KinSweepDev& S, const KinOutDev& 
 // SSA-heavy models (Schlogl 4x4: 4 lanes, 2.1x) and wide models (C5 128x256:
 // 16 lanes, 1.7x); mid-size models (C4 33x39) are faster one thread per
 // simulation (returns 1).
+// Measured on B200 (profiles/r1_philox_lanes.txt): lane groups pay
+// off for small models (Schlogl: 4 lanes 122 ms vs 176 ms); for large ones the
+// thread-per-simulation kernel with its state in global memory is faster
+// (C5 128x256: 1236 ms vs 2244 ms with 16 lanes).
 int stochastic_group_pick_lanes(int n_species, int n_reactions) {
   const int w = n_species > n_reactions ? n_species : n_reactions;
-  if (w <= 8) return 4;
-  if (w >= 128) return 16;
-  return 1;
+  return w <= 8 ? 4 : 1;
 }
 
 cudaError_t launch_stochastic_group(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
