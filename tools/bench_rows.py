@@ -56,6 +56,7 @@ def main():
         "lsoda_c3": (W.c3_config(side=256), 4096),
         "dopri5_c3": (W.c3_config(side=256, method=MethodKind.Ode), 4096),
         "dopri5_c4": (W.c4_config(method=MethodKind.Ode), 2048),
+        "tau_c5": (W.c5_config(), 1024),
     }
     for name, ((net, cfg), sample) in cases.items():
         if cfg.method.kind == MethodKind.Cle:
