@@ -347,7 +347,13 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
   if (kCount && O.work) O.work[s] = H.flops;
 }
 
-template <bool kCount, bool kPhilox>
+// doubles of per-warp state (the bitmask words rounded up to whole doubles)
+__host__ __device__ __forceinline__ size_t hybrid_warp_doubles(const KinTables& T, const KinSweepDev& S) {
+  const size_t words = (static_cast<size_t>(T.m) + 31) / 32;
+  return (static_cast<size_t>(kVecs) * (T.n + 1) + T.m + S.n_axes) * kBlock + (words * kBlock + 1) / 2;
+}
+
+template <bool kCount, bool kPhilox, bool kGlobal>
 __global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ KinTables T,
                                                         const __grid_constant__ KinSweepDev S, KinOutDev O,
                                                         unsigned long long* __restrict__ next) {
@@ -355,10 +361,12 @@ __global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ 
   constexpr int B = kBlock;
   const int tid = threadIdx.x, lane = tid & 31;
   const int n1 = T.n + 1;
-  double* V = smem + tid;
-  double* a = smem + static_cast<size_t>(kVecs) * n1 * B + tid;
+  // state in shared memory, or (kGlobal) in this block's region of global memory
+  double* base = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * hybrid_warp_doubles(T, S) : smem;
+  double* V = base + tid;
+  double* a = base + static_cast<size_t>(kVecs) * n1 * B + tid;
   double* av = a + static_cast<size_t>(T.m) * B;
-  uint32_t* slowm = reinterpret_cast<uint32_t*>(smem + static_cast<size_t>(kVecs * n1 + T.m + S.n_axes) * B) + tid;
+  uint32_t* slowm = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(kVecs * n1 + T.m + S.n_axes) * B) + tid;
   for (;;) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(next, 32ULL);
@@ -372,6 +380,8 @@ __global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ 
 
 }  // namespace
 
+size_t hybrid_state_doubles_per_warp(const KinTables& T, const KinSweepDev& S) { return hybrid_warp_doubles(T, S); }
+
 size_t hybrid_smem_bytes(const KinTables& T, const KinSweepDev& S) {
   const size_t words = (static_cast<size_t>(T.m) + 31) / 32;
   return (static_cast<size_t>(kVecs) * (T.n + 1) + T.m + S.n_axes) * kBlock * sizeof(double) +
@@ -381,11 +391,13 @@ size_t hybrid_smem_bytes(const KinTables& T, const KinSweepDev& S) {
 cudaError_t launch_hybrid(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                           unsigned long long* counter, cudaStream_t stream) {
   if (S.n_local == 0) return cudaSuccess;
-  const size_t smem = hybrid_smem_bytes(T, S);
+  const size_t smem = S.gstate ? 0 : hybrid_smem_bytes(T, S);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   const bool ph = S.rng_mode == KIN_RNG_PHILOX;
-  auto kern = count ? (ph ? hybrid_kernel<true, true> : hybrid_kernel<true, false>)
-                    : (ph ? hybrid_kernel<false, true> : hybrid_kernel<false, false>);
+  auto kern = S.gstate ? (count ? (ph ? hybrid_kernel<true, true, true> : hybrid_kernel<true, false, true>)
+                                : (ph ? hybrid_kernel<false, true, true> : hybrid_kernel<false, false, true>))
+                       : (count ? (ph ? hybrid_kernel<true, true, false> : hybrid_kernel<true, false, false>)
+                                : (ph ? hybrid_kernel<false, true, false> : hybrid_kernel<false, false, false>));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -395,7 +407,8 @@ cudaError_t launch_hybrid(const KinTables& T, const KinSweepDev& S, const KinOut
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t warps = (S.n_local + 31) / 32;
-  const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  if (S.gstate && resident > S.gstate_warps) resident = S.gstate_warps;
   const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;

@@ -41,6 +41,7 @@ cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev
 
 // kin_hybrid.cu: hybrid PDMP sweep (one thread per simulation, smem state).
 size_t hybrid_smem_bytes(const KinTables& T, const KinSweepDev& S);
+size_t hybrid_state_doubles_per_warp(const KinTables& T, const KinSweepDev& S);
 cudaError_t launch_hybrid(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                           unsigned long long* counter, cudaStream_t stream);
 

@@ -27,7 +27,18 @@ def decay_chain(n):
     return ReactionNetwork.create(sp, [], rx)
 
 
-@pytest.mark.parametrize("kind,n", [(MethodKind.Hybrid, 64), (MethodKind.Ode, 300), (MethodKind.Lsoda, 64)])
+def test_large_hybrid_model_runs_from_global_memory(engine, oracle):
+    """A hybrid model whose 15 vectors per simulation exceed shared memory runs
+    with its state in global memory, bit-exact with the oracle."""
+    net = decay_chain(64)
+    cfg = SweepConfig([], 40, method(MethodKind.Hybrid), 1, 1.0, uniform_grid(1.0, 5))
+    d, keep = make_sweep_desc(net, cfg, seed_mode=abi.SEED_ENSEMBLE)
+    ref = oracle.sweep(net, d, want_traj=True)
+    got = engine.sweep(net, cfg, seed_mode=abi.SEED_ENSEMBLE, want_traj=True)
+    assert np.array_equal(ref["meta"], got["meta"]) and np.array_equal(ref["traj"], got["traj"])
+
+
+@pytest.mark.parametrize("kind,n", [(MethodKind.Ode, 300), (MethodKind.Lsoda, 64)])
 def test_model_too_large_for_kernel_is_input_error(engine, kind, n):
     net = decay_chain(n)
     cfg = SweepConfig([], 4, method(kind), 1, 1.0, uniform_grid(1.0, 3))
@@ -84,13 +95,13 @@ def test_zero_runs_is_input_error(engine):
 
 
 def test_failed_submit_leaves_engine_usable():
-    """A sweep that fails to enqueue (here: state too large for the hybrid
+    """A sweep that fails to enqueue (here: state too large for the LSODA
     kernel) returns its in-flight chunks' buffers; the context keeps working."""
     from paper_1309_7695_b200 import Engine
     eng = Engine([0, 0])
     try:
         big = decay_chain(64)
-        cfg = SweepConfig([], 64, method(MethodKind.Hybrid), 1, 1.0, uniform_grid(1.0, 3))
+        cfg = SweepConfig([], 64, method(MethodKind.Lsoda), 1, 1.0, uniform_grid(1.0, 3))
         for _ in range(3):
             with pytest.raises(ValidationError, match="too large"):
                 eng.sweep(big, cfg)

@@ -50,9 +50,10 @@ def main():
     eng = Engine([0])
     rows = {}
     cases = {
-        "ssa_c1": (W.c1_config(MethodKind.Ssa, side=128), 4096),
-        "cle_c1": (W.c1_config(MethodKind.Cle, side=128), 4096),
-        "hybrid_c1": (W.c1_config(MethodKind.Hybrid, side=128), 1024),
+        # sweeps large enough to fill the GPU (>= 65,536 simulations)
+        "ssa_c1": (W.c1_config(MethodKind.Ssa, side=256), 4096),
+        "cle_c1": (W.c1_config(MethodKind.Cle, side=256), 4096),
+        "hybrid_c1": (W.c1_config(MethodKind.Hybrid, side=256), 1024),
         "lsoda_c3": (W.c3_config(side=256), 4096),
         "dopri5_c3": (W.c3_config(side=256, method=MethodKind.Ode), 4096),
         "dopri5_c4": (W.c4_config(method=MethodKind.Ode), 2048),
