@@ -708,9 +708,18 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
     bf.kernel_name = "cle_kernel";
   } else if (kind == KIN_METHOD_LSODA) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
-    if (kin::lsoda_smem_bytes(*T, SD) > 227 * 1024) {
-      set_err(err, KIN_ERR_INPUT, "model too large for the LSODA kernel (per-simulation state exceeds shared memory)");
-      return KIN_ERR_INPUT;
+    // Nordsieck array, Jacobian and LU per simulation: in global memory when a
+    // warp's state would take more than 48 KB of shared memory (KIN_LSODA_GSTATE
+    // =0/1 forces the choice)
+    bool gst = kin::lsoda_smem_bytes(*T, SD) > 48 * 1024;
+    if (const char* v = std::getenv("KIN_LSODA_GSTATE")) gst = std::atoi(v) != 0;
+    if (gst) {
+      int sms = 0;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sl.device);
+      const uint64_t cap = std::min<uint64_t>((S + 31) / 32, static_cast<uint64_t>(sms) * 24);
+      KIN_CUDA(bf.gstate.ensure(cap * kin::lsoda_state_doubles_per_warp(*T, SD)), "cudaMalloc simulation state");
+      SD.gstate = bf.gstate.p;
+      SD.gstate_warps = cap;
     }
     e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, bf.st);
     bf.kernel_name = "lsoda_kernel";

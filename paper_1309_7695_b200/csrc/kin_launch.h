@@ -29,6 +29,7 @@ cudaError_t launch_dopri5(const KinTables& T, const KinSweepDev& S, const KinOut
 // kin_lsoda.cu: LSODA-style Adams/BDF, thread per simulation, state in smem.
 // coeffs: elco [2][13][14] then tesco [2][13][3] (device).
 size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S);
+size_t lsoda_state_doubles_per_warp(const KinTables& T, const KinSweepDev& S);
 cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, const double* coeffs,
                          unsigned long long* counter, cudaStream_t stream);
 

@@ -526,7 +526,13 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   if (kCount && O.work) O.work[s] = L.flops;
 }
 
-template <bool kCount>
+// doubles of per-warp state (the pivot ints rounded up to whole doubles)
+__host__ __device__ __forceinline__ size_t lsoda_warp_doubles(const KinTables& T, const KinSweepDev& S) {
+  const size_t n = static_cast<size_t>(T.n);
+  return (18 * n + 2 * n * n + T.m + S.n_axes) * kBlock + (n * kBlock + 1) / 2;
+}
+
+template <bool kCount, bool kGlobal>
 __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ KinTables T,
                                                        const __grid_constant__ KinSweepDev S, KinOutDev O,
                                                        const double* __restrict__ co,
@@ -535,7 +541,10 @@ __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ K
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
   const int n = T.n;
   const size_t nd = static_cast<size_t>(18 * n + 2 * n * n + T.m + S.n_axes) * B;
-  int* ism = reinterpret_cast<int*>(smem + nd);
+  // state in shared memory, or (kGlobal: models too large for it) in this
+  // block's region of global memory, same layout
+  double* sbase = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * lsoda_warp_doubles(T, S) : smem;
+  int* ism = reinterpret_cast<int*>(sbase + nd);
   for (;;) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(next, 32ULL);
@@ -543,12 +552,14 @@ __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ K
     if (base >= S.n_local) break;
     const uint64_t s = base + lane;
     const unsigned mask = __ballot_sync(0xFFFFFFFFu, s < S.n_local);
-    if (s < S.n_local) lsoda_one<kCount>(T, S, O, co, s, smem, ism, B, tid, mask);
+    if (s < S.n_local) lsoda_one<kCount>(T, S, O, co, s, sbase, ism, B, tid, mask);
     __syncwarp();
   }
 }
 
 }  // namespace
+
+size_t lsoda_state_doubles_per_warp(const KinTables& T, const KinSweepDev& S) { return lsoda_warp_doubles(T, S); }
 
 size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S) {
   const int n = T.n;
@@ -559,9 +570,10 @@ size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S) {
 cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count, const double* coeffs,
                          unsigned long long* counter, cudaStream_t stream) {
   if (S.n_local == 0) return cudaSuccess;
-  const size_t smem = lsoda_smem_bytes(T, S);
+  const size_t smem = S.gstate ? 0 : lsoda_smem_bytes(T, S);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  auto kern = count ? lsoda_kernel<true> : lsoda_kernel<false>;
+  auto kern = S.gstate ? (count ? lsoda_kernel<true, true> : lsoda_kernel<false, true>)
+                       : (count ? lsoda_kernel<true, false> : lsoda_kernel<false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
@@ -571,7 +583,8 @@ cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutD
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   const uint64_t warps = (S.n_local + 31) / 32;
-  const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  if (S.gstate && resident > S.gstate_warps) resident = S.gstate_warps;
   const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;

@@ -38,7 +38,19 @@ def test_large_hybrid_model_runs_from_global_memory(engine, oracle):
     assert np.array_equal(ref["meta"], got["meta"]) and np.array_equal(ref["traj"], got["traj"])
 
 
-@pytest.mark.parametrize("kind,n", [(MethodKind.Ode, 300), (MethodKind.Lsoda, 64)])
+@pytest.mark.parametrize("kind", [MethodKind.Lsoda, MethodKind.Hybrid])
+def test_large_model_from_global_memory_lsoda_c4(engine, oracle, kind):
+    """C4 (33 species) with LSODA / hybrid: state beyond shared memory runs from
+    global memory, bit-exact with the oracle."""
+    net, cfg = W.c4_config(method=kind)
+    d, keep = make_sweep_desc(net, cfg, sim_range=(500, 564))
+    ref = oracle.sweep(net, d, want_traj=True)
+    got = engine.sweep(net, cfg, sim_range=(500, 564), want_traj=True)
+    assert np.array_equal(ref["status"], got["status"]) and np.array_equal(ref["meta"], got["meta"])
+    assert np.array_equal(ref["traj"], got["traj"])
+
+
+@pytest.mark.parametrize("kind,n", [(MethodKind.Ode, 300)])
 def test_model_too_large_for_kernel_is_input_error(engine, kind, n):
     net = decay_chain(n)
     cfg = SweepConfig([], 4, method(kind), 1, 1.0, uniform_grid(1.0, 3))
@@ -95,13 +107,14 @@ def test_zero_runs_is_input_error(engine):
 
 
 def test_failed_submit_leaves_engine_usable():
-    """A sweep that fails to enqueue (here: state too large for the LSODA
-    kernel) returns its in-flight chunks' buffers; the context keeps working."""
+    """A sweep that fails to enqueue (here: more species than the Dopri5
+    kernel's widest lane group holds) returns its in-flight chunks' buffers;
+    the context keeps working."""
     from paper_1309_7695_b200 import Engine
     eng = Engine([0, 0])
     try:
-        big = decay_chain(64)
-        cfg = SweepConfig([], 64, method(MethodKind.Lsoda), 1, 1.0, uniform_grid(1.0, 3))
+        big = decay_chain(300)
+        cfg = SweepConfig([], 64, method(MethodKind.Ode), 1, 1.0, uniform_grid(1.0, 3))
         for _ in range(3):
             with pytest.raises(ValidationError, match="too large"):
                 eng.sweep(big, cfg)
