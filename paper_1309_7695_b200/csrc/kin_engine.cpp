@@ -2,17 +2,22 @@
 // include/kin_abi.h.
 //
 // Replaces the reference's ensemble layer (proj/include/kinetics/ensemble.hpp):
-//   parameter_sweep  ensemble.hpp:126-130  -> kin_sweep_run (KIN_SEED_SWEEP)
-//   run_ensemble     ensemble.hpp:91-99    -> kin_sweep_run (KIN_SEED_ENSEMBLE)
-//   run_single       ensemble.hpp:73-76    -> kin_sweep_run (KIN_SEED_DIRECT)
+//   parameter_sweep  ensemble.hpp:126-130  -> kin_sweep_run / kin_sweep_submit (KIN_SEED_SWEEP)
+//   run_ensemble     ensemble.hpp:91-99    -> kin_ensemble_run (KIN_SEED_ENSEMBLE)
+//   run_single       ensemble.hpp:73-76    -> kin_run_single (KIN_SEED_DIRECT)
+//   merge_statistics ensemble.hpp:56-57    -> kin_stats_merge
 // and the model loader ReactionNetwork::create (model.hpp:47-53).
 //
 // The reference's worker pool (contiguous run ranges per std::thread,
-// ensemble.hpp:91-96) becomes one host thread per GPU of the context; the
-// simulation index space is cut into whole-point chunks assigned cyclically to
-// the GPUs (balances the cost gradient along the sweep axes).  Per-run results
+// ensemble.hpp:91-96) becomes the context's GPUs: the simulation index space
+// is cut into whole-point chunks assigned cyclically to the devices (balances
+// the cost gradient along the sweep axes), or — for ranges with fewer points
+// than devices — into equal run ranges whose cut points' statistics are
+// Chan-merged in ascending chunk order.  The calling thread enqueues every
+// chunk asynchronously (kernels on one of the device's two compute streams,
+// copy-out on its copy stream); kin_sweep_wait collects them.  Per-run results
 // depend only on the global simulation index, never on the device count
-// (SPEC.md:449).  No collective: each GPU copies its chunk's outputs straight
+// (SPEC.md:449).  No collective: each device copies its chunk's outputs straight
 // into the caller's host buffers at the chunk's global offset.
 #include <cuda_runtime.h>
 
