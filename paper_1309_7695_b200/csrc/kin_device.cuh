@@ -88,8 +88,13 @@ __device__ __forceinline__ uint64_t sim_seed(const KinSweepDev& S, uint64_t sim)
 }
 
 // ---- xoshiro256++ stream (rng.cpp:25-52) ------------------------------------
+// With a one-value lookahead: `nx` already holds the next output, so a draw
+// hands it out at once and the state advance (a serial chain of 64-bit integer
+// operations) overlaps the arithmetic that consumes the value.  Same outputs
+// in the same order as rng.cpp; the cost is one extra step per stream.
 struct Xoshiro {
   uint64_t s0, s1, s2, s3;
+  uint64_t nx;
 
   __device__ __forceinline__ void seed(uint64_t seed) {
     s0 = splitmix64_mix(seed);
@@ -97,9 +102,10 @@ struct Xoshiro {
     s2 = splitmix64_mix(seed + 2 * kPhi64);
     s3 = splitmix64_mix(seed + 3 * kPhi64);
     if ((s0 | s1 | s2 | s3) == 0) s0 = kPhi64;
+    nx = step();
   }
   __device__ __forceinline__ static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
-  __device__ __forceinline__ uint64_t next() {
+  __device__ __forceinline__ uint64_t step() {
     const uint64_t out = rotl(s0 + s3, 23) + s0;
     const uint64_t sh = s1 << 17;
     s2 ^= s0;
@@ -108,6 +114,11 @@ struct Xoshiro {
     s0 ^= s3;
     s2 ^= sh;
     s3 = rotl(s3, 45);
+    return out;
+  }
+  __device__ __forceinline__ uint64_t next() {
+    const uint64_t out = nx;
+    nx = step();
     return out;
   }
   // ((x >> 11) + 0.5) * 2^-53: exact in double, identical on every platform.
