@@ -32,11 +32,16 @@ constexpr int kL = 13;  // Nordsieck vectors (Adams max order 12)
 
 __device__ __constant__ double c_sm1[13] = {0.0, 0.5, 0.575, 0.55, 0.45, 0.35, 0.25, 0.2, 0.15, 0.1, 0.075, 0.05, 0.025};
 
+// kN > 0: the species count is a compile-time constant (small models: every
+// loop over species unrolls and the indexing folds); kN = 0: runtime T.n.
+template <int kN>
 struct Lsoda {
   const KinTables& T;
   const KinSweepDev& S;
   const double* co;  // elco [2][13][14] then tesco [2][13][3]
-  int B, n, m;
+  int n_rt, m;
+  static constexpr int B = kBlock;
+  __device__ __forceinline__ int N() const { return kN > 0 ? kN : n_rt; }
   double *Z, *acor, *savf, *ewt, *y, *tmp, *P, *J2, *a, *av;
   int* piv;
   uint64_t flops;
@@ -46,7 +51,7 @@ struct Lsoda {
   __device__ __forceinline__ double tesco(int meth, int q, int i) const {
     return __ldg(co + 2 * 13 * 14 + (meth * 13 + q) * 3 + i);
   }
-  __device__ __forceinline__ double& z(int j, int i) const { return Z[(j * n + i) * B]; }
+  __device__ __forceinline__ double& z(int j, int i) const { return Z[(j * N() + i) * B]; }
   __device__ __forceinline__ double& v(double* base, int i) const { return base[i * B]; }
   __device__ __forceinline__ double rate(int j) const {
     const int ax = KIN_RD_AXIS(tab_rdesc(T, j));
@@ -62,7 +67,7 @@ struct Lsoda {
       for (int t = 0; t < nt; ++t) aj = aj * combinations(yy[KIN_RD_SPECIES(d, t) * B], KIN_RD_STOICH(d, t));
       a[j * B] = aj;
     }
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < N(); ++i) {
       double s = 0.0;
       const int p1 = tab_row_ptr(T, i + 1);
       for (int p = tab_row_ptr(T, i); p < p1; ++p) {
@@ -75,7 +80,7 @@ struct Lsoda {
   }
   template <bool C>
   __device__ void jacobian(const double* yy, double* J) {
-    for (int q = 0; q < n * n; ++q) J[q * B] = 0.0;
+    for (int q = 0; q < N() * N(); ++q) J[q * B] = 0.0;
     for (int k = 0; k < m; ++k) {
       const uint64_t d = tab_rdesc(T, k);
       const int nt = KIN_RD_NTERMS(d);
@@ -94,7 +99,7 @@ struct Lsoda {
         const int c1 = tab_col_ptr(T, k + 1);
         for (int c = tab_col_ptr(T, k); c < c1; ++c) {
           const uint32_t e = tab_col(T, c);
-          double& jj = J[(KIN_NU_INDEX(e) * n + s) * B];
+          double& jj = J[(KIN_NU_INDEX(e) * N() + s) * B];
           jj = jj + static_cast<double>(KIN_NU_DELTA(e)) * dd;
         }
         if (C) flops += 4 + nt + 2 * static_cast<uint64_t>(c1 - tab_col_ptr(T, k));
@@ -103,67 +108,68 @@ struct Lsoda {
   }
   template <bool C>
   __device__ bool lu_factor() {
-    for (int k = 0; k < n; ++k) {
+    for (int k = 0; k < N(); ++k) {
       int pr = k;
-      double best = fabs(P[(k * n + k) * B]);
-      for (int i = k + 1; i < n; ++i) {
-        const double c = fabs(P[(i * n + k) * B]);
+      double best = fabs(P[(k * N() + k) * B]);
+      for (int i = k + 1; i < N(); ++i) {
+        const double c = fabs(P[(i * N() + k) * B]);
         if (c > best) { best = c; pr = i; }
       }
       piv[k * B] = pr;
       if (best == 0.0) return false;
       if (pr != k)
-        for (int j = 0; j < n; ++j) {
-          const double t0 = P[(k * n + j) * B];
-          P[(k * n + j) * B] = P[(pr * n + j) * B];
-          P[(pr * n + j) * B] = t0;
+        for (int j = 0; j < N(); ++j) {
+          const double t0 = P[(k * N() + j) * B];
+          P[(k * N() + j) * B] = P[(pr * N() + j) * B];
+          P[(pr * N() + j) * B] = t0;
         }
-      const double inv = 1.0 / P[(k * n + k) * B];
-      for (int i = k + 1; i < n; ++i) {
-        const double l = P[(i * n + k) * B] * inv;
-        P[(i * n + k) * B] = l;
-        for (int j = k + 1; j < n; ++j) P[(i * n + j) * B] = P[(i * n + j) * B] - l * P[(k * n + j) * B];
+      const double inv = 1.0 / P[(k * N() + k) * B];
+      for (int i = k + 1; i < N(); ++i) {
+        const double l = P[(i * N() + k) * B] * inv;
+        P[(i * N() + k) * B] = l;
+        for (int j = k + 1; j < N(); ++j) P[(i * N() + j) * B] = P[(i * N() + j) * B] - l * P[(k * N() + j) * B];
       }
     }
-    if (C) flops += static_cast<uint64_t>(2 * n * n * n / 3 + n);
+    if (C) flops += static_cast<uint64_t>(2 * N() * N() * N() / 3 + N());
     return true;
   }
   template <bool C>
   __device__ void lu_solve(double* b) {
-    for (int k = 0; k < n; ++k) {
+    for (int k = 0; k < N(); ++k) {
       const int pk = piv[k * B];
       if (pk != k) {
         const double t0 = b[k * B];
         b[k * B] = b[pk * B];
         b[pk * B] = t0;
       }
-      for (int i = k + 1; i < n; ++i) b[i * B] = b[i * B] - P[(i * n + k) * B] * b[k * B];
+      for (int i = k + 1; i < N(); ++i) b[i * B] = b[i * B] - P[(i * N() + k) * B] * b[k * B];
     }
-    for (int i = n - 1; i >= 0; --i) {
+    for (int i = N() - 1; i >= 0; --i) {
       double s = b[i * B];
-      for (int j = i + 1; j < n; ++j) s = s - P[(i * n + j) * B] * b[j * B];
-      b[i * B] = s / P[(i * n + i) * B];
+      for (int j = i + 1; j < N(); ++j) s = s - P[(i * N() + j) * B] * b[j * B];
+      b[i * B] = s / P[(i * N() + i) * B];
     }
-    if (C) flops += static_cast<uint64_t>(2 * n * n);
+    if (C) flops += static_cast<uint64_t>(2 * N() * N());
   }
   template <bool C>
   __device__ double wrms(const double* vv) {
     double s = 0.0;
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < N(); ++i) {
       const double q = vv[i * B] / ewt[i * B];
       s = s + q * q;
     }
-    if (C) flops += 3 * static_cast<uint64_t>(n) + 2;
-    return sqrt(s / n);
+    if (C) flops += 3 * static_cast<uint64_t>(N()) + 2;
+    return sqrt(s / N());
   }
 };
 
-template <bool kCount>
+template <bool kCount, int kN>
 __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, const double* co, uint64_t s,
-                          double* smem_base, int* ismem_base, int B, int tid, unsigned mask) {
+                          double* smem_base, int* ismem_base, int tid, unsigned mask) {
+  constexpr int B = kBlock;
   const uint64_t sim = S.sim_begin + s;
-  const int n = T.n, m = T.m, G = T.n_grid;
-  Lsoda L{T, S, co, B, n, m};
+  const int n = kN > 0 ? kN : T.n, m = T.m, G = T.n_grid;
+  Lsoda<kN> L{T, S, co, T.n, m};
   double* p = smem_base + tid;
   L.Z = p;
   p += kL * n * B;
@@ -225,7 +231,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
       L.z(0, i) = L.y[i * B];
       L.ewt[i * B] = rtol * fabs(L.y[i * B]) + atol;
     }
-    L.rhs<kCount>(L.y, L.savf);
+    L.template rhs<kCount>(L.y, L.savf);
     double h;
     if (S.h_init > 0.0) {
       h = S.h_init;
@@ -273,16 +279,16 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) - L.z(j + 1, i);
     };
     auto form_p = [&](const double* yy) {
-      L.jacobian<kCount>(yy, L.P);
+      L.template jacobian<kCount>(yy, L.P);
       const double hl0 = h * el0;
       for (int q = 0; q < n * n; ++q) L.P[q * B] = -hl0 * L.P[q * B];
       for (int i = 0; i < n; ++i) L.P[(i * n + i) * B] = L.P[(i * n + i) * B] + 1.0;
       hl0_p = hl0;
-      have_p = L.lu_factor<kCount>();
+      have_p = L.template lu_factor<kCount>();
       return have_p;
     };
     auto jac_norm = [&](const double* yy) {
-      L.jacobian<kCount>(yy, L.J2);
+      L.template jacobian<kCount>(yy, L.J2);
       double nm = 0.0;
       for (int i = 0; i < n; ++i) {
         double sr = 0.0;
@@ -315,7 +321,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
         bool conv = false;
         for (;;) {
           for (int i = 0; i < n; ++i) L.y[i * B] = L.z(0, i);
-          L.rhs<kCount>(L.y, L.savf);
+          L.template rhs<kCount>(L.y, L.savf);
           if (meth == 1 && ipup) {
             if (!form_p(L.y)) { status = KIN_SIM_NONFINITE; break; }
             ipup = false;
@@ -330,8 +336,8 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             double del;
             if (meth == 1) {
               for (int i = 0; i < n; ++i) L.tmp[i * B] = h * L.savf[i * B] - (L.z(1, i) + L.acor[i * B]);
-              L.lu_solve<kCount>(L.tmp);
-              del = L.wrms<kCount>(L.tmp);
+              L.template lu_solve<kCount>(L.tmp);
+              del = L.template wrms<kCount>(L.tmp);
               for (int i = 0; i < n; ++i) {
                 L.acor[i * B] = L.acor[i * B] + L.tmp[i * B];
                 L.y[i * B] = L.z(0, i) + el0 * L.acor[i * B];
@@ -339,7 +345,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             } else {
               for (int i = 0; i < n; ++i) L.tmp[i * B] = h * L.savf[i * B] - L.z(1, i);
               for (int i = 0; i < n; ++i) L.acor[i * B] = L.tmp[i * B] - L.acor[i * B];
-              del = L.wrms<kCount>(L.acor);
+              del = L.template wrms<kCount>(L.acor);
               for (int i = 0; i < n; ++i) {
                 L.y[i * B] = L.z(0, i) + el0 * L.tmp[i * B];
                 L.acor[i * B] = L.tmp[i * B];
@@ -354,7 +360,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             ++mm;
             if (mm == 3 || (mm >= 2 && del > 2.0 * delp)) break;
             delp = del;
-            L.rhs<kCount>(L.y, L.savf);
+            L.template rhs<kCount>(L.y, L.savf);
           }
           if (status != 0 || conv) break;
           if (meth == 1 && !jcur) { ipup = true; continue; }
@@ -370,7 +376,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           continue;
         }
         jcur = false;
-        dsm = L.wrms<kCount>(L.acor) / L.tesco(meth, nq, 1);
+        dsm = L.template wrms<kCount>(L.acor) / L.tesco(meth, nq, 1);
         if (dsm > 1.0) {
           unpredict();
           ++n_rej;
@@ -378,7 +384,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           if (kflag <= -3) {
             for (int i = 0; i < n; ++i) L.y[i * B] = L.z(0, i);
             h = h * 0.1;
-            L.rhs<kCount>(L.y, L.savf);
+            L.template rhs<kCount>(L.y, L.savf);
             for (int i = 0; i < n; ++i) L.z(1, i) = h * L.savf[i * B];
             set_order(meth, 1);
             ialth = 5;
@@ -388,7 +394,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           const double rhsm = 1.0 / (1.2 * pm_pow(dsm, 1.0 / (nq + 1)) + 1.2e-6);
           double rhdn = 0.0;
           if (nq > 1) {
-            const double ddn = L.wrms<kCount>(&L.z(nq, 0)) / L.tesco(meth, nq, 0);
+            const double ddn = L.template wrms<kCount>(&L.z(nq, 0)) / L.tesco(meth, nq, 0);
             rhdn = 1.0 / (1.3 * pm_pow(ddn, 1.0 / nq) + 1.3e-6);
           }
           double rh;
@@ -436,12 +442,12 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
         double rhup = 0.0;
         if (nq < maxord()) {
           for (int i = 0; i < n; ++i) L.tmp[i * B] = L.acor[i * B] - L.z(kL - 1, i);
-          const double dup = L.wrms<kCount>(L.tmp) / L.tesco(meth, nq, 2);
+          const double dup = L.template wrms<kCount>(L.tmp) / L.tesco(meth, nq, 2);
           rhup = 1.0 / (1.4 * pm_pow(dup, 1.0 / (nq + 2)) + 1.4e-6);
         }
         double rhdn = 0.0;
         if (nq > 1) {
-          const double ddn = L.wrms<kCount>(&L.z(nq, 0)) / L.tesco(meth, nq, 0);
+          const double ddn = L.template wrms<kCount>(&L.z(nq, 0)) / L.tesco(meth, nq, 0);
           rhdn = 1.0 / (1.3 * pm_pow(ddn, 1.0 / nq) + 1.3e-6);
         }
         double pdnorm = -1.0;
@@ -532,13 +538,14 @@ __host__ __device__ __forceinline__ size_t lsoda_warp_doubles(const KinTables& T
   return (18 * n + 2 * n * n + T.m + S.n_axes) * kBlock + (n * kBlock + 1) / 2;
 }
 
-template <bool kCount, bool kGlobal>
+template <bool kCount, bool kGlobal, int kN>
 __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ KinTables T,
                                                        const __grid_constant__ KinSweepDev S, KinOutDev O,
                                                        const double* __restrict__ co,
                                                        unsigned long long* __restrict__ next) {
   extern __shared__ double smem[];
-  const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+  constexpr int B = kBlock;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int n = T.n;
   const size_t nd = static_cast<size_t>(18 * n + 2 * n * n + T.m + S.n_axes) * B;
   // state in shared memory, or (kGlobal: models too large for it) in this
@@ -552,7 +559,7 @@ __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ K
     if (base >= S.n_local) break;
     const uint64_t s = base + lane;
     const unsigned mask = __ballot_sync(0xFFFFFFFFu, s < S.n_local);
-    if (s < S.n_local) lsoda_one<kCount>(T, S, O, co, s, sbase, ism, B, tid, mask);
+    if (s < S.n_local) lsoda_one<kCount, kN>(T, S, O, co, s, sbase, ism, tid, mask);
     __syncwarp();
   }
 }
@@ -572,8 +579,21 @@ cudaError_t launch_lsoda(const KinTables& T, const KinSweepDev& S, const KinOutD
   if (S.n_local == 0) return cudaSuccess;
   const size_t smem = S.gstate ? 0 : lsoda_smem_bytes(T, S);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  auto kern = S.gstate ? (count ? lsoda_kernel<true, true> : lsoda_kernel<false, true>)
-                       : (count ? lsoda_kernel<true, false> : lsoda_kernel<false, false>);
+  // small models: the kernel specialised on the species count (kN = T.n)
+  using KernT = void (*)(const KinTables, const KinSweepDev, KinOutDev, const double*, unsigned long long*);
+  KernT kern = nullptr;
+  if (S.gstate) {
+    kern = count ? lsoda_kernel<true, true, 0> : lsoda_kernel<false, true, 0>;
+  } else {
+    switch (T.n) {
+#define KIN_LSODA_CASE(k) \
+  case k: kern = count ? lsoda_kernel<true, false, k> : lsoda_kernel<false, false, k>; break;
+      KIN_LSODA_CASE(1) KIN_LSODA_CASE(2) KIN_LSODA_CASE(3) KIN_LSODA_CASE(4)
+      KIN_LSODA_CASE(5) KIN_LSODA_CASE(6) KIN_LSODA_CASE(7) KIN_LSODA_CASE(8)
+#undef KIN_LSODA_CASE
+      default: kern = count ? lsoda_kernel<true, false, 0> : lsoda_kernel<false, false, 0>;
+    }
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;
