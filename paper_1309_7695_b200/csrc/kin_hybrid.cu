@@ -47,18 +47,22 @@ constexpr int kVecs = 15;
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
 
-template <bool kCount>
+// kN > 0: species count fixed at compile time (small models: loops over the
+// N+1 components unroll); kN = 0: runtime T.n.
+template <bool kCount, int kN>
 struct Hybrid {
   const KinTables& T;
   const KinSweepDev& S;
   TableModel<double, kBlock> sm;  // propensities over y (x = y[0..n-1])
-  int n, m, n1;
-  double* V;         // kVecs vectors of n1, [vec][comp][thread]
+  int n_rt, m, n1_rt;
+  __device__ __forceinline__ int N() const { return kN > 0 ? kN : n_rt; }
+  __device__ __forceinline__ int N1() const { return kN > 0 ? kN + 1 : n1_rt; }
+  double* V;         // kVecs vectors of N1(), [vec][comp][thread]
   uint32_t* slowm;   // [word][thread]
   uint64_t flops = 0;
 
-  __device__ __forceinline__ double& v(int vec, int i) const { return V[(static_cast<size_t>(vec) * n1 + i) * kBlock]; }
-  __device__ __forceinline__ double* vp(int vec) const { return V + static_cast<size_t>(vec) * n1 * kBlock; }
+  __device__ __forceinline__ double& v(int vec, int i) const { return V[(static_cast<size_t>(vec) * N1() + i) * kBlock]; }
+  __device__ __forceinline__ double* vp(int vec) const { return V + static_cast<size_t>(vec) * N1() * kBlock; }
   __device__ __forceinline__ bool slow(int j) const { return (slowm[(j >> 5) * kBlock] >> (j & 31)) & 1u; }
 
   // augmented RHS: f = (sum_fast nu a (row order), sum_slow a) at state `yv`
@@ -66,7 +70,7 @@ struct Hybrid {
     TableModel<double, kBlock> st{T, vp(yv), sm.a, sm.av};
     for (int j = 0; j < m; ++j) sm.a[j * kBlock] = st.prop(j);
     if (kCount) flops += static_cast<uint64_t>(T.fprop);
-    for (int i = 0; i < n; ++i) {
+    for (int i = 0; i < N(); ++i) {
       double acc = 0.0;
       const int p1 = tab_row_ptr(T, i + 1), p0 = tab_row_ptr(T, i);
       for (int p = p0; p < p1; ++p) {
@@ -80,7 +84,7 @@ struct Hybrid {
     double g = 0.0;
     for (int j = 0; j < m; ++j)
       if (slow(j)) g = g + sm.a[j * kBlock];
-    v(fv, n) = g;
+    v(fv, N()) = g;
     if (kCount) flops += static_cast<uint64_t>(m);
   }
 
@@ -92,13 +96,13 @@ struct Hybrid {
 
 enum { Y = 0, K1, K2, K3, K4, K5, K6, K7, YN, YS, R1, R2, R3, R4, R5 };
 
-template <bool kCount, bool kPhilox>
+template <bool kCount, bool kPhilox, int kN>
 __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, uint64_t s,
                                     double* V, double* a, double* av, uint32_t* slowm) {
   constexpr int B = kBlock;
   const uint64_t sim = S.sim_begin + s;
-  const int n = T.n, m = T.m, G = T.n_grid, n1 = n + 1;
-  Hybrid<kCount> H{T, S, TableModel<double, kBlock>{T, V, a, av}, n, m, n1, V, slowm};
+  const int n = kN > 0 ? kN : T.n, m = T.m, G = T.n_grid, n1 = n + 1;
+  Hybrid<kCount, kN> H{T, S, TableModel<double, kBlock>{T, V, a, av}, T.n, m, T.n + 1, V, slowm};
   stoch::init_state<double, kBlock>(T, S, sim, n, V, av);  // y[0..n-1] = x0 (vector Y is the first)
   const uint64_t seed = sim_seed(S, sim);
   Xoshiro rng;
@@ -353,7 +357,7 @@ __host__ __device__ __forceinline__ size_t hybrid_warp_doubles(const KinTables& 
   return (static_cast<size_t>(kVecs) * (T.n + 1) + T.m + S.n_axes) * kBlock + (words * kBlock + 1) / 2;
 }
 
-template <bool kCount, bool kPhilox, bool kGlobal>
+template <bool kCount, bool kPhilox, bool kGlobal, int kN>
 __global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ KinTables T,
                                                         const __grid_constant__ KinSweepDev S, KinOutDev O,
                                                         unsigned long long* __restrict__ next) {
@@ -373,7 +377,7 @@ __global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ 
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     if (base >= S.n_local) break;
     const uint64_t s = base + lane;
-    if (s < S.n_local) simulate_hybrid_one<kCount, kPhilox>(T, S, O, s, V, a, av, slowm);
+    if (s < S.n_local) simulate_hybrid_one<kCount, kPhilox, kN>(T, S, O, s, V, a, av, slowm);
     __syncwarp();
   }
 }
@@ -394,10 +398,23 @@ cudaError_t launch_hybrid(const KinTables& T, const KinSweepDev& S, const KinOut
   const size_t smem = S.gstate ? 0 : hybrid_smem_bytes(T, S);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   const bool ph = S.rng_mode == KIN_RNG_PHILOX;
-  auto kern = S.gstate ? (count ? (ph ? hybrid_kernel<true, true, true> : hybrid_kernel<true, false, true>)
-                                : (ph ? hybrid_kernel<false, true, true> : hybrid_kernel<false, false, true>))
-                       : (count ? (ph ? hybrid_kernel<true, true, false> : hybrid_kernel<true, false, false>)
-                                : (ph ? hybrid_kernel<false, true, false> : hybrid_kernel<false, false, false>));
+  using KernT = void (*)(const KinTables, const KinSweepDev, KinOutDev, unsigned long long*);
+  KernT kern = nullptr;
+  if (S.gstate) {
+    kern = count ? (ph ? hybrid_kernel<true, true, true, 0> : hybrid_kernel<true, false, true, 0>)
+                 : (ph ? hybrid_kernel<false, true, true, 0> : hybrid_kernel<false, false, true, 0>);
+  } else if (!count && T.n <= 8) {  // small models: specialised on the species count
+    switch (T.n) {
+#define KIN_HYB_CASE(k) \
+  case k: kern = ph ? hybrid_kernel<false, true, false, k> : hybrid_kernel<false, false, false, k>; break;
+      KIN_HYB_CASE(1) KIN_HYB_CASE(2) KIN_HYB_CASE(3) KIN_HYB_CASE(4)
+      KIN_HYB_CASE(5) KIN_HYB_CASE(6) KIN_HYB_CASE(7) KIN_HYB_CASE(8)
+#undef KIN_HYB_CASE
+    }
+  } else {
+    kern = count ? (ph ? hybrid_kernel<true, true, false, 0> : hybrid_kernel<true, false, false, 0>)
+                 : (ph ? hybrid_kernel<false, true, false, 0> : hybrid_kernel<false, false, false, 0>);
+  }
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0, per_sm = 0;

@@ -36,6 +36,9 @@ def test_hybrid_bit_exact_vs_oracle(engine, oracle, rng_mode):
     assert np.array_equal(ref["work"], got["work"])
     diff = np.argwhere(ref["traj"] != got["traj"])
     assert diff.size == 0, f"{len(diff)} samples differ, first {diff[:3].tolist()}"
+    # without work counting the launch takes the kernel specialised on N (C1: 4)
+    fast = engine.sweep(net, cfg, rng_mode=rng_mode, want_traj=True)
+    assert np.array_equal(fast["traj"], ref["traj"]) and np.array_equal(fast["meta"], ref["meta"])
 
 
 def test_hybrid_swept_thresholds_and_order3(engine, oracle):
