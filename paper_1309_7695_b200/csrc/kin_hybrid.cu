@@ -1,436 +1,51 @@
-// kin_hybrid.cu — hybrid PDMP sweep kernel (hybrid.hpp:14-62).
-//
-// One thread per simulation, persistent warps.  Mirrors oracle/kin_oracle.cpp
-// simulate_hybrid / hybrid_segment operation for operation (compiled with
-// -fmad=false; step control and the jump threshold E = -ln u use the portable
-// log/pow of kin_pmath.cuh), so trajectories are bit-identical to the oracle's:
-//   per segment: partition_reactions (slow iff a_j < theta_a or a reactant
-//   amount < theta_x), horizon min(t + repartition_interval, t_end), E = -ln u;
-//   Dormand-Prince 5(4) on (x, G) with dx/dt = sum_fast nu_j a_j (row order)
-//   and dG/dt = sum_slow a_j; where G reaches E, bisection on the dense output
-//   to 1e-10 relative in t; the firing slow reaction by the ssa_select rule
-//   over the slow set; nu_j added to the continuous state, clamped at 0.
-// Per-simulation state: 15 vectors of N+1 doubles (y, k1..k7, yn, ys, r1..r5),
-// a[M], the sweep coordinates and a slow-set bitmask, in shared memory with the
-// [slot][thread] layout (conflict-free; lanes touch consecutive words).
-#include "kin_launch.h"
-#include "kin_pmath.cuh"
-#include "kin_stochastic_impl.cuh"
+// kin_hybrid.cu — hybrid PDMP sweep: launch dispatch and the generic kernel
+// variants.  Kernel: kin_hybrid_impl.cuh; the variants specialised on the
+// species count are instantiated in kin_hybrid_n*.cu (parallel compilation).
+#include "kin_hybrid_impl.cuh"
 
 namespace kin {
+namespace hyb {
+#define KIN_HYB_EXTERN(k) extern template KIN_HYB_SIG(false, true, false, k); extern template KIN_HYB_SIG(false, false, false, k);
+KIN_HYB_EXTERN(1) KIN_HYB_EXTERN(2) KIN_HYB_EXTERN(3) KIN_HYB_EXTERN(4)
+KIN_HYB_EXTERN(5) KIN_HYB_EXTERN(6) KIN_HYB_EXTERN(7) KIN_HYB_EXTERN(8)
+#undef KIN_HYB_EXTERN
+}  // namespace hyb
 
-namespace {
-
-using pmath::pm_log;
-using pmath::pm_pow;
-constexpr int kBlock = 32;  // one warp per block: the per-thread state is large
-using stoch::TableModel;
-
-// Dormand-Prince 5(4) tableau (the oracle's dp:: constants)
-constexpr double c_a21 = 1.0 / 5.0;
-constexpr double c_a31 = 3.0 / 40.0, c_a32 = 9.0 / 40.0;
-constexpr double c_a41 = 44.0 / 45.0, c_a42 = -56.0 / 15.0, c_a43 = 32.0 / 9.0;
-constexpr double c_a51 = 19372.0 / 6561.0, c_a52 = -25360.0 / 2187.0, c_a53 = 64448.0 / 6561.0, c_a54 = -212.0 / 729.0;
-constexpr double c_a61 = 9017.0 / 3168.0, c_a62 = -355.0 / 33.0, c_a63 = 46732.0 / 5247.0, c_a64 = 49.0 / 176.0,
-                 c_a65 = -5103.0 / 18656.0;
-constexpr double c_a71 = 35.0 / 384.0, c_a73 = 500.0 / 1113.0, c_a74 = 125.0 / 192.0, c_a75 = -2187.0 / 6784.0,
-                 c_a76 = 11.0 / 84.0;
-constexpr double c_e1 = 71.0 / 57600.0, c_e3 = -71.0 / 16695.0, c_e4 = 71.0 / 1920.0, c_e5 = -17253.0 / 339200.0,
-                 c_e6 = 22.0 / 525.0, c_e7 = -1.0 / 40.0;
-constexpr double c_d1 = -12715105075.0 / 11282082432.0, c_d3 = 87487479700.0 / 32700410799.0,
-                 c_d4 = -10690763975.0 / 1880347072.0, c_d5 = 701980252875.0 / 199316789632.0,
-                 c_d6 = -1453857185.0 / 822651844.0, c_d7 = 69997945.0 / 29380423.0;
-constexpr double kSafe = 0.9, kFacMinInv = 5.0, kFacMaxInv = 0.1;
-constexpr double kBeta = 0.04, kExpo1 = 0.2 - kBeta * 0.75;
-constexpr int kVecs = 15;
-
-__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
-__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
-
-// kN > 0: species count fixed at compile time (small models: loops over the
-// N+1 components unroll); kN = 0: runtime T.n.
-template <bool kCount, int kN>
-struct Hybrid {
-  const KinTables& T;
-  const KinSweepDev& S;
-  TableModel<double, kBlock> sm;  // propensities over y (x = y[0..n-1])
-  int n_rt, m, n1_rt;
-  __device__ __forceinline__ int N() const { return kN > 0 ? kN : n_rt; }
-  __device__ __forceinline__ int N1() const { return kN > 0 ? kN + 1 : n1_rt; }
-  double* V;         // kVecs vectors of N1(), [vec][comp][thread]
-  uint32_t* slowm;   // [word][thread]
-  uint64_t flops = 0;
-
-  __device__ __forceinline__ double& v(int vec, int i) const { return V[(static_cast<size_t>(vec) * N1() + i) * kBlock]; }
-  __device__ __forceinline__ double* vp(int vec) const { return V + static_cast<size_t>(vec) * N1() * kBlock; }
-  __device__ __forceinline__ bool slow(int j) const { return (slowm[(j >> 5) * kBlock] >> (j & 31)) & 1u; }
-
-  // augmented RHS: f = (sum_fast nu a (row order), sum_slow a) at state `yv`
-  __device__ void rhs(int yv, int fv) {
-    TableModel<double, kBlock> st{T, vp(yv), sm.a, sm.av};
-    for (int j = 0; j < m; ++j) sm.a[j * kBlock] = st.prop(j);
-    if (kCount) flops += static_cast<uint64_t>(T.fprop);
-    for (int i = 0; i < N(); ++i) {
-      double acc = 0.0;
-      const int p1 = tab_row_ptr(T, i + 1), p0 = tab_row_ptr(T, i);
-      for (int p = p0; p < p1; ++p) {
-        const uint32_t e = tab_row(T, p);
-        const int j = KIN_NU_INDEX(e);
-        if (!slow(j)) acc = acc + static_cast<double>(KIN_NU_DELTA(e)) * sm.a[j * kBlock];
-      }
-      v(fv, i) = acc;
-      if (kCount) flops += 2 * static_cast<uint64_t>(p1 - p0);
-    }
-    double g = 0.0;
-    for (int j = 0; j < m; ++j)
-      if (slow(j)) g = g + sm.a[j * kBlock];
-    v(fv, N()) = g;
-    if (kCount) flops += static_cast<uint64_t>(m);
-  }
-
-  __device__ __forceinline__ double dense(double th, int i) const {
-    const double th1 = 1.0 - th;
-    return v(10, i) + th * (v(11, i) + th1 * (v(12, i) + th * (v(13, i) + th1 * v(14, i))));
-  }
-};
-
-enum { Y = 0, K1, K2, K3, K4, K5, K6, K7, YN, YS, R1, R2, R3, R4, R5 };
-
-template <bool kCount, bool kPhilox, int kN>
-__device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, uint64_t s,
-                                    double* V, double* a, double* av, uint32_t* slowm) {
-  constexpr int B = kBlock;
-  const uint64_t sim = S.sim_begin + s;
-  const int n = kN > 0 ? kN : T.n, m = T.m, G = T.n_grid, n1 = n + 1;
-  Hybrid<kCount, kN> H{T, S, TableModel<double, kBlock>{T, V, a, av}, T.n, m, T.n + 1, V, slowm};
-  stoch::init_state<double, kBlock>(T, S, sim, n, V, av);  // y[0..n-1] = x0 (vector Y is the first)
-  const uint64_t seed = sim_seed(S, sim);
-  Xoshiro rng;
-  if (!kPhilox) rng.seed(seed);
-  const double t_end = S.t_end, rtol = S.rel_tol, atol = S.abs_tol;
-  const double hmax = S.h_max > 0.0 ? S.h_max : KIN_INF;
-  const double rep = S.hyb_rep > 0.0 ? S.hyb_rep : t_end / 100.0;
-  uint64_t meta[6] = {0, 0, 0, 0, 0, 0};
-  bool floored = false;
-  int status = 0;
-  double t = 0.0;
-  int gi = 0;
-  auto emit_state = [&]() {
-    double* o = O.traj + (static_cast<size_t>(s) * G + gi) * n;
-    for (int i = 0; i < n; ++i) o[i] = H.v(Y, i);
-    ++gi;
-  };
-  while (gi < G && tab_grid(T, S, gi) <= t) emit_state();
-  uint64_t attempts = 0, seg = 0;
-  while (t < t_end) {
-    // partition_reactions at the current state
-    {
-      TableModel<double, kBlock> st{T, V, a, av};
-      const int words = (m + 31) >> 5;
-      for (int w = 0; w < words; ++w) slowm[w * B] = 0u;
-      for (int j = 0; j < m; ++j) {
-        const double aj = st.prop(j);
-        a[j * B] = aj;
-        bool sl = aj < S.hyb_theta_a;
-        const uint64_t d = tab_rdesc(T, j);
-        const int nt = KIN_RD_NTERMS(d);
-        for (int q = 0; q < nt; ++q) sl |= H.v(Y, KIN_RD_SPECIES(d, q)) < S.hyb_theta_x;
-        if (sl) slowm[(j >> 5) * B] |= 1u << (j & 31);
-      }
-      if (kCount) H.flops += static_cast<uint64_t>(T.fprop);
-    }
-    const double t_hor = t + rep < t_end ? t + rep : t_end;
-    PhiloxSite site(seed, seg, 0);
-    const double u = kPhilox ? site.uniform() : rng.uniform();
-    const double E = -pm_log(u);
-    if (kCount) H.flops += 3;
-    // ---- hybrid_segment ---------------------------------------------------
-    bool jumped = false;
-    {
-      H.v(Y, n) = 0.0;
-      H.rhs(Y, K1);
-      double h;
-      if (S.h_init > 0.0) {
-        h = S.h_init;
-      } else {
-        double dnf = 0.0, dny = 0.0;
-        for (int i = 0; i < n1; ++i) {
-          const double sk = atol + rtol * fabs(H.v(Y, i));
-          const double qf = H.v(K1, i) / sk, qy = H.v(Y, i) / sk;
-          dnf = dnf + qf * qf;
-          dny = dny + qy * qy;
-        }
-        h = (dnf <= 1e-10 || dny <= 1e-10) ? 1.0e-6 : sqrt(dny / dnf) * 0.01;
-        if (h > hmax) h = hmax;
-        for (int i = 0; i < n1; ++i) H.v(YS, i) = H.v(Y, i) + h * H.v(K1, i);
-        H.rhs(YS, K2);
-        double der2 = 0.0;
-        for (int i = 0; i < n1; ++i) {
-          const double sk = atol + rtol * fabs(H.v(Y, i));
-          const double q = (H.v(K2, i) - H.v(K1, i)) / sk;
-          der2 = der2 + q * q;
-        }
-        der2 = sqrt(der2) / h;
-        const double der12 = dmax(der2, sqrt(dnf));
-        const double h1 = der12 <= 1e-15 ? dmax(1.0e-6, h * 1.0e-3) : pm_pow(0.01 / der12, 0.2);
-        h = dmin(100.0 * h, h1);
-        if (h > hmax) h = hmax;
-        if (kCount) H.flops += 15 * static_cast<uint64_t>(n1) + 12;
-      }
-      double facold = 1.0e-4;
-      bool last_rejected = false;
-      while (t < t_hor) {
-        if (attempts++ >= S.max_steps) { status = KIN_SIM_BUDGET; break; }
-        double hh = h < hmax ? h : hmax;
-        bool hit = false;
-        if (t + hh >= t_hor) { hh = t_hor - t; hit = true; }
-        if (!(hh > 0.0) || t + hh == t) { status = KIN_SIM_STEP_UNDERFLOW; break; }
-        for (int i = 0; i < n1; ++i) H.v(YS, i) = H.v(Y, i) + hh * (c_a21 * H.v(K1, i));
-        H.rhs(YS, K2);
-        for (int i = 0; i < n1; ++i) H.v(YS, i) = H.v(Y, i) + hh * (c_a31 * H.v(K1, i) + c_a32 * H.v(K2, i));
-        H.rhs(YS, K3);
-        for (int i = 0; i < n1; ++i)
-          H.v(YS, i) = H.v(Y, i) + hh * (c_a41 * H.v(K1, i) + c_a42 * H.v(K2, i) + c_a43 * H.v(K3, i));
-        H.rhs(YS, K4);
-        for (int i = 0; i < n1; ++i)
-          H.v(YS, i) =
-              H.v(Y, i) + hh * (c_a51 * H.v(K1, i) + c_a52 * H.v(K2, i) + c_a53 * H.v(K3, i) + c_a54 * H.v(K4, i));
-        H.rhs(YS, K5);
-        for (int i = 0; i < n1; ++i)
-          H.v(YS, i) = H.v(Y, i) + hh * (c_a61 * H.v(K1, i) + c_a62 * H.v(K2, i) + c_a63 * H.v(K3, i) +
-                                         c_a64 * H.v(K4, i) + c_a65 * H.v(K5, i));
-        H.rhs(YS, K6);
-        for (int i = 0; i < n1; ++i)
-          H.v(YN, i) = H.v(Y, i) + hh * (c_a71 * H.v(K1, i) + c_a73 * H.v(K3, i) + c_a74 * H.v(K4, i) +
-                                         c_a75 * H.v(K5, i) + c_a76 * H.v(K6, i));
-        H.rhs(YN, K7);
-        double sum = 0.0;
-        bool finite = true;
-        for (int i = 0; i < n1; ++i) {
-          const double e = hh * (c_e1 * H.v(K1, i) + c_e3 * H.v(K3, i) + c_e4 * H.v(K4, i) + c_e5 * H.v(K5, i) +
-                                 c_e6 * H.v(K6, i) + c_e7 * H.v(K7, i));
-          const double sk = atol + rtol * dmax(fabs(H.v(Y, i)), fabs(H.v(YN, i)));
-          const double q = e / sk;
-          sum = sum + q * q;
-          finite &= isfinite(H.v(YN, i));
-        }
-        const double err = sqrt(sum / static_cast<double>(n1));
-        if (kCount) H.flops += 63 * static_cast<uint64_t>(n1) + 4;
-        if (!finite || !isfinite(err)) { status = KIN_SIM_NONFINITE; break; }
-        const double fac11 = pm_pow(err, kExpo1);
-        if (err > 1.0) {
-          h = hh / dmin(kFacMinInv, fac11 / kSafe);
-          last_rejected = true;
-          ++meta[1];
-          if (kCount) H.flops += 3;
-          continue;
-        }
-        double fac = fac11 / pm_pow(facold, kBeta);
-        fac = dmax(kFacMaxInv, dmin(kFacMinInv, fac / kSafe));
-        double hnew = hh / fac;
-        facold = dmax(err, 1.0e-4);
-        for (int i = 0; i < n1; ++i) {
-          H.v(R1, i) = H.v(Y, i);
-          const double yd = H.v(YN, i) - H.v(Y, i);
-          H.v(R2, i) = yd;
-          const double bs = hh * H.v(K1, i) - yd;
-          H.v(R3, i) = bs;
-          H.v(R4, i) = yd - hh * H.v(K7, i) - bs;
-          H.v(R5, i) = hh * (c_d1 * H.v(K1, i) + c_d3 * H.v(K3, i) + c_d4 * H.v(K4, i) + c_d5 * H.v(K5, i) +
-                             c_d6 * H.v(K6, i) + c_d7 * H.v(K7, i));
-        }
-        if (last_rejected && hnew > hh) hnew = hh;
-        last_rejected = false;
-        h = hnew;
-        ++meta[0];
-        if (kCount) H.flops += 18 * static_cast<uint64_t>(n1) + 8;
-        const double tprev = t;
-        const double tnew = hit ? t_hor : t + hh;
-        if (H.v(YN, n) >= E) {
-          double lo = 0.0, hi = 1.0;
-          for (int it = 0; it < 200; ++it) {
-            const double tl = tprev + lo * hh, th = tprev + hi * hh;
-            if (!(th - tl > 1e-10 * fabs(th))) break;
-            const double mid = 0.5 * (lo + hi);
-            if (H.dense(mid, n) >= E) hi = mid; else lo = mid;
-            if (kCount) H.flops += 12;
-          }
-          const double ts = hi == 1.0 ? tnew : tprev + hi * hh;
-          while (gi < G && tab_grid(T, S, gi) < ts) {
-            double* o = O.traj + (static_cast<size_t>(s) * G + gi) * n;
-            const double th = (tab_grid(T, S, gi) - tprev) / hh;
-            for (int i = 0; i < n; ++i) {
-              double vv = H.dense(th, i);
-              if (vv < 0.0) { vv = 0.0; floored = true; }
-              o[i] = vv;
-            }
-            if (kCount) H.flops += 8 * static_cast<uint64_t>(n) + 3;
-            ++gi;
-          }
-          for (int i = 0; i < n; ++i) {
-            double vv = hi == 1.0 ? H.v(YN, i) : H.dense(hi, i);
-            if (vv < 0.0) { vv = 0.0; floored = true; }
-            H.v(Y, i) = vv;
-          }
-          t = ts;
-          jumped = true;
-          break;
-        }
-        t = tnew;
-        for (int i = 0; i < n1; ++i) {
-          H.v(Y, i) = H.v(YN, i);
-          H.v(K1, i) = H.v(K7, i);
-        }
-        while (gi < G && tab_grid(T, S, gi) <= t) {
-          double* o = O.traj + (static_cast<size_t>(s) * G + gi) * n;
-          if (tab_grid(T, S, gi) == t) {
-            for (int i = 0; i < n; ++i) {
-              double vv = H.v(Y, i);
-              if (vv < 0.0) { vv = 0.0; floored = true; }
-              o[i] = vv;
-            }
-          } else {
-            const double th = (tab_grid(T, S, gi) - tprev) / hh;
-            for (int i = 0; i < n; ++i) {
-              double vv = H.dense(th, i);
-              if (vv < 0.0) { vv = 0.0; floored = true; }
-              o[i] = vv;
-            }
-            if (kCount) H.flops += 8 * static_cast<uint64_t>(n) + 3;
-          }
-          ++gi;
-        }
-        bool lifted = false;
-        for (int i = 0; i < n; ++i)
-          if (H.v(Y, i) < 0.0) { H.v(Y, i) = 0.0; lifted = true; }
-        if (lifted) {
-          floored = true;
-          H.rhs(Y, K1);
-        }
-      }
-    }
-    if (status) break;
-    if (jumped) {
-      TableModel<double, kBlock> st{T, V, a, av};
-      for (int j = 0; j < m; ++j) a[j * B] = st.prop(j);
-      if (kCount) H.flops += static_cast<uint64_t>(T.fprop);
-      double as = 0.0;
-      for (int j = 0; j < m; ++j)
-        if (H.slow(j)) as = as + a[j * B];
-      const double u2 = kPhilox ? site.uniform() : rng.uniform();
-      if (as > 0.0) {
-        const double target = u2 * as;
-        double c = 0.0;
-        int sel = -1, last = -1;
-        for (int j = 0; j < m; ++j) {
-          if (!H.slow(j)) continue;
-          if (a[j * B] > 0.0) last = j;
-          c = c + a[j * B];
-          if (c > target) { sel = j; break; }
-        }
-        if (sel < 0) sel = last;
-        const int p1 = tab_col_ptr(T, sel + 1);
-        for (int p = tab_col_ptr(T, sel); p < p1; ++p) {
-          const uint32_t e = tab_col(T, p);
-          double& vv = H.v(Y, KIN_NU_INDEX(e));
-          vv = vv + static_cast<double>(KIN_NU_DELTA(e));
-          if (vv < 0.0) { vv = 0.0; ++meta[2]; }
-        }
-        ++meta[4];
-        if (kCount) H.flops += 2 * static_cast<uint64_t>(m) + 1;
-      }
-      while (gi < G && tab_grid(T, S, gi) <= t) emit_state();
-    }
-    ++seg;
-  }
-  while (gi < G) emit_state();
-  meta[5] = floored ? 1 : 0;
-  uint64_t* me = O.meta + s * 6;
-  for (int q = 0; q < 6; ++q) me[q] = meta[q];
-  O.status[s] = status;
-  if (kCount && O.work) O.work[s] = H.flops;
-}
-
-// doubles of per-warp state (the bitmask words rounded up to whole doubles)
-__host__ __device__ __forceinline__ size_t hybrid_warp_doubles(const KinTables& T, const KinSweepDev& S) {
-  const size_t words = (static_cast<size_t>(T.m) + 31) / 32;
-  return (static_cast<size_t>(kVecs) * (T.n + 1) + T.m + S.n_axes) * kBlock + (words * kBlock + 1) / 2;
-}
-
-template <bool kCount, bool kPhilox, bool kGlobal, int kN>
-__global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ KinTables T,
-                                                        const __grid_constant__ KinSweepDev S, KinOutDev O,
-                                                        unsigned long long* __restrict__ next) {
-  extern __shared__ double smem[];
-  constexpr int B = kBlock;
-  const int tid = threadIdx.x, lane = tid & 31;
-  const int n1 = T.n + 1;
-  // state in shared memory, or (kGlobal) in this block's region of global memory
-  double* base = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * hybrid_warp_doubles(T, S) : smem;
-  double* V = base + tid;
-  double* a = base + static_cast<size_t>(kVecs) * n1 * B + tid;
-  double* av = a + static_cast<size_t>(T.m) * B;
-  uint32_t* slowm = reinterpret_cast<uint32_t*>(base + static_cast<size_t>(kVecs * n1 + T.m + S.n_axes) * B) + tid;
-  for (;;) {
-    unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(next, 32ULL);
-    base = __shfl_sync(0xFFFFFFFFu, base, 0);
-    if (base >= S.n_local) break;
-    const uint64_t s = base + lane;
-    if (s < S.n_local) simulate_hybrid_one<kCount, kPhilox, kN>(T, S, O, s, V, a, av, slowm);
-    __syncwarp();
-  }
-}
-
-}  // namespace
-
-size_t hybrid_state_doubles_per_warp(const KinTables& T, const KinSweepDev& S) { return hybrid_warp_doubles(T, S); }
+size_t hybrid_state_doubles_per_warp(const KinTables& T, const KinSweepDev& S) { return hyb::hybrid_warp_doubles(T, S); }
 
 size_t hybrid_smem_bytes(const KinTables& T, const KinSweepDev& S) {
   const size_t words = (static_cast<size_t>(T.m) + 31) / 32;
-  return (static_cast<size_t>(kVecs) * (T.n + 1) + T.m + S.n_axes) * kBlock * sizeof(double) +
-         words * kBlock * sizeof(uint32_t);
+  return (static_cast<size_t>(hyb::kVecs) * (T.n + 1) + T.m + S.n_axes) * hyb::kBlock * sizeof(double) +
+         words * hyb::kBlock * sizeof(uint32_t);
 }
 
 cudaError_t launch_hybrid(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, bool count,
                           unsigned long long* counter, cudaStream_t stream) {
+  using namespace hyb;
   if (S.n_local == 0) return cudaSuccess;
   const size_t smem = S.gstate ? 0 : hybrid_smem_bytes(T, S);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   const bool ph = S.rng_mode == KIN_RNG_PHILOX;
-  using KernT = void (*)(const KinTables, const KinSweepDev, KinOutDev, unsigned long long*);
-  KernT kern = nullptr;
-  if (S.gstate) {
-    kern = count ? (ph ? hybrid_kernel<true, true, true, 0> : hybrid_kernel<true, false, true, 0>)
-                 : (ph ? hybrid_kernel<false, true, true, 0> : hybrid_kernel<false, false, true, 0>);
-  } else if (!count && T.n <= 8) {  // small models: specialised on the species count
+  if (S.gstate)
+    return count ? (ph ? launch_k<true, true, true, 0>(T, S, O, counter, smem, stream)
+                       : launch_k<true, false, true, 0>(T, S, O, counter, smem, stream))
+                 : (ph ? launch_k<false, true, true, 0>(T, S, O, counter, smem, stream)
+                       : launch_k<false, false, true, 0>(T, S, O, counter, smem, stream));
+  if (!count && T.n <= 8) {  // small models: specialised on the species count
     switch (T.n) {
-#define KIN_HYB_CASE(k) \
-  case k: kern = ph ? hybrid_kernel<false, true, false, k> : hybrid_kernel<false, false, false, k>; break;
+#define KIN_HYB_CASE(k)                                                   \
+  case k:                                                                 \
+    return ph ? launch_k<false, true, false, k>(T, S, O, counter, smem, stream) \
+              : launch_k<false, false, false, k>(T, S, O, counter, smem, stream);
       KIN_HYB_CASE(1) KIN_HYB_CASE(2) KIN_HYB_CASE(3) KIN_HYB_CASE(4)
       KIN_HYB_CASE(5) KIN_HYB_CASE(6) KIN_HYB_CASE(7) KIN_HYB_CASE(8)
 #undef KIN_HYB_CASE
     }
-  } else {
-    kern = count ? (ph ? hybrid_kernel<true, true, false, 0> : hybrid_kernel<true, false, false, 0>)
-                 : (ph ? hybrid_kernel<false, true, false, 0> : hybrid_kernel<false, false, false, 0>);
   }
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t warps = (S.n_local + 31) / 32;
-  uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
-  if (S.gstate && resident > S.gstate_warps) resident = S.gstate_warps;
-  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
-  e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
-  if (e != cudaSuccess) return e;
-  kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter);
-  return cudaGetLastError();
+  return count ? (ph ? launch_k<true, true, false, 0>(T, S, O, counter, smem, stream)
+                     : launch_k<true, false, false, 0>(T, S, O, counter, smem, stream))
+               : (ph ? launch_k<false, true, false, 0>(T, S, O, counter, smem, stream)
+                     : launch_k<false, false, false, 0>(T, S, O, counter, smem, stream));
 }
 
 }  // namespace kin
