@@ -87,6 +87,20 @@ __device__ __forceinline__ uint64_t sim_seed(const KinSweepDev& S, uint64_t sim)
   return derive_run_seed(derive_run_seed(S.master_seed, point), run);
 }
 
+// Sweep coordinates of global simulation `sim` (Cartesian points, last axis
+// fastest, R runs per point: SPEC.md:438-446) into av[ax * stride].  Out of
+// line: the 64-bit divisions are long instruction sequences, and this runs
+// once per simulation.
+static __device__ __noinline__ void decode_point(const KinSweepDev& S, uint64_t sim, double* av, int stride) {
+  uint64_t rem = sim / S.runs;
+  for (int ax = S.n_axes - 1; ax >= 0; --ax) {
+    const uint64_t nv = static_cast<uint64_t>(S.axis_n[ax]);
+    const uint64_t q = rem / nv;
+    av[ax * stride] = __ldg(S.axis_values[ax] + (rem - q * nv));
+    rem = q;
+  }
+}
+
 // ---- xoshiro256++ stream (rng.cpp:25-52) ------------------------------------
 // With a one-value lookahead: `nx` already holds the next output, so a draw
 // hands it out at once and the state advance (a serial chain of 64-bit integer
@@ -282,6 +296,29 @@ __device__ __forceinline__ uint64_t poisson(Rng& rng, double mean, uint64_t& flo
   }
 }
 
+// x(x-1)(x-2)/6: out of line, so the runtime-stoichiometry propensity loops
+// (inlined many times in the ODE/hybrid kernels) do not each carry a double
+// division; the JIT's constant stoichiometries still fold it inline.
+__device__ __forceinline__ double combinations3_inline(double x) {
+  return __ddiv_rn(__dmul_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), __dsub_rn(x, 2.0)), 6.0);
+}
+static __device__ __noinline__ double combinations3(double x) { return combinations3_inline(x); }
+// compile-time stoichiometry (the per-model JIT): everything inline
+template <int kS>
+__device__ __forceinline__ double combinations_c(double x) {
+  double h;
+  if constexpr (kS == 1) {
+    h = x;
+  } else if constexpr (kS == 2) {
+    h = __dmul_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), 0.5);
+  } else if constexpr (kS == 3) {
+    h = combinations3_inline(x);
+  } else {
+    return 1.0;
+  }
+  return h < 0.0 ? 0.0 : h;
+}
+
 // combinations (model.hpp:145-149) + order-3 extension; clamp >= 0.
 __device__ __forceinline__ double combinations(double x, int s) {
   double h;
@@ -290,7 +327,7 @@ __device__ __forceinline__ double combinations(double x, int s) {
   } else if (s == 2) {
     h = __dmul_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), 0.5);  // == /2.0 exactly (power of two)
   } else if (s == 3) {
-    h = __ddiv_rn(__dmul_rn(__dmul_rn(x, __dsub_rn(x, 1.0)), __dsub_rn(x, 2.0)), 6.0);
+    h = combinations3(x);
   } else {
     return 1.0;
   }

@@ -10,9 +10,15 @@
 //   and dG/dt = sum_slow a_j; where G reaches E, bisection on the dense output
 //   to 1e-10 relative in t; the firing slow reaction by the ssa_select rule
 //   over the slow set; nu_j added to the continuous state, clamped at 0.
-// Per-simulation state: 15 vectors of N+1 doubles (y, k1..k7, yn, ys, r1..r5),
-// a[M], the sweep coordinates and a slow-set bitmask, in shared memory with the
-// [slot][thread] layout (conflict-free; lanes touch consecutive words).
+// Per-simulation state: 8 vectors of N+1 doubles (y, k1..k6, ys), a[M], the
+// sweep coordinates and a slow-set bitmask, in shared memory with the
+// [slot][thread] layout (conflict-free; lanes touch consecutive words).  k7
+// reuses k2's slot and yn reuses ys's (a72 = e2 = d2 = 0: k2 is dead once
+// stage 6 is formed, ys once yn is); the dense-output coefficients r1..r5 are
+// formed on demand from y, yn, k1, k3..k7 with the oracle's expressions, so
+// they round identically.  The six stages run as one loop over a coefficient
+// table so the RHS (propensities + fast/slow sums) is inlined once, not six
+// times (instruction-cache footprint).
 #pragma once
 #include "kin_launch.h"
 #include "kin_pmath.cuh"
@@ -43,7 +49,15 @@ constexpr double c_d1 = -12715105075.0 / 11282082432.0, c_d3 = 87487479700.0 / 3
                  c_d6 = -1453857185.0 / 822651844.0, c_d7 = 69997945.0 / 29380423.0;
 constexpr double kSafe = 0.9, kFacMinInv = 5.0, kFacMaxInv = 0.1;
 constexpr double kBeta = 0.04, kExpo1 = 0.2 - kBeta * 0.75;
-constexpr int kVecs = 15;
+constexpr int kVecs = 8;
+// stage s (0..5) input: y + h * sum_k c_stage[s][k] k_{k+1}, summed left to right
+// (stage 7 skips the zero a72)
+__constant__ double c_stage[6][6] = {{c_a21, 0, 0, 0, 0, 0},
+                                     {c_a31, c_a32, 0, 0, 0, 0},
+                                     {c_a41, c_a42, c_a43, 0, 0, 0},
+                                     {c_a51, c_a52, c_a53, c_a54, 0, 0},
+                                     {c_a61, c_a62, c_a63, c_a64, c_a65, 0},
+                                     {c_a71, 0, c_a73, c_a74, c_a75, c_a76}};
 
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
@@ -89,13 +103,29 @@ struct Hybrid {
     if (kCount) flops += static_cast<uint64_t>(m);
   }
 
-  __device__ __forceinline__ double dense(double th, int i) const {
-    const double th1 = 1.0 - th;
-    return v(10, i) + th * (v(11, i) + th1 * (v(12, i) + th * (v(13, i) + th1 * v(14, i))));
-  }
 };
 
-enum { Y = 0, K1, K2, K3, K4, K5, K6, K7, YN, YS, R1, R2, R3, R4, R5 };
+enum { Y = 0, K1, K2, K3, K4, K5, K6, YS, K7 = K2, YN = YS };
+
+// Dense output of the accepted step for one component (the oracle's r1..r5).
+struct Dense5 {
+  double r1, r2, r3, r4, r5;
+  template <class HT>
+  __device__ __forceinline__ Dense5(const HT& H, int i, double hh) {
+    r1 = H.v(Y, i);
+    const double yd = H.v(YN, i) - H.v(Y, i);
+    r2 = yd;
+    const double bs = hh * H.v(K1, i) - yd;
+    r3 = bs;
+    r4 = yd - hh * H.v(K7, i) - bs;
+    r5 = hh * (c_d1 * H.v(K1, i) + c_d3 * H.v(K3, i) + c_d4 * H.v(K4, i) + c_d5 * H.v(K5, i) + c_d6 * H.v(K6, i) +
+               c_d7 * H.v(K7, i));
+  }
+  __device__ __forceinline__ double at(double th) const {
+    const double th1 = 1.0 - th;
+    return r1 + th * (r2 + th1 * (r3 + th * (r4 + th1 * r5)));
+  }
+};
 
 template <bool kCount, bool kPhilox, int kN>
 __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, uint64_t s,
@@ -186,25 +216,16 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         bool hit = false;
         if (t + hh >= t_hor) { hh = t_hor - t; hit = true; }
         if (!(hh > 0.0) || t + hh == t) { status = KIN_SIM_STEP_UNDERFLOW; break; }
-        for (int i = 0; i < n1; ++i) H.v(YS, i) = H.v(Y, i) + hh * (c_a21 * H.v(K1, i));
-        H.rhs(YS, K2);
-        for (int i = 0; i < n1; ++i) H.v(YS, i) = H.v(Y, i) + hh * (c_a31 * H.v(K1, i) + c_a32 * H.v(K2, i));
-        H.rhs(YS, K3);
-        for (int i = 0; i < n1; ++i)
-          H.v(YS, i) = H.v(Y, i) + hh * (c_a41 * H.v(K1, i) + c_a42 * H.v(K2, i) + c_a43 * H.v(K3, i));
-        H.rhs(YS, K4);
-        for (int i = 0; i < n1; ++i)
-          H.v(YS, i) =
-              H.v(Y, i) + hh * (c_a51 * H.v(K1, i) + c_a52 * H.v(K2, i) + c_a53 * H.v(K3, i) + c_a54 * H.v(K4, i));
-        H.rhs(YS, K5);
-        for (int i = 0; i < n1; ++i)
-          H.v(YS, i) = H.v(Y, i) + hh * (c_a61 * H.v(K1, i) + c_a62 * H.v(K2, i) + c_a63 * H.v(K3, i) +
-                                         c_a64 * H.v(K4, i) + c_a65 * H.v(K5, i));
-        H.rhs(YS, K6);
-        for (int i = 0; i < n1; ++i)
-          H.v(YN, i) = H.v(Y, i) + hh * (c_a71 * H.v(K1, i) + c_a73 * H.v(K3, i) + c_a74 * H.v(K4, i) +
-                                         c_a75 * H.v(K5, i) + c_a76 * H.v(K6, i));
-        H.rhs(YN, K7);
+#pragma unroll 1
+        for (int st = 0; st < 6; ++st) {
+          for (int i = 0; i < n1; ++i) {
+            double acc = c_stage[st][0] * H.v(K1, i);
+            for (int k = 1; k <= st; ++k)
+              if (st != 5 || k != 1) acc = acc + c_stage[st][k] * H.v(K1 + k, i);
+            H.v(YS, i) = H.v(Y, i) + hh * acc;  // yn for st = 5 (same slot)
+          }
+          H.rhs(YS, st == 5 ? K7 : K2 + st);
+        }
         double sum = 0.0;
         bool finite = true;
         for (int i = 0; i < n1; ++i) {
@@ -230,16 +251,6 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         fac = dmax(kFacMaxInv, dmin(kFacMinInv, fac / kSafe));
         double hnew = hh / fac;
         facold = dmax(err, 1.0e-4);
-        for (int i = 0; i < n1; ++i) {
-          H.v(R1, i) = H.v(Y, i);
-          const double yd = H.v(YN, i) - H.v(Y, i);
-          H.v(R2, i) = yd;
-          const double bs = hh * H.v(K1, i) - yd;
-          H.v(R3, i) = bs;
-          H.v(R4, i) = yd - hh * H.v(K7, i) - bs;
-          H.v(R5, i) = hh * (c_d1 * H.v(K1, i) + c_d3 * H.v(K3, i) + c_d4 * H.v(K4, i) + c_d5 * H.v(K5, i) +
-                             c_d6 * H.v(K6, i) + c_d7 * H.v(K7, i));
-        }
         if (last_rejected && hnew > hh) hnew = hh;
         last_rejected = false;
         h = hnew;
@@ -249,11 +260,12 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         const double tnew = hit ? t_hor : t + hh;
         if (H.v(YN, n) >= E) {
           double lo = 0.0, hi = 1.0;
+          const Dense5 dg(H, n, hh);
           for (int it = 0; it < 200; ++it) {
             const double tl = tprev + lo * hh, th = tprev + hi * hh;
             if (!(th - tl > 1e-10 * fabs(th))) break;
             const double mid = 0.5 * (lo + hi);
-            if (H.dense(mid, n) >= E) hi = mid; else lo = mid;
+            if (dg.at(mid) >= E) hi = mid; else lo = mid;
             if (kCount) H.flops += 12;
           }
           const double ts = hi == 1.0 ? tnew : tprev + hi * hh;
@@ -261,7 +273,7 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
             double* o = O.traj + (static_cast<size_t>(s) * G + gi) * n;
             const double th = (tab_grid(T, S, gi) - tprev) / hh;
             for (int i = 0; i < n; ++i) {
-              double vv = H.dense(th, i);
+              double vv = Dense5(H, i, hh).at(th);
               if (vv < 0.0) { vv = 0.0; floored = true; }
               o[i] = vv;
             }
@@ -269,7 +281,7 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
             ++gi;
           }
           for (int i = 0; i < n; ++i) {
-            double vv = hi == 1.0 ? H.v(YN, i) : H.dense(hi, i);
+            double vv = hi == 1.0 ? H.v(YN, i) : Dense5(H, i, hh).at(hi);
             if (vv < 0.0) { vv = 0.0; floored = true; }
             H.v(Y, i) = vv;
           }
@@ -278,28 +290,30 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
           break;
         }
         t = tnew;
-        for (int i = 0; i < n1; ++i) {
-          H.v(Y, i) = H.v(YN, i);
-          H.v(K1, i) = H.v(K7, i);
-        }
+        // grid samples inside the step (before y <- yn, k1 <- k7: the dense
+        // output is formed from this step's vectors)
         while (gi < G && tab_grid(T, S, gi) <= t) {
           double* o = O.traj + (static_cast<size_t>(s) * G + gi) * n;
           if (tab_grid(T, S, gi) == t) {
             for (int i = 0; i < n; ++i) {
-              double vv = H.v(Y, i);
+              double vv = H.v(YN, i);
               if (vv < 0.0) { vv = 0.0; floored = true; }
               o[i] = vv;
             }
           } else {
             const double th = (tab_grid(T, S, gi) - tprev) / hh;
             for (int i = 0; i < n; ++i) {
-              double vv = H.dense(th, i);
+              double vv = Dense5(H, i, hh).at(th);
               if (vv < 0.0) { vv = 0.0; floored = true; }
               o[i] = vv;
             }
             if (kCount) H.flops += 8 * static_cast<uint64_t>(n) + 3;
           }
           ++gi;
+        }
+        for (int i = 0; i < n1; ++i) {
+          H.v(Y, i) = H.v(YN, i);
+          H.v(K1, i) = H.v(K7, i);
         }
         bool lifted = false;
         for (int i = 0; i < n; ++i)

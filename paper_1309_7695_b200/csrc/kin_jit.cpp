@@ -120,7 +120,7 @@ std::string generate_policy(const JitModel& m) {
     else o << "tab_rate(T, " << j << ")";
     o << ";";
     for (int p = m.rt_ptr[j]; p < m.rt_ptr[j + 1]; ++p)
-      o << " aj = __dmul_rn(aj, combinations(xv(" << m.rt_species[p] << "), " << m.rt_stoich[p] << "));";
+      o << " aj = __dmul_rn(aj, combinations_c<" << m.rt_stoich[p] << ">(xv(" << m.rt_species[p] << ")));";
     o << " return aj;\n";
   }
   o << "    }\n    return 0.0;\n  }\n";

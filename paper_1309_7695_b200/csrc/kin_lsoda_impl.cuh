@@ -37,6 +37,45 @@ constexpr int kBlock = 32;
 constexpr int kL = 13;  // Nordsieck vectors (Adams max order 12)
 
 
+// The RHS and the weighted RMS norm are called from several places in the
+// step; out of line they exist once in the kernel's code (each inlined copy,
+// with its species loop unrolled and its correctly rounded divisions, costs
+// instruction-cache space the step loop needs).
+template <int kN>
+__device__ __noinline__ void rhs_out_of_line(const KinTables& T, const double* av, double* a, int m, int n_rt,
+                                             const double* yy, double* f) {
+  constexpr int B = kBlock;
+  const int n = kN > 0 ? kN : n_rt;
+  for (int j = 0; j < m; ++j) {
+    const uint64_t d = tab_rdesc(T, j);
+    const int ax = KIN_RD_AXIS(d);
+    double aj = ax < 0 ? tab_rate(T, j) : av[ax * B];
+    const int nt = KIN_RD_NTERMS(d);
+    for (int t = 0; t < nt; ++t) aj = aj * combinations(yy[KIN_RD_SPECIES(d, t) * B], KIN_RD_STOICH(d, t));
+    a[j * B] = aj;
+  }
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    const int p1 = tab_row_ptr(T, i + 1);
+    for (int p = tab_row_ptr(T, i); p < p1; ++p) {
+      const uint32_t e = tab_row(T, p);
+      s = s + static_cast<double>(KIN_NU_DELTA(e)) * a[KIN_NU_INDEX(e) * B];
+    }
+    f[i * B] = s;
+  }
+}
+template <int kN>
+__device__ __noinline__ double wrms_out_of_line(const double* vv, const double* ewt, int n_rt) {
+  constexpr int B = kBlock;
+  const int n = kN > 0 ? kN : n_rt;
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double q = vv[i * B] / ewt[i * B];
+    s = s + q * q;
+  }
+  return sqrt(s / n);
+}
+
 // kN > 0: the species count is a compile-time constant (small models: every
 // loop over species unrolls and the indexing folds); kN = 0: runtime T.n.
 template <int kN>
@@ -64,23 +103,8 @@ struct Lsoda {
   }
   // rre_rhs (oracle order): a_j then dx_i = sum over the nu row
   template <bool C>
-  __device__ void rhs(const double* yy, double* f) {
-    for (int j = 0; j < m; ++j) {
-      const uint64_t d = tab_rdesc(T, j);
-      double aj = rate(j);
-      const int nt = KIN_RD_NTERMS(d);
-      for (int t = 0; t < nt; ++t) aj = aj * combinations(yy[KIN_RD_SPECIES(d, t) * B], KIN_RD_STOICH(d, t));
-      a[j * B] = aj;
-    }
-    for (int i = 0; i < N(); ++i) {
-      double s = 0.0;
-      const int p1 = tab_row_ptr(T, i + 1);
-      for (int p = tab_row_ptr(T, i); p < p1; ++p) {
-        const uint32_t e = tab_row(T, p);
-        s = s + static_cast<double>(KIN_NU_DELTA(e)) * a[KIN_NU_INDEX(e) * B];
-      }
-      f[i * B] = s;
-    }
+  __device__ __forceinline__ void rhs(const double* yy, double* f) {
+    rhs_out_of_line<kN>(T, av, a, m, N(), yy, f);
     if (C) flops += F_rhs;
   }
   template <bool C>
@@ -157,14 +181,9 @@ struct Lsoda {
     if (C) flops += static_cast<uint64_t>(2 * N() * N());
   }
   template <bool C>
-  __device__ double wrms(const double* vv) {
-    double s = 0.0;
-    for (int i = 0; i < N(); ++i) {
-      const double q = vv[i * B] / ewt[i * B];
-      s = s + q * q;
-    }
+  __device__ __forceinline__ double wrms(const double* vv) {
     if (C) flops += 3 * static_cast<uint64_t>(N()) + 2;
-    return sqrt(s / N());
+    return wrms_out_of_line<kN>(vv, ewt, N());
   }
 };
 
@@ -199,15 +218,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   L.flops = 0;
   L.F_rhs = static_cast<uint64_t>(T.fprop) + 2 * static_cast<uint64_t>(T.nnz);
 
-  {
-    uint64_t rem = sim / S.runs;
-    for (int ax = S.n_axes - 1; ax >= 0; --ax) {
-      const uint64_t nv = static_cast<uint64_t>(S.axis_n[ax]);
-      const uint64_t q = rem / nv;
-      L.av[ax * B] = __ldg(S.axis_values[ax] + (rem - q * nv));
-      rem = q;
-    }
-  }
+  decode_point(S, sim, L.av, B);
   const double rtol = S.rel_tol, atol = S.abs_tol;
   const double hmax = S.h_max > 0.0 ? S.h_max : __builtin_huge_val();
   const double t_end = S.t_end;
@@ -265,6 +276,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
     auto set_order = [&](int mm, int q) { meth = mm; nq = q; el0 = L.elco(meth, nq, 0); };
     auto rescale = [&](double rh) {
       double r = rh;
+#pragma unroll 1
       for (int j = 1; j <= nq; ++j) {
         for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) * r;
         r = r * rh;
@@ -273,13 +285,17 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
       if (kCount) L.flops += static_cast<uint64_t>(nq) * (n + 1);
     };
     auto predict = [&]() {
+#pragma unroll 1
       for (int k = 0; k < nq; ++k)
+#pragma unroll 1
         for (int j = nq - 1; j >= k; --j)
           for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) + L.z(j + 1, i);
       if (kCount) L.flops += static_cast<uint64_t>(nq) * (nq + 1) / 2 * n;
     };
     auto unpredict = [&]() {
+#pragma unroll 1
       for (int k = nq - 1; k >= 0; --k)
+#pragma unroll 1
         for (int j = k; j <= nq - 1; ++j)
           for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) - L.z(j + 1, i);
     };
@@ -419,6 +435,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
         // accepted
         ++nst;
         ++n_acc;
+#pragma unroll 1
         for (int j = 0; j <= nq; ++j) {
           const double e = L.elco(meth, nq, j);
           for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) + e * L.acor[i * B];
@@ -430,6 +447,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           const double sg = (tab_grid(T, S, gi) - t) / h;
           for (int i = 0; i < n; ++i) {
             double vv = L.z(nq, i);
+#pragma unroll 1
             for (int j = nq - 1; j >= 0; --j) vv = L.z(j, i) + sg * vv;
             L.tmp[i * B] = vv;
           }

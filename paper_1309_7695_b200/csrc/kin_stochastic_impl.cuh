@@ -198,13 +198,7 @@ __device__ __forceinline__ int ssa_select(const Model& sm, int M, double a0, dou
 template <class XT, int B = kBlock>
 __device__ __forceinline__ bool init_state(const KinTables& T, const KinSweepDev& S, uint64_t sim, int N, XT* x,
                                            double* av) {
-  uint64_t rem = sim / S.runs;
-  for (int ax = S.n_axes - 1; ax >= 0; --ax) {
-    const uint64_t nv = static_cast<uint64_t>(S.axis_n[ax]);
-    const uint64_t q = rem / nv;
-    av[ax * B] = __ldg(S.axis_values[ax] + (rem - q * nv));
-    rem = q;
-  }
+  decode_point(S, sim, av, B);
   bool ovf = false;
   for (int i = 0; i < N; ++i) {
     const int ax = tab_x0_axis(T, i);

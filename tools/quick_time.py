@@ -27,8 +27,11 @@ cfgs = {
     "c5_tau": W.c5_config(),
     "c5_ode": W.c5_config(method=MethodKind.Ode),
     "c1_hybrid": W.c1_config(MethodKind.Hybrid, side=128),
+    "c1_hybrid256": W.c1_config(MethodKind.Hybrid, side=256),
     "c1_cle": W.c1_config(MethodKind.Cle, side=128),
 }
+for _k in ("c1_hybrid", "c1_hybrid256"):
+    cfgs[_k][1].method = __import__("paper_1309_7695_b200").ensemble.Method(MethodKind.Hybrid, theta_x=100.0, theta_a=10.0)
 cfgs["c1_cle"][1].method = __import__("paper_1309_7695_b200").ensemble.Method(MethodKind.Cle, tau=0.05)
 names = sys.argv[1:] or list(cfgs)
 err = abi.KinError()
