@@ -417,6 +417,10 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, KIN_STOCH_BLOCK, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaSuccess;
+  {  // development knob: cap the resident warps per SM (residency studies)
+    const int cap = jit_knob("KIN_JIT_WARPS_PER_SM", 0);
+    if (cap > 0 && cap < per_sm) per_sm = cap;
+  }
   const uint64_t blocks = (S.n_local + KIN_STOCH_BLOCK - 1) / KIN_STOCH_BLOCK;
   uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
   if (S.gstate && S.gstate_warps < resident) resident = S.gstate_warps;
