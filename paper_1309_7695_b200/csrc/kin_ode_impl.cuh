@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
       const int ax = s_rate_axis[j];
       double aj = ax < 0 ? s_rate[j] : av[ax];
       const int p1 = s_rt_ptr[j + 1];
+#pragma unroll 1
       for (int p = s_rt_ptr[j]; p < p1; ++p) {
         const uint32_t e = s_rt[p];
         aj = aj * combinations(xs[KIN_TERM_SPECIES(e)], KIN_TERM_STOICH(e));
@@ -143,6 +144,7 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
       double acc = 0.0;
       if (i < N) {
         const int p1 = s_row_ptr[i + 1];
+#pragma unroll 1
         for (int p = s_row_ptr[i]; p < p1; ++p) {
           const uint32_t e = s_row[p];
           acc = acc + static_cast<double>(KIN_NU_DELTA(e)) * a[KIN_NU_INDEX(e)];
