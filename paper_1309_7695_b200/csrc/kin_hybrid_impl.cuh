@@ -83,11 +83,13 @@ struct Hybrid {
   // augmented RHS: f = (sum_fast nu a (row order), sum_slow a) at state `yv`
   __device__ void rhs(int yv, int fv) {
     TableModel<double, kBlock> st{T, vp(yv), sm.a, sm.av};
+#pragma unroll 1
     for (int j = 0; j < m; ++j) sm.a[j * kBlock] = st.prop(j);
     if (kCount) flops += static_cast<uint64_t>(T.fprop);
     for (int i = 0; i < N(); ++i) {
       double acc = 0.0;
       const int p1 = tab_row_ptr(T, i + 1), p0 = tab_row_ptr(T, i);
+#pragma unroll 1
       for (int p = p0; p < p1; ++p) {
         const uint32_t e = tab_row(T, p);
         const int j = KIN_NU_INDEX(e);
@@ -97,6 +99,7 @@ struct Hybrid {
       if (kCount) flops += 2 * static_cast<uint64_t>(p1 - p0);
     }
     double g = 0.0;
+#pragma unroll 1
     for (int j = 0; j < m; ++j)
       if (slow(j)) g = g + sm.a[j * kBlock];
     v(fv, N()) = g;

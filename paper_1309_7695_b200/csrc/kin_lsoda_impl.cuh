@@ -46,17 +46,20 @@ __device__ __noinline__ void rhs_out_of_line(const KinTables& T, const double* a
                                              const double* yy, double* f) {
   constexpr int B = kBlock;
   const int n = kN > 0 ? kN : n_rt;
+#pragma unroll 1
   for (int j = 0; j < m; ++j) {
     const uint64_t d = tab_rdesc(T, j);
     const int ax = KIN_RD_AXIS(d);
     double aj = ax < 0 ? tab_rate(T, j) : av[ax * B];
     const int nt = KIN_RD_NTERMS(d);
+#pragma unroll 1
     for (int t = 0; t < nt; ++t) aj = aj * combinations(yy[KIN_RD_SPECIES(d, t) * B], KIN_RD_STOICH(d, t));
     a[j * B] = aj;
   }
   for (int i = 0; i < n; ++i) {
     double s = 0.0;
     const int p1 = tab_row_ptr(T, i + 1);
+#pragma unroll 1
     for (int p = tab_row_ptr(T, i); p < p1; ++p) {
       const uint32_t e = tab_row(T, p);
       s = s + static_cast<double>(KIN_NU_DELTA(e)) * a[KIN_NU_INDEX(e) * B];
@@ -110,6 +113,7 @@ struct Lsoda {
   template <bool C>
   __device__ void jacobian(const double* yy, double* J) {
     for (int q = 0; q < N() * N(); ++q) J[q * B] = 0.0;
+#pragma unroll 1
     for (int k = 0; k < m; ++k) {
       const uint64_t d = tab_rdesc(T, k);
       const int nt = KIN_RD_NTERMS(d);
@@ -126,6 +130,7 @@ struct Lsoda {
         for (int q = 0; q < nt; ++q)
           if (q != p) dd = dd * combinations(yy[KIN_RD_SPECIES(d, q) * B], KIN_RD_STOICH(d, q));
         const int c1 = tab_col_ptr(T, k + 1);
+#pragma unroll 1
         for (int c = tab_col_ptr(T, k); c < c1; ++c) {
           const uint32_t e = tab_col(T, c);
           double& jj = J[(KIN_NU_INDEX(e) * N() + s) * B];

@@ -103,6 +103,7 @@ struct TableModel {
   // x += nu[:, j] * k  (k signed: negative undoes a rejected leap)
   __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const {
     const int p1 = tab_col_ptr(T, j + 1);
+#pragma unroll 1
     for (int p = tab_col_ptr(T, j); p < p1; ++p) {
       const uint32_t e = tab_col(T, p);
       XT* xs = x + KIN_NU_INDEX(e) * B;
@@ -119,6 +120,7 @@ struct TableModel {
   __device__ __forceinline__ bool fire(int j, bool& ovf) const {
     bool neg = false;
     const int p1 = tab_col_ptr(T, j + 1);
+#pragma unroll 1
     for (int p = tab_col_ptr(T, j); p < p1; ++p) {
       const uint32_t e = tab_col(T, p);
       XT* xs = x + KIN_NU_INDEX(e) * B;
@@ -159,6 +161,7 @@ struct TableModel {
   }
   __device__ __forceinline__ void dep_update(int sel) const {
     const int q1 = tab_dep_ptr(T, sel + 1);
+#pragma unroll 1
     for (int q = tab_dep_ptr(T, sel); q < q1; ++q) {
       const int k = tab_dep(T, q);
       a[k * B] = prop(k);
