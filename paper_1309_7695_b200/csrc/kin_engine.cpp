@@ -687,7 +687,9 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   const int kind = d->method.kind;
   bf.last_int_state = false;  // set below only by the int32-state stochastic launch
   if (kind == KIN_METHOD_ODE) {
-    e = kin::launch_dopri5(*T, SD, O, want_work, 0, bf.st);
+    int ode_lanes = 0;  // 0: by species count (ode_pick_lanes); KIN_ODE_LANES overrides (residency studies)
+    if (const char* v = std::getenv("KIN_ODE_LANES")) ode_lanes = std::atoi(v);
+    e = kin::launch_dopri5(*T, SD, O, want_work, ode_lanes, bf.st);
     bf.kernel_name = "dopri5_kernel";
   } else if (kind == KIN_METHOD_HYBRID) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
