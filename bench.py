@@ -168,10 +168,21 @@ def dist_setup(n_gpus: int):
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if _backend() == "gloo":
+            # functional check of the N>1 path on a box with fewer GPUs than
+            # ranks (ranks share devices; never a reported number)
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def _backend():
+    return os.environ.get("KIN_BENCH_BACKEND", "nccl")
 
 
 def barrier(world):
@@ -185,7 +196,7 @@ def max_over_ranks(world, value: float, local: int) -> float:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([value], dtype=torch.float64, device="cpu" if _backend() == "gloo" else f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -195,7 +206,7 @@ def sum_over_ranks(world, value: float, local: int) -> float:
         return value
     import torch
     import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device=f"cuda:{local}")
+    t = torch.tensor([value], dtype=torch.float64, device="cpu" if _backend() == "gloo" else f"cuda:{local}")
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
