@@ -89,7 +89,7 @@ struct Lsoda {
   int n_rt, m;
   static constexpr int B = kBlock;
   __device__ __forceinline__ int N() const { return kN > 0 ? kN : n_rt; }
-  double *Z, *acor, *savf, *ewt, *y, *tmp, *P, *J2, *a, *av;
+  double *Z, *acor, *savf, *ewt, *y, *tmp, *P, *a, *av;
   int* piv;
   uint64_t flops;
   uint64_t F_rhs;
@@ -139,6 +139,53 @@ struct Lsoda {
         if (C) flops += 4 + nt + 2 * static_cast<uint64_t>(c1 - tab_col_ptr(T, k));
       }
     }
+  }
+  // max_i (sum_j |J_ij| ewt_j) / ewt_i without storing J: row i is formed in
+  // tmp by walking row i of nu (reactions ascending), so each J_ij receives the
+  // oracle's contributions (rre_jacobian: reactions ascending) in its order.
+  template <bool C>
+  __device__ double jac_norm_rows(const double* yy) {
+    double nm = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < N(); ++i) {
+      for (int s = 0; s < N(); ++s) tmp[s * B] = 0.0;
+      const int p1 = tab_row_ptr(T, i + 1);
+#pragma unroll 1
+      for (int pr = tab_row_ptr(T, i); pr < p1; ++pr) {
+        const uint32_t e = tab_row(T, pr);
+        const int k = KIN_NU_INDEX(e);
+        const double dl = static_cast<double>(KIN_NU_DELTA(e));
+        const uint64_t d = tab_rdesc(T, k);
+        const int nt = KIN_RD_NTERMS(d);
+        const double rk = rate(k);
+#pragma unroll 1
+        for (int p = 0; p < nt; ++p) {
+          const int s = KIN_RD_SPECIES(d, p), st = KIN_RD_STOICH(d, p);
+          const double xs = yy[s * B];
+          const double h = combinations(xs, st);
+          double dh;
+          if (st == 1) dh = xs < 0.0 ? 0.0 : 1.0;
+          else if (st == 2) dh = h > 0.0 ? xs - 0.5 : 0.0;
+          else dh = h > 0.0 ? ((3.0 * xs - 6.0) * xs + 2.0) / 6.0 : 0.0;
+          double dd = rk * dh;
+          for (int q = 0; q < nt; ++q)
+            if (q != p) dd = dd * combinations(yy[KIN_RD_SPECIES(d, q) * B], KIN_RD_STOICH(d, q));
+          tmp[s * B] = tmp[s * B] + dl * dd;
+        }
+      }
+      double sr = 0.0;
+      for (int j = 0; j < N(); ++j) sr = sr + fabs(tmp[j * B]) * ewt[j * B];
+      nm = fmax(nm, sr / ewt[i * B]);
+    }
+    if (C) {  // the oracle's count: rre_jacobian, then the norm
+#pragma unroll 1
+      for (int k = 0; k < m; ++k) {
+        const int nt = KIN_RD_NTERMS(tab_rdesc(T, k));
+        flops += static_cast<uint64_t>(nt) * (4 + nt + 2 * static_cast<uint64_t>(tab_col_ptr(T, k + 1) - tab_col_ptr(T, k)));
+      }
+      flops += 2 * static_cast<uint64_t>(N()) * N() + N();
+    }
+    return nm;
   }
   template <bool C>
   __device__ bool lu_factor() {
@@ -213,8 +260,6 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   L.tmp = p;
   p += n * B;
   L.P = p;
-  p += n * n * B;
-  L.J2 = p;
   p += n * n * B;
   L.a = p;
   p += m * B;
@@ -313,17 +358,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
       have_p = L.template lu_factor<kCount>();
       return have_p;
     };
-    auto jac_norm = [&](const double* yy) {
-      L.template jacobian<kCount>(yy, L.J2);
-      double nm = 0.0;
-      for (int i = 0; i < n; ++i) {
-        double sr = 0.0;
-        for (int j = 0; j < n; ++j) sr = sr + fabs(L.J2[(i * n + j) * B]) * L.ewt[j * B];
-        nm = fmax(nm, sr / L.ewt[i * B]);
-      }
-      if (kCount) L.flops += 2 * static_cast<uint64_t>(n) * n + n;
-      return nm;
-    };
+    auto jac_norm = [&](const double* yy) { return L.template jac_norm_rows<kCount>(yy); };
     auto cm1 = [&](int q) { return L.tesco(0, q, 1) * L.elco(0, q, q); };
     auto cm2 = [&](int q) { return L.tesco(1, q, 1) * L.elco(1, q, q); };
 
@@ -563,7 +598,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
 // doubles of per-warp state (the pivot ints rounded up to whole doubles)
 __host__ __device__ __forceinline__ size_t lsoda_warp_doubles(const KinTables& T, const KinSweepDev& S) {
   const size_t n = static_cast<size_t>(T.n);
-  return (18 * n + 2 * n * n + T.m + S.n_axes) * kBlock + (n * kBlock + 1) / 2;
+  return (18 * n + n * n + T.m + S.n_axes) * kBlock + (n * kBlock + 1) / 2;
 }
 
 template <bool kCount, bool kGlobal, int kN>
@@ -575,7 +610,7 @@ __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ K
   constexpr int B = kBlock;
   const int tid = threadIdx.x, lane = tid & 31;
   const int n = T.n;
-  const size_t nd = static_cast<size_t>(18 * n + 2 * n * n + T.m + S.n_axes) * B;
+  const size_t nd = static_cast<size_t>(18 * n + n * n + T.m + S.n_axes) * B;
   // state in shared memory, or (kGlobal: models too large for it) in this
   // block's region of global memory, same layout
   double* sbase = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * lsoda_warp_doubles(T, S) : smem;
