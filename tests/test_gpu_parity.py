@@ -377,16 +377,16 @@ def test_c4_ode_tolerance(engine, oracle, rng):
 @pytest.mark.parametrize("rng", [(0, 512), (30000, 30256), (65536 - 256, 65536)])
 def test_c3_brusselator_lsoda_bit_exact(engine, oracle, rng):
     net, cfg = W.c3_config(side=256)
-    ref, got = both(engine, oracle, net, cfg, sim_range=rng)
-    assert_bit_exact(ref, got)
+    ref, got = both(engine, oracle, net, cfg, sim_range=rng, want_work=True)
+    assert_bit_exact(ref, got, work=True)  # work: the oracle's flop accounting, step for step
 
 
 def test_robertson_lsoda_bit_exact(engine, oracle):
     g = np.concatenate([[0.0], np.logspace(-4, 4, 33)])
     ic = IntegratorConfig(rel_tol=1e-6, abs_tol=1e-6, max_steps=200000)
     cfg = SweepConfig([SweepAxis("k3", [1e-3, 1e-2, 1e-1])], 1, Method(MethodKind.Lsoda, integrator=ic), 0, 1e4, g)
-    ref, got = both(engine, oracle, W.robertson(1e6), cfg)
-    assert_bit_exact(ref, got)
+    ref, got = both(engine, oracle, W.robertson(1e6), cfg, want_work=True)
+    assert_bit_exact(ref, got, work=True)
     assert got["meta"][:, 0].max() < 2000
 
 
