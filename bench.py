@@ -402,6 +402,18 @@ def bench_ours(args, world, rank, local):
                      "traffic": traffic, "traffic_source": traffic_src},
     }
     res["clocks"] = clk.summary()
+    # The same kernel against the HBM roofline, for completeness: its DRAM
+    # traffic (committed ncu capture) over the live kernel time, against the
+    # measured copy bandwidth in MEASURED_PEAKS.json.  Far below 1 by design —
+    # the per-simulation state lives in shared memory, only the trajectories
+    # stream out — which is why the binding roofline is FP64 / issue, not HBM.
+    pk = REPO / "MEASURED_PEAKS.json"
+    if traffic and pk.exists():
+        hbm = json.loads(pk.read_text()).get("hbm_gbs")
+        if hbm:
+            ach = traffic / (tau_avg_ms / 1e3) / 1e9
+            res["roofline"]["hbm"] = {"achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
     # Instruction-issue roofline of the same kernel: the warp-instructions one
     # launch of this (deterministic) workload executes, from the committed ncu
     # capture, over the live kernel time and the issue peak at the sampled SM
