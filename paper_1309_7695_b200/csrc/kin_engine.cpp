@@ -648,6 +648,7 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   KIN_CUDA(bf.grid.ensure(std::max<int>(G, 1)), "cudaMalloc grid");
   KinSweepDev SD;
   std::memset(&SD, 0, sizeof(SD));
+  SD.warp_lanes = 32;  // the launchers lower it for launches that cannot fill the GPU
   SD.kind = d->method.kind;
   SD.rng_mode = d->rng_mode;
   SD.tau = d->method.tau;

@@ -31,6 +31,7 @@
 
 #include "../../include/kin_abi.h"
 #include "kin_jit.h"
+#include "kin_launch.h"
 
 namespace kin {
 
@@ -421,14 +422,16 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
     const int cap = jit_knob("KIN_JIT_WARPS_PER_SM", 0);
     if (cap > 0 && cap < per_sm) per_sm = cap;
   }
-  const uint64_t blocks = (S.n_local + KIN_STOCH_BLOCK - 1) / KIN_STOCH_BLOCK;
   uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
   if (S.gstate && S.gstate_warps < resident) resident = S.gstate_warps;
+  KinSweepDev SW = S;
+  SW.warp_lanes = kin_warp_lanes(S.n_local, resident);
+  const uint64_t blocks = (S.n_local + SW.warp_lanes - 1) / SW.warp_lanes;
   const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   KinTables* Tp = const_cast<KinTables*>(&T);
-  KinSweepDev* Sp = const_cast<KinSweepDev*>(&S);
+  KinSweepDev* Sp = &SW;
   KinOutDev Oc = O;
   void* args[] = {Tp, Sp, &Oc, &counter, &ovf_flag};
   e = cudaLaunchKernel(fn, dim3(grid), dim3(KIN_STOCH_BLOCK), args, smem, stream);

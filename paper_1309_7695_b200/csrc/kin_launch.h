@@ -9,6 +9,15 @@
 
 namespace kin {
 
+// Simulations per warp for a persistent thread-per-simulation SSA/tau launch
+// over n_local simulations with `resident` warps: 32, or fewer when the launch
+// would leave resident warps empty (a sweep of 16,384 simulations fills only
+// 512 warps of 32; as 2,048 warps of 8 it fills 14 per SM).  It pays where the
+// lanes' control flow is data-dependent (C2: 162 -> 75 ms); the CLE and hybrid
+// kernels, with uniform work per simulation, keep full warps.  KIN_WARP_LANES
+// overrides (studies).
+int kin_warp_lanes(uint64_t n_local, uint64_t resident);
+
 // kin_stochastic.cu: SSA / tau-adaptive / tau-fixed, thread per simulation.
 // `counter` is a device word used by the persistent warps to fetch work;
 // int_state stores amounts as int32 (more resident simulations) and sets

@@ -26,7 +26,20 @@
 #include "kin_launch.h"
 #include "kin_stochastic_impl.cuh"
 
+#include <cstdlib>
+
 namespace kin {
+
+int kin_warp_lanes(uint64_t n_local, uint64_t resident) {
+  if (const char* v = std::getenv("KIN_WARP_LANES")) {
+    const int w = std::atoi(v);
+    if (w >= 1 && w <= 32) return w;
+  }
+  if (resident == 0) return 32;
+  const uint64_t w = (n_local + resident - 1) / resident;
+  return w >= 32 ? 32 : (w < 1 ? 1 : static_cast<int>(w));
+}
+
 
 namespace {
 
@@ -177,10 +190,10 @@ __global__ void __launch_bounds__(stoch::kBlock) cle_kernel(const __grid_constan
   double* x = smem + static_cast<size_t>(T.m + S.n_axes) * B + tid;
   for (;;) {
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(next, 32ULL);
+    if (lane == 0) base = atomicAdd(next, static_cast<unsigned long long>(S.warp_lanes));
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     if (base >= S.n_local) break;
-    const uint64_t s = base + lane;
+    const uint64_t s = lane < S.warp_lanes ? base + lane : S.n_local;  // lanes >= warp_lanes idle
     if (s < S.n_local) simulate_cle_one<kCount, kPhilox>(T, S, O, s, x, a, av);
     __syncwarp();
   }
@@ -251,13 +264,15 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t blocks = (S.n_local + kBlock - 1) / kBlock;
   uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
   if (S.gstate && resident > S.gstate_warps) resident = S.gstate_warps;
+  KinSweepDev SW = S;
+  SW.warp_lanes = kin_warp_lanes(S.n_local, resident);
+  const uint64_t blocks = (S.n_local + SW.warp_lanes - 1) / SW.warp_lanes;
   const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter, ovf_flag);
+  kern<<<grid, kBlock, smem, stream>>>(T, SW, O, counter, ovf_flag);
   return cudaGetLastError();
 }
 
@@ -289,12 +304,14 @@ cudaError_t launch_cle(const KinTables& T, const KinSweepDev& S, const KinOutDev
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlock, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  const uint64_t blocks = (S.n_local + kBlock - 1) / kBlock;
   const uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  KinSweepDev SW = S;
+  SW.warp_lanes = 32;  // a fixed number of steps per simulation: lanes stay converged, full warps issue least
+  const uint64_t blocks = (S.n_local + SW.warp_lanes - 1) / SW.warp_lanes;
   const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kBlock, smem, stream>>>(T, S, O, counter);
+  kern<<<grid, kBlock, smem, stream>>>(T, SW, O, counter);
   return cudaGetLastError();
 }
 

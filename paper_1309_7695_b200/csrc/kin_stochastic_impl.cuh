@@ -406,10 +406,10 @@ __device__ __forceinline__ void stochastic_body(const KinTables& T, const KinSwe
   XT* x = reinterpret_cast<XT*>(base + static_cast<size_t>(T.m + S.n_axes) * B) + tid;
   for (;;) {
     unsigned long long base = 0;
-    if (lane == 0) base = atomicAdd(next, 32ULL);
+    if (lane == 0) base = atomicAdd(next, static_cast<unsigned long long>(S.warp_lanes));
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     if (base >= S.n_local) break;
-    const uint64_t s = base + lane;
+    const uint64_t s = lane < S.warp_lanes ? base + lane : S.n_local;  // lanes >= warp_lanes idle
     if (s < S.n_local) simulate_one<Model, kCount, kPhilox, XT>(T, S, O, s, x, a, av, ovf_flag);
     __syncwarp();
   }

@@ -107,6 +107,11 @@ struct KinSweepDev {
   // grid never exceeds gstate_warps blocks.
   double* gstate;
   uint64_t gstate_warps;
+  // Simulations per warp of the thread-per-simulation kernels (1..32): fewer
+  // than 32 when a launch cannot fill the resident warps, so that more warps
+  // (each with fewer, less divergent lanes) share the latency.  Set by the
+  // launchers (kin_warp_lanes); the per-simulation results do not depend on it.
+  int32_t warp_lanes;
 };
 
 // Device outputs of one launch (local simulation index s in [0, n_local)).

@@ -430,3 +430,21 @@ def test_run_single_direct_seed(engine, oracle):
     d, keep = make_sweep_desc(net, cfg, seed_mode=abi.SEED_DIRECT)
     ref = oracle.sweep(net, d)
     assert np.array_equal(tr.samples, ref["traj"][0]) and tr.seed == 123456789
+
+
+@pytest.mark.parametrize("jit", ["0", "1"])
+def test_warp_lanes_invariance(engine, oracle, jit, monkeypatch):
+    """Simulations per warp (kin_warp_lanes: fewer than 32 for launches that
+    cannot fill the GPU) never change a result: 1, 7, 32 and the automatic
+    choice give the oracle's trajectories, table and JIT kernels alike."""
+    net, cfg = W.c2_config(points=4, runs=40)
+    monkeypatch.setenv("KIN_JIT", jit)
+    d, keep = make_sweep_desc(net, cfg)
+    ref = oracle.sweep(net, d, want_traj=True, want_work=True)
+    for w in ("1", "7", "32", None):
+        if w is None:
+            monkeypatch.delenv("KIN_WARP_LANES", raising=False)
+        else:
+            monkeypatch.setenv("KIN_WARP_LANES", w)
+        got = engine.sweep(net, cfg, want_traj=True, want_work=True)
+        assert_bit_exact(ref, got, work=True)

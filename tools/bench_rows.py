@@ -51,6 +51,8 @@ def main():
     rows = {}
     cases = {
         # sweeps large enough to fill the GPU (>= 65,536 simulations)
+        "tau_c1": (W.c1_config(MethodKind.TauAdaptive, side=256), 4096),
+        "tau_c2": (W.c2_config(), 2048),
         "ssa_c1": (W.c1_config(MethodKind.Ssa, side=256), 4096),
         "cle_c1": (W.c1_config(MethodKind.Cle, side=256), 4096),
         "hybrid_c1": (W.c1_config(MethodKind.Hybrid, side=256), 1024),

@@ -21,6 +21,8 @@ cfgs = {
     "c4_tau": W.c4_config(),
     "c4_ode": W.c4_config(method=MethodKind.Ode),
     "c1_tau": W.c1_config(),
+    "c1_tau128": W.c1_config(side=128),
+    "c1_ssa128": W.c1_config(MethodKind.Ssa, side=128),
     "c2": W.c2_config(),
     "c3_ode": W.c3_config(method=MethodKind.Ode),
     "c3_lsoda": W.c3_config(),
