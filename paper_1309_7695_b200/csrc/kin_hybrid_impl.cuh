@@ -16,9 +16,9 @@
 // reuses k2's slot and yn reuses ys's (a72 = e2 = d2 = 0: k2 is dead once
 // stage 6 is formed, ys once yn is); the dense-output coefficients r1..r5 are
 // formed on demand from y, yn, k1, k3..k7 with the oracle's expressions, so
-// they round identically.  The six stages run as one loop over a coefficient
-// table so the RHS (propensities + fast/slow sums) is inlined once, not six
-// times (instruction-cache footprint).
+// they round identically.  The six stages run as one loop (each stage's input
+// straight-line behind a warp-uniform switch) so the RHS (propensities +
+// fast/slow sums) is inlined once, not six times (instruction-cache footprint).
 #pragma once
 #include "kin_launch.h"
 #include "kin_pmath.cuh"
@@ -50,15 +50,6 @@ constexpr double c_d1 = -12715105075.0 / 11282082432.0, c_d3 = 87487479700.0 / 3
 constexpr double kSafe = 0.9, kFacMinInv = 5.0, kFacMaxInv = 0.1;
 constexpr double kBeta = 0.04, kExpo1 = 0.2 - kBeta * 0.75;
 constexpr int kVecs = 8;
-// stage s (0..5) input: y + h * sum_k c_stage[s][k] k_{k+1}, summed left to right
-// (stage 7 skips the zero a72)
-__constant__ double c_stage[6][6] = {{c_a21, 0, 0, 0, 0, 0},
-                                     {c_a31, c_a32, 0, 0, 0, 0},
-                                     {c_a41, c_a42, c_a43, 0, 0, 0},
-                                     {c_a51, c_a52, c_a53, c_a54, 0, 0},
-                                     {c_a61, c_a62, c_a63, c_a64, c_a65, 0},
-                                     {c_a71, 0, c_a73, c_a74, c_a75, c_a76}};
-
 __device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }  // std::min
 
@@ -109,6 +100,42 @@ struct Hybrid {
 };
 
 enum { Y = 0, K1, K2, K3, K4, K5, K6, YS, K7 = K2, YN = YS };
+
+// Stage ST's input y + h * sum_k a_{ST+2,k+1} k_{k+1} as straight-line code
+// (coefficients folded, the zero a72 skipped), summed left to right like the
+// oracle; one instantiation per stage behind a warp-uniform switch, so the
+// RHS call after it stays a single site.
+__host__ __device__ constexpr double stage_coef(int st, int k) {
+  return st == 0 ? c_a21
+       : st == 1 ? (k == 0 ? c_a31 : c_a32)
+       : st == 2 ? (k == 0 ? c_a41 : k == 1 ? c_a42 : c_a43)
+       : st == 3 ? (k == 0 ? c_a51 : k == 1 ? c_a52 : k == 2 ? c_a53 : c_a54)
+       : st == 4 ? (k == 0 ? c_a61 : k == 1 ? c_a62 : k == 2 ? c_a63 : k == 3 ? c_a64 : c_a65)
+                 : (k == 0 ? c_a71 : k == 1 ? 0.0 : k == 2 ? c_a73 : k == 3 ? c_a74 : k == 4 ? c_a75 : c_a76);
+}
+template <int ST, int K>
+__device__ __forceinline__ double stage_sum(double acc, double kv0, double kv1, double kv2, double kv3, double kv4) {
+  if constexpr (K > ST) {
+    return acc;
+  } else if constexpr (ST == 5 && K == 1) {  // a72 = 0: not a term of the oracle's sum
+    return stage_sum<ST, K + 1>(acc, kv0, kv1, kv2, kv3, kv4);
+  } else {
+    constexpr double c = stage_coef(ST, K);
+    const double kv = K == 1 ? kv0 : K == 2 ? kv1 : K == 3 ? kv2 : K == 4 ? kv3 : kv4;  // k_{K+1}
+    return stage_sum<ST, K + 1>(acc + c * kv, kv0, kv1, kv2, kv3, kv4);
+  }
+}
+template <int ST, class HT>
+__device__ __forceinline__ void stage_input(const HT& H, int n1, double hh) {
+  for (int i = 0; i < n1; ++i) {
+    constexpr double c0 = stage_coef(ST, 0);
+    const double acc0 = c0 * H.v(K1, i);
+    const double acc = stage_sum<ST, 1>(acc0, ST >= 1 ? H.v(K2, i) : 0.0, ST >= 2 ? H.v(K3, i) : 0.0,
+                                        ST >= 3 ? H.v(K4, i) : 0.0, ST >= 4 ? H.v(K5, i) : 0.0,
+                                        ST >= 5 ? H.v(K6, i) : 0.0);
+    H.v(YS, i) = H.v(Y, i) + hh * acc;  // yn for ST = 5 (same slot)
+  }
+}
 
 // Dense output of the accepted step for one component (the oracle's r1..r5).
 struct Dense5 {
@@ -221,11 +248,13 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         if (!(hh > 0.0) || t + hh == t) { status = KIN_SIM_STEP_UNDERFLOW; break; }
 #pragma unroll 1
         for (int st = 0; st < 6; ++st) {
-          for (int i = 0; i < n1; ++i) {
-            double acc = c_stage[st][0] * H.v(K1, i);
-            for (int k = 1; k <= st; ++k)
-              if (st != 5 || k != 1) acc = acc + c_stage[st][k] * H.v(K1 + k, i);
-            H.v(YS, i) = H.v(Y, i) + hh * acc;  // yn for st = 5 (same slot)
+          switch (st) {
+            case 0: stage_input<0>(H, n1, hh); break;
+            case 1: stage_input<1>(H, n1, hh); break;
+            case 2: stage_input<2>(H, n1, hh); break;
+            case 3: stage_input<3>(H, n1, hh); break;
+            case 4: stage_input<4>(H, n1, hh); break;
+            default: stage_input<5>(H, n1, hh); break;
           }
           H.rhs(YS, st == 5 ? K7 : K2 + st);
         }
