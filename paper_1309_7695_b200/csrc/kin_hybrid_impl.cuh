@@ -84,15 +84,18 @@ struct Hybrid {
       for (int p = p0; p < p1; ++p) {
         const uint32_t e = tab_row(T, p);
         const int j = KIN_NU_INDEX(e);
-        if (!slow(j)) acc = acc + static_cast<double>(KIN_NU_DELTA(e)) * sm.a[j * kBlock];
+        const double t = acc + static_cast<double>(KIN_NU_DELTA(e)) * sm.a[j * kBlock];
+        acc = slow(j) ? acc : t;  // a select, not a branch per entry (same value as the oracle's skip)
       }
       v(fv, i) = acc;
       if (kCount) flops += 2 * static_cast<uint64_t>(p1 - p0);
     }
     double g = 0.0;
 #pragma unroll 1
-    for (int j = 0; j < m; ++j)
-      if (slow(j)) g = g + sm.a[j * kBlock];
+    for (int j = 0; j < m; ++j) {
+      const double t = g + sm.a[j * kBlock];
+      g = slow(j) ? t : g;
+    }
     v(fv, N()) = g;
     if (kCount) flops += static_cast<uint64_t>(m);
   }
