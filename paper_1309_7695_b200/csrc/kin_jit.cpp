@@ -143,6 +143,20 @@ std::string generate_policy(const JitModel& m) {
   // and overflow the instruction cache on larger models, so above
   // kInlineTauMaxSpecies the species are walked by a warp-uniform, non-unrolled
   // loop whose switch holds only each species' mu/sigma^2 sums (one tau_bound).
+  // mu += d*a_j, s2 += d^2*a_j.  For d = +-1 the products are exactly +-a_j,
+  // and an intrinsic multiply by 1.0 is not folded: emit the add / subtract
+  // (x + (-a) and x - a are the same IEEE operation), so each unit term costs
+  // two DADDs instead of two DMUL + DADD pairs — bit-identical sums.
+  auto tau_terms = [&](int d, int j) {
+    std::ostringstream t;
+    const std::string aj = "a[" + std::to_string(j) + " * B]";
+    if (d == 1) t << " mu = __dadd_rn(mu, " << aj << "); s2 = __dadd_rn(s2, " << aj << ");";
+    else if (d == -1) t << " mu = __dsub_rn(mu, " << aj << "); s2 = __dadd_rn(s2, " << aj << ");";
+    else
+      t << " mu = __dadd_rn(mu, __dmul_rn(" << dlit(d) << ", " << aj << "));"
+        << " s2 = __dadd_rn(s2, __dmul_rn(" << dlit(static_cast<double>(d) * d) << ", " << aj << "));";
+    return t.str();
+  };
   int n_act = 0;
   for (int i = 0; i < m.n; ++i) n_act += m.row_ptr[i] != m.row_ptr[i + 1];
   o << "  template <bool kCount> __device__ __forceinline__ double select_tau(double eps, uint64_t& flops) const {\n"
@@ -154,8 +168,7 @@ std::string generate_policy(const JitModel& m) {
       o << "    { double mu = 0.0, s2 = 0.0;";
       for (int p = p0; p < p1; ++p) {
         const int j = m.row_reaction[p], d = m.row_delta[p];
-        o << " mu = __dadd_rn(mu, __dmul_rn(" << dlit(d) << ", a[" << j << " * B]));"
-          << " s2 = __dadd_rn(s2, __dmul_rn(" << dlit(static_cast<double>(d) * d) << ", a[" << j << " * B]));";
+        o << tau_terms(d, j);
       }
       o << "\n      if (kCount) flops += " << 4 * (p1 - p0) << ";\n"
         << "      if (!(mu == 0.0 && s2 == 0.0)) tau = tau_bound<kCount>(tau, eps, xv(" << i << "), " << dlit(m.g[i])
@@ -171,8 +184,7 @@ std::string generate_policy(const JitModel& m) {
       o << "        case " << q++ << ": sp = " << i << "; g = " << dlit(m.g[i]) << "; nt = " << 4 * (p1 - p0) << ";";
       for (int p = p0; p < p1; ++p) {
         const int j = m.row_reaction[p], d = m.row_delta[p];
-        o << " mu = __dadd_rn(mu, __dmul_rn(" << dlit(d) << ", a[" << j << " * B]));"
-          << " s2 = __dadd_rn(s2, __dmul_rn(" << dlit(static_cast<double>(d) * d) << ", a[" << j << " * B]));";
+        o << tau_terms(d, j);
       }
       o << " break;\n";
     }
