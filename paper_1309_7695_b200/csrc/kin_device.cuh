@@ -136,8 +136,10 @@ struct Xoshiro {
     return out;
   }
   // ((x >> 11) + 0.5) * 2^-53: exact in double, identical on every platform.
-  __device__ __forceinline__ double uniform() {
-    return __dmul_rn(__dadd_rn(static_cast<double>(next() >> 11), 0.5), 0x1.0p-53);
+  __device__ __forceinline__ double uniform() { return uniform_from_bits(bits53()); }
+  __device__ __forceinline__ uint64_t bits53() { return next() >> 11; }
+  __device__ __forceinline__ static double uniform_from_bits(uint64_t b) {
+    return __dmul_rn(__dadd_rn(static_cast<double>(b), 0.5), 0x1.0p-53);
   }
 };
 
@@ -173,14 +175,18 @@ struct PhiloxSite {
   __device__ __forceinline__ PhiloxSite(uint64_t seed, uint64_t event, uint32_t site)
       : k0(static_cast<uint32_t>(seed)), k1(static_cast<uint32_t>(seed >> 32)), slot(site),
         ev_lo(static_cast<uint32_t>(event)), ev_hi(static_cast<uint32_t>(event >> 32)), blk(0), half(0) {}
-  __device__ __forceinline__ double uniform() {
+  __device__ __forceinline__ uint64_t bits53() {
     if (half == 0) philox_block(k0, k1, slot, ev_lo, ev_hi, blk, buf);
     const uint64_t x = half == 0 ? (static_cast<uint64_t>(buf[1]) << 32 | buf[0])
                                  : (static_cast<uint64_t>(buf[3]) << 32 | buf[2]);
     if (half == 1) ++blk;
     half ^= 1;
-    return __dmul_rn(__dadd_rn(static_cast<double>(x >> 11), 0.5), 0x1.0p-53);
+    return x >> 11;
   }
+  __device__ __forceinline__ static double uniform_from_bits(uint64_t b) {
+    return __dmul_rn(__dadd_rn(static_cast<double>(b), 0.5), 0x1.0p-53);
+  }
+  __device__ __forceinline__ double uniform() { return uniform_from_bits(bits53()); }
 };
 
 // mean / k, correctly rounded.  Division by a power of two is exact scaling, so
@@ -220,21 +226,22 @@ template <bool kCount, class Rng>
 __device__ __forceinline__ uint64_t poisson(Rng& rng, double mean, uint64_t& flops, const double* lgamma_tab) {
   if (!(mean > 0.0)) return 0;
   if (mean < 10.0) {
-    const double u = rng.uniform();
+    const uint64_t ub = rng.bits53();  // u = ((ub + 0.5) * 2^-53), formed in double only if needed
     // Fast decision path (returns exactly the k of the reference algorithm):
     // search an approximate CDF c'_k in FP32.  Error budget relative to the
     // reference's c_k (whose own rounding, (k+2)*2^-52, is negligible):
     //   p'_0 = __expf(-float(mean)): <= 13 float ulp (1.55e-6) + mean*2^-24
     //          (<= 6e-7) = 2.15e-6 for mean in (0,10);
     //   each recursion step p' *= float(mean)*rcp(k): 4 roundings, <= 2.4e-7;
-    //   each cumulative add: <= 6e-8;  float(u): <= 6e-8.
-    // So |c'_k - c_k| <= (2.15e-6 + 3e-7*k) c_k <= 1.42e-5 c_k for k <= 40, and a
+    //   each cumulative add: <= 6e-8;  u' = fma(float(ub), 2^-53, 2^-54) in FP32
+    //   (the 53 bits rounded to 24, one FMA rounding): <= 1.2e-7 relative to u.
+    // So |c'_k - c_k| <= (2.25e-6 + 3e-7*k) c_k <= 1.43e-5 c_k for k <= 40, and a
     // guard G = 4e-5 (> 2x that) makes "u < c'_k(1-G) and u > c'_{k-1}(1+G)"
     // imply the reference stops at exactly k.  Otherwise (probability ~1e-4 per
     // draw) run the exact algorithm below.
     {
       constexpr float G = 4e-5f;
-      const float uf = static_cast<float>(u);
+      const float uf = __fmaf_rn(__ull2float_rn(ub), 0x1p-53f, 0x1p-54f);
       const float mf = static_cast<float>(mean);
       float pf = __expf(-mf);
       float cf = pf, cprev = 0.0f;
@@ -250,6 +257,7 @@ __device__ __forceinline__ uint64_t poisson(Rng& rng, double mean, uint64_t& flo
         return static_cast<uint64_t>(kk);
       }
     }
+    const double u = Rng::uniform_from_bits(ub);
     double p = exp(-mean);
     double c = p;
     uint64_t k = 0;
