@@ -203,12 +203,13 @@ __device__ __forceinline__ double div_small(double mean, int k) {
 
 // draw_poisson (rng.cpp:68-109): inversion below mean 10, Hormann PTRS above.
 // `flops` receives the algorithmic op count (same accounting as the oracle).
-// correctly rounded float reciprocals 1/k, k = 1..40 (index 0 unused)
-__device__ __constant__ float c_rcp40[41] = {
+// correctly rounded float reciprocals 1/k, k = 1..40 (index 0 unused, 41 a pad)
+__device__ __constant__ float c_rcp40[42] = {
     0.0f, 1.0f / 1, 1.0f / 2, 1.0f / 3, 1.0f / 4, 1.0f / 5, 1.0f / 6, 1.0f / 7, 1.0f / 8, 1.0f / 9, 1.0f / 10,
     1.0f / 11, 1.0f / 12, 1.0f / 13, 1.0f / 14, 1.0f / 15, 1.0f / 16, 1.0f / 17, 1.0f / 18, 1.0f / 19, 1.0f / 20,
     1.0f / 21, 1.0f / 22, 1.0f / 23, 1.0f / 24, 1.0f / 25, 1.0f / 26, 1.0f / 27, 1.0f / 28, 1.0f / 29, 1.0f / 30,
-    1.0f / 31, 1.0f / 32, 1.0f / 33, 1.0f / 34, 1.0f / 35, 1.0f / 36, 1.0f / 37, 1.0f / 38, 1.0f / 39, 1.0f / 40};
+    1.0f / 31, 1.0f / 32, 1.0f / 33, 1.0f / 34, 1.0f / 35, 1.0f / 36, 1.0f / 37, 1.0f / 38, 1.0f / 39, 1.0f / 40,
+    0.0f};
 
 // lgamma(z) for z >= KIN_LGAMMA_N + 1 by the Stirling series (terms to z^-7;
 // truncation < 1e-25 there, i.e. within an ulp like libm's lgamma) — far
@@ -246,11 +247,25 @@ __device__ __forceinline__ uint64_t poisson(Rng& rng, double mean, uint64_t& flo
       float pf = __expf(-mf);
       float cf = pf, cprev = 0.0f;
       int kk = 0;
+      // Two terms per trip (the same float operations as one per trip): the
+      // second term's multiply and add overlap the first one's test, halving
+      // the loop's branch + dependent-compare chain.  c_rcp40[41] is a pad.
       while (uf > cf * (1.0f + G) && kk < 40) {
-        ++kk;
-        pf = pf * (mf * c_rcp40[kk]);
-        cprev = cf;
-        cf = cf + pf;
+        const float p1 = pf * (mf * c_rcp40[kk + 1]);
+        const float p2 = p1 * (mf * c_rcp40[kk + 2]);
+        const float c1 = cf + p1;
+        const float c2 = c1 + p2;
+        if (!(uf > c1 * (1.0f + G)) || kk + 1 >= 40) {
+          kk += 1;
+          pf = p1;
+          cprev = cf;
+          cf = c1;
+          break;
+        }
+        kk += 2;
+        pf = p2;
+        cprev = c1;
+        cf = c2;
       }
       if (kk < 40 && uf < cf * (1.0f - G) && (kk == 0 || uf > cprev * (1.0f + G))) {
         if (kCount) flops += 3 + 3 * static_cast<uint64_t>(kk);
