@@ -188,12 +188,23 @@ template <class Model>
 __device__ __forceinline__ int ssa_select(const Model& sm, int M, double a0, double u2) {
   const double target = __dmul_rn(u2, a0);
   double c = 0.0;
-  int sel = -1, last = -1;
-  for (int j = 0; j < M; ++j) {
+  int sel = -1, last = -1, j = 0;
+  // two reactions per trip (same additions in the same order): both loads and
+  // the second sum issue before the first test
+  for (; j + 1 < M; j += 2) {
+    const double a1 = sm.aval(j), a2 = sm.aval(j + 1);
+    const double c1 = __dadd_rn(c, a1);
+    const double c2 = __dadd_rn(c1, a2);
+    if (a1 > 0.0) last = j;
+    if (c1 > target) { sel = j; break; }
+    if (a2 > 0.0) last = j + 1;
+    if (c2 > target) { sel = j + 1; break; }
+    c = c2;
+  }
+  if (sel < 0 && j < M) {
     const double aj = sm.aval(j);
     if (aj > 0.0) last = j;
-    c = __dadd_rn(c, aj);
-    if (c > target) { sel = j; break; }
+    if (__dadd_rn(c, aj) > target) sel = j;
   }
   return sel < 0 ? last : sel;
 }
