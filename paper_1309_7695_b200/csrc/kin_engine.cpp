@@ -771,6 +771,10 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
         KIN_CUDA(bf.gstate.ensure(cap * per), "cudaMalloc simulation state");
         SD.gstate = bf.gstate.p;
         SD.gstate_warps = cap;
+        // amounts in shared memory, propensities in global (JIT kernel only;
+        // it applies the size rule); KIN_GSTATE_SPLIT=0 keeps all state global
+        SD.gstate_x_smem = 1;
+        if (const char* v = std::getenv("KIN_GSTATE_SPLIT")) SD.gstate_x_smem = std::atoi(v) != 0;
       }
       KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), bf.st), "memset");
       bool used = false;

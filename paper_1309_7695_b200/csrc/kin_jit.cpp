@@ -244,12 +244,12 @@ const char* const kNvrtcOpts[5] = {"--gpu-architecture=sm_100a", "-fmad=false", 
 
 // NVRTC: policy source -> sm_100a cubin.  Returns false with the log on error.
 bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_state, bool global_state,
-                   std::vector<char>* cubin, std::string* log) {
+                   bool smem_x, std::vector<char>* cubin, std::string* log) {
   std::string src = "#include \"kin_stochastic_impl.cuh\"\n" + policy +
-                    "extern \"C\" __global__ void __launch_bounds__(KIN_STOCH_BLOCK) kin_jit_stoch(\n"
+                    "extern \"C\" __global__ void __launch_bounds__(KIN_STOCH_BLOCK, KMINB_) kin_jit_stoch(\n"
                     "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
                     "    unsigned long long* __restrict__ next, int* ovf) {\n"
-                    "  kin::stoch::stochastic_body<kin::stoch::GenModel<XT_>, KCOUNT_, KPHILOX_, XT_, KGLOBAL_>(T, S, O, next, ovf);\n"
+                    "  kin::stoch::stochastic_body<kin::stoch::GenModel<XT_>, KCOUNT_, KPHILOX_, XT_, KGLOBAL_, KSMEMX_>(T, S, O, next, ovf);\n"
                     "}\n";
   std::vector<const char*> hs, hn;
   for (const auto& h : kJitHeaders) {
@@ -266,8 +266,12 @@ bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_
   const std::string d_c = std::string("-DKCOUNT_=") + (count ? "true" : "false");
   const std::string d_p = std::string("-DKPHILOX_=") + (philox ? "true" : "false");
   const std::string d_g = std::string("-DKGLOBAL_=") + (global_state ? "true" : "false");
+  const std::string d_x = std::string("-DKSMEMX_=") + (smem_x ? "true" : "false");
+  // split layout: its 16 KB of shared memory per warp allows 13 resident warps
+  // per SM; ask the register allocator for that many (development knob)
+  const std::string d_b = "-DKMINB_=" + std::to_string(smem_x ? jit_knob("KIN_JIT_SPLIT_MINB", 1) : 1);
   const char* opts[] = {kNvrtcOpts[0], kNvrtcOpts[1], kNvrtcOpts[2], kNvrtcOpts[3], kNvrtcOpts[4],
-                        d_xt.c_str(),  d_c.c_str(),   d_p.c_str(),   d_g.c_str()};
+                        d_xt.c_str(),  d_c.c_str(),   d_p.c_str(),   d_g.c_str(),   d_x.c_str(), d_b.c_str()};
   const nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
   size_t log_size = 0;
   nvrtcGetProgramLogSize(prog, &log_size);
@@ -352,13 +356,14 @@ void write_file(const std::string& p, const std::vector<char>& data) {
 }
 
 std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool philox, bool int_state,
-                                   bool global_state) {
+                                   bool global_state, bool smem_x) {
   auto jk = std::make_shared<JitKernel>();
   std::vector<char> cubin;
   const std::string path =
-      cache_path(policy + (count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") + (global_state ? "G" : "S"));
+      cache_path(policy + (count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
+                 (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S"));
   if (!read_file(path, &cubin)) {
-    if (!nvrtc_compile(policy, count, philox, int_state, global_state, &cubin, &jk->log)) {
+    if (!nvrtc_compile(policy, count, philox, int_state, global_state, smem_x, &cubin, &jk->log)) {
       if (jit_debug()) std::fprintf(stderr, "[kin_jit] compile failed:\n%s\n", jk->log.c_str());
       return jk;
     }
@@ -380,7 +385,7 @@ std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool p
 
 bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log) {
   std::vector<char> cubin;
-  return nvrtc_compile(generate_policy(model), count, philox, int_state, false, &cubin, log);
+  return nvrtc_compile(generate_policy(model), count, philox, int_state, false, false, &cubin, log);
 }
 
 // KIN_JIT=0: never; KIN_JIT=1: always; unset: launches of >= 8,192
@@ -403,8 +408,12 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
   const bool philox = S.rng_mode == KIN_RNG_PHILOX;
   const std::string policy = generate_policy(model);
   const bool global_state = S.gstate != nullptr;
+  // split layout (x[] in shared memory, a[] + av[] global) when x[] takes at
+  // most 16 KB per warp (>= 13 resident warps/SM): C5 tau 1075 -> 906 ms
+  const size_t smem_x_bytes = static_cast<size_t>(T.n) * KIN_STOCH_BLOCK * (int_state ? sizeof(int32_t) : sizeof(double));
+  const bool smem_x = global_state && S.gstate_x_smem != 0 && smem_x_bytes <= 16 * 1024;
   const std::string key = policy + (count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
-                          (global_state ? "G" : "S");
+                          (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S");
   std::shared_ptr<JitKernel> jk;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -412,14 +421,13 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
     if (it != g_cache.end()) {
       jk = it->second;
     } else {
-      jk = compile(policy, count, philox, int_state, global_state);
+      jk = compile(policy, count, philox, int_state, global_state, smem_x);
       g_cache[key] = jk;
     }
   }
   if (!jk->ok) return cudaSuccess;  // caller falls back to the table-driven kernel
-  const size_t smem = S.gstate ? 0
-                              : static_cast<size_t>(T.m + S.n_axes) * KIN_STOCH_BLOCK * sizeof(double) +
-                                    static_cast<size_t>(T.n) * KIN_STOCH_BLOCK * (int_state ? sizeof(int32_t) : sizeof(double));
+  const size_t smem = S.gstate ? (smem_x ? smem_x_bytes : 0)
+                              : static_cast<size_t>(T.m + S.n_axes) * KIN_STOCH_BLOCK * sizeof(double) + smem_x_bytes;
   if (smem > 227 * 1024) return cudaSuccess;
   const void* fn = reinterpret_cast<const void*>(jk->kern);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -392,15 +392,17 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   if (kCount && O.work) O.work[s] = flops;
 }
 
-// doubles of per-warp state: a[M] + av[axes] doubles and x[N] of XT, per lane
-template <class XT>
+// doubles of per-warp global state: a[M] + av[axes] doubles and (unless the
+// amounts live in shared memory) x[N] of XT, per lane
+template <class XT, bool kSmemX = false>
 __host__ __device__ __forceinline__ size_t gstate_warp_doubles(const KinTables& T, const KinSweepDev& S) {
-  return static_cast<size_t>(T.m + S.n_axes) * kBlock + (static_cast<size_t>(T.n) * sizeof(XT) + 7) / 8 * kBlock;
+  return static_cast<size_t>(T.m + S.n_axes) * kBlock +
+         (kSmemX ? 0 : (static_cast<size_t>(T.n) * sizeof(XT) + 7) / 8 * kBlock);
 }
 
 // Kernel body shared by the table-driven kernel (kin_stochastic.cu) and the
 // per-model JIT kernels (kin_jit.cpp).  Block = one warp; persistent warps.
-template <class Model, bool kCount, bool kPhilox, class XT, bool kGlobal = false>
+template <class Model, bool kCount, bool kPhilox, class XT, bool kGlobal = false, bool kSmemX = false>
 __device__ __forceinline__ void stochastic_body(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
                                                 unsigned long long* __restrict__ next, int* ovf_flag) {
   extern __shared__ double smem[];
@@ -411,10 +413,13 @@ __device__ __forceinline__ void stochastic_body(const KinTables& T, const KinSwe
   // layout, still coalesced; L1/L2-cached)
   // (a compile-time choice: with one pointer for both, every access would be a
   // generic load/store instead of LDS/STS)
-  double* base = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * gstate_warp_doubles<XT>(T, S) : smem;
+  // (kSmemX, large models: x[] alone in shared memory — the leap updates and
+  // propensity reads hit LDS/STS — and a[] + av[] in global memory)
+  double* base = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * gstate_warp_doubles<XT, kSmemX>(T, S) : smem;
   double* a = base + tid;
   double* av = base + static_cast<size_t>(T.m) * B + tid;
-  XT* x = reinterpret_cast<XT*>(base + static_cast<size_t>(T.m + S.n_axes) * B) + tid;
+  XT* x = (kGlobal && kSmemX) ? reinterpret_cast<XT*>(smem) + tid
+                              : reinterpret_cast<XT*>(base + static_cast<size_t>(T.m + S.n_axes) * B) + tid;
   for (;;) {
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(next, static_cast<unsigned long long>(S.warp_lanes));

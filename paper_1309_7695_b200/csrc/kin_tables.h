@@ -112,6 +112,10 @@ struct KinSweepDev {
   // (each with fewer, less divergent lanes) share the latency.  Set by the
   // launchers (kin_warp_lanes); the per-simulation results do not depend on it.
   int32_t warp_lanes;
+  // Global-memory state only: nonzero keeps the amounts x[] in shared memory
+  // (the JIT kernel's split layout); the propensity cache stays in gstate.
+  // Read by the launchers on the host.
+  int32_t gstate_x_smem;
 };
 
 // Device outputs of one launch (local simulation index s in [0, n_local)).

@@ -157,6 +157,23 @@ def test_table_kernel_global_state_bit_exact(engine, oracle, gstate, monkeypatch
     assert_bit_exact(ref, got, work=True)
 
 
+@pytest.mark.parametrize("split", ["0", "1"])
+def test_jit_global_state_layouts_bit_exact(engine, oracle, split, monkeypatch):
+    """JIT kernel with global-memory state: all of it global, or the split layout
+    (amounts in shared memory, propensity cache global); same results, both RNG
+    modes, with work counts."""
+    monkeypatch.setenv("KIN_JIT", "1")
+    monkeypatch.setenv("KIN_GSTATE", "1")
+    monkeypatch.setenv("KIN_GSTATE_SPLIT", split)
+    net, cfg = W.c4_config()
+    for rng in (abi.RNG_COMPAT, abi.RNG_PHILOX):
+        ref, got = both(engine, oracle, net, cfg, sim_range=(3000, 3256), want_work=True, rng_mode=rng)
+        assert_bit_exact(ref, got, work=True)
+    net, cfg = W.c5_config()
+    ref, got = both(engine, oracle, net, cfg, sim_range=(2000, 2064))
+    assert_bit_exact(ref, got)
+
+
 def test_int32_amount_overflow_retry(engine, oracle):
     """Amounts are kept as int32 on the device when they start far inside the
     range; a run that leaves it is transparently re-run with double amounts."""

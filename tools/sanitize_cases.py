@@ -17,7 +17,7 @@ sys.path.insert(0, ".")
 from paper_1309_7695_b200 import Engine, abi, workloads as W  # noqa: E402
 from paper_1309_7695_b200.ensemble import Method, MethodKind  # noqa: E402
 
-KNOBS = ("KIN_JIT", "KIN_INT_STATE", "KIN_GSTATE", "KIN_HYBRID_GSTATE", "KIN_LSODA_GSTATE", "KIN_GROUP_LANES")
+KNOBS = ("KIN_JIT", "KIN_INT_STATE", "KIN_GSTATE", "KIN_GSTATE_SPLIT", "KIN_HYBRID_GSTATE", "KIN_LSODA_GSTATE", "KIN_GROUP_LANES")
 
 
 def run(eng, label, net, cfg, env=None, **kw):
@@ -40,6 +40,8 @@ def main():
         run(eng, f"tau table gstate {tag}", *c1, {"KIN_JIT": "0", "KIN_GSTATE": "1"}, rng_mode=rng)
         run(eng, f"tau jit {tag}", *c1, {"KIN_JIT": "1"}, rng_mode=rng, want_work=True)
         run(eng, f"tau jit gstate {tag}", *c1, {"KIN_JIT": "1", "KIN_GSTATE": "1"}, rng_mode=rng)
+        run(eng, f"tau jit gstate all-global {tag}", *c1, {"KIN_JIT": "1", "KIN_GSTATE": "1", "KIN_GSTATE_SPLIT": "0"},
+            rng_mode=rng)
     for lanes in ("1", "4", "16"):
         run(eng, f"tau philox lane group {lanes}", *c1, {"KIN_GROUP_LANES": lanes}, rng_mode=abi.RNG_PHILOX)
     net, cfg = W.c4_config()
