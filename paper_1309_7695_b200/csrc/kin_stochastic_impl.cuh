@@ -329,10 +329,15 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     // streams are swapped by value so they stay in registers.
     long long sign = 1;
     for (;;) {
+      // a_{j+1} is loaded while reaction j draws (global-memory state: hides
+      // the load latency behind the Poisson draw)
+      double a_next = sm.aval(0);
 #pragma unroll 1
       for (int j = 0; j < M; ++j) {
         uint64_t k, fl = 0;
-        const double mean = __dmul_rn(sm.aval(j), tau);
+        const double aj = a_next;
+        if (j + 1 < M) a_next = sm.aval(j + 1);
+        const double mean = __dmul_rn(aj, tau);
         if (kPhilox) {
           PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
           k = poisson<kCount>(src, mean, fl, S.lgamma_tab);
