@@ -4,21 +4,35 @@
 BASELINE.json metric: "simulations/sec for N-sim parameter sweep at 1/2/4/8
 B200 vs CPU ref (all cores)".  Workload (BASELINE.json
 configs[3]): the 33-species x 39-reaction Ras-scale synthetic model swept over
-two rate constants on a 256x256 log grid (65,536 points, 1 run each), every
-point simulated with BOTH reference methods: tau-adaptive tau-leaping with the
-SSA fallback (compat RNG: bit-exact with the reference stream) and the
-Dopri5 RRE integration (Method::Ode).  One step = both sweeps = 131,072
-simulations per GPU (weak scaling: rank r simulates sweep points
-[r*65536, (r+1)*65536) of a 256N x 256 grid).
+two rate constants on a log grid, every point simulated with BOTH reference
+methods: tau-adaptive tau-leaping with the SSA fallback (compat RNG: bit-exact
+with the reference stream) and the Dopri5 RRE integration (Method::Ode).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--scaling weak|strong]
+
+Scaling: weak (default) = a 256N x 256 grid, 65,536 points per GPU; strong =
+the north star's 65,536-point sweep split over the N GPUs.  One step = the
+sweep by both methods (2 simulations per point).
+
+Multi-GPU, two launch forms, one partitioner (kin_sweep_plan: every device
+gets ONE launch over an interleaved point set — points d, d+N, d+2N, ... — via
+a device-side index map; no collective on the data path):
+  * torchrun (one process per GPU): rank r passes the descriptor shard (r, N);
+  * plain `--gpus N` in one process: an engine context over devices 0..N-1
+    (kin_sweep_launch with slot -1); fails if fewer than N GPUs are visible.
 
 Arms:
-  ours       value = device-resident throughput (kin_sweep_launch: simulation +
-             per-point statistics kernels; inputs already in HBM; CUDA events on
-             the engine stream; L2 flushed between steps); e2e = kin_sweep_run
-             with host buffers (H2D of the sweep tables, D2H of every
-             simulation's time series + TrajectoryMeta + status) on the host clock.
+  ours       value = device-resident throughput (kin_sweep_launch, inputs in
+             HBM, CUDA events on the engine streams, max over devices/ranks, L2
+             flushed between steps; the step produces per-simulation
+             trajectories + TrajectoryMeta + status — no R=1 statistics
+             copies); e2e = kin_sweep_submit/kin_sweep_wait with pinned host
+             buffers (H2D of the sweep tables, D2H of every simulation's time
+             series + meta + status).  After timing, the timed step's own
+             outputs are compared with the CPU oracle over the WHOLE sweep
+             (N=1): bit-exact for tau-leaping, 10x tolerance for Dopri5
+             ("parity" in the JSON line).
   reference  the CPU oracle (C++ restatement of the reference path; the
              reference ships no simulator .cpp to compile) on all host threads,
              on a bounded strided sample of the same sweep, per step.
@@ -28,7 +42,6 @@ from __future__ import annotations
 import argparse
 import ctypes as C
 import json
-import math
 import os
 import subprocess
 import sys
@@ -43,37 +56,39 @@ sys.path.insert(0, str(REPO))
 
 METRIC = "simulations/sec for N-sim parameter sweep at 1/2/4/8 B200 vs CPU ref (all cores)"
 UNIT = "simulations/s"
-SIDE = 256  # per-GPU sweep is SIDE x SIDE points
-CPU_SAMPLE_CHUNKS = 8
-CPU_SAMPLE_CHUNK = 1024  # 8 chunks of 1,024 points spread over the sweep
+SIDE = 256                 # the per-GPU (weak) / total (strong) sweep is SIDE x SIDE points
+REF_SAMPLE_CHUNKS = 16     # reference arm: 16 chunks of 1,024 points per method per step
+REF_SAMPLE_CHUNK = 1024
+CPU_BASELINE_MIN_S = 60.0  # the CPU baseline runs >= 60 s of wall time
 
 
-def workload(n_gpus: int):
+def workload(n_side_mult: int):
+    """C4 with the first axis extended to SIDE*n_side_mult values over the same range."""
     from paper_1309_7695_b200 import workloads as W
-    from paper_1309_7695_b200.ensemble import MethodKind
+    from paper_1309_7695_b200.ensemble import MethodKind, SweepAxis
     net, tau_cfg = W.c4_config(side=SIDE)
-    if n_gpus > 1:  # weak scaling: extend the first axis to 256*N values over the same range
-        from paper_1309_7695_b200.ensemble import SweepAxis
+    if n_side_mult > 1:
         pa = net.params()[net.param_index("kon0")].value
-        tau_cfg.axes[0] = SweepAxis("kon0", W.logspace_around(pa, SIDE * n_gpus))
+        tau_cfg.axes[0] = SweepAxis("kon0", W.logspace_around(pa, SIDE * n_side_mult))
     _, ode_cfg = W.c4_config(side=SIDE, method=MethodKind.Ode)
     ode_cfg.axes = tau_cfg.axes
     return net, tau_cfg, ode_cfg
 
 
-def config_block(n_gpus: int):
+def config_block(n_gpus: int, scaling: str, points_total: int):
     return {
-        "workload": "C4 Ras/cAMP/PKA-scale synthetic (33 species x 39 reactions), 256x256 log sweep of 2 rate "
-                    "constants per GPU, each point simulated by tau-adaptive tau-leaping (+SSA fallback, compat "
-                    "xoshiro256++ stream) AND Dopri5 RRE; t_end=100, 101 grid points",
+        "workload": "C4 Ras/cAMP/PKA-scale synthetic (33 species x 39 reactions), log sweep of 2 rate constants "
+                    f"({points_total} points in total, {'65,536 per GPU' if scaling == 'weak' else 'split over the GPUs'}),"
+                    " each point simulated by tau-adaptive tau-leaping (+SSA fallback, compat xoshiro256++ stream) "
+                    "AND Dopri5 RRE; t_end=100, 101 grid points",
         "model": "ras_scale(seed=0x5A5C)",
-        "sweep_points_per_gpu": SIDE * SIDE,
-        "sims_per_step_per_gpu": 2 * SIDE * SIDE,
-        "global_batch": 2 * SIDE * SIDE * n_gpus,
+        "sweep_points": points_total,
+        "global_batch": 2 * points_total,
         "seq_len": 101,
-        "parallelism": f"sweep sharded by point range over {n_gpus} GPU(s), no collective on the data path; "
-                       "on each GPU the tau and Dopri5 sweeps of a step run concurrently on two streams",
-        "l2": "flushed between timed steps (256 MiB write); outputs 2x1.75 GB per step also exceed L2",
+        "parallelism": f"sweep partitioned over {n_gpus} GPU(s) by interleaved points (kin_sweep_plan: one launch "
+                       "per device, device-side index map), no collective on the data path; on each GPU the tau and "
+                       "Dopri5 sweeps of a step run concurrently on two streams",
+        "l2": "flushed between timed steps (256 MiB write); outputs 2x1.75 GB per GPU per step also exceed L2",
     }
 
 
@@ -124,25 +139,6 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def cpu_sample_ranges(n_sims: int):
-    stride = n_sims // CPU_SAMPLE_CHUNKS
-    return [(k * stride, k * stride + CPU_SAMPLE_CHUNK) for k in range(CPU_SAMPLE_CHUNKS)]
-
-
-def run_cpu_sample(net, tau_cfg, ode_cfg, workers: int):
-    """One CPU-oracle pass over the bounded sample; returns (sims, seconds)."""
-    from oracle import oracle as O
-    from paper_1309_7695_b200.ensemble import make_sweep_desc
-    sims = 0
-    t0 = time.perf_counter()
-    for cfg in (tau_cfg, ode_cfg):
-        for rng in cpu_sample_ranges(SIDE * SIDE):
-            d, keep = make_sweep_desc(net, cfg, sim_range=rng)
-            O.sweep(net, d, workers=workers, want_traj=True, want_stats=False)
-            sims += rng[1] - rng[0]
-    return sims, time.perf_counter() - t0
-
-
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -160,8 +156,69 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def ref_sample_ranges(n_sims: int):
+    stride = n_sims // REF_SAMPLE_CHUNKS
+    return [(k * stride, k * stride + REF_SAMPLE_CHUNK) for k in range(REF_SAMPLE_CHUNKS)]
+
+
+def run_ref_sample(net, tau_cfg, ode_cfg, workers: int):
+    """One CPU-oracle pass over the reference arm's bounded sample; (sims, s)."""
+    from oracle import oracle as O
+    from paper_1309_7695_b200.ensemble import make_sweep_desc
+    sims = 0
+    t0 = time.perf_counter()
+    for cfg in (tau_cfg, ode_cfg):
+        for rng in ref_sample_ranges(SIDE * SIDE):
+            d, keep = make_sweep_desc(net, cfg, sim_range=rng)
+            O.sweep(net, d, workers=workers, want_traj=True, want_stats=False)
+            sims += rng[1] - rng[0]
+    return sims, time.perf_counter() - t0
+
+
+def cpu_baseline_and_parity(net, tau_cfg, ode_cfg, gpu_tau, gpu_ode, workers: int):
+    """The oracle over the WHOLE 65,536-point sweep, both methods, repeated until
+    >= 60 s of wall time (the CPU baseline); its first pass checks the timed
+    GPU step's outputs (tau: bit-exact trajectories + meta + status; Dopri5:
+    within 10 (atol + rtol |y|) at every grid point)."""
+    from oracle import oracle as O
+    from paper_1309_7695_b200.ensemble import make_sweep_desc
+    d_tau, k1 = make_sweep_desc(net, tau_cfg)
+    d_ode, k2 = make_sweep_desc(net, ode_cfg)
+    outs = [None, None]
+    parity = {}
+    sims, secs, passes = 0, 0.0, 0
+    while secs < CPU_BASELINE_MIN_S or passes == 0:
+        for mi, d in enumerate((d_tau, d_ode)):
+            t0 = time.perf_counter()
+            outs[mi] = O.sweep(net, d, workers=workers, want_traj=True, want_stats=False, out=outs[mi])
+            secs += time.perf_counter() - t0
+            sims += SIDE * SIDE
+        if passes == 0:
+            ref_t, ref_o = outs
+            if gpu_tau is not None:
+                ok_t = (np.array_equal(ref_t["traj"], gpu_tau["traj"]) and np.array_equal(ref_t["meta"], gpu_tau["meta"])
+                        and np.array_equal(ref_t["status"], gpu_tau["status"]))
+                ic = ode_cfg.method.integrator
+                bound = 10.0 * (ic.abs_tol + ic.rel_tol * np.abs(ref_o["traj"]))
+                worst = float(np.max(np.abs(gpu_ode["traj"] - ref_o["traj"]) / bound))
+                parity = {"tau": "bit-exact" if ok_t else "MISMATCH",
+                          "tau_simulations_compared": int(ref_t["traj"].shape[0]),
+                          "ode": "within 10x tolerance" if worst <= 1.0 else "MISMATCH",
+                          "ode_worst_error_over_bound": worst,
+                          "ode_simulations_compared": int(ref_o["traj"].shape[0]),
+                          "what": "the timed step's own device outputs (last timed step, fetched after timing) vs the "
+                                  "CPU oracle over the whole sweep"}
+        passes += 1
+    return {"value": sims / secs, "unit": UNIT, "cores": workers, "kind": "port",
+            "sample": f"the whole 65,536-point C4 sweep by both methods, {passes} passes ({sims} simulations, "
+                      f"{secs:.1f} s wall)",
+            "cpu": cpu_model(),
+            "what": "oracle/ C++20 restatement of the reference path (the reference ships only rng.cpp), -O3 "
+                    "-DNDEBUG, std::thread pool over contiguous run ranges (ensemble.hpp:91-99)"}, parity
+
+
 # ---------------------------------------------------------------------------
-def dist_setup(n_gpus: int):
+def dist_setup():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -191,23 +248,13 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(world, value: float, local: int) -> float:
+def reduce_over_ranks(world, value: float, local: int, op: str) -> float:
     if world == 1:
         return value
     import torch
     import torch.distributed as dist
     t = torch.tensor([value], dtype=torch.float64, device="cpu" if _backend() == "gloo" else f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
-def sum_over_ranks(world, value: float, local: int) -> float:
-    if world == 1:
-        return value
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([value], dtype=torch.float64, device="cpu" if _backend() == "gloo" else f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
 
 
@@ -221,141 +268,158 @@ def read_profile_entry(kernel):
     return {}
 
 
-def read_profile_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
-    the committed `ncu --set full` capture summary (profiles/ncu_summary.json)."""
-    p = REPO / "profiles" / "ncu_summary.json"
-    if p.exists():
-        try:
-            d = json.loads(p.read_text()).get("kernels", {}).get(kernel)
-            if d:
-                return d.get("dram_bytes_per_launch"), d.get("source")
-        except Exception:
-            pass
-    return None, None
-
-
 # ---------------------------------------------------------------------------
 def bench_ours(args, world, rank, local):
     import torch
     from paper_1309_7695_b200 import abi
-    from paper_1309_7695_b200.ensemble import Engine, make_sweep_desc
+    from paper_1309_7695_b200.ensemble import Engine, local_size, make_sweep_desc
 
-    from paper_1309_7695_b200 import shard
-    n = world
-    net, tau_cfg, ode_cfg = workload(n)
-    per = SIDE * SIDE
-    rng = shard.rank_range(per * n, 1, rank, n)  # whole points, rank-contiguous
-    eng = Engine([local])
-    lib = eng.lib
-    h = eng.model(net)
+    # devices this process drives: its own under torchrun, 0..N-1 otherwise
+    if world > 1:
+        devices = [local]
+        n_gpus = world
+    else:
+        n_gpus = args.gpus
+        visible = torch.cuda.device_count()
+        if visible < n_gpus:
+            raise SystemExit(f"--gpus {n_gpus} needs {n_gpus} visible GPUs, found {visible}")
+        devices = list(range(n_gpus))
+    mult = n_gpus if args.scaling == "weak" else 1
+    net, tau_cfg, ode_cfg = workload(mult)
+    points_total = SIDE * SIDE * mult
+    shard = (rank, world) if world > 1 else None
+    d_tau, k1 = make_sweep_desc(net, tau_cfg, shard=shard)
+    d_ode, k2 = make_sweep_desc(net, ode_cfg, shard=shard)
+    n_pts_local, n_local = local_size(d_tau)  # this process's simulations per method
+    slot = 0 if len(devices) == 1 else -1     # -1: every device of the context, one part each
     err = abi.KinError()
-    d_tau, k1 = make_sweep_desc(net, tau_cfg, sim_range=rng)
-    d_ode, k2 = make_sweep_desc(net, ode_cfg, sim_range=rng)
 
     def check(rc):
         if rc != 0:
             raise RuntimeError(f"engine error {rc}: {err.text()}")
 
-    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{local}")
+    eng = Engine(devices)
+    lib = eng.lib
+    h = eng.model(net)
+    D = len(devices)
+    dev0 = devices[0]
 
     # -- algorithmic work of the dominant kernel (instrumented variant, untimed)
-    check(lib.kin_sweep_launch(eng.ctx, h, C.byref(d_tau), 0, 0, 1, C.byref(err)))
-    check(lib.kin_sweep_sync(eng.ctx, 0, C.byref(err)))
-    work = np.zeros(per, np.uint64)
-    status = np.zeros(per, np.int32)
-    meta = np.zeros((per, 6), np.uint64)
+    check(lib.kin_sweep_launch(eng.ctx, h, C.byref(d_tau), slot, 0, 1, C.byref(err)))
+    check(lib.kin_sweep_sync(eng.ctx, slot, C.byref(err)))
+    work = np.zeros(n_local, np.uint64)
+    status = np.zeros(n_local, np.int32)
+    meta = np.zeros((n_local, 6), np.uint64)
     o = abi.KinSweepOut(None, abi.ptr(meta, C.c_uint64), abi.ptr(status, C.c_int32), None, None,
                         abi.ptr(work, C.c_uint64))
-    check(lib.kin_sweep_fetch(eng.ctx, 0, C.byref(o), C.byref(err)))
+    check(lib.kin_sweep_fetch(eng.ctx, slot, C.byref(o), C.byref(err)))
     if (status != 0).any():
         raise RuntimeError("simulation failures in the benchmark sweep")
-    tau_flops = float(work.sum())
+    tau_flops = float(work.sum())  # this process's tau simulations, all its devices
 
     peak = C.c_double()
     check(lib.kin_measure_fp64_peak(eng.ctx, C.byref(peak), C.byref(err)))
 
-    tau_kernel = []
-    # The step's two sweeps are independent jobs: the device-resident step runs
-    # them concurrently on two device slots of this GPU (the tau sweep on slot 0,
-    # Dopri5 on slot 1), so the Dopri5 blocks fill the SMs the tau kernel's tail
-    # leaves idle.  Timed from stream 0, which waits for stream 1's sweep.
-    eng2 = Engine([local, local])
-    h2 = eng2.model(net)
-    st1 = torch.cuda.ExternalStream(lib.kin_ctx_stream(eng2.ctx, 1), device=f"cuda:{local}")
-    stream = torch.cuda.ExternalStream(lib.kin_ctx_stream(eng2.ctx, 0), device=f"cuda:{local}")
-    ev_go = torch.cuda.Event()
-    ev_ode = torch.cuda.Event()
+    # The step's two sweeps are independent jobs: they run concurrently on two
+    # contexts over the same devices (tau on A, Dopri5 on B), so the Dopri5
+    # blocks fill the SMs the tau kernel's tail leaves idle.  Per device: the
+    # step is timed on A's stream, which waits for B's sweep.
+    engA, engB = Engine(devices), Engine(devices)
+    hA, hB = engA.model(net), engB.model(net)
+    sA = [torch.cuda.ExternalStream(lib.kin_ctx_stream(engA.ctx, i), device=f"cuda:{dv}") for i, dv in enumerate(devices)]
+    sB = [torch.cuda.ExternalStream(lib.kin_ctx_stream(engB.ctx, i), device=f"cuda:{dv}") for i, dv in enumerate(devices)]
+    ev_go = [torch.cuda.Event() for _ in devices]
+    ev_b = [torch.cuda.Event() for _ in devices]
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in devices]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in devices]
+    flush = [torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=f"cuda:{dv}") for dv in devices]
 
-    def step():
-        ev_go.record(stream)
-        st1.wait_event(ev_go)
-        check(lib.kin_sweep_launch(eng2.ctx, h2, C.byref(d_tau), 0, 1, 0, C.byref(err)))
-        check(lib.kin_sweep_launch(eng2.ctx, h2, C.byref(d_ode), 1, 1, 0, C.byref(err)))
-        ev_ode.record(st1)
-        stream.wait_event(ev_ode)
-
-    def step_tau_ms():
-        tau_kernel.append(lib.kin_sweep_kernel_name(eng2.ctx, 0).decode())
-        ms_tau, ms_st = C.c_double(), C.c_double()
-        check(lib.kin_sweep_kernel_ms(eng2.ctx, 0, C.byref(ms_tau), C.byref(ms_st), C.byref(err)))
-        return ms_tau.value
+    def step(timed):
+        for i, dv in enumerate(devices):
+            with torch.cuda.device(dv):
+                if timed:
+                    with torch.cuda.stream(sA[i]):
+                        flush[i].fill_(1.0)  # L2 flush, outside the timed events
+                    ev0[i].record(sA[i])
+                ev_go[i].record(sA[i])
+                sB[i].wait_event(ev_go[i])
+        check(lib.kin_sweep_launch(engA.ctx, hA, C.byref(d_tau), slot, 0, 0, C.byref(err)))
+        check(lib.kin_sweep_launch(engB.ctx, hB, C.byref(d_ode), slot, 0, 0, C.byref(err)))
+        for i, dv in enumerate(devices):
+            with torch.cuda.device(dv):
+                ev_b[i].record(sB[i])
+                sA[i].wait_event(ev_b[i])
+                if timed:
+                    ev1[i].record(sA[i])
 
     def sync_both():
-        for sl in (0, 1):
-            check(lib.kin_sweep_sync(eng2.ctx, sl, C.byref(err)))
+        check(lib.kin_sweep_sync(engA.ctx, slot, C.byref(err)))
+        check(lib.kin_sweep_sync(engB.ctx, slot, C.byref(err)))
+
+    def tau_kernel_ms():
+        ms = []
+        for i in range(D):
+            a, b = C.c_double(), C.c_double()
+            check(lib.kin_sweep_kernel_ms(engA.ctx, i, C.byref(a), C.byref(b), C.byref(err)))
+            ms.append(a.value)
+        return max(ms)
 
     for _ in range(args.warmup):
-        step()
+        step(False)
         sync_both()
 
     step_ms, tau_ms = [], []
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
     barrier(world)
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    for dv in devices:
+        torch.cuda.synchronize(dv)
+    with ClockSampler(dev0) as clk:
         for _ in range(args.steps):
-            with torch.cuda.stream(stream):
-                flush.fill_(1.0)  # L2 flush, outside the timed events
-            ev0.record(stream)
-            step()
-            ev1.record(stream)
+            step(True)
             sync_both()
-            ev1.synchronize()
-            tau_ms.append(step_tau_ms())
-            step_ms.append(ev0.elapsed_time(ev1))
-    torch.cuda.synchronize()
+            for i in range(D):
+                ev1[i].synchronize()
+            step_ms.append(max(ev0[i].elapsed_time(ev1[i]) for i in range(D)))  # max over devices
+            tau_ms.append(tau_kernel_ms())
+    for dv in devices:
+        torch.cuda.synchronize(dv)
     barrier(world)
-    total_ms = max_over_ranks(world, float(np.sum(step_ms)), local)
-    sims_step = 2 * per * n
+    total_ms = reduce_over_ranks(world, float(np.sum(step_ms)), local, "max")  # max over ranks
+    sims_step = 2 * points_total
     value = sims_step * args.steps / (total_ms / 1e3)
     tau_avg_ms = float(np.mean(tau_ms))
-    achieved = tau_flops / (tau_avg_ms / 1e3) / 1e12
+    kname = lib.kin_sweep_kernel_name(engA.ctx, 0).decode()
 
-    # -- end to end through the public API: kin_sweep_run with host buffers,
-    # returning what the engine produces per simulation (Trajectory samples
-    # [S][G][N] in the reference layout, TrajectoryMeta, status) — the
-    # run_ensemble/RunSink output; H2D of the sweep tables inside the call.
-    import torch as _t
+    # the timed step's own outputs (kept for the parity check against the oracle)
     G, N = len(tau_cfg.grid), net.species_count()
+    gpu_out = None
+    if world == 1 and n_gpus == 1 and not args.no_cpu_baseline:
+        gpu_out = []
+        for e in (engA, engB):
+            r = {"traj": np.empty((n_local, G, N)), "meta": np.empty((n_local, 6), np.uint64),
+                 "status": np.empty(n_local, np.int32)}
+            oo = abi.KinSweepOut(abi.ptr(r["traj"], C.c_double), abi.ptr(r["meta"], C.c_uint64),
+                                 abi.ptr(r["status"], C.c_int32), None, None, None)
+            check(lib.kin_sweep_fetch(e.ctx, slot, C.byref(oo), C.byref(err)))
+            gpu_out.append(r)
 
+    # -- end to end through the public API: kin_sweep_run (async form) with
+    # pinned host buffers, returning what the engine produces per simulation
+    # (Trajectory samples [S][G][N], TrajectoryMeta, status) — the
+    # run_ensemble/RunSink output; H2D of the sweep tables inside the call.
     def pinned_out():
-        traj_h = _t.empty((per, G, N), dtype=_t.float64, pin_memory=True).numpy()
-        meta_h = _t.empty((per, 6), dtype=_t.int64, pin_memory=True).numpy().view(np.uint64)
-        st_h = _t.empty(per, dtype=_t.int32, pin_memory=True).numpy()
+        traj_h = torch.empty((n_local, G, N), dtype=torch.float64, pin_memory=True).numpy()
+        meta_h = torch.empty((n_local, 6), dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        st_h = torch.empty(n_local, dtype=torch.int32, pin_memory=True).numpy()
         return abi.KinSweepOut(abi.ptr(traj_h, C.c_double), abi.ptr(meta_h, C.c_uint64), abi.ptr(st_h, C.c_int32),
                                None, None, None), (traj_h, meta_h, st_h)
 
-    # two steps in flight: double-buffered pinned outputs per method
-    bufs = [[pinned_out() for _ in range(2)] for _ in range(2)]
+    bufs = [[pinned_out() for _ in range(2)] for _ in range(2)]  # two steps in flight, per method
 
     def submit_step(k):
         tickets = []
         for mi, d in enumerate((d_tau, d_ode)):
             t = C.c_uint64()
-            check(lib.kin_sweep_submit(eng.ctx, h, C.byref(d), C.byref(bufs[k % 2][mi][0]), C.byref(t),
-                                       C.byref(err)))
+            check(lib.kin_sweep_submit(eng.ctx, h, C.byref(d), C.byref(bufs[k % 2][mi][0]), C.byref(t), C.byref(err)))
             tickets.append(t.value)
         return tickets
 
@@ -376,83 +440,90 @@ def bench_ours(args, world, rank, local):
     barrier(world)
     t0 = time.perf_counter()
     e2e_run(args.steps)
-    t_e2e = max_over_ranks(world, time.perf_counter() - t0, local)
+    t_e2e = reduce_over_ranks(world, time.perf_counter() - t0, local, "max")
     barrier(world)
     e2e_value = sims_step * args.steps / t_e2e
     bytes_axes = sum(len(a.values) for a in tau_cfg.axes) * 8 + G * 8
-    h2d = 2 * (bytes_axes + 31 * 1024)  # sweep tables + packed model tables, both methods
-    d2h = 2 * (per * G * N * 8 + per * 6 * 8 + per * 4)
+    h2d = 2 * (bytes_axes + 31 * 1024) * D  # sweep tables + packed model tables, both methods, per device
+    d2h = 2 * (n_local * G * N * 8 + n_local * 6 * 8 + n_local * 4)  # this process's outputs, both methods
 
-    kname = tau_kernel[-1]
-    traffic, traffic_src = read_profile_traffic(kname)
+    # roofline of the dominant kernel: this process's tau flops over the
+    # slowest device's tau-kernel time (per device: flops/D over its own time)
+    achieved = tau_flops / D / (tau_avg_ms / 1e3) / 1e12
     res = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (deterministic generator, seed 0x5A5C)", "config": config_block(n),
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic generator, seed 0x5A5C)",
+        "config": config_block(n_gpus, args.scaling, points_total),
         "impl": "ours",
+        "launch": "torchrun: one process per GPU, descriptor shard (rank, world)" if world > 1 else
+                  f"one process, engine context over {D} device(s)",
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "api": "kin_sweep_submit/kin_sweep_wait (async kin_sweep_run) -> per-simulation time series [S][G][N] + TrajectoryMeta + status into pinned host buffers (run_ensemble/RunSink output), both methods; two steps in flight, double-buffered outputs, every step's H2D and D2H inside the timed region"},
-        "gpu_launches": 4 * args.steps,
+                "api": "kin_sweep_submit/kin_sweep_wait (async kin_sweep_run) -> per-simulation time series [S][G][N] "
+                       "+ TrajectoryMeta + status into pinned host buffers (run_ensemble/RunSink output), both methods; "
+                       "two steps in flight, double-buffered outputs, every step's H2D and D2H inside the timed region"
+                       + ("; per-rank host buffers (each rank holds its shard)" if world > 1 else "")},
+        "gpu_launches": 2 * args.steps * D,
         "breakdown": {"tau_kernel_ms": tau_avg_ms, "step_ms": float(np.mean(step_ms)),
-                      "tau_leaps_per_sim": float(meta[:, 0].mean()), "ssa_fallback_steps_per_sim": float(meta[:, 3].mean())},
+                      "tau_leaps_per_sim": float(meta[:, 0].mean()),
+                      "ssa_fallback_steps_per_sim": float(meta[:, 3].mean()),
+                      "statistics": "not computed in the timed step (R = 1: per-point mean/m2 would be copies)"},
         "roofline": {"bound": "fp64", "kernel": f"{kname} (tau-leap + SSA fallback)",
                      "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s", "frac": achieved / peak.value,
-                     "peak_source": "measured DFMA microbenchmark (kin_measure_fp64_peak) in this run; FP64 is not in MEASURED_PEAKS.json",
-                     "algorithmic_flops_per_launch": tau_flops,
-                     "traffic": traffic, "traffic_source": traffic_src},
+                     "peak_source": "measured DFMA microbenchmark (kin_measure_fp64_peak) in this run; FP64 is not "
+                                    "in MEASURED_PEAKS.json",
+                     "algorithmic_flops_per_launch": tau_flops / D},
     }
     res["clocks"] = clk.summary()
-    # The same kernel against the HBM roofline, for completeness: its DRAM
-    # traffic (committed ncu capture) over the live kernel time, against the
-    # measured copy bandwidth in MEASURED_PEAKS.json.  Far below 1 by design —
-    # the per-simulation state lives in shared memory, only the trajectories
-    # stream out — which is why the binding roofline is FP64 / issue, not HBM.
+    ent = read_profile_entry(kname)
+    res["roofline"]["traffic"] = ent.get("dram_bytes_per_launch")
+    res["roofline"]["traffic_source"] = ent.get("source")
+    # The same kernel against the HBM roofline: its DRAM traffic (committed ncu
+    # capture) over the live kernel time, against MEASURED_PEAKS.json.
     pk = REPO / "MEASURED_PEAKS.json"
-    if traffic and pk.exists():
+    if res["roofline"]["traffic"] and pk.exists() and n_gpus == 1:
         hbm = json.loads(pk.read_text()).get("hbm_gbs")
         if hbm:
-            ach = traffic / (tau_avg_ms / 1e3) / 1e9
+            ach = res["roofline"]["traffic"] / (tau_avg_ms / 1e3) / 1e9
             res["roofline"]["hbm"] = {"achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"}
-    # Instruction-issue roofline of the same kernel: the warp-instructions one
-    # launch of this (deterministic) workload executes, from the committed ncu
-    # capture, over the live kernel time and the issue peak at the sampled SM
-    # clock (148 SMs x 4 schedulers x 1 warp-instruction per cycle).
-    ent = read_profile_entry(kname)
+    # Instruction-issue roofline of the same kernel (warp instructions of one
+    # launch of this deterministic workload, from the committed ncu capture).
     winst = ent.get("warp_instructions_per_launch")
-    if winst and res["clocks"].get("sm_mhz"):
-        import torch as _tt
-        sms = _tt.cuda.get_device_properties(local).multi_processor_count
+    if winst and res["clocks"].get("sm_mhz") and n_gpus == 1:
+        sms = torch.cuda.get_device_properties(dev0).multi_processor_count
         peak_issue = sms * 4 * res["clocks"]["sm_mhz"] * 1e6
         achieved_issue = winst / (tau_avg_ms / 1e3)
         res["roofline"]["issue"] = {"achieved_warp_inst_per_s": achieved_issue, "peak_warp_inst_per_s": peak_issue,
                                     "frac": achieved_issue / peak_issue, "warp_instructions_per_launch": winst,
                                     "source": ent.get("source")}
-    eng2.close()
+    engA.close()
+    engB.close()
     eng.close()
-    return res
+    return res, (net, tau_cfg, ode_cfg, gpu_out)
 
 
 def bench_reference(args, world, rank):
     """CPU reference arm: the oracle on all host threads, bounded sample per step."""
-    n = world
     net, tau_cfg, ode_cfg = workload(1)
     threads = host_threads()
     for _ in range(args.warmup):
-        run_cpu_sample(net, tau_cfg, ode_cfg, threads)
+        run_ref_sample(net, tau_cfg, ode_cfg, threads)
     sims = 0
     secs = 0.0
     for _ in range(args.steps):
-        s, t = run_cpu_sample(net, tau_cfg, ode_cfg, threads)
+        s, t = run_ref_sample(net, tau_cfg, ode_cfg, threads)
         sims += s
         secs += t
     value = sims / secs
-    sample = (f"{CPU_SAMPLE_CHUNKS} chunks x {CPU_SAMPLE_CHUNK} points spread evenly over the 65,536-point sweep, "
-              "both methods (16,384 simulations per step)")
+    sample = (f"{REF_SAMPLE_CHUNKS} chunks x {REF_SAMPLE_CHUNK} points spread evenly over the 65,536-point sweep, "
+              f"both methods ({2 * REF_SAMPLE_CHUNKS * REF_SAMPLE_CHUNK} simulations per step; {sims} simulations, "
+              f"{secs:.1f} s timed)")
     return {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (deterministic generator, seed 0x5A5C)", "config": config_block(1),
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (deterministic generator, seed 0x5A5C)",
+        "config": config_block(world, args.scaling, SIDE * SIDE * (world if args.scaling == "weak" else 1)),
         "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample,
                          "cpu": cpu_model(),
@@ -468,6 +539,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
@@ -478,20 +550,18 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:
             return
-        print(json.dumps(bench_reference(args, world, rank)))
+        print(json.dumps(bench_reference(args, max(world, args.gpus), rank)))
         return
 
-    world, rank, local = dist_setup(args.gpus)
-    res = bench_ours(args, world, rank, local)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        net, tau_cfg, ode_cfg = workload(1)
-        threads = host_threads()
-        s, t = run_cpu_sample(net, tau_cfg, ode_cfg, threads)
-        res["cpu_baseline"] = {
-            "value": s / t, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{CPU_SAMPLE_CHUNKS} chunks x {CPU_SAMPLE_CHUNK} points spread over the sweep, both methods "
-                      f"({s} simulations, {t:.1f} s wall)",
-            "cpu": cpu_model()}
+    world, rank, local = dist_setup()
+    res, (net, tau_cfg, ode_cfg, gpu_out) = bench_ours(args, world, rank, local)
+    if rank == 0 and world == 1 and args.gpus == 1 and not args.no_cpu_baseline:
+        base, parity = cpu_baseline_and_parity(net, tau_cfg, ode_cfg, gpu_out[0], gpu_out[1], host_threads())
+        res["cpu_baseline"] = base
+        res["parity"] = parity
+        if parity.get("tau") != "bit-exact" or parity.get("ode") != "within 10x tolerance":
+            print(json.dumps(res))
+            raise SystemExit("parity check of the timed step FAILED")
     if rank == 0:
         print(json.dumps(res))
     if world > 1:

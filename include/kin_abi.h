@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define KIN_ABI_VERSION 2
+#define KIN_ABI_VERSION 3
 
 /* ---- status codes (cli.hpp:8-13 ExitCode; errors.hpp classes) ------------ */
 enum kin_status {
@@ -104,7 +104,19 @@ typedef struct kin_method {
   double theta_x;              /* amount_threshold, reference default 100 (may be +inf) */
   double theta_a;              /* propensity_threshold, reference default 10 */
   double repartition_interval; /* 0 selects t_end / 100 */
+  /* tau-leap firing law (TauAdaptive / TauFixed): enum kin_firing */
+  int32_t firing;
 } kin_method;
+
+enum kin_firing {
+  KIN_FIRING_POISSON = 0,   /* k_j ~ Poisson(a_j tau), reject + halve on a negative
+                               amount (stochastic.hpp:53-57) — the reference */
+  KIN_FIRING_BINOMIAL = 1   /* extension (north star): k_j ~ Binomial(n_j, p_j) with n_j the
+                               reactant-limited firing bound after the reactions before j
+                               consumed theirs, p_j = min(1, a_j tau / n_j): amounts never
+                               go negative, so a leap is never rejected (Tian & Burrage 2004,
+                               Chatterjee et al. 2005, sequential form) */
+};
 
 /* ---- sweep: SweepConfig (ensemble.hpp:101-113) ---------------------------- */
 enum kin_axis_kind {
@@ -146,7 +158,46 @@ typedef struct kin_sweep_desc {
      whose runs all lie inside the shard. */
   uint64_t sim_begin;
   uint64_t sim_end;
+  /* interleaved point shard (multi-GPU across processes): this call
+     simulates only the points p of [sim_begin, sim_end) (whole points: both
+     bounds multiples of runs_per_point) with (p - p_first) % shard_count ==
+     shard_index, and its outputs are COMPACT in shard order (local point k =
+     global point p_first + shard_index + k*shard_count).  shard_count <= 1:
+     every simulation of the range, outputs in global order. */
+  int32_t shard_index;
+  int32_t shard_count;
+  int32_t output_mode;    /* enum kin_output_mode */
+  int32_t lanes_per_sim;  /* 0 = automatic; Dopri5: 1/2/4/8/16/32 lanes per simulation;
+                             Philox stochastic: 1 (thread per simulation) or 2..32 */
+  uint32_t variant;       /* 0 = automatic; OR of enum kin_variant flags (forced kernel
+                             choices — studies and tests; results never depend on them) */
+  int32_t reserved_;
 } kin_sweep_desc;
+
+enum kin_output_mode {
+  KIN_OUTPUT_FULL = 0,        /* every array the kin_sweep_out pointers request */
+  KIN_OUTPUT_STATS_ONLY = 1   /* parameter_sweep / run_ensemble without a RunSink: per-point
+                                 mean/m2 (+ meta/status/work) only; trajectories are never
+                                 materialised whole — the runs go through a bounded device
+                                 buffer in run-ascending sub-launches whose Welford
+                                 accumulators continue across sub-launches (same result
+                                 as KIN_OUTPUT_FULL, bit for bit); out->traj is ignored */
+};
+
+enum kin_variant {
+  KIN_VARIANT_TABLE = 1u << 0,        /* stochastic: table-driven kernel, never the per-model JIT */
+  KIN_VARIANT_JIT = 1u << 1,          /* stochastic: per-model JIT at any size */
+  KIN_VARIANT_DOUBLE_STATE = 1u << 2, /* stochastic: double amounts (no int32 state) */
+  KIN_VARIANT_GLOBAL_STATE = 1u << 3, /* per-simulation state in global memory */
+  KIN_VARIANT_SMEM_STATE = 1u << 4,   /* per-simulation state in shared memory */
+  KIN_VARIANT_NO_SPLIT = 1u << 5      /* JIT global state: keep x[] global too */
+};
+/* variant bits 8..13: simulations per warp (1..32) of the thread-per-simulation
+   SSA/tau kernels; 0 = the occupancy fill rule */
+#define KIN_VARIANT_WARP_LANES(w) ((uint32_t)(w) << 8)
+/* variant bits 16..31: KIN_OUTPUT_STATS_ONLY window in simulations (tests;
+   0 = the automatic 2 GiB trajectory budget) */
+#define KIN_VARIANT_STATS_WINDOW(s) ((uint32_t)(s) << 16)
 
 /* ---- outputs (caller-allocated HOST buffers; any may be NULL) ------------- */
 typedef struct kin_sweep_out {
@@ -220,16 +271,42 @@ int kin_run_single(kin_ctx* ctx, const kin_model* model, const kin_method* metho
                    const double* grid, int32_t n_grid, uint64_t seed, int32_t rng_mode, double* samples,
                    uint64_t* meta, kin_error* err);
 
-/* The chunk plan kin_sweep_run uses for n_devices GPUs over simulations
-   [s0, s1) with R runs per point: n_chunks = (n_devices == 1 ? 1 : min(#points,
-   4*n_devices)) whole-point chunks (boundaries snapped to multiples of R) — or,
-   when the range touches fewer points than devices (run_ensemble), min(S,
-   n_devices) equal run ranges whose cut points get their statistics Chan-merged
-   in ascending chunk order (ensemble.hpp:91-99).  Chunk c -> device
-   c % n_devices.  bounds receives n_chunks+1 entries (capacity max_chunks+1).
+/* One device's share of a call (the partitioner's plan; ensemble.hpp:91-99
+   worker ranges become devices).  Either INTERLEAVED — n_points whole points,
+   global point pt_first + k*pt_stride for local point k, each with its R runs
+   (the kernels map local -> global simulation index on the device) — or
+   CONTIGUOUS — global simulations [sim_begin, sim_end).  Outputs land in the
+   caller's layout at local simulation out_first + k*out_pitch (+ run), rows of
+   R simulations (interleaved) or one row of sim_end - sim_begin (contiguous). */
+typedef struct kin_sweep_part {
+  int32_t device;       /* context device slot */
+  int32_t interleaved;
+  uint64_t sim_begin, sim_end;          /* contiguous parts */
+  uint64_t pt_first, pt_stride, n_points; /* interleaved parts */
+  uint64_t out_first, out_pitch;        /* caller-local simulation index of the first
+                                           row and the distance between rows */
+} kin_sweep_part;
+
+/* The plan kin_sweep_run uses for n_devices GPUs over simulations [s0, s1)
+   with R runs per point and the caller's shard (shard_index, shard_count):
+   * one device: one part (everything);
+   * whole points and at least as many points as devices: ONE interleaved part
+     per device — device d takes the caller's points d, d+D, d+2D, ... (cyclic
+     by point: balances the cost gradient along the sweep axes, and every
+     device gets a single full-occupancy launch);
+   * fewer points than devices (run_ensemble): min(S, D) equal contiguous run
+     ranges whose cut points get their statistics Chan-merged in ascending
+     part order (the reference's per-worker accumulators, ensemble.hpp:91-99);
+   * a range that cuts points: D contiguous whole-point chunks.
    Pure host function (no device needed). */
-int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t runs_per_point, int32_t n_devices,
-                   int32_t max_chunks, uint64_t* bounds, int32_t* n_chunks, kin_error* err);
+int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t runs_per_point, int32_t n_devices, int32_t shard_index,
+                   int32_t shard_count, int32_t max_parts, kin_sweep_part* parts, int32_t* n_parts,
+                   kin_error* err);
+
+/* Caller-local sizes of a descriptor (its sim range and shard): n_points
+   points with statistics (whole points inside the call) and n_sims
+   simulations (the length of traj/meta/status/work). */
+int kin_sweep_local_size(const kin_sweep_desc* desc, uint64_t* n_points, uint64_t* n_sims, kin_error* err);
 
 /* Asynchronous form of kin_sweep_run: enqueue the sweep (kernels on the
    device's compute stream, copy-out into `out` on its copy stream)
@@ -245,7 +322,10 @@ int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err);
    Runs the sweep on device `device_slot` of the context into context-owned
    device buffers, on the context's stream, WITHOUT any host copies.  The
    results stay resident until the next call; kin_sweep_fetch copies them out.
-   kin_sweep_launch does not synchronize. */
+   kin_sweep_launch does not synchronize.  device_slot = -1: every slot of the
+   context, each with its part of kin_sweep_plan (one launch per device);
+   kin_sweep_sync / kin_sweep_fetch with -1 then cover all slots (fetch
+   assembles the caller's layout). */
 int kin_sweep_launch(kin_ctx* ctx, const kin_model* model,
                      const kin_sweep_desc* desc, int32_t device_slot,
                      int32_t want_stats, int32_t want_work, kin_error* err);
@@ -272,6 +352,11 @@ uint64_t kin_derive_run_seed(uint64_t master, uint64_t index);  /* ensemble.hpp:
 int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
                          int32_t n, uint64_t* out_bits, kin_error* err);
 
+/* Device binomial draws (the KIN_FIRING_BINOMIAL sampler) from RngStream(seed):
+   n_draws values of Binomial(n_trials, p), raw counts. */
+int kin_device_binomial_draws(kin_ctx* ctx, uint64_t seed, uint64_t n_trials, double p, int32_t n_draws,
+                              uint64_t* out, kin_error* err);
+
 /* Device unit seams (SPEC's from_uniforms / from_counts / from_normals forms):
    one function of the path on one state x[N] of `model`, through the same
    device code the sweep kernels run (propensities from the packed tables).
@@ -279,7 +364,11 @@ int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
      kind 1 select_tau (stochastic.hpp:40-46)         params {eps} -> out[0] = tau (+inf if a0 = 0)
      kind 2 ssa_step_from_uniforms (:28-32)           params {u1, u2} -> out {dt, j} ({+inf, -1} if a0 = 0)
      kind 3 tau_leap_step_from_counts (:59-62)        params counts[M] -> out[0..N-1] = x', out[N] = rejected
-     kind 4 cle_step_from_normals (:71-75)            params {h, z[M]} -> out[0..N-1] = x', out[N] = clamped */
+     kind 4 cle_step_from_normals (:71-75)            params {h, z[M]} -> out[0..N-1] = x', out[N] = clamped
+     kind 5 rre_rhs (deterministic.hpp:85-88)         out[N] = dx/dt = nu a(x)
+     kind 6 rk_step (deterministic.hpp:26-36)         params {h, rel_tol, abs_tol} -> out[0..N-1] =
+                                                      y(t+h) (5th order), out[N] = error norm,
+                                                      out[N+1..2N] = f(y(t+h)) (FSAL) */
 int kin_device_unit(kin_ctx* ctx, const kin_model* model, int32_t kind, const double* x, const double* params,
                     int32_t n_params, double* out, int32_t out_cap, kin_error* err);
 

@@ -173,6 +173,26 @@ int ssa_select(const Network& net, const double* a, double a0, double u2) {
   return last;
 }
 
+// One reaction of the sequential binomial leap (KIN_FIRING_BINOMIAL, kin_abi.h):
+// k_j ~ Binomial(n_j, a_j tau / n_j), n_j = min over reactants of
+// floor(x_s / stoich_s) at the amounts left after reactions 0..j-1 of this leap
+// fired, so no amount can go negative and no leap is rejected; a zero-order
+// reaction (no reactant bound) fires Poisson(a_j tau).  Draws in reaction order.
+template <class Src>
+std::uint64_t binomial_fire(const Network& net, Src& src, const double* x, int j, double mean, std::uint64_t* pf) {
+  if (net.rt_ptr[j] == net.rt_ptr[j + 1]) return poisson_from(src, mean, pf);
+  if (!(mean > 0.0)) return 0;
+  double lim = kInf;
+  for (int p = net.rt_ptr[j]; p < net.rt_ptr[j + 1]; ++p) {
+    const double v = std::floor(x[net.rt_species[p]] / static_cast<double>(net.rt_stoich[p]));
+    if (v < lim) lim = v;
+  }
+  if (pf) *pf += static_cast<std::uint64_t>(net.rt_ptr[j + 1] - net.rt_ptr[j]);
+  if (!(lim > 0.0)) return 0;
+  if (pf) *pf += 1;
+  return binomial_from(src, static_cast<std::uint64_t>(lim), mean / lim, pf);
+}
+
 template <bool C>
 int simulate_stochastic(const Network& net, const double* rates, const double* x0,
                         const kin_method& method, double t_end, const double* grid,
@@ -271,7 +291,26 @@ int simulate_stochastic(const Network& net, const double* rates, const double* x
     const double gap = t_stop - t;
     if constexpr (C) w->flops += 1;
     if (!(tau < gap)) { tau = gap; hit = true; }
-    for (;;) {
+    if (method.firing == KIN_FIRING_BINOMIAL) {
+      // sequential binomial leap: bounded by reactant availability, never rejected
+      for (int i = 0; i < n; ++i) xn[i] = x[i];
+      for (int j = 0; j < m; ++j) {
+        std::uint64_t kj;
+        if (philox) {
+          PhiloxSite src(seed, ev, static_cast<std::uint32_t>(j));
+          kj = binomial_fire(net, src, xn, j, a[j] * tau, pf);
+        } else {
+          kj = binomial_fire(net, rng, xn, j, a[j] * tau, pf);
+        }
+        if (kj == 0) continue;
+        const double kd = static_cast<double>(kj);
+        for (int p = net.col_ptr[j]; p < net.col_ptr[j + 1]; ++p)
+          xn[net.col_species[p]] = xn[net.col_species[p]] + static_cast<double>(net.col_delta[p]) * kd;
+      }
+      if (philox) ++ev;
+      if constexpr (C) w->flops += static_cast<std::uint64_t>(m) + 2 * static_cast<std::uint64_t>(net.col_ptr[m]);
+    }
+    for (; method.firing != KIN_FIRING_BINOMIAL;) {
       if (philox) {
         for (int j = 0; j < m; ++j) {
           PhiloxSite src(seed, ev, static_cast<std::uint32_t>(j));
@@ -1497,6 +1536,12 @@ void kin_oracle_philox_draws(uint64_t seed, int kind, double mean, int n, uint64
   }
 }
 
+// n_draws Binomial(n_trials, p) draws from one stream (KIN_FIRING_BINOMIAL sampler).
+void kin_oracle_binomial_draws(uint64_t seed, uint64_t n_trials, double p, int n_draws, uint64_t* out) {
+  Stream r(seed);
+  for (int q = 0; q < n_draws; ++q) out[q] = binomial_from(r, n_trials, p, nullptr);
+}
+
 // One stream: n_each draw_poisson for each mean in order, then n_normal
 // draw_normal (SURVEY Appendix A flag-insensitivity digest).  Normals as bits.
 void kin_oracle_rng_sequence(uint64_t seed, const double* means, int n_means, int n_each, int n_normal,
@@ -1647,6 +1692,45 @@ int kin_oracle_rre_rhs(const kin_model_desc* d, const double* x, double* dx, kin
   return KIN_OK;
 }
 
+// rk_step (deterministic.hpp:26-36): one Dormand-Prince 5(4) step of size h
+// from x with k1 = f(x) — the stage/error expressions of integrate_rre above.
+// out: y5[N], err (sqrt(mean((e_i/sk_i)^2)), sk_i = atol + rtol*max(|y_i|,|y5_i|)),
+// then k7 = f(y5)[N].
+int kin_oracle_rk_step(const kin_model_desc* d, const double* x, double h, double rtol, double atol, double* out,
+                       kin_error* err) {
+  using namespace dp;
+  Network net;
+  if (int rc = load(d, &net, err)) return rc;
+  const int n = net.n;
+  std::vector<double> r(net.m), a(net.m);
+  for (int j = 0; j < net.m; ++j) r[j] = net.rate_param[j] >= 0 ? net.params[net.rate_param[j]] : net.rate_base[j];
+  std::vector<double> y(x, x + n), k1(n), k2(n), k3(n), k4(n), k5(n), k6(n), k7(n), ys(n), yn(n);
+  rre_rhs<false>(net, r.data(), y.data(), a.data(), k1.data(), nullptr);
+  for (int i = 0; i < n; ++i) ys[i] = y[i] + h * (a21 * k1[i]);
+  rre_rhs<false>(net, r.data(), ys.data(), a.data(), k2.data(), nullptr);
+  for (int i = 0; i < n; ++i) ys[i] = y[i] + h * (a31 * k1[i] + a32 * k2[i]);
+  rre_rhs<false>(net, r.data(), ys.data(), a.data(), k3.data(), nullptr);
+  for (int i = 0; i < n; ++i) ys[i] = y[i] + h * (a41 * k1[i] + a42 * k2[i] + a43 * k3[i]);
+  rre_rhs<false>(net, r.data(), ys.data(), a.data(), k4.data(), nullptr);
+  for (int i = 0; i < n; ++i) ys[i] = y[i] + h * (a51 * k1[i] + a52 * k2[i] + a53 * k3[i] + a54 * k4[i]);
+  rre_rhs<false>(net, r.data(), ys.data(), a.data(), k5.data(), nullptr);
+  for (int i = 0; i < n; ++i) ys[i] = y[i] + h * (a61 * k1[i] + a62 * k2[i] + a63 * k3[i] + a64 * k4[i] + a65 * k5[i]);
+  rre_rhs<false>(net, r.data(), ys.data(), a.data(), k6.data(), nullptr);
+  for (int i = 0; i < n; ++i) yn[i] = y[i] + h * (a71 * k1[i] + a73 * k3[i] + a74 * k4[i] + a75 * k5[i] + a76 * k6[i]);
+  rre_rhs<false>(net, r.data(), yn.data(), a.data(), k7.data(), nullptr);
+  double sum = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double e = h * (e1 * k1[i] + e3 * k3[i] + e4 * k4[i] + e5 * k5[i] + e6 * k6[i] + e7 * k7[i]);
+    const double sk = atol + rtol * std::max(std::fabs(y[i]), std::fabs(yn[i]));
+    const double q = e / sk;
+    sum = sum + q * q;
+  }
+  for (int i = 0; i < n; ++i) out[i] = yn[i];
+  out[n] = std::sqrt(sum / static_cast<double>(n));
+  for (int i = 0; i < n; ++i) out[n + 1 + i] = k7[i];
+  return KIN_OK;
+}
+
 // Chan merge (ensemble.hpp:31-33,56-57) of b into a.
 void kin_oracle_stats_merge(uint64_t* na, double* mean_a, double* m2_a, uint64_t nb,
                             const double* mean_b, const double* m2_b, uint64_t len) {
@@ -1682,11 +1766,28 @@ int kin_oracle_sweep(const kin_model_desc* md, const kin_sweep_desc* d, kin_swee
   const std::uint64_t s0 = d->sim_begin;
   const std::uint64_t s1 = d->sim_end == 0 ? L.n_sims : std::min<std::uint64_t>(d->sim_end, L.n_sims);
   if (s0 > s1) { set_err(err, KIN_ERR_USAGE, "empty or inverted simulation range"); return KIN_ERR_USAGE; }
-  const std::uint64_t S = s1 - s0;
+  // interleaved point shard (kin_abi.h kin_sweep_desc): local simulation s is
+  // run s % R of global point p_first + shard_index + (s / R) * shard_count
+  const bool sharded = d->shard_count > 1;
+  if (sharded && (d->shard_index < 0 || d->shard_index >= d->shard_count || s0 % L.runs || s1 % L.runs)) {
+    set_err(err, KIN_ERR_INPUT, "bad shard");
+    return KIN_ERR_INPUT;
+  }
+  const std::uint64_t R = L.runs;
+  std::uint64_t S = s1 - s0;
+  if (sharded) {
+    const std::uint64_t P = S / R, n = static_cast<std::uint64_t>(d->shard_count);
+    S = (P > static_cast<std::uint64_t>(d->shard_index) ? (P - d->shard_index + n - 1) / n : 0) * R;
+  }
+  auto global_of = [&](std::uint64_t s) -> std::uint64_t {
+    if (!sharded) return s0 + s;
+    const std::uint64_t k = s / R;
+    return (s0 / R + d->shard_index + static_cast<std::uint64_t>(d->shard_count) * k) * R + (s - k * R);
+  };
   const int G = d->n_grid, N = net.n;
   const size_t per = static_cast<size_t>(G) * N;
   std::vector<double> tmp_traj;
-  double* traj = out ? out->traj : nullptr;
+  double* traj = (out && d->output_mode != KIN_OUTPUT_STATS_ONLY) ? out->traj : nullptr;
   const bool need_stats = out && (out->mean || out->m2);
   if (!traj && need_stats) { tmp_traj.resize(S * per); traj = tmp_traj.data(); }
   std::vector<std::uint64_t> tmp_meta;
@@ -1699,20 +1800,21 @@ int kin_oracle_sweep(const kin_model_desc* md, const kin_sweep_desc* d, kin_swee
     sc.resize(N, net.m);
     std::vector<double> scratch_traj(per);
     std::uint64_t meta_local[6];
-    for (std::uint64_t s = lo; s < hi; ++s) {
-      double* tr = traj ? traj + (s - s0) * per : scratch_traj.data();
-      std::uint64_t* me = (out && out->meta) ? out->meta + (s - s0) * 6 : meta_local;
+    for (std::uint64_t s = lo; s < hi; ++s) {  // s: local index
+      double* tr = traj ? traj + s * per : scratch_traj.data();
+      std::uint64_t* me = (out && out->meta) ? out->meta + s * 6 : meta_local;
       Work w;
-      const int st = count ? run_one<true>(net, d, s, tr, me, sc, &w) : run_one<false>(net, d, s, tr, me, sc, nullptr);
-      status[s - s0] = st;
-      if (count) out->work[s - s0] = w.flops;
+      const std::uint64_t g = global_of(s);
+      const int st = count ? run_one<true>(net, d, g, tr, me, sc, &w) : run_one<false>(net, d, g, tr, me, sc, nullptr);
+      status[s] = st;
+      if (count) out->work[s] = w.flops;
     }
   };
   std::vector<std::thread> pool;
   const std::uint64_t chunk = (S + workers - 1) / std::max(workers, 1);
   for (int wk = 0; wk < workers; ++wk) {
-    const std::uint64_t lo = s0 + std::min<std::uint64_t>(S, wk * chunk);
-    const std::uint64_t hi = s0 + std::min<std::uint64_t>(S, (wk + 1) * chunk);
+    const std::uint64_t lo = std::min<std::uint64_t>(S, wk * chunk);
+    const std::uint64_t hi = std::min<std::uint64_t>(S, (wk + 1) * chunk);
     if (lo >= hi) continue;
     if (workers == 1) body(lo, hi); else pool.emplace_back(body, lo, hi);
   }
@@ -1720,7 +1822,7 @@ int kin_oracle_sweep(const kin_model_desc* md, const kin_sweep_desc* d, kin_swee
   if (out && out->status) for (std::uint64_t s = 0; s < S; ++s) out->status[s] = status[s];
   for (std::uint64_t s = 0; s < S; ++s) {
     if (status[s] != KIN_SIM_OK) {
-      const std::uint64_t g = s0 + s;
+      const std::uint64_t g = global_of(s);
       if (err) {
         err->code = KIN_ERR_SIMULATION;
         err->sim_status = status[s];
@@ -1734,14 +1836,16 @@ int kin_oracle_sweep(const kin_model_desc* md, const kin_sweep_desc* d, kin_swee
     }
   }
   if (need_stats) {
-    const std::uint64_t p0 = (s0 + L.runs - 1) / L.runs;
-    const std::uint64_t p1 = s1 / L.runs;
+    // local points: whole points of the local index space (a shard is whole points)
+    const std::uint64_t p0 = sharded ? 0 : (s0 + L.runs - 1) / L.runs;
+    const std::uint64_t p1 = sharded ? S / L.runs : s1 / L.runs;
+    const std::uint64_t first = sharded ? 0 : s0;  // global index of local simulation 0
     for (std::uint64_t p = p0; p < p1; ++p) {
       double* mean = out->mean ? out->mean + (p - p0) * per : nullptr;
       double* m2 = out->m2 ? out->m2 + (p - p0) * per : nullptr;
       std::vector<double> mv(per, 0.0), qv(per, 0.0);
       for (std::uint64_t r = 0; r < L.runs; ++r)
-        welford_add(r + 1, traj + (p * L.runs + r - s0) * per, mv.data(), qv.data(), per);
+        welford_add(r + 1, traj + (p * L.runs + r - first) * per, mv.data(), qv.data(), per);
       if (mean) std::memcpy(mean, mv.data(), per * sizeof(double));
       if (m2) std::memcpy(m2, qv.data(), per * sizeof(double));
     }

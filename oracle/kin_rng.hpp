@@ -18,6 +18,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include "kin_portable_math.hpp"
+
 #ifdef KIN_ORACLE_REF_RNG
 #include "kinetics/rng.hpp"
 #endif
@@ -125,6 +127,126 @@ std::uint64_t poisson_from(Src& src, double mean, std::uint64_t* flops) {
     if (flops) *flops += 11;
     if (lhs <= rhs) return static_cast<std::uint64_t>(kf);
   }
+}
+
+// ---- binomial draws (KIN_FIRING_BINOMIAL; no reference counterpart: the
+// north star's "Poisson/binomial reaction firing").  Binomial(n, p) over any
+// uniform source: BINV inversion (Kachitvichyanukul & Schmeiser 1988) when
+// n*min(p,1-p) < 10, else Hormann's BTRD (1993); p > 1/2 draws n - Bin(n, 1-p).
+// Only correctly rounded operations and the portable log/exp
+// (kin_portable_math.hpp), so the CUDA sampler (kin_device.cuh binomial())
+// reproduces every draw bit for bit.  Flop counting as draw_poisson's.
+inline double binom_fc(double k) {  // Stirling correction of ln k! (Hormann 1993, table for k < 10)
+  static constexpr double kTab[10] = {0.08106146679532726, 0.04134069595540929, 0.02767792568499834,
+                                      0.02079067210376509, 0.01664469118982119, 0.01387612882307075,
+                                      0.01189670994589177, 0.01041126526197209, 0.009255462182712733,
+                                      0.008330563433362871};
+  if (k < 10.0) return kTab[static_cast<int>(k)];
+  const double rk = 1.0 / (k + 1.0);
+  const double rk2 = rk * rk;
+  return (1.0 / 12.0 - (1.0 / 360.0 - rk2 / 1260.0) * rk2) * rk;
+}
+
+template <class Src>
+std::uint64_t binomial_from(Src& src, std::uint64_t n, double p, std::uint64_t* flops) {
+  if (n == 0 || !(p > 0.0)) return 0;
+  if (p >= 1.0) return n;
+  const bool flip = p > 0.5;
+  const double q = flip ? 1.0 - p : p;
+  const double fn = static_cast<double>(n);
+  const double np = fn * q;
+  std::uint64_t fl = flip ? 2 : 1;
+  std::uint64_t k = 0;
+  if (np < 10.0) {  // BINV: one uniform, CDF search
+    const double s = q / (1.0 - q);
+    const double a = (fn + 1.0) * s;
+    double f = pm_exp(fn * pm_log(1.0 - q));
+    double c = f;
+    const double u = src.draw_uniform();
+    const std::uint64_t kmax = n < 255 ? n : 255;
+    while (u > c && k < kmax) {
+      ++k;
+      f = f * (a / static_cast<double>(k) - s);
+      c = c + f;
+    }
+    fl += 10 + 4 * k;
+  } else {  // BTRD
+    const double m = std::floor((fn + 1.0) * q);
+    const double r = q / (1.0 - q);
+    const double nr = (fn + 1.0) * r;
+    const double npq = np * (1.0 - q);
+    const double spq = std::sqrt(npq);
+    const double b = 1.15 + 2.53 * spq;
+    const double a = -0.0873 + 0.0248 * b + 0.01 * q;
+    const double c = np + 0.5;
+    const double alpha = (2.83 + 5.1 / b) * spq;
+    const double vr = 0.92 - 4.2 / b;
+    const double urvr = 0.86 * vr;
+    fl += 22;
+    for (;;) {
+      double v = src.draw_uniform();
+      double u;
+      fl += 2;
+      if (v <= urvr) {
+        u = v / vr - 0.43;
+        const double kf = std::floor((2.0 * a / (0.5 - std::fabs(u)) + b) * u + c);
+        fl += 8;
+        k = kf < 0.0 ? 0 : (kf > fn ? n : static_cast<std::uint64_t>(kf));
+        break;
+      }
+      if (v >= vr) {
+        u = src.draw_uniform() - 0.5;
+        fl += 3;
+      } else {
+        u = v / vr - 0.93;
+        u = (u < 0.0 ? -0.5 : 0.5) - u;
+        v = src.draw_uniform() * vr;
+        fl += 6;
+      }
+      const double us = 0.5 - std::fabs(u);
+      const double kf = std::floor((2.0 * a / us + b) * u + c);
+      fl += 6;
+      if (kf < 0.0 || kf > fn) continue;
+      v = v * alpha / (a / (us * us) + b);
+      const double km = std::fabs(kf - m);
+      fl += 6;
+      if (km <= 15.0) {  // recursive f(k)/f(m)
+        double f = 1.0;
+        if (m < kf) {
+          double i = m;
+          do {
+            i = i + 1.0;
+            f = f * (nr / i - r);
+            fl += 4;
+          } while (i != kf);
+        } else if (m > kf) {
+          double i = kf;
+          do {
+            i = i + 1.0;
+            v = v * (nr / i - r);
+            fl += 4;
+          } while (i != m);
+        }
+        if (v <= f) { k = static_cast<std::uint64_t>(kf); break; }
+        continue;
+      }
+      v = pm_log(v);  // squeeze, then the final acceptance test
+      const double rho = (km / npq) * (((km / 3.0 + 0.625) * km + 1.0 / 6.0) / npq + 0.5);
+      const double t = -km * km / (2.0 * npq);
+      fl += 13;
+      if (v < t - rho) { k = static_cast<std::uint64_t>(kf); break; }
+      if (v > t + rho) continue;
+      const double nm = fn - m + 1.0;
+      const double h = (m + 0.5) * pm_log((m + 1.0) / (r * nm)) + binom_fc(m) + binom_fc(fn - m);
+      const double nk = fn - kf + 1.0;
+      const double rhs = h + (fn + 1.0) * pm_log(nm / nk) + (kf + 0.5) * pm_log(nk * r / (kf + 1.0)) -
+                         binom_fc(kf) - binom_fc(fn - kf);
+      fl += 54;
+      if (v <= rhs) { k = static_cast<std::uint64_t>(kf); break; }
+    }
+  }
+  if (flops) *flops += fl;
+  return flip ? n - k : k;
 }
 
 inline std::uint64_t Xoshiro256pp::draw_poisson(double mean, std::uint64_t* flops) {

@@ -49,6 +49,9 @@ def load(ref: bool = False) -> C.CDLL:
     lib.kin_oracle_rng_draws.argtypes = [C.c_uint64, C.c_int, C.c_double, C.c_int, u64p]
     lib.kin_oracle_rng_sequence.restype = None
     lib.kin_oracle_rng_sequence.argtypes = [C.c_uint64, f64p, C.c_int, C.c_int, C.c_int, u64p]
+    lib.kin_oracle_binomial_draws.restype = None
+    lib.kin_oracle_binomial_draws.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_int, u64p]
+    lib.kin_oracle_rk_step.argtypes = [M, f64p, C.c_double, C.c_double, C.c_double, f64p, E]
     lib.kin_oracle_philox_block.restype = None
     lib.kin_oracle_philox_block.argtypes = [C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
     lib.kin_oracle_philox_draws.restype = None
@@ -82,6 +85,24 @@ def rng_draws_sequence(seed: int, means, n_each: int, n_normal: int, ref: bool =
     out = np.zeros(len(m) * n_each + n_normal, dtype=np.uint64)
     load(ref).kin_oracle_rng_sequence(seed, abi.ptr(m, C.c_double), len(m), n_each, n_normal, abi.ptr(out, C.c_uint64))
     return out
+
+
+def binomial_draws(seed: int, n_trials: int, p: float, n: int, ref: bool = False) -> np.ndarray:
+    out = np.zeros(n, dtype=np.uint64)
+    load(ref).kin_oracle_binomial_draws(seed, int(n_trials), float(p), n, abi.ptr(out, C.c_uint64))
+    return out
+
+
+def rk_step(net, x, h, rtol=1e-6, atol=1e-9):
+    """rk_step (deterministic.hpp:26-36): (y5, err, k7)."""
+    x = _f64(x)
+    n = len(x)
+    out = np.zeros(2 * n + 1)
+    err = abi.KinError()
+    rc = load().kin_oracle_rk_step(C.byref(net.desc()), abi.ptr(x, C.c_double), float(h), float(rtol), float(atol),
+                                   abi.ptr(out, C.c_double), C.byref(err))
+    assert rc == 0, err.text()
+    return out[:n], float(out[n]), out[n + 1:]
 
 
 def philox_block(key, ctr):
@@ -197,7 +218,7 @@ def stats_merge(na, mean_a, m2_a, nb, mean_b, m2_b):
 
 
 def sweep(net, sdesc, *, workers: int | None = None, want_traj=True, want_stats=False, want_work=False,
-          ref: bool = False, raise_on_error=True):
+          ref: bool = False, raise_on_error=True, out: dict | None = None):
     """Run a kin_sweep_desc on the CPU oracle.  Returns dict of numpy arrays
     (traj [S,G,N], meta [S,6], status [S], mean/m2 [P,G,N], work [S])."""
     lib = load(ref)
@@ -207,12 +228,21 @@ def sweep(net, sdesc, *, workers: int | None = None, want_traj=True, want_stats=
     if rc:
         raise ValueError(err.text())
     s0 = sdesc.sim_begin
-    s1 = sdesc.sim_end or nsims.value
-    S = s1 - s0
+    s1 = min(sdesc.sim_end, nsims.value) if sdesc.sim_end else nsims.value
     G, N = sdesc.n_grid, net.species_count()
     R = sdesc.runs_per_point
-    P = max(0, s1 // R - (s0 + R - 1) // R)
-    res = {
+    if sdesc.shard_count > 1:  # interleaved point shard: compact local layout
+        n_pts = (s1 - s0) // R
+        P = (n_pts - sdesc.shard_index + sdesc.shard_count - 1) // sdesc.shard_count if n_pts > sdesc.shard_index else 0
+        S = P * R
+    else:
+        S = s1 - s0
+        P = max(0, s1 // R - (s0 + R - 1) // R)
+    if out is not None and out.get("traj") is not None and out["traj"].shape == (S, G, N):
+        res = out  # caller-owned arrays of the right shapes (repeated timing passes)
+    else:
+        res = None
+    res = res or {
         "traj": np.zeros((S, G, N)) if want_traj else None,
         "meta": np.zeros((S, 6), dtype=np.uint64),
         "status": np.zeros(S, dtype=np.int32),

@@ -24,6 +24,11 @@ METHOD_SSA, METHOD_TAU_ADAPTIVE, METHOD_TAU_FIXED, METHOD_CLE, METHOD_ODE, METHO
 AXIS_PARAM, AXIS_INITIAL = 0, 1
 RNG_COMPAT, RNG_PHILOX = 0, 1
 SEED_SWEEP, SEED_ENSEMBLE, SEED_DIRECT = 0, 1, 2
+FIRING_POISSON, FIRING_BINOMIAL = 0, 1
+OUTPUT_FULL, OUTPUT_STATS_ONLY = 0, 1
+# enum kin_variant (forced kernel choices; 0 = automatic)
+VARIANT_TABLE, VARIANT_JIT, VARIANT_DOUBLE_STATE = 1 << 0, 1 << 1, 1 << 2
+VARIANT_GLOBAL_STATE, VARIANT_SMEM_STATE, VARIANT_NO_SPLIT = 1 << 3, 1 << 4, 1 << 5
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
@@ -50,7 +55,7 @@ class KinIntegratorConfig(C.Structure):
 class KinMethod(C.Structure):
     _fields_ = [("kind", C.c_int32), ("tau", C.c_double), ("epsilon", C.c_double),
                 ("integrator", KinIntegratorConfig), ("theta_x", C.c_double), ("theta_a", C.c_double),
-                ("repartition_interval", C.c_double)]
+                ("repartition_interval", C.c_double), ("firing", C.c_int32)]
 
 
 class KinSweepAxis(C.Structure):
@@ -65,7 +70,16 @@ class KinSweepDesc(C.Structure):
         ("seed_mode", C.c_int32), ("rng_mode", C.c_int32),
         ("t_end", C.c_double), ("n_grid", C.c_int32), ("grid", f64p),
         ("sim_begin", C.c_uint64), ("sim_end", C.c_uint64),
+        ("shard_index", C.c_int32), ("shard_count", C.c_int32), ("output_mode", C.c_int32),
+        ("lanes_per_sim", C.c_int32), ("variant", C.c_uint32), ("reserved_", C.c_int32),
     ]
+
+
+class KinSweepPart(C.Structure):
+    """kin_sweep_part: one device's share of a call (the partitioner's plan)."""
+    _fields_ = [("device", C.c_int32), ("interleaved", C.c_int32), ("sim_begin", C.c_uint64),
+                ("sim_end", C.c_uint64), ("pt_first", C.c_uint64), ("pt_stride", C.c_uint64),
+                ("n_points", C.c_uint64), ("out_first", C.c_uint64), ("out_pitch", C.c_uint64)]
 
 
 class KinSweepOut(C.Structure):
@@ -101,7 +115,7 @@ ABI_SYMBOLS = (
     "kin_model_text_param_index", "kin_model_render",
     "kin_format_double", "kin_fnv1a64", "kin_fnv1a64_update", "kin_csv_render", "kin_csv_write",
     "kin_device_unit", "kin_ensemble_run", "kin_run_single", "kin_stats_merge", "kin_visible_devices", "kin_ctx_create", "kin_ctx_destroy", "kin_ctx_device_count", "kin_model_upload",
-    "kin_model_free", "kin_sweep_size", "kin_sweep_plan", "kin_sweep_run", "kin_sweep_submit", "kin_sweep_wait", "kin_sweep_launch", "kin_sweep_sync",
+    "kin_model_free", "kin_sweep_size", "kin_sweep_local_size", "kin_sweep_plan", "kin_device_binomial_draws", "kin_sweep_run", "kin_sweep_submit", "kin_sweep_wait", "kin_sweep_launch", "kin_sweep_sync",
     "kin_sweep_fetch", "kin_ctx_stream", "kin_sweep_kernel_ms", "kin_sweep_kernel_name", "kin_splitmix64_mix", "kin_derive_run_seed",
     "kin_device_rng_draws", "kin_jit_check", "kin_measure_fp64_peak", "kin_status_string", "kin_abi_version",
 )
@@ -124,7 +138,10 @@ def _declare(lib: C.CDLL) -> C.CDLL:
         "kin_model_upload": (C.c_int, [vp, C.POINTER(KinModelDesc), C.POINTER(vp), E]),
         "kin_model_free": (None, [vp]),
         "kin_sweep_size": (C.c_int, [C.POINTER(KinSweepDesc), u64p, u64p, E]),
-        "kin_sweep_plan": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, u64p, i32p, E]),
+        "kin_sweep_local_size": (C.c_int, [C.POINTER(KinSweepDesc), u64p, u64p, E]),
+        "kin_sweep_plan": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                     C.POINTER(KinSweepPart), i32p, E]),
+        "kin_device_binomial_draws": (C.c_int, [vp, C.c_uint64, C.c_uint64, C.c_double, C.c_int32, u64p, E]),
         "kin_sweep_run": (C.c_int, [vp, vp, C.POINTER(KinSweepDesc), C.POINTER(KinSweepOut), E]),
         "kin_sweep_submit": (C.c_int, [vp, vp, C.POINTER(KinSweepDesc), C.POINTER(KinSweepOut), u64p, E]),
         "kin_sweep_wait": (C.c_int, [vp, C.c_uint64, E]),

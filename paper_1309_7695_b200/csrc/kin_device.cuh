@@ -15,6 +15,7 @@
 #endif
 
 #include "kin_tables.h"
+#include "kin_pmath.cuh"
 #include "../../include/kin_abi.h"
 
 namespace kin {
@@ -77,6 +78,15 @@ __host__ __device__ __forceinline__ uint64_t splitmix64_mix(uint64_t v) {
 }
 __host__ __device__ __forceinline__ uint64_t derive_run_seed(uint64_t master, uint64_t i) {
   return splitmix64_mix(master + i * kPhi64);
+}
+
+// Global simulation index of launch-local simulation s (kin_tables.h
+// KinSweepDev: contiguous or interleaved parts).
+__device__ __forceinline__ uint64_t global_sim(const KinSweepDev& S, uint64_t s) {
+  const uint64_t l = S.local_begin + s;
+  if (S.pt_stride == 0) return S.sim_begin + l;
+  const uint64_t k = l / S.runs;
+  return (S.pt_first + k * S.pt_stride) * S.runs + (l - k * S.runs);
 }
 
 // Seed of global simulation `sim` (kin_abi.h enum kin_seed_mode).
@@ -317,6 +327,139 @@ __device__ __forceinline__ uint64_t poisson(Rng& rng, double mean, uint64_t& flo
     const double lhs = log(arg);
     if (lhs <= rhs) return static_cast<uint64_t>(kf);
   }
+}
+
+// ---- Binomial(n, p) (KIN_FIRING_BINOMIAL): BINV inversion when
+// n*min(p,1-p) < 10, Hormann's BTRD otherwise; p > 1/2 draws n - Bin(n, 1-p).
+// Mirrors oracle/kin_rng.hpp binomial_from operation for operation (this code
+// is compiled with -fmad=false and uses the portable log/exp), so every draw
+// and its flop count are bit-identical to the oracle's.
+__device__ __forceinline__ double binom_fc(double k) {
+  if (k < 10.0) {
+    switch (static_cast<int>(k)) {
+      case 0: return 0.08106146679532726;
+      case 1: return 0.04134069595540929;
+      case 2: return 0.02767792568499834;
+      case 3: return 0.02079067210376509;
+      case 4: return 0.01664469118982119;
+      case 5: return 0.01387612882307075;
+      case 6: return 0.01189670994589177;
+      case 7: return 0.01041126526197209;
+      case 8: return 0.009255462182712733;
+      default: return 0.008330563433362871;
+    }
+  }
+  const double rk = 1.0 / (k + 1.0);
+  const double rk2 = rk * rk;
+  return (1.0 / 12.0 - (1.0 / 360.0 - rk2 / 1260.0) * rk2) * rk;
+}
+
+template <class Rng>
+static __device__ __noinline__ uint64_t binomial_btrd(Rng& rng, double fn, double q, double np, uint64_t& fl) {
+  using pmath::pm_log;
+  const uint64_t n = static_cast<uint64_t>(fn);
+  const double m = floor((fn + 1.0) * q);
+  const double r = q / (1.0 - q);
+  const double nr = (fn + 1.0) * r;
+  const double npq = np * (1.0 - q);
+  const double spq = sqrt(npq);
+  const double b = 1.15 + 2.53 * spq;
+  const double a = -0.0873 + 0.0248 * b + 0.01 * q;
+  const double c = np + 0.5;
+  const double alpha = (2.83 + 5.1 / b) * spq;
+  const double vr = 0.92 - 4.2 / b;
+  const double urvr = 0.86 * vr;
+  fl += 22;
+  for (;;) {
+    double v = rng.uniform();
+    double u;
+    fl += 2;
+    if (v <= urvr) {
+      u = v / vr - 0.43;
+      const double kf = floor((2.0 * a / (0.5 - fabs(u)) + b) * u + c);
+      fl += 8;
+      return kf < 0.0 ? 0 : (kf > fn ? n : static_cast<uint64_t>(kf));
+    }
+    if (v >= vr) {
+      u = rng.uniform() - 0.5;
+      fl += 3;
+    } else {
+      u = v / vr - 0.93;
+      u = (u < 0.0 ? -0.5 : 0.5) - u;
+      v = rng.uniform() * vr;
+      fl += 6;
+    }
+    const double us = 0.5 - fabs(u);
+    const double kf = floor((2.0 * a / us + b) * u + c);
+    fl += 6;
+    if (kf < 0.0 || kf > fn) continue;
+    v = v * alpha / (a / (us * us) + b);
+    const double km = fabs(kf - m);
+    fl += 6;
+    if (km <= 15.0) {
+      double f = 1.0;
+      if (m < kf) {
+        double i = m;
+        do {
+          i = i + 1.0;
+          f = f * (nr / i - r);
+          fl += 4;
+        } while (i != kf);
+      } else if (m > kf) {
+        double i = kf;
+        do {
+          i = i + 1.0;
+          v = v * (nr / i - r);
+          fl += 4;
+        } while (i != m);
+      }
+      if (v <= f) return static_cast<uint64_t>(kf);
+      continue;
+    }
+    v = pm_log(v);
+    const double rho = (km / npq) * (((km / 3.0 + 0.625) * km + 1.0 / 6.0) / npq + 0.5);
+    const double t = -km * km / (2.0 * npq);
+    fl += 13;
+    if (v < t - rho) return static_cast<uint64_t>(kf);
+    if (v > t + rho) continue;
+    const double nm = fn - m + 1.0;
+    const double h = (m + 0.5) * pm_log((m + 1.0) / (r * nm)) + binom_fc(m) + binom_fc(fn - m);
+    const double nk = fn - kf + 1.0;
+    const double rhs = h + (fn + 1.0) * pm_log(nm / nk) + (kf + 0.5) * pm_log(nk * r / (kf + 1.0)) - binom_fc(kf) -
+                       binom_fc(fn - kf);
+    fl += 54;
+    if (v <= rhs) return static_cast<uint64_t>(kf);
+  }
+}
+
+template <bool kCount, class Rng>
+__device__ __forceinline__ uint64_t binomial(Rng& rng, uint64_t n, double p, uint64_t& flops) {
+  if (n == 0 || !(p > 0.0)) return 0;
+  if (p >= 1.0) return n;
+  const bool flip = p > 0.5;
+  const double q = flip ? 1.0 - p : p;
+  const double fn = static_cast<double>(n);
+  const double np = fn * q;
+  uint64_t fl = flip ? 2 : 1;
+  uint64_t k = 0;
+  if (np < 10.0) {  // BINV
+    const double s = q / (1.0 - q);
+    const double a = (fn + 1.0) * s;
+    double f = pmath::pm_exp(fn * pmath::pm_log(1.0 - q));
+    double c = f;
+    const double u = rng.uniform();
+    const uint64_t kmax = n < 255 ? n : 255;
+    while (u > c && k < kmax) {
+      ++k;
+      f = f * (a / static_cast<double>(k) - s);
+      c = c + f;
+    }
+    fl += 10 + 4 * k;
+  } else {
+    k = binomial_btrd(rng, fn, q, np, fl);
+  }
+  if (kCount) flops += fl;
+  return flip ? n - k : k;
 }
 
 // x(x-1)(x-2)/6: out of line, so the runtime-stoichiometry propensity loops

@@ -47,6 +47,109 @@ void set_err(kin_error* e, int code, const std::string& msg) {
   std::snprintf(e->message, sizeof(e->message), "%s", msg.c_str());
 }
 
+// Kernel-variant choices come from kin_sweep_desc (lanes_per_sim, variant);
+// these environment variables are TEST/STUDY overrides only, read once per
+// process (never per launch): -1 / 0 = not set.
+struct EnvOverrides {
+  int int_state = -1, gstate = -1, gstate_split = -1, hybrid_gstate = -1, lsoda_gstate = -1;
+  int ode_lanes = 0, group_lanes = 0;
+};
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoi(v) : dflt;
+}
+
+const EnvOverrides& env_overrides() {
+  static const EnvOverrides ov = [] {
+    EnvOverrides o;
+    o.int_state = env_int("KIN_INT_STATE", -1);
+    o.gstate = env_int("KIN_GSTATE", -1);
+    o.gstate_split = env_int("KIN_GSTATE_SPLIT", -1);
+    o.hybrid_gstate = env_int("KIN_HYBRID_GSTATE", -1);
+    o.lsoda_gstate = env_int("KIN_LSODA_GSTATE", -1);
+    o.ode_lanes = env_int("KIN_ODE_LANES", 0);
+    o.group_lanes = env_int("KIN_GROUP_LANES", 0);
+    return o;
+  }();
+  return ov;
+}
+
+// ---- the partitioner (kin_abi.h kin_sweep_plan) ---------------------------------
+// The reference's worker pool (contiguous run ranges per std::thread,
+// ensemble.hpp:91-96) becomes the context's devices.
+struct PlanPart {
+  int dev = 0;
+  bool inter = false;
+  uint64_t s0 = 0, s1 = 0;                       // contiguous
+  uint64_t pt_first = 0, pt_stride = 0, n_pts = 0;  // interleaved
+  uint64_t out_first = 0, out_pitch = 0;         // caller-local sims
+};
+
+int plan_parts(uint64_t s0, uint64_t s1, uint64_t R, int D, int sh_i, int sh_n, std::vector<PlanPart>* parts,
+               std::string* msg) {
+  parts->clear();
+  if (R == 0 || D < 1 || s1 < s0) { *msg = "bad plan arguments"; return KIN_ERR_USAGE; }
+  if (sh_n <= 1) { sh_n = 1; sh_i = 0; }
+  if (sh_i < 0 || sh_i >= sh_n) { *msg = "shard_index out of range"; return KIN_ERR_INPUT; }
+  const uint64_t S = s1 - s0;
+  const bool whole = s0 % R == 0 && s1 % R == 0;
+  if (sh_n > 1 && !whole) { *msg = "a sharded call needs a range of whole points"; return KIN_ERR_INPUT; }
+  if (S == 0) return KIN_OK;
+  const uint64_t P0 = s0 / R, P1 = s1 / R;
+  if (sh_n > 1 || (whole && D > 1 && P1 - P0 >= static_cast<uint64_t>(D))) {
+    // interleaved: device d takes the caller's points d, d+D, ... (cyclic by point)
+    const uint64_t n = static_cast<uint64_t>(sh_n);
+    const uint64_t K = P1 - P0 > static_cast<uint64_t>(sh_i) ? (P1 - P0 - sh_i + n - 1) / n : 0;
+    for (int d = 0; d < D; ++d) {
+      if (K <= static_cast<uint64_t>(d)) break;
+      PlanPart p;
+      p.dev = d;
+      p.inter = true;
+      p.pt_first = P0 + sh_i + n * d;
+      p.pt_stride = n * D;
+      p.n_pts = (K - d + D - 1) / D;
+      p.out_first = static_cast<uint64_t>(d) * R;
+      p.out_pitch = static_cast<uint64_t>(D) * R;
+      if (D == 1 && n == 1) {  // one device, no shard: a plain contiguous range
+        p.inter = false;
+        p.s0 = s0;
+        p.s1 = s1;
+        p.out_first = 0;
+      }
+      parts->push_back(p);
+    }
+    return KIN_OK;
+  }
+  std::vector<uint64_t> bounds{s0};
+  const uint64_t points = (s1 - 1) / R - s0 / R + 1;  // points the range touches
+  if (D > 1 && points < static_cast<uint64_t>(D)) {
+    // fewer points than devices (run_ensemble): split the runs evenly; the
+    // statistics of a point cut by a part edge are Chan-merged across its parts
+    const uint64_t n_chunks = std::min<uint64_t>(S, static_cast<uint64_t>(D));
+    for (uint64_t c = 1; c < n_chunks; ++c) bounds.push_back(s0 + S * c / n_chunks);
+  } else if (D > 1) {
+    // a range that cuts points: D whole-point chunks (edges snapped to points)
+    for (int c = 1; c < D; ++c) {
+      uint64_t b = s0 + S * c / D;
+      b = (b + R - 1) / R * R;
+      b = std::min(std::max(b, bounds.back()), s1);
+      bounds.push_back(b);
+    }
+  }
+  bounds.push_back(s1);
+  for (size_t c = 0; c + 1 < bounds.size(); ++c) {
+    if (bounds[c] >= bounds[c + 1]) continue;
+    PlanPart p;
+    p.dev = static_cast<int>(c % D);
+    p.s0 = bounds[c];
+    p.s1 = bounds[c + 1];
+    p.out_first = bounds[c] - s0;
+    parts->push_back(p);
+  }
+  return KIN_OK;
+}
+
 // ---- model (ReactionNetwork::create, model.hpp:47-53) -------------------------
 struct HostModel {
   int n = 0, m = 0;
@@ -219,6 +322,13 @@ int validate_sweep(const HostModel& net, const kin_sweep_desc* d, const Layout& 
   }
   if (d->seed_mode == KIN_SEED_DIRECT && L.S != 1) { *msg = "direct seeding needs exactly one simulation"; return KIN_ERR_INPUT; }
   if (d->rng_mode != KIN_RNG_COMPAT && d->rng_mode != KIN_RNG_PHILOX) { *msg = "unknown rng_mode"; return KIN_ERR_INPUT; }
+  if (M.firing != KIN_FIRING_POISSON && M.firing != KIN_FIRING_BINOMIAL) { *msg = "unknown firing law"; return KIN_ERR_INPUT; }
+  if (d->output_mode != KIN_OUTPUT_FULL && d->output_mode != KIN_OUTPUT_STATS_ONLY) { *msg = "unknown output_mode"; return KIN_ERR_INPUT; }
+  if (d->lanes_per_sim < 0 || d->lanes_per_sim > 32) { *msg = "lanes_per_sim must be in [0, 32]"; return KIN_ERR_INPUT; }
+  if (d->shard_count < 0 || (d->shard_count > 1 && (d->shard_index < 0 || d->shard_index >= d->shard_count))) {
+    *msg = "shard_index out of range";
+    return KIN_ERR_INPUT;
+  }
   return KIN_OK;
 }
 
@@ -427,8 +537,12 @@ struct Buffers {
   cudaEvent_t ev_done = nullptr, ev_copied = nullptr;
   bool timed_stats = false;
   uint64_t s0 = 0, s1 = 0, P0 = 0, nP = 0, R = 1;
+  PlanPart part;  // the caller-layout mapping of this launch (copy_out)
   int G = 0, N = 0;
   bool have_stats = false, have_work = false, valid = false;
+  bool stats_only = false;     // KIN_OUTPUT_STATS_ONLY launch: no trajectory copy-out
+  uint64_t base_point = 0, point_end = 0;  // device-resident form: the call's point range
+  uint64_t stats_row0 = 0;     // first whole point's row in mean/m2
   std::unique_ptr<KinTables> last_T;
   KinSweepDev last_SD{};
   KinOutDev last_O{};
@@ -489,7 +603,15 @@ struct Job {
   std::vector<Part> parts;
   kin_sweep_out out{};
   uint64_t s0 = 0, s1 = 0, base_point = 0;
+  uint64_t n_local = 0, np_local = 0;  // caller-local simulations / statistics points
+  int sh_i = 0, sh_n = 1;
   Layout L;
+  // global simulation index of caller-local simulation s
+  uint64_t global_of(uint64_t s) const {
+    if (sh_n <= 1) return s0 + s;
+    const uint64_t k = s / L.R;
+    return (s0 / L.R + sh_i + static_cast<uint64_t>(sh_n) * k) * L.R + (s - k * L.R);
+  }
   int32_t* status_pinned = nullptr;  // when the caller did not ask for status
   int rc = KIN_OK;
   kin_error err{};
@@ -507,6 +629,10 @@ struct kin_ctx {
 struct kin_model {
   kin_ctx* ctx;
   HostModel host;
+  // per-model JIT policies, one per sweep-axis binding of the rates (generated
+  // once, not per launch)
+  std::mutex jit_mu;
+  std::map<std::vector<int>, std::unique_ptr<kin::JitModel>> jit_cache;
 };
 
 namespace {
@@ -571,6 +697,33 @@ int copy_d2h(Slot& sl, cudaStream_t st, void* dst, const void* src, size_t bytes
   return KIN_OK;
 }
 
+// `rows` contiguous device rows of row_bytes each into host rows dpitch bytes
+// apart (an interleaved part's points into the caller's layout): one 2D copy
+// into pinned memory, else row by row through the staging path.
+int copy_d2h_rows(Slot& sl, cudaStream_t st, void* dst, size_t dpitch, const void* src, size_t row_bytes,
+                  uint64_t rows, bool sync, kin_error* err) {
+  if (rows == 0 || row_bytes == 0) return KIN_OK;
+  if (rows == 1 || dpitch == row_bytes) return copy_d2h(sl, st, dst, src, row_bytes * rows, sync, err);
+  if (is_pinned(dst)) {
+    KIN_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, row_bytes, row_bytes, rows, cudaMemcpyDeviceToHost, st), "D2H 2D");
+    if (sync) KIN_CUDA(cudaStreamSynchronize(st), "D2H sync");
+    return KIN_OK;
+  }
+  // pageable: gather whole rows through a pinned bounce buffer
+  const size_t piece = size_t{32} << 20;
+  const uint64_t per = std::max<uint64_t>(1, piece / row_bytes);
+  std::vector<char> tmp;
+  for (uint64_t r0 = 0; r0 < rows; r0 += per) {
+    const uint64_t nr = std::min<uint64_t>(per, rows - r0);
+    tmp.resize(nr * row_bytes);
+    if (int rc = copy_d2h(sl, st, tmp.data(), static_cast<const char*>(src) + r0 * row_bytes, nr * row_bytes, true, err))
+      return rc;
+    for (uint64_t r = 0; r < nr; ++r)
+      std::memcpy(static_cast<char*>(dst) + (r0 + r) * dpitch, tmp.data() + r * row_bytes, row_bytes);
+  }
+  return KIN_OK;
+}
+
 // Model structure + sweep binding for the per-model JIT kernel.
 kin::JitModel jit_model(const HostModel& H, const kin_sweep_desc* d) {
   kin::JitModel j;
@@ -609,35 +762,200 @@ kin::JitModel jit_model(const HostModel& H, const kin_sweep_desc* d) {
   return j;
 }
 
-// Launch the simulation kernels for global sims [s0, s1) on a slot (device-resident).
-// Statistics kernels of a launch (whole points, then the partial points).
+// The model's JIT policy for this sweep's rate bindings, built once per binding.
+const kin::JitModel& jit_model_cached(const kin_model* model, const kin_sweep_desc* d) {
+  kin_model* m = const_cast<kin_model*>(model);
+  std::vector<int> key(m->host.m, -1);
+  std::vector<int> param_axis(m->host.params.size(), -1);
+  for (int ax = 0; ax < d->n_axes; ++ax)
+    if (d->axes[ax].kind == KIN_AXIS_PARAM) param_axis[d->axes[ax].index] = ax;
+  for (int r = 0; r < m->host.m; ++r)
+    if (m->host.rate_param[r] >= 0) key[r] = param_axis[m->host.rate_param[r]];
+  std::lock_guard<std::mutex> lk(m->jit_mu);
+  auto it = m->jit_cache.find(key);
+  if (it != m->jit_cache.end()) return *it->second;
+  auto jm = std::make_unique<kin::JitModel>(jit_model(m->host, d));
+  kin::jit_prepare(jm.get());
+  const kin::JitModel& ref = *jm;
+  m->jit_cache.emplace(std::move(key), std::move(jm));
+  return ref;
+}
+
+// Statistics kernels of a FULL-mode launch (whole points, then the partial points).
 int launch_stats(Slot& sl, Buffers& bf, kin_error* err) {
+  (void)sl;
   const size_t gn = static_cast<size_t>(bf.last_gn);
   if (bf.have_stats) {
-    cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.R, bf.last_base, bf.nP, bf.mean.p, bf.m2.p,
+    cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.R, bf.last_base, bf.nP, 0, bf.mean.p, bf.m2.p,
                                             bf.st);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
   }
   for (int k = 0; k < bf.n_partial; ++k) {
-    cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.partial_n[k], bf.partial_base[k], 1,
+    cudaError_t e = kin::launch_point_stats(bf.traj.p, bf.last_gn, bf.partial_n[k], bf.partial_base[k], 1, 0,
                                             bf.pmean.p + k * gn, bf.pm2.p + k * gn, bf.st);
     if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
   }
   return KIN_OK;
 }
 
-int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc* d, const Layout& L, uint64_t s0,
-                 uint64_t s1, bool want_stats, bool want_work, kin_error* err, bool want_partials = false) {
+// The simulation kernel of one launch (SD.local_begin / SD.n_local select the
+// simulations; O is indexed from 0).  Picks the kernel variant from the method,
+// the descriptor (lanes_per_sim, variant flags), the model's size and — for
+// studies and tests only — the process's environment overrides.
+int launch_sim(Slot& sl, Buffers& bf, const kin_model* model, const kin_sweep_desc* d, KinTables& T,
+               KinSweepDev& SD, const KinOutDev& O, bool want_work, bool allow_int_state, kin_error* err) {
+  const HostModel& H = model->host;
+  const EnvOverrides& ov = env_overrides();
+  const uint32_t var = d->variant;
+  const uint64_t S = SD.n_local;
+  auto pick_gstate = [&](bool automatic, int env) {
+    if (var & KIN_VARIANT_GLOBAL_STATE) return true;
+    if (var & KIN_VARIANT_SMEM_STATE) return false;
+    if (env >= 0) return env != 0;
+    return automatic;
+  };
+  auto global_state_for = [&](size_t per_warp_doubles) -> int {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sl.device);
+    const uint64_t cap = std::min<uint64_t>((S + 31) / 32, static_cast<uint64_t>(sms) * 24);
+    KIN_CUDA(bf.gstate.ensure(cap * per_warp_doubles), "cudaMalloc simulation state");
+    SD.gstate = bf.gstate.p;
+    SD.gstate_warps = cap;
+    return KIN_OK;
+  };
+  cudaError_t e = cudaSuccess;
+  const int kind = d->method.kind;
+  bf.last_int_state = false;  // set below only by the int32-state stochastic launch
+  if (kind == KIN_METHOD_ODE) {
+    // lanes per simulation: the descriptor's, else by species count (ode_pick_lanes)
+    const int ode_lanes = d->lanes_per_sim > 0 ? d->lanes_per_sim : ov.ode_lanes;
+    e = kin::launch_dopri5(T, SD, O, want_work, ode_lanes, bf.st);
+    bf.kernel_name = "dopri5_kernel";
+  } else if (kind == KIN_METHOD_HYBRID) {
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
+    // the Dopri5 vectors per simulation: in global memory when a warp's state
+    // would take more than 48 KB of shared memory (<= 4 warps/SM, or no launch
+    // at all above 227 KB).  (Measured on C1, 20.6 KB/warp: shared 97.5 ms,
+    // global 100.4 ms.)
+    if (pick_gstate(kin::hybrid_smem_bytes(T, SD) > 48 * 1024, ov.hybrid_gstate))
+      if (int rc = global_state_for(kin::hybrid_state_doubles_per_warp(T, SD))) return rc;
+    e = kin::launch_hybrid(T, SD, O, want_work, bf.counter.p, bf.st);
+    bf.kernel_name = "hybrid_kernel";
+  } else if (kind == KIN_METHOD_CLE) {
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
+    e = kin::launch_cle(T, SD, O, want_work, bf.counter.p, bf.st);
+    bf.kernel_name = "cle_kernel";
+  } else if (kind == KIN_METHOD_LSODA) {
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
+    // Nordsieck array, Jacobian and LU per simulation: in global memory when a
+    // warp's state would take more than 48 KB of shared memory
+    if (pick_gstate(kin::lsoda_smem_bytes(T, SD) > 48 * 1024, ov.lsoda_gstate))
+      if (int rc = global_state_for(kin::lsoda_state_doubles_per_warp(T, SD))) return rc;
+    e = kin::launch_lsoda(T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, bf.st);
+    bf.kernel_name = "lsoda_kernel";
+  } else {
+    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
+    KIN_CUDA(bf.ovf.ensure(1), "cudaMalloc overflow flag");
+    // Philox mode: L lanes per simulation (the descriptor's lanes_per_sim; 1 =
+    // one thread per simulation).  Compat mode is one thread per simulation:
+    // the reference stream is sequential within a run.
+    int lanes = d->lanes_per_sim > 0 ? d->lanes_per_sim : ov.group_lanes;
+    if (d->rng_mode != KIN_RNG_PHILOX) {
+      if (d->lanes_per_sim > 1) {
+        set_err(err, KIN_ERR_INPUT, "lanes_per_sim > 1 needs rng_mode PHILOX for stochastic methods");
+        return KIN_ERR_INPUT;
+      }
+      lanes = 1;
+    } else if (lanes <= 0) {
+      lanes = kin::stochastic_group_pick_lanes(H.n, H.m);
+    }
+    if (SD.firing == KIN_FIRING_BINOMIAL) lanes = 1;  // the binomial leap is sequential over reactions
+    if (lanes != 1) {
+      e = kin::launch_stochastic_group(T, SD, O, want_work, lanes, bf.counter.p, bf.st);
+      bf.kernel_name = "stochastic_group_kernel";
+    } else {
+      // int32 amounts when every initial amount is far inside int32 range
+      double xmax = 0.0;
+      for (double v : H.x0) xmax = std::max(xmax, v);
+      for (int ax = 0; ax < d->n_axes; ++ax)
+        if (d->axes[ax].kind == KIN_AXIS_INITIAL)
+          for (int v = 0; v < d->axes[ax].n_values; ++v) xmax = std::max(xmax, d->axes[ax].values[v]);
+      bool int_state = allow_int_state && xmax < 1073741824.0 && !(var & KIN_VARIANT_DOUBLE_STATE) &&
+                       ov.int_state != 0;
+      // Large models: when a warp's state would take more than 24 KB of shared
+      // memory (fewer than ~9 resident warps per SM), keep it in global memory
+      // instead — same [slot][lane] layout, L1/L2-cached — and let registers
+      // set the residency.
+      const size_t smem_warp = static_cast<size_t>(T.m + SD.n_axes) * 32 * sizeof(double) +
+                               static_cast<size_t>(T.n) * 32 * (int_state ? sizeof(int32_t) : sizeof(double));
+      if (pick_gstate(smem_warp > 24 * 1024, ov.gstate)) {
+        // sized for double amounts: the int32-overflow re-run reuses it
+        if (int rc = global_state_for(static_cast<size_t>(T.m + SD.n_axes + T.n) * 32)) return rc;
+        // amounts in shared memory, propensities in global (JIT kernel only;
+        // it applies the size rule)
+        SD.gstate_x_smem = !(var & KIN_VARIANT_NO_SPLIT) && ov.gstate_split != 0;
+      }
+      KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), bf.st), "memset");
+      bool used = false;
+      const int force_jit = (var & KIN_VARIANT_TABLE) ? 0 : ((var & KIN_VARIANT_JIT) ? 1 : -1);
+      if (kin::jit_wanted(S, force_jit)) {
+        const kin::JitModel& jm = jit_model_cached(model, d);
+        e = kin::launch_stochastic_jit(jm, T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, bf.st, &used);
+      }
+      if (e == cudaSuccess && !used)
+        e = kin::launch_stochastic(T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, bf.st);
+      bf.last_jit = used;
+      bf.kernel_name = used ? "kin_jit_stoch" : "stochastic_kernel";
+      bf.last_int_state = int_state;
+    }
+    if (bf.last_int_state) {
+      if (!bf.last_T) bf.last_T.reset(new KinTables);
+      *bf.last_T = T;
+      bf.last_SD = SD;
+      bf.last_O = O;
+      bf.last_count = want_work;
+    }
+  }
+  if (e == cudaErrorInvalidConfiguration) {
+    // the launchers' own pre-check: the per-simulation state of this model does
+    // not fit the kernel's shared-memory budget (a property of the input)
+    cudaGetLastError();
+    set_err(err, KIN_ERR_INPUT,
+            std::string("model too large for the ") + bf.kernel_name +
+                " (per-simulation state exceeds the shared-memory budget)");
+    return KIN_ERR_INPUT;
+  }
+  if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
+  return KIN_OK;
+}
+
+// Device trajectory budget of a KIN_OUTPUT_STATS_ONLY launch (doubles): the
+// runs stream through a buffer of at most this many samples.
+constexpr size_t kStatsOnlyBudget = size_t{1} << 28;  // 2 GiB
+
+// Launch one part of a call on a slot (device-resident results in bf).
+int launch_range(Slot& sl, Buffers& bf, const kin_model* model, const kin_sweep_desc* d, const Layout& L,
+                 const PlanPart& part, bool want_stats, bool want_work, kin_error* err, bool want_partials = false) {
+  const HostModel& H = model->host;
   if (!bf.st) bf.st = sl.stream;
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
   KinTables* T = new KinTables;
   std::unique_ptr<KinTables> Tguard(T);
   std::string msg;
   if (int rc = pack_tables(H, d, T, &msg)) { set_err(err, rc, msg); return rc; }
-  const uint64_t S = s1 - s0;
+  const uint64_t R = L.R;
+  const uint64_t S = part.inter ? part.n_pts * R : part.s1 - part.s0;
   const int G = d->n_grid, N = H.n;
   const size_t gn = static_cast<size_t>(G) * N;
-  KIN_CUDA(bf.traj.ensure(std::max<size_t>(gn * S, 1)), "cudaMalloc traj");
+  const bool stats_only = d->output_mode == KIN_OUTPUT_STATS_ONLY;
+  // trajectory buffer: every simulation (FULL) or a bounded run window (STATS_ONLY)
+  uint64_t window = S;
+  if (stats_only) {
+    const uint64_t forced = d->variant >> 16;  // KIN_VARIANT_STATS_WINDOW (tests)
+    window = forced ? forced : kStatsOnlyBudget / std::max<size_t>(gn, 1);
+    window = std::max<uint64_t>(1, std::min<uint64_t>(S, window));
+  }
+  KIN_CUDA(bf.traj.ensure(std::max<size_t>(gn * window, 1)), "cudaMalloc traj");
   KIN_CUDA(bf.meta.ensure(std::max<uint64_t>(S * 6, 1)), "cudaMalloc meta");
   KIN_CUDA(bf.status.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc status");
   if (want_work) KIN_CUDA(bf.work.ensure(std::max<uint64_t>(S, 1)), "cudaMalloc work");
@@ -648,11 +966,15 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
   KIN_CUDA(bf.grid.ensure(std::max<int>(G, 1)), "cudaMalloc grid");
   KinSweepDev SD;
   std::memset(&SD, 0, sizeof(SD));
-  SD.warp_lanes = 32;  // the launchers lower it for launches that cannot fill the GPU
+  // simulations per warp of the thread-per-simulation stochastic kernels:
+  // the descriptor's request (variant bits 8..13), else the launchers' fill rule
+  SD.warp_lanes = static_cast<int32_t>((d->variant >> 8) & 0x3F);
+  if (SD.warp_lanes > 32) SD.warp_lanes = 32;
   SD.kind = d->method.kind;
   SD.rng_mode = d->rng_mode;
   SD.tau = d->method.tau;
   SD.epsilon = d->method.epsilon;
+  SD.firing = (SD.kind == KIN_METHOD_TAU_ADAPTIVE || SD.kind == KIN_METHOD_TAU_FIXED) ? d->method.firing : 0;
   SD.rel_tol = d->method.integrator.rel_tol;
   SD.abs_tol = d->method.integrator.abs_tol;
   SD.h_init = d->method.integrator.h_init;
@@ -673,185 +995,140 @@ int launch_range(Slot& sl, Buffers& bf, const HostModel& H, const kin_sweep_desc
     at += d->axes[ax].n_values;
   }
   if (G) KIN_CUDA(cudaMemcpyAsync(bf.grid.p, d->grid, sizeof(double) * G, cudaMemcpyHostToDevice, bf.st), "H2D grid");
-  SD.runs = L.R;
+  SD.runs = R;
   SD.master_seed = d->master_seed;
-  SD.sim_begin = s0;
+  SD.sim_begin = part.inter ? 0 : part.s0;
+  SD.pt_first = part.inter ? part.pt_first : 0;
+  SD.pt_stride = part.inter ? part.pt_stride : 0;
+  SD.local_begin = 0;
   SD.n_local = S;
   SD.t_end = d->t_end;
   SD.grid = bf.grid.p;
   SD.lgamma_tab = sl.lgamma_tab.p;
-  KinOutDev O{bf.traj.p, bf.meta.p, bf.status.p, want_work ? bf.work.p : nullptr};
   if (!bf.tev[0])
     for (auto& ev : bf.tev) KIN_CUDA(cudaEventCreate(&ev), "event");
   KIN_CUDA(cudaEventRecord(bf.tev[0], bf.st), "event");
-  cudaError_t e;
-  const int kind = d->method.kind;
-  bf.last_int_state = false;  // set below only by the int32-state stochastic launch
-  if (kind == KIN_METHOD_ODE) {
-    int ode_lanes = 0;  // 0: by species count (ode_pick_lanes); KIN_ODE_LANES overrides (residency studies)
-    if (const char* v = std::getenv("KIN_ODE_LANES")) ode_lanes = std::atoi(v);
-    e = kin::launch_dopri5(*T, SD, O, want_work, ode_lanes, bf.st);
-    bf.kernel_name = "dopri5_kernel";
-  } else if (kind == KIN_METHOD_HYBRID) {
-    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
-    // the 15 Dopri5 vectors per simulation: in global memory when a warp's
-    // state would take more than 48 KB of shared memory (<= 4 warps/SM, or no
-    // launch at all above 227 KB); KIN_HYBRID_GSTATE=0/1 forces the choice.
-    // (Measured on C1, 20.6 KB/warp: shared 97.5 ms, global 100.4 ms.)
-    bool gst = kin::hybrid_smem_bytes(*T, SD) > 48 * 1024;
-    if (const char* v = std::getenv("KIN_HYBRID_GSTATE")) gst = std::atoi(v) != 0;
-    if (gst) {
-      int sms = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sl.device);
-      const uint64_t cap = std::min<uint64_t>((S + 31) / 32, static_cast<uint64_t>(sms) * 24);
-      KIN_CUDA(bf.gstate.ensure(cap * kin::hybrid_state_doubles_per_warp(*T, SD)), "cudaMalloc simulation state");
-      SD.gstate = bf.gstate.p;
-      SD.gstate_warps = cap;
-    }
-    e = kin::launch_hybrid(*T, SD, O, want_work, bf.counter.p, bf.st);
-    bf.kernel_name = "hybrid_kernel";
-  } else if (kind == KIN_METHOD_CLE) {
-    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
-    e = kin::launch_cle(*T, SD, O, want_work, bf.counter.p, bf.st);
-    bf.kernel_name = "cle_kernel";
-  } else if (kind == KIN_METHOD_LSODA) {
-    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
-    // Nordsieck array, Jacobian and LU per simulation: in global memory when a
-    // warp's state would take more than 48 KB of shared memory (KIN_LSODA_GSTATE
-    // =0/1 forces the choice)
-    bool gst = kin::lsoda_smem_bytes(*T, SD) > 48 * 1024;
-    if (const char* v = std::getenv("KIN_LSODA_GSTATE")) gst = std::atoi(v) != 0;
-    if (gst) {
-      int sms = 0;
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sl.device);
-      const uint64_t cap = std::min<uint64_t>((S + 31) / 32, static_cast<uint64_t>(sms) * 24);
-      KIN_CUDA(bf.gstate.ensure(cap * kin::lsoda_state_doubles_per_warp(*T, SD)), "cudaMalloc simulation state");
-      SD.gstate = bf.gstate.p;
-      SD.gstate_warps = cap;
-    }
-    e = kin::launch_lsoda(*T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, bf.st);
-    bf.kernel_name = "lsoda_kernel";
-  } else {
-    KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
-    KIN_CUDA(bf.ovf.ensure(1), "cudaMalloc overflow flag");
-    // Philox mode: L lanes per simulation (KIN_GROUP_LANES overrides; 1 = one
-    // thread per simulation).  Compat mode is always one thread per simulation.
-    int lanes = 0;
-    if (const char* v = std::getenv("KIN_GROUP_LANES")) lanes = std::atoi(v);
-    if (d->rng_mode != KIN_RNG_PHILOX) lanes = 1;
-    else if (lanes <= 0) lanes = kin::stochastic_group_pick_lanes(H.n, H.m);
-    if (lanes != 1) {
-      e = kin::launch_stochastic_group(*T, SD, O, want_work, lanes, bf.counter.p, bf.st);
-      bf.last_int_state = false;
-      bf.kernel_name = "stochastic_group_kernel";
-    } else {
-      // int32 amounts when every initial amount is far inside int32 range
-      // (KIN_INT_STATE=0 forces doubles)
-      double xmax = 0.0;
-      for (double v : H.x0) xmax = std::max(xmax, v);
-      for (int ax = 0; ax < d->n_axes; ++ax)
-        if (d->axes[ax].kind == KIN_AXIS_INITIAL)
-          for (int v = 0; v < d->axes[ax].n_values; ++v) xmax = std::max(xmax, d->axes[ax].values[v]);
-      bool int_state = xmax < 1073741824.0;
-      if (const char* v = std::getenv("KIN_INT_STATE")) int_state = int_state && std::atoi(v) != 0;
-      // Large models: when a warp's state would take more than 24 KB of shared
-      // memory (fewer than ~9 resident warps per SM), keep it in global memory
-      // instead — same [slot][lane] layout, L1/L2-cached — and let registers
-      // set the residency (KIN_GSTATE=0/1 forces the choice).
-      const size_t smem_warp = static_cast<size_t>(T->m + SD.n_axes) * 32 * sizeof(double) +
-                               static_cast<size_t>(T->n) * 32 * (int_state ? sizeof(int32_t) : sizeof(double));
-      bool gst = smem_warp > 24 * 1024;
-      if (const char* v = std::getenv("KIN_GSTATE")) gst = std::atoi(v) != 0;
-      if (gst) {
-        int sms = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, sl.device);
-        const uint64_t cap = std::min<uint64_t>((S + 31) / 32, static_cast<uint64_t>(sms) * 24);
-        // sized for double amounts: the int32-overflow re-run reuses it
-        const size_t per = static_cast<size_t>(T->m + SD.n_axes + T->n) * 32;
-        KIN_CUDA(bf.gstate.ensure(cap * per), "cudaMalloc simulation state");
-        SD.gstate = bf.gstate.p;
-        SD.gstate_warps = cap;
-        // amounts in shared memory, propensities in global (JIT kernel only;
-        // it applies the size rule); KIN_GSTATE_SPLIT=0 keeps all state global
-        SD.gstate_x_smem = 1;
-        if (const char* v = std::getenv("KIN_GSTATE_SPLIT")) SD.gstate_x_smem = std::atoi(v) != 0;
-      }
-      KIN_CUDA(cudaMemsetAsync(bf.ovf.p, 0, sizeof(int), bf.st), "memset");
-      bool used = false;
-      e = cudaSuccess;
-      if (kin::jit_wanted(S)) {
-        const kin::JitModel jm = jit_model(H, d);
-        e = kin::launch_stochastic_jit(jm, *T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, bf.st, &used);
-      }
-      if (e == cudaSuccess && !used)
-        e = kin::launch_stochastic(*T, SD, O, want_work, bf.counter.p, bf.ovf.p, int_state, bf.st);
-      bf.last_jit = used;
-      bf.kernel_name = used ? "kin_jit_stoch" : "stochastic_kernel";
-      bf.last_int_state = int_state;
-    }
-    if (bf.last_int_state) {
-      if (!bf.last_T) bf.last_T.reset(new KinTables);
-      *bf.last_T = *T;
-      bf.last_SD = SD;
-      bf.last_O = O;
-      bf.last_count = want_work;
-    }
-  }
-  if (e == cudaErrorInvalidConfiguration) {
-    // the launchers' own pre-check: the per-simulation state of this model does
-    // not fit the kernel's shared-memory budget (a property of the input)
-    cudaGetLastError();
-    set_err(err, KIN_ERR_INPUT,
-            std::string("model too large for the ") + bf.kernel_name +
-                " (per-simulation state exceeds the shared-memory budget)");
-    return KIN_ERR_INPUT;
-  }
-  if (e != cudaSuccess) return cuda_fail(err, e, "simulation kernel launch");
-  KIN_CUDA(cudaEventRecord(bf.tev[1], bf.st), "event");
-  bf.timed_stats = false;
-  // per-point statistics for points entirely inside [s0, s1), and (when the
-  // caller merges chunks) partial statistics of the points cut by a chunk edge
-  const uint64_t P0 = (s0 + L.R - 1) / L.R, P1 = s1 / L.R;
-  const uint64_t nP = P1 > P0 ? P1 - P0 : 0;
+  // Points of this part, in part-local order: local point t holds part-local
+  // simulations [t*R - off, (t+1)*R - off) clipped to [0, S) (off: the first
+  // simulation's run index inside its point; interleaved parts are whole points).
+  const uint64_t off = part.inter ? 0 : part.s0 % R;
+  const uint64_t n_touch = S ? (S - 1 + off) / R + 1 : 0;
+  const bool head_partial = off != 0;
+  const bool tail_partial = S && (S + off) % R != 0;
+  const uint64_t t_whole0 = head_partial ? 1 : 0;
+  const uint64_t t_whole1 = tail_partial ? n_touch - 1 : n_touch;
+  const uint64_t nP = t_whole1 > t_whole0 ? t_whole1 - t_whole0 : 0;
   bf.n_partial = 0;
-  if (want_stats && want_partials && S) {
-    auto add = [&](uint64_t g0, uint64_t g1) {
-      const int k = bf.n_partial++;
-      bf.partial_point[k] = g0 / L.R;
-      bf.partial_n[k] = g1 - g0;
-      bf.partial_base[k] = g0 - s0;
-    };
-    uint64_t head_end = s0;
-    if (s0 % L.R != 0) {
-      head_end = std::min(s1, (s0 / L.R + 1) * L.R);
-      add(s0, head_end);
+  if (!stats_only) {
+    KinOutDev O{bf.traj.p, bf.meta.p, bf.status.p, want_work ? bf.work.p : nullptr};
+    if (int rc = launch_sim(sl, bf, model, d, *T, SD, O, want_work, true, err)) return rc;
+    KIN_CUDA(cudaEventRecord(bf.tev[1], bf.st), "event");
+    // per-point statistics for points entirely inside the part, and (when the
+    // caller merges parts) partial statistics of the points cut by a part edge
+    if (want_stats && want_partials && S) {
+      auto add = [&](uint64_t l0, uint64_t l1) {
+        const int k = bf.n_partial++;
+        bf.partial_point[k] = (part.s0 + l0) / R;
+        bf.partial_n[k] = l1 - l0;
+        bf.partial_base[k] = l0;
+      };
+      if (head_partial) add(0, std::min(S, R - off));
+      if (tail_partial && (n_touch > 1 || !head_partial)) add((n_touch - 1) * R - off, S);
     }
-    const uint64_t tail0 = (s1 / L.R) * L.R;
-    if (s1 % L.R != 0 && tail0 >= head_end && tail0 < s1) add(tail0, s1);
+    bf.last_base = t_whole0 * R - off;
+  } else {
+    // STATS_ONLY: run-ascending windows of at most `window` simulations; after
+    // each window the statistics kernel continues the Welford accumulators of
+    // the points it touched (acc[t] = mean/m2 of local point t), so the result
+    // is the same operation sequence as one Welford pass over all runs.
+    SD.gstate_x_smem = 0;
+    if (want_stats && n_touch) {
+      KIN_CUDA(bf.mean.ensure(gn * n_touch), "cudaMalloc mean");
+      KIN_CUDA(bf.m2.ensure(gn * n_touch), "cudaMalloc m2");
+    }
+    for (uint64_t l0 = 0; l0 < S; l0 += window) {
+      const uint64_t l1 = std::min(S, l0 + window);
+      KinSweepDev SW = SD;
+      SW.local_begin = l0;
+      SW.n_local = l1 - l0;
+      KinOutDev O{bf.traj.p, bf.meta.p + l0 * 6, bf.status.p + l0, want_work ? bf.work.p + l0 : nullptr};
+      if (int rc = launch_sim(sl, bf, model, d, *T, SW, O, want_work, false, err)) return rc;
+      if (!want_stats) continue;
+      // points touched by [l0, l1): a run of (t, first run in window, runs)
+      uint64_t l = l0;
+      while (l < l1) {
+        const uint64_t t = (l + off) / R;
+        const uint64_t t_begin = t * R > off ? t * R - off : 0;  // part-local first sim of point t
+        const uint64_t t_end = std::min(S, (t + 1) * R - off);
+        const uint64_t done = l - t_begin;                    // runs of t before this window
+        if (done == 0 && t_end - t_begin == R && l + R <= l1) {
+          // a run of whole fresh points
+          const uint64_t k = std::min<uint64_t>((l1 - l) / R, t_whole1 > t ? t_whole1 - t : 1);
+          cudaError_t e = kin::launch_point_stats(bf.traj.p, static_cast<int>(gn), R, l - l0, k, 0,
+                                                  bf.mean.p + t * gn, bf.m2.p + t * gn, bf.st);
+          if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
+          l += k * R;
+        } else {
+          const uint64_t runs = std::min(t_end, l1) - l;
+          cudaError_t e = kin::launch_point_stats(bf.traj.p, static_cast<int>(gn), runs, l - l0, 1, done,
+                                                  bf.mean.p + t * gn, bf.m2.p + t * gn, bf.st);
+          if (e != cudaSuccess) return cuda_fail(err, e, "statistics kernel launch");
+          l += runs;
+        }
+      }
+    }
+    KIN_CUDA(cudaEventRecord(bf.tev[1], bf.st), "event");
+    if (want_stats && want_partials && S) {
+      auto add = [&](uint64_t t, uint64_t l0, uint64_t l1) {
+        const int k = bf.n_partial++;
+        bf.partial_point[k] = (part.s0 + l0) / R;
+        bf.partial_n[k] = l1 - l0;
+        bf.partial_base[k] = t;  // STATS_ONLY: the accumulator row
+      };
+      if (head_partial) add(0, 0, std::min(S, R - off));
+      if (tail_partial && (n_touch > 1 || !head_partial)) add(n_touch - 1, (n_touch - 1) * R - off, S);
+      if (bf.n_partial) {
+        KIN_CUDA(bf.pmean.ensure(gn * 2), "cudaMalloc partial mean");
+        KIN_CUDA(bf.pm2.ensure(gn * 2), "cudaMalloc partial m2");
+        for (int k = 0; k < bf.n_partial; ++k) {
+          KIN_CUDA(cudaMemcpyAsync(bf.pmean.p + k * gn, bf.mean.p + bf.partial_base[k] * gn, gn * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, bf.st), "D2D partial");
+          KIN_CUDA(cudaMemcpyAsync(bf.pm2.p + k * gn, bf.m2.p + bf.partial_base[k] * gn, gn * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, bf.st), "D2D partial");
+        }
+      }
+    }
+  }
+  bf.timed_stats = false;
+  if (!stats_only && want_stats) {
     if (bf.n_partial) {
       KIN_CUDA(bf.pmean.ensure(gn * 2), "cudaMalloc partial mean");
       KIN_CUDA(bf.pm2.ensure(gn * 2), "cudaMalloc partial m2");
     }
-  }
-  if (want_stats && nP) {
-    KIN_CUDA(bf.mean.ensure(gn * nP), "cudaMalloc mean");
-    KIN_CUDA(bf.m2.ensure(gn * nP), "cudaMalloc m2");
+    if (nP) {
+      KIN_CUDA(bf.mean.ensure(gn * nP), "cudaMalloc mean");
+      KIN_CUDA(bf.m2.ensure(gn * nP), "cudaMalloc m2");
+    }
   }
   bf.last_gn = static_cast<int>(gn);
-  bf.R = L.R;
+  bf.R = R;
   bf.nP = nP;
-  bf.last_base = P0 * L.R - s0;
   bf.have_stats = want_stats && nP;
-  if (int rc = launch_stats(sl, bf, err)) return rc;
-  if (bf.have_stats || bf.n_partial) {
-    KIN_CUDA(cudaEventRecord(bf.tev[2], bf.st), "event");
-    bf.timed_stats = true;
+  bf.stats_only = stats_only;
+  bf.stats_row0 = stats_only ? t_whole0 : 0;
+  if (!stats_only) {
+    if (int rc = launch_stats(sl, bf, err)) return rc;
+    if (bf.have_stats || bf.n_partial) {
+      KIN_CUDA(cudaEventRecord(bf.tev[2], bf.st), "event");
+      bf.timed_stats = true;
+    }
   }
   bf.pending_check = bf.last_int_state;
   bf.last_S = S;
-  bf.s0 = s0;
-  bf.s1 = s1;
-  bf.P0 = P0;
+  bf.s0 = part.inter ? 0 : part.s0;
+  bf.s1 = bf.s0 + S;
+  bf.P0 = part.inter ? 0 : (part.s0 + R - 1) / R;
+  bf.part = part;
   bf.G = G;
   bf.N = N;
   bf.have_work = want_work;
@@ -882,26 +1159,41 @@ int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
 // base_point of the caller's arrays).  async: on the slot's copy stream, left
 // in flight (the caller orders it after the launch); otherwise synchronous on
 // the compute stream.
-int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, bool sync,
-             kin_error* err) {
+int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_point, bool sync, kin_error* err) {
   cudaStream_t st = sync ? bf.st : sl.copy_stream;
   const uint64_t S = bf.s1 - bf.s0;
   const size_t gn = static_cast<size_t>(bf.G) * bf.N;
-  const uint64_t so = bf.s0 - base_sim;
-  if (out->traj && S && gn)  // device layout == host layout [S][G][N]: one contiguous copy
-    if (int rc = copy_d2h(sl, st, out->traj + so * gn, bf.traj.p, gn * S * sizeof(double), sync, err)) return rc;
+  const PlanPart& pt = bf.part;
+  // per-simulation arrays: one row (contiguous part) or one row of R runs per
+  // point, rows out_pitch simulations apart in the caller's layout (interleaved)
+  const uint64_t rows = pt.inter ? pt.n_pts : 1;
+  const uint64_t row = pt.inter ? bf.R : S;
+  const uint64_t pitch = pt.inter ? pt.out_pitch : S;
+  const uint64_t so = pt.out_first;
+  auto put = [&](void* dst_base, size_t elem, const void* src) -> int {
+    return copy_d2h_rows(sl, st, static_cast<char*>(dst_base) + so * elem, pitch * elem, src, row * elem, rows, sync,
+                         err);
+  };
+  // traj: device layout == host layout [S][G][N] (STATS_ONLY never materialises it)
+  if (out->traj && S && gn && !bf.stats_only)
+    if (int rc = put(out->traj, gn * sizeof(double), bf.traj.p)) return rc;
   if (out->meta && S)
-    if (int rc = copy_d2h(sl, st, out->meta + so * 6, bf.meta.p, S * 6 * sizeof(uint64_t), sync, err)) return rc;
+    if (int rc = put(out->meta, 6 * sizeof(uint64_t), bf.meta.p)) return rc;
   if (out->status && S)
-    if (int rc = copy_d2h(sl, st, out->status + so, bf.status.p, S * sizeof(int32_t), sync, err)) return rc;
+    if (int rc = put(out->status, sizeof(int32_t), bf.status.p)) return rc;
   if (out->work && S && bf.have_work)
-    if (int rc = copy_d2h(sl, st, out->work + so, bf.work.p, S * sizeof(uint64_t), sync, err)) return rc;
+    if (int rc = put(out->work, sizeof(uint64_t), bf.work.p)) return rc;
   if (bf.have_stats) {
-    const uint64_t po = bf.P0 - base_point;
+    const uint64_t prow = pt.inter ? 1 : bf.nP, prows = pt.inter ? pt.n_pts : 1;
+    const uint64_t ppitch = pt.inter ? pt.out_pitch / bf.R : bf.nP;
+    const uint64_t po = pt.inter ? pt.out_first / bf.R : bf.P0 - base_point;
+    const size_t eb = gn * sizeof(double);
+    const double* src_mean = bf.mean.p + bf.stats_row0 * gn;
+    const double* src_m2 = bf.m2.p + bf.stats_row0 * gn;
     if (out->mean)
-      if (int rc = copy_d2h(sl, st, out->mean + po * gn, bf.mean.p, bf.nP * gn * sizeof(double), sync, err)) return rc;
+      if (int rc = copy_d2h_rows(sl, st, out->mean + po * gn, ppitch * eb, src_mean, prow * eb, prows, sync, err)) return rc;
     if (out->m2)
-      if (int rc = copy_d2h(sl, st, out->m2 + po * gn, bf.m2.p, bf.nP * gn * sizeof(double), sync, err)) return rc;
+      if (int rc = copy_d2h_rows(sl, st, out->m2 + po * gn, ppitch * eb, src_m2, prow * eb, prows, sync, err)) return rc;
   }
   if (bf.n_partial) {
     const size_t need = static_cast<size_t>(bf.n_partial) * gn;
@@ -922,9 +1214,9 @@ int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_sim,
   return KIN_OK;
 }
 
-int fetch_range(Slot& sl, Buffers& bf, kin_sweep_out* out, uint64_t base_sim, uint64_t base_point, kin_error* err) {
+int fetch_range(Slot& sl, Buffers& bf, kin_sweep_out* out, uint64_t base_point, kin_error* err) {
   if (int rc = finish_launch(sl, bf, err)) return rc;
-  return copy_out(sl, bf, out, base_sim, base_point, true, err);
+  return copy_out(sl, bf, out, base_point, true, err);
 }
 
 // Chunk plan of kin_sweep_run (see kin_abi.h kin_sweep_plan).
@@ -951,31 +1243,6 @@ void stats_merge(uint64_t* na, double* mean_a, double* m2_a, uint64_t nb, const 
   *na += nb;
 }
 
-std::vector<uint64_t> plan_chunks(uint64_t s0, uint64_t s1, uint64_t R, int D) {
-  const uint64_t S = s1 - s0;
-  if (D <= 1 || S == 0) return {s0, s1};
-  const uint64_t points = (s1 - 1) / R - s0 / R + 1;  // points the range touches
-  std::vector<uint64_t> bounds;
-  bounds.push_back(s0);
-  if (points < static_cast<uint64_t>(D)) {
-    // fewer points than devices (run_ensemble): split the runs evenly; the
-    // statistics of a point cut by a chunk edge are merged across its chunks
-    const uint64_t n_chunks = std::min<uint64_t>(S, static_cast<uint64_t>(D));
-    for (uint64_t c = 1; c < n_chunks; ++c) bounds.push_back(s0 + S * c / n_chunks);
-  } else {
-    const uint64_t n_chunks = std::min<uint64_t>(std::max<uint64_t>(S / std::max<uint64_t>(R, 1), 1),
-                                                 4 * static_cast<uint64_t>(D));
-    for (uint64_t c = 1; c < n_chunks; ++c) {
-      uint64_t b = s0 + S * c / n_chunks;
-      b = (b + R - 1) / R * R;  // snap to a point boundary
-      b = std::min(std::max(b, bounds.back()), s1);
-      bounds.push_back(b);
-    }
-  }
-  bounds.push_back(s1);
-  return bounds;
-}
-
 int prepare(const kin_model* model, const kin_sweep_desc* desc, Layout* L, uint64_t* s0, uint64_t* s1,
             kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
@@ -986,7 +1253,52 @@ int prepare(const kin_model* model, const kin_sweep_desc* desc, Layout* L, uint6
   *s0 = desc->sim_begin;
   *s1 = desc->sim_end == 0 ? L->S : std::min<uint64_t>(desc->sim_end, L->S);
   if (*s0 > *s1) { set_err(err, KIN_ERR_USAGE, "inverted simulation range"); return KIN_ERR_USAGE; }
+  if (desc->shard_count > 1 && (*s0 % L->R != 0 || *s1 % L->R != 0)) {
+    set_err(err, KIN_ERR_INPUT, "a sharded call needs a range of whole points");
+    return KIN_ERR_INPUT;
+  }
   return KIN_OK;
+}
+
+// Caller-local sizes of a call: simulations and statistics points.
+void local_sizes(const kin_sweep_desc* d, const Layout& L, uint64_t s0, uint64_t s1, uint64_t* n_sims,
+                 uint64_t* n_points) {
+  if (d->shard_count > 1) {
+    const uint64_t P = (s1 - s0) / L.R, n = static_cast<uint64_t>(d->shard_count);
+    const uint64_t K = P > static_cast<uint64_t>(d->shard_index) ? (P - d->shard_index + n - 1) / n : 0;
+    *n_sims = K * L.R;
+    *n_points = K;
+  } else {
+    *n_sims = s1 - s0;
+    const uint64_t p0 = (s0 + L.R - 1) / L.R, p1 = s1 / L.R;
+    *n_points = p1 > p0 ? p1 - p0 : 0;
+  }
+}
+
+// Points cut by part edges: Chan-merge their per-part statistics in ascending
+// part order (ensemble.hpp:91-99: per-worker accumulators merged in ascending
+// worker-range order) into the caller's mean/m2.
+void merge_partials(const std::vector<Buffers*>& bufs, const kin_sweep_out& out, uint64_t base_point,
+                    uint64_t point_end) {
+  if (!out.mean && !out.m2) return;
+  std::map<uint64_t, std::pair<uint64_t, std::vector<double>>> acc;  // point -> (n, [mean | m2])
+  size_t gn = 0;
+  for (const Buffers* bp : bufs) {
+    const Buffers& bf = *bp;
+    gn = static_cast<size_t>(bf.last_gn);
+    for (int k = 0; k < bf.n_partial; ++k) {
+      auto& a = acc[bf.partial_point[k]];
+      if (a.second.empty()) a.second.assign(2 * gn, 0.0);
+      stats_merge(&a.first, a.second.data(), a.second.data() + gn, bf.partial_n[k], bf.h_pmean + k * gn,
+                  bf.h_pm2 + k * gn, gn);
+    }
+  }
+  for (const auto& kv : acc) {
+    const uint64_t pt = kv.first;
+    if (pt < base_point || pt >= point_end) continue;  // not whole inside the call's range: no statistics
+    if (out.mean) std::memcpy(out.mean + (pt - base_point) * gn, kv.second.second.data(), gn * sizeof(double));
+    if (out.m2) std::memcpy(out.m2 + (pt - base_point) * gn, kv.second.second.data() + gn, gn * sizeof(double));
+  }
 }
 
 }  // namespace
@@ -1047,7 +1359,12 @@ int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err)
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     // lgamma(k+1) from the host libm (the oracle's, glibc) for the PTRS test
     std::vector<double> lg(KIN_LGAMMA_N);
-    for (int k = 0; k < KIN_LGAMMA_N; ++k) lg[k] = std::lgamma(static_cast<double>(k) + 1.0);
+    // (lgamma_r: glibc's lgamma writes the global signgam — a data race when
+    // contexts are created from several threads)
+    for (int k = 0; k < KIN_LGAMMA_N; ++k) {
+      int sign = 0;
+      lg[k] = lgamma_r(static_cast<double>(k) + 1.0, &sign);
+    }
     KIN_CUDA(sl->lgamma_tab.ensure(KIN_LGAMMA_N), "cudaMalloc lgamma table");
     KIN_CUDA(cudaMemcpy(sl->lgamma_tab.p, lg.data(), sizeof(double) * KIN_LGAMMA_N, cudaMemcpyHostToDevice), "H2D lgamma");
     std::vector<double> co;
@@ -1130,23 +1447,33 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
   if (int rc = prepare(model, desc, &job->L, &s0, &s1, err)) return rc;
   const Layout& L = job->L;
   if (out) job->out = *out;
+  if (desc->output_mode == KIN_OUTPUT_STATS_ONLY) job->out.traj = nullptr;
   job->s0 = s0;
   job->s1 = s1;
+  job->sh_n = desc->shard_count > 1 ? desc->shard_count : 1;
+  job->sh_i = job->sh_n > 1 ? desc->shard_index : 0;
   job->base_point = (s0 + L.R - 1) / L.R;
-  const uint64_t S = s1 - s0;
+  local_sizes(desc, L, s0, s1, &job->n_local, &job->np_local);
+  const uint64_t S = job->n_local;
   if (!job->out.status && S) {
     KIN_CUDA(cudaMallocHost(&job->status_pinned, sizeof(int32_t) * S), "pinned status");
     job->out.status = job->status_pinned;
   }
   const int D = static_cast<int>(ctx->slots.size());
-  const std::vector<uint64_t> bounds = plan_chunks(s0, s1, L.R, D);
+  std::vector<PlanPart> plan;
+  {
+    std::string msg;
+    if (int rc = plan_parts(s0, s1, L.R, D, job->sh_i, job->sh_n, &plan, &msg)) {
+      set_err(err, rc, msg);
+      if (job->status_pinned) cudaFreeHost(job->status_pinned);
+      return rc;
+    }
+  }
   const bool stats = job->out.mean || job->out.m2;
+  const bool partials = stats && plan.size() > 1 && !plan[0].inter;
   auto enqueue = [&]() -> int {
-    for (size_t c = 0; c + 1 < bounds.size(); ++c) {
-      const uint64_t c0 = bounds[c], c1 = bounds[c + 1];
-      if (c0 >= c1) continue;
-      const int dv = static_cast<int>(c % D);
-      Slot& sl = *ctx->slots[dv];
+    for (const PlanPart& part : plan) {
+      Slot& sl = *ctx->slots[part.dev];
       std::lock_guard<std::mutex> lk(sl.mu);
       KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
       Buffers* bf;
@@ -1156,10 +1483,9 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
       } else {
         bf = new Buffers;
       }
-      job->parts.push_back({dv, bf});
+      job->parts.push_back({part.dev, bf});
       bf->st = (sl.job_rr++ & 1u) ? sl.aux_stream : sl.stream;
-      const bool partials = stats && bounds.size() > 2;
-      if (int rc = launch_range(sl, *bf, model->host, desc, L, c0, c1, stats, job->out.work != nullptr, err, partials))
+      if (int rc = launch_range(sl, *bf, model, desc, L, part, stats, job->out.work != nullptr, err, partials))
         return rc;
       if (!bf->ev_done) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_done, cudaEventDisableTiming), "event");
       if (!bf->ev_copied) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_copied, cudaEventDisableTiming), "event");
@@ -1167,13 +1493,13 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
       KIN_CUDA(cudaEventRecord(bf->ev_done, bf->st), "event");
       // copy-out on the copy stream, overlapping the next launches on `stream`
       KIN_CUDA(cudaStreamWaitEvent(sl.copy_stream, bf->ev_done, 0), "stream wait");
-      if (int rc = copy_out(sl, *bf, &job->out, s0, job->base_point, false, err)) return rc;
+      if (int rc = copy_out(sl, *bf, &job->out, job->base_point, false, err)) return rc;
       KIN_CUDA(cudaEventRecord(bf->ev_copied, sl.copy_stream), "event");
     }
     return KIN_OK;
   };
   if (int rc = enqueue()) {
-    // a chunk failed to enqueue: drain the chunks already in flight and give
+    // a part failed to enqueue: drain the parts already in flight and give
     // their buffers back, so nothing writes into `out` after we return
     for (auto& part : job->parts) {
       Slot& sl = *ctx->slots[part.slot];
@@ -1181,9 +1507,11 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
       if (part.buf->st) cudaStreamSynchronize(part.buf->st);
       cudaStreamSynchronize(sl.copy_stream);
       std::lock_guard<std::mutex> lk(sl.mu);
+      part.buf->pending_check = false;
       sl.pool.emplace_back(part.buf);
     }
     job->parts.clear();
+    if (job->status_pinned) cudaFreeHost(job->status_pinned);
     return rc;
   }
   std::lock_guard<std::mutex> lk(ctx->jobs_mu);
@@ -1206,6 +1534,9 @@ int kin_ensemble_run(kin_ctx* ctx, const kin_model* model, const kin_method* met
   d.t_end = t_end;
   d.n_grid = n_grid;
   d.grid = grid;
+  // no trajectories requested (no RunSink): statistics only, runs streamed
+  // through a bounded device window
+  if (out && !out->traj) d.output_mode = KIN_OUTPUT_STATS_ONLY;
   return kin_sweep_run(ctx, model, &d, out, err);
 }
 
@@ -1244,48 +1575,29 @@ int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
   for (auto& part : job->parts) {
     Slot& sl = *ctx->slots[part.slot];
     Buffers& bf = *part.buf;
-    if (rc == KIN_OK) {
-      cudaError_t ce = cudaSetDevice(sl.device);
-      if (ce == cudaSuccess) ce = cudaEventSynchronize(bf.ev_copied);
-      if (ce != cudaSuccess) {
-        rc = cuda_fail(err, ce, "copy-out");
-        continue;
-      }
-      if (bf.pending_check && *bf.ovf_host) {
-        // an int32 amount overflowed: redo this chunk with double amounts
-        std::lock_guard<std::mutex> lk(sl.mu);
-        bf.pending_check = true;
-        if ((rc = finish_launch(sl, bf, err)) == KIN_OK)
-          rc = copy_out(sl, bf, &job->out, job->s0, job->base_point, true, err);
-      }
+    // every part's copy-out is waited for, even after an error: its buffers go
+    // back to the pool and its D2H must not write into `out` after we return
+    cudaError_t ce = cudaSetDevice(sl.device);
+    if (ce == cudaSuccess) ce = cudaEventSynchronize(bf.ev_copied);
+    if (ce != cudaSuccess) {
+      if (rc == KIN_OK) rc = cuda_fail(err, ce, "copy-out");
+      cudaStreamSynchronize(bf.st);
+      cudaStreamSynchronize(sl.copy_stream);
       bf.pending_check = false;
+      continue;
     }
+    if (rc == KIN_OK && bf.pending_check && *bf.ovf_host) {
+      // an int32 amount overflowed: redo this part with double amounts
+      std::lock_guard<std::mutex> lk(sl.mu);
+      bf.pending_check = true;
+      if ((rc = finish_launch(sl, bf, err)) == KIN_OK) rc = copy_out(sl, bf, &job->out, job->base_point, true, err);
+    }
+    bf.pending_check = false;
   }
-  // points cut by chunk edges: Chan-merge their per-chunk statistics in
-  // ascending chunk order (ensemble.hpp:91-99: per-worker accumulators merged
-  // in ascending worker-range order)
-  if (rc == KIN_OK && (job->out.mean || job->out.m2)) {
-    std::map<uint64_t, std::pair<uint64_t, std::vector<double>>> acc;  // point -> (n, [mean | m2])
-    size_t gn = 0;
-    for (auto& part : job->parts) {
-      const Buffers& bf = *part.buf;
-      gn = static_cast<size_t>(bf.last_gn);
-      for (int k = 0; k < bf.n_partial; ++k) {
-        auto& a = acc[bf.partial_point[k]];
-        if (a.second.empty()) a.second.assign(2 * gn, 0.0);
-        stats_merge(&a.first, a.second.data(), a.second.data() + gn, bf.partial_n[k], bf.h_pmean + k * gn,
-                    bf.h_pm2 + k * gn, gn);
-      }
-    }
-    const uint64_t P_first = job->base_point, P_end = job->s1 / job->L.R;
-    for (const auto& kv : acc) {
-      const uint64_t pt = kv.first;
-      if (pt < P_first || pt >= P_end) continue;  // not whole inside the sweep range: no statistics
-      if (job->out.mean)
-        std::memcpy(job->out.mean + (pt - P_first) * gn, kv.second.second.data(), gn * sizeof(double));
-      if (job->out.m2)
-        std::memcpy(job->out.m2 + (pt - P_first) * gn, kv.second.second.data() + gn, gn * sizeof(double));
-    }
+  if (rc == KIN_OK) {
+    std::vector<Buffers*> bufs;
+    for (auto& part : job->parts) bufs.push_back(part.buf);
+    merge_partials(bufs, job->out, job->base_point, job->s1 / job->L.R);
   }
   for (auto& part : job->parts) {
     Slot& sl = *ctx->slots[part.slot];
@@ -1294,11 +1606,11 @@ int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
   }
   job->parts.clear();
   if (rc == KIN_OK) {
-    const uint64_t S = job->s1 - job->s0;
-    for (uint64_t s = 0; s < S; ++s) {
+    const uint64_t S = job->n_local;
+    for (uint64_t s = 0; s < S; ++s) {  // caller-local order is ascending in the global index
       const int32_t st = job->out.status[s];
       if (st != KIN_SIM_OK) {
-        const uint64_t g = job->s0 + s;
+        const uint64_t g = job->global_of(s);
         if (err) {
           err->code = KIN_ERR_SIMULATION;
           err->sim_status = st;
@@ -1318,52 +1630,110 @@ int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
   return rc;
 }
 
-int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t R, int32_t D, int32_t max_chunks, uint64_t* bounds,
-                   int32_t* n_chunks, kin_error* err) {
+int kin_sweep_plan(uint64_t s0, uint64_t s1, uint64_t R, int32_t D, int32_t sh_i, int32_t sh_n, int32_t max_parts,
+                   kin_sweep_part* parts, int32_t* n_parts, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
-  if (s1 < s0 || R == 0 || D < 1 || !bounds || !n_chunks) { set_err(err, KIN_ERR_USAGE, "bad argument"); return KIN_ERR_USAGE; }
-  const std::vector<uint64_t> b = plan_chunks(s0, s1, R, D);
-  if (static_cast<int64_t>(b.size()) - 1 > max_chunks) { set_err(err, KIN_ERR_USAGE, "max_chunks too small"); return KIN_ERR_USAGE; }
-  for (size_t i = 0; i < b.size(); ++i) bounds[i] = b[i];
-  *n_chunks = static_cast<int32_t>(b.size() - 1);
+  if (!n_parts || (max_parts > 0 && !parts)) { set_err(err, KIN_ERR_USAGE, "bad argument"); return KIN_ERR_USAGE; }
+  std::vector<PlanPart> plan;
+  std::string msg;
+  if (int rc = plan_parts(s0, s1, R, D, sh_i, sh_n, &plan, &msg)) { set_err(err, rc, msg); return rc; }
+  if (static_cast<int64_t>(plan.size()) > max_parts) { set_err(err, KIN_ERR_USAGE, "max_parts too small"); return KIN_ERR_USAGE; }
+  for (size_t i = 0; i < plan.size(); ++i) {
+    const PlanPart& p = plan[i];
+    kin_sweep_part& q = parts[i];
+    std::memset(&q, 0, sizeof q);
+    q.device = p.dev;
+    q.interleaved = p.inter ? 1 : 0;
+    q.sim_begin = p.s0;
+    q.sim_end = p.s1;
+    q.pt_first = p.pt_first;
+    q.pt_stride = p.pt_stride;
+    q.n_points = p.n_pts;
+    q.out_first = p.out_first;
+    q.out_pitch = p.out_pitch;
+  }
+  *n_parts = static_cast<int32_t>(plan.size());
+  return KIN_OK;
+}
+
+int kin_sweep_local_size(const kin_sweep_desc* desc, uint64_t* np, uint64_t* ns, kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  Layout L;
+  std::string msg;
+  if (int rc = sweep_layout(desc, &L, &msg)) { set_err(err, rc, msg); return rc; }
+  const uint64_t s0 = desc->sim_begin;
+  const uint64_t s1 = desc->sim_end == 0 ? L.S : std::min<uint64_t>(desc->sim_end, L.S);
+  if (s0 > s1) { set_err(err, KIN_ERR_USAGE, "inverted simulation range"); return KIN_ERR_USAGE; }
+  uint64_t a = 0, b = 0;
+  local_sizes(desc, L, s0, s1, &a, &b);
+  if (ns) *ns = a;
+  if (np) *np = b;
   return KIN_OK;
 }
 
 int kin_sweep_launch(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc, int32_t slot,
                      int32_t want_stats, int32_t want_work, kin_error* err) {
-  if (!ctx || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) {
+  if (!ctx || slot < -1 || slot >= static_cast<int32_t>(ctx->slots.size())) {
     set_err(err, KIN_ERR_USAGE, "bad context/slot");
     return KIN_ERR_USAGE;
   }
   Layout L;
   uint64_t s0, s1;
   if (int rc = prepare(model, desc, &L, &s0, &s1, err)) return rc;
-  Slot& sl = *ctx->slots[slot];
-  std::lock_guard<std::mutex> lk(sl.mu);
-  return launch_range(sl, sl.main, model->host, desc, L, s0, s1, want_stats != 0, want_work != 0, err);
+  const int sh_n = desc->shard_count > 1 ? desc->shard_count : 1, sh_i = sh_n > 1 ? desc->shard_index : 0;
+  std::vector<PlanPart> plan;
+  std::string msg;
+  const int D = slot < 0 ? static_cast<int>(ctx->slots.size()) : 1;
+  if (int rc = plan_parts(s0, s1, L.R, D, sh_i, sh_n, &plan, &msg)) { set_err(err, rc, msg); return rc; }
+  for (int dv = 0; dv < static_cast<int>(ctx->slots.size()); ++dv) ctx->slots[dv]->main.valid = slot >= 0 && dv != slot && ctx->slots[dv]->main.valid;
+  const bool partials = want_stats && plan.size() > 1 && !plan[0].inter;
+  for (const PlanPart& p : plan) {
+    Slot& sl = *ctx->slots[slot < 0 ? p.dev : slot];
+    std::lock_guard<std::mutex> lk(sl.mu);
+    if (int rc = launch_range(sl, sl.main, model, desc, L, p, want_stats != 0, want_work != 0, err, partials)) return rc;
+    sl.main.base_point = (s0 + L.R - 1) / L.R;
+    sl.main.point_end = s1 / L.R;
+  }
+  return KIN_OK;
 }
 
 int kin_sweep_sync(kin_ctx* ctx, int32_t slot, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
-  if (!ctx || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) {
+  if (!ctx || slot < -1 || slot >= static_cast<int32_t>(ctx->slots.size())) {
     set_err(err, KIN_ERR_USAGE, "bad context/slot");
     return KIN_ERR_USAGE;
   }
-  Slot& sl = *ctx->slots[slot];
-  std::lock_guard<std::mutex> lk(sl.mu);
-  return finish_launch(sl, sl.main, err);
+  for (int dv = 0; dv < static_cast<int>(ctx->slots.size()); ++dv) {
+    if (slot >= 0 && dv != slot) continue;
+    Slot& sl = *ctx->slots[dv];
+    std::lock_guard<std::mutex> lk(sl.mu);
+    if (!sl.main.valid) continue;
+    if (int rc = finish_launch(sl, sl.main, err)) return rc;
+  }
+  return KIN_OK;
 }
 
 int kin_sweep_fetch(kin_ctx* ctx, int32_t slot, kin_sweep_out* out, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
-  if (!ctx || !out || slot < 0 || slot >= static_cast<int32_t>(ctx->slots.size())) {
+  if (!ctx || !out || slot < -1 || slot >= static_cast<int32_t>(ctx->slots.size())) {
     set_err(err, KIN_ERR_USAGE, "bad argument");
     return KIN_ERR_USAGE;
   }
-  Slot& sl = *ctx->slots[slot];
-  std::lock_guard<std::mutex> lk(sl.mu);
-  if (!sl.main.valid) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
-  return fetch_range(sl, sl.main, out, sl.main.s0, sl.main.P0, err);
+  std::vector<Buffers*> bufs;
+  uint64_t base_point = 0, point_end = 0;
+  for (int dv = 0; dv < static_cast<int>(ctx->slots.size()); ++dv) {
+    if (slot >= 0 && dv != slot) continue;
+    Slot& sl = *ctx->slots[dv];
+    std::lock_guard<std::mutex> lk(sl.mu);
+    if (!sl.main.valid) continue;
+    if (int rc = fetch_range(sl, sl.main, out, sl.main.base_point, err)) return rc;
+    bufs.push_back(&sl.main);
+    base_point = sl.main.base_point;
+    point_end = sl.main.point_end;
+  }
+  if (bufs.empty()) { set_err(err, KIN_ERR_USAGE, "nothing launched on this slot"); return KIN_ERR_USAGE; }
+  merge_partials(bufs, *out, base_point, point_end);
+  return KIN_OK;
 }
 
 int kin_jit_check(const kin_model_desc* desc, const kin_sweep_desc* sweep, char* log, int32_t log_cap,
@@ -1423,16 +1793,35 @@ int kin_device_rng_draws(kin_ctx* ctx, uint64_t seed, int32_t kind, double mean,
   return KIN_OK;
 }
 
+int kin_device_binomial_draws(kin_ctx* ctx, uint64_t seed, uint64_t n_trials, double p, int32_t n, uint64_t* out,
+                              kin_error* err) {
+  if (err) std::memset(err, 0, sizeof(*err));
+  if (!ctx || ctx->slots.empty() || n < 0 || (n > 0 && !out)) {
+    set_err(err, KIN_ERR_USAGE, "bad argument");
+    return KIN_ERR_USAGE;
+  }
+  Slot& sl = *ctx->slots[0];
+  KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
+  uint64_t* d = nullptr;
+  KIN_CUDA(cudaMalloc(&d, sizeof(uint64_t) * std::max(n, 1)), "cudaMalloc");
+  cudaError_t e = kin::launch_binomial_draws(seed, n_trials, p, n, d, sl.stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, sl.stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(sl.stream);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(err, e, "binomial draws");
+  return KIN_OK;
+}
+
 int kin_device_unit(kin_ctx* ctx, const kin_model* model, int32_t kind, const double* x, const double* params,
                     int32_t n_params, double* out, int32_t out_cap, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
-  if (!ctx || ctx->slots.empty() || !model || !x || !out || kind < 0 || kind > 4) {
+  if (!ctx || ctx->slots.empty() || !model || !x || !out || kind < 0 || kind > 6) {
     set_err(err, KIN_ERR_USAGE, "bad argument");
     return KIN_ERR_USAGE;
   }
   const HostModel& H = model->host;
-  const int need_params[5] = {0, 1, 2, H.m, 1 + H.m};
-  const int need_out[5] = {H.m, 1, 2, H.n + 1, H.n + 1};
+  const int need_params[7] = {0, 1, 2, H.m, 1 + H.m, 0, 3};
+  const int need_out[7] = {H.m, 1, 2, H.n + 1, H.n + 1, H.n, 2 * H.n + 1};
   if (n_params < need_params[kind] || (need_params[kind] && !params) || out_cap < need_out[kind]) {
     set_err(err, KIN_ERR_USAGE, "params/out too small for this unit");
     return KIN_ERR_USAGE;

@@ -164,7 +164,7 @@ template <bool kCount, bool kPhilox, int kN>
 __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, uint64_t s,
                                     double* V, double* a, double* av, uint32_t* slowm) {
   constexpr int B = kBlock;
-  const uint64_t sim = S.sim_begin + s;
+  const uint64_t sim = global_sim(S, s);
   const int n = kN > 0 ? kN : T.n, m = T.m, G = T.n_grid, n1 = n + 1;
   Hybrid<kCount, kN> H{T, S, TableModel<double, kBlock>{T, V, a, av}, T.n, m, T.n + 1, V, slowm};
   stoch::init_state<double, kBlock>(T, S, sim, n, V, av);  // y[0..n-1] = x0 (vector Y is the first)

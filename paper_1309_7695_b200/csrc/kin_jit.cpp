@@ -18,6 +18,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -73,9 +74,17 @@ constexpr int kInlinePropsMaxReactions = 1 << 30;
 
 // Development knobs (KIN_JIT_TAU_INLINE / KIN_JIT_APPLY_SWITCH override the
 // thresholds; they change the generated source, hence the cache key).
+// Read once per process and name (study knobs, never per launch).
 int jit_knob(const char* name, int dflt) {
-  const char* v = std::getenv(name);
-  return v && *v ? std::atoi(v) : dflt;
+  static std::mutex mu;
+  static std::map<std::string, int> seen;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = seen.find(name);
+  if (it == seen.end()) {
+    const char* v = std::getenv(name);
+    it = seen.emplace(name, v && *v ? std::atoi(v) : INT32_MIN).first;
+  }
+  return it->second == INT32_MIN ? dflt : it->second;
 }
 
 // Model policy source for one model structure (see kin_stochastic_impl.cuh
@@ -244,7 +253,7 @@ const char* const kNvrtcOpts[5] = {"--gpu-architecture=sm_100a", "-fmad=false", 
 
 // NVRTC: policy source -> sm_100a cubin.  Returns false with the log on error.
 bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_state, bool global_state,
-                   bool smem_x, std::vector<char>* cubin, std::string* log) {
+                   bool smem_x, int firing, std::vector<char>* cubin, std::string* log) {
   std::string src = "#include \"kin_stochastic_impl.cuh\"\n" + policy +
                     "extern \"C\" __global__ void __launch_bounds__(KIN_STOCH_BLOCK, KMINB_) kin_jit_stoch(\n"
                     "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
@@ -270,8 +279,10 @@ bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_
   // split layout: its 16 KB of shared memory per warp allows 13 resident warps
   // per SM; ask the register allocator for that many (development knob)
   const std::string d_b = "-DKMINB_=" + std::to_string(smem_x ? jit_knob("KIN_JIT_SPLIT_MINB", 1) : 1);
+  const std::string d_f = "-DKFIRING_=" + std::to_string(firing);
   const char* opts[] = {kNvrtcOpts[0], kNvrtcOpts[1], kNvrtcOpts[2], kNvrtcOpts[3], kNvrtcOpts[4],
-                        d_xt.c_str(),  d_c.c_str(),   d_p.c_str(),   d_g.c_str(),   d_x.c_str(), d_b.c_str()};
+                        d_xt.c_str(),  d_c.c_str(),   d_p.c_str(),   d_g.c_str(),   d_x.c_str(), d_b.c_str(),
+                        d_f.c_str()};
   const nvrtcResult rc = nvrtcCompileProgram(prog, static_cast<int>(sizeof(opts) / sizeof(opts[0])), opts);
   size_t log_size = 0;
   nvrtcGetProgramLogSize(prog, &log_size);
@@ -355,15 +366,20 @@ void write_file(const std::string& p, const std::vector<char>& data) {
   else std::remove(tmp.c_str());
 }
 
+// Variant part of a kernel's cache key.
+std::string variant_key(bool count, bool philox, bool int_state, bool global_state, bool smem_x, int firing) {
+  return std::string(count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
+         (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S") +
+         (firing ? "B" : "");
+}
+
 std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool philox, bool int_state,
-                                   bool global_state, bool smem_x) {
+                                   bool global_state, bool smem_x, int firing) {
   auto jk = std::make_shared<JitKernel>();
   std::vector<char> cubin;
-  const std::string path =
-      cache_path(policy + (count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
-                 (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S"));
+  const std::string path = cache_path(policy + variant_key(count, philox, int_state, global_state, smem_x, firing));
   if (!read_file(path, &cubin)) {
-    if (!nvrtc_compile(policy, count, philox, int_state, global_state, smem_x, &cubin, &jk->log)) {
+    if (!nvrtc_compile(policy, count, philox, int_state, global_state, smem_x, firing, &cubin, &jk->log)) {
       if (jit_debug()) std::fprintf(stderr, "[kin_jit] compile failed:\n%s\n", jk->log.c_str());
       return jk;
     }
@@ -385,16 +401,24 @@ std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool p
 
 bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log) {
   std::vector<char> cubin;
-  return nvrtc_compile(generate_policy(model), count, philox, int_state, false, false, &cubin, log);
+  return nvrtc_compile(generate_policy(model), count, philox, int_state, false, false, 0, &cubin, log);
 }
 
 // KIN_JIT=0: never; KIN_JIT=1: always; unset: launches of >= 8,192
 // simulations (where the one-time NVRTC compilation, ~10 s per variant, cached
 // in memory and on disk, is amortised).
-bool jit_wanted(uint64_t n_sims) {
-  const char* v = std::getenv("KIN_JIT");
-  if (v && *v) return std::atoi(v) != 0;
+bool jit_wanted(uint64_t n_sims, int force) {
+  if (force >= 0) return force != 0;
+  static const int env = [] {
+    const char* v = std::getenv("KIN_JIT");
+    return (v && *v) ? (std::atoi(v) != 0 ? 1 : 0) : -1;
+  }();
+  if (env >= 0) return env != 0;
   return n_sims >= 8192;
+}
+
+void jit_prepare(JitModel* model) {
+  if (model->policy.empty()) model->policy = generate_policy(*model);
 }
 
 cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S,
@@ -406,14 +430,14 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
     return cudaSuccess;
   }
   const bool philox = S.rng_mode == KIN_RNG_PHILOX;
-  const std::string policy = generate_policy(model);
+  const std::string policy = model.policy.empty() ? generate_policy(model) : model.policy;
   const bool global_state = S.gstate != nullptr;
   // split layout (x[] in shared memory, a[] + av[] global) when x[] takes at
   // most 16 KB per warp (>= 13 resident warps/SM): C5 tau 1075 -> 906 ms
   const size_t smem_x_bytes = static_cast<size_t>(T.n) * KIN_STOCH_BLOCK * (int_state ? sizeof(int32_t) : sizeof(double));
   const bool smem_x = global_state && S.gstate_x_smem != 0 && smem_x_bytes <= 16 * 1024;
-  const std::string key = policy + (count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
-                          (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S");
+  const int firing = S.firing == KIN_FIRING_BINOMIAL ? 1 : 0;
+  const std::string key = policy + variant_key(count, philox, int_state, global_state, smem_x, firing);
   std::shared_ptr<JitKernel> jk;
   {
     std::lock_guard<std::mutex> lk(g_mu);
@@ -421,7 +445,7 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
     if (it != g_cache.end()) {
       jk = it->second;
     } else {
-      jk = compile(policy, count, philox, int_state, global_state, smem_x);
+      jk = compile(policy, count, philox, int_state, global_state, smem_x, firing);
       g_cache[key] = jk;
     }
   }
@@ -445,7 +469,7 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
   uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
   if (S.gstate && S.gstate_warps < resident) resident = S.gstate_warps;
   KinSweepDev SW = S;
-  SW.warp_lanes = kin_warp_lanes(S.n_local, resident);
+  SW.warp_lanes = S.warp_lanes > 0 ? S.warp_lanes : kin_warp_lanes(S.n_local, resident);
   const uint64_t blocks = (S.n_local + SW.warp_lanes - 1) / SW.warp_lanes;
   const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);

@@ -19,9 +19,15 @@ struct JitModel {
   std::vector<int> row_ptr, row_reaction, row_delta; // nu rows
   std::vector<int> dep_ptr, dep;                     // propensity dependency graph
   std::vector<double> g;                             // highest reactant order per species
+  std::string policy;                                // generated source (jit_prepare), "" = not yet
 };
 
-bool jit_wanted(uint64_t n_sims);  // KIN_JIT=0/1 overrides the size policy
+// Generate the model's policy source once (cached in the JitModel).
+void jit_prepare(JitModel* model);
+
+// force: 1 always, 0 never, -1 by size (KIN_JIT=0/1, read once per process,
+// overrides the size policy for tests)
+bool jit_wanted(uint64_t n_sims, int force = -1);
 
 // Generate + NVRTC-compile the policy without loading it (no GPU needed).
 bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log);

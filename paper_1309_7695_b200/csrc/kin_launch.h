@@ -57,9 +57,12 @@ cudaError_t launch_hybrid(const KinTables& T, const KinSweepDev& S, const KinOut
 
 // kin_post.cu: statistics and utilities.
 // per-point Welford over runs (ascending run order) of traj_dev [n_local][G*N]
-// starting at local simulation first_sim -> mean/m2 [P][G*N]
+// starting at local simulation first_sim -> mean/m2 [P][G*N]; n_done > 0
+// continues accumulators holding the point's first n_done runs
 cudaError_t launch_point_stats(const double* traj_dev, int gn, uint64_t runs, uint64_t first_sim, uint64_t n_points,
-                               double* mean, double* m2, cudaStream_t stream);
+                               uint64_t n_done, double* mean, double* m2, cudaStream_t stream);
+cudaError_t launch_binomial_draws(uint64_t seed, uint64_t n_trials, double p, int n, uint64_t* out,
+                                  cudaStream_t stream);
 cudaError_t launch_rng_draws(uint64_t seed, int kind, double mean, int n, uint64_t* out, const double* lgamma_tab,
                              cudaStream_t stream);
 cudaError_t measure_fp64_peak(cudaStream_t stream, double* tflops);

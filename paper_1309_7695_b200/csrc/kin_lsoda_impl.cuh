@@ -243,7 +243,7 @@ template <bool kCount, int kN>
 __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, const double* co, uint64_t s,
                           double* smem_base, int* ismem_base, int tid, unsigned mask) {
   constexpr int B = kBlock;
-  const uint64_t sim = S.sim_begin + s;
+  const uint64_t sim = global_sim(S, s);
   const int n = kN > 0 ? kN : T.n, m = T.m, G = T.n_grid;
   Lsoda<kN> L{T, S, co, T.n, m};
   double* p = smem_base + tid;

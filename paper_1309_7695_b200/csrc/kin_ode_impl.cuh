@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * gpb + grp;
   if (s >= S.n_local) return;  // whole groups retire together
   const int N = T.n, M = T.m, G = T.n_grid;
-  const uint64_t sim = S.sim_begin + s;
+  const uint64_t sim = global_sim(S, s);
   Group<L> grpc;
   grpc.mask = (L == 32) ? 0xFFFFFFFFu : (((1u << L) - 1u) << ((threadIdx.x & 31) / L * L));
 

@@ -5,7 +5,9 @@
 // kernels' step sequences are reproducible bit for bit.  The oracle carries an
 // independent copy (oracle/kin_portable_math.hpp).  Accuracy ~1e-15 relative.
 #pragma once
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
 
 namespace kin {
 namespace pmath {

@@ -21,9 +21,12 @@ namespace {
 // One thread per (point, grid*species element): the point's runs are
 // consecutive [sim][g][n] rows, so each run's read is coalesced across the
 // threads of a point and the [P][G][N] writes are contiguous.
+// n_done > 0 continues accumulators that already hold the first n_done runs
+// (a KIN_OUTPUT_STATS_ONLY window boundary inside a point): the same Welford
+// operations as one pass over all runs.  Continuation needs both outputs.
 __global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ traj, int gn, uint64_t runs,
-                                                    uint64_t base, uint64_t n_points, double* __restrict__ mean,
-                                                    double* __restrict__ m2) {
+                                                    uint64_t base, uint64_t n_points, uint64_t n_done,
+                                                    double* __restrict__ mean, double* __restrict__ m2) {
   const uint64_t total = n_points * static_cast<uint64_t>(gn);
   for (uint64_t e = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -31,15 +34,28 @@ __global__ void __launch_bounds__(256) stats_kernel(const double* __restrict__ t
     const uint64_t q = e - p * gn;
     const double* col = traj + (base + p * runs) * gn + q;
     double mu = 0.0, s2 = 0.0;
+    if (n_done) {
+      mu = mean[e];
+      s2 = m2[e];
+    }
     for (uint64_t r = 0; r < runs; ++r) {
       const double xv = __ldcs(col + r * gn);
       const double delta = __dsub_rn(xv, mu);
-      mu = __dadd_rn(mu, __ddiv_rn(delta, static_cast<double>(r + 1)));
+      mu = __dadd_rn(mu, __ddiv_rn(delta, static_cast<double>(n_done + r + 1)));
       s2 = __dadd_rn(s2, __dmul_rn(delta, __dsub_rn(xv, mu)));
     }
     if (mean) __stcs(mean + e, mu);
     if (m2) __stcs(m2 + e, s2);
   }
+}
+
+// n Binomial(n_trials, p) draws from RngStream(seed) (the KIN_FIRING_BINOMIAL sampler).
+__global__ void binomial_kernel(uint64_t seed, uint64_t n_trials, double p, int n, uint64_t* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Xoshiro rng;
+  rng.seed(seed);
+  uint64_t fl = 0;
+  for (int q = 0; q < n; ++q) out[q] = binomial<false>(rng, n_trials, p, fl);
 }
 
 __global__ void rng_kernel(uint64_t seed, int kind, double mean, int n, uint64_t* out, const double* lgamma_tab) {
@@ -110,11 +126,17 @@ __global__ void __launch_bounds__(256) dfma_kernel(double* out, int iters, doubl
 }  // namespace
 
 cudaError_t launch_point_stats(const double* traj_dev, int gn, uint64_t runs, uint64_t base, uint64_t n_points,
-                               double* mean, double* m2, cudaStream_t st) {
+                               uint64_t n_done, double* mean, double* m2, cudaStream_t st) {
   if (n_points == 0 || gn == 0) return cudaSuccess;
   const uint64_t total = n_points * static_cast<uint64_t>(gn);
   const unsigned blocks = static_cast<unsigned>(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-  stats_kernel<<<blocks, 256, 0, st>>>(traj_dev, gn, runs, base, n_points, mean, m2);
+  stats_kernel<<<blocks, 256, 0, st>>>(traj_dev, gn, runs, base, n_points, n_done, mean, m2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_binomial_draws(uint64_t seed, uint64_t n_trials, double p, int n, uint64_t* out,
+                                  cudaStream_t st) {
+  binomial_kernel<<<1, 32, 0, st>>>(seed, n_trials, p, n, out);
   return cudaGetLastError();
 }
 

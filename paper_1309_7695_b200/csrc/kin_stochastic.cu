@@ -31,10 +31,12 @@
 namespace kin {
 
 int kin_warp_lanes(uint64_t n_local, uint64_t resident) {
-  if (const char* v = std::getenv("KIN_WARP_LANES")) {
-    const int w = std::atoi(v);
-    if (w >= 1 && w <= 32) return w;
-  }
+  static const int forced = [] {  // study/test override, read once per process
+    const char* v = std::getenv("KIN_WARP_LANES");
+    const int w = v ? std::atoi(v) : 0;
+    return (w >= 1 && w <= 32) ? w : 0;
+  }();
+  if (forced) return forced;
   if (resident == 0) return 32;
   const uint64_t w = (n_local + resident - 1) / resident;
   return w >= 32 ? 32 : (w < 1 ? 1 : static_cast<int>(w));
@@ -97,7 +99,7 @@ template <bool kCount, bool kPhilox>
 __device__ __forceinline__ void simulate_cle_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
                                                  uint64_t s, double* x, double* a, double* av) {
   constexpr int B = kBlock;
-  const uint64_t sim = S.sim_begin + s;
+  const uint64_t sim = global_sim(S, s);
   const TableModel<double> sm{T, x, a, av};
   const int N = T.n, M = T.m, G = T.n_grid;
   stoch::init_state<double>(T, S, sim, N, x, av);
@@ -202,6 +204,80 @@ __global__ void __launch_bounds__(stoch::kBlock) cle_kernel(const __grid_constan
 // ---- unit seams (kin_device_unit): one path function on one state, through
 // the same device code the sweep kernels run.  One thread; the state sits in
 // shared memory with the kernels' [slot][thread] stride.
+// rre_rhs (deterministic.hpp:85-88, oracle rre_rhs): a(y) from the packed
+// tables, then dx_i = sum over the nu row in reaction order; y[i*ys], f[i*fs].
+// Compiled with -fmad=false (this TU): the oracle's roundings.
+__device__ void unit_rhs(const KinTables& T, const TableModel<double>& sm, const double* y, double* f, int fs) {
+  constexpr int B = kBlock;
+  const int N = T.n, M = T.m;
+  double* x = sm.x;
+  for (int i = 0; i < N; ++i) x[i * B] = y[i * B];
+  for (int j = 0; j < M; ++j) sm.a[j * B] = sm.prop(j);
+  for (int i = 0; i < N; ++i) {
+    double acc = 0.0;
+    for (int p = tab_row_ptr(T, i); p < tab_row_ptr(T, i + 1); ++p) {
+      const uint32_t e = tab_row(T, p);
+      acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(KIN_NU_DELTA(e)), sm.a[KIN_NU_INDEX(e) * B]));
+    }
+    f[i * fs] = acc;
+  }
+}
+
+// rk_step (deterministic.hpp:26-36): one Dormand-Prince 5(4) step of size h
+// from y (k1 = f(y)); out = {y5[N], err, k7[N]} with err = sqrt(mean((e_i /
+// sk_i)^2)), sk_i = atol + rtol * max(|y_i|, |y5_i|) — the stage and error
+// expressions of the oracle's integrate_rre, operation for operation.
+__device__ void unit_rk_step(const KinTables& T, const TableModel<double>& sm, const double* x_in, double h,
+                             double rtol, double atol, double* out) {
+  constexpr int B = kBlock;
+  const int N = T.n;
+  constexpr double a21 = 1.0 / 5.0;
+  constexpr double a31 = 3.0 / 40.0, a32 = 9.0 / 40.0;
+  constexpr double a41 = 44.0 / 45.0, a42 = -56.0 / 15.0, a43 = 32.0 / 9.0;
+  constexpr double a51 = 19372.0 / 6561.0, a52 = -25360.0 / 2187.0, a53 = 64448.0 / 6561.0, a54 = -212.0 / 729.0;
+  constexpr double a61 = 9017.0 / 3168.0, a62 = -355.0 / 33.0, a63 = 46732.0 / 5247.0, a64 = 49.0 / 176.0,
+                   a65 = -5103.0 / 18656.0;
+  constexpr double a71 = 35.0 / 384.0, a73 = 500.0 / 1113.0, a74 = 125.0 / 192.0, a75 = -2187.0 / 6784.0,
+                   a76 = 11.0 / 84.0;
+  constexpr double e1 = 71.0 / 57600.0, e3 = -71.0 / 16695.0, e4 = 71.0 / 1920.0, e5 = -17253.0 / 339200.0,
+                   e6 = 22.0 / 525.0, e7 = -1.0 / 40.0;
+  // stage vectors after the kernel's x/a scratch: y, k1..k7, ys (stride B)
+  double* y = sm.a + static_cast<size_t>(T.m) * B * 2 + static_cast<size_t>(N) * B;
+  double* k[8];
+  for (int q = 0; q < 8; ++q) k[q] = y + static_cast<size_t>(q + 1) * N * B;
+  double* ys = y + static_cast<size_t>(9) * N * B;
+  for (int i = 0; i < N; ++i) y[i * B] = x_in[i];
+  unit_rhs(T, sm, y, k[1], B);
+  for (int i = 0; i < N; ++i) ys[i * B] = y[i * B] + h * (a21 * k[1][i * B]);
+  unit_rhs(T, sm, ys, k[2], B);
+  for (int i = 0; i < N; ++i) ys[i * B] = y[i * B] + h * (a31 * k[1][i * B] + a32 * k[2][i * B]);
+  unit_rhs(T, sm, ys, k[3], B);
+  for (int i = 0; i < N; ++i) ys[i * B] = y[i * B] + h * (a41 * k[1][i * B] + a42 * k[2][i * B] + a43 * k[3][i * B]);
+  unit_rhs(T, sm, ys, k[4], B);
+  for (int i = 0; i < N; ++i)
+    ys[i * B] = y[i * B] + h * (a51 * k[1][i * B] + a52 * k[2][i * B] + a53 * k[3][i * B] + a54 * k[4][i * B]);
+  unit_rhs(T, sm, ys, k[5], B);
+  for (int i = 0; i < N; ++i)
+    ys[i * B] = y[i * B] + h * (a61 * k[1][i * B] + a62 * k[2][i * B] + a63 * k[3][i * B] + a64 * k[4][i * B] +
+                                a65 * k[5][i * B]);
+  unit_rhs(T, sm, ys, k[6], B);
+  for (int i = 0; i < N; ++i)
+    out[i] = y[i * B] + h * (a71 * k[1][i * B] + a73 * k[3][i * B] + a74 * k[4][i * B] + a75 * k[5][i * B] +
+                             a76 * k[6][i * B]);
+  for (int i = 0; i < N; ++i) ys[i * B] = out[i];
+  unit_rhs(T, sm, ys, k[7], B);
+  double sum = 0.0;
+  for (int i = 0; i < N; ++i) {
+    const double e = h * (e1 * k[1][i * B] + e3 * k[3][i * B] + e4 * k[4][i * B] + e5 * k[5][i * B] +
+                          e6 * k[6][i * B] + e7 * k[7][i * B]);
+    const double sk = atol + rtol * fmax(fabs(y[i * B]), fabs(out[i]));
+    const double q = e / sk;
+    sum = sum + q * q;
+  }
+  out[N] = sqrt(sum / static_cast<double>(N));
+  for (int i = 0; i < N; ++i) out[N + 1 + i] = k[7][i * B];
+}
+
 __global__ void __launch_bounds__(32) unit_kernel(const __grid_constant__ KinTables T, int kind, const double* x_in,
                                                   const double* params, double* out) {
   extern __shared__ double smem[];
@@ -238,6 +314,10 @@ __global__ void __launch_bounds__(32) unit_kernel(const __grid_constant__ KinTab
     const uint64_t c = cle_clamp<B>(x, N, &bad);
     for (int i = 0; i < N; ++i) out[i] = x[i * B];
     out[N] = static_cast<double>(c);
+  } else if (kind == 5) {                                   // rre_rhs
+    unit_rhs(T, sm, x, out, 1);
+  } else if (kind == 6) {                                   // rk_step (one DP5(4) step)
+    unit_rk_step(T, sm, x, params[0], params[1], params[2], out);
   }
 }
 
@@ -267,7 +347,7 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
   uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
   if (S.gstate && resident > S.gstate_warps) resident = S.gstate_warps;
   KinSweepDev SW = S;
-  SW.warp_lanes = kin_warp_lanes(S.n_local, resident);
+  SW.warp_lanes = S.warp_lanes > 0 ? S.warp_lanes : kin_warp_lanes(S.n_local, resident);
   const uint64_t blocks = (S.n_local + SW.warp_lanes - 1) / SW.warp_lanes;
   const unsigned grid = static_cast<unsigned>(blocks < resident ? blocks : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
@@ -280,7 +360,8 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
 
 cudaError_t launch_unit(const KinTables& T, int kind, const double* x, const double* params, double* out,
                         cudaStream_t stream) {
-  const size_t smem = static_cast<size_t>(T.m + T.n) * kBlock * sizeof(double);
+  // a[M] + x[N] (+ the rk_step stage vectors: M + 10 N more, see unit_rk_step)
+  const size_t smem = static_cast<size_t>(2 * T.m + 11 * T.n) * kBlock * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

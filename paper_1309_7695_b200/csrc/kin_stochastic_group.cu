@@ -62,7 +62,7 @@ __host__ __device__ __forceinline__ int sim_stride(int n, int m, int n_axes) {
 template <int L, bool kCount>
 __device__ void simulate_group(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, uint64_t s,
                                double* x, double* a, double* kk, double* av, int lane, const GroupSync<L>& gs) {
-  const uint64_t sim = S.sim_begin + s;
+  const uint64_t sim = global_sim(S, s);
   const int N = T.n, M = T.m, G = T.n_grid;
 
   if (lane == 0) {

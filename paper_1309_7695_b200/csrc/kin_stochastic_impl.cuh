@@ -209,6 +209,38 @@ __device__ __forceinline__ int ssa_select(const Model& sm, int M, double a0, dou
   return sel < 0 ? last : sel;
 }
 
+// The firing law of a launch: a compile-time constant in the per-model JIT
+// kernels (KFIRING_), the sweep's field in the table-driven kernel.
+#ifdef KFIRING_
+#define KIN_FIRING_OF(S) (KFIRING_)
+#else
+#define KIN_FIRING_OF(S) ((S).firing)
+#endif
+
+// One reaction of the sequential binomial leap (KIN_FIRING_BINOMIAL; oracle
+// binomial_fire): k_j ~ Binomial(n_j, a_j tau / n_j) with n_j = min over
+// reactants of floor(x_s / stoich_s) at the current amounts (the reactions
+// before j in this leap already applied), Poisson(a_j tau) for a zero-order
+// reaction.  Amounts never go negative, so the leap is never rejected.
+template <bool kCount, class Model, class Rng>
+__device__ __forceinline__ uint64_t binomial_fire(const KinTables& T, const Model& sm, int j, double mean, Rng& rng,
+                                                  uint64_t& flops, const double* lgamma_tab) {
+  const uint64_t d = tab_rdesc(T, j);
+  const int nt = KIN_RD_NTERMS(d);
+  if (nt == 0) return poisson<kCount>(rng, mean, flops, lgamma_tab);
+  if (!(mean > 0.0)) return 0;
+  double lim = KIN_INF;
+  for (int t = 0; t < nt; ++t) {
+    const double x = sm.xv(KIN_RD_SPECIES(d, t));
+    const double v = floor(__ddiv_rn(x, static_cast<double>(KIN_RD_STOICH(d, t))));
+    if (v < lim) lim = v;
+  }
+  if (kCount) flops += static_cast<uint64_t>(nt);
+  if (!(lim > 0.0)) return 0;
+  if (kCount) flops += 1;
+  return binomial<kCount>(rng, static_cast<uint64_t>(lim), __ddiv_rn(mean, lim), flops);
+}
+
 template <class XT, int B = kBlock>
 __device__ __forceinline__ bool init_state(const KinTables& T, const KinSweepDev& S, uint64_t sim, int N, XT* x,
                                            double* av) {
@@ -227,7 +259,7 @@ template <class Model, bool kCount, bool kPhilox, class XT>
 __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
                                              uint64_t s, XT* x, double* a, double* av, int* ovf_flag) {
   constexpr int B = kBlock;
-  const uint64_t sim = S.sim_begin + s;
+  const uint64_t sim = global_sim(S, s);
   const Model sm{T, x, a, av};
   const int N = sm.n(), M = sm.m(), G = T.n_grid;
 
@@ -321,6 +353,34 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
     const double gap = __dsub_rn(t_stop, t);
     if (kCount) flops += 1;
     if (!(tau < gap)) { tau = gap; hit = true; }
+    if (KIN_FIRING_OF(S) == KIN_FIRING_BINOMIAL) {
+      // sequential binomial leap: one attempt, never rejected
+#pragma unroll 1
+      for (int j = 0; j < M; ++j) {
+        uint64_t k, fl = 0;
+        const double mean = __dmul_rn(sm.aval(j), tau);
+        if (kPhilox) {
+          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
+          k = binomial_fire<kCount>(T, sm, j, mean, src, fl, S.lgamma_tab);
+        } else {
+          k = binomial_fire<kCount>(T, sm, j, mean, rng, fl, S.lgamma_tab);
+        }
+        if (kCount) flops += fl;
+        if (k != 0) sm.apply(j, static_cast<long long>(k), ovf);
+      }
+      if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
+      ++ev;
+      if (ovf) break;
+      if (hit) {
+        t = t_stop;
+      } else {
+        t = __dadd_rn(t, tau);
+        if (kCount) flops += 1;
+      }
+      ++n_steps;
+      while (gi < G && tab_grid(T, S, gi) <= t) emit();
+      continue;
+    }
     Xoshiro saved = rng, resume;
     // One Poisson call site (code size): pass 0 draws and applies; a rejected
     // attempt runs pass 1, which replays the same draws (the saved stream is

@@ -97,8 +97,17 @@ struct KinSweepDev {
   const double* axis_values[KIN_MAX_AXES];  // device pointers
   uint64_t runs;        // runs per point R
   uint64_t master_seed;
-  uint64_t sim_begin;   // global index of local simulation 0
+  uint64_t sim_begin;   // contiguous parts: global index of part-local simulation 0
   uint64_t n_local;     // simulations in this launch
+  // Interleaved parts (pt_stride > 0): part-local simulation l = k*runs + r is
+  // run r of global point pt_first + k*pt_stride (kin_sweep_part).  A launch
+  // covers part-local simulations [local_begin, local_begin + n_local); its
+  // outputs are indexed from 0 (global_sim() below).
+  uint64_t pt_first;
+  uint64_t pt_stride;
+  uint64_t local_begin;
+  int32_t firing;       // enum kin_firing (tau methods)
+  int32_t pad_firing_;
   double t_end;
   const double* grid;   // device pointer [n_grid]
   const double* lgamma_tab;  // device pointer [KIN_LGAMMA_N]: glibc lgamma(k+1)
@@ -107,7 +116,8 @@ struct KinSweepDev {
   // grid never exceeds gstate_warps blocks.
   double* gstate;
   uint64_t gstate_warps;
-  // Simulations per warp of the thread-per-simulation kernels (1..32): fewer
+  // Simulations per warp of the thread-per-simulation kernels (1..32; 0 from
+  // the engine = the launcher's fill rule kin_warp_lanes): fewer
   // than 32 when a launch cannot fill the resident warps, so that more warps
   // (each with fewer, less divergent lanes) share the latency.  Set by the
   // launchers (kin_warp_lanes); the per-simulation results do not depend on it.

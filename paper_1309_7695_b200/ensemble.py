@@ -56,6 +56,8 @@ class Method:
     theta_x: float = 100.0
     theta_a: float = 10.0
     repartition_interval: float = 0.0
+    # tau-leap firing law: abi.FIRING_POISSON (the reference) or abi.FIRING_BINOMIAL
+    firing: int = abi.FIRING_POISSON
 
     def deterministic(self) -> bool:
         return self.kind in (MethodKind.Ode, MethodKind.Lsoda)
@@ -67,7 +69,7 @@ class Method:
 
     def c(self) -> abi.KinMethod:
         return abi.KinMethod(int(self.kind), self.tau, self.epsilon, self.integrator.c(), float(self.theta_x),
-                             float(self.theta_a), float(self.repartition_interval))
+                             float(self.theta_a), float(self.repartition_interval), int(self.firing))
 
 
 @dataclass
@@ -166,8 +168,12 @@ def _meta(row) -> TrajectoryMeta:
 
 
 def make_sweep_desc(network: ReactionNetwork, config: SweepConfig, *, seed_mode: int = abi.SEED_SWEEP,
-                    rng_mode: int = abi.RNG_COMPAT, sim_range=None):
-    """Pack a SweepConfig into kin_sweep_desc.  Returns (desc, keepalive)."""
+                    rng_mode: int = abi.RNG_COMPAT, sim_range=None, shard=None, output_mode: int = abi.OUTPUT_FULL,
+                    lanes_per_sim: int = 0, variant: int = 0):
+    """Pack a SweepConfig into kin_sweep_desc.  Returns (desc, keepalive).
+    ``shard=(index, count)`` selects the interleaved point shard (multi-GPU
+    across processes); ``variant`` ORs abi.VARIANT_* flags (forced kernel
+    choices, studies and tests)."""
     if int(config.runs_per_point) < 1:
         raise ValidationError("runs_per_point must be >= 1")  # the engine's sweep_layout check
     keep = []
@@ -191,10 +197,22 @@ def make_sweep_desc(network: ReactionNetwork, config: SweepConfig, *, seed_mode:
     grid = np.ascontiguousarray(config.grid, dtype=np.float64)
     keep += [axes, grid]
     s0, s1 = sim_range if sim_range else (0, 0)
+    sh_i, sh_n = shard if shard else (0, 0)
     d = abi.KinSweepDesc(config.method.c(), len(config.axes), axes, int(config.runs_per_point),
                          int(config.master_seed) & 0xFFFFFFFFFFFFFFFF, seed_mode, rng_mode, float(config.t_end),
-                         len(grid), abi.ptr(grid, C.c_double) if len(grid) else None, s0, s1)
+                         len(grid), abi.ptr(grid, C.c_double) if len(grid) else None, s0, s1, int(sh_i), int(sh_n),
+                         int(output_mode), int(lanes_per_sim), int(variant), 0)
     return d, keep
+
+
+def local_size(desc: abi.KinSweepDesc):
+    """(points with statistics, simulations) of a descriptor's own range/shard."""
+    np_, ns = C.c_uint64(), C.c_uint64()
+    err = abi.KinError()
+    rc = abi.load_library().kin_sweep_local_size(C.byref(desc), C.byref(np_), C.byref(ns), C.byref(err))
+    if rc:
+        raise ValidationError(err.text())
+    return int(np_.value), int(ns.value)
 
 
 def sweep_size(config: SweepConfig):
@@ -249,11 +267,12 @@ class Engine:
         return h
 
     def submit(self, network: ReactionNetwork, config: SweepConfig, out: dict, *, seed_mode=abi.SEED_SWEEP,
-               rng_mode=abi.RNG_COMPAT, sim_range=None):
+               rng_mode=abi.RNG_COMPAT, sim_range=None, **desc_kw):
         """Asynchronous sweep (kin_sweep_submit): results land in the numpy
         arrays of `out` (keys as in sweep(); pinned memory for overlap) once
         wait(ticket) returns."""
-        d, keep = make_sweep_desc(network, config, seed_mode=seed_mode, rng_mode=rng_mode, sim_range=sim_range)
+        d, keep = make_sweep_desc(network, config, seed_mode=seed_mode, rng_mode=rng_mode, sim_range=sim_range,
+                                  **desc_kw)
         o = abi.KinSweepOut(abi.ptr(out.get("traj"), C.c_double), abi.ptr(out.get("meta"), C.c_uint64),
                             abi.ptr(out.get("status"), C.c_int32), abi.ptr(out.get("mean"), C.c_double),
                             abi.ptr(out.get("m2"), C.c_double), abi.ptr(out.get("work"), C.c_uint64))
@@ -273,6 +292,7 @@ class Engine:
         _raise(rc, err)
 
     UNIT_PROPENSITIES, UNIT_SELECT_TAU, UNIT_SSA_STEP, UNIT_TAU_LEAP, UNIT_CLE_STEP = 0, 1, 2, 3, 4
+    UNIT_RRE_RHS, UNIT_RK_STEP = 5, 6
 
     def unit(self, network: ReactionNetwork, kind: int, x, params=()) -> np.ndarray:
         """kin_device_unit: one path function on one state, on the GPU (the
@@ -280,7 +300,7 @@ class Engine:
         xs = np.ascontiguousarray(x, dtype=np.float64)
         ps = np.ascontiguousarray(params, dtype=np.float64)
         n, m = network.species_count(), network.reaction_count()
-        out = np.zeros(max(m, n + 1, 2))
+        out = np.zeros(max(m, 2 * n + 1, 2))
         err = abi.KinError()
         rc = self.lib.kin_device_unit(self.ctx, self.model(network), int(kind), abi.ptr(xs, C.c_double),
                                       abi.ptr(ps, C.c_double) if ps.size else None, int(ps.size),
@@ -289,17 +309,17 @@ class Engine:
         return out
 
     def sweep(self, network: ReactionNetwork, config: SweepConfig, *, seed_mode=abi.SEED_SWEEP,
-              rng_mode=abi.RNG_COMPAT, sim_range=None, want_traj=True, want_stats=True, want_work=False):
+              rng_mode=abi.RNG_COMPAT, sim_range=None, want_traj=True, want_stats=True, want_work=False,
+              **desc_kw):
         """Bulk form: returns dict of numpy arrays (traj [S,G,N], meta [S,6],
-        status [S], mean/m2 [P,G,N], work [S])."""
-        d, keep = make_sweep_desc(network, config, seed_mode=seed_mode, rng_mode=rng_mode, sim_range=sim_range)
-        P, S_all = sweep_size(config)
-        R = int(config.runs_per_point)
-        s0, s1 = sim_range if sim_range else (0, S_all)
-        s1 = s1 or S_all
-        S = s1 - s0
+        status [S], mean/m2 [P,G,N], work [S]) for the descriptor's own range
+        and shard (``desc_kw``: shard, output_mode, lanes_per_sim, variant)."""
+        d, keep = make_sweep_desc(network, config, seed_mode=seed_mode, rng_mode=rng_mode, sim_range=sim_range,
+                                  **desc_kw)
+        Pr, S = local_size(d)
         G, N = len(config.grid), network.species_count()
-        Pr = max(0, s1 // R - (s0 + R - 1) // R)
+        if d.output_mode == abi.OUTPUT_STATS_ONLY:
+            want_traj = False
         res = {
             "traj": np.empty((S, G, N)) if want_traj else None,
             "meta": np.empty((S, 6), dtype=np.uint64),
@@ -344,7 +364,8 @@ def parameter_sweep(network: ReactionNetwork, config: SweepConfig, workers: Opti
     device count of ``engine`` plays its role (per-run results never depend on
     it, SPEC.md:449)."""
     eng = engine or default_engine()
-    res = eng.sweep(network, config, want_traj=False, want_stats=True)
+    # statistics only: the runs stream through a bounded device window
+    res = eng.sweep(network, config, want_traj=False, want_stats=True, output_mode=abi.OUTPUT_STATS_ONLY)
     grid = np.asarray(config.grid, dtype=np.float64)
     shape = [len(ax.values) for ax in config.axes]
     points = []

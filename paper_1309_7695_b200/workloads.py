@@ -63,9 +63,12 @@ def robertson(omega=1e6):
 
 
 # ---- C1 Michaelis-Menten (Wilkinson) ----------------------------------------
-def michaelis_menten():
-    return _net([("S", 301), ("E", 120), ("ES", 0), ("P", 0)],
-                [("c1", 1.66e-3), ("c2", 1e-4), ("c3", 0.1)],
+def michaelis_menten(omega: int = 1):
+    """Wilkinson's parameterisation; omega > 1 scales the volume (amounts x
+    omega, binding rate / omega): the same mean dynamics with leaps instead of
+    SSA bursts (the tau-leap regime)."""
+    return _net([("S", 301 * omega), ("E", 120 * omega), ("ES", 0), ("P", 0)],
+                [("c1", 1.66e-3 / omega), ("c2", 1e-4), ("c3", 0.1)],
                 [("bind", {"E": 1, "S": 1}, {"ES": 1}, "c1"),
                  ("unbind", {"ES": 1}, {"E": 1, "S": 1}, "c2"),
                  ("convert", {"ES": 1}, {"E": 1, "P": 1}, "c3")])

@@ -28,7 +28,7 @@ def test_library_exports_every_symbol():
     lib = abi.load_library()
     for name in declared_functions():
         assert hasattr(lib, name), name
-    assert lib.kin_abi_version() == 2
+    assert lib.kin_abi_version() == 3
     nm = subprocess.run(["nm", "-D", "--defined-only", str(abi.LIB_PATH)], capture_output=True, text=True).stdout
     for name in declared_functions():
         assert re.search(rf"\bT {name}\b", nm), name

@@ -7,6 +7,8 @@ from pathlib import Path
 import numpy as np
 import pytest
 
+from paper_1309_7695_b200 import abi
+
 GOLD = Path(__file__).parent / "golden"
 sys.path.insert(0, str(GOLD))
 from make_golden import cases  # noqa: E402
@@ -15,13 +17,12 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("case", [c[0] for c in cases()])
-@pytest.mark.parametrize("jit", ["0", "1"])
-def test_engine_matches_reference_rng_golden(engine, case, jit, monkeypatch):
-    monkeypatch.setenv("KIN_JIT", jit)
+@pytest.mark.parametrize("jit", [abi.VARIANT_TABLE, abi.VARIANT_JIT])
+def test_engine_matches_reference_rng_golden(engine, case, jit):
     for name, net, cfg, seed_mode, rng in cases():
         if name != case:
             continue
-        got = engine.sweep(net, cfg, seed_mode=seed_mode, sim_range=rng, want_stats=False)
+        got = engine.sweep(net, cfg, seed_mode=seed_mode, sim_range=rng, want_stats=False, variant=jit)
         g = np.load(GOLD / f"traj_{name}.npz")
         assert np.array_equal(got["traj"], g["traj"])
         assert np.array_equal(got["meta"], g["meta"])

@@ -22,11 +22,13 @@ pytestmark = pytest.mark.gpu
 
 
 def both(engine, oracle, net, cfg, *, sim_range=None, seed_mode=abi.SEED_SWEEP, want_work=False, stats=False,
-         rng_mode=abi.RNG_COMPAT):
-    d, keep = make_sweep_desc(net, cfg, seed_mode=seed_mode, sim_range=sim_range, rng_mode=rng_mode)
+         rng_mode=abi.RNG_COMPAT, **desc_kw):
+    """The same descriptor through the oracle and the engine (desc_kw: shard,
+    output_mode, lanes_per_sim, variant — kernel choices the oracle ignores)."""
+    d, keep = make_sweep_desc(net, cfg, seed_mode=seed_mode, sim_range=sim_range, rng_mode=rng_mode, **desc_kw)
     ref = oracle.sweep(net, d, want_traj=True, want_stats=stats, want_work=want_work)
     got = engine.sweep(net, cfg, seed_mode=seed_mode, sim_range=sim_range, want_traj=True, want_stats=stats,
-                       want_work=want_work, rng_mode=rng_mode)
+                       want_work=want_work, rng_mode=rng_mode, **desc_kw)
     return ref, got
 
 
@@ -147,30 +149,28 @@ def test_c5_random_network_bit_exact(engine, oracle):
     assert_bit_exact(ref, got)
 
 
-@pytest.mark.parametrize("gstate", ["0", "1"])
-def test_table_kernel_global_state_bit_exact(engine, oracle, gstate, monkeypatch):
+@pytest.mark.parametrize("gstate", [abi.VARIANT_SMEM_STATE, abi.VARIANT_GLOBAL_STATE])
+def test_table_kernel_global_state_bit_exact(engine, oracle, gstate):
     """Table kernel with the state in shared or global memory: same results."""
-    monkeypatch.setenv("KIN_JIT", "0")
-    monkeypatch.setenv("KIN_GSTATE", gstate)
     net, cfg = W.c4_config()
-    ref, got = both(engine, oracle, net, cfg, sim_range=(3000, 3256), want_work=True)
+    ref, got = both(engine, oracle, net, cfg, sim_range=(3000, 3256), want_work=True,
+                    variant=abi.VARIANT_TABLE | gstate)
     assert_bit_exact(ref, got, work=True)
 
 
-@pytest.mark.parametrize("split", ["0", "1"])
-def test_jit_global_state_layouts_bit_exact(engine, oracle, split, monkeypatch):
+@pytest.mark.parametrize("split", [abi.VARIANT_NO_SPLIT, 0])
+def test_jit_global_state_layouts_bit_exact(engine, oracle, split):
     """JIT kernel with global-memory state: all of it global, or the split layout
     (amounts in shared memory, propensity cache global); same results, both RNG
     modes, with work counts."""
-    monkeypatch.setenv("KIN_JIT", "1")
-    monkeypatch.setenv("KIN_GSTATE", "1")
-    monkeypatch.setenv("KIN_GSTATE_SPLIT", split)
+    v = abi.VARIANT_JIT | abi.VARIANT_GLOBAL_STATE | split
     net, cfg = W.c4_config()
     for rng in (abi.RNG_COMPAT, abi.RNG_PHILOX):
-        ref, got = both(engine, oracle, net, cfg, sim_range=(3000, 3256), want_work=True, rng_mode=rng)
+        ref, got = both(engine, oracle, net, cfg, sim_range=(3000, 3256), want_work=True, rng_mode=rng, variant=v,
+                        lanes_per_sim=1)
         assert_bit_exact(ref, got, work=True)
     net, cfg = W.c5_config()
-    ref, got = both(engine, oracle, net, cfg, sim_range=(2000, 2064))
+    ref, got = both(engine, oracle, net, cfg, sim_range=(2000, 2064), variant=v)
     assert_bit_exact(ref, got)
 
 
@@ -187,20 +187,18 @@ def test_int32_amount_overflow_retry(engine, oracle):
         assert got["traj"][:, -1, 0].max() > 2**31  # crossed the int32 range
 
 
-@pytest.mark.parametrize("int_state", ["0", "1"])
-def test_c4_double_and_int32_amounts_agree(engine, oracle, int_state, monkeypatch):
-    monkeypatch.setenv("KIN_INT_STATE", int_state)
+@pytest.mark.parametrize("variant", [abi.VARIANT_DOUBLE_STATE, 0])
+def test_c4_double_and_int32_amounts_agree(engine, oracle, variant):
     net, cfg = W.c4_config()
-    ref, got = both(engine, oracle, net, cfg, sim_range=(7000, 7256), want_work=True)
+    ref, got = both(engine, oracle, net, cfg, sim_range=(7000, 7256), want_work=True, variant=variant)
     assert_bit_exact(ref, got, work=True)
 
 
 # ---- per-model JIT kernels (NVRTC, kin_jit.cpp): same results as the table kernel --
 @pytest.mark.parametrize("case", ["c4", "c4_double", "c4_philox", "c4_gstate", "c5_gstate", "c2", "c1_ssa", "taufixed",
                                   "overflow"])
-def test_jit_kernel_bit_exact(engine, oracle, case, monkeypatch):
-    monkeypatch.setenv("KIN_JIT", "1")
-    kw = dict(want_work=True)
+def test_jit_kernel_bit_exact(engine, oracle, case):
+    kw = dict(want_work=True, variant=abi.VARIANT_JIT)
     if case == "c5_gstate":  # large model: per-simulation state in global memory (KinSweepDev::gstate)
         net, cfg = W.c5_config(n_grid=11)
         kw["sim_range"] = (40000, 40256)
@@ -208,11 +206,11 @@ def test_jit_kernel_bit_exact(engine, oracle, case, monkeypatch):
         net, cfg = W.c4_config()
         kw["sim_range"] = (12000, 12512)
         if case == "c4_double":
-            monkeypatch.setenv("KIN_INT_STATE", "0")
+            kw["variant"] |= abi.VARIANT_DOUBLE_STATE
         if case == "c4_gstate":
-            monkeypatch.setenv("KIN_GSTATE", "1")
+            kw["variant"] |= abi.VARIANT_GLOBAL_STATE
         if case == "c4_philox":
-            monkeypatch.setenv("KIN_GROUP_LANES", "1")
+            kw["lanes_per_sim"] = 1
             kw["rng_mode"] = abi.RNG_PHILOX
     elif case == "c2":
         net, cfg = W.c2_config()
@@ -229,7 +227,7 @@ def test_jit_kernel_bit_exact(engine, oracle, case, monkeypatch):
                                      [Reaction("birth", {}, {0: 1}, 2e9, 0), Reaction("conv", {1: 1}, {0: 1}, 1.0)])
         cfg = SweepConfig([SweepAxis("lam", [1e8, 2e9])], 8, Method(MethodKind.TauAdaptive), 3, 1.0,
                           uniform_grid(1.0, 11))
-        kw = {}
+        kw = dict(variant=abi.VARIANT_JIT)
     ref, got = both(engine, oracle, net, cfg, **kw)
     assert_bit_exact(ref, got, work=bool(kw.get("want_work")))
 
@@ -247,17 +245,15 @@ def _launch_kernel_ms(engine, net, d, reps=3):
     return best
 
 
-@pytest.mark.parametrize("int_state", ["0", "1"])
-def test_jit_kernel_not_slower_than_table(engine, monkeypatch, int_state):
+@pytest.mark.parametrize("int_state", [abi.VARIANT_DOUBLE_STATE, 0])
+def test_jit_kernel_not_slower_than_table(engine, int_state):
     """Performance guard: the per-model JIT kernel must not lose to the
     table-driven kernel on C4 (a register-to-memory demotion of the RNG state
     once made the int32 JIT variant 33x slower while staying bit-exact)."""
-    monkeypatch.setenv("KIN_INT_STATE", int_state)
     net, cfg = W.c4_config()
-    d, keep = make_sweep_desc(net, cfg, sim_range=(0, 16384))
-    monkeypatch.setenv("KIN_JIT", "0")
+    d, keep = make_sweep_desc(net, cfg, sim_range=(0, 16384), variant=int_state | abi.VARIANT_TABLE)
     t_table = _launch_kernel_ms(engine, net, d)
-    monkeypatch.setenv("KIN_JIT", "1")
+    d, keep = make_sweep_desc(net, cfg, sim_range=(0, 16384), variant=int_state | abi.VARIANT_JIT)
     t_jit = _launch_kernel_ms(engine, net, d)
     print(f"int_state={int_state}: table {t_table:.2f} ms, jit {t_jit:.2f} ms")
     assert t_jit < 1.2 * t_table, (t_jit, t_table)
@@ -314,12 +310,12 @@ def test_device_philox_draws(engine, oracle):
         assert np.array_equal(out, oracle.philox_draws(77, kind, 1000, mean)), (kind, mean)
 
 
-@pytest.mark.parametrize("lanes", ["0", "1", "4", "32"])
+@pytest.mark.parametrize("lanes", [0, 1, 4, 32])
 @pytest.mark.parametrize("case", ["c1", "c4", "c2", "bd_ssa", "taufixed", "c5"])
-def test_philox_mode_bit_exact(engine, oracle, case, lanes, monkeypatch):
+def test_philox_mode_bit_exact(engine, oracle, case, lanes):
     """Philox mode through the lane-group kernel (auto / 4 / 32 lanes per
-    simulation) and the thread-per-simulation kernel (lanes=1)."""
-    monkeypatch.setenv("KIN_GROUP_LANES", lanes)
+    simulation, kin_sweep_desc.lanes_per_sim) and the thread-per-simulation
+    kernel (lanes=1)."""
     sm, rng = abi.SEED_SWEEP, None
     if case == "c1":
         net, cfg = W.c1_config(MethodKind.TauAdaptive)
@@ -340,7 +336,8 @@ def test_philox_mode_bit_exact(engine, oracle, case, lanes, monkeypatch):
         net = W.birth_death(x0=3)
         cfg = SweepConfig([SweepAxis("lam", [0.5, 5.0, 50.0])], 128, Method(MethodKind.TauFixed, tau=0.5), 11, 10.0,
                           uniform_grid(10.0, 21))
-    ref, got = both(engine, oracle, net, cfg, sim_range=rng, seed_mode=sm, want_work=True, rng_mode=abi.RNG_PHILOX)
+    ref, got = both(engine, oracle, net, cfg, sim_range=rng, seed_mode=sm, want_work=True, rng_mode=abi.RNG_PHILOX,
+                    lanes_per_sim=lanes)
     assert_bit_exact(ref, got, work=True)
 
 
@@ -449,19 +446,14 @@ def test_run_single_direct_seed(engine, oracle):
     assert np.array_equal(tr.samples, ref["traj"][0]) and tr.seed == 123456789
 
 
-@pytest.mark.parametrize("jit", ["0", "1"])
-def test_warp_lanes_invariance(engine, oracle, jit, monkeypatch):
+@pytest.mark.parametrize("jit", [abi.VARIANT_TABLE, abi.VARIANT_JIT])
+def test_warp_lanes_invariance(engine, oracle, jit):
     """Simulations per warp (kin_warp_lanes: fewer than 32 for launches that
     cannot fill the GPU) never change a result: 1, 7, 32 and the automatic
     choice give the oracle's trajectories, table and JIT kernels alike."""
     net, cfg = W.c2_config(points=4, runs=40)
-    monkeypatch.setenv("KIN_JIT", jit)
     d, keep = make_sweep_desc(net, cfg)
     ref = oracle.sweep(net, d, want_traj=True, want_work=True)
-    for w in ("1", "7", "32", None):
-        if w is None:
-            monkeypatch.delenv("KIN_WARP_LANES", raising=False)
-        else:
-            monkeypatch.setenv("KIN_WARP_LANES", w)
-        got = engine.sweep(net, cfg, want_traj=True, want_work=True)
+    for w in (1, 7, 32, 0):
+        got = engine.sweep(net, cfg, want_traj=True, want_work=True, variant=jit | (w << 8))
         assert_bit_exact(ref, got, work=True)

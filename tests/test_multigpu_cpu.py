@@ -1,10 +1,10 @@
-"""N>1 path on CPU: world_size-2 gloo processes shard a sweep by whole-point
-ranges (the bench's torchrun layout), each rank simulates its shard, rank 0
-gathers; the result must equal the single-process run bit for bit (per-run
-output independent of the device count).  The per-rank simulator
-here is the CPU oracle standing in for a GPU; the sharding and gather logic is
-the product's (paper_1309_7695_b200/shard.py).  Also checks the engine's
-in-process chunk plan (kin_sweep_plan)."""
+"""N>1 path on CPU: world_size-2 gloo processes shard a sweep by interleaved
+points (kin_sweep_desc shard: the bench's torchrun layout), each rank simulates
+its shard, rank 0 gathers; the result must equal the single-process run bit for
+bit (per-run output independent of the device count).  The per-rank
+simulator here is the CPU oracle (the same descriptor the engine takes; the
+engine itself runs this test on the GPU in tests/test_gpu_multislot.py).  Also
+checks the engine's in-process plan (kin_sweep_plan)."""
 import os
 import socket
 
@@ -29,12 +29,10 @@ def _worker(rank, world, port, which, out_q):
     from oracle import oracle as O
     net, cfg = {"c1": lambda: W.c1_config(MethodKind.TauAdaptive, side=8),
                 "c2": lambda: W.c2_config(points=4, runs=16)}[which]()
-    P, S = sweep_size(cfg)
-    s0, s1 = shard.rank_range(P, cfg.runs_per_point, rank, world)
-    d, keep = make_sweep_desc(net, cfg, sim_range=(s0, s1))
+    d, keep = make_sweep_desc(net, cfg, shard=shard.rank_shard(rank, world))
     r = O.sweep(net, d, workers=1, want_stats=True)
     parts = [None] * world
-    dist.all_gather_object(parts, (s0, s1, r["traj"], r["mean"], r["m2"]))
+    dist.all_gather_object(parts, (rank, world, r["traj"], r["mean"], r["m2"]))
     if rank == 0:
         out_q.put(parts)
     dist.barrier()
@@ -58,28 +56,52 @@ def test_two_rank_shard_equals_single_process(which):
                 "c2": lambda: W.c2_config(points=4, runs=16)}[which]()
     d, keep = make_sweep_desc(net, cfg)
     full = O.sweep(net, d, workers=3, want_stats=True)
-    assert parts[0][0] == 0 and parts[0][1] == parts[1][0] and parts[1][1] == len(full["traj"])
-    assert np.array_equal(shard.gather([p[2] for p in parts]), full["traj"])
-    assert np.array_equal(shard.gather([p[3] for p in parts]), full["mean"])
-    assert np.array_equal(shard.gather([p[4] for p in parts]), full["m2"])
+    R = cfg.runs_per_point
+    assert np.array_equal(shard.scatter_shards([p[2] for p in parts], R), full["traj"])
+    assert np.array_equal(shard.scatter_shards([p[3] for p in parts], 1), full["mean"])
+    assert np.array_equal(shard.scatter_shards([p[4] for p in parts], 1), full["m2"])
 
 
-@pytest.mark.parametrize("s0,s1,R,D", [(0, 65536, 1, 8), (0, 16384, 256, 8), (100, 1000, 7, 3), (0, 10, 1, 1),
-                                        (5, 5, 1, 4), (0, 512, 256, 8), (0, 10000, 10000, 4), (3, 9, 100, 8)])
-def test_engine_chunk_plan(s0, s1, R, D):
-    chunks = shard.plan(s0, s1, R, D)
-    assert chunks[0][0] == s0 and chunks[-1][1] == s1
-    for (a0, a1, dv), (b0, b1, _) in zip(chunks, chunks[1:]):
-        assert a1 == b0 and a0 <= a1
-    points = (s1 - 1) // R - s0 // R + 1 if s1 > s0 else 0
-    for c0, c1, dv in chunks[1:]:
-        if c0 not in (s0, s1) and points >= D:
-            assert c0 % R == 0  # whole points: every interior boundary on a point boundary
-    if 0 < points < D:  # fewer points than devices: the runs are split evenly
-        assert len(chunks) == min(s1 - s0, D)
-    assert [c[2] for c in chunks] == [i % D for i in range(len(chunks))]
-    if D == 1:
-        assert len(chunks) == 1
+def _part_sims(p, R):
+    """(caller-local index, global simulation) pairs of one kin_sweep_part."""
+    if p.interleaved:
+        for k in range(p.n_points):
+            for r in range(R):
+                yield p.out_first + k * p.out_pitch + r, (p.pt_first + k * p.pt_stride) * R + r
+    else:
+        for i, g in enumerate(range(p.sim_begin, p.sim_end)):
+            yield p.out_first + i, g
+
+
+@pytest.mark.parametrize("s0,s1,R,D,sh", [(0, 65536, 1, 8, (0, 1)), (0, 16384, 256, 8, (0, 1)),
+                                          (100, 1000, 7, 3, (0, 1)), (0, 10, 1, 1, (0, 1)), (5, 5, 1, 4, (0, 1)),
+                                          (0, 512, 256, 8, (0, 1)), (0, 10000, 10000, 4, (0, 1)),
+                                          (3, 9, 100, 8, (0, 1)), (0, 65536, 1, 8, (3, 8)), (0, 1000, 10, 3, (1, 2)),
+                                          (70, 770, 7, 4, (2, 3)), (0, 30, 1, 8, (5, 8)), (0, 12, 1, 2, (0, 1))])
+def test_engine_plan_covers_the_call(s0, s1, R, D, sh):
+    """kin_sweep_plan: the parts cover the caller's simulations exactly once, in
+    the caller's layout (global order, or the shard's compact interleaved order),
+    one part per device at most; whole points and >= D points interleave."""
+    parts = shard.plan(s0, s1, R, D, sh)
+    i, n = sh
+    if n > 1:
+        pts = list(range(s0 // R, s1 // R))[i::n]
+        want = [p * R + r for p in pts for r in range(R)]
+    else:
+        want = list(range(s0, s1))
+    got = {}
+    for p in parts:
+        for loc, g in _part_sims(p, R):
+            assert loc not in got
+            got[loc] = g
+    assert sorted(got) == list(range(len(want)))
+    assert [got[k] for k in range(len(want))] == want
+    assert len({p.device for p in parts}) == len(parts) and all(0 <= p.device < D for p in parts)
+    points = (s1 - s0) // R if s0 % R == 0 and s1 % R == 0 else -1
+    if D > 1 and (n > 1 or points >= D):
+        assert all(p.interleaved for p in parts)
+    if D == 1 and n == 1 and s1 > s0:
+        assert len(parts) == 1 and not parts[0].interleaved
 
 
 def test_rank_range_partition():
@@ -88,6 +110,13 @@ def test_rank_range_partition():
         assert rngs[0][0] == 0 and rngs[-1][1] == P * R
         assert all(a[1] == b[0] for a, b in zip(rngs, rngs[1:]))
         assert all(r[0] % R == 0 for r in rngs)
+
+
+def test_scatter_shards_inverts_the_interleave():
+    R, P, W = 3, 11, 4
+    full = np.arange(P * R * 2).reshape(P * R, 2)
+    parts = [full.reshape(P, R, 2)[r::W].reshape(-1, 2) for r in range(W)]
+    assert np.array_equal(shard.scatter_shards(parts, R), full)
 
 
 def test_merge_statistics_matches_oracle():

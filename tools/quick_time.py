@@ -43,13 +43,12 @@ print("fp64 peak TFLOP/s", peak.value, flush=True)
 import os
 for name in names:
     base, _, mode = name.partition(":")
+    lanes = 0
     if "@" in mode:
         mode, lanes = mode.split("@")
-        os.environ["KIN_GROUP_LANES"] = lanes
-    else:
-        os.environ.pop("KIN_GROUP_LANES", None)
     net, cfg = cfgs[base]
-    d, keep = make_sweep_desc(net, cfg, rng_mode=abi.RNG_PHILOX if mode == "philox" else abi.RNG_COMPAT)
+    d, keep = make_sweep_desc(net, cfg, rng_mode=abi.RNG_PHILOX if mode == "philox" else abi.RNG_COMPAT,
+                              lanes_per_sim=int(lanes))
     h = eng.model(net)
     # counting pass
     rc = lib.kin_sweep_launch(eng.ctx, h, C.byref(d), 0, 0, 1, C.byref(err)); assert rc == 0, err.text()
