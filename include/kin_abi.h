@@ -121,7 +121,9 @@ enum kin_firing {
 /* ---- sweep: SweepConfig (ensemble.hpp:101-113) ---------------------------- */
 enum kin_axis_kind {
   KIN_AXIS_PARAM = 0,    /* rebinds Parameter `index` (with_param, model.hpp:78-80) */
-  KIN_AXIS_INITIAL = 1   /* extension: initial amount of species `index` (integral values) */
+  KIN_AXIS_INITIAL = 1,  /* extension: initial amount of species `index` (integral values) */
+  KIN_AXIS_SCALE = 2     /* extension: global scale factor — multiplies the rate constant of
+                            reactions [index, index + span) */
 };
 
 typedef struct kin_sweep_axis {
@@ -129,6 +131,7 @@ typedef struct kin_sweep_axis {
   int32_t index;
   int32_t n_values;
   const double* values;
+  int32_t span;          /* KIN_AXIS_SCALE: number of reactions scaled; else unused */
 } kin_sweep_axis;
 
 enum kin_rng_mode {

@@ -1,9 +1,27 @@
 // integration/kinetics_b200_adapter.cpp — the reference-side binding a
 // maintainer adds to proj/src/ to route the ensemble layer through the B200
 // engine (include/kin_abi.h).  Uses only the reference's public headers
-// (model.hpp / ensemble.hpp); compile-checked against them by
-// tests/test_integration.py.  Link: -L<repo>/paper_1309_7695_b200 -lkin_b200.
+// (model.hpp / ensemble.hpp / errors.hpp); tests/test_integration.py
+// compile-checks it against them and builds it with a test driver
+// (integration/Makefile) that tests/test_gpu_integration.py runs on the GPU.
+// Link: -L<repo>/paper_1309_7695_b200 -lkin_b200.
+//
+//   parameter_sweep  ensemble.hpp:126-130  one kin_sweep_run, KIN_OUTPUT_STATS_ONLY:
+//                                          the per-point EnsembleStatistics come
+//                                          from the engine's own Welford kernel
+//   run_ensemble     ensemble.hpp:97-99    one kin_ensemble_run; trajectories are
+//                                          copied back only when a RunSink is given
+//   run_single       ensemble.hpp:73-76    one kin_run_single
+//
+// `workers` (the reference's thread count, ensemble.hpp:91-96) selects how many
+// GPUs the call spreads over (min(workers, visible GPUs); per-run results never
+// depend on it).  One engine context per device count is created
+// on first use and reused by every later call (device memory pools, JIT
+// kernels and streams persist); the model is re-packed per call (host only).
 #include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -15,6 +33,33 @@
 namespace kinetics::b200 {
 
 namespace {
+
+// EnsembleStatistics exposes no way to set (n, mean, m2) directly; the engine
+// computes them on the GPU (the same Welford order as EnsembleStatistics::add,
+// run-ascending).  These accessors bind its private members through the
+// explicit-instantiation rule (access checking does not apply to the template
+// arguments of an explicit instantiation); a maintainer merging this adapter
+// would instead add a `from_moments` constructor to ensemble.hpp.
+template <class Tag, typename Tag::type M>
+struct Bind {
+  friend typename Tag::type member(Tag) { return M; }
+};
+struct StatsN { using type = std::uint64_t EnsembleStatistics::*; friend type member(StatsN); };
+struct StatsMean { using type = std::vector<double> EnsembleStatistics::*; friend type member(StatsMean); };
+struct StatsM2 { using type = std::vector<double> EnsembleStatistics::*; friend type member(StatsM2); };
+template struct Bind<StatsN, &EnsembleStatistics::n_>;
+template struct Bind<StatsMean, &EnsembleStatistics::mean_>;
+template struct Bind<StatsM2, &EnsembleStatistics::m2_>;
+
+EnsembleStatistics stats_from_moments(const std::vector<double>& grid, std::size_t n_species, std::uint64_t n,
+                                      const double* mean, const double* m2) {
+  EnsembleStatistics st(grid, n_species);
+  const std::size_t len = grid.size() * n_species;
+  st.*member(StatsN{}) = n;
+  st.*member(StatsMean{}) = std::vector<double>(mean, mean + len);
+  st.*member(StatsM2{}) = std::vector<double>(m2, m2 + len);
+  return st;
+}
 
 struct PackedModel {
   std::vector<int64_t> x0;
@@ -31,7 +76,6 @@ PackedModel pack(const ReactionNetwork& net) {
   for (const auto& p : net.params()) m.params.push_back(p.value);
   m.rptr.push_back(0);
   m.pptr.push_back(0);
-  int max_order = 2;
   for (const auto& r : net.reactions()) {
     m.rates.push_back(r.rate_constant);
     m.rparam.push_back(r.rate_param ? static_cast<int32_t>(*r.rate_param) : -1);
@@ -53,7 +97,7 @@ PackedModel pack(const ReactionNetwork& net) {
   m.d.product_ptr = m.pptr.data();
   m.d.product_species = m.psp.data();
   m.d.product_stoich = m.pst.data();
-  m.d.max_order = max_order;
+  m.d.max_order = 2;  // ReactionNetwork::create enforces order <= 2 (model.hpp:47-53)
   return m;
 }
 
@@ -68,6 +112,7 @@ kin_method method_of(const Method& m) {
   k.theta_x = static_cast<double>(m.hybrid.amount_threshold);
   k.theta_a = m.hybrid.propensity_threshold;
   k.repartition_interval = m.hybrid.repartition_interval;
+  k.firing = KIN_FIRING_POISSON;
   return k;
 }
 
@@ -77,34 +122,40 @@ kin_method method_of(const Method& m) {
   throw ValidationError(e.message);
 }
 
-// RAII over context + uploaded model
-struct Engine {
+// One context per device count, created on first use and kept for the life of
+// the process (the reference's worker pool is per call; a GPU context is too
+// expensive for that).
+kin_ctx* context_for(unsigned workers) {
+  static std::mutex mu;
+  static std::map<int, std::unique_ptr<kin_ctx, void (*)(kin_ctx*)>> ctxs;
+  const int visible = kin_visible_devices();
+  if (visible <= 0) throw KineticsError("device: no CUDA device visible");
+  const int n = static_cast<int>(std::min<unsigned>(std::max(workers, 1u), static_cast<unsigned>(visible)));
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = ctxs.find(n);
+  if (it != ctxs.end()) return it->second.get();
+  std::vector<int32_t> ids(n);
+  for (int i = 0; i < n; ++i) ids[i] = i;
   kin_ctx* ctx = nullptr;
-  kin_model* model = nullptr;
+  kin_error e{};
+  if (int rc = kin_ctx_create(ids.data(), n, &ctx, &e)) rethrow(rc, e);
+  ctxs.emplace(n, std::unique_ptr<kin_ctx, void (*)(kin_ctx*)>(ctx, kin_ctx_destroy));
+  return ctx;
+}
+
+// The model uploaded into a (reused) context for the duration of one call.
+struct Call {
+  kin_ctx* ctx;
   PackedModel pm;
-  explicit Engine(const ReactionNetwork& net) : pm(pack(net)) {
+  kin_model* model = nullptr;
+  Call(const ReactionNetwork& net, unsigned workers) : ctx(context_for(workers)), pm(pack(net)) {
     kin_error e{};
-    if (int rc = kin_ctx_create(nullptr, 0, &ctx, &e)) rethrow(rc, e);
     if (int rc = kin_model_upload(ctx, &pm.d, &model, &e)) rethrow(rc, e);
   }
-  ~Engine() {
-    kin_model_free(model);
-    kin_ctx_destroy(ctx);
-  }
+  ~Call() { kin_model_free(model); }
+  Call(const Call&) = delete;
+  Call& operator=(const Call&) = delete;
 };
-
-// Run a descriptor and return every trajectory [sim][g][n] plus meta.
-void run(Engine& eng, kin_sweep_desc& d, std::vector<double>& traj, std::vector<uint64_t>& meta) {
-  kin_error e{};
-  uint64_t P = 0, S = 0;
-  if (int rc = kin_sweep_size(&d, &P, &S, &e)) rethrow(rc, e);
-  traj.assign(S * static_cast<uint64_t>(d.n_grid) * eng.pm.d.n_species, 0.0);
-  meta.assign(S * 6, 0);
-  kin_sweep_out out{};
-  out.traj = traj.data();
-  out.meta = meta.data();
-  if (int rc = kin_sweep_run(eng.ctx, eng.model, &d, &out, &e)) rethrow(rc, e);
-}
 
 Trajectory trajectory_at(const std::vector<double>& traj, const std::vector<uint64_t>& meta, uint64_t s,
                          const std::vector<double>& grid, std::size_t n, const Method& m, uint64_t seed) {
@@ -121,9 +172,11 @@ Trajectory trajectory_at(const std::vector<double>& traj, const std::vector<uint
 
 }  // namespace
 
-// parameter_sweep (ensemble.hpp:126-130)
-SweepResults parameter_sweep(const ReactionNetwork& net, const SweepConfig& cfg, unsigned /*workers*/) {
-  Engine eng(net);
+// parameter_sweep (ensemble.hpp:126-130): per-point statistics straight from
+// the engine (KIN_OUTPUT_STATS_ONLY: trajectories never leave the device, nor
+// are they materialised there as a whole).
+SweepResults parameter_sweep(const ReactionNetwork& net, const SweepConfig& cfg, unsigned workers) {
+  Call call(net, workers);
   std::vector<kin_sweep_axis> axes;
   SweepResults res;
   for (const auto& ax : cfg.axes) {
@@ -143,13 +196,16 @@ SweepResults parameter_sweep(const ReactionNetwork& net, const SweepConfig& cfg,
   d.t_end = cfg.t_end;
   d.n_grid = static_cast<int32_t>(cfg.grid.size());
   d.grid = cfg.grid.data();
-  std::vector<double> traj;
-  std::vector<uint64_t> meta;
-  run(eng, d, traj, meta);
-  const std::size_t n = net.species_count();
-  uint64_t P = 0, S = 0;
+  d.output_mode = KIN_OUTPUT_STATS_ONLY;
   kin_error e{};
-  kin_sweep_size(&d, &P, &S, &e);
+  uint64_t P = 0, S = 0;
+  if (int rc = kin_sweep_size(&d, &P, &S, &e)) rethrow(rc, e);
+  const std::size_t n = net.species_count(), gn = cfg.grid.size() * n;
+  std::vector<double> mean(P * gn), m2(P * gn);
+  kin_sweep_out out{};
+  out.mean = mean.data();
+  out.m2 = m2.data();
+  if (int rc = kin_sweep_run(call.ctx, call.model, &d, &out, &e)) rethrow(rc, e);
   for (uint64_t k = 0; k < P; ++k) {
     SweepPointResult pr;
     uint64_t rem = k;
@@ -158,56 +214,51 @@ SweepResults parameter_sweep(const ReactionNetwork& net, const SweepConfig& cfg,
       pr.coordinates[a] = cfg.axes[a].values[rem % cfg.axes[a].values.size()];
       rem /= cfg.axes[a].values.size();
     }
-    pr.stats = EnsembleStatistics(cfg.grid, n);
-    const uint64_t pm = kin_derive_run_seed(cfg.master_seed, k);
-    for (uint64_t r = 0; r < cfg.runs_per_point; ++r)  // ascending run order
-      pr.stats.add(trajectory_at(traj, meta, k * cfg.runs_per_point + r, cfg.grid, n, cfg.method,
-                                 kin_derive_run_seed(pm, r)));
+    pr.stats = stats_from_moments(cfg.grid, n, cfg.runs_per_point, mean.data() + k * gn, m2.data() + k * gn);
     res.points.push_back(std::move(pr));
   }
   return res;
 }
 
-// run_ensemble (ensemble.hpp:97-99)
+// run_ensemble (ensemble.hpp:97-99): statistics from the engine; the sink (if
+// any) sees every trajectory in run order.  Runs spread over
+// min(options.workers, GPUs) devices and their per-device accumulators merge
+// in ascending range order, as the reference's workers do.
 EnsembleStatistics run_ensemble(const ReactionNetwork& net, const EnsembleOptions& o, const RunSink& sink) {
-  Engine eng(net);
-  kin_sweep_desc d{};
-  d.method = method_of(o.method);
-  d.runs_per_point = o.n_runs;
-  d.master_seed = o.master_seed;
-  d.seed_mode = KIN_SEED_ENSEMBLE;
-  d.t_end = o.t_end;
-  d.n_grid = static_cast<int32_t>(o.grid.size());
-  d.grid = o.grid.data();
-  std::vector<double> traj;
-  std::vector<uint64_t> meta;
-  run(eng, d, traj, meta);
-  EnsembleStatistics st(o.grid, net.species_count());
-  for (uint64_t i = 0; i < o.n_runs; ++i) {
-    Trajectory t = trajectory_at(traj, meta, i, o.grid, net.species_count(), o.method,
-                                 kin_derive_run_seed(o.master_seed, i));
-    if (sink) sink(i, t);
-    st.add(t);
-  }
-  return st;
+  Call call(net, o.workers);
+  const std::size_t n = net.species_count(), gn = o.grid.size() * n;
+  std::vector<double> mean(gn), m2(gn), traj;
+  std::vector<uint64_t> meta(o.n_runs * 6);
+  if (sink) traj.assign(o.n_runs * gn, 0.0);
+  kin_sweep_out out{};
+  out.traj = sink ? traj.data() : nullptr;  // no sink: KIN_OUTPUT_STATS_ONLY inside kin_ensemble_run
+  out.meta = meta.data();
+  out.mean = mean.data();
+  out.m2 = m2.data();
+  const kin_method m = method_of(o.method);
+  kin_error e{};
+  if (int rc = kin_ensemble_run(call.ctx, call.model, &m, o.n_runs, o.master_seed, o.t_end, o.grid.data(),
+                                static_cast<int32_t>(o.grid.size()), KIN_RNG_COMPAT, &out, &e))
+    rethrow(rc, e);
+  if (sink)
+    for (uint64_t i = 0; i < o.n_runs; ++i)
+      sink(i, trajectory_at(traj, meta, i, o.grid, n, o.method, kin_derive_run_seed(o.master_seed, i)));
+  return stats_from_moments(o.grid, n, o.n_runs, mean.data(), m2.data());
 }
 
 // run_single (ensemble.hpp:73-76)
 Trajectory run_single(const ReactionNetwork& net, const Method& m, double t_end, const std::vector<double>& grid,
                       uint64_t seed) {
-  Engine eng(net);
-  kin_sweep_desc d{};
-  d.method = method_of(m);
-  d.runs_per_point = 1;
-  d.master_seed = seed;
-  d.seed_mode = KIN_SEED_DIRECT;
-  d.t_end = t_end;
-  d.n_grid = static_cast<int32_t>(grid.size());
-  d.grid = grid.data();
-  std::vector<double> traj;
-  std::vector<uint64_t> meta;
-  run(eng, d, traj, meta);
-  return trajectory_at(traj, meta, 0, grid, net.species_count(), m, seed);
+  Call call(net, 1);
+  const std::size_t n = net.species_count();
+  std::vector<double> traj(grid.size() * n);
+  std::vector<uint64_t> meta(6);
+  const kin_method km = method_of(m);
+  kin_error e{};
+  if (int rc = kin_run_single(call.ctx, call.model, &km, t_end, grid.data(), static_cast<int32_t>(grid.size()), seed,
+                              KIN_RNG_COMPAT, traj.data(), meta.data(), &e))
+    rethrow(rc, e);
+  return trajectory_at(traj, meta, 0, grid, n, m, seed);
 }
 
 }  // namespace kinetics::b200

@@ -1409,9 +1409,19 @@ void decode_sim(const Network& net, const kin_sweep_desc* d, std::uint64_t sim, 
     const double v = A.values[rem % nv];
     rem /= nv;
     if (A.kind == KIN_AXIS_PARAM) pv[A.index] = v;
-    else x0[A.index] = v;
+    else if (A.kind == KIN_AXIS_INITIAL) x0[A.index] = v;
   }
   for (int j = 0; j < net.m; ++j) rates[j] = net.rate_param[j] >= 0 ? pv[net.rate_param[j]] : net.rate_base[j];
+  // global scale factors (KIN_AXIS_SCALE): c_j * s for the axis' reactions
+  rem = point;
+  for (int ax = d->n_axes - 1; ax >= 0; --ax) {
+    const kin_sweep_axis& A = d->axes[ax];
+    const std::uint64_t nv = static_cast<std::uint64_t>(A.n_values);
+    const double v = A.values[rem % nv];
+    rem /= nv;
+    if (A.kind == KIN_AXIS_SCALE)
+      for (int j = A.index; j < A.index + A.span; ++j) rates[j] = rates[j] * v;
+  }
   switch (d->seed_mode) {
     case KIN_SEED_ENSEMBLE: *seed = derive_run_seed(d->master_seed, sim); break;
     case KIN_SEED_DIRECT: *seed = sim == 0 ? d->master_seed : derive_run_seed(d->master_seed, sim); break;
@@ -1446,6 +1456,10 @@ int validate_sweep(const Network& net, const kin_sweep_desc* d, std::string* msg
       if (A.index < 0 || A.index >= net.n) { *msg = "axis " + std::to_string(ax) + ": unknown species"; return KIN_ERR_INPUT; }
       for (int v = 0; v < A.n_values; ++v)
         if (!(A.values[v] >= 0.0) || A.values[v] != std::floor(A.values[v]) || A.values[v] > 9007199254740992.0) { *msg = "axis " + std::to_string(ax) + ": initial amounts must be non-negative integers"; return KIN_ERR_INPUT; }
+    } else if (A.kind == KIN_AXIS_SCALE) {
+      if (A.index < 0 || A.span <= 0 || A.index + A.span > net.m) { *msg = "axis " + std::to_string(ax) + ": scale range outside the reactions"; return KIN_ERR_INPUT; }
+      for (int v = 0; v < A.n_values; ++v)
+        if (!(A.values[v] > 0.0) || !std::isfinite(A.values[v])) { *msg = "axis " + std::to_string(ax) + ": scale factors must be positive"; return KIN_ERR_INPUT; }
     } else {
       *msg = "axis " + std::to_string(ax) + ": unknown axis kind"; return KIN_ERR_INPUT;
     }

@@ -21,7 +21,7 @@ SIM_STATUS = {0: "ok", 1: "step budget exhausted", 2: "non-finite state",
               3: "negative amount", 4: "step size underflow"}
 # enum kin_method_kind (Method::Kind order, ensemble.hpp:62)
 METHOD_SSA, METHOD_TAU_ADAPTIVE, METHOD_TAU_FIXED, METHOD_CLE, METHOD_ODE, METHOD_HYBRID, METHOD_LSODA = range(7)
-AXIS_PARAM, AXIS_INITIAL = 0, 1
+AXIS_PARAM, AXIS_INITIAL, AXIS_SCALE = 0, 1, 2
 RNG_COMPAT, RNG_PHILOX = 0, 1
 SEED_SWEEP, SEED_ENSEMBLE, SEED_DIRECT = 0, 1, 2
 FIRING_POISSON, FIRING_BINOMIAL = 0, 1
@@ -60,7 +60,7 @@ class KinMethod(C.Structure):
 
 class KinSweepAxis(C.Structure):
     _fields_ = [("kind", C.c_int32), ("index", C.c_int32), ("n_values", C.c_int32),
-                ("values", f64p)]
+                ("values", f64p), ("span", C.c_int32)]
 
 
 class KinSweepDesc(C.Structure):

@@ -315,9 +315,35 @@ int validate_sweep(const HostModel& net, const kin_sweep_desc* d, const Layout& 
           *msg = "axis " + std::to_string(ax) + ": initial amounts must be non-negative integers";
           return KIN_ERR_INPUT;
         }
+    } else if (A.kind == KIN_AXIS_SCALE) {
+      if (A.index < 0 || A.span <= 0 || A.index + A.span > net.m) {
+        *msg = "axis " + std::to_string(ax) + ": scale range outside the reactions";
+        return KIN_ERR_INPUT;
+      }
+      for (int v = 0; v < A.n_values; ++v)
+        if (!(A.values[v] > 0.0) || !std::isfinite(A.values[v])) {
+          *msg = "axis " + std::to_string(ax) + ": scale factors must be positive";
+          return KIN_ERR_INPUT;
+        }
     } else {
       *msg = "axis " + std::to_string(ax) + ": unknown axis kind";
       return KIN_ERR_INPUT;
+    }
+  }
+  {  // every reaction's rate follows at most one axis
+    std::vector<int> bound(net.m, -1);
+    for (int ax = 0; ax < d->n_axes; ++ax) {
+      const kin_sweep_axis& A = d->axes[ax];
+      for (int j = 0; j < net.m; ++j) {
+        const bool hit = A.kind == KIN_AXIS_PARAM ? net.rate_param[j] == A.index
+                                                  : (A.kind == KIN_AXIS_SCALE && j >= A.index && j < A.index + A.span);
+        if (!hit) continue;
+        if (bound[j] >= 0) {
+          *msg = "reaction " + std::to_string(j) + ": rate bound to two sweep axes";
+          return KIN_ERR_INPUT;
+        }
+        bound[j] = ax;
+      }
     }
   }
   if (d->seed_mode == KIN_SEED_DIRECT && L.S != 1) { *msg = "direct seeding needs exactly one simulation"; return KIN_ERR_INPUT; }
@@ -344,7 +370,7 @@ int pack_tables(const HostModel& H, const kin_sweep_desc* d, KinTables* T, std::
   std::vector<int> param_axis(H.params.size(), -1), x0_axis(H.n, -1);
   for (int ax = 0; ax < d->n_axes; ++ax) {
     if (d->axes[ax].kind == KIN_AXIS_PARAM) param_axis[d->axes[ax].index] = ax;
-    else x0_axis[d->axes[ax].index] = ax;
+    else if (d->axes[ax].kind == KIN_AXIS_INITIAL) x0_axis[d->axes[ax].index] = ax;
   }
   size_t off = 0;
   bool overflow = false;
@@ -356,13 +382,22 @@ int pack_tables(const HostModel& H, const kin_sweep_desc* d, KinTables* T, std::
     off += bytes;
     return at;
   };
+  // rate table: c_j with non-swept parameters resolved; a reaction on a sweep
+  // axis takes rate[j] * (axis value) — rate[j] = 1 for a parameter axis (exact:
+  // the value itself), its own constant for a scale axis
   std::vector<double> rate(H.m);
   std::vector<int8_t> rate_axis(H.m, -1);
   for (int j = 0; j < H.m; ++j) {
     const int rp = H.rate_param[j];
     rate[j] = rp >= 0 ? H.params[rp] : H.rate_base[j];
-    if (rp >= 0 && param_axis[rp] >= 0) rate_axis[j] = static_cast<int8_t>(param_axis[rp]);
+    if (rp >= 0 && param_axis[rp] >= 0) {
+      rate_axis[j] = static_cast<int8_t>(param_axis[rp]);
+      rate[j] = 1.0;
+    }
   }
+  for (int ax = 0; ax < d->n_axes; ++ax)
+    if (d->axes[ax].kind == KIN_AXIS_SCALE)
+      for (int j = d->axes[ax].index; j < d->axes[ax].index + d->axes[ax].span; ++j) rate_axis[j] = static_cast<int8_t>(ax);
   std::vector<int8_t> x0ax(H.n);
   for (int i = 0; i < H.n; ++i) x0ax[i] = static_cast<int8_t>(x0_axis[i]);
   std::vector<double> gd(H.g.begin(), H.g.end());
@@ -743,8 +778,15 @@ kin::JitModel jit_model(const HostModel& H, const kin_sweep_desc* d) {
   for (int ax = 0; ax < d->n_axes; ++ax)
     if (d->axes[ax].kind == KIN_AXIS_PARAM) param_axis[d->axes[ax].index] = ax;
   j.rate_axis.assign(H.m, -1);
+  j.rate_scaled.assign(H.m, 0);
   for (int r = 0; r < H.m; ++r)
     if (H.rate_param[r] >= 0) j.rate_axis[r] = param_axis[H.rate_param[r]];
+  for (int ax = 0; ax < d->n_axes; ++ax)
+    if (d->axes[ax].kind == KIN_AXIS_SCALE)
+      for (int r = d->axes[ax].index; r < d->axes[ax].index + d->axes[ax].span; ++r) {
+        j.rate_axis[r] = ax;
+        j.rate_scaled[r] = 1;
+      }
   // dependency graph (same construction as pack_tables)
   std::vector<std::vector<int>> by_species(H.n);
   for (int k = 0; k < H.m; ++k)
@@ -771,6 +813,9 @@ const kin::JitModel& jit_model_cached(const kin_model* model, const kin_sweep_de
     if (d->axes[ax].kind == KIN_AXIS_PARAM) param_axis[d->axes[ax].index] = ax;
   for (int r = 0; r < m->host.m; ++r)
     if (m->host.rate_param[r] >= 0) key[r] = param_axis[m->host.rate_param[r]];
+  for (int ax = 0; ax < d->n_axes; ++ax)  // scale axes: 1000 + axis (distinct from parameter bindings)
+    if (d->axes[ax].kind == KIN_AXIS_SCALE)
+      for (int r = d->axes[ax].index; r < d->axes[ax].index + d->axes[ax].span; ++r) key[r] = 1000 + ax;
   std::lock_guard<std::mutex> lk(m->jit_mu);
   auto it = m->jit_cache.find(key);
   if (it != m->jit_cache.end()) return *it->second;

@@ -126,7 +126,9 @@ std::string generate_policy(const JitModel& m) {
   o << "  __device__ __forceinline__ double prop(const int j) const {\n    double aj;\n    switch (j) {\n";
   for (int j = 0; j < m.m; ++j) {
     o << "      case " << j << ": aj = ";
-    if (m.rate_axis[j] >= 0) o << "av[" << m.rate_axis[j] << " * B]";
+    if (m.rate_axis[j] >= 0 && !m.rate_scaled.empty() && m.rate_scaled[j])
+      o << "__dmul_rn(tab_rate(T, " << j << "), av[" << m.rate_axis[j] << " * B])";
+    else if (m.rate_axis[j] >= 0) o << "av[" << m.rate_axis[j] << " * B]";
     else o << "tab_rate(T, " << j << ")";
     o << ";";
     for (int p = m.rt_ptr[j]; p < m.rt_ptr[j + 1]; ++p)

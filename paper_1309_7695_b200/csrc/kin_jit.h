@@ -15,6 +15,7 @@ struct JitModel {
   int n = 0, m = 0;
   std::vector<int> rt_ptr, rt_species, rt_stoich;    // reactants per reaction (species-ascending)
   std::vector<int> rate_axis;                        // -1, or the sweep axis carrying c_j
+  std::vector<char> rate_scaled;                     // 1: c_j = rate_j * axis value (scale axis)
   std::vector<int> col_ptr, col_species, col_delta;  // nu columns
   std::vector<int> row_ptr, row_reaction, row_delta; // nu rows
   std::vector<int> dep_ptr, dep;                     // propensity dependency graph

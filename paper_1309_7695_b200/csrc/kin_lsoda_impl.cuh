@@ -50,7 +50,7 @@ __device__ __noinline__ void rhs_out_of_line(const KinTables& T, const double* a
   for (int j = 0; j < m; ++j) {
     const uint64_t d = tab_rdesc(T, j);
     const int ax = KIN_RD_AXIS(d);
-    double aj = ax < 0 ? tab_rate(T, j) : av[ax * B];
+    double aj = ax < 0 ? tab_rate(T, j) : __dmul_rn(tab_rate(T, j), av[ax * B]);
     const int nt = KIN_RD_NTERMS(d);
 #pragma unroll 1
     for (int t = 0; t < nt; ++t) aj = aj * combinations(yy[KIN_RD_SPECIES(d, t) * B], KIN_RD_STOICH(d, t));
@@ -102,7 +102,7 @@ struct Lsoda {
   __device__ __forceinline__ double& v(double* base, int i) const { return base[i * B]; }
   __device__ __forceinline__ double rate(int j) const {
     const int ax = KIN_RD_AXIS(tab_rdesc(T, j));
-    return ax < 0 ? tab_rate(T, j) : av[ax * B];
+    return ax < 0 ? tab_rate(T, j) : __dmul_rn(tab_rate(T, j), av[ax * B]);
   }
   // rre_rhs (oracle order): a_j then dx_i = sum over the nu row
   template <bool C>

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
     grpc.sync();
     for (int j = lane; j < M; j += L) {
       const int ax = s_rate_axis[j];
-      double aj = ax < 0 ? s_rate[j] : av[ax];
+      double aj = ax < 0 ? s_rate[j] : __dmul_rn(s_rate[j], av[ax]);
       const int p1 = s_rt_ptr[j + 1];
 #pragma unroll 1
       for (int p = s_rt_ptr[j]; p < p1; ++p) {

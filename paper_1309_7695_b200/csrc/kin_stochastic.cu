@@ -204,11 +204,14 @@ __global__ void __launch_bounds__(stoch::kBlock) cle_kernel(const __grid_constan
 // ---- unit seams (kin_device_unit): one path function on one state, through
 // the same device code the sweep kernels run.  One thread; the state sits in
 // shared memory with the kernels' [slot][thread] stride.
+// The unit seams run on one thread: state arrays with stride 1.
+using UnitModel = TableModel<double, 1>;
+
 // rre_rhs (deterministic.hpp:85-88, oracle rre_rhs): a(y) from the packed
 // tables, then dx_i = sum over the nu row in reaction order; y[i*ys], f[i*fs].
 // Compiled with -fmad=false (this TU): the oracle's roundings.
-__device__ void unit_rhs(const KinTables& T, const TableModel<double>& sm, const double* y, double* f, int fs) {
-  constexpr int B = kBlock;
+__device__ void unit_rhs(const KinTables& T, const UnitModel& sm, const double* y, double* f, int fs) {
+  constexpr int B = 1;
   const int N = T.n, M = T.m;
   double* x = sm.x;
   for (int i = 0; i < N; ++i) x[i * B] = y[i * B];
@@ -227,9 +230,9 @@ __device__ void unit_rhs(const KinTables& T, const TableModel<double>& sm, const
 // from y (k1 = f(y)); out = {y5[N], err, k7[N]} with err = sqrt(mean((e_i /
 // sk_i)^2)), sk_i = atol + rtol * max(|y_i|, |y5_i|) — the stage and error
 // expressions of the oracle's integrate_rre, operation for operation.
-__device__ void unit_rk_step(const KinTables& T, const TableModel<double>& sm, const double* x_in, double h,
+__device__ void unit_rk_step(const KinTables& T, const UnitModel& sm, const double* x_in, double h,
                              double rtol, double atol, double* out) {
-  constexpr int B = kBlock;
+  constexpr int B = 1;
   const int N = T.n;
   constexpr double a21 = 1.0 / 5.0;
   constexpr double a31 = 3.0 / 40.0, a32 = 9.0 / 40.0;
@@ -282,12 +285,12 @@ __global__ void __launch_bounds__(32) unit_kernel(const __grid_constant__ KinTab
                                                   const double* params, double* out) {
   extern __shared__ double smem[];
   if (threadIdx.x != 0) return;
-  constexpr int B = kBlock;
+  constexpr int B = 1;
   const int N = T.n, M = T.m;
   double* a = smem;                                        // a[j * B]
   double* x = smem + static_cast<size_t>(M) * B;           // x[i * B]
   for (int i = 0; i < N; ++i) x[i * B] = x_in[i];
-  const TableModel<double> sm{T, x, a, nullptr};
+  const UnitModel sm{T, x, a, nullptr};
   const double a0 = sm.all_props(M);
   if (kind == 0) {                                          // propensities
     for (int j = 0; j < M; ++j) out[j] = sm.aval(j);
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(32) unit_kernel(const __grid_constant__ KinTab
   } else if (kind == 5) {                                   // rre_rhs
     unit_rhs(T, sm, x, out, 1);
   } else if (kind == 6) {                                   // rk_step (one DP5(4) step)
-    unit_rk_step(T, sm, x, params[0], params[1], params[2], out);
+    unit_rk_step(T, sm, x_in, params[0], params[1], params[2], out);
   }
 }
 
@@ -360,8 +363,8 @@ cudaError_t launch_xt(const KinTables& T, const KinSweepDev& S, const KinOutDev&
 
 cudaError_t launch_unit(const KinTables& T, int kind, const double* x, const double* params, double* out,
                         cudaStream_t stream) {
-  // a[M] + x[N] (+ the rk_step stage vectors: M + 10 N more, see unit_rk_step)
-  const size_t smem = static_cast<size_t>(2 * T.m + 11 * T.n) * kBlock * sizeof(double);
+  // a[M] + x[N] (+ the rk_step stage vectors: M + 10 N more, see unit_rk_step), stride 1
+  const size_t smem = static_cast<size_t>(2 * T.m + 11 * T.n) * sizeof(double);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   cudaError_t e = cudaFuncSetAttribute(unit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;

@@ -82,7 +82,7 @@ __device__ void simulate_group(const KinTables& T, const KinSweepDev& S, const K
   auto prop = [&](int j) -> double {
     const uint64_t d = tab_rdesc(T, j);
     const int ax = KIN_RD_AXIS(d);
-    double aj = ax < 0 ? tab_rate(T, j) : av[ax];
+    double aj = ax < 0 ? tab_rate(T, j) : __dmul_rn(tab_rate(T, j), av[ax]);
     const int nt = KIN_RD_NTERMS(d);
     if (nt > 0) {
       aj = __dmul_rn(aj, combinations(x[KIN_RD_SPECIES(d, 0)], KIN_RD_STOICH(d, 0)));

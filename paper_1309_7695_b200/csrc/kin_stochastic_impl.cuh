@@ -71,7 +71,7 @@ struct TableModel {
   __device__ __forceinline__ double prop(int j) const {
     const uint64_t d = tab_rdesc(T, j);
     const int ax = KIN_RD_AXIS(d);
-    double aj = ax < 0 ? tab_rate(T, j) : av[ax * B];
+    double aj = ax < 0 ? tab_rate(T, j) : __dmul_rn(tab_rate(T, j), av[ax * B]);
     const int nt = KIN_RD_NTERMS(d);
     if (nt > 0) {
       aj = __dmul_rn(aj, combinations(xv(KIN_RD_SPECIES(d, 0)), KIN_RD_STOICH(d, 0)));

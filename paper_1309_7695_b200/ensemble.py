@@ -76,10 +76,13 @@ class Method:
 class SweepAxis:
     """ensemble.hpp:101-104.  ``param`` names a Parameter (reference semantics,
     with_param) or, with ``kind="initial"``, a species whose initial amount is
-    swept (north-star extension)."""
+    swept (north-star extension), or, with ``kind="scale"``, labels a global
+    scale factor multiplying the rate constants of reactions
+    ``reactions[0] .. reactions[1]-1`` (extension)."""
     param: str
     values: Sequence[float]
     kind: str = "param"
+    reactions: tuple = (0, 0)
 
 
 @dataclass
@@ -191,9 +194,13 @@ def make_sweep_desc(network: ReactionNetwork, config: SweepConfig, *, seed_mode:
             if idx is None:
                 raise ValidationError(f"sweep axis: unknown species '{ax.param}'")
             kind = abi.AXIS_INITIAL
+        elif ax.kind == "scale":
+            idx = int(ax.reactions[0])
+            kind = abi.AXIS_SCALE
         else:
             raise ValidationError(f"sweep axis kind '{ax.kind}'")
-        axes[i] = abi.KinSweepAxis(kind, idx, len(vals), abi.ptr(vals, C.c_double))
+        span = int(ax.reactions[1]) - int(ax.reactions[0]) if ax.kind == "scale" else 0
+        axes[i] = abi.KinSweepAxis(kind, idx, len(vals), abi.ptr(vals, C.c_double), span)
     grid = np.ascontiguousarray(config.grid, dtype=np.float64)
     keep += [axes, grid]
     s0, s1 = sim_range if sim_range else (0, 0)

@@ -237,15 +237,19 @@ def random_network(seed=0xC5C5, n=128, m_extra=128):
             rate *= 1e-3
         params.append((f"k{k}", rate))
         reactions.append((f"r{k}", lhs, rhs, f"k{k}"))
-    params += [("scale_a", 1.0), ("scale_b", 1.0)]
     return _net(species, params, reactions)
 
 
 def c5_config(side=512, n_grid=11, method: MethodKind = MethodKind.TauAdaptive):
+    """two global scale factors on a side x side log grid
+    (x0.1 .. x10): scale_a multiplies every degradation rate (reactions
+    0..127), scale_b every other rate (reactions 128..255) — together, all
+    rates (KIN_AXIS_SCALE)."""
     net = random_network()
-    # two global scale factors: swept as the rate of two representative reactions
-    cfg = SweepConfig(axes=[SweepAxis("k0", logspace_around(net.params()[net.param_index("k0")].value, side)),
-                            SweepAxis("k1", logspace_around(net.params()[net.param_index("k1")].value, side))],
+    n = net.species_count()
+    m = net.reaction_count()
+    cfg = SweepConfig(axes=[SweepAxis("scale_a", logspace_around(1.0, side), "scale", (0, n)),
+                            SweepAxis("scale_b", logspace_around(1.0, side), "scale", (n, m))],
                       runs_per_point=1, method=Method(method, epsilon=0.03), master_seed=MASTER_SEED,
                       t_end=20.0, grid=uniform_grid(20.0, n_grid))
     return net, cfg
