@@ -1261,6 +1261,7 @@ int integrate_lsoda(const Network& net, const double* rates, const double* x0, c
       // ---- accepted ----
       ++nst;
       ++meta[0];
+      if (meth == 1) ++meta[3];  // accepted BDF steps (the stiff share; TrajectoryMeta slot 3)
       for (int j = 0; j <= nq; ++j) {
         double* zj = Zr(j);
         const double e = el[j];

@@ -273,7 +273,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   const double hmax = S.h_max > 0.0 ? S.h_max : __builtin_huge_val();
   const double t_end = S.t_end;
   bool floored = false;
-  uint64_t n_acc = 0, n_rej = 0;
+  uint64_t n_acc = 0, n_rej = 0, n_bdf = 0;  // n_bdf: accepted BDF steps (meta[3])
   int status = 0;
 
   auto emit = [&](int g, const double* vv) {
@@ -475,6 +475,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
         // accepted
         ++nst;
         ++n_acc;
+        if (meth == 1) ++n_bdf;
 #pragma unroll 1
         for (int j = 0; j <= nq; ++j) {
           const double e = L.elco(meth, nq, j);
@@ -588,7 +589,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   me[0] = n_acc;
   me[1] = n_rej;
   me[2] = 0;
-  me[3] = 0;
+  me[3] = n_bdf;
   me[4] = 0;
   me[5] = floored ? 1 : 0;
   O.status[s] = status;

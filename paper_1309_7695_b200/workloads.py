@@ -114,13 +114,26 @@ def brusselator(omega=1000.0, A=1.0, B=3.0, stiff=1.0):
                  ("outflow", {"X": 1}, {"E": 1}, "kE")], max_order=3)
 
 
-def c3_config(side=256, method: MethodKind = MethodKind.Lsoda, omega=1000.0, stiff=1.0):
-    net = brusselator(omega, stiff=stiff)
+def c3_config(side=256, method: MethodKind = MethodKind.Lsoda, omega=1000.0, stiff=1.0, A=1.0, B=3.0):
+    net = brusselator(omega, A=A, B=B, stiff=stiff)
     vals = [float(round(v)) for v in np.linspace(0.0, 5.0 * omega, side)]
     cfg = SweepConfig(axes=[SweepAxis("X", vals, "initial"), SweepAxis("Y", vals, "initial")], runs_per_point=1,
                       method=Method(method, integrator=IntegratorConfig(rel_tol=1e-6, abs_tol=1e-9 * omega)),
                       master_seed=MASTER_SEED, t_end=20.0, grid=uniform_grid(20.0, 201))
     return net, cfg
+
+
+def c3_stiff_config(side=256, method: MethodKind = MethodKind.Lsoda):
+    """Stiff Brusselator (SURVEY §8d C3 second variant, BASELINE configs[2]):
+    autocatalysis and conversion x1000 with A = 2, B = 3 (B < 1 + A^2: a stable
+    focus at X = 2 Omega, Y = 1.5 Omega, so X stays >> 1 molecule).  The
+    Jacobian's eigenvalues there are about -4 and -1000: a stiffness ratio of
+    ~250, where an explicit integrator is held to h ~ 3e-3 by stability and
+    BDF takes steps set by the slow mode.  Omega = 1e6 keeps X >> 1 molecule on
+    every path from the swept initial states (at Omega = 1e3 a start with
+    little Y lets conversion drain X below one molecule, where the clamped
+    combinatorial factor X(X-1)/2 switches the autocatalysis off for good)."""
+    return c3_config(side=side, method=method, omega=1e6, stiff=1000.0, A=2.0, B=3.0)
 
 
 # ---- C4 Ras/cAMP/PKA-scale synthetic (33 species, 39 reactions) -------------
