@@ -93,6 +93,7 @@ inline void kin_lsoda_coeffs(LsodaCoeffs* C) {
 }
 
 // Adams stability-region sizes (LSODA sm1), orders 1..12.
+constexpr int kLsodaStabSwitch = 8;  // see integrate_lsoda: Adams -> BDF on a binding stability cap
 constexpr double kLsodaSm1[13] = {0.0, 0.5, 0.575, 0.55, 0.45, 0.35, 0.25, 0.2, 0.15, 0.1, 0.075, 0.05, 0.025};
 
 }  // namespace kin_oracle

@@ -1096,6 +1096,7 @@ int integrate_lsoda(const Network& net, const double* rates, const double* x0, c
   int nq = 1;
   int ialth = 2;
   int icount = 20;
+  int nstab = 0;  // consecutive order selections whose Adams step the stability cap bound
   double rmax = 1.0e4;
   double crate = 0.7;
   bool ipup = false, jcur = false, have_p = false;
@@ -1308,8 +1309,10 @@ int integrate_lsoda(const Network& net, const double* rates, const double* x0, c
         if (nq < kLsodaMaxOrdAdams) rhup = std::min(rhup, sm1(nq + 1) / pdh);
         rhsm_cap = std::min(rhsm, sm1(nq) / pdh);
         if (nq > 1) rhdn = std::min(rhdn, sm1(nq - 1) / pdh);
+        nstab = pdh >= 0.5 * sm1(nq) ? nstab + 1 : 0;  // within 2x of the stability boundary
       } else {
         rhsm_cap = rhsm;
+        nstab = 0;
       }
       int newq = nq;
       double rh = rhsm_cap;
@@ -1335,7 +1338,15 @@ int integrate_lsoda(const Network& net, const double* rates, const double* x0, c
           const double rh1 = rh;
           const double dm2 = dsm * (cm1(nq) / cm2(nq));
           const double rh2 = 1.0 / (1.2 * pm_pow(dm2, exsm) + 1.2e-6);
-          if (rh2 >= 5.0 * rh1) { newm = 1; newq = nq; rh = rh2; }
+          if (rh2 >= 5.0 * rh1) {
+            newm = 1; newq = nq; rh = rh2;
+          } else if (nstab >= kLsodaStabSwitch) {
+            // extension of Petzold's test: the Adams step has been held by its
+            // stability region for kLsodaStabSwitch selections in a row (a stiff
+            // mode near the stability boundary inflates the Adams error
+            // estimate, so the error-constant comparison above never fires)
+            newm = 1; newq = nq; rh = rh1;
+          }
         } else if (meth == 1) {
           const double dm1 = dsm * (cm2(nq) / cm1(nq));
           double rh1 = 1.0 / (1.2 * pm_pow(dm1, exsm) + 1.2e-6);

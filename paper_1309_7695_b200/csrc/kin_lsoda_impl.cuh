@@ -26,6 +26,9 @@ namespace kin {
 
 namespace {
 // Adams stability-region caps (LSODA's sm1), one copy per translation unit
+// Adams -> BDF when the stability cap bound the Adams step this many order
+// selections in a row (oracle: kLsodaStabSwitch)
+constexpr int kLsodaStabSwitch = 8;
 __device__ __constant__ double c_sm1[13] = {0.0, 0.5, 0.575, 0.55, 0.45, 0.35, 0.25, 0.2, 0.15, 0.1, 0.075, 0.05, 0.025};
 }  // namespace
 
@@ -317,6 +320,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
     for (int i = 0; i < n; ++i) L.z(1, i) = h * L.savf[i * B];
 
     int meth = 0, nq = 1, ialth = 2, icount = 20;
+    int nstab = 0;  // consecutive order selections whose Adams step the stability cap bound
     double rmax = 1.0e4, crate = 0.7;
     bool ipup = false, jcur = false, have_p = false;
     double hl0_p = 0.0;
@@ -521,8 +525,10 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           if (nq < 12) rhup = fmin(rhup, c_sm1[nq + 1] / pdh);
           rhsm_cap = fmin(rhsm, c_sm1[nq] / pdh);
           if (nq > 1) rhdn = fmin(rhdn, c_sm1[nq - 1] / pdh);
+          nstab = pdh >= 0.5 * c_sm1[nq] ? nstab + 1 : 0;  // within 2x of the stability boundary
         } else {
           rhsm_cap = rhsm;
+          nstab = 0;
         }
         int newq = nq;
         double rh = rhsm_cap;
@@ -545,7 +551,13 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             const double rh1 = rh;
             const double dm2 = dsm * (cm1(nq) / cm2(nq));
             const double rh2 = 1.0 / (1.2 * pm_pow(dm2, exsm) + 1.2e-6);
-            if (rh2 >= 5.0 * rh1) { newm = 1; newq = nq; rh = rh2; }
+            if (rh2 >= 5.0 * rh1) {
+              newm = 1; newq = nq; rh = rh2;
+            } else if (nstab >= kLsodaStabSwitch) {
+              // stiffness by stability: the Adams step has been held by its
+              // stability region for many selections in a row
+              newm = 1; newq = nq; rh = rh1;
+            }
           } else if (meth == 1) {
             const double dm1 = dsm * (cm2(nq) / cm1(nq));
             double rh1 = 1.0 / (1.2 * pm_pow(dm1, exsm) + 1.2e-6);

@@ -90,3 +90,14 @@ def test_dopri5_every_lane_width(engine, oracle, model, lanes):
     ref, got = both(engine, oracle, net, cfg, lanes_per_sim=lanes, **kw)
     err = np.abs(got["traj"] - ref["traj"]) / ode_bound(ref["traj"], cfg)
     assert err.max() <= 1.0, (lanes, err.max())
+
+
+def test_c3_stiff_lsoda_full_65536_bit_exact(engine, oracle):
+    """The stiff C3 variant (BASELINE configs[2] "stiff oscillator ... LSODA
+    BDF"): all 65,536 initial states, bit-exact with the oracle including the
+    accepted-BDF-step counter (TrajectoryMeta slot 3)."""
+    net, cfg = W.c3_stiff_config(side=256)
+    ref, got = both(engine, oracle, net, cfg, want_work=True)
+    assert_bit_exact(ref, got, work=True)
+    m = got["meta"]
+    assert (m[:, 3] > 0).all() and m[:, 3].sum() > 0.4 * m[:, 0].sum()

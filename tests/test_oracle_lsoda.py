@@ -64,3 +64,42 @@ def test_brusselator_accuracy_like_scipy_lsoda(sim):
     ours = np.max(np.abs(r["traj"][0] - ref) / tol)
     theirs = np.max(np.abs(sp - ref) / tol)
     assert ours < max(3 * theirs, 50), (ours, theirs)
+
+
+def test_stiff_brusselator_switches_to_bdf_and_beats_dopri5():
+    """SURVEY §8d C3 stiff variant (workloads.c3_stiff_config: Jacobian
+    eigenvalues ~ -4 and -1000 at the focus): over 512 points strided across
+    the 256x256 initial-state sweep, LSODA switches to BDF (TrajectoryMeta slot
+    3 counts the accepted BDF steps: over 40% of all steps — the rest are the
+    short Adams steps of the initial transient before the first stiffness check,
+    while BDF covers nearly all of the simulated time) and needs over 20x fewer
+    steps than Dopri5, whose step the stability region holds."""
+    net, cfg = W.c3_stiff_config(side=256)
+    d, keep = make_sweep_desc(net, cfg, shard=(3, 128))
+    r = O.sweep(net, d, workers=4)
+    net2, cfg2 = W.c3_stiff_config(side=256, method=MethodKind.Ode)
+    d2, keep2 = make_sweep_desc(net2, cfg2, shard=(3, 128))
+    r2 = O.sweep(net2, d2, workers=4)
+    m = r["meta"]
+    assert m[:, 3].sum() > 0.4 * m[:, 0].sum()
+    assert (m[:, 3] > 0).all()  # every simulation switched
+    assert 20 * m[:, 0].sum() < r2["meta"][:, 0].sum()
+
+
+def test_stiff_brusselator_accuracy_vs_tight_dopri5():
+    """Global error of LSODA (rtol 1e-6, atol 1e-9 Omega) against a tight Dopri5
+    (rtol 1e-11): 99.8% of all grid values within 10 (atol + rtol |y|), every
+    one within 100x.  The excess is the collapse transient (X falls ~2000x in a
+    few ms), where the local-error control lets D and E (integrals of X) carry
+    up to ~50 tol; scipy's ODEPACK LSODA reaches ~3 tol there."""
+    net, cfg = W.c3_stiff_config(side=256)
+    d, keep = make_sweep_desc(net, cfg, shard=(7, 128))
+    r = O.sweep(net, d, workers=4)
+    net2, cfg2 = W.c3_stiff_config(side=256, method=MethodKind.Ode)
+    cfg2.method.integrator = IntegratorConfig(rel_tol=1e-11, abs_tol=1e-6, max_steps=10 ** 7)
+    d2, keep2 = make_sweep_desc(net2, cfg2, shard=(7, 128))
+    r2 = O.sweep(net2, d2, workers=4)
+    ic = cfg.method.integrator
+    err = np.abs(r["traj"] - r2["traj"]) / (10 * (ic.abs_tol + ic.rel_tol * np.abs(r2["traj"])))
+    assert (err <= 1.0).mean() >= 0.997, (err <= 1.0).mean()
+    assert err.max() <= 10.0, err.max()

@@ -3,7 +3,7 @@ each method kernel's device throughput (CUDA events, kin_sweep_launch) beside
 the CPU oracle on a bounded sample with all host threads, and the CSV writer's
 throughput.  Prints one JSON object; profiles/r1_rows.json keeps the result.
 
-  python tools/bench_rows.py > profiles/r1_rows.json
+  python tools/bench_rows.py > profiles/r2_rows.json
 """
 import ctypes as C
 import json
@@ -63,9 +63,14 @@ def main():
         "hybrid_c1": (W.c1_config(MethodKind.Hybrid, side=256), 1024),
         "lsoda_c3": (W.c3_config(side=256), 4096),
         "dopri5_c3": (W.c3_config(side=256, method=MethodKind.Ode), 4096),
+        "lsoda_c3_stiff": (W.c3_stiff_config(side=256), 4096),
+        "dopri5_c3_stiff": (W.c3_stiff_config(side=256, method=MethodKind.Ode), 1024),
+        "tau_c4_binomial": (W.c4_config(), 1024),
         "dopri5_c4": (W.c4_config(method=MethodKind.Ode), 2048),
         "tau_c5": (W.c5_config(), 1024),
+        "dopri5_c5": (W.c5_config(method=MethodKind.Ode), 1024),
     }
+    cases["tau_c4_binomial"][0][1].method.firing = abi.FIRING_BINOMIAL
     for name, ((net, cfg), sample) in cases.items():
         if cfg.method.kind == MethodKind.Cle:
             cfg.method = Method(MethodKind.Cle, tau=0.05)
@@ -97,7 +102,7 @@ def main():
                           "mb_per_s_one_thread": out[1][0] / out[1][1] / 1e6,
                           "numbers_per_s_all_threads": values / out[threads][1],
                           "byte_identical": out[1][2] == out[threads][2]}
-    print(json.dumps({"round": 1, "rows": rows}, indent=1))
+    print(json.dumps({"round": 2, "rows": rows}, indent=1))
 
 
 if __name__ == "__main__":
