@@ -33,6 +33,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/kin_abi.h"
 #include "kin_device.cuh"
 #include "kin_jit.h"
@@ -40,6 +42,17 @@
 #include "kin_tables.h"
 
 namespace {
+
+// NVTX ranges (SURVEY §5 tracing): host-side phases of a call — the sweep
+// table upload, each device's simulation + statistics launches, the copy-out
+// enqueue and the wait — visible in Nsight Systems / ncu --nvtx.  Header-only
+// NVTX v3: a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 void set_err(kin_error* e, int code, const std::string& msg) {
   if (!e) return;
@@ -849,6 +862,7 @@ int launch_stats(Slot& sl, Buffers& bf, kin_error* err) {
 // studies and tests only — the process's environment overrides.
 int launch_sim(Slot& sl, Buffers& bf, const kin_model* model, const kin_sweep_desc* d, KinTables& T,
                KinSweepDev& SD, const KinOutDev& O, bool want_work, bool allow_int_state, kin_error* err) {
+  NvtxRange nv("kin: simulation kernel launch");
   const HostModel& H = model->host;
   const EnvOverrides& ov = env_overrides();
   const uint32_t var = d->variant;
@@ -981,6 +995,7 @@ constexpr size_t kStatsOnlyBudget = size_t{1} << 28;  // 2 GiB
 // Launch one part of a call on a slot (device-resident results in bf).
 int launch_range(Slot& sl, Buffers& bf, const kin_model* model, const kin_sweep_desc* d, const Layout& L,
                  const PlanPart& part, bool want_stats, bool want_work, kin_error* err, bool want_partials = false) {
+  NvtxRange nv("kin: launch part (tables + H2D + kernels)");
   const HostModel& H = model->host;
   if (!bf.st) bf.st = sl.stream;
   KIN_CUDA(cudaSetDevice(sl.device), "cudaSetDevice");
@@ -1205,6 +1220,7 @@ int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
 // in flight (the caller orders it after the launch); otherwise synchronous on
 // the compute stream.
 int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_point, bool sync, kin_error* err) {
+  NvtxRange nv("kin: copy-out (D2H into the caller layout)");
   cudaStream_t st = sync ? bf.st : sl.copy_stream;
   const uint64_t S = bf.s1 - bf.s0;
   const size_t gn = static_cast<size_t>(bf.G) * bf.N;
@@ -1487,6 +1503,7 @@ int kin_sweep_run(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* de
 int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc* desc, kin_sweep_out* out,
                      uint64_t* ticket, kin_error* err) {
   if (!ctx || !ticket) { set_err(err, KIN_ERR_USAGE, "null argument"); return KIN_ERR_USAGE; }
+  NvtxRange nv("kin_sweep_submit");
   auto job = std::make_unique<Job>();
   uint64_t s0, s1;
   if (int rc = prepare(model, desc, &job->L, &s0, &s1, err)) return rc;
@@ -1608,6 +1625,7 @@ int kin_run_single(kin_ctx* ctx, const kin_model* model, const kin_method* metho
 
 int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
   if (err) std::memset(err, 0, sizeof(*err));
+  NvtxRange nv("kin_sweep_wait");
   std::unique_ptr<Job> job;
   if (!ctx) { set_err(err, KIN_ERR_USAGE, "null context"); return KIN_ERR_USAGE; }
   {
