@@ -245,7 +245,11 @@ int load_model(const kin_model_desc* d, HostModel* H, std::string* msg) {
     for (int s = 0; s < n; ++s) {
       const int dl = nu[static_cast<size_t>(s) * m + j];
       if (dl == 0) continue;
-      if (dl < -128 || dl > 127) { *msg = "reaction " + std::to_string(j) + ": net stoichiometry out of range"; return KIN_ERR_INPUT; }
+      if (dl < -128 || dl > 127) {
+        *msg = "reaction " + std::to_string(j) + ": net stoichiometry " + std::to_string(dl) +
+               " out of range (the device tables hold net changes in [-128, 127])";
+        return KIN_ERR_INPUT;
+      }
       M.col_species.push_back(s);
       M.col_delta.push_back(dl);
     }
@@ -425,7 +429,7 @@ int pack_tables(const HostModel& H, const kin_sweep_desc* d, KinTables* T, std::
   for (size_t p = 0; p < row.size(); ++p)
     row[p] = static_cast<uint32_t>(H.row_reaction[p]) | (static_cast<uint32_t>(H.row_delta[p] + 128) << 16);
   for (size_t p = 0; p < H.rt_stoich.size(); ++p)
-    if (H.rt_stoich[p] > 255) { *msg = "stoichiometry out of range"; return KIN_ERR_INPUT; }
+    if (H.rt_stoich[p] > 255) { *msg = "reactant stoichiometry above 255 is not supported by the device tables"; return KIN_ERR_INPUT; }
   T->off_rate = put(rate.data(), rate.size() * 8, 8);
   T->off_x0 = put(H.x0.data(), H.x0.size() * 8, 8);
   T->off_g = put(gd.data(), gd.size() * 8, 8);

@@ -401,6 +401,12 @@ std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool p
 
 }  // namespace
 
+// doubles of one block's global-state region that the kernel touches: a[M] +
+// av[axes] per lane (+ x[N] when the amounts are not in shared memory)
+size_t gstate_live_doubles(const KinTables& T, const KinSweepDev& S, bool x_in_smem) {
+  return static_cast<size_t>(T.m + S.n_axes) * KIN_STOCH_BLOCK + (x_in_smem ? 0 : static_cast<size_t>(T.n) * KIN_STOCH_BLOCK);
+}
+
 bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log) {
   std::vector<char> cubin;
   return nvrtc_compile(generate_policy(model), count, philox, int_state, false, false, 0, &cubin, log);
@@ -480,7 +486,36 @@ cudaError_t launch_stochastic_jit(const JitModel& model, const KinTables& T, con
   KinSweepDev* Sp = &SW;
   KinOutDev Oc = O;
   void* args[] = {Tp, Sp, &Oc, &counter, &ovf_flag};
+  // Global-memory state: the live part (the resident blocks' regions) is
+  // rewritten every leap; ask L2 to keep it (persisting access-policy window
+  // over exactly those bytes) instead of writing it back to HBM.
+  bool window = false;
+  if (global_state && jit_knob("KIN_JIT_L2_PERSIST", 1) != 0) {
+    const size_t live = static_cast<size_t>(grid) *
+                        (smem_x ? gstate_live_doubles(T, S, true) : gstate_live_doubles(T, S, false)) * sizeof(double);
+    int max_persist = 0, max_window = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    if (max_persist > 0 && max_window > 0 && live > 0) {
+      const size_t bytes = std::min<size_t>(live, static_cast<size_t>(max_window));
+      cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(bytes, static_cast<size_t>(max_persist)));
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.base_ptr = S.gstate;
+      v.accessPolicyWindow.num_bytes = bytes;
+      v.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(max_persist) / bytes));
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      window = cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v) == cudaSuccess;
+      cudaGetLastError();
+    }
+  }
   e = cudaLaunchKernel(fn, dim3(grid), dim3(KIN_STOCH_BLOCK), args, smem, stream);
+  if (window) {  // later work on this stream (statistics, copies) streams normally
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.num_bytes = 0;
+    cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaGetLastError();
+  }
   if (e == cudaSuccess) *used = true;
   return e;
 }
