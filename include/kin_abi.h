@@ -237,7 +237,12 @@ void kin_stats_merge(uint64_t* n_a, double* mean_a, double* m2_a, uint64_t n_b, 
 /* Number of CUDA devices visible to this process (0 without a GPU). */
 int32_t kin_visible_devices(void);
 
-/* One host thread per device; device_ids NULL/n=0 → device 0. */
+/* A context over the listed devices (device_ids NULL/n=0 → device 0; the same
+   id may repeat: several slots on one GPU).  Every launch is asynchronous, so
+   the calling thread enqueues all devices' work (kernels on per-device
+   streams, copy-out on a copy stream) and returns; kin_sweep_wait collects.
+   Calls on one context are serialised per device slot (internal locks);
+   separate contexts are independent. */
 int kin_ctx_create(const int32_t* device_ids, int32_t n_devices, kin_ctx** out,
                    kin_error* err);
 void kin_ctx_destroy(kin_ctx* ctx);
