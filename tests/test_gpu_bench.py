@@ -45,3 +45,18 @@ def test_reference_arm_line():
     assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["e2e"]["d2h_bytes_per_step"] == 0
     cb = j["cpu_baseline"]
     assert cb["kind"] in ("port", "reference") and cb["cores"] >= 1 and cb["value"] == j["value"]
+
+
+def test_bench_refuses_more_gpus_than_visible():
+    """`--gpus N` without torchrun drives N devices in one process and fails
+    loudly when fewer are visible (never a silent one-GPU run)."""
+    import torch
+    n = torch.cuda.device_count() + 1
+    r = subprocess.run([sys.executable, str(REPO / "bench.py"), "--gpus", str(n), "--steps", "3", "--warmup", "3",
+                        "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=REPO)
+    assert r.returncode != 0 and f"needs {n} visible GPUs" in (r.stderr + r.stdout)
+
+
+def test_bench_strong_scaling_line():
+    j = run_bench("--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--scaling", "strong")
+    assert j["scaling"] == "strong" and j["config"]["sweep_points"] == 65536 and j["value"] > 0
