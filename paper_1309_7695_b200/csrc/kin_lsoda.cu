@@ -15,6 +15,9 @@ size_t lsoda_state_doubles_per_warp(const KinTables& T, const KinSweepDev& S) { 
 
 size_t lsoda_smem_bytes(const KinTables& T, const KinSweepDev& S) {
   const int n = T.n;
+  // N <= 4: the iteration matrix, its LU factors and pivots are in registers
+  if (lsd::kLsodaRegLU && n >= 1 && n <= 4)
+    return static_cast<size_t>(18 * n + T.m + S.n_axes) * lsd::kBlock * sizeof(double);
   return static_cast<size_t>(18 * n + n * n + T.m + S.n_axes) * lsd::kBlock * sizeof(double) +
          static_cast<size_t>(n) * lsd::kBlock * sizeof(int);
 }

@@ -37,6 +37,13 @@ namespace lsd {
 using pmath::pm_pow;
 
 constexpr int kBlock = 32;
+// N <= 4: keep the iteration matrix P = I - h l0 J and its LU factors in
+// registers (fully unrolled, constant indices) instead of shared memory.
+// Implemented and bit-exact (tests/test_gpu_*.py ran green with it on), but
+// measured slower on the B200: C3 31.8 -> 35.5 ms, stiff C3 15.0 -> 16.1 ms
+// (167 registers against 126; the unrolled factorisation with predicated row
+// swaps costs more than the shared-memory version saves), so it is off.
+constexpr bool kLsodaRegLU = false;
 constexpr int kL = 13;  // Nordsieck vectors (Adams max order 12)
 
 
@@ -91,11 +98,15 @@ struct Lsoda {
   const double* co;  // elco [2][13][14] then tesco [2][13][3]
   int n_rt, m;
   static constexpr int B = kBlock;
+  // the register-resident P/LU variant (kLsodaRegLU above)
+  static constexpr bool kRegLU = kLsodaRegLU && kN >= 1 && kN <= 4;
   __device__ __forceinline__ int N() const { return kN > 0 ? kN : n_rt; }
   double *Z, *acor, *savf, *ewt, *y, *tmp, *P, *a, *av;
   int* piv;
   uint64_t flops;
   uint64_t F_rhs;
+  double pr[kRegLU ? kN * kN : 1];
+  int pv[kRegLU ? kN : 1];
 
   __device__ __forceinline__ double elco(int meth, int q, int i) const { return __ldg(co + (meth * 13 + q) * 14 + i); }
   __device__ __forceinline__ double tesco(int meth, int q, int i) const {
@@ -146,36 +157,119 @@ struct Lsoda {
   // max_i (sum_j |J_ij| ewt_j) / ewt_i without storing J: row i is formed in
   // tmp by walking row i of nu (reactions ascending), so each J_ij receives the
   // oracle's contributions (rre_jacobian: reactions ascending) in its order.
+  // row i of J = nu * da/dx into tmp[s*B], walking row i of nu (reactions
+  // ascending): each J_is receives the oracle's contributions (rre_jacobian:
+  // reactions ascending) in its order
+  __device__ __forceinline__ void jac_row(const double* yy, int i) {
+    for (int s = 0; s < N(); ++s) tmp[s * B] = 0.0;
+    const int p1 = tab_row_ptr(T, i + 1);
+#pragma unroll 1
+    for (int prw = tab_row_ptr(T, i); prw < p1; ++prw) {
+      const uint32_t e = tab_row(T, prw);
+      const int k = KIN_NU_INDEX(e);
+      const double dl = static_cast<double>(KIN_NU_DELTA(e));
+      const uint64_t d = tab_rdesc(T, k);
+      const int nt = KIN_RD_NTERMS(d);
+      const double rk = rate(k);
+#pragma unroll 1
+      for (int p = 0; p < nt; ++p) {
+        const int s = KIN_RD_SPECIES(d, p), st = KIN_RD_STOICH(d, p);
+        const double xs = yy[s * B];
+        const double h = combinations(xs, st);
+        double dh;
+        if (st == 1) dh = xs < 0.0 ? 0.0 : 1.0;
+        else if (st == 2) dh = h > 0.0 ? xs - 0.5 : 0.0;
+        else dh = h > 0.0 ? ((3.0 * xs - 6.0) * xs + 2.0) / 6.0 : 0.0;
+        double dd = rk * dh;
+        for (int q = 0; q < nt; ++q)
+          if (q != p) dd = dd * combinations(yy[KIN_RD_SPECIES(d, q) * B], KIN_RD_STOICH(d, q));
+        tmp[s * B] = tmp[s * B] + dl * dd;
+      }
+    }
+  }
+  // the oracle's rre_jacobian flop count
+  __device__ __forceinline__ uint64_t jac_flops() const {
+    uint64_t f = 0;
+#pragma unroll 1
+    for (int k = 0; k < m; ++k) {
+      const int nt = KIN_RD_NTERMS(tab_rdesc(T, k));
+      f += static_cast<uint64_t>(nt) * (4 + nt + 2 * static_cast<uint64_t>(tab_col_ptr(T, k + 1) - tab_col_ptr(T, k)));
+    }
+    return f;
+  }
+  // kRegLU: P = I - hl0 J built row by row into registers, then factored there
+  template <bool C>
+  __device__ __forceinline__ bool form_lu_reg(const double* yy, double hl0) {
+#pragma unroll
+    for (int i = 0; i < (kRegLU ? kN : 0); ++i) {
+      jac_row(yy, i);
+#pragma unroll
+      for (int s = 0; s < (kRegLU ? kN : 0); ++s) pr[i * kN + s] = -hl0 * tmp[s * B];
+    }
+    if (C) flops += jac_flops();
+#pragma unroll
+    for (int i = 0; i < (kRegLU ? kN : 0); ++i) pr[i * kN + i] = pr[i * kN + i] + 1.0;
+#pragma unroll
+    for (int k = 0; k < (kRegLU ? kN : 0); ++k) {
+      int prow = k;
+      double best = fabs(pr[k * kN + k]);
+#pragma unroll
+      for (int i = k + 1; i < kN; ++i) {
+        const double c = fabs(pr[i * kN + k]);
+        if (c > best) { best = c; prow = i; }
+      }
+      pv[k] = prow;
+      if (best == 0.0) return false;
+#pragma unroll
+      for (int i = k + 1; i < kN; ++i)
+        if (prow == i) {
+#pragma unroll
+          for (int j = 0; j < kN; ++j) {
+            const double t0 = pr[k * kN + j];
+            pr[k * kN + j] = pr[i * kN + j];
+            pr[i * kN + j] = t0;
+          }
+        }
+      const double inv = 1.0 / pr[k * kN + k];
+#pragma unroll
+      for (int i = k + 1; i < kN; ++i) {
+        const double l = pr[i * kN + k] * inv;
+        pr[i * kN + k] = l;
+#pragma unroll
+        for (int j = k + 1; j < kN; ++j) pr[i * kN + j] = pr[i * kN + j] - l * pr[k * kN + j];
+      }
+    }
+    if (C) flops += static_cast<uint64_t>(2 * kN * kN * kN / 3 + kN);
+    return true;
+  }
+  template <bool C>
+  __device__ __forceinline__ void lu_solve_reg(double* b) {
+#pragma unroll
+    for (int k = 0; k < (kRegLU ? kN : 0); ++k) {
+      const int pk = pv[k];
+      if (pk != k) {
+        const double t0 = b[k * B];
+        b[k * B] = b[pk * B];
+        b[pk * B] = t0;
+      }
+#pragma unroll
+      for (int i = k + 1; i < kN; ++i) b[i * B] = b[i * B] - pr[i * kN + k] * b[k * B];
+    }
+#pragma unroll
+    for (int i = (kRegLU ? kN : 0) - 1; i >= 0; --i) {
+      double s = b[i * B];
+#pragma unroll
+      for (int j = i + 1; j < kN; ++j) s = s - pr[i * kN + j] * b[j * B];
+      b[i * B] = s / pr[i * kN + i];
+    }
+    if (C) flops += static_cast<uint64_t>(2 * kN * kN);
+  }
   template <bool C>
   __device__ double jac_norm_rows(const double* yy) {
     double nm = 0.0;
 #pragma unroll 1
     for (int i = 0; i < N(); ++i) {
-      for (int s = 0; s < N(); ++s) tmp[s * B] = 0.0;
-      const int p1 = tab_row_ptr(T, i + 1);
-#pragma unroll 1
-      for (int pr = tab_row_ptr(T, i); pr < p1; ++pr) {
-        const uint32_t e = tab_row(T, pr);
-        const int k = KIN_NU_INDEX(e);
-        const double dl = static_cast<double>(KIN_NU_DELTA(e));
-        const uint64_t d = tab_rdesc(T, k);
-        const int nt = KIN_RD_NTERMS(d);
-        const double rk = rate(k);
-#pragma unroll 1
-        for (int p = 0; p < nt; ++p) {
-          const int s = KIN_RD_SPECIES(d, p), st = KIN_RD_STOICH(d, p);
-          const double xs = yy[s * B];
-          const double h = combinations(xs, st);
-          double dh;
-          if (st == 1) dh = xs < 0.0 ? 0.0 : 1.0;
-          else if (st == 2) dh = h > 0.0 ? xs - 0.5 : 0.0;
-          else dh = h > 0.0 ? ((3.0 * xs - 6.0) * xs + 2.0) / 6.0 : 0.0;
-          double dd = rk * dh;
-          for (int q = 0; q < nt; ++q)
-            if (q != p) dd = dd * combinations(yy[KIN_RD_SPECIES(d, q) * B], KIN_RD_STOICH(d, q));
-          tmp[s * B] = tmp[s * B] + dl * dd;
-        }
-      }
+      jac_row(yy, i);
       double sr = 0.0;
       for (int j = 0; j < N(); ++j) sr = sr + fabs(tmp[j * B]) * ewt[j * B];
       nm = fmax(nm, sr / ewt[i * B]);
@@ -262,8 +356,10 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   p += n * B;
   L.tmp = p;
   p += n * B;
-  L.P = p;
-  p += n * n * B;
+  if constexpr (!Lsoda<kN>::kRegLU) {
+    L.P = p;
+    p += n * n * B;
+  }
   L.a = p;
   p += m * B;
   L.av = p;
@@ -354,6 +450,12 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) - L.z(j + 1, i);
     };
     auto form_p = [&](const double* yy) {
+      if constexpr (Lsoda<kN>::kRegLU) {
+        const double hl0 = h * el0;
+        hl0_p = hl0;
+        have_p = L.template form_lu_reg<kCount>(yy, hl0);
+        return have_p;
+      }
       L.template jacobian<kCount>(yy, L.P);
       const double hl0 = h * el0;
       for (int q = 0; q < n * n; ++q) L.P[q * B] = -hl0 * L.P[q * B];
@@ -401,7 +503,8 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             double del;
             if (meth == 1) {
               for (int i = 0; i < n; ++i) L.tmp[i * B] = h * L.savf[i * B] - (L.z(1, i) + L.acor[i * B]);
-              L.template lu_solve<kCount>(L.tmp);
+              if constexpr (Lsoda<kN>::kRegLU) L.template lu_solve_reg<kCount>(L.tmp);
+              else L.template lu_solve<kCount>(L.tmp);
               del = L.template wrms<kCount>(L.tmp);
               for (int i = 0; i < n; ++i) {
                 L.acor[i * B] = L.acor[i * B] + L.tmp[i * B];
@@ -615,7 +718,12 @@ __host__ __device__ __forceinline__ size_t lsoda_warp_doubles(const KinTables& T
 }
 
 template <bool kCount, bool kGlobal, int kN>
-__global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ KinTables T,
+// __maxnreg__ rather than __launch_bounds__(32): with the launch bounds
+// ptxas held these kernels at 128 registers and spilled (the generic variant
+// 316 bytes, the N = 4 one 352 with the register LU); 200 lets them allocate
+// what they use (N = 4: 167 registers, no spills) — residency is set by the
+// shared-memory state anyway.
+__global__ void __maxnreg__(200) lsoda_kernel(const __grid_constant__ KinTables T,
                                                        const __grid_constant__ KinSweepDev S, KinOutDev O,
                                                        const double* __restrict__ co,
                                                        unsigned long long* __restrict__ next) {
@@ -623,7 +731,7 @@ __global__ void __launch_bounds__(kBlock) lsoda_kernel(const __grid_constant__ K
   constexpr int B = kBlock;
   const int tid = threadIdx.x, lane = tid & 31;
   const int n = T.n;
-  const size_t nd = static_cast<size_t>(18 * n + n * n + T.m + S.n_axes) * B;
+  const size_t nd = static_cast<size_t>(18 * n + (Lsoda<kN>::kRegLU ? 0 : n * n) + T.m + S.n_axes) * B;
   // state in shared memory, or (kGlobal: models too large for it) in this
   // block's region of global memory, same layout
   double* sbase = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * lsoda_warp_doubles(T, S) : smem;

@@ -26,6 +26,9 @@ cfgs = {
     "c2": W.c2_config(),
     "c3_ode": W.c3_config(method=MethodKind.Ode),
     "c3_lsoda": W.c3_config(),
+    "c3s_lsoda": W.c3_stiff_config(),
+    "c3s_ode": W.c3_stiff_config(method=MethodKind.Ode),
+    "c4_lsoda": W.c4_config(method=MethodKind.Lsoda, side=64),
     "c5_tau": W.c5_config(),
     "c5_ode": W.c5_config(method=MethodKind.Ode),
     "c1_hybrid": W.c1_config(MethodKind.Hybrid, side=128),
