@@ -35,6 +35,8 @@ cfgs = {
     "c1_hybrid256": W.c1_config(MethodKind.Hybrid, side=256),
     "c1_cle": W.c1_config(MethodKind.Cle, side=128),
 }
+cfgs["c4_tau_bin"] = W.c4_config()
+cfgs["c4_tau_bin"][1].method.firing = abi.FIRING_BINOMIAL
 for _k in ("c1_hybrid", "c1_hybrid256"):
     cfgs[_k][1].method = __import__("paper_1309_7695_b200").ensemble.Method(MethodKind.Hybrid, theta_x=100.0, theta_a=10.0)
 cfgs["c1_cle"][1].method = __import__("paper_1309_7695_b200").ensemble.Method(MethodKind.Cle, tau=0.05)
