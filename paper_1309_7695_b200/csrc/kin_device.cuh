@@ -443,18 +443,52 @@ __device__ __forceinline__ uint64_t binomial(Rng& rng, uint64_t n, double p, uin
   uint64_t fl = flip ? 2 : 1;
   uint64_t k = 0;
   if (np < 10.0) {  // BINV
-    const double s = q / (1.0 - q);
-    const double a = (fn + 1.0) * s;
-    double f = pmath::pm_exp(fn * pmath::pm_log(1.0 - q));
-    double c = f;
-    const double u = rng.uniform();
-    const uint64_t kmax = n < 255 ? n : 255;
-    while (u > c && k < kmax) {
-      ++k;
-      f = f * (a / static_cast<double>(k) - s);
-      c = c + f;
+    const uint64_t ub = rng.bits53();  // the one uniform, formed in double only if needed
+    bool done = false;
+    // Fast decision path (returns exactly the k of the algorithm below): the
+    // CDF search in FP32.  Relative error of c'_k against the exact c_k:
+    // f'_0 = __expf(n log1pf(-q)) <= 4e-6 (|n log(1-q)| < 14), each step
+    // p' *= s (n+1-k) rcp(k) (no cancellation; n+1-k exact below 2^24) <= 5e-7,
+    // each cumulative add 6e-8: <= 1.8e-5 for k <= 24, and u' from the 53 bits
+    // <= 1.2e-7.  A guard G = 1e-4 (> 5x that) makes "u < c'_k (1-G) and
+    // u > c'_{k-1} (1+G)" imply the exact search stops at k; otherwise (a few
+    // 1e-4 of the draws, or n >= 2^24, or k > 24) the exact search runs.
+    if (n < (1ull << 24)) {
+      constexpr float G = 1e-4f;
+      const float uf = __fmaf_rn(__ull2float_rn(ub), 0x1p-53f, 0x1p-54f);
+      const float qf = static_cast<float>(q);
+      const float sf = qf / (1.0f - qf);
+      const float nf = static_cast<float>(n);
+      float pf = __expf(nf * log1pf(-qf));
+      float cf = pf, cprev = 0.0f;
+      const int kcap = n < 24 ? static_cast<int>(n) : 24;
+      int kk = 0;
+      while (uf > cf * (1.0f + G) && kk < kcap) {
+        ++kk;
+        pf = pf * (sf * (nf + 1.0f - static_cast<float>(kk)) * c_rcp40[kk]);
+        cprev = cf;
+        cf = cf + pf;
+      }
+      if (kk < kcap && uf < cf * (1.0f - G) && (kk == 0 || uf > cprev * (1.0f + G))) {
+        k = static_cast<uint64_t>(kk);
+        fl += 10 + 4 * k;
+        done = true;
+      }
     }
-    fl += 10 + 4 * k;
+    if (!done) {
+      const double s = q / (1.0 - q);
+      const double a = (fn + 1.0) * s;
+      double f = pmath::pm_exp(fn * pmath::pm_log(1.0 - q));
+      double c = f;
+      const double u = Rng::uniform_from_bits(ub);
+      const uint64_t kmax = n < 255 ? n : 255;
+      while (u > c && k < kmax) {
+        ++k;
+        f = f * (a / static_cast<double>(k) - s);
+        c = c + f;
+      }
+      fl += 10 + 4 * k;
+    }
   } else {
     k = binomial_btrd(rng, fn, q, np, fl);
   }
