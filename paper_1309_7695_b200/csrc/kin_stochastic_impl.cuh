@@ -232,7 +232,9 @@ __device__ __forceinline__ uint64_t binomial_fire(const KinTables& T, const Mode
   double lim = KIN_INF;
   for (int t = 0; t < nt; ++t) {
     const double x = sm.xv(KIN_RD_SPECIES(d, t));
-    const double v = floor(__ddiv_rn(x, static_cast<double>(KIN_RD_STOICH(d, t))));
+    const int st = KIN_RD_STOICH(d, t);
+    // floor(x / st): x / 1 and x / 2 are exact scalings (= x, x * 0.5)
+    const double v = st == 1 ? x : floor(st == 2 ? __dmul_rn(x, 0.5) : __ddiv_rn(x, 3.0));
     if (v < lim) lim = v;
   }
   if (kCount) flops += static_cast<uint64_t>(nt);
