@@ -63,6 +63,9 @@ std::string dlit(double v) {
   return s;
 }
 
+// Largest model whose SSA events are branch-free (select, update and
+// propensity refresh the same instructions on every lane, whatever `sel`).
+constexpr int kUniformSsaMaxReactions = 8;
 // Largest model whose divergent SSA updates are emitted as a switch.
 constexpr int kSwitchMaxReactions = 8;
 // Largest number of species with a nu row whose select_tau is fully inlined.
@@ -221,7 +224,33 @@ std::string generate_policy(const JitModel& m) {
   // serialises a warp over every distinct case it holds (up to M of them).
   // Small models keep the straight-line cases; larger ones walk the tables
   // (TableModel: the lanes stay converged, only trip counts differ).
-  if (m.m <= kSwitchMaxReactions) {
+  if (m.m <= jit_knob("KIN_JIT_UNIFORM_SSA", kUniformSsaMaxReactions)) {
+    // Branch-free SSA event: each touched species takes its delta for `j`
+    // from a select chain (a zero delta rewrites the same amount), and every
+    // propensity is re-evaluated (a pure function of x: the untouched ones
+    // get the same values) — the lanes of a warp never split over `sel`.
+    std::vector<int> touched(m.n, 0);
+    for (int p = 0; p < m.col_ptr[m.m]; ++p) touched[m.col_species[p]] = 1;
+    o << "  static constexpr bool kUniformSsa = true;\n  static constexpr bool kFlatBurst = true;\n"
+         "  static constexpr int kM = " << m.m << ";\n";
+    o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const {\n    bool neg = false;\n";
+    for (int i = 0; i < m.n; ++i) {
+      if (!touched[i]) continue;
+      std::vector<int> d(m.m, 0);
+      for (int j = 0; j < m.m; ++j)
+        for (int p = m.col_ptr[j]; p < m.col_ptr[j + 1]; ++p)
+          if (m.col_species[p] == i) d[j] += m.col_delta[p];
+      o << "    { const int d = ";
+      for (int j = 0; j + 1 < m.m; ++j) o << "j == " << j << " ? " << d[j] << " : ";
+      o << d[m.m - 1] << "; const bool ng = upd1(" << i << ", d, ovf); neg |= d != 0 && ng; }\n";
+    }
+    o << "    return neg;\n  }\n";
+    o << "  __device__ __forceinline__ void dep_update(int) const {\n";
+    for (int j = 0; j < m.m; ++j) o << "    a[" << j << " * B] = prop(" << j << ");\n";
+    o << "  }\n";
+  } else if (m.m <= kSwitchMaxReactions) {
+    o << "  static constexpr bool kUniformSsa = false;\n  static constexpr bool kFlatBurst = false;\n"
+         "  static constexpr int kM = " << m.m << ";\n";
     o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const {\n    bool neg = false;\n    switch (j) {\n";
     for (int j = 0; j < m.m; ++j) {
       o << "      case " << j << ":";
@@ -239,6 +268,8 @@ std::string generate_policy(const JitModel& m) {
     }
     o << "    }\n  }\n";
   } else {
+    o << "  static constexpr bool kUniformSsa = false;\n  static constexpr bool kFlatBurst = false;\n"
+         "  static constexpr int kM = " << m.m << ";\n";
     o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const { return TableModel<XT>{T, x, a, av}.fire(j, ovf); }\n"
          "  __device__ __forceinline__ void dep_update(int sel) const { TableModel<XT>{T, x, a, av}.dep_update(sel); }\n";
   }

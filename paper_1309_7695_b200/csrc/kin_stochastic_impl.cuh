@@ -57,6 +57,9 @@ __device__ __forceinline__ double tau_bound(double tau, double eps, double x, do
 // the launch with the double variant — results are identical either way).
 template <class XT, int kB = kBlock>
 struct TableModel {
+  static constexpr bool kUniformSsa = false;
+  static constexpr bool kFlatBurst = false;
+  static constexpr int kM = 0;
   const KinTables& T;
   XT* x;             // x[i * B]
   double* a;         // a[j * B]
@@ -187,6 +190,19 @@ __device__ __forceinline__ double ssa_dt(double u1, double a0) { return __ddiv_r
 template <class Model>
 __device__ __forceinline__ int ssa_select(const Model& sm, int M, double a0, double u2) {
   const double target = __dmul_rn(u2, a0);
+  if constexpr (Model::kUniformSsa) {
+    // small models: every partial sum, predicated picks (no data-dependent exit)
+    double c = 0.0;
+    int sel = -1, last = -1;
+#pragma unroll
+    for (int j = 0; j < Model::kM; ++j) {
+      const double aj = sm.aval(j);
+      c = __dadd_rn(c, aj);
+      if (sel < 0 && aj > 0.0) last = j;
+      if (sel < 0 && c > target) sel = j;
+    }
+    return sel < 0 ? last : sel;
+  }
   double c = 0.0;
   int sel = -1, last = -1, j = 0;
   // two reactions per trip (same additions in the same order): both loads and
@@ -291,155 +307,170 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   bool a_valid = false;
   double a0 = 0.0;
 
-  while (t < t_end && !ovf) {
-    if (++used > budget) { status = KIN_SIM_BUDGET; break; }
-    if (!a_valid) a0 = sm.all_props(M);
-    a_valid = false;
-    if (kCount) flops += F_prop + M;
-    if (a0 == 0.0) break;
+  // Small models (Model::kFlatBurst): one flat loop, one step per trip — a
+  // decision (then a leap, or the first event of an SSA burst) or the next
+  // event of a burst.  A burst nested inside the decision loop holds every
+  // lane of the warp at the loop head until the warp's longest burst ends: a
+  // lane that leapt advanced one leap per 100 events of its neighbours (C2:
+  // 73 -> 50 ms).  b: position in the burst, -1 at a decision; it saturates
+  // at 100 (pure SSA never leaves its burst).
+  int b = -1;
+  for (;;) {
+    if (b < 0) {
+      if (!(t < t_end) || ovf) break;
+      if (++used > budget) { status = KIN_SIM_BUDGET; break; }
+      if (!a_valid) a0 = sm.all_props(M);
+      a_valid = false;
+      if (kCount) flops += F_prop + M;
+      if (a0 == 0.0) break;
 
-    double tau = 0.0;
-    bool burst = false;
-    if (kind == 0) {
-      burst = true;
-    } else if (kind == 1) {
-      tau = sm.template select_tau<kCount>(S.epsilon, flops);
-      if (kCount) flops += 1;
-      burst = tau < __ddiv_rn(10.0, a0);
-    } else {
-      tau = S.tau;
-    }
-
-    if (burst) {
-      bool stop = false;
-      for (int b = 0;; ++b) {
-        if (b > 0) {
-          if (kind != 0 && b >= 100) { a_valid = true; break; }
-          if (++used > budget) { status = KIN_SIM_BUDGET; stop = true; break; }
-          if (kCount) flops += F_prop + M;
-          if (a0 == 0.0) { stop = true; break; }
-        }
-        double u1, u2;
-        if (kPhilox) {
-          PhiloxSite src(seed, ev++, kPhiloxSsaSite);
-          u1 = src.uniform();
-          u2 = src.uniform();
-        } else {
-          u1 = rng.uniform();
-          u2 = rng.uniform();
-        }
-        const double dt = ssa_dt(u1, a0);
-        const double tn = __dadd_rn(t, dt);
-        if (kCount) flops += 8;
-        if (tn > t_end) { t = t_end; stop = true; break; }
-        while (gi < G && tab_grid(T, S, gi) < tn) emit();
-        const int sel = ssa_select(sm, M, a0, u2);
-        if (kCount) flops += 1 + static_cast<uint64_t>(sel + 1);
-        if (sm.fire(sel, ovf)) { status = KIN_SIM_NEGATIVE; stop = true; break; }
-        if (ovf) { stop = true; break; }
-        if (kCount) flops += static_cast<uint64_t>(sm.col_len(sel));
-        t = tn;
-        if (kind == 0) ++n_steps; else ++n_ssa;
-        while (gi < G && tab_grid(T, S, gi) <= t) emit();
-        // re-evaluate the propensities that changed, then a0 in oracle order
-        sm.dep_update(sel);
-        a0 = sm.sum_props(M);
-      }
-      if (stop) break;
-      continue;
-    }
-
-    // Poisson leap truncated at the next grid time; reject -> halve
-    const double t_stop = (gi < G && tab_grid(T, S, gi) < t_end) ? tab_grid(T, S, gi) : t_end;
-    bool hit = false;
-    const double gap = __dsub_rn(t_stop, t);
-    if (kCount) flops += 1;
-    if (!(tau < gap)) { tau = gap; hit = true; }
-    if (KIN_FIRING_OF(S) == KIN_FIRING_BINOMIAL) {
-      // sequential binomial leap: one attempt, never rejected
-#pragma unroll 1
-      for (int j = 0; j < M; ++j) {
-        uint64_t k, fl = 0;
-        const double mean = __dmul_rn(sm.aval(j), tau);
-        if (kPhilox) {
-          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
-          k = binomial_fire<kCount>(T, sm, j, mean, src, fl, S.lgamma_tab);
-        } else {
-          k = binomial_fire<kCount>(T, sm, j, mean, rng, fl, S.lgamma_tab);
-        }
-        if (kCount) flops += fl;
-        if (k != 0) sm.apply(j, static_cast<long long>(k), ovf);
-      }
-      if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
-      ++ev;
-      if (ovf) break;
-      if (hit) {
-        t = t_stop;
+      double tau = 0.0;
+      bool burst = false;
+      if (kind == 0) {
+        burst = true;
+      } else if (kind == 1) {
+        tau = sm.template select_tau<kCount>(S.epsilon, flops);
+        if (kCount) flops += 1;
+        burst = tau < __ddiv_rn(10.0, a0);
       } else {
-        t = __dadd_rn(t, tau);
-        if (kCount) flops += 1;
+        tau = S.tau;
       }
-      ++n_steps;
-      while (gi < G && tab_grid(T, S, gi) <= t) emit();
-      continue;
-    }
-    Xoshiro saved = rng, resume;
-    // One Poisson call site (code size): pass 0 draws and applies; a rejected
-    // attempt runs pass 1, which replays the same draws (the saved stream is
-    // swapped into `rng`, or the same Philox counters) and subtracts them, then
-    // resumes the stream where pass 0 left it and retries with tau/2.  The
-    // streams are swapped by value so they stay in registers.
-    long long sign = 1;
-    for (;;) {
-      // a_{j+1} is loaded while reaction j draws (global-memory state: hides
-      // the load latency behind the Poisson draw)
-      double a_next = sm.aval(0);
+      if (burst) {
+        b = 0;
+      } else {
+        // Poisson leap truncated at the next grid time; reject -> halve
+        const double t_stop = (gi < G && tab_grid(T, S, gi) < t_end) ? tab_grid(T, S, gi) : t_end;
+        bool hit = false;
+        const double gap = __dsub_rn(t_stop, t);
+        if (kCount) flops += 1;
+        if (!(tau < gap)) { tau = gap; hit = true; }
+        if (KIN_FIRING_OF(S) == KIN_FIRING_BINOMIAL) {
+          // sequential binomial leap: one attempt, never rejected
 #pragma unroll 1
-      for (int j = 0; j < M; ++j) {
-        uint64_t k, fl = 0;
-        const double aj = a_next;
-        if (j + 1 < M) a_next = sm.aval(j + 1);
-        const double mean = __dmul_rn(aj, tau);
-        if (kPhilox) {
-          PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
-          k = poisson<kCount>(src, mean, fl, S.lgamma_tab);
-        } else {
-          k = poisson<kCount>(rng, mean, fl, S.lgamma_tab);
+          for (int j = 0; j < M; ++j) {
+            uint64_t k, fl = 0;
+            const double mean = __dmul_rn(sm.aval(j), tau);
+            if (kPhilox) {
+              PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
+              k = binomial_fire<kCount>(T, sm, j, mean, src, fl, S.lgamma_tab);
+            } else {
+              k = binomial_fire<kCount>(T, sm, j, mean, rng, fl, S.lgamma_tab);
+            }
+            if (kCount) flops += fl;
+            if (k != 0) sm.apply(j, static_cast<long long>(k), ovf);
+          }
+          if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
+          ++ev;
+          if (ovf) break;
+          if (hit) {
+            t = t_stop;
+          } else {
+            t = __dadd_rn(t, tau);
+            if (kCount) flops += 1;
+          }
+          ++n_steps;
+          while (gi < G && tab_grid(T, S, gi) <= t) emit();
+          continue;
         }
-        if (kCount && sign > 0) flops += fl;
-        if (k != 0) sm.apply(j, sign * static_cast<long long>(k), ovf);
-      }
-      if (sign < 0) {
-        // undone: continue the stream with half the step
-        sign = 1;
-        ++ev;
-        rng = resume;
-        saved = rng;
-        ++n_rej;
-        tau = __dmul_rn(tau, 0.5);
-        hit = false;
-        if (kCount) flops += 1;
+        Xoshiro saved = rng, resume;
+        // One Poisson call site (code size): pass 0 draws and applies; a rejected
+        // attempt runs pass 1, which replays the same draws (the saved stream is
+        // swapped into `rng`, or the same Philox counters) and subtracts them, then
+        // resumes the stream where pass 0 left it and retries with tau/2.  The
+        // streams are swapped by value so they stay in registers.
+        long long sign = 1;
+        for (;;) {
+          // a_{j+1} is loaded while reaction j draws (global-memory state: hides
+          // the load latency behind the Poisson draw)
+          double a_next = sm.aval(0);
+#pragma unroll 1
+          for (int j = 0; j < M; ++j) {
+            uint64_t k, fl = 0;
+            const double aj = a_next;
+            if (j + 1 < M) a_next = sm.aval(j + 1);
+            const double mean = __dmul_rn(aj, tau);
+            if (kPhilox) {
+              PhiloxSite src(seed, ev, static_cast<uint32_t>(j));
+              k = poisson<kCount>(src, mean, fl, S.lgamma_tab);
+            } else {
+              k = poisson<kCount>(rng, mean, fl, S.lgamma_tab);
+            }
+            if (kCount && sign > 0) flops += fl;
+            if (k != 0) sm.apply(j, sign * static_cast<long long>(k), ovf);
+          }
+          if (sign < 0) {
+            // undone: continue the stream with half the step
+            sign = 1;
+            ++ev;
+            rng = resume;
+            saved = rng;
+            ++n_rej;
+            tau = __dmul_rn(tau, 0.5);
+            hit = false;
+            if (kCount) flops += 1;
+            continue;
+          }
+          if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
+          if (ovf) break;
+          if (!sm.any_negative()) {
+            ++ev;
+            break;
+          }
+          sign = -1;
+          resume = rng;
+          rng = saved;
+        }
+        if (ovf) break;
+        if (hit) {
+          t = t_stop;
+        } else {
+          t = __dadd_rn(t, tau);
+          if (kCount) flops += 1;
+        }
+        ++n_steps;
+        while (gi < G && tab_grid(T, S, gi) <= t) emit();
         continue;
       }
-      if (kCount) flops += static_cast<uint64_t>(M) + 2 * static_cast<uint64_t>(T.nnz);
-      if (ovf) break;
-      if (!sm.any_negative()) {
-        ++ev;
-        break;
+    }
+    // the burst's events: one per trip of the outer loop (kFlat), or the whole
+    // burst here (large models, whose rare bursts cost less than the extra
+    // per-trip divergence of the flat form: C4 94 vs 103 ms)
+    bool done = false;
+    do {
+      if (b > 0) {
+        if (kind != 0 && b >= 100) { a_valid = true; b = -1; break; }
+        if (++used > budget) { status = KIN_SIM_BUDGET; done = true; break; }
+        if (kCount) flops += F_prop + M;
+        if (a0 == 0.0) { done = true; break; }
       }
-      sign = -1;
-      resume = rng;
-      rng = saved;
-    }
-    if (ovf) break;
-    if (hit) {
-      t = t_stop;
-    } else {
-      t = __dadd_rn(t, tau);
-      if (kCount) flops += 1;
-    }
-    ++n_steps;
-    while (gi < G && tab_grid(T, S, gi) <= t) emit();
+      double u1, u2;
+      if (kPhilox) {
+        PhiloxSite src(seed, ev++, kPhiloxSsaSite);
+        u1 = src.uniform();
+        u2 = src.uniform();
+      } else {
+        u1 = rng.uniform();
+        u2 = rng.uniform();
+      }
+      const double dt = ssa_dt(u1, a0);
+      const double tn = __dadd_rn(t, dt);
+      if (kCount) flops += 8;
+      if (tn > t_end) { t = t_end; done = true; break; }
+      while (gi < G && tab_grid(T, S, gi) < tn) emit();
+      const int sel = ssa_select(sm, M, a0, u2);
+      if (kCount) flops += 1 + static_cast<uint64_t>(sel + 1);
+      if (sm.fire(sel, ovf)) { status = KIN_SIM_NEGATIVE; done = true; break; }
+      if (ovf) { done = true; break; }
+      if (kCount) flops += static_cast<uint64_t>(sm.col_len(sel));
+      t = tn;
+      if (kind == 0) ++n_steps; else ++n_ssa;
+      while (gi < G && tab_grid(T, S, gi) <= t) emit();
+      // re-evaluate the propensities that changed, then a0 in oracle order
+      sm.dep_update(sel);
+      a0 = sm.sum_props(M);
+      if (b < 100) ++b;
+    } while (!Model::kFlatBurst);
+    if (done) break;
   }
   if (ovf) {
     status = KIN_SIM_INTERNAL_RETRY;
