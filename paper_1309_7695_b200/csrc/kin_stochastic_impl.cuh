@@ -297,13 +297,21 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   const uint64_t budget = S.max_steps;
   const uint64_t F_prop = static_cast<uint64_t>(T.fprop);
 
+  // time of grid point gi (+inf past the end).  Small models keep it in a
+  // register (read once per grid point instead of twice per SSA event: C2
+  // 51 -> 47 ms); for C4 the two extra registers cross the 128-register line
+  // at which 14 warps per SM fit (4 per scheduler): 94 -> 156 ms.
+  constexpr bool kTg = Model::kFlatBurst;
+  double tg = (kTg && G > 0) ? tab_grid(T, S, 0) : KIN_INF;
+  auto next_grid = [&]() { return kTg ? tg : (gi < G ? tab_grid(T, S, gi) : KIN_INF); };
   auto emit = [&]() {
     double* o = O.traj + (static_cast<size_t>(s) * G + gi) * N;  // [sim][g][n]: one contiguous run per emit
     for (int i = 0; i < N; ++i) o[i] = sm.xv(i);
     ++gi;
+    if (kTg) tg = gi < G ? tab_grid(T, S, gi) : KIN_INF;
   };
 
-  while (gi < G && tab_grid(T, S, gi) <= t) emit();
+  while (next_grid() <= t) emit();
   bool a_valid = false;
   double a0 = 0.0;
 
@@ -339,7 +347,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         b = 0;
       } else {
         // Poisson leap truncated at the next grid time; reject -> halve
-        const double t_stop = (gi < G && tab_grid(T, S, gi) < t_end) ? tab_grid(T, S, gi) : t_end;
+        const double t_stop = next_grid() < t_end ? next_grid() : t_end;
         bool hit = false;
         const double gap = __dsub_rn(t_stop, t);
         if (kCount) flops += 1;
@@ -369,7 +377,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
             if (kCount) flops += 1;
           }
           ++n_steps;
-          while (gi < G && tab_grid(T, S, gi) <= t) emit();
+          while (next_grid() <= t) emit();
           continue;
         }
         Xoshiro saved = rng, resume;
@@ -428,7 +436,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
           if (kCount) flops += 1;
         }
         ++n_steps;
-        while (gi < G && tab_grid(T, S, gi) <= t) emit();
+        while (next_grid() <= t) emit();
         continue;
       }
     }
@@ -456,7 +464,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
       const double tn = __dadd_rn(t, dt);
       if (kCount) flops += 8;
       if (tn > t_end) { t = t_end; done = true; break; }
-      while (gi < G && tab_grid(T, S, gi) < tn) emit();
+      while (next_grid() < tn) emit();
       const int sel = ssa_select(sm, M, a0, u2);
       if (kCount) flops += 1 + static_cast<uint64_t>(sel + 1);
       if (sm.fire(sel, ovf)) { status = KIN_SIM_NEGATIVE; done = true; break; }
@@ -464,10 +472,16 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
       if (kCount) flops += static_cast<uint64_t>(sm.col_len(sel));
       t = tn;
       if (kind == 0) ++n_steps; else ++n_ssa;
-      while (gi < G && tab_grid(T, S, gi) <= t) emit();
+      while (next_grid() <= t) emit();
       // re-evaluate the propensities that changed, then a0 in oracle order
-      sm.dep_update(sel);
-      a0 = sm.sum_props(M);
+      // (small models: all of them, summed as they are produced — the same
+      // values without the shared-memory round trip)
+      if constexpr (Model::kUniformSsa) {
+        a0 = sm.all_props(M);
+      } else {
+        sm.dep_update(sel);
+        a0 = sm.sum_props(M);
+      }
       if (b < 100) ++b;
     } while (!Model::kFlatBurst);
     if (done) break;
