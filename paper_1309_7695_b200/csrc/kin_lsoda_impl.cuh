@@ -591,16 +591,40 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
         if (kCount) L.flops += 2 * static_cast<uint64_t>(nq + 1) * n;
         const double tprev = t;
         t = tn;
-        while (gi < G && tab_grid(T, S, gi) <= t && tab_grid(T, S, gi) > tprev) {
-          const double sg = (tab_grid(T, S, gi) - t) / h;
-          for (int i = 0; i < n; ++i) {
-            double vv = L.z(nq, i);
+        for (;;) {
+          if (!(gi < G)) break;
+          const double tg = tab_grid(T, S, gi);
+          if (!(tg <= t && tg > tprev)) break;
+          const double sg = (tg - t) / h;
+          if constexpr (kN > 0) {
+            // Horner over the Nordsieck columns with the species as the inner
+            // (unrolled) loop: kN independent chains instead of kN serial
+            // ones — each species' operations and their order unchanged
+            double vv[kN > 0 ? kN : 1];
+#pragma unroll
+            for (int i = 0; i < kN; ++i) vv[i] = L.z(nq, i);
 #pragma unroll 1
-            for (int j = nq - 1; j >= 0; --j) vv = L.z(j, i) + sg * vv;
-            L.tmp[i * B] = vv;
+            for (int j = nq - 1; j >= 0; --j)
+#pragma unroll
+              for (int i = 0; i < kN; ++i) vv[i] = L.z(j, i) + sg * vv[i];
+            double* o = O.traj + (static_cast<size_t>(s) * G + gi) * n;  // emit() from registers
+#pragma unroll
+            for (int i = 0; i < kN; ++i) {
+              double vi = vv[i];
+              if (vi < 0.0) { vi = 0.0; floored = true; }
+              o[i] = vi;
+            }
+            ++gi;
+          } else {
+            for (int i = 0; i < n; ++i) {
+              double vv = L.z(nq, i);
+#pragma unroll 1
+              for (int j = nq - 1; j >= 0; --j) vv = L.z(j, i) + sg * vv;
+              L.tmp[i * B] = vv;
+            }
+            emit(gi++, L.tmp);
           }
           if (kCount) L.flops += 2 * static_cast<uint64_t>(nq) * n + 2;
-          emit(gi++, L.tmp);
         }
         break;
       }
