@@ -473,13 +473,26 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
     // predictor / corrector / error-test code runs with the warp together
     // instead of drifting apart into 32 serial simulations.
     bool running = t < t_end && status == 0;
+    bool fresh = true;  // the next attempt starts a new step (ewt, kflag, ncf reset)
+    int kflag = 0, ncf = 0;
+    double dsm = 0.0;
     while (__any_sync(mask, running)) {
       if (!running) continue;
       do {
-      for (int i = 0; i < n; ++i) L.ewt[i * B] = rtol * fabs(L.z(0, i)) + atol;
-      int kflag = 0, ncf = 0;
-      double dsm = 0.0;
-      for (;;) {
+      if (fresh) {
+        for (int i = 0; i < n; ++i) L.ewt[i * B] = rtol * fabs(L.z(0, i)) + atol;
+        kflag = 0;
+        ncf = 0;
+        dsm = 0.0;
+        fresh = false;
+      }
+      // ONE attempt per trip of the warp loop: a lane whose step was rejected
+      // retries on the next trip while the others take their next step (as
+      // one attempt loop per trip, every lane waited out the warp's most
+      // rejected step: with ~9% of attempts rejected, nearly every trip ran
+      // two attempts).  `continue` below ends the trip without accepting.
+      bool accepted = false;
+      do {
         if (attempts++ >= S.max_steps) { status = KIN_SIM_BUDGET; break; }
         if (!(h > 0.0) || t + h == t) { status = KIN_SIM_STEP_UNDERFLOW; break; }
         if (meth == 1 && (!have_p || fabs(h * el0 / hl0_p - 1.0) > 0.3 || nst >= nslp + 20)) ipup = true;
@@ -626,9 +639,10 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           }
           if (kCount) L.flops += 2 * static_cast<uint64_t>(nq) * n + 2;
         }
-        break;
-      }
-      if (status != 0) break;
+        accepted = true;
+      } while (0);
+      if (status != 0 || !accepted) break;
+      fresh = true;
       // order / step / method selection
       --ialth;
       if (ialth == 0) {
