@@ -585,6 +585,7 @@ struct Buffers {
   DevBuf<int> ovf;
   int* ovf_host = nullptr;  // pinned copy of the overflow flag
   cudaStream_t st = nullptr;  // compute stream of this launch (one of the slot's)
+  cudaStream_t cs = nullptr;  // copy stream of its async copy-out (paired with st)
   cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};  // sim start, sim end, stats end
   cudaEvent_t ev_done = nullptr, ev_copied = nullptr;
   bool timed_stats = false;
@@ -635,7 +636,10 @@ struct Slot {
   cudaStream_t aux_stream = nullptr;   // kernels of the alternate async jobs: two independent
                                        // sweeps in flight overlap (one fills the SMs the
                                        // other's tail leaves idle)
-  cudaStream_t copy_stream = nullptr;  // copy-out of async jobs
+  cudaStream_t copy_stream = nullptr;  // copy-out of the async jobs on `stream`
+  cudaStream_t aux_copy_stream = nullptr;  // ... and of those on `aux_stream`: a job's D2H
+                                           // starts when its own kernel ends, not behind
+                                           // the other stream's (longer) job
   unsigned job_rr = 0;
   DevBuf<double> lgamma_tab;  // glibc lgamma(k+1), k < KIN_LGAMMA_N
   DevBuf<double> lsoda_co;    // cfode elco/tesco
@@ -1225,7 +1229,7 @@ int finish_launch(Slot& sl, Buffers& bf, kin_error* err) {
 // the compute stream.
 int copy_out(Slot& sl, Buffers& bf, const kin_sweep_out* out, uint64_t base_point, bool sync, kin_error* err) {
   NvtxRange nv("kin: copy-out (D2H into the caller layout)");
-  cudaStream_t st = sync ? bf.st : sl.copy_stream;
+  cudaStream_t st = sync ? bf.st : (bf.cs ? bf.cs : sl.copy_stream);
   const uint64_t S = bf.s1 - bf.s0;
   const size_t gn = static_cast<size_t>(bf.G) * bf.N;
   const PlanPart& pt = bf.part;
@@ -1422,6 +1426,7 @@ int kin_ctx_create(const int32_t* ids, int32_t n, kin_ctx** out, kin_error* err)
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->stream, cudaStreamNonBlocking), "cudaStreamCreate");
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->aux_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     KIN_CUDA(cudaStreamCreateWithFlags(&sl->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    KIN_CUDA(cudaStreamCreateWithFlags(&sl->aux_copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     // lgamma(k+1) from the host libm (the oracle's, glibc) for the PTRS test
     std::vector<double> lg(KIN_LGAMMA_N);
     // (lgamma_r: glibc's lgamma writes the global signgam — a data race when
@@ -1454,6 +1459,7 @@ void kin_ctx_destroy(kin_ctx* ctx) {
     cudaStreamSynchronize(sl->stream);
     cudaStreamSynchronize(sl->aux_stream);
     cudaStreamSynchronize(sl->copy_stream);
+    cudaStreamSynchronize(sl->aux_copy_stream);
     sl->main.release();
     for (auto& b : sl->pool) b->release();
     sl->lgamma_tab.release();
@@ -1463,6 +1469,7 @@ void kin_ctx_destroy(kin_ctx* ctx) {
     cudaStreamDestroy(sl->stream);
     cudaStreamDestroy(sl->aux_stream);
     cudaStreamDestroy(sl->copy_stream);
+    cudaStreamDestroy(sl->aux_copy_stream);
   }
   delete ctx;
 }
@@ -1550,7 +1557,9 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
         bf = new Buffers;
       }
       job->parts.push_back({part.dev, bf});
-      bf->st = (sl.job_rr++ & 1u) ? sl.aux_stream : sl.stream;
+      const bool aux = sl.job_rr++ & 1u;
+      bf->st = aux ? sl.aux_stream : sl.stream;
+      bf->cs = aux ? sl.aux_copy_stream : sl.copy_stream;
       if (int rc = launch_range(sl, *bf, model, desc, L, part, stats, job->out.work != nullptr, err, partials))
         return rc;
       if (!bf->ev_done) KIN_CUDA(cudaEventCreateWithFlags(&bf->ev_done, cudaEventDisableTiming), "event");
@@ -1558,9 +1567,9 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
       if (!bf->ovf_host) KIN_CUDA(cudaMallocHost(&bf->ovf_host, sizeof(int)), "pinned flag");
       KIN_CUDA(cudaEventRecord(bf->ev_done, bf->st), "event");
       // copy-out on the copy stream, overlapping the next launches on `stream`
-      KIN_CUDA(cudaStreamWaitEvent(sl.copy_stream, bf->ev_done, 0), "stream wait");
+      KIN_CUDA(cudaStreamWaitEvent(bf->cs, bf->ev_done, 0), "stream wait");
       if (int rc = copy_out(sl, *bf, &job->out, job->base_point, false, err)) return rc;
-      KIN_CUDA(cudaEventRecord(bf->ev_copied, sl.copy_stream), "event");
+      KIN_CUDA(cudaEventRecord(bf->ev_copied, bf->cs), "event");
     }
     return KIN_OK;
   };
@@ -1572,6 +1581,7 @@ int kin_sweep_submit(kin_ctx* ctx, const kin_model* model, const kin_sweep_desc*
       cudaSetDevice(sl.device);
       if (part.buf->st) cudaStreamSynchronize(part.buf->st);
       cudaStreamSynchronize(sl.copy_stream);
+      cudaStreamSynchronize(sl.aux_copy_stream);
       std::lock_guard<std::mutex> lk(sl.mu);
       part.buf->pending_check = false;
       sl.pool.emplace_back(part.buf);
@@ -1650,6 +1660,7 @@ int kin_sweep_wait(kin_ctx* ctx, uint64_t ticket, kin_error* err) {
       if (rc == KIN_OK) rc = cuda_fail(err, ce, "copy-out");
       cudaStreamSynchronize(bf.st);
       cudaStreamSynchronize(sl.copy_stream);
+      cudaStreamSynchronize(sl.aux_copy_stream);
       bf.pending_check = false;
       continue;
     }
