@@ -478,6 +478,32 @@ int pack_tables(const HostModel& H, const kin_sweep_desc* d, KinTables* T, std::
   T->off_rate_axis = put(rate_axis.data(), rate_axis.size(), 1);
   T->off_x0_axis = put(x0ax.data(), x0ax.size(), 1);
   if (overflow) { *msg = "model too large for the device tables"; return KIN_ERR_INPUT; }
+  // Work-balancing orders for kernels that spread a simulation's species /
+  // reactions over L lanes (Dopri5: lane l takes slots l, l+L, ...): sorted by
+  // descending nu-row length / reactant-term count, so the lanes of a warp
+  // walk rows of similar length together.  Optional (offset 0 = identity).
+  {
+    std::vector<int16_t> sp(H.n), rx(H.m);
+    for (int i = 0; i < H.n; ++i) sp[i] = static_cast<int16_t>(i);
+    for (int j = 0; j < H.m; ++j) rx[j] = static_cast<int16_t>(j);
+    std::stable_sort(sp.begin(), sp.end(), [&](int16_t u, int16_t v) {
+      return H.row_ptr[u + 1] - H.row_ptr[u] > H.row_ptr[v + 1] - H.row_ptr[v];
+    });
+    std::stable_sort(rx.begin(), rx.end(), [&](int16_t u, int16_t v) {
+      return H.rt_ptr[u + 1] - H.rt_ptr[u] > H.rt_ptr[v + 1] - H.rt_ptr[v];
+    });
+    const size_t save = off;
+    const uint32_t o1 = put(sp.data(), sp.size() * 2, 2);
+    const uint32_t o2 = put(rx.data(), rx.size() * 2, 2);
+    if (overflow || o1 == 0 || o2 == 0) {
+      overflow = false;
+      off = save;
+      T->off_sp_perm = T->off_rx_perm = 0;
+    } else {
+      T->off_sp_perm = o1;
+      T->off_rx_perm = o2;
+    }
+  }
   // the grid rides along when it fits (offset 0 = "use the global copy")
   const size_t save = off;
   const uint32_t og = put(d->grid, static_cast<size_t>(d->n_grid) * 8, 8);

@@ -98,6 +98,15 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
   const uint32_t* s_row = reinterpret_cast<const uint32_t*>(tblob + T.off_row);
   double* a = xs + N;
   double* av = a + M;
+  // lane slot -> species / reaction: the work-balancing orders of kin_tables.h
+  // for wide groups (C5, L = 32: 271 -> 232 ms); at L <= 8 the lookups cost
+  // more than the balance saves (C4 9.3 -> 9.4 ms, C3 2.6 -> 2.8 ms)
+  constexpr bool kPerm = L >= 16;
+  const int16_t* s_sp =
+      (kPerm && T.off_sp_perm) ? reinterpret_cast<const int16_t*>(tblob + T.off_sp_perm) : nullptr;
+  const int16_t* s_rx =
+      (kPerm && T.off_rx_perm) ? reinterpret_cast<const int16_t*>(tblob + T.off_rx_perm) : nullptr;
+  auto species = [&](int slot) { return s_sp ? static_cast<int>(s_sp[slot]) : slot; };
 
   if (lane == 0) {
     uint64_t rem = sim / S.runs;
@@ -113,9 +122,10 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
   double y[SL], k1[SL], k2[SL], k3[SL], k4[SL], k5[SL], k6[SL], k7[SL], yn[SL];
 #pragma unroll
   for (int q = 0; q < SL; ++q) {
-    const int i = lane + q * L;
+    const int slot = lane + q * L;
     y[q] = 0.0;
-    if (i < N) {
+    if (slot < N) {
+      const int i = species(slot);
       const int ax = tab_x0_axis(T, i);
       y[q] = ax < 0 ? tab_x0(T, i) : av[ax];
     }
@@ -126,7 +136,8 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
   // RHS of the stage state already published in xs: dx = nu * a(xs).
   auto rhs = [&](double* out) {
     grpc.sync();
-    for (int j = lane; j < M; j += L) {
+    for (int jj = lane; jj < M; jj += L) {
+      const int j = s_rx ? static_cast<int>(s_rx[jj]) : jj;
       const int ax = s_rate_axis[j];
       double aj = ax < 0 ? s_rate[j] : __dmul_rn(s_rate[j], av[ax]);
       const int p1 = s_rt_ptr[j + 1];
@@ -140,9 +151,10 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
     grpc.sync();
 #pragma unroll
     for (int q = 0; q < SL; ++q) {
-      const int i = lane + q * L;
+      const int slot = lane + q * L;
       double acc = 0.0;
-      if (i < N) {
+      if (slot < N) {
+        const int i = species(slot);
         const int p1 = s_row_ptr[i + 1];
 #pragma unroll 1
         for (int p = s_row_ptr[i]; p < p1; ++p) {
@@ -157,16 +169,16 @@ __global__ void __launch_bounds__(128, 4) dopri5_kernel(const __grid_constant__ 
   auto publish = [&](const double* v) {
 #pragma unroll
     for (int q = 0; q < SL; ++q) {
-      const int i = lane + q * L;
-      if (i < N) xs[i] = v[q];
+      const int slot = lane + q * L;
+      if (slot < N) xs[species(slot)] = v[q];
     }
   };
   auto emit = [&](int g, const double* v) {
     double* o = O.traj + (static_cast<size_t>(s) * G + g) * N;  // [sim][g][n]
 #pragma unroll
     for (int q = 0; q < SL; ++q) {
-      const int i = lane + q * L;
-      if (i < N) o[i] = v[q];
+      const int slot = lane + q * L;
+      if (slot < N) o[species(slot)] = v[q];
     }
   };
 

@@ -74,9 +74,9 @@ struct KinTables {
   uint32_t off_rdesc;     // uint64 [m]   packed reaction descriptor (KIN_RD_* below)
   uint32_t off_dep_ptr;   // int16  [m+1] reactions whose propensity changes when j fires
   uint32_t off_dep;       // uint16 [..]
-  uint32_t pad1_;
+  uint32_t off_sp_perm;   // int16  [n]   species by descending nu-row length (0: identity; Dopri5 lane slots)
   uint32_t used;
-  uint32_t pad_;
+  uint32_t off_rx_perm;   // int16  [m]   reactions by descending reactant-term count (0: identity)
   alignas(16) unsigned char blob[KIN_TABLE_BYTES];
 };
 
