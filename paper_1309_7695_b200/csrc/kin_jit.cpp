@@ -70,6 +70,8 @@ constexpr int kUniformSsaMaxReactions = 8;
 constexpr int kSwitchMaxReactions = 8;
 // Largest number of species with a nu row whose select_tau is fully inlined.
 constexpr int kInlineTauMaxSpecies = 8;
+// Smallest M whose select_tau walks four species per trip (large models).
+constexpr int kGroupTauMinReactions = 64;
 // Largest nnz(nu) whose leap update is a switch of straight-line updates.
 constexpr int kSwitchApplyMaxNnz = 16;
 // Largest M whose all_props is straight-line (above: uniform loop over prop(j)).
@@ -188,6 +190,39 @@ std::string generate_policy(const JitModel& m) {
         << "      if (!(mu == 0.0 && s2 == 0.0)) tau = tau_bound<kCount>(tau, eps, xv(" << i << "), " << dlit(m.g[i])
         << ", mu, s2, flops); }\n";
     }
+  } else if (m.m >= kGroupTauMinReactions) {
+    // large models (propensity cache in global memory): four species per
+    // trip, their row loads issued together, then four tau_bound in species
+    // order (one switch dispatch and one memory latency per four species)
+    constexpr int kG = 4;
+    const int n_grp = (n_act + kG - 1) / kG;
+    o << "#pragma unroll 1\n    for (int q = 0; q < " << n_grp << "; ++q) {\n"
+         "      double mu[" << kG << "] = {}, s2[" << kG << "] = {}, g[" << kG << "] = {1.0, 1.0, 1.0, 1.0};\n"
+         "      int sp[" << kG << "] = {}, nt = 0;\n      switch (q) {\n";
+    int q = 0;
+    for (int i = 0; i < m.n; ++i) {
+      const int p0 = m.row_ptr[i], p1 = m.row_ptr[i + 1];
+      if (p0 == p1) continue;
+      const int u = q % kG;
+      if (u == 0) o << "        case " << q / kG << ":";
+      o << " { double& mu_ = mu[" << u << "]; double& s2_ = s2[" << u << "]; sp[" << u << "] = " << i << "; g[" << u
+        << "] = " << dlit(m.g[i]) << "; nt += " << 4 * (p1 - p0) << ";";
+      for (int p = p0; p < p1; ++p) {
+        std::string t = tau_terms(m.row_delta[p], m.row_reaction[p]);
+        for (size_t k; (k = t.find("mu = __d")) != std::string::npos;) t.replace(k, 8, "mu_ = __d");
+        for (size_t k; (k = t.find("s2 = __d")) != std::string::npos;) t.replace(k, 8, "s2_ = __d");
+        for (size_t k; (k = t.find("(mu, ")) != std::string::npos;) t.replace(k, 5, "(mu_, ");
+        for (size_t k; (k = t.find("(s2, ")) != std::string::npos;) t.replace(k, 5, "(s2_, ");
+        o << t;
+      }
+      o << " }";
+      ++q;
+      if (q % kG == 0 || q == n_act) o << " break;\n";
+    }
+    o << "      }\n      if (kCount) flops += nt;\n"
+         "#pragma unroll\n      for (int u = 0; u < " << kG << "; ++u)\n"
+         "        if (!(mu[u] == 0.0 && s2[u] == 0.0)) tau = tau_bound<kCount>(tau, eps, xv(sp[u]), g[u], mu[u], s2[u], flops);\n"
+         "    }\n";
   } else {
     o << "#pragma unroll 1\n    for (int q = 0; q < " << n_act << "; ++q) {\n"
          "      double mu = 0.0, s2 = 0.0, g = 1.0; int sp = 0, nt = 0;\n      switch (q) {\n";
