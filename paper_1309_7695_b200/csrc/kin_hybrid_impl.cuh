@@ -450,7 +450,9 @@ cudaError_t launch_k(const KinTables& T, const KinSweepDev& S, const KinOutDev& 
   uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
   if (S.gstate && resident > S.gstate_warps) resident = S.gstate_warps;
   KinSweepDev SW = S;
-  SW.warp_lanes = 32;  // uniform step work per simulation: full warps (fewer lanes measured 1.56x slower)
+  // uniform step work per simulation: full warps (fewer lanes measured 1.56x
+  // slower); a sweep's variant may request another width (study / tests)
+  SW.warp_lanes = S.warp_lanes > 0 ? S.warp_lanes : 32;
   const uint64_t warps = (S.n_local + SW.warp_lanes - 1) / SW.warp_lanes;
   const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
   e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);

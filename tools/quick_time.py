@@ -48,7 +48,10 @@ print("fp64 peak TFLOP/s", peak.value, flush=True)
 import os
 for name in names:
     base, _, mode = name.partition(":")
-    lanes, rng = 0, None
+    lanes, rng, variant = 0, None, 0
+    if "%" in base:  # name%W: warp lanes W (KIN_VARIANT_WARP_LANES)
+        base, _, w = base.partition("%")
+        variant = int(w) << 8
     if "[" in base:  # name[a-b]: simulations a..b-1 only
         base, _, r = base.partition("[")
         rng = tuple(int(v) for v in r.rstrip("]").split("-"))
@@ -56,7 +59,7 @@ for name in names:
         mode, lanes = mode.split("@")
     net, cfg = cfgs[base]
     d, keep = make_sweep_desc(net, cfg, rng_mode=abi.RNG_PHILOX if mode == "philox" else abi.RNG_COMPAT,
-                              lanes_per_sim=int(lanes), sim_range=rng)
+                              lanes_per_sim=int(lanes), sim_range=rng, variant=variant)
     h = eng.model(net)
     # counting pass
     rc = lib.kin_sweep_launch(eng.ctx, h, C.byref(d), 0, 0, 1, C.byref(err)); assert rc == 0, err.text()
