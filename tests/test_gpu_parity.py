@@ -232,6 +232,44 @@ def test_jit_kernel_bit_exact(engine, oracle, case):
     assert_bit_exact(ref, got, work=bool(kw.get("want_work")))
 
 
+@pytest.mark.parametrize("case", ["c2_philox", "c2_taufixed", "c1_tau", "schlogl_ssa"])
+def test_jit_small_model_flat_loop_bit_exact(engine, oracle, case):
+    """Small models (M <= 8) run the JIT kernel's flat decision/event loop with
+    branch-free SSA events (predicated selection, delta select chains, full
+    propensity refresh): same trajectories, meta and work counts as the
+    oracle in both RNG modes and every method kind."""
+    kw = dict(want_work=True, variant=abi.VARIANT_JIT)
+    if case.startswith("c2"):
+        net, cfg = W.c2_config()
+        kw["sim_range"] = (9500, 9756)  # includes the sweep's longest (SSA-dominated) simulations
+        if case == "c2_philox":
+            kw["rng_mode"], kw["lanes_per_sim"] = abi.RNG_PHILOX, 1
+        else:
+            cfg.method = Method(MethodKind.TauFixed, tau=0.01)
+    elif case == "c1_tau":
+        net, cfg = W.c1_config(MethodKind.TauAdaptive, side=16)
+    else:
+        net, cfg = W.c2_config(points=4, runs=64)
+        cfg.method = Method(MethodKind.Ssa)
+    ref, got = both(engine, oracle, net, cfg, **kw)
+    assert_bit_exact(ref, got, work=True)
+
+
+@pytest.mark.parametrize("kind", [MethodKind.Ssa, MethodKind.TauAdaptive])
+def test_jit_small_model_budget_inside_burst(engine, oracle, kind):
+    """A step budget that runs out inside an SSA burst of the flat loop: the
+    same failing simulation (lowest index) as the oracle."""
+    net, cfg = W.c2_config(points=4, runs=64)
+    cfg.method = Method(kind, integrator=IntegratorConfig(max_steps=1500))
+    d, keep = make_sweep_desc(net, cfg, variant=abi.VARIANT_JIT)
+    ref = oracle.sweep(net, d, raise_on_error=False)
+    assert ref["rc"] == abi.KIN_ERR_SIMULATION
+    with pytest.raises(SimulationError) as ei:
+        engine.sweep(net, cfg, variant=abi.VARIANT_JIT)
+    assert ei.value.sim_index == ref["error"].sim_index
+    assert ei.value.sim_status == 1  # KIN_SIM_BUDGET
+
+
 def _launch_kernel_ms(engine, net, d, reps=3):
     import ctypes as C
     lib, err, h = engine.lib, abi.KinError(), engine.model(net)
