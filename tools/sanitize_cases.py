@@ -70,6 +70,15 @@ def main():
     run(eng, "dopri5 C4 slice", net, cfg, sim_range=(0, 256))
     net, cfg = W.c2_config(points=2, runs=16)
     run(eng, "C2 order-3 tau", net, cfg, want_stats=True)
+    # small-model JIT: flat decision/event loop, branch-free SSA events
+    run(eng, "C2 jit flat loop", net, cfg, V.VARIANT_JIT, want_work=True)
+    run(eng, "C2 jit flat loop philox", net, cfg, V.VARIANT_JIT, rng_mode=abi.RNG_PHILOX, lanes_per_sim=1)
+    # large-model JIT (grouped select_tau, chunked SSA selection, split state)
+    net, cfg = W.c5_config(n_grid=5)
+    run(eng, "C5 jit split state", net, cfg, V.VARIANT_JIT, sim_range=(0, 64))
+    # Dopri5 with 32-lane groups and the work-balancing slot orders
+    net, cfg = W.c5_config(method=MethodKind.Ode, n_grid=5)
+    run(eng, "dopri5 C5 L=32 slice", net, cfg, sim_range=(0, 16))
     # the device unit seams
     U = eng.UNIT_PROPENSITIES
     bd = W.birth_death(lam=5.0, c=1.0)
@@ -89,6 +98,19 @@ def main():
     run(eng2, "two-slot stats-only", net, cfg, output_mode=abi.OUTPUT_STATS_ONLY, want_stats=True)
     net, cfg = W.c1_config(MethodKind.TauAdaptive, side=4)
     run(eng2, "two-slot cut range", net, cfg, sim_range=(3, 13), want_stats=True)
+    # async jobs on both compute streams (and their two copy streams)
+    outs, tickets = [], []
+    for k in range(3):
+        S = 16
+        o = {"traj": np.zeros((S, len(cfg.grid), net.species_count())), "meta": np.zeros((S, 6), np.uint64),
+             "status": np.zeros(S, np.int32), "mean": np.zeros((16, len(cfg.grid), net.species_count())),
+             "m2": np.zeros((16, len(cfg.grid), net.species_count()))}
+        outs.append(o)
+        tickets.append(eng2.submit(net, cfg, o))
+    for t, o in zip(tickets, outs):
+        eng2.wait(t)
+        assert (o["status"] == 0).all() and np.isfinite(o["traj"]).all()
+    print("ok async jobs on two streams", flush=True)
     eng2.close()
     print("sanitize cases: all ran")
 
