@@ -19,6 +19,7 @@
 #include <unistd.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -195,10 +196,12 @@ std::string generate_policy(const JitModel& m) {
     // four species per trip: their row sums formed together (one switch
     // dispatch per four species, the loads of all four rows in flight —
     // global memory on large models), then four tau_bound in species order
-    constexpr int kG = 4;
+    const int kG = std::max(1, std::min(16, jit_knob("KIN_JIT_TAU_GROUP", 4)));
     const int n_grp = (n_act + kG - 1) / kG;
+    std::string ones = "1.0";
+    for (int u = 1; u < kG; ++u) ones += ", 1.0";
     o << "#pragma unroll 1\n    for (int q = 0; q < " << n_grp << "; ++q) {\n"
-         "      double mu[" << kG << "] = {}, s2[" << kG << "] = {}, g[" << kG << "] = {1.0, 1.0, 1.0, 1.0};\n"
+         "      double mu[" << kG << "] = {}, s2[" << kG << "] = {}, g[" << kG << "] = {" << ones << "};\n"
          "      int sp[" << kG << "] = {}, nt = 0;\n      switch (q) {\n";
     int q = 0;
     for (int i = 0; i < m.n; ++i) {
