@@ -85,3 +85,21 @@ def test_random_network_bit_exact(engine, oracle, case, kind, kernel):
     assert engine.lib.kin_sweep_sync(engine.ctx, 0, C.byref(err)) == 0, err.text()
     name = engine.lib.kin_sweep_kernel_name(engine.ctx, 0).decode()
     assert name == ("kin_jit_stoch" if kernel == "jit" else "stochastic_kernel"), name
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"s{c[0]}_n{c[1]}_m{c[2]}_o{c[3]}_x{c[4]}" for c in CASES])
+@pytest.mark.parametrize("mode", ["philox", "binomial", "binomial_philox"])
+def test_random_network_rng_and_firing_modes(engine, oracle, case, mode):
+    """The same networks with Philox streams (thread-per-simulation JIT) and
+    with binomial firing: bit-exact against the oracle's same mode."""
+    net = random_network(*case)
+    method = Method(MethodKind.TauAdaptive)
+    if mode.startswith("binomial"):
+        method.firing = abi.FIRING_BINOMIAL
+    cfg = SweepConfig([SweepAxis("k_sweep", [0.5, 1.0, 2.0, 4.0])], 16, method, 2000 + case[0], 1.0,
+                      uniform_grid(1.0, 11))
+    kw = dict(want_work=True, variant=abi.VARIANT_JIT)
+    if mode.endswith("philox"):
+        kw.update(rng_mode=abi.RNG_PHILOX, lanes_per_sim=1)
+    ref, got = both(engine, oracle, net, cfg, **kw)
+    assert_bit_exact(ref, got, work=True)
