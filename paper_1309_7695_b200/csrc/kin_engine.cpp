@@ -932,8 +932,17 @@ int launch_sim(Slot& sl, Buffers& bf, const kin_model* model, const kin_sweep_de
     // global 100.4 ms.)
     if (pick_gstate(kin::hybrid_smem_bytes(T, SD) > 48 * 1024, ov.hybrid_gstate))
       if (int rc = global_state_for(kin::hybrid_state_doubles_per_warp(T, SD))) return rc;
-    e = kin::launch_hybrid(T, SD, O, want_work, bf.counter.p, bf.st);
-    bf.kernel_name = "hybrid_kernel";
+    // the per-model JIT variant (straight-line propensities and row sums) for
+    // the launches the JIT rule takes (>= 8,192 simulations, or forced)
+    bool used = false;
+    const int force_jit = (var & KIN_VARIANT_TABLE) ? 0 : ((var & KIN_VARIANT_JIT) ? 1 : -1);
+    if (kin::jit_wanted(S, force_jit)) {
+      const kin::JitModel& jm = jit_model_cached(model, d);
+      e = kin::launch_hybrid_jit(jm, T, SD, O, want_work, bf.counter.p, SD.gstate ? 0 : kin::hybrid_smem_bytes(T, SD),
+                                 bf.st, &used);
+    }
+    if (e == cudaSuccess && !used) e = kin::launch_hybrid(T, SD, O, want_work, bf.counter.p, bf.st);
+    bf.kernel_name = used ? "kin_jit_hybrid" : "hybrid_kernel";
   } else if (kind == KIN_METHOD_CLE) {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
     e = kin::launch_cle(T, SD, O, want_work, bf.counter.p, bf.st);
@@ -1849,7 +1858,11 @@ int kin_jit_check(const kin_model_desc* desc, const kin_sweep_desc* sweep, char*
   if (!sweep) { set_err(err, KIN_ERR_USAGE, "null sweep"); return KIN_ERR_USAGE; }
   const kin::JitModel jm = jit_model(H, sweep);
   std::string lg;
-  const bool ok = kin::jit_compile_check(jm, false, sweep->rng_mode == KIN_RNG_PHILOX, true, &lg);
+  // the method's JIT kernel: the hybrid PDMP kernel for KIN_METHOD_HYBRID,
+  // else the stochastic (SSA / tau-leaping) kernel
+  const bool philox = sweep->rng_mode == KIN_RNG_PHILOX;
+  const bool ok = sweep->method.kind == KIN_METHOD_HYBRID ? kin::jit_compile_check_hybrid(jm, false, philox, &lg)
+                                                          : kin::jit_compile_check(jm, false, philox, true, &lg);
   if (log && log_cap > 0) std::snprintf(log, static_cast<size_t>(log_cap), "%s", lg.c_str());
   if (!ok) { set_err(err, KIN_ERR_INPUT, "NVRTC compilation of the model kernel failed"); return KIN_ERR_INPUT; }
   return KIN_OK;

@@ -20,9 +20,11 @@
 // straight-line behind a warp-uniform switch) so the RHS (propensities +
 // fast/slow sums) is inlined once, not six times (instruction-cache footprint).
 #pragma once
+#ifndef __CUDACC_RTC__
 #include "kin_launch.h"
+#endif
+#include "kin_stochastic_impl.cuh"  // (first: it brings the fixed-width types NVRTC lacks)
 #include "kin_pmath.cuh"
-#include "kin_stochastic_impl.cuh"
 
 namespace kin {
 namespace hyb {
@@ -55,11 +57,14 @@ __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : 
 
 // kN > 0: species count fixed at compile time (small models: loops over the
 // N+1 components unroll); kN = 0: runtime T.n.
-template <bool kCount, int kN>
+// PM: the propensity / row-sum policy — TableModel (walks the packed tables)
+// or the per-model JIT's GenModel<double> (straight-line code, kin_jit.cpp):
+// the same operations in the same order either way.
+template <bool kCount, int kN, class PM>
 struct Hybrid {
   const KinTables& T;
   const KinSweepDev& S;
-  TableModel<double, kBlock> sm;  // propensities over y (x = y[0..n-1])
+  PM sm;  // propensities over y (x = y[0..n-1])
   int n_rt, m, n1_rt;
   __device__ __forceinline__ int N() const { return kN > 0 ? kN : n_rt; }
   __device__ __forceinline__ int N1() const { return kN > 0 ? kN + 1 : n1_rt; }
@@ -73,31 +78,10 @@ struct Hybrid {
 
   // augmented RHS: f = (sum_fast nu a (row order), sum_slow a) at state `yv`
   __device__ void rhs(int yv, int fv) {
-    TableModel<double, kBlock> st{T, vp(yv), sm.a, sm.av};
-#pragma unroll 1
-    for (int j = 0; j < m; ++j) sm.a[j * kBlock] = st.prop(j);
-    if (kCount) flops += static_cast<uint64_t>(T.fprop);
-    for (int i = 0; i < N(); ++i) {
-      double acc = 0.0;
-      const int p1 = tab_row_ptr(T, i + 1), p0 = tab_row_ptr(T, i);
-#pragma unroll 1
-      for (int p = p0; p < p1; ++p) {
-        const uint32_t e = tab_row(T, p);
-        const int j = KIN_NU_INDEX(e);
-        const double t = acc + static_cast<double>(KIN_NU_DELTA(e)) * sm.a[j * kBlock];
-        acc = slow(j) ? acc : t;  // a select, not a branch per entry (same value as the oracle's skip)
-      }
-      v(fv, i) = acc;
-      if (kCount) flops += 2 * static_cast<uint64_t>(p1 - p0);
-    }
-    double g = 0.0;
-#pragma unroll 1
-    for (int j = 0; j < m; ++j) {
-      const double t = g + sm.a[j * kBlock];
-      g = slow(j) ? t : g;
-    }
-    v(fv, N()) = g;
-    if (kCount) flops += static_cast<uint64_t>(m);
+    PM st{T, vp(yv), sm.a, sm.av};
+    st.props_only();
+    if (kCount) flops += static_cast<uint64_t>(T.fprop) + 2 * static_cast<uint64_t>(T.nnz) + static_cast<uint64_t>(m);
+    st.hyb_rows(slowm, vp(fv), N());
   }
 
 };
@@ -160,13 +144,13 @@ struct Dense5 {
   }
 };
 
-template <bool kCount, bool kPhilox, int kN>
+template <bool kCount, bool kPhilox, int kN, class PM>
 __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, uint64_t s,
                                     double* V, double* a, double* av, uint32_t* slowm) {
   constexpr int B = kBlock;
   const uint64_t sim = global_sim(S, s);
   const int n = kN > 0 ? kN : T.n, m = T.m, G = T.n_grid, n1 = n + 1;
-  Hybrid<kCount, kN> H{T, S, TableModel<double, kBlock>{T, V, a, av}, T.n, m, T.n + 1, V, slowm};
+  Hybrid<kCount, kN, PM> H{T, S, PM{T, V, a, av}, T.n, m, T.n + 1, V, slowm};
   stoch::init_state<double, kBlock>(T, S, sim, n, V, av);  // y[0..n-1] = x0 (vector Y is the first)
   const uint64_t seed = sim_seed(S, sim);
   Xoshiro rng;
@@ -407,10 +391,9 @@ __host__ __device__ __forceinline__ size_t hybrid_warp_doubles(const KinTables& 
   return (static_cast<size_t>(kVecs) * (T.n + 1) + T.m + S.n_axes) * kBlock + (words * kBlock + 1) / 2;
 }
 
-template <bool kCount, bool kPhilox, bool kGlobal, int kN>
-__global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ KinTables T,
-                                                        const __grid_constant__ KinSweepDev S, KinOutDev O,
-                                                        unsigned long long* __restrict__ next) {
+template <bool kCount, bool kPhilox, bool kGlobal, int kN, class PM>
+__device__ __forceinline__ void hybrid_body(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                                            unsigned long long* __restrict__ next) {
   extern __shared__ double smem[];
   constexpr int B = kBlock;
   const int tid = threadIdx.x, lane = tid & 31;
@@ -427,10 +410,19 @@ __global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ 
     base = __shfl_sync(0xFFFFFFFFu, base, 0);
     if (base >= S.n_local) break;
     const uint64_t s = lane < S.warp_lanes ? base + lane : S.n_local;  // lanes >= warp_lanes idle
-    if (s < S.n_local) simulate_hybrid_one<kCount, kPhilox, kN>(T, S, O, s, V, a, av, slowm);
+    if (s < S.n_local) simulate_hybrid_one<kCount, kPhilox, kN, PM>(T, S, O, s, V, a, av, slowm);
     __syncwarp();
   }
 }
+
+template <bool kCount, bool kPhilox, bool kGlobal, int kN>
+__global__ void __launch_bounds__(kBlock) hybrid_kernel(const __grid_constant__ KinTables T,
+                                                        const __grid_constant__ KinSweepDev S, KinOutDev O,
+                                                        unsigned long long* __restrict__ next) {
+  hybrid_body<kCount, kPhilox, kGlobal, kN, TableModel<double, kBlock>>(T, S, O, next);
+}
+
+#ifndef __CUDACC_RTC__
 
 
 // Host launcher of one kernel variant (explicitly instantiated across several
@@ -464,6 +456,7 @@ cudaError_t launch_k(const KinTables& T, const KinSweepDev& S, const KinOutDev& 
 #define KIN_HYB_SIG(kc, kp, kg, kn)                                                                           \
   cudaError_t launch_k<kc, kp, kg, kn>(const KinTables&, const KinSweepDev&, const KinOutDev&, unsigned long long*, \
                                        size_t, cudaStream_t)
+#endif  // __CUDACC_RTC__
 
 }  // namespace hyb
 }  // namespace kin

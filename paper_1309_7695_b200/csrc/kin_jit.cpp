@@ -316,6 +316,32 @@ std::string generate_policy(const JitModel& m) {
     << "#pragma unroll\n    for (int i = 0; i < " << m.n << "; ++i) neg |= x[i * B] < static_cast<XT>(0);\n"
     << "    return neg;\n  }\n";
   o << "  __device__ __forceinline__ int col_len(int j) const { return tab_col_ptr(T, j + 1) - tab_col_ptr(T, j); }\n";
+  // hybrid PDMP (kin_hybrid_impl.cuh; TableModel::props_only / hyb_rows):
+  // straight-line propensities and row sums, the slow-set words read once
+  o << "  __device__ __forceinline__ void props_only() const {\n";
+  for (int j = 0; j < m.m; ++j) o << "    a[" << j << " * B] = prop(" << j << ");\n";
+  o << "  }\n";
+  o << "  __device__ __forceinline__ void hyb_rows(const uint32_t* slowm, double* f, int) const {\n";
+  const int words = (m.m + 31) / 32;
+  for (int w = 0; w < words; ++w) o << "    const uint32_t w" << w << " = slowm[" << w << " * B];\n";
+  auto slow = [](int j) { return "((w" + std::to_string(j >> 5) + " >> " + std::to_string(j & 31) + ") & 1u)"; };
+  for (int i = 0; i < m.n; ++i) {
+    o << "    { double acc = 0.0;";
+    for (int p = m.row_ptr[i]; p < m.row_ptr[i + 1]; ++p) {
+      const int j = m.row_reaction[p], d = m.row_delta[p];
+      const std::string aj = "a[" + std::to_string(j) + " * B]";
+      std::string t;
+      if (d == 1) t = "__dadd_rn(acc, " + aj + ")";
+      else if (d == -1) t = "__dsub_rn(acc, " + aj + ")";
+      else t = "__dadd_rn(acc, __dmul_rn(" + dlit(d) + ", " + aj + "))";
+      o << " { const double t = " << t << "; acc = " << slow(j) << " ? acc : t; }";
+    }
+    o << " f[" << i << " * B] = acc; }\n";
+  }
+  o << "    double g = 0.0;\n";
+  for (int j = 0; j < m.m; ++j)
+    o << "    { const double t = __dadd_rn(g, a[" << j << " * B]); g = " << slow(j) << " ? t : g; }\n";
+  o << "    f[" << m.n << " * B] = g;\n  }\n";
   o << "};\n}}  // namespace kin::stoch\n";
   return o.str();
 }
@@ -324,14 +350,25 @@ const char* const kNvrtcOpts[5] = {"--gpu-architecture=sm_100a", "-fmad=false", 
                                    "-default-device"};
 
 // NVRTC: policy source -> sm_100a cubin.  Returns false with the log on error.
+// hyb_kn >= 0: the hybrid PDMP kernel (kin_jit_hybrid) specialised on that
+// species count (0 = runtime), else the stochastic kernel (kin_jit_stoch).
 bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_state, bool global_state,
-                   bool smem_x, int firing, std::vector<char>* cubin, std::string* log) {
-  std::string src = "#include \"kin_stochastic_impl.cuh\"\n" + policy +
-                    "extern \"C\" __global__ void __launch_bounds__(KIN_STOCH_BLOCK, KMINB_) kin_jit_stoch(\n"
-                    "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
-                    "    unsigned long long* __restrict__ next, int* ovf) {\n"
-                    "  kin::stoch::stochastic_body<kin::stoch::GenModel<XT_>, KCOUNT_, KPHILOX_, XT_, KGLOBAL_, KSMEMX_>(T, S, O, next, ovf);\n"
-                    "}\n";
+                   bool smem_x, int firing, std::vector<char>* cubin, std::string* log, int hyb_kn) {
+  std::string src =
+      hyb_kn >= 0
+          ? "#include \"kin_hybrid_impl.cuh\"\n" + policy +
+                "extern \"C\" __global__ void __launch_bounds__(32) kin_jit_hybrid(\n"
+                "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
+                "    unsigned long long* __restrict__ next) {\n"
+                "  kin::hyb::hybrid_body<KCOUNT_, KPHILOX_, KGLOBAL_, " + std::to_string(hyb_kn) +
+                ", kin::stoch::GenModel<double>>(T, S, O, next);\n"
+                "}\n"
+          : "#include \"kin_stochastic_impl.cuh\"\n" + policy +
+                "extern \"C\" __global__ void __launch_bounds__(KIN_STOCH_BLOCK, KMINB_) kin_jit_stoch(\n"
+                "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
+                "    unsigned long long* __restrict__ next, int* ovf) {\n"
+                "  kin::stoch::stochastic_body<kin::stoch::GenModel<XT_>, KCOUNT_, KPHILOX_, XT_, KGLOBAL_, KSMEMX_>(T, S, O, next, ovf);\n"
+                "}\n";
   std::vector<const char*> hs, hn;
   for (const auto& h : kJitHeaders) {
     hn.push_back(h.name);
@@ -439,26 +476,28 @@ void write_file(const std::string& p, const std::vector<char>& data) {
 }
 
 // Variant part of a kernel's cache key.
-std::string variant_key(bool count, bool philox, bool int_state, bool global_state, bool smem_x, int firing) {
+std::string variant_key(bool count, bool philox, bool int_state, bool global_state, bool smem_x, int firing,
+                        int hyb_kn = -1) {
   return std::string(count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
          (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S") +
-         (firing ? "B" : "");
+         (firing ? "B" : "") + (hyb_kn >= 0 ? "Y" + std::to_string(hyb_kn) : "");
 }
 
 std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool philox, bool int_state,
-                                   bool global_state, bool smem_x, int firing) {
+                                   bool global_state, bool smem_x, int firing, int hyb_kn = -1) {
   auto jk = std::make_shared<JitKernel>();
   std::vector<char> cubin;
-  const std::string path = cache_path(policy + variant_key(count, philox, int_state, global_state, smem_x, firing));
+  const std::string path =
+      cache_path(policy + variant_key(count, philox, int_state, global_state, smem_x, firing, hyb_kn));
   if (!read_file(path, &cubin)) {
-    if (!nvrtc_compile(policy, count, philox, int_state, global_state, smem_x, firing, &cubin, &jk->log)) {
+    if (!nvrtc_compile(policy, count, philox, int_state, global_state, smem_x, firing, &cubin, &jk->log, hyb_kn)) {
       if (jit_debug()) std::fprintf(stderr, "[kin_jit] compile failed:\n%s\n", jk->log.c_str());
       return jk;
     }
     write_file(path, cubin);
   }
   if (cudaLibraryLoadData(&jk->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
-      cudaLibraryGetKernel(&jk->kern, jk->lib, "kin_jit_stoch") != cudaSuccess) {
+      cudaLibraryGetKernel(&jk->kern, jk->lib, hyb_kn >= 0 ? "kin_jit_hybrid" : "kin_jit_stoch") != cudaSuccess) {
     jk->log += "\ncudaLibraryLoadData/GetKernel failed";
     cudaGetLastError();
     return jk;
@@ -479,7 +518,67 @@ size_t gstate_live_doubles(const KinTables& T, const KinSweepDev& S, bool x_in_s
 
 bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log) {
   std::vector<char> cubin;
-  return nvrtc_compile(generate_policy(model), count, philox, int_state, false, false, 0, &cubin, log);
+  return nvrtc_compile(generate_policy(model), count, philox, int_state, false, false, 0, &cubin, log, -1);
+}
+
+int hybrid_jit_kn(const JitModel& model) { return model.n <= 8 ? model.n : 0; }
+
+bool jit_compile_check_hybrid(const JitModel& model, bool count, bool philox, std::string* log) {
+  std::vector<char> cubin;
+  return nvrtc_compile(generate_policy(model), count, philox, false, false, false, 0, &cubin, log,
+                       hybrid_jit_kn(model));
+}
+
+cudaError_t launch_hybrid_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                              bool count, unsigned long long* counter, size_t smem, cudaStream_t stream,
+                              bool* used) {
+  *used = false;
+  if (S.n_local == 0) {
+    *used = true;
+    return cudaSuccess;
+  }
+  const bool philox = S.rng_mode == KIN_RNG_PHILOX;
+  const std::string policy = model.policy.empty() ? generate_policy(model) : model.policy;
+  const bool global_state = S.gstate != nullptr;
+  const int kn = hybrid_jit_kn(model);
+  const std::string key = policy + variant_key(count, philox, false, global_state, false, 0, kn);
+  std::shared_ptr<JitKernel> jk;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+      jk = it->second;
+    } else {
+      jk = compile(policy, count, philox, false, global_state, false, 0, kn);
+      g_cache[key] = jk;
+    }
+  }
+  if (!jk->ok) return cudaSuccess;  // caller falls back to the table-driven kernel
+  if (smem > 227 * 1024) return cudaSuccess;
+  const void* fn = reinterpret_cast<const void*>(jk->kern);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaSuccess;
+  uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  if (S.gstate && S.gstate_warps < resident) resident = S.gstate_warps;
+  KinSweepDev SW = S;
+  SW.warp_lanes = S.warp_lanes > 0 ? S.warp_lanes : 32;  // as the table-driven hybrid kernel
+  const uint64_t warps = (S.n_local + SW.warp_lanes - 1) / SW.warp_lanes;
+  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  KinTables* Tp = const_cast<KinTables*>(&T);
+  KinSweepDev* Sp = &SW;
+  KinOutDev Oc = O;
+  void* args[] = {Tp, Sp, &Oc, &counter};
+  e = cudaLaunchKernel(fn, dim3(grid), dim3(32), args, smem, stream);
+  if (e == cudaSuccess) *used = true;
+  return e;
 }
 
 // KIN_JIT=0: never; KIN_JIT=1: always; unset: launches of >= 8,192

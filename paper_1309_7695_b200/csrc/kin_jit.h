@@ -32,6 +32,11 @@ bool jit_wanted(uint64_t n_sims, int force = -1);
 
 // Generate + NVRTC-compile the policy without loading it (no GPU needed).
 bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log);
+// the hybrid PDMP kernel specialised per model (kin_hybrid_impl.cuh with the
+// generated GenModel<double> as its propensity / row-sum policy)
+bool jit_compile_check_hybrid(const JitModel& model, bool count, bool philox, std::string* log);
+cudaError_t launch_hybrid_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                              bool count, unsigned long long* counter, size_t smem, cudaStream_t stream, bool* used);
 
 // Launch the specialised kernel; *used = false means "not available" (NVRTC
 // failure or unsupported configuration): the caller launches the table kernel.

@@ -103,6 +103,36 @@ struct TableModel {
     for (int j = 0; j < M; ++j) a0 = __dadd_rn(a0, aval(j));
     return a0;
   }
+  // hybrid PDMP (kin_hybrid_impl.cuh): a[] at x, without the sum
+  __device__ __forceinline__ void props_only() const {
+#pragma unroll 1
+    for (int j = 0; j < T.m; ++j) a[j * B] = prop(j);
+  }
+  // hybrid PDMP: f_i = sum over the fast reactions of nu_ij a_j (row order),
+  // f_N = sum over the slow ones of a_j (reaction order); slow(j) = bit j of
+  // the per-lane mask words slowm[w * B]
+  __device__ __forceinline__ void hyb_rows(const uint32_t* slowm, double* f, int n) const {
+    auto slow = [&](int j) { return ((slowm[(j >> 5) * B] >> (j & 31)) & 1u) != 0u; };
+    for (int i = 0; i < n; ++i) {
+      double acc = 0.0;
+      const int p1 = tab_row_ptr(T, i + 1), p0 = tab_row_ptr(T, i);
+#pragma unroll 1
+      for (int p = p0; p < p1; ++p) {
+        const uint32_t e = tab_row(T, p);
+        const int j = KIN_NU_INDEX(e);
+        const double t = acc + static_cast<double>(KIN_NU_DELTA(e)) * a[j * B];
+        acc = slow(j) ? acc : t;  // a select, not a branch per entry (same value as the oracle's skip)
+      }
+      f[i * B] = acc;
+    }
+    double g = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < T.m; ++j) {
+      const double t = g + a[j * B];
+      g = slow(j) ? t : g;
+    }
+    f[n * B] = g;
+  }
   // x += nu[:, j] * k  (k signed: negative undoes a rejected leap)
   __device__ __forceinline__ void apply(int j, long long k, bool& ovf) const {
     const int p1 = tab_col_ptr(T, j + 1);

@@ -41,6 +41,42 @@ def test_hybrid_bit_exact_vs_oracle(engine, oracle, rng_mode):
     assert np.array_equal(fast["traj"], ref["traj"]) and np.array_equal(fast["meta"], ref["meta"])
 
 
+@pytest.mark.parametrize("case", ["c1", "c1_philox", "c2_order3", "c4", "c1_work"])
+def test_hybrid_jit_kernel_bit_exact(engine, oracle, case):
+    """The per-model JIT hybrid kernel (kin_jit_hybrid: straight-line
+    propensities and row sums from the generated policy, the same operations
+    in the same order) against the oracle — and the kernel that ran is the JIT
+    one (a failed compilation would fall back to the table kernel)."""
+    import ctypes as C
+    kw = dict(variant=abi.VARIANT_JIT)
+    want_work = case == "c1_work"
+    if case.startswith("c1"):
+        net, cfg = W.c1_config(MethodKind.Hybrid, side=16)
+        cfg.method = hybrid()
+        if case == "c1_philox":
+            kw["rng_mode"] = abi.RNG_PHILOX
+    elif case == "c2_order3":
+        net, cfg = W.c2_config(points=4, runs=16)
+        cfg.method = hybrid(theta_x=50.0, theta_a=5.0, repartition_interval=0.5)
+    else:  # 33 species: the runtime-N (kN = 0) specialisation
+        net, cfg = W.c4_config()
+        cfg.method = hybrid()
+        kw["sim_range"] = (1000, 1064)
+    d, keep = make_sweep_desc(net, cfg, **kw)
+    ref = oracle.sweep(net, d, want_traj=True, want_work=want_work)
+    got = engine.sweep(net, cfg, want_traj=True, want_work=want_work, **kw)
+    assert np.array_equal(ref["status"], got["status"])
+    assert np.array_equal(ref["meta"], got["meta"])
+    if want_work:
+        assert np.array_equal(ref["work"], got["work"])
+    diff = np.argwhere(ref["traj"] != got["traj"])
+    assert diff.size == 0, f"{len(diff)} samples differ, first {diff[:3].tolist()}"
+    err = abi.KinError()
+    assert engine.lib.kin_sweep_launch(engine.ctx, engine.model(net), C.byref(d), 0, 0, 0, C.byref(err)) == 0
+    assert engine.lib.kin_sweep_sync(engine.ctx, 0, C.byref(err)) == 0, err.text()
+    assert engine.lib.kin_sweep_kernel_name(engine.ctx, 0).decode() == "kin_jit_hybrid"
+
+
 def test_hybrid_swept_thresholds_and_order3(engine, oracle):
     net, cfg = W.c2_config(points=2, runs=8)
     cfg.method = hybrid(theta_x=50.0, theta_a=5.0, repartition_interval=0.5)
