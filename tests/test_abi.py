@@ -75,16 +75,20 @@ def test_missing_library_fails_loudly(tmp_path):
         abi.load_library(tmp_path / "nope.so")
 
 
-@pytest.mark.parametrize("which", ["c1", "c2", "c4", "c5", "iso"])
+@pytest.mark.parametrize("which", ["c1", "c2", "c4", "c5", "iso", "c1_hybrid", "c4_hybrid"])
 def test_jit_kernel_compiles_without_gpu(which):
-    """The per-model specialised kernel source is generated and compiled by
-    NVRTC for sm_100a (no GPU needed)."""
+    """The per-model specialised kernel source (the stochastic kernel, or the
+    hybrid PDMP kernel for a hybrid sweep) is generated and compiled by NVRTC
+    for sm_100a (no GPU needed)."""
     import time
     from paper_1309_7695_b200 import workloads as W
     from paper_1309_7695_b200.ensemble import Method, MethodKind, SweepAxis, SweepConfig, make_sweep_desc
     if which == "iso":
         net = W.isomerization()
         cfg = SweepConfig([SweepAxis("kf", [1.0, 2.0])], 4, Method(MethodKind.Ssa), 1, 1.0, [0.0, 1.0])
+    elif which.endswith("_hybrid"):
+        net, cfg = getattr(W, f"{which[:2]}_config")()
+        cfg.method = Method(MethodKind.Hybrid, theta_x=100.0, theta_a=10.0)
     else:
         net, cfg = getattr(W, f"{which}_config")()
     d, keep = make_sweep_desc(net, cfg)
