@@ -5,7 +5,7 @@ from pathlib import Path
 out = Path(sys.argv[1])
 items = [("kin_stochastic_impl.cuh", "kin_stochastic_impl.cuh"), ("kin_device.cuh", "kin_device.cuh"),
          ("kin_tables.h", "kin_tables.h"), ("kin_pmath.cuh", "kin_pmath.cuh"),
-         ("kin_hybrid_impl.cuh", "kin_hybrid_impl.cuh"), ("../../include/kin_abi.h", "../../include/kin_abi.h")]
+         ("kin_hybrid_impl.cuh", "kin_hybrid_impl.cuh"), ("kin_lsoda_impl.cuh", "kin_lsoda_impl.cuh"), ("../../include/kin_abi.h", "../../include/kin_abi.h")]
 lines = ["struct JitHeader { const char* name; const char* text; };", "static const JitHeader kJitHeaders[] = {"]
 for name, path in items:
     text = Path(path).read_text()

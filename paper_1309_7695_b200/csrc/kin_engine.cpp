@@ -953,8 +953,17 @@ int launch_sim(Slot& sl, Buffers& bf, const kin_model* model, const kin_sweep_de
     // warp's state would take more than 48 KB of shared memory
     if (pick_gstate(kin::lsoda_smem_bytes(T, SD) > 48 * 1024, ov.lsoda_gstate))
       if (int rc = global_state_for(kin::lsoda_state_doubles_per_warp(T, SD))) return rc;
-    e = kin::launch_lsoda(T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, bf.st);
-    bf.kernel_name = "lsoda_kernel";
+    // the per-model JIT variant (straight-line RHS) for the launches the JIT
+    // rule takes (>= 8,192 simulations, or forced)
+    bool used = false;
+    const int force_jit = (var & KIN_VARIANT_TABLE) ? 0 : ((var & KIN_VARIANT_JIT) ? 1 : -1);
+    if (kin::jit_wanted(S, force_jit)) {
+      const kin::JitModel& jm = jit_model_cached(model, d);
+      e = kin::launch_lsoda_jit(jm, T, SD, O, sl.lsoda_co.p, want_work, bf.counter.p,
+                                SD.gstate ? 0 : kin::lsoda_smem_bytes(T, SD), bf.st, &used);
+    }
+    if (e == cudaSuccess && !used) e = kin::launch_lsoda(T, SD, O, want_work, sl.lsoda_co.p, bf.counter.p, bf.st);
+    bf.kernel_name = used ? "kin_jit_lsoda" : "lsoda_kernel";
   } else {
     KIN_CUDA(bf.counter.ensure(1), "cudaMalloc counter");
     KIN_CUDA(bf.ovf.ensure(1), "cudaMalloc overflow flag");
@@ -1862,7 +1871,8 @@ int kin_jit_check(const kin_model_desc* desc, const kin_sweep_desc* sweep, char*
   // else the stochastic (SSA / tau-leaping) kernel
   const bool philox = sweep->rng_mode == KIN_RNG_PHILOX;
   const bool ok = sweep->method.kind == KIN_METHOD_HYBRID ? kin::jit_compile_check_hybrid(jm, false, philox, &lg)
-                                                          : kin::jit_compile_check(jm, false, philox, true, &lg);
+                  : sweep->method.kind == KIN_METHOD_LSODA ? kin::jit_compile_check_lsoda(jm, false, &lg)
+                                                           : kin::jit_compile_check(jm, false, philox, true, &lg);
   if (log && log_cap > 0) std::snprintf(log, static_cast<size_t>(log_cap), "%s", lg.c_str());
   if (!ok) { set_err(err, KIN_ERR_INPUT, "NVRTC compilation of the model kernel failed"); return KIN_ERR_INPUT; }
   return KIN_OK;

@@ -342,6 +342,21 @@ std::string generate_policy(const JitModel& m) {
   for (int j = 0; j < m.m; ++j)
     o << "    { const double t = __dadd_rn(g, a[" << j << " * B]); g = " << slow(j) << " ? t : g; }\n";
   o << "    f[" << m.n << " * B] = g;\n  }\n";
+  o << "  static constexpr bool kJit = true;\n";
+  // LSODA (kin_lsoda_impl.cuh; rre_rhs): f_i = sum over the nu row of d * a_j
+  o << "  __device__ __forceinline__ void rre_rows(double* f, int) const {\n";
+  for (int i = 0; i < m.n; ++i) {
+    o << "    { double acc = 0.0;";
+    for (int p = m.row_ptr[i]; p < m.row_ptr[i + 1]; ++p) {
+      const int j = m.row_reaction[p], d = m.row_delta[p];
+      const std::string aj = "a[" + std::to_string(j) + " * B]";
+      if (d == 1) o << " acc = __dadd_rn(acc, " << aj << ");";
+      else if (d == -1) o << " acc = __dsub_rn(acc, " << aj << ");";
+      else o << " acc = __dadd_rn(acc, __dmul_rn(" << dlit(d) << ", " << aj << "));";
+    }
+    o << " f[" << i << " * B] = acc; }\n";
+  }
+  o << "  }\n";
   o << "};\n}}  // namespace kin::stoch\n";
   return o.str();
 }
@@ -350,17 +365,31 @@ const char* const kNvrtcOpts[5] = {"--gpu-architecture=sm_100a", "-fmad=false", 
                                    "-default-device"};
 
 // NVRTC: policy source -> sm_100a cubin.  Returns false with the log on error.
-// hyb_kn >= 0: the hybrid PDMP kernel (kin_jit_hybrid) specialised on that
-// species count (0 = runtime), else the stochastic kernel (kin_jit_stoch).
+// Which kernel a JIT variant is (`spec`): < 0 the stochastic kernel
+// (kin_jit_stoch); 0..99 the hybrid PDMP kernel (kin_jit_hybrid) specialised
+// on kN = spec species (0 = runtime); >= 100 the LSODA kernel (kin_jit_lsoda)
+// with kN = spec - 100.
+constexpr int kSpecLsoda = 100;
+const char* spec_kernel_name(int spec) {
+  return spec < 0 ? "kin_jit_stoch" : (spec < kSpecLsoda ? "kin_jit_hybrid" : "kin_jit_lsoda");
+}
 bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_state, bool global_state,
-                   bool smem_x, int firing, std::vector<char>* cubin, std::string* log, int hyb_kn) {
+                   bool smem_x, int firing, std::vector<char>* cubin, std::string* log, int spec) {
   std::string src =
-      hyb_kn >= 0
+      spec >= kSpecLsoda
+          ? "#include \"kin_stochastic_impl.cuh\"\n#include \"kin_lsoda_impl.cuh\"\n" + policy +
+                "extern \"C\" __global__ void __maxnreg__(200) kin_jit_lsoda(\n"
+                "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
+                "    const double* __restrict__ co, unsigned long long* __restrict__ next) {\n"
+                "  kin::lsd::lsoda_body<KCOUNT_, KGLOBAL_, " + std::to_string(spec - kSpecLsoda) +
+                ", kin::stoch::GenModel<double>>(T, S, O, co, next);\n"
+                "}\n"
+      : spec >= 0
           ? "#include \"kin_hybrid_impl.cuh\"\n" + policy +
                 "extern \"C\" __global__ void __launch_bounds__(32) kin_jit_hybrid(\n"
                 "    const __grid_constant__ KinTables T, const __grid_constant__ KinSweepDev S, KinOutDev O,\n"
                 "    unsigned long long* __restrict__ next) {\n"
-                "  kin::hyb::hybrid_body<KCOUNT_, KPHILOX_, KGLOBAL_, " + std::to_string(hyb_kn) +
+                "  kin::hyb::hybrid_body<KCOUNT_, KPHILOX_, KGLOBAL_, " + std::to_string(spec) +
                 ", kin::stoch::GenModel<double>>(T, S, O, next);\n"
                 "}\n"
           : "#include \"kin_stochastic_impl.cuh\"\n" + policy +
@@ -477,27 +506,27 @@ void write_file(const std::string& p, const std::vector<char>& data) {
 
 // Variant part of a kernel's cache key.
 std::string variant_key(bool count, bool philox, bool int_state, bool global_state, bool smem_x, int firing,
-                        int hyb_kn = -1) {
+                        int spec = -1) {
   return std::string(count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
          (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S") +
-         (firing ? "B" : "") + (hyb_kn >= 0 ? "Y" + std::to_string(hyb_kn) : "");
+         (firing ? "B" : "") + (spec >= 0 ? "Y" + std::to_string(spec) : "");
 }
 
 std::shared_ptr<JitKernel> compile(const std::string& policy, bool count, bool philox, bool int_state,
-                                   bool global_state, bool smem_x, int firing, int hyb_kn = -1) {
+                                   bool global_state, bool smem_x, int firing, int spec = -1) {
   auto jk = std::make_shared<JitKernel>();
   std::vector<char> cubin;
   const std::string path =
-      cache_path(policy + variant_key(count, philox, int_state, global_state, smem_x, firing, hyb_kn));
+      cache_path(policy + variant_key(count, philox, int_state, global_state, smem_x, firing, spec));
   if (!read_file(path, &cubin)) {
-    if (!nvrtc_compile(policy, count, philox, int_state, global_state, smem_x, firing, &cubin, &jk->log, hyb_kn)) {
+    if (!nvrtc_compile(policy, count, philox, int_state, global_state, smem_x, firing, &cubin, &jk->log, spec)) {
       if (jit_debug()) std::fprintf(stderr, "[kin_jit] compile failed:\n%s\n", jk->log.c_str());
       return jk;
     }
     write_file(path, cubin);
   }
   if (cudaLibraryLoadData(&jk->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess ||
-      cudaLibraryGetKernel(&jk->kern, jk->lib, hyb_kn >= 0 ? "kin_jit_hybrid" : "kin_jit_stoch") != cudaSuccess) {
+      cudaLibraryGetKernel(&jk->kern, jk->lib, spec_kernel_name(spec)) != cudaSuccess) {
     jk->log += "\ncudaLibraryLoadData/GetKernel failed";
     cudaGetLastError();
     return jk;
@@ -527,6 +556,63 @@ bool jit_compile_check_hybrid(const JitModel& model, bool count, bool philox, st
   std::vector<char> cubin;
   return nvrtc_compile(generate_policy(model), count, philox, false, false, false, 0, &cubin, log,
                        hybrid_jit_kn(model));
+}
+
+int lsoda_jit_spec(const JitModel& model) { return kSpecLsoda + (model.n <= 8 ? model.n : 0); }
+
+bool jit_compile_check_lsoda(const JitModel& model, bool count, std::string* log) {
+  std::vector<char> cubin;
+  return nvrtc_compile(generate_policy(model), count, false, false, false, false, 0, &cubin, log,
+                       lsoda_jit_spec(model));
+}
+
+cudaError_t launch_lsoda_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                             const double* coeffs, bool count, unsigned long long* counter, size_t smem,
+                             cudaStream_t stream, bool* used) {
+  *used = false;
+  if (S.n_local == 0) {
+    *used = true;
+    return cudaSuccess;
+  }
+  const std::string policy = model.policy.empty() ? generate_policy(model) : model.policy;
+  const bool global_state = S.gstate != nullptr;
+  const int spec = lsoda_jit_spec(model);
+  const std::string key = policy + variant_key(count, false, false, global_state, false, 0, spec);
+  std::shared_ptr<JitKernel> jk;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_cache.find(key);
+    if (it != g_cache.end()) {
+      jk = it->second;
+    } else {
+      jk = compile(policy, count, false, false, global_state, false, 0, spec);
+      g_cache[key] = jk;
+    }
+  }
+  if (!jk->ok) return cudaSuccess;  // caller falls back to the table-driven kernel
+  if (smem > 227 * 1024) return cudaSuccess;
+  const void* fn = reinterpret_cast<const void*>(jk->kern);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaSuccess;
+  const uint64_t warps = (S.n_local + 31) / 32;
+  uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
+  if (S.gstate && S.gstate_warps < resident) resident = S.gstate_warps;
+  const unsigned grid = static_cast<unsigned>(warps < resident ? warps : resident);
+  e = cudaMemsetAsync(counter, 0, sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  KinTables* Tp = const_cast<KinTables*>(&T);
+  KinSweepDev* Sp = const_cast<KinSweepDev*>(&S);
+  KinOutDev Oc = O;
+  void* args[] = {Tp, Sp, &Oc, &coeffs, &counter};
+  e = cudaLaunchKernel(fn, dim3(grid), dim3(32), args, smem, stream);
+  if (e == cudaSuccess) *used = true;
+  return e;
 }
 
 cudaError_t launch_hybrid_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S, const KinOutDev& O,

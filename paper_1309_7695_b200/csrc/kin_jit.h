@@ -37,6 +37,11 @@ bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_
 bool jit_compile_check_hybrid(const JitModel& model, bool count, bool philox, std::string* log);
 cudaError_t launch_hybrid_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
                               bool count, unsigned long long* counter, size_t smem, cudaStream_t stream, bool* used);
+// the LSODA kernel with the generated policy's straight-line RHS
+bool jit_compile_check_lsoda(const JitModel& model, bool count, std::string* log);
+cudaError_t launch_lsoda_jit(const JitModel& model, const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                             const double* coeffs, bool count, unsigned long long* counter, size_t smem,
+                             cudaStream_t stream, bool* used);
 
 // Launch the specialised kernel; *used = false means "not available" (NVRTC
 // failure or unsupported configuration): the caller launches the table kernel.

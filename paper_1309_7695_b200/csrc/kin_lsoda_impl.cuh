@@ -19,8 +19,13 @@
 // bit-identical to the oracle's.
 #pragma once
 #include "kin_device.cuh"
+#ifndef __CUDACC_RTC__
 #include "kin_launch.h"
+#endif
 #include "kin_pmath.cuh"
+#ifndef KIN_INF
+#define KIN_INF __longlong_as_double(0x7FF0000000000000LL)
+#endif
 
 namespace kin {
 
@@ -89,9 +94,16 @@ __device__ __noinline__ double wrms_out_of_line(const double* vv, const double* 
   return sqrt(s / n);
 }
 
+// The RHS policy: TablePM walks the packed tables (rhs_out_of_line); the
+// per-model JIT passes its generated GenModel<double> (kin_jit.cpp: straight-
+// line propensities and nu rows, the same operations in the same order).
+struct TablePM {
+  static constexpr bool kJit = false;
+};
+
 // kN > 0: the species count is a compile-time constant (small models: every
 // loop over species unrolls and the indexing folds); kN = 0: runtime T.n.
-template <int kN>
+template <int kN, class PM = TablePM>
 struct Lsoda {
   const KinTables& T;
   const KinSweepDev& S;
@@ -121,7 +133,13 @@ struct Lsoda {
   // rre_rhs (oracle order): a_j then dx_i = sum over the nu row
   template <bool C>
   __device__ __forceinline__ void rhs(const double* yy, double* f) {
-    rhs_out_of_line<kN>(T, av, a, m, N(), yy, f);
+    if constexpr (PM::kJit) {
+      const PM st{T, const_cast<double*>(yy), a, av};
+      st.props_only();
+      st.rre_rows(f, N());
+    } else {
+      rhs_out_of_line<kN>(T, av, a, m, N(), yy, f);
+    }
     if (C) flops += F_rhs;
   }
   template <bool C>
@@ -336,13 +354,13 @@ struct Lsoda {
   }
 };
 
-template <bool kCount, int kN>
+template <bool kCount, int kN, class PM>
 __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOutDev& O, const double* co, uint64_t s,
                           double* smem_base, int* ismem_base, int tid, unsigned mask) {
   constexpr int B = kBlock;
   const uint64_t sim = global_sim(S, s);
   const int n = kN > 0 ? kN : T.n, m = T.m, G = T.n_grid;
-  Lsoda<kN> L{T, S, co, T.n, m};
+  Lsoda<kN, PM> L{T, S, co, T.n, m};
   double* p = smem_base + tid;
   L.Z = p;
   p += kL * n * B;
@@ -356,7 +374,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
   p += n * B;
   L.tmp = p;
   p += n * B;
-  if constexpr (!Lsoda<kN>::kRegLU) {
+  if constexpr (!Lsoda<kN, PM>::kRegLU) {
     L.P = p;
     p += n * n * B;
   }
@@ -369,7 +387,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
 
   decode_point(S, sim, L.av, B);
   const double rtol = S.rel_tol, atol = S.abs_tol;
-  const double hmax = S.h_max > 0.0 ? S.h_max : __builtin_huge_val();
+  const double hmax = S.h_max > 0.0 ? S.h_max : KIN_INF;  // (NVRTC has no __builtin_huge_val)
   const double t_end = S.t_end;
   bool floored = false;
   uint64_t n_acc = 0, n_rej = 0, n_bdf = 0;  // n_bdf: accepted BDF steps (meta[3])
@@ -450,7 +468,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) - L.z(j + 1, i);
     };
     auto form_p = [&](const double* yy) {
-      if constexpr (Lsoda<kN>::kRegLU) {
+      if constexpr (Lsoda<kN, PM>::kRegLU) {
         const double hl0 = h * el0;
         hl0_p = hl0;
         have_p = L.template form_lu_reg<kCount>(yy, hl0);
@@ -516,7 +534,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             double del;
             if (meth == 1) {
               for (int i = 0; i < n; ++i) L.tmp[i * B] = h * L.savf[i * B] - (L.z(1, i) + L.acor[i * B]);
-              if constexpr (Lsoda<kN>::kRegLU) L.template lu_solve_reg<kCount>(L.tmp);
+              if constexpr (Lsoda<kN, PM>::kRegLU) L.template lu_solve_reg<kCount>(L.tmp);
               else L.template lu_solve<kCount>(L.tmp);
               del = L.template wrms<kCount>(L.tmp);
               for (int i = 0; i < n; ++i) {
@@ -755,21 +773,14 @@ __host__ __device__ __forceinline__ size_t lsoda_warp_doubles(const KinTables& T
   return (18 * n + n * n + T.m + S.n_axes) * kBlock + (n * kBlock + 1) / 2;
 }
 
-template <bool kCount, bool kGlobal, int kN>
-// __maxnreg__ rather than __launch_bounds__(32): with the launch bounds
-// ptxas held these kernels at 128 registers and spilled (the generic variant
-// 316 bytes, the N = 4 one 352 with the register LU); 200 lets them allocate
-// what they use (N = 4: 167 registers, no spills) — residency is set by the
-// shared-memory state anyway.
-__global__ void __maxnreg__(200) lsoda_kernel(const __grid_constant__ KinTables T,
-                                                       const __grid_constant__ KinSweepDev S, KinOutDev O,
-                                                       const double* __restrict__ co,
-                                                       unsigned long long* __restrict__ next) {
+template <bool kCount, bool kGlobal, int kN, class PM>
+__device__ __forceinline__ void lsoda_body(const KinTables& T, const KinSweepDev& S, const KinOutDev& O,
+                                           const double* __restrict__ co, unsigned long long* __restrict__ next) {
   extern __shared__ double smem[];
   constexpr int B = kBlock;
   const int tid = threadIdx.x, lane = tid & 31;
   const int n = T.n;
-  const size_t nd = static_cast<size_t>(18 * n + (Lsoda<kN>::kRegLU ? 0 : n * n) + T.m + S.n_axes) * B;
+  const size_t nd = static_cast<size_t>(18 * n + (Lsoda<kN, PM>::kRegLU ? 0 : n * n) + T.m + S.n_axes) * B;
   // state in shared memory, or (kGlobal: models too large for it) in this
   // block's region of global memory, same layout
   double* sbase = kGlobal ? S.gstate + static_cast<size_t>(blockIdx.x) * lsoda_warp_doubles(T, S) : smem;
@@ -781,10 +792,24 @@ __global__ void __maxnreg__(200) lsoda_kernel(const __grid_constant__ KinTables 
     if (base >= S.n_local) break;
     const uint64_t s = base + lane;
     const unsigned mask = __ballot_sync(0xFFFFFFFFu, s < S.n_local);
-    if (s < S.n_local) lsoda_one<kCount, kN>(T, S, O, co, s, sbase, ism, tid, mask);
+    if (s < S.n_local) lsoda_one<kCount, kN, PM>(T, S, O, co, s, sbase, ism, tid, mask);
     __syncwarp();
   }
 }
+
+// __maxnreg__ rather than __launch_bounds__(32): with the launch bounds
+// ptxas held these kernels at 128 registers and spilled (the generic variant
+// 316 bytes, the N = 4 one 352 with the register LU); 200 lets them allocate
+// what they use (N = 4: 167 registers, no spills) — residency is set by the
+// shared-memory state anyway.
+template <bool kCount, bool kGlobal, int kN>
+__global__ void __maxnreg__(200) lsoda_kernel(const __grid_constant__ KinTables T,
+                                               const __grid_constant__ KinSweepDev S, KinOutDev O,
+                                               const double* __restrict__ co, unsigned long long* __restrict__ next) {
+  lsoda_body<kCount, kGlobal, kN, TablePM>(T, S, O, co, next);
+}
+
+#ifndef __CUDACC_RTC__
 
 
 // Host launcher of one kernel variant (explicitly instantiated across several
@@ -814,6 +839,7 @@ cudaError_t launch_k(const KinTables& T, const KinSweepDev& S, const KinOutDev& 
 #define KIN_LSODA_SIG(kc, kg, kn)                                                                                \
   cudaError_t launch_k<kc, kg, kn>(const KinTables&, const KinSweepDev&, const KinOutDev&, const double*,       \
                                    unsigned long long*, size_t, cudaStream_t)
+#endif  // __CUDACC_RTC__
 
 }  // namespace lsd
 }  // namespace kin

@@ -75,7 +75,7 @@ def test_missing_library_fails_loudly(tmp_path):
         abi.load_library(tmp_path / "nope.so")
 
 
-@pytest.mark.parametrize("which", ["c1", "c2", "c4", "c5", "iso", "c1_hybrid", "c4_hybrid"])
+@pytest.mark.parametrize("which", ["c1", "c2", "c4", "c5", "iso", "c1_hybrid", "c4_hybrid", "c3_lsoda"])
 def test_jit_kernel_compiles_without_gpu(which):
     """The per-model specialised kernel source (the stochastic kernel, or the
     hybrid PDMP kernel for a hybrid sweep) is generated and compiled by NVRTC
@@ -86,6 +86,8 @@ def test_jit_kernel_compiles_without_gpu(which):
     if which == "iso":
         net = W.isomerization()
         cfg = SweepConfig([SweepAxis("kf", [1.0, 2.0])], 4, Method(MethodKind.Ssa), 1, 1.0, [0.0, 1.0])
+    elif which == "c3_lsoda":
+        net, cfg = W.c3_config()
     elif which.endswith("_hybrid"):
         net, cfg = getattr(W, f"{which[:2]}_config")()
         cfg.method = Method(MethodKind.Hybrid, theta_x=100.0, theta_a=10.0)

@@ -106,15 +106,15 @@ def test_random_network_rng_and_firing_modes(engine, oracle, case, mode):
 
 
 @pytest.mark.parametrize("case", CASES, ids=[f"s{c[0]}_n{c[1]}_m{c[2]}_o{c[3]}_x{c[4]}" for c in CASES])
-@pytest.mark.parametrize("kind", [MethodKind.Lsoda, MethodKind.Hybrid, "hybrid_jit", MethodKind.Ode])
+@pytest.mark.parametrize("kind", [MethodKind.Lsoda, "lsoda_jit", MethodKind.Hybrid, "hybrid_jit", MethodKind.Ode])
 def test_random_network_integrators(engine, oracle, case, kind):
-    """LSODA (Adams/BDF switching) and the hybrid PDMP (table and per-model
-    JIT kernels) bit-exact against the oracle on the random networks; Dopri5
-    within 10x its tolerance."""
+    """LSODA (Adams/BDF switching) and the hybrid PDMP, each through the
+    table and the per-model JIT kernels, bit-exact against the oracle on the
+    random networks; Dopri5 within 10x its tolerance."""
     net = random_network(*case)
     kw = {}
-    if kind == "hybrid_jit":
-        kind, kw = MethodKind.Hybrid, dict(variant=abi.VARIANT_JIT)
+    if kind in ("hybrid_jit", "lsoda_jit"):
+        kind, kw = (MethodKind.Hybrid if kind == "hybrid_jit" else MethodKind.Lsoda), dict(variant=abi.VARIANT_JIT)
     cfg = SweepConfig([SweepAxis("k_sweep", [0.5, 1.0, 2.0, 4.0])], 4, Method(kind), 3000 + case[0], 1.0,
                       uniform_grid(1.0, 11))
     ref, got = both(engine, oracle, net, cfg, **kw)

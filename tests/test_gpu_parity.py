@@ -270,6 +270,36 @@ def test_jit_small_model_budget_inside_burst(engine, oracle, kind):
     assert ei.value.sim_status == 1  # KIN_SIM_BUDGET
 
 
+@pytest.mark.parametrize("case", ["c3", "c3_stiff", "c4_slice", "robertson", "c3_work"])
+def test_lsoda_jit_kernel_bit_exact(engine, oracle, case):
+    """The per-model JIT LSODA kernel (kin_jit_lsoda: the generated policy's
+    straight-line propensities and nu rows as the RHS) against the oracle,
+    bit for bit incl. the BDF counter — and the JIT kernel is the one that ran."""
+    import ctypes as C
+    kw = dict(variant=abi.VARIANT_JIT)
+    if case in ("c3", "c3_work"):
+        net, cfg = W.c3_config(side=16)
+    elif case == "c3_stiff":
+        net, cfg = W.c3_stiff_config(side=16)
+    elif case == "c4_slice":
+        net, cfg = W.c4_config(method=MethodKind.Lsoda)
+        kw["sim_range"] = (5000, 5032)
+    else:  # stiff kinetics, mostly BDF (the configuration of test_robertson_lsoda_bit_exact)
+        net = W.robertson(1e6)
+        g = np.concatenate([[0.0], np.logspace(-4, 4, 33)])
+        ic = IntegratorConfig(rel_tol=1e-6, abs_tol=1e-6, max_steps=200000)
+        cfg = SweepConfig([SweepAxis("k3", [1e-3, 1e-2, 1e-1])], 1, Method(MethodKind.Lsoda, integrator=ic), 0, 1e4, g)
+    want_work = case == "c3_work"
+    d, keep = make_sweep_desc(net, cfg, **kw)
+    ref = oracle.sweep(net, d, want_traj=True, want_work=want_work)
+    got = engine.sweep(net, cfg, want_traj=True, want_work=want_work, **kw)
+    assert_bit_exact(ref, got, work=want_work)
+    err = abi.KinError()
+    assert engine.lib.kin_sweep_launch(engine.ctx, engine.model(net), C.byref(d), 0, 0, 0, C.byref(err)) == 0
+    assert engine.lib.kin_sweep_sync(engine.ctx, 0, C.byref(err)) == 0, err.text()
+    assert engine.lib.kin_sweep_kernel_name(engine.ctx, 0).decode() == "kin_jit_lsoda"
+
+
 def _launch_kernel_ms(engine, net, d, reps=3):
     import ctypes as C
     lib, err, h = engine.lib, abi.KinError(), engine.model(net)
