@@ -78,6 +78,9 @@ constexpr int kGroupTauMinReactions = 1;
 constexpr int kSwitchApplyMaxNnz = 16;
 // Largest M whose all_props is straight-line (above: uniform loop over prop(j)).
 constexpr int kInlinePropsMaxReactions = 1 << 30;
+// Flat-loop models: SSA events per trip of the flat loop (see
+// kin_stochastic_impl.cuh simulate_one).
+constexpr int kBurstQuantumDefault = 4;
 
 // Development knobs (KIN_JIT_TAU_INLINE / KIN_JIT_APPLY_SWITCH override the
 // thresholds; they change the generated source, hence the cache key).
@@ -271,7 +274,8 @@ std::string generate_policy(const JitModel& m) {
     std::vector<int> touched(m.n, 0);
     for (int p = 0; p < m.col_ptr[m.m]; ++p) touched[m.col_species[p]] = 1;
     o << "  static constexpr bool kUniformSsa = true;\n  static constexpr bool kFlatBurst = true;\n"
-         "  static constexpr int kM = " << m.m << ";\n";
+         "  static constexpr int kM = " << m.m << ";\n"
+         "  static constexpr int kBurstQuantum = " << std::max(1, std::min(64, jit_knob("KIN_JIT_BURST_K", kBurstQuantumDefault))) << ";\n";
     o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const {\n    bool neg = false;\n";
     for (int i = 0; i < m.n; ++i) {
       if (!touched[i]) continue;
@@ -289,6 +293,7 @@ std::string generate_policy(const JitModel& m) {
     o << "  }\n";
   } else if (m.m <= kSwitchMaxReactions) {
     o << "  static constexpr bool kUniformSsa = false;\n  static constexpr bool kFlatBurst = false;\n"
+         "  static constexpr int kBurstQuantum = 1;\n"
          "  static constexpr int kM = " << m.m << ";\n";
     o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const {\n    bool neg = false;\n    switch (j) {\n";
     for (int j = 0; j < m.m; ++j) {
@@ -308,6 +313,7 @@ std::string generate_policy(const JitModel& m) {
     o << "    }\n  }\n";
   } else {
     o << "  static constexpr bool kUniformSsa = false;\n  static constexpr bool kFlatBurst = false;\n"
+         "  static constexpr int kBurstQuantum = 1;\n"
          "  static constexpr int kM = " << m.m << ";\n";
     o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const { return TableModel<XT>{T, x, a, av}.fire(j, ovf); }\n"
          "  __device__ __forceinline__ void dep_update(int sel) const { TableModel<XT>{T, x, a, av}.dep_update(sel); }\n";

@@ -59,6 +59,7 @@ template <class XT, int kB = kBlock>
 struct TableModel {
   static constexpr bool kUniformSsa = false;
   static constexpr bool kFlatBurst = false;
+  static constexpr int kBurstQuantum = 1;
   static constexpr int kM = 0;
   const KinTables& T;
   XT* x;             // x[i * B]
@@ -373,11 +374,15 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
 
   // Small models (Model::kFlatBurst): one flat loop, one step per trip — a
   // decision (then a leap, or the first event of an SSA burst) or the next
-  // event of a burst.  A burst nested inside the decision loop holds every
-  // lane of the warp at the loop head until the warp's longest burst ends: a
-  // lane that leapt advanced one leap per 100 events of its neighbours (C2:
-  // 73 -> 50 ms).  b: position in the burst, -1 at a decision; it saturates
-  // at 100 (pure SSA never leaves its burst).
+  // Model::kBurstQuantum events of a burst.  A burst nested inside the
+  // decision loop holds every lane of the warp at the loop head until the
+  // warp's longest burst ends: a lane that leapt advanced one leap per 100
+  // events of its neighbours (C2: 73 -> 50 ms); one event per trip instead
+  // makes a bursting lane pay a neighbour's whole leap per event.  A few
+  // events per trip (a leap costs ~10 events) balances the two: C2 46.7 ms at
+  // 1, 39.5 at 2, 36.5-37.0 at 4, 39.6 at 8, 44.0 at 16.  b: position in the
+  // burst, -1 at a decision; it saturates at 100 (pure SSA never leaves its
+  // burst).  Per-simulation results do not depend on the quantum.
   int b = -1;
   for (;;) {
     if (b < 0) {
@@ -496,10 +501,11 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         continue;
       }
     }
-    // the burst's events: one per trip of the outer loop (kFlat), or the whole
+    // the burst's events: kBurstQuantum per trip of the outer loop (kFlat), or the whole
     // burst here (large models, whose rare bursts cost less than the extra
     // per-trip divergence of the flat form: C4 94 vs 103 ms)
     bool done = false;
+    int quantum = 0;
     do {
       if (b > 0) {
         if (kind != 0 && b >= 100) { a_valid = true; b = -1; break; }
@@ -539,7 +545,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
         a0 = sm.sum_props(M);
       }
       if (b < 100) ++b;
-    } while (!Model::kFlatBurst);
+    } while (!Model::kFlatBurst || ++quantum < Model::kBurstQuantum);
     if (done) break;
   }
   if (ovf) {
