@@ -312,8 +312,14 @@ std::string generate_policy(const JitModel& m) {
     }
     o << "    }\n  }\n";
   } else {
-    o << "  static constexpr bool kUniformSsa = false;\n  static constexpr bool kFlatBurst = false;\n"
-         "  static constexpr int kBurstQuantum = 1;\n"
+    // Flat loop when the state lives in global memory (C5: 1208 -> 1074 ms at
+    // four events per trip; 16: 1134, 64: 1222); shared-memory layouts keep
+    // the nested burst (C4: 89.1 vs 90.5-92.4 ms flat — the flat form needs
+    // 135 registers, past the 128 at which 14 warps per SM fit)
+    const int flat = jit_knob("KIN_JIT_FLAT_LARGE", -1);
+    o << "  static constexpr bool kUniformSsa = false;\n  static constexpr bool kFlatBurst = "
+      << (flat < 0 ? "KGLOBAL_" : flat ? "true" : "false") << ";\n"
+         "  static constexpr int kBurstQuantum = " << std::max(1, jit_knob("KIN_JIT_BURST_K_LARGE", 4)) << ";\n"
          "  static constexpr int kM = " << m.m << ";\n";
     o << "  __device__ __forceinline__ bool fire(int j, bool& ovf) const { return TableModel<XT>{T, x, a, av}.fire(j, ovf); }\n"
          "  __device__ __forceinline__ void dep_update(int sel) const { TableModel<XT>{T, x, a, av}.dep_update(sel); }\n";
@@ -422,7 +428,7 @@ bool nvrtc_compile(const std::string& policy, bool count, bool philox, bool int_
   const std::string d_x = std::string("-DKSMEMX_=") + (smem_x ? "true" : "false");
   // split layout: its 16 KB of shared memory per warp allows 13 resident warps
   // per SM; ask the register allocator for that many (development knob)
-  const std::string d_b = "-DKMINB_=" + std::to_string(smem_x ? jit_knob("KIN_JIT_SPLIT_MINB", 1) : 1);
+  const std::string d_b = "-DKMINB_=" + std::to_string(smem_x ? jit_knob("KIN_JIT_SPLIT_MINB", 1) : jit_knob("KIN_JIT_MINB", 1));
   const std::string d_f = "-DKFIRING_=" + std::to_string(firing);
   const char* opts[] = {kNvrtcOpts[0], kNvrtcOpts[1], kNvrtcOpts[2], kNvrtcOpts[3], kNvrtcOpts[4],
                         d_xt.c_str(),  d_c.c_str(),   d_p.c_str(),   d_g.c_str(),   d_x.c_str(), d_b.c_str(),
@@ -515,6 +521,7 @@ std::string variant_key(bool count, bool philox, bool int_state, bool global_sta
                         int spec = -1) {
   return std::string(count ? "C" : "c") + (philox ? "P" : "p") + (int_state ? "I" : "D") +
          (global_state ? (smem_x ? "H" + std::to_string(jit_knob("KIN_JIT_SPLIT_MINB", 1)) : "G") : "S") +
+         (jit_knob("KIN_JIT_MINB", 1) != 1 ? "M" + std::to_string(jit_knob("KIN_JIT_MINB", 1)) : "") +
          (firing ? "B" : "") + (spec >= 0 ? "Y" + std::to_string(spec) : "");
 }
 

@@ -358,7 +358,7 @@ __device__ __forceinline__ void simulate_one(const KinTables& T, const KinSweepD
   // register (read once per grid point instead of twice per SSA event: C2
   // 51 -> 47 ms); for C4 the two extra registers cross the 128-register line
   // at which 14 warps per SM fit (4 per scheduler): 94 -> 156 ms.
-  constexpr bool kTg = Model::kFlatBurst;
+  constexpr bool kTg = Model::kFlatBurst && Model::kUniformSsa;
   double tg = (kTg && G > 0) ? tab_grid(T, S, 0) : KIN_INF;
   auto next_grid = [&]() { return kTg ? tg : (gi < G ? tab_grid(T, S, gi) : KIN_INF); };
   auto emit = [&]() {
