@@ -560,7 +560,10 @@ size_t gstate_live_doubles(const KinTables& T, const KinSweepDev& S, bool x_in_s
 
 bool jit_compile_check(const JitModel& model, bool count, bool philox, bool int_state, std::string* log) {
   std::vector<char> cubin;
-  return nvrtc_compile(generate_policy(model), count, philox, int_state, false, false, 0, &cubin, log, -1);
+  // KIN_JIT_CHECK_LAYOUT=G|H: the global-state / split layouts (offline register study)
+  const char* lay = std::getenv("KIN_JIT_CHECK_LAYOUT");
+  const bool g = lay && (*lay == 'G' || *lay == 'H'), h = lay && *lay == 'H';
+  return nvrtc_compile(generate_policy(model), count, philox, int_state, g, h, 0, &cubin, log, -1);
 }
 
 int hybrid_jit_kn(const JitModel& model) { return model.n <= 8 ? model.n : 0; }
