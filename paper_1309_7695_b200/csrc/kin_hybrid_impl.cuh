@@ -32,6 +32,9 @@ namespace hyb {
 
 using pmath::pm_log;
 using pmath::pm_pow;
+// x^y out of line (three sites in the step loop; each inlined copy is ~100
+// instructions of the kernel's instruction-cache working set).  Same operations.
+static __device__ __noinline__ double pm_pow_out(double x, double y) { return pm_pow(x, y); }
 constexpr int kBlock = 32;  // one warp per block: the per-thread state is large
 using stoch::TableModel;
 
@@ -220,7 +223,7 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         }
         der2 = sqrt(der2) / h;
         const double der12 = dmax(der2, sqrt(dnf));
-        const double h1 = der12 <= 1e-15 ? dmax(1.0e-6, h * 1.0e-3) : pm_pow(0.01 / der12, 0.2);
+        const double h1 = der12 <= 1e-15 ? dmax(1.0e-6, h * 1.0e-3) : pm_pow_out(0.01 / der12, 0.2);
         h = dmin(100.0 * h, h1);
         if (h > hmax) h = hmax;
         if (kCount) H.flops += 15 * static_cast<uint64_t>(n1) + 12;
@@ -258,7 +261,7 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         const double err = sqrt(sum / static_cast<double>(n1));
         if (kCount) H.flops += 63 * static_cast<uint64_t>(n1) + 4;
         if (!finite || !isfinite(err)) { status = KIN_SIM_NONFINITE; break; }
-        const double fac11 = pm_pow(err, kExpo1);
+        const double fac11 = pm_pow_out(err, kExpo1);
         if (err > 1.0) {
           h = hh / dmin(kFacMinInv, fac11 / kSafe);
           last_rejected = true;
@@ -266,7 +269,7 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
           if (kCount) H.flops += 3;
           continue;
         }
-        double fac = fac11 / pm_pow(facold, kBeta);
+        double fac = fac11 / pm_pow_out(facold, kBeta);
         fac = dmax(kFacMaxInv, dmin(kFacMinInv, fac / kSafe));
         double hnew = hh / fac;
         facold = dmax(err, 1.0e-4);

@@ -41,6 +41,20 @@ namespace lsd {
 
 using pmath::pm_pow;
 
+// Step-ratio factors 1 / (c * x^e + cs) of the order/step selection (LSODE
+// rhsm/rhup/rhdn and LSODA's method-switch ratios), out of line: each inlined
+// copy was ~150 instructions (portable log + exp + two divisions) at seven
+// sites, all in the kernel's instruction-cache working set (ncu: no_instruction
+// 2.38 warps per issue on C3), executed once per nq+1 steps.  Same operations,
+// same results; C3 21.2 -> 18.7-19.1 ms, stiff C3 11.8 -> 10.8 ms.  (The
+// Jacobian row/matrix out of line as well measured slower: 21.6 ms.)
+static __device__ __noinline__ double step_ratio_e(double x, double e, double c, double cs) {
+  return 1.0 / (c * pm_pow(x, e) + cs);
+}
+static __device__ __noinline__ double step_ratio_q(double x, int q, double c, double cs) {
+  return 1.0 / (c * pm_pow(x, 1.0 / q) + cs);
+}
+
 constexpr int kBlock = 32;
 // N <= 4: keep the iteration matrix P = I - h l0 J and its LU factors in
 // registers (fully unrolled, constant indices) instead of shared memory.
@@ -590,11 +604,11 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             if (meth == 1) ipup = true;
             continue;
           }
-          const double rhsm = 1.0 / (1.2 * pm_pow(dsm, 1.0 / (nq + 1)) + 1.2e-6);
+          const double rhsm = step_ratio_q(dsm, nq + 1, 1.2, 1.2e-6);
           double rhdn = 0.0;
           if (nq > 1) {
             const double ddn = L.template wrms<kCount>(&L.z(nq, 0)) / L.tesco(meth, nq, 0);
-            rhdn = 1.0 / (1.3 * pm_pow(ddn, 1.0 / nq) + 1.3e-6);
+            rhdn = step_ratio_q(ddn, nq, 1.3, 1.3e-6);
           }
           double rh;
           if (rhsm >= rhdn) {
@@ -664,18 +678,18 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
       // order / step / method selection
       --ialth;
       if (ialth == 0) {
-        const double rhsm = 1.0 / (1.2 * pm_pow(dsm, 1.0 / (nq + 1)) + 1.2e-6);
+        const double rhsm = step_ratio_q(dsm, nq + 1, 1.2, 1.2e-6);
         double rhsm_cap;
         double rhup = 0.0;
         if (nq < maxord()) {
           for (int i = 0; i < n; ++i) L.tmp[i * B] = L.acor[i * B] - L.z(kL - 1, i);
           const double dup = L.template wrms<kCount>(L.tmp) / L.tesco(meth, nq, 2);
-          rhup = 1.0 / (1.4 * pm_pow(dup, 1.0 / (nq + 2)) + 1.4e-6);
+          rhup = step_ratio_q(dup, nq + 2, 1.4, 1.4e-6);
         }
         double rhdn = 0.0;
         if (nq > 1) {
           const double ddn = L.template wrms<kCount>(&L.z(nq, 0)) / L.tesco(meth, nq, 0);
-          rhdn = 1.0 / (1.3 * pm_pow(ddn, 1.0 / nq) + 1.3e-6);
+          rhdn = step_ratio_q(ddn, nq, 1.3, 1.3e-6);
         }
         double pdnorm = -1.0;
         if (meth == 0) {
@@ -709,7 +723,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
           if (meth == 0 && nq <= 5) {
             const double rh1 = rh;
             const double dm2 = dsm * (cm1(nq) / cm2(nq));
-            const double rh2 = 1.0 / (1.2 * pm_pow(dm2, exsm) + 1.2e-6);
+            const double rh2 = step_ratio_e(dm2, exsm, 1.2, 1.2e-6);
             if (rh2 >= 5.0 * rh1) {
               newm = 1; newq = nq; rh = rh2;
             } else if (nstab >= kLsodaStabSwitch) {
@@ -719,7 +733,7 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
             }
           } else if (meth == 1) {
             const double dm1 = dsm * (cm2(nq) / cm1(nq));
-            double rh1 = 1.0 / (1.2 * pm_pow(dm1, exsm) + 1.2e-6);
+            double rh1 = step_ratio_e(dm1, exsm, 1.2, 1.2e-6);
             double rh1it = 2.0 * rh1;
             const double pdh = pdnorm * h;
             if (pdh * rh1 > 1e-5) rh1it = c_sm1[nq] / pdh;
