@@ -466,20 +466,58 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
       h = h * rh;
       if (kCount) L.flops += static_cast<uint64_t>(nq) * (n + 1);
     };
+    // kN > 0: the value each update adds (predict: z(j+1) as just updated;
+    // unpredict: z(j+1) before its own update) is carried in registers
+    // instead of re-read from shared memory — the same additions in the same
+    // order, one load per element instead of two
     auto predict = [&]() {
+      if constexpr (kN > 0) {
 #pragma unroll 1
-      for (int k = 0; k < nq; ++k)
+        for (int k = 0; k < nq; ++k) {
+          double c[kN > 0 ? kN : 1];
+#pragma unroll
+          for (int i = 0; i < kN; ++i) c[i] = L.z(nq, i);
 #pragma unroll 1
-        for (int j = nq - 1; j >= k; --j)
-          for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) + L.z(j + 1, i);
+          for (int j = nq - 1; j >= k; --j)
+#pragma unroll
+            for (int i = 0; i < kN; ++i) {
+              const double v = L.z(j, i) + c[i];
+              L.z(j, i) = v;
+              c[i] = v;
+            }
+        }
+      } else {
+#pragma unroll 1
+        for (int k = 0; k < nq; ++k)
+#pragma unroll 1
+          for (int j = nq - 1; j >= k; --j)
+            for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) + L.z(j + 1, i);
+      }
       if (kCount) L.flops += static_cast<uint64_t>(nq) * (nq + 1) / 2 * n;
     };
     auto unpredict = [&]() {
+      if constexpr (kN > 0) {
 #pragma unroll 1
-      for (int k = nq - 1; k >= 0; --k)
+        for (int k = nq - 1; k >= 0; --k) {
+          double c[kN > 0 ? kN : 1];
+#pragma unroll
+          for (int i = 0; i < kN; ++i) c[i] = L.z(k, i);
 #pragma unroll 1
-        for (int j = k; j <= nq - 1; ++j)
-          for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) - L.z(j + 1, i);
+          for (int j = k; j <= nq - 1; ++j)
+#pragma unroll
+            for (int i = 0; i < kN; ++i) {
+              const double nx = L.z(j + 1, i);
+              L.z(j, i) = c[i] - nx;
+              c[i] = nx;
+            }
+        }
+      } else {
+#pragma unroll 1
+        for (int k = nq - 1; k >= 0; --k)
+#pragma unroll 1
+          for (int j = k; j <= nq - 1; ++j)
+            for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) - L.z(j + 1, i);
+      }
     };
     auto form_p = [&](const double* yy) {
       if constexpr (Lsoda<kN, PM>::kRegLU) {
@@ -628,10 +666,22 @@ __device__ void lsoda_one(const KinTables& T, const KinSweepDev& S, const KinOut
         ++nst;
         ++n_acc;
         if (meth == 1) ++n_bdf;
+        if constexpr (kN > 0) {  // acor held in registers across the rows
+          double ac[kN > 0 ? kN : 1];
+#pragma unroll
+          for (int i = 0; i < kN; ++i) ac[i] = L.acor[i * B];
 #pragma unroll 1
-        for (int j = 0; j <= nq; ++j) {
-          const double e = L.elco(meth, nq, j);
-          for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) + e * L.acor[i * B];
+          for (int j = 0; j <= nq; ++j) {
+            const double e = L.elco(meth, nq, j);
+#pragma unroll
+            for (int i = 0; i < kN; ++i) L.z(j, i) = L.z(j, i) + e * ac[i];
+          }
+        } else {
+#pragma unroll 1
+          for (int j = 0; j <= nq; ++j) {
+            const double e = L.elco(meth, nq, j);
+            for (int i = 0; i < n; ++i) L.z(j, i) = L.z(j, i) + e * L.acor[i * B];
+          }
         }
         if (kCount) L.flops += 2 * static_cast<uint64_t>(nq + 1) * n;
         const double tprev = t;
