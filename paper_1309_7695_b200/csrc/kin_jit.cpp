@@ -667,6 +667,7 @@ cudaError_t launch_hybrid_jit(const JitModel& model, const KinTables& T, const K
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaSuccess;
+  if (const int cap = jit_knob("KIN_JIT_HYBRID_WARPS_PER_SM", 0); cap > 0 && cap < per_sm) per_sm = cap;  // study knob
   uint64_t resident = static_cast<uint64_t>(per_sm) * sms;
   if (S.gstate && S.gstate_warps < resident) resident = S.gstate_warps;
   KinSweepDev SW = S;
