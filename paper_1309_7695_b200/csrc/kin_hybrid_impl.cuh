@@ -229,6 +229,12 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         if (kCount) H.flops += 15 * static_cast<uint64_t>(n1) + 12;
       }
       double facold = 1.0e-4;
+      // pm_pow(facold, kBeta) = pm_exp(kBeta * pm_log(facold)): facold is the
+      // last accepted err (>= 1e-4, where pm_pow's clamp is idle) or 1e-4, so
+      // its log is the one already taken for that step's fac11 (or log 1e-4):
+      // one log per step instead of two, the same values
+      const double lfo_min = pm_log(1.0e-4);
+      double lfo = lfo_min;
       bool last_rejected = false;
       while (t < t_hor) {
         if (attempts++ >= S.max_steps) { status = KIN_SIM_BUDGET; break; }
@@ -261,7 +267,8 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
         const double err = sqrt(sum / static_cast<double>(n1));
         if (kCount) H.flops += 63 * static_cast<uint64_t>(n1) + 4;
         if (!finite || !isfinite(err)) { status = KIN_SIM_NONFINITE; break; }
-        const double fac11 = pm_pow_out(err, kExpo1);
+        const double lerr = pm_log(err < 1e-300 ? 1e-300 : (err > 1e300 ? 1e300 : err));  // pm_pow's clamp
+        const double fac11 = pmath::pm_exp(kExpo1 * lerr);
         if (err > 1.0) {
           h = hh / dmin(kFacMinInv, fac11 / kSafe);
           last_rejected = true;
@@ -269,10 +276,11 @@ __device__ void simulate_hybrid_one(const KinTables& T, const KinSweepDev& S, co
           if (kCount) H.flops += 3;
           continue;
         }
-        double fac = fac11 / pm_pow_out(facold, kBeta);
+        double fac = fac11 / pmath::pm_exp(kBeta * lfo);
         fac = dmax(kFacMaxInv, dmin(kFacMinInv, fac / kSafe));
         double hnew = hh / fac;
         facold = dmax(err, 1.0e-4);
+        lfo = facold == err ? lerr : lfo_min;
         if (last_rejected && hnew > hh) hnew = hh;
         last_rejected = false;
         h = hnew;
