@@ -354,6 +354,24 @@ __device__ __forceinline__ double binom_fc(double k) {
   return (1.0 / 12.0 - (1.0 / 360.0 - rk2 / 1260.0) * rk2) * rk;
 }
 
+// BINV's exact CDF search (the guard-band fallback of the FP32 decision path
+// in binomial() below, a few 1e-4 of the draws): out of line, so its portable
+// log/exp stay out of the leap loop's instruction-cache working set.
+static __device__ __noinline__ uint64_t binv_exact(double u, double q, double fn, uint64_t n) {
+  const double s = q / (1.0 - q);
+  const double a = (fn + 1.0) * s;
+  double f = pmath::pm_exp(fn * pmath::pm_log(1.0 - q));
+  double c = f;
+  const uint64_t kmax = n < 255 ? n : 255;
+  uint64_t k = 0;
+  while (u > c && k < kmax) {
+    ++k;
+    f = f * (a / static_cast<double>(k) - s);
+    c = c + f;
+  }
+  return k;
+}
+
 template <class Rng>
 static __device__ __noinline__ uint64_t binomial_btrd(Rng& rng, double fn, double q, double np, uint64_t& fl) {
   using pmath::pm_log;
@@ -476,17 +494,7 @@ __device__ __forceinline__ uint64_t binomial(Rng& rng, uint64_t n, double p, uin
       }
     }
     if (!done) {
-      const double s = q / (1.0 - q);
-      const double a = (fn + 1.0) * s;
-      double f = pmath::pm_exp(fn * pmath::pm_log(1.0 - q));
-      double c = f;
-      const double u = Rng::uniform_from_bits(ub);
-      const uint64_t kmax = n < 255 ? n : 255;
-      while (u > c && k < kmax) {
-        ++k;
-        f = f * (a / static_cast<double>(k) - s);
-        c = c + f;
-      }
+      k = binv_exact(Rng::uniform_from_bits(ub), q, fn, n);
       fl += 10 + 4 * k;
     }
   } else {
