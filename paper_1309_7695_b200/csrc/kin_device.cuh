@@ -526,6 +526,20 @@ __device__ __forceinline__ double combinations_c(double x) {
   }
   return h < 0.0 ? 0.0 : h;
 }
+// d h(x, kS) / dx as the LSODA Jacobian takes it (kin_lsoda_impl.cuh jac_row,
+// the oracle's rre_jacobian): compile-time stoichiometry for the per-model JIT
+template <int kS>
+__device__ __forceinline__ double jac_dh(double x) {
+  if constexpr (kS == 1) {
+    return x < 0.0 ? 0.0 : 1.0;
+  } else if constexpr (kS == 2) {
+    return combinations_c<2>(x) > 0.0 ? __dsub_rn(x, 0.5) : 0.0;
+  } else {
+    return combinations_c<3>(x) > 0.0
+               ? __ddiv_rn(__dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(3.0, x), 6.0), x), 2.0), 6.0)
+               : 0.0;
+  }
+}
 
 // combinations (model.hpp:145-149) + order-3 extension; clamp >= 0.
 __device__ __forceinline__ double combinations(double x, int s) {

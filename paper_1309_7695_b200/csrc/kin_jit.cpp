@@ -370,6 +370,67 @@ std::string generate_policy(const JitModel& m) {
     o << " f[" << i << " * B] = acc; }\n";
   }
   o << "  }\n";
+  // LSODA's Jacobian J = nu * da/dx (rre_jacobian), straight-line for small
+  // models (kin_lsoda_impl.cuh Lsoda::jac_row / jacobian: the same products
+  // and sums in the same order as their table walks; x = the state vector)
+  int jac_work = 0;
+  for (int j = 0; j < m.m; ++j) {
+    const int nt = m.rt_ptr[j + 1] - m.rt_ptr[j];
+    jac_work += nt * (m.col_ptr[j + 1] - m.col_ptr[j]);
+  }
+  const bool jit_jac = m.n <= 8 && jac_work <= jit_knob("KIN_JIT_JAC_MAX", 64);
+  o << "  static constexpr bool kJitJac = " << (jit_jac ? "true" : "false") << ";\n";
+  auto rate_expr = [&](int j) {
+    if (m.rate_axis[j] >= 0) return "__dmul_rn(tab_rate(T, " + std::to_string(j) + "), av[" + std::to_string(m.rate_axis[j]) + " * B])";
+    return "tab_rate(T, " + std::to_string(j) + ")";
+  };
+  // dd of term p of reaction j: rk * dh(x_s) * prod over the other terms
+  auto term_dd = [&](int j, int p) {
+    std::ostringstream t;
+    t << "double dd = __dmul_rn(rk, jac_dh<" << m.rt_stoich[p] << ">(xv(" << m.rt_species[p] << ")));";
+    for (int q = m.rt_ptr[j]; q < m.rt_ptr[j + 1]; ++q)
+      if (q != p) t << " dd = __dmul_rn(dd, combinations_c<" << m.rt_stoich[q] << ">(xv(" << m.rt_species[q] << ")));";
+    return t.str();
+  };
+  auto add_term = [&](const std::string& dst, int d) {
+    if (d == 1) return dst + " = __dadd_rn(" + dst + ", dd);";
+    if (d == -1) return dst + " = __dsub_rn(" + dst + ", dd);";
+    return dst + " = __dadd_rn(" + dst + ", __dmul_rn(" + dlit(d) + ", dd));";
+  };
+  o << "  __device__ __forceinline__ void jac_row(int i, double* tmp) const {\n";
+  if (jit_jac) {
+    o << "#pragma unroll\n    for (int s = 0; s < " << m.n << "; ++s) tmp[s * B] = 0.0;\n    switch (i) {\n";
+    for (int i = 0; i < m.n; ++i) {
+      o << "      case " << i << ":";
+      for (int pr = m.row_ptr[i]; pr < m.row_ptr[i + 1]; ++pr) {
+        const int j = m.row_reaction[pr], d = m.row_delta[pr];
+        if (m.rt_ptr[j + 1] == m.rt_ptr[j]) continue;  // zero-order: no x dependence
+        o << " { const double rk = " << rate_expr(j) << ";";
+        for (int p = m.rt_ptr[j]; p < m.rt_ptr[j + 1]; ++p)
+          o << " { " << term_dd(j, p) << " " << add_term("tmp[" + std::to_string(m.rt_species[p]) + " * B]", d) << " }";
+        o << " }";
+      }
+      o << " break;\n";
+    }
+    o << "    }\n";
+  }
+  o << "  }\n";
+  o << "  __device__ __forceinline__ void jac_full(double* J) const {\n";
+  if (jit_jac) {
+    o << "#pragma unroll\n    for (int q = 0; q < " << m.n * m.n << "; ++q) J[q * B] = 0.0;\n";
+    for (int j = 0; j < m.m; ++j) {
+      if (m.rt_ptr[j + 1] == m.rt_ptr[j]) continue;
+      o << "    { const double rk = " << rate_expr(j) << ";";
+      for (int p = m.rt_ptr[j]; p < m.rt_ptr[j + 1]; ++p) {
+        o << " { " << term_dd(j, p);
+        for (int c = m.col_ptr[j]; c < m.col_ptr[j + 1]; ++c)
+          o << " " << add_term("J[" + std::to_string(m.col_species[c] * m.n + m.rt_species[p]) + " * B]", m.col_delta[c]);
+        o << " }";
+      }
+      o << " }\n";
+    }
+  }
+  o << "  }\n";
   o << "};\n}}  // namespace kin::stoch\n";
   return o.str();
 }

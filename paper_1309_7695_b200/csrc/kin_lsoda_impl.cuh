@@ -113,6 +113,7 @@ __device__ __noinline__ double wrms_out_of_line(const double* vv, const double* 
 // line propensities and nu rows, the same operations in the same order).
 struct TablePM {
   static constexpr bool kJit = false;
+  static constexpr bool kJitJac = false;
 };
 
 // kN > 0: the species count is a compile-time constant (small models: every
@@ -158,6 +159,12 @@ struct Lsoda {
   }
   template <bool C>
   __device__ void jacobian(const double* yy, double* J) {
+    if constexpr (PM::kJitJac) {  // the per-model straight-line matrix (kin_jit.cpp)
+      const PM st{T, const_cast<double*>(yy), a, av};
+      st.jac_full(J);
+      if (C) flops += jac_flops();
+      return;
+    }
     for (int q = 0; q < N() * N(); ++q) J[q * B] = 0.0;
 #pragma unroll 1
     for (int k = 0; k < m; ++k) {
@@ -193,6 +200,11 @@ struct Lsoda {
   // ascending): each J_is receives the oracle's contributions (rre_jacobian:
   // reactions ascending) in its order
   __device__ __forceinline__ void jac_row(const double* yy, int i) {
+    if constexpr (PM::kJitJac) {  // the per-model straight-line row (kin_jit.cpp)
+      const PM st{T, const_cast<double*>(yy), a, av};
+      st.jac_row(i, tmp);
+      return;
+    }
     for (int s = 0; s < N(); ++s) tmp[s * B] = 0.0;
     const int p1 = tab_row_ptr(T, i + 1);
 #pragma unroll 1
