@@ -101,3 +101,35 @@ def test_jit_kernel_compiles_without_gpu(which):
     rc = lib.kin_jit_check(C.byref(net.desc()), C.byref(d), log, len(log), C.byref(err))
     assert rc == 0, log.value.decode()[-2000:]
     assert time.time() - t0 < 60
+
+
+@pytest.mark.parametrize("which,jac,flat,quantum", [("c3_lsoda", True, None, None), ("c2", None, "true", 4),
+                                                      ("c4", False, "KGLOBAL_", 4), ("c5", False, "KGLOBAL_", 4)])
+def test_jit_policy_choices(which, jac, flat, quantum, tmp_path, monkeypatch):
+    """The generated per-model policy carries the compile-time choices the
+    kernels rely on: LSODA's straight-line Jacobian for small models (C3) and
+    the table walk above the size limit (C4, C5); the flat decision/event loop
+    with four SSA events per trip for small models (C2); for the larger models
+    (C4, C5) the flat loop is tied to the global-state layout (KGLOBAL_: C5's
+    split layout takes it, C4's shared-memory layout keeps the nested burst)."""
+    import re
+    from paper_1309_7695_b200 import workloads as W
+    from paper_1309_7695_b200.ensemble import make_sweep_desc
+    net, cfg = W.c3_config() if which == "c3_lsoda" else getattr(W, f"{which}_config")()
+    d, keep = make_sweep_desc(net, cfg)
+    monkeypatch.setenv("KIN_JIT_DUMP", str(tmp_path))
+    monkeypatch.setenv("KIN_JIT_CACHE", str(tmp_path / "cache"))
+    lib = abi.load_library()
+    log = C.create_string_buffer(1 << 16)
+    err = abi.KinError()
+    assert lib.kin_jit_check(C.byref(net.desc()), C.byref(d), log, len(log), C.byref(err)) == 0, log.value.decode()
+    src = "".join(p.read_text() for p in tmp_path.glob("kin_jit_*.cu"))
+    if jac is not None:
+        assert f"static constexpr bool kJitJac = {'true' if jac else 'false'};" in src
+        if jac:
+            assert "jac_dh<" in src and "void jac_full(double* J)" in src
+    if flat is not None:
+        f = re.search(r"static constexpr bool kFlatBurst = (\w+);", src)
+        q = re.search(r"static constexpr int kBurstQuantum = (\d+);", src)
+        assert f and q, "no flat-loop choice in the policy"
+        assert f.group(1) == flat and int(q.group(1)) == quantum
